@@ -1,0 +1,318 @@
+"""Pins for the CPU oracle (oracle/) against the paper and the mathematics.
+
+Nothing here compares the oracle with itself: each check uses the paper's
+printed/hand-derived values (tests/golden/, each cited), brute force of a
+definition, Python's stable ``sorted``, an independent Cartesian-tree
+derivation of the plan, or the paper's bounds.
+"""
+import itertools
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from tests import refcheck as R
+
+
+# --------------------------------------------------------------------------
+# Power
+# --------------------------------------------------------------------------
+def test_power_golden(golden_dir):
+    for row in R.read_table(os.path.join(golden_dir, "power_examples.txt")):
+        n, i, j, k, p = map(int, row)
+        assert oracle.power_brute(n, i, j, k) == p, row
+        assert oracle.power(n, i, j, k) == p, row
+
+
+def test_power_exhaustive_small_n():
+    """AC2: closed form == brute-force definition for all i<j<k<=n, n<=64."""
+    lib = oracle.lib()
+    bad = 0
+    for n in range(2, 65):
+        for i in range(0, n):
+            for j in range(i + 1, n):
+                for k in range(j + 1, n + 1):
+                    if lib.orc_power(n, i, j, k) != lib.orc_power_brute(n, i, j, k):
+                        bad += 1
+    assert bad == 0
+
+
+def test_power_xor_form_pow2():
+    """For n = 2^L the power is L + 1 - floor(lg((i+j) XOR (j+k))),
+    a different closed form: exact rational a=(i+j)/2^(L+1), b=(j+k)/2^(L+1)."""
+    rng = np.random.default_rng(7)
+    for _ in range(20000):
+        L = int(rng.integers(1, 35))
+        n = 1 << L
+        i, j, k = sorted(int(x) for x in rng.choice(n + 1, 3, replace=False)) if n > 3 else (0, 1, 2)
+        if not (i < j < k <= n):
+            continue
+        expect = L + 1 - (((i + j) ^ (j + k)).bit_length() - 1)
+        assert oracle.power(n, i, j, k) == expect, (n, i, j, k)
+
+
+def test_power_general_n_bisection():
+    """General n: Python big-integer bisection of the binary expansions of a, b."""
+    rng = np.random.default_rng(11)
+    for _ in range(5000):
+        n = int(rng.integers(3, 1 << 34))
+        i, j, k = sorted(int(x) for x in rng.integers(0, n + 1, 3))
+        if not (i < j < k):
+            continue
+        # first p with floor(a 2^p) != floor(b 2^p), a=(i+j)/2n, b=(j+k)/2n
+        p = 1
+        while ((i + j) << p) // (2 * n) == ((j + k) << p) // (2 * n):
+            p += 1
+        assert oracle.power(n, i, j, k) == p
+
+
+# --------------------------------------------------------------------------
+# minrun
+# --------------------------------------------------------------------------
+def test_minrun_golden(golden_dir):
+    for n, m in R.read_table(os.path.join(golden_dir, "minrun_examples.txt")):
+        assert oracle.minrun(int(n)) == int(m)
+
+
+def test_minrun_powers_of_two():
+    for L in range(6, 40):
+        assert oracle.minrun(1 << L) == 32
+
+
+# --------------------------------------------------------------------------
+# Golden plans
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["plan_g1", "plan_g2", "plan_g4", "plan_g5",
+                                  "plan_spec_twoRuns"])
+@pytest.mark.parametrize("variant", [oracle.VARIANT_A, oracle.VARIANT_B])
+def test_golden_plans_with_keys(golden_dir, name, variant):
+    g = R.read_golden(os.path.join(golden_dir, name + ".txt"))
+    keys = g["keys"]
+    n = g["n"][0]
+    assert len(keys) == n
+    ko, vo, plan, st = oracle.sort(keys, np.arange(n, dtype=np.uint32), variant=variant,
+                                   minrun_override=g["minrun"][0])
+    assert list(plan.run_start) == g["runs"]
+    assert list(plan.run_kind) == g["kinds"]
+    got = [tuple(int(m[f]) for f in ("i", "j", "k", "power")) for m in plan.merges]
+    assert got == g["merge"]
+    if "M" in g:
+        assert st["merge_cost_M"] == g["M"][0]
+    if "out_prefix" in g:
+        pre = g["out_prefix"]
+        pairs = [(int(ko[t]), int(vo[t])) for t in range(len(pre) // 2)]
+        assert pairs == list(zip(pre[0::2], pre[1::2]))
+    rk, rv = R.stable_sorted(keys)
+    assert (ko == rk).all() and (vo == rv).all()
+    p2, _ = oracle.plan(keys, minrun_override=g["minrun"][0])
+    assert (p2.run_start == plan.run_start).all() and (p2.merges == plan.merges).all()
+
+
+def test_golden_plan_g3_policy(golden_dir):
+    g = R.read_golden(os.path.join(golden_dir, "plan_g3.txt"))
+    mg, ms = oracle.policy(g["n"][0], g["runs"])
+    got = [tuple(int(m[f]) for f in ("i", "j", "k", "power")) for m in mg]
+    assert got == g["merge"]
+
+
+def test_extract_run_golden(golden_dir):
+    for (mr,), keys, runs, kinds in R.read_table(os.path.join(golden_dir, "extract_run_examples.txt"), sep="|"):
+        k = np.array([int(x) for x in keys], np.uint32)
+        ko, vo, plan, st = oracle.sort(k, minrun_override=int(mr))
+        assert [int(x) for x in plan.run_start] == [int(x) for x in runs]
+        assert [int(x) for x in plan.run_kind] == [int(x) for x in kinds]
+        assert list(ko) == sorted(k.tolist())
+
+
+def test_entropy_golden(golden_dir):
+    for lens, (h,) in R.read_table(os.path.join(golden_dir, "entropy_examples.txt"), sep="|"):
+        assert abs(R.entropy([int(x) for x in lens]) - float(h)) < 1e-12
+
+
+# --------------------------------------------------------------------------
+# Output == stable sort (F1), exhaustive on tiny inputs (AC1)
+# --------------------------------------------------------------------------
+def _check_case(keys, minrun_override, variants=(0, 1)):
+    n = len(keys)
+    rk, rv = R.stable_sorted(keys)
+    plans = []
+    stats = []
+    for var in variants:
+        ko, vo, plan, st = oracle.sort(keys, np.arange(n, dtype=np.uint32), variant=var,
+                                       minrun_override=minrun_override)
+        assert (ko.view(np.uint8) == rk.view(np.uint8)).all(), (keys, var)
+        assert (vo == rv).all(), (keys, var)
+        plans.append(plan)
+        stats.append(st)
+    return plans, stats
+
+
+def test_exhaustive_permutations():
+    for n in range(0, 8):
+        for mr in (1, 2, 3, 0):
+            for perm in itertools.permutations(range(n)):
+                _check_case(np.array(perm, np.uint32), mr)
+
+
+def test_exhaustive_binary_arrays():
+    for n in range(0, 13):
+        for mr in (1, 2, 0):
+            for bits in range(1 << n):
+                keys = np.array([(bits >> t) & 1 for t in range(n)], np.uint32)
+                _check_case(keys, mr)
+
+
+def _random_case(rng, n, dtype):
+    kind = rng.integers(0, 5)
+    if dtype == np.float32:
+        pool = np.array([0.0, -0.0, 1.0, -1.0, np.nan, -np.nan, np.inf, -np.inf, 2.5, -2.5],
+                        np.float32)
+        x = pool[rng.integers(0, len(pool), n)]
+        bits = x.view(np.uint32).copy()
+        # a few NaNs with distinct payloads
+        m = rng.random(n) < 0.05
+        bits[m] = np.uint32(0x7FC00000) | rng.integers(0, 1 << 20, int(m.sum())).astype(np.uint32)
+        return bits.view(np.float32)
+    hi = 1 << (48 if dtype == np.uint64 else 31)
+    if kind == 0:
+        x = rng.integers(0, 8, n)
+    elif kind == 1:
+        x = rng.integers(0, hi, n)
+    elif kind == 2:  # presorted runs, some reversed
+        x = rng.integers(0, 50, n)
+        cuts = np.sort(rng.integers(0, n + 1, max(1, n // 20)))
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            seg = np.sort(x[a:b])
+            x[a:b] = seg[::-1] if rng.random() < 0.3 else seg
+    elif kind == 3:  # strictly descending stretches
+        x = np.arange(n)[::-1].copy()
+        x[rng.integers(0, max(n, 1), max(1, n // 50))] = 7
+    else:
+        x = np.sort(rng.integers(0, 100, n))
+    return x.astype(dtype)
+
+
+@pytest.mark.parametrize("dtype", [np.uint32, np.uint64, np.float32])
+def test_random_structured(dtype):
+    rng = np.random.default_rng(5)
+    for trial in range(60):
+        n = int(rng.integers(0, 3000))
+        keys = _random_case(rng, n, dtype)
+        mr = int(rng.choice([0, 1, 2, 5]))
+        plans, stats = _check_case(keys, mr)
+        a, b = plans
+        assert (a.run_start == b.run_start).all() and (a.run_kind == b.run_kind).all()
+        assert (a.merges == b.merges).all()
+        minrun = stats[0]["minrun"]
+        R.check_runs(keys, a.run_start, a.run_kind, minrun)
+
+
+# --------------------------------------------------------------------------
+# Plan == Cartesian-tree post-order of brute-force powers (F3, F4)
+# --------------------------------------------------------------------------
+def test_plan_is_cartesian_postorder():
+    rng = np.random.default_rng(3)
+    for trial in range(300):
+        n = int(rng.integers(2, 200))
+        r = int(rng.integers(1, min(n, 40) + 1))
+        starts = [0] + sorted(int(x) for x in rng.choice(np.arange(1, n), r - 1, replace=False))
+        mg, ms = oracle.policy(n, starts)
+        got = [tuple(int(m[f]) for f in ("i", "j", "k", "power")) for m in mg]
+        assert got == R.cartesian_postorder(n, starts, oracle.power_brute)
+        assert ms <= math.ceil(math.log2(n)) + 1
+
+
+# --------------------------------------------------------------------------
+# Counters and bounds (reading R8/R11)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [1000, 30000, 200003])
+def test_counters_and_bounds(n):
+    rng = np.random.default_rng(n)
+    for structure in range(3):
+        if structure == 0:
+            keys = rng.integers(0, 1 << 31, n).astype(np.uint32)
+        elif structure == 1:
+            keys = _random_case(rng, n, np.uint32)
+        else:
+            keys = np.sort(rng.integers(0, 1000, n)).astype(np.uint32)
+            keys[rng.integers(0, n, n // 100)] = 3
+        (pa, pb), (sa, sb) = _check_case(keys, 0)
+        M = sa["merge_cost_M"]
+        lens = np.diff(np.append(pa.run_start, n)).astype(np.int64)
+        H = R.entropy(lens.tolist())
+        assert M == int(sum(int(m["k"]) - int(m["i"]) for m in pa.merges))
+        assert M <= n * (H + 2) + 1e-9
+        assert sa["max_stack"] <= math.ceil(math.log2(n)) + 1
+        # comparisons: identical between variants (both merge left-to-right)
+        assert sa["comp_merge"] == sb["comp_merge"]
+        assert sa["comp_runs"] == sb["comp_runs"]
+        assert sa["comp_merge"] <= M - sa["merges"]             # each merge stops early
+        assert sa["comp_merge"] + n - 1 <= M + n                # P:457 (merge phase)
+        # moves: merge output written exactly once per merged element (R8)
+        assert sa["moves_merge_out"] == M and sb["moves_merge_out"] == M
+        # A: Fig. 1 copies the left run: <= 1.5M+n is about the smaller run;
+        # with the left run the staging is sum |left| (reported, R11)
+        assert sa["moves_staging"] == int(sum(int(m["j"]) - int(m["i"]) for m in pa.merges))
+        # B: extraction pushes n, Copy moves in [0, 2n]  -> merge-phase moves <= M + 3n
+        assert sb["moves_staging"] == n
+        assert sb["moves_copy"] <= 2 * n
+        assert sb["moves_merge_out"] + sb["moves_staging"] + sb["moves_copy"] <= M + 3 * n
+
+
+@pytest.mark.parametrize("n", [10**3, 10**4, 10**5, 10**6])
+def test_vm_memory_law(n):
+    """VM extra memory O(sqrt(n T log n)).  Constants are 'parity
+    unpinned'; checked against the SPEC S:572 guidance law."""
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 1 << 31, n).astype(np.uint32)
+    vals = np.arange(n, dtype=np.uint32)
+    _, _, plan, st = oracle.sort(keys, vals, variant=oracle.VARIANT_B)
+    T = 2
+    P = st["page_elems"]
+    assert P == oracle.page_size(n, T)
+    lg = math.ceil(math.log2(n))
+    words = st["peak_extra_pages"] * P * T + st["peak_meta_words"]
+    assert words <= (lg + 4) * P * T + (math.ceil(n / P) + lg + 16)
+    assert st["peak_extra_pages"] <= lg + 4
+    # far below Pingpong's n*T and CPython's n/2*T words (Fig. 4)
+    assert words <= 0.10 * n * T or n < 10**4
+
+
+def test_page_size_rule():
+    # largest power of two <= sqrt(n/(T log2 n)), clamped to [16, n] (R9)
+    assert oracle.page_size(1 << 20, 1) == 128     # sqrt(2^20/20) = 228.9
+    assert oracle.page_size(10**7, 30) == 64       # sqrt(1e7/(30*23.25)) = 119.7
+    assert oracle.page_size(100, 1) == 16
+    assert oracle.page_size(1 << 24, 2) == 512     # sqrt(2^24/48) = 591.2
+
+
+def test_f32_order():
+    """Reading R5: -0.0 < +0.0, NaN last, all NaNs equal (keep input order)."""
+    lib = oracle.lib()
+    b = lambda x: int(np.array([x], np.float32).view(np.uint32)[0])
+    assert lib.orc_less(oracle.F32, b(-0.0), b(0.0)) == 1
+    assert lib.orc_less(oracle.F32, b(0.0), b(-0.0)) == 0
+    assert lib.orc_less(oracle.F32, b(np.inf), b(np.nan)) == 1
+    assert lib.orc_less(oracle.F32, b(np.nan), b(-np.nan)) == 0
+    assert lib.orc_less(oracle.F32, b(-np.nan), b(np.nan)) == 0
+    assert lib.orc_less(oracle.F32, b(-np.inf), b(-1e30)) == 1
+    assert lib.orc_less(oracle.U64, 1 << 40, (1 << 40) + 1) == 1
+
+
+def test_degenerate():
+    for n in (0, 1):
+        keys = np.arange(n, dtype=np.uint32)
+        ko, vo, plan, st = oracle.sort(keys)
+        assert len(plan.merges) == 0 and len(plan.run_start) == n
+    # sorted input -> one run, M = 0
+    keys = np.arange(1000, dtype=np.uint32)
+    _, _, plan, st = oracle.sort(keys)
+    assert len(plan.run_start) == 1 and st["merge_cost_M"] == 0
+    # random permutation at n = 2^16: all runs 32 long (minrun), perfect tree, M = 11 n
+    rng = np.random.default_rng(1)
+    keys = rng.permutation(1 << 16).astype(np.uint32)
+    _, _, plan, st = oracle.sort(keys)
+    assert (np.diff(np.append(plan.run_start, 1 << 16)) == 32).all()
+    assert st["merge_cost_M"] == 11 * (1 << 16)
