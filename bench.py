@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Virtual-Memory Powersort hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one stable sort of one synthetic batch: the whole hot path (run
+detection, node powers, merge tree + schedule, leaf engine, every level
+merge) on cfg5 -- n = 2^30 u32 keys + u32 payload per GPU.
+Timing: CUDA events on the sorting stream around each sort, W warm-up steps,
+K timed steps bracketed by barrier + synchronize, max over ranks.  Between
+steps the input is restored by an untimed device copy from a pristine
+buffer (8 GiB, which also flushes the 126 MB L2).  Prints ONE JSON line.
+
+--impl reference times the CPU oracle (oracle/, plain single-threaded C) on
+a bounded cfg5-shaped sample per step, on the host, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sorted keys/sec (Gkeys/s) at 1/2/4/8 B200 and % of HBM merge-tree roofline"
+UNIT = "Gkeys/s"
+WORKLOAD = ("cfg5: n=2^30 u32 keys + u32 payload (= index) per GPU; segments 1+Geom0(1/4096), "
+            "50% i.i.d. uniform unsorted / 50% sorted ascending, 5% of those reversed; "
+            "unbounded scratch")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--log2n", type=int, default=30, help="per-GPU n = 2^log2n (default: cfg5's 2^30)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-log2", type=int, default=25)
+    ap.add_argument("--ref-sample-log2", type=int, default=23)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index: int):
+        self.dev = dev_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return model, os.cpu_count()
+
+
+def oracle_sample_rate(log2n: int, seed: int = 5):
+    """Oracle (variant A, single thread) on a cfg5-shaped sample -> (Gkeys/s, seconds)."""
+    import oracle
+    import workloads as W
+    k, v = W.cfg5(n=1 << log2n, seed=seed, device="cpu")
+    kn, vn = W.to_numpy(k), W.to_numpy(v)
+    t0 = time.perf_counter()
+    oracle.sort(kn, vn, variant=oracle.VARIANT_A)
+    dt = time.perf_counter() - t0
+    return (1 << log2n) / dt / 1e9, dt
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    model, ncpu = cpu_info()
+    import oracle
+    oracle.build()
+    for w in range(args.warmup):
+        oracle_sample_rate(min(args.ref_sample_log2, 20), seed=100 + w)
+    times = []
+    for s in range(args.steps):
+        _, dt = oracle_sample_rate(args.ref_sample_log2, seed=5 + s)
+        times.append(dt)
+    ms = 1000 * statistics.mean(times)
+    n_s = 1 << args.ref_sample_log2
+    val = n_s / (ms / 1000) / 1e9
+    sample = (f"cfg5-shaped sample of n=2^{args.ref_sample_log2} per step (seeds 5..{4 + args.steps}); "
+              "oracle variant A (copy-merge), single thread")
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+           "config": {"workload": WORKLOAD, "sample_n": n_s},
+           "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": sample, "cpu": model, "host_cores": ncpu},
+           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_27147_b200 as vm
+    import workloads as W
+    from paper_2605_27147_b200 import build as vbuild
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    vbuild.build()
+    vm.lib()
+
+    n = 1 << args.log2n
+    keys0, vals0 = W.cfg5(n=n, device=dev, rank=rank)
+    keys = torch.empty_like(keys0)
+    vals = torch.empty_like(vals0)
+    ws = vm.Workspace()
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (untimed)
+    stats = None
+    for w in range(max(args.warmup, 1)):
+        keys.copy_(keys0)
+        vals.copy_(vals0)
+        st = vm.sort_(keys, vals, workspace=ws, stats=(w == 0))
+        if w == 0:
+            stats = st
+    torch.cuda.synchronize()
+
+    # timed steps
+    vm.profile_enable(True)
+    clocks = ClockSampler(local)
+    step_ms, merge_ms, merge_bytes, phases, launches = [], [], [], [], 0
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for s in range(args.steps):
+        keys.copy_(keys0)
+        vals.copy_(vals0)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        vm.sort_(keys, vals, workspace=ws)
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        pr = vm.profile_read()
+        launches += pr.get("launches", 0)
+        if "merge_ms" in pr:
+            merge_ms.append(pr["merge_ms"])
+            merge_bytes.append(pr["merge_bytes"])
+            phases.append(pr)
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    vm.profile_enable(False)
+
+    # verify the last output (exact stable-sort properties on device)
+    a = keys.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    pv = vals.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    ok = bool((a[1:] >= a[:-1]).all()) and bool(((pv[1:] > pv[:-1]) | (a[1:] != a[:-1])).all())
+    del a, pv
+
+    t_local = statistics.mean(step_ms)
+    t = torch.tensor([t_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = n * world / (ms / 1000) / 1e9
+
+    peak, peak_src = load_peaks()
+    mm = statistics.mean(merge_ms) if merge_ms else None
+    mb = statistics.mean(merge_bytes) if merge_bytes else None
+    w_bytes = 8
+    M = stats["merge_cost_M"]
+    roof = None
+    if mm and mb:
+        achieved = mb / (mm / 1000) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "merge_level_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get("bytes_per_launch")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "kernel": "k_merge_level (all level launches of a step)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_step": mb, "merge_launches_per_step": phases[-1]["merge_launches"],
+                "kernel_ms_per_step": mm}
+    tree = {"bytes_2wM": 2 * w_bytes * M, "M_over_n": M / n,
+            "t_roof_ms_at_peak": 2 * w_bytes * M / (peak * 1e9) * 1000,
+            "frac_of_roofline": (2 * w_bytes * M / (peak * 1e9) * 1000) / ms,
+            "fused_M_share": stats["fused_M"] / M if M else 0.0}
+    ph = {}
+    if phases:
+        for key in ("plan_ms", "leaf_ms", "partition_ms", "merge_ms", "total_ms"):
+            ph[key] = statistics.mean(p[key] for p in phases)
+
+    # end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hk = torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)
+        hv = torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)
+        hk.copy_(keys0)
+        hv.copy_(vals0)
+        ok_ = torch.empty_like(hk)
+        ov_ = torch.empty_like(hv)
+        ks = max(1, min(args.steps, 3))
+        for _ in range(1):
+            keys.copy_(hk, non_blocking=True); vals.copy_(hv, non_blocking=True)
+            vm.sort_(keys, vals, workspace=ws)
+            ok_.copy_(keys, non_blocking=True); ov_.copy_(vals, non_blocking=True)
+        torch.cuda.synchronize()
+        barrier()
+        et = []
+        for _ in range(ks):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            keys.copy_(hk, non_blocking=True)
+            vals.copy_(hv, non_blocking=True)
+            vm.sort_(keys, vals, workspace=ws)
+            ok_.copy_(keys, non_blocking=True)
+            ov_.copy_(vals, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            et.append(e0.elapsed_time(e1))
+        te = torch.tensor([statistics.mean(et)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n * world / (float(te.item()) / 1000) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+               "ms_per_step": float(te.item()), "steps": ks}
+        del hk, hv, ok_, ov_
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        model, ncpu = cpu_info()
+        v, dt = oracle_sample_rate(args.cpu_sample_log2)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"cfg5-shaped sample n=2^{args.cpu_sample_log2} (seed 5), oracle variant A, "
+                         f"{dt:.1f} s single-threaded",
+               "cpu": model, "host_cores": ncpu}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+               "config": {"workload": WORKLOAD, "n_per_gpu": n, "n_total": n * world,
+                          "key": "u32", "payload": "u32", "scratch": "unbounded",
+                          "parallelism": f"dp{world}" if world > 1 else "single",
+                          "timing": "CUDA events around each sort on its stream; input restored "
+                                    "by an untimed 8 GiB device copy between steps (flushes L2)",
+                          "runs": stats["runs"], "merge_cost_M": M, "max_power": stats["max_power"],
+                          "levels_executed": stats["levels_executed"]},
+               "roofline": roof, "tree_roofline": tree, "phases_ms": ph,
+               "cpu_baseline": cpu, "e2e": e2e,
+               "gpu_launches": launches, "clocks": clk, "verified": ok}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

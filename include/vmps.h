@@ -1,0 +1,154 @@
+/*
+ * vmps.h -- C ABI of the B200-native (sm_100a) Virtual-Memory Powersort hot
+ * path (arXiv 2605.27147).  libvmps.so exports exactly the functions below.
+ *
+ * The operation.  vmps_sort_keys / vmps_sort_pairs compute the stable sort of
+ * n items (key, optional u32 payload) in place -- Alg. 1 "Abstract Powersort"
+ * sorts input[0,n) in place -- by merging the
+ * array's natural runs along the Powersort merge tree:
+ *   - runs: ExtractRun with minrun extension by insertion sort
+ *     ("l = ceil(l/2) until l < 64"); strictly descending runs are
+ *     reversed (BASELINE.json north_star; reading R3);
+ *   - node powers (Theorem): the power of the boundary between runs
+ *     [i,j) and [j,k) is the least p with an integer c such that
+ *     (i+j)/2n < c 2^-p <= (j+k)/2n;
+ *   - merges: every merge is stable, ties taken from the left run (Alg. 2,
+ *     P:657 "a[x_a] <= b[x_b]").
+ * The output is the unique stable sort (F1), bit-identical to the
+ * oracle.  vmps_merge_plan reports Alg. 1's merge sequence.
+ *
+ * Conventions (all functions):
+ *   - Pointers are DEVICE pointers unless the name starts with h_ (host).
+ *   - Key order: VMPS_KEY_U32 / VMPS_KEY_U64 unsigned; VMPS_KEY_F32 is a
+ *     total order in which -0.0 precedes +0.0, every NaN is greater than every
+ *     non-NaN and all NaNs compare equal (stable among themselves); output
+ *     keys keep their bit patterns (reading R5).
+ *   - n < 2^32 per call (32-bit positions inside the library); larger n
+ *     returns VMPS_ERR_INVALID_ARG.
+ *   - Ownership: keys, vals and ws are caller-owned and must stay valid until
+ *     the work enqueued on `stream` completes.  The library allocates no
+ *     device memory; it uses the caller's workspace (size from
+ *     vmps_workspace_bytes, 256-byte aligned).
+ *   - Asynchrony: all device work is enqueued on `stream` (0 = legacy
+ *     default stream).  Functions return after enqueueing, except that a
+ *     non-NULL h_stats / h_num_runs synchronises `stream` to read results.
+ *   - Errors: arguments are validated before anything is enqueued.
+ *       VMPS_ERR_INVALID_ARG  NULL pointer with n > 1, unknown key type,
+ *                             n >= 2^32, misaligned pointer (keys/vals must be
+ *                             16-byte aligned), cap_runs too small (the needed
+ *                             count is still written to *h_num_runs);
+ *       VMPS_ERR_BUDGET       ws_bytes smaller than vmps_workspace_bytes(), or
+ *                             scratch_elems below the bounded mode's minimum;
+ *       VMPS_ERR_CUDA         a CUDA launch/runtime error (detail:
+ *                             vmps_last_error());
+ *     n <= 1 is a no-op returning VMPS_OK.  There is no CPU fallback.
+ *   - Thread safety: calls on different streams with different workspaces may
+ *     run concurrently; the vmps_test_* hooks are process-global and are not.
+ */
+#ifndef VMPS_H
+#define VMPS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { VMPS_KEY_U32 = 0, VMPS_KEY_U64 = 1, VMPS_KEY_F32 = 2 } vmps_key_t;
+
+typedef enum {
+  VMPS_OK = 0,
+  VMPS_ERR_INVALID_ARG = 1,
+  VMPS_ERR_ALLOC = 2,
+  VMPS_ERR_BUDGET = 3,
+  VMPS_ERR_CUDA = 4,
+  VMPS_ERR_NCCL = 5,
+  VMPS_ERR_INTERNAL = 6
+} vmps_status_t;
+
+/* scratch_elems value selecting the unbounded (ping-pong) mode */
+#define VMPS_SCRATCH_UNBOUNDED (-1LL)
+
+/* Run kinds reported by vmps_merge_plan (bit flags). */
+#define VMPS_RUN_ASC 0u
+#define VMPS_RUN_DESC 1u /* strictly descending, reversed */
+#define VMPS_RUN_EXT 2u  /* shorter than minrun, extended by insertion sort */
+
+/* Statistics; filled only when a non-NULL h_stats is passed (synchronises). */
+typedef struct {
+  uint64_t n;
+  uint64_t runs;           /* r: runs after ExtractRun */
+  uint64_t merges;         /* r - 1 */
+  uint64_t merge_cost_M;   /* sum of merge input lengths */
+  uint64_t fused_M;        /* part of M executed inside block-local sorts */
+  uint64_t reversed_elems; /* elements of strictly descending runs */
+  uint64_t extended_runs;  /* runs extended to minrun */
+  uint32_t max_power;      /* largest node power */
+  uint32_t levels_executed;/* merge levels with at least one HBM merge */
+  uint32_t minrun;
+  uint32_t block_elems;    /* bounded mode: block size P_blk (0 if unbounded) */
+  uint64_t rounds;         /* bounded mode: merge rounds (0 if unbounded) */
+  uint64_t peak_extra_device_bytes; /* workspace bytes actually used */
+  uint64_t scratch_bytes;  /* element scratch part of it */
+  uint64_t metadata_bytes; /* plan / table / relocation metadata part of it */
+} vmps_stats_t;
+
+/* One merge of the plan: [i,j) with [j,k) at node power `power`; `order` is
+ * the rank in Alg. 1's execution order (records are written in that order). */
+typedef struct {
+  uint64_t i, j, k;
+  uint32_t power;
+  uint32_t order;
+} vmps_merge_rec_t;
+
+/* Workspace size for a sort (has_vals: payload present) or, with
+ * has_vals = -1, for vmps_merge_plan.  scratch_elems as in vmps_sort_*. */
+vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals,
+                                   int64_t scratch_elems, size_t* h_bytes);
+
+/* Stable in-place sort of keys[0,n) (layout: contiguous array of the key
+ * type).  scratch_elems: VMPS_SCRATCH_UNBOUNDED, or a cap on element scratch
+ * (bounded mode: the output is identical; BASELINE.json north_star (4)). */
+vmps_status_t vmps_sort_keys(void* keys, uint64_t n, vmps_key_t kt, int64_t scratch_elems,
+                             void* ws, size_t ws_bytes, void* stream, vmps_stats_t* h_stats);
+
+/* As vmps_sort_keys; vals[0,n) (u32) is permuted with its keys. */
+vmps_status_t vmps_sort_pairs(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt,
+                              int64_t scratch_elems, void* ws, size_t ws_bytes, void* stream,
+                              vmps_stats_t* h_stats);
+
+/* The merge plan of Alg. 1 for keys[0,n) (keys are only read):
+ * run_start[r] (ascending, run_start[0] = 0), run_kind[r] (VMPS_RUN_* bits),
+ * merges[r-1] in Alg. 1's execution order.  cap_runs = capacity of
+ * run_start/run_kind (merges needs cap_runs - 1).  *h_num_runs receives r
+ * (synchronises); if r > cap_runs nothing is written and
+ * VMPS_ERR_INVALID_ARG is returned. */
+vmps_status_t vmps_merge_plan(const void* keys, uint64_t n, vmps_key_t kt, uint64_t* run_start,
+                              uint8_t* run_kind, vmps_merge_rec_t* merges, uint64_t cap_runs,
+                              uint64_t* h_num_runs, void* ws, size_t ws_bytes, void* stream);
+
+/* Human-readable status; the last CUDA error detail of this thread. */
+const char* vmps_status_string(vmps_status_t s);
+const char* vmps_last_error(void);
+
+/* Bench hooks (process-global, not thread safe).  With profiling on, each
+ * sort records CUDA events on its stream around its phases; after the stream
+ * is synchronised, vmps_profile_read fills h_ms[0..cap): [0] run detection +
+ * plan, [1] leaf engine, [2] all level partitions, [3] all level merges,
+ * [4] total; h_launches[0] = kernels launched by the last sort, h_launches[1]
+ * = level-merge launches, h_bytes[0] = algorithmic bytes of the level merges
+ * (2 w (M - fused M)).  Returns the number of values written. */
+void vmps_profile_enable(int on);
+int vmps_profile_read(double* h_ms, int cap, uint64_t* h_launches, uint64_t* h_bytes);
+
+/* Test-only hooks (process-global, not thread safe).  minrun = 0 restores
+ * the paper's rule; otherwise 1..64 forces minrun.  Z (fused-subtree limit),
+ * T_out (merge tile) and P_blk (bounded block) = 0 restore defaults. */
+void vmps_test_set_minrun(uint32_t minrun);
+void vmps_test_set_tiles(uint32_t fuse_z, uint32_t merge_tile, uint32_t block_elems);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

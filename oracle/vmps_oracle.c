@@ -64,7 +64,8 @@ typedef struct ctx {
   int key_type;
   uint64_t n;
   uint64_t minrun;
-  item* a;               /* the input array, as items */
+  item* a;               /* the input array, as items (NULL in the plan-only pass) */
+  const void* raw;       /* plan-only pass: the caller's keys, read in place */
   uint64_t* counter;     /* comparison counter currently charged */
   orc_stats_t* st;
   /* plan output */
@@ -82,6 +83,19 @@ typedef struct ctx {
 static int less(ctx* c, const item* x, const item* y) {
   (*c->counter)++;
   return orc_less(c->key_type, x->key, y->key);
+}
+
+/* key of input position i for run detection (items, or raw keys when dry) */
+static uint64_t key_at(const ctx* c, uint64_t i) {
+  if (c->a) return c->a[i].key;
+  if (c->key_type == ORC_U64) return ((const uint64_t*)c->raw)[i];
+  return ((const uint32_t*)c->raw)[i];
+}
+
+/* "a[x] < a[y]" on the unmodified input, counted */
+static int less_at(ctx* c, uint64_t x, uint64_t y) {
+  (*c->counter)++;
+  return orc_less(c->key_type, key_at(c, x), key_at(c, y));
 }
 
 /* ------------------------------------------------------------------------ */
@@ -138,15 +152,15 @@ uint64_t orc_page_size(uint64_t n, uint32_t T) {
 /* Natural run scan on the unmodified input a[s..n): returns its end e and
  * whether it is strictly descending.  Reads only positions >= s, which no
  * earlier run has touched (Alg. 1 consumes work left to right). */
-static uint64_t natural_run(ctx* c, const item* a, uint64_t s, int* desc) {
+static uint64_t natural_run(ctx* c, uint64_t s, int* desc) {
   uint64_t n = c->n, e;
-  if (s + 1 < n && less(c, &a[s + 1], &a[s])) {
+  if (s + 1 < n && less_at(c, s + 1, s)) {
     e = s + 2;
-    while (e < n && less(c, &a[e], &a[e - 1])) e++;
+    while (e < n && less_at(c, e, e - 1)) e++;
     *desc = 1;
   } else {
     e = s + 1;
-    while (e < n && !less(c, &a[e], &a[e - 1])) e++;
+    while (e < n && !less_at(c, e, e - 1)) e++;
     *desc = 0;
   }
   return e;
@@ -197,9 +211,8 @@ static void emit_run(ctx* c, uint64_t s, uint8_t kind) {
 }
 
 /* The run [s, e) with its kind, per ExtractRun: returns e. */
-static uint64_t run_bounds(ctx* c, const item* a, uint64_t s, int* desc, uint64_t* nat_end,
-                           uint8_t* kind) {
-  uint64_t e = natural_run(c, a, s, desc);
+static uint64_t run_bounds(ctx* c, uint64_t s, int* desc, uint64_t* nat_end, uint8_t* kind) {
+  uint64_t e = natural_run(c, s, desc);
   *nat_end = e;
   *kind = *desc ? ORC_KIND_DESC : ORC_KIND_ASC;
   if (e - s < c->minrun) {
@@ -278,7 +291,7 @@ static buf a_extract_run(ctx* c, uint64_t s) {
   int desc;
   uint64_t nat;
   uint8_t kind;
-  uint64_t e = run_bounds(c, c->a, s, &desc, &nat, &kind);
+  uint64_t e = run_bounds(c, s, &desc, &nat, &kind);
   accessor r = {arr_at, c->a + s};
   if (desc) reverse_run(c, &r, nat - s);
   if (e > nat) insertion_extend(c, &r, nat - s, e - s);
@@ -470,7 +483,7 @@ static buf b_extract_run(ctx* c, uint64_t s) {
   uint8_t kind;
   /* work's remaining elements still sit at their original positions (input
    * pages are only reused after being fully popped), so scan a[] directly */
-  uint64_t e = run_bounds(c, c->a, s, &desc, &nat, &kind);
+  uint64_t e = run_bounds(c, s, &desc, &nat, &kind);
   int h = vm_new_pbuf(c);
   for (uint64_t t = s; t < e; ++t) {
     item it = pbuf_pop_front(c, c->vm->work);
@@ -593,7 +606,7 @@ static buf d_extract_run(ctx* c, uint64_t s) {
   int desc;
   uint64_t nat;
   uint8_t kind;
-  uint64_t e = run_bounds(c, c->a, s, &desc, &nat, &kind);
+  uint64_t e = run_bounds(c, s, &desc, &nat, &kind);
   emit_run(c, s, kind);
   buf b = {s, e, 0};
   return b;
@@ -629,11 +642,14 @@ static int run_common(int key_type, void* keys, uint32_t* vals, uint64_t n, int 
   c.run_kind = run_kind;
   c.cap_runs = cap_runs;
   c.merges = merges;
-  c.a = (item*)malloc(n * sizeof(item));
-  if (!c.a) return ORC_ENOMEM;
-  for (uint64_t t = 0; t < n; ++t) {
-    c.a[t].key = key_type == ORC_U64 ? ((const uint64_t*)keys)[t] : ((const uint32_t*)keys)[t];
-    c.a[t].val = vals ? vals[t] : (uint32_t)t;
+  c.raw = keys;
+  if (!dry) {
+    c.a = (item*)malloc(n * sizeof(item));
+    if (!c.a) return ORC_ENOMEM;
+    for (uint64_t t = 0; t < n; ++t) {
+      c.a[t].key = key_type == ORC_U64 ? ((const uint64_t*)keys)[t] : ((const uint32_t*)keys)[t];
+      c.a[t].val = vals ? vals[t] : (uint32_t)t;
+    }
   }
   strategy S;
   if (dry) {

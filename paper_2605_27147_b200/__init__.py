@@ -1,0 +1,233 @@
+"""B200-native (sm_100a) Virtual-Memory Powersort hot path -- Python binding.
+
+Thin ctypes marshalling over ``libvmps.so`` (C ABI in ``include/vmps.h``):
+torch supplies device memory, the current CUDA stream and (for the
+multi-GPU path) process groups; every step of the sort runs in the library's
+CUDA kernels.  There is no CPU fallback: importing works anywhere, but any
+call raises if ``libvmps.so`` is missing or no CUDA device is present.
+
+Names follow include/vmps.h: ``sort_`` (vmps_sort_keys / vmps_sort_pairs),
+``merge_plan`` (vmps_merge_plan), ``workspace_bytes``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvmps.so")
+
+KEY_U32, KEY_U64, KEY_F32 = 0, 1, 2
+SCRATCH_UNBOUNDED = -1
+RUN_ASC, RUN_DESC, RUN_EXT = 0, 1, 2
+
+_STATUS = {0: "ok", 1: "invalid argument", 2: "allocation failed", 3: "budget too small",
+           4: "CUDA error", 5: "NCCL error", 6: "internal error"}
+
+
+class VmpsError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str = ""):
+        self.status = status
+        super().__init__(f"{where}: {_STATUS.get(status, status)}" + (f" ({detail})" if detail else ""))
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("runs", ctypes.c_uint64), ("merges", ctypes.c_uint64),
+                ("merge_cost_M", ctypes.c_uint64), ("fused_M", ctypes.c_uint64),
+                ("reversed_elems", ctypes.c_uint64), ("extended_runs", ctypes.c_uint64),
+                ("max_power", ctypes.c_uint32), ("levels_executed", ctypes.c_uint32),
+                ("minrun", ctypes.c_uint32), ("block_elems", ctypes.c_uint32),
+                ("rounds", ctypes.c_uint64), ("peak_extra_device_bytes", ctypes.c_uint64),
+                ("scratch_bytes", ctypes.c_uint64), ("metadata_bytes", ctypes.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+class MergeRec(ctypes.Structure):
+    _fields_ = [("i", ctypes.c_uint64), ("j", ctypes.c_uint64), ("k", ctypes.c_uint64),
+                ("power", ctypes.c_uint32), ("order", ctypes.c_uint32)]
+
+
+EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_merge_plan",
+           "vmps_status_string", "vmps_last_error", "vmps_profile_enable", "vmps_profile_read",
+           "vmps_test_set_minrun", "vmps_test_set_tiles")
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libvmps.so (built in-tree by ``build.py``); raise loudly if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2605_27147_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, u64, i64, sz = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64, ctypes.c_size_t
+        L.vmps_workspace_bytes.argtypes = [u64, ctypes.c_int, ctypes.c_int, i64, ctypes.POINTER(sz)]
+        L.vmps_sort_keys.argtypes = [vp, u64, ctypes.c_int, i64, vp, sz, vp, ctypes.POINTER(Stats)]
+        L.vmps_sort_pairs.argtypes = [vp, vp, u64, ctypes.c_int, i64, vp, sz, vp, ctypes.POINTER(Stats)]
+        L.vmps_merge_plan.argtypes = [vp, u64, ctypes.c_int, vp, vp, vp, u64, ctypes.POINTER(u64),
+                                      vp, sz, vp]
+        for f in ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_merge_plan"):
+            getattr(L, f).restype = ctypes.c_int
+        L.vmps_status_string.restype = ctypes.c_char_p
+        L.vmps_status_string.argtypes = [ctypes.c_int]
+        L.vmps_last_error.restype = ctypes.c_char_p
+        L.vmps_last_error.argtypes = []
+        L.vmps_profile_enable.argtypes = [ctypes.c_int]
+        L.vmps_profile_enable.restype = None
+        L.vmps_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                                        ctypes.POINTER(u64), ctypes.POINTER(u64)]
+        L.vmps_profile_read.restype = ctypes.c_int
+        L.vmps_test_set_minrun.argtypes = [ctypes.c_uint32]
+        L.vmps_test_set_minrun.restype = None
+        L.vmps_test_set_tiles.argtypes = [ctypes.c_uint32] * 3
+        L.vmps_test_set_tiles.restype = None
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise VmpsError(rc, where, lib().vmps_last_error().decode())
+
+
+def key_type(t: torch.Tensor) -> int:
+    if t.dtype in (torch.uint32, torch.int32):
+        return KEY_U32
+    if t.dtype in (torch.uint64, torch.int64):
+        return KEY_U64
+    if t.dtype == torch.float32:
+        return KEY_F32
+    raise TypeError(f"unsupported key dtype {t.dtype} (u32/u64/f32; int32/int64 are read as unsigned)")
+
+
+def workspace_bytes(n: int, kt: int, has_vals: int, scratch: int = SCRATCH_UNBOUNDED) -> int:
+    out = ctypes.c_size_t(0)
+    _check(lib().vmps_workspace_bytes(n, kt, has_vals, scratch, ctypes.byref(out)),
+           "vmps_workspace_bytes")
+    return int(out.value)
+
+
+class Workspace:
+    """A reusable device workspace (grown on demand) for repeated sorts."""
+
+    def __init__(self, device=None):
+        self.device = torch.device(device) if device is not None else None
+        self.buf = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
+            self.buf = None
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_default_ws: dict = {}
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def sort_(keys: torch.Tensor, values: torch.Tensor | None = None, scratch: int | None = None,
+          stats: bool = False, workspace: Workspace | None = None):
+    """Stable in-place sort of a contiguous CUDA tensor of u32/u64/f32 keys
+    (optionally permuting a u32/int32 payload) on the current stream.
+    Returns a stats dict when ``stats`` (synchronises), else None."""
+    if not keys.is_cuda:
+        raise ValueError("keys must be a CUDA tensor (no CPU fallback)")
+    if not keys.is_contiguous() or keys.dim() != 1:
+        raise ValueError("keys must be a contiguous 1-D tensor")
+    kt = key_type(keys)
+    n = keys.numel()
+    if values is not None:
+        if values.dtype not in (torch.uint32, torch.int32) or values.numel() != n:
+            raise ValueError("values must be u32/int32 with the same length as keys")
+        if not values.is_contiguous() or values.device != keys.device:
+            raise ValueError("values must be contiguous on the keys' device")
+    sc = SCRATCH_UNBOUNDED if scratch is None else int(scratch)
+    nbytes = workspace_bytes(n, kt, 1 if values is not None else 0, sc)
+    ws = workspace if workspace is not None else _default_ws.setdefault(keys.device, Workspace())
+    buf = ws.get(nbytes, keys.device)
+    st = Stats()
+    sp = ctypes.byref(st) if stats else None
+    L = lib()
+    with torch.cuda.device(keys.device):
+        s = _stream_ptr(keys.device)
+        if values is None:
+            rc = L.vmps_sort_keys(keys.data_ptr(), n, kt, sc, buf.data_ptr(), buf.numel(), s, sp)
+            _check(rc, "vmps_sort_keys")
+        else:
+            rc = L.vmps_sort_pairs(keys.data_ptr(), values.data_ptr(), n, kt, sc, buf.data_ptr(),
+                                   buf.numel(), s, sp)
+            _check(rc, "vmps_sort_pairs")
+    return st.as_dict() if stats else None
+
+
+@dataclass
+class Plan:
+    run_start: torch.Tensor  # int64 [r] (device)
+    run_kind: torch.Tensor   # uint8 [r] (device), RUN_* bits
+    merges: torch.Tensor     # int64 [r-1, 4] (i, j, k, power) in Alg. 1's execution order
+
+
+def merge_plan(keys: torch.Tensor, workspace: Workspace | None = None) -> Plan:
+    """Alg. 1's merge plan of a CUDA key tensor (keys are only read)."""
+    if not keys.is_cuda or not keys.is_contiguous() or keys.dim() != 1:
+        raise ValueError("keys must be a contiguous 1-D CUDA tensor")
+    kt = key_type(keys)
+    n = keys.numel()
+    dev = keys.device
+    nbytes = workspace_bytes(n, kt, -1)
+    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    buf = ws.get(nbytes, dev)
+    L = lib()
+    nr = ctypes.c_uint64(0)
+    cap = max(n, 1)
+    # run count bound: n // minrun + 2 (minrun from the paper's rule or the test hook)
+    rs = torch.empty(cap + 1, dtype=torch.int64, device=dev)
+    rk = torch.empty(cap + 1, dtype=torch.uint8, device=dev)
+    mg = torch.empty((cap + 1) * 4, dtype=torch.int64, device=dev)  # 32-byte records
+    with torch.cuda.device(dev):
+        rc = L.vmps_merge_plan(keys.data_ptr(), n, kt, rs.data_ptr(), rk.data_ptr(), mg.data_ptr(),
+                               cap, ctypes.byref(nr), buf.data_ptr(), buf.numel(), _stream_ptr(dev))
+        _check(rc, "vmps_merge_plan")
+    r = int(nr.value)
+    recs = mg[: 4 * max(r - 1, 0)].view(-1, 4)
+    power = (recs[:, 3] & 0xFFFFFFFF)
+    merges = torch.stack([recs[:, 0], recs[:, 1], recs[:, 2], power], dim=1)
+    return Plan(rs[:r], rk[:r], merges)
+
+
+def profile_enable(on: bool = True) -> None:
+    """Bench hook: record CUDA events around each phase of every sort."""
+    lib().vmps_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """Phase times (ms) of the last sort (its stream must be synchronised)."""
+    ms = (ctypes.c_double * 5)()
+    nl = (ctypes.c_uint64 * 2)()
+    nb = (ctypes.c_uint64 * 3)()
+    k = lib().vmps_profile_read(ms, 5, nl, nb)
+    out = {"launches": int(nl[0]), "merge_launches": int(nl[1])}
+    if k == 5:
+        out.update(plan_ms=ms[0], leaf_ms=ms[1], partition_ms=ms[2], merge_ms=ms[3], total_ms=ms[4],
+                   merge_bytes=int(nb[0]), M=int(nb[1]), fused_M=int(nb[2]))
+    return out
+
+
+def test_set_minrun(m: int) -> None:
+    """Test hook: force minrun (0 = the paper's rule)."""
+    lib().vmps_test_set_minrun(m)
+
+
+def test_set_tiles(fuse_z: int = 0, merge_tile: int = 0, block_elems: int = 0) -> None:
+    """Test hook: shrink fused-subtree / merge-tile / bounded-block sizes (0 = default)."""
+    lib().vmps_test_set_tiles(fuse_z, merge_tile, block_elems)

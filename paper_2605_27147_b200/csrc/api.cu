@@ -1,0 +1,585 @@
+// api.cu -- C ABI (include/vmps.h) and stream-ordered orchestration of the
+// hot path: run detection -> powers / merge tree / schedule -> leaf engine ->
+// one partition + one merge launch per tree level.  No host synchronisation
+// happens between launches; only h_stats / h_num_runs read results back.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "engine.cuh"
+#include "plan.cuh"
+#include "runs.cuh"
+#include "vmps_internal.cuh"
+
+namespace vmps {
+
+static uint32_t g_minrun_override = 0;
+static uint32_t g_fuse_z = 0;
+static uint32_t g_tout = 0;
+static uint32_t g_blk = 0;
+static thread_local std::string g_err;
+
+// ---- bench profiling (process-global) ----
+static bool g_prof = false;
+static cudaEvent_t g_ev[256];
+static bool g_ev_init = false;
+static int g_ev_n = 0;
+static uint64_t g_nl = 0;         // kernels launched by the current sort
+static uint64_t g_nl_merge = 0;   // level-merge launches
+static int g_prof_lvl[128][2];    // (start, end) event index per merge launch
+static int g_prof_part[128][2];   // per partition launch
+static int g_prof_nm = 0, g_prof_np = 0;
+static int g_prof_mark[4] = {-1, -1, -1, -1};  // begin, after plan, after leaf, end
+static unsigned long long* g_prof_host = nullptr;  // pinned copy of counters
+static int g_prof_wbytes = 0;
+
+static int prof_event(cudaStream_t s) {
+  if (!g_prof || g_ev_n >= 256) return -1;
+  if (!g_ev_init) {
+    for (int i = 0; i < 256; ++i) cudaEventCreate(&g_ev[i]);
+    cudaHostAlloc((void**)&g_prof_host, 64, cudaHostAllocDefault);
+    g_ev_init = true;
+  }
+  cudaEventRecord(g_ev[g_ev_n], s);
+  return g_ev_n++;
+}
+static void prof_reset() {
+  g_ev_n = 0;
+  g_nl = 0;
+  g_nl_merge = 0;
+  g_prof_nm = g_prof_np = 0;
+  for (int i = 0; i < 4; ++i) g_prof_mark[i] = -1;
+}
+
+static uint32_t minrun_rule(uint64_t n) {
+  uint64_t l = n;
+  while (l >= 64) l = (l + 1) / 2;
+  return (uint32_t)l;
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t scan_tmp_words(size_t len) {
+  size_t nb = (len + SCAN_TILE - 1) / SCAN_TILE;
+  if (nb <= 1) return 2;
+  return 2 * nb + scan_tmp_words(nb);
+}
+
+struct Cfg {
+  uint64_t n;
+  int kt;
+  int hv;         // 1 with payload, 0 keys only, -1 plan only
+  uint32_t minrun, fuse_z, tout;
+};
+
+static Cfg make_cfg(uint64_t n, int kt, int hv) {
+  Cfg c;
+  c.n = n;
+  c.kt = kt;
+  c.hv = hv;
+  c.minrun = g_minrun_override ? g_minrun_override : minrun_rule(n);
+  c.fuse_z = g_fuse_z ? g_fuse_z : DEFAULT_FUSE_Z;
+  c.tout = g_tout ? g_tout : DEFAULT_TOUT;
+  return c;
+}
+
+static size_t key_bytes(int kt) { return kt == VMPS_KEY_U64 ? 8 : 4; }
+
+// Carve the workspace; with base == nullptr only the size is computed.
+static size_t carve(const Cfg& c, Work* w, char* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> void* {
+    void* p = base ? (void*)(base + off) : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  const uint64_t n = c.n;
+  Work t;
+  memset(&t, 0, sizeof(t));
+  t.n = (uint32_t)n;
+  t.minrun = c.minrun;
+  t.ns = 3 * c.minrun;
+  t.ntiles = (uint32_t)((n + RT - 1) / RT);
+  t.rmax = (uint32_t)(n / std::max<uint32_t>(c.minrun, 1) + 2);
+  t.fuse_z = c.fuse_z;
+  t.tout = c.tout;
+  t.kt = c.kt;
+  t.has_vals = c.hv;
+  const size_t R = (size_t)t.rmax + 2;
+  if (c.hv >= 0) {
+    t.k1 = take(n * key_bytes(c.kt));
+    t.v1 = c.hv ? (uint32_t*)take(n * 4) : nullptr;
+  }
+  t.bits = (uint32_t*)take(((size_t)t.ntiles * RT_WORDS + RT_WORDS + 8) * 4);
+  t.tile_tab = (uint32_t*)take((size_t)t.ntiles * t.ns * 4);
+  uint32_t m = t.ntiles;
+  t.chain_m[0] = m;
+  t.chain_levels = 0;
+  while (m > (uint32_t)CHAIN_G) {
+    m = (m + CHAIN_G - 1) / CHAIN_G;
+    t.chain_tab[t.chain_levels] = (uint64_t*)take((size_t)m * t.ns * 8);
+    t.chain_levels++;
+    t.chain_m[t.chain_levels] = m;
+  }
+  for (int l = 0; l <= t.chain_levels; ++l) t.chain_entry[l] = (uint64_t*)take((size_t)t.chain_m[l] * 8);
+  t.run_start = (uint32_t*)take(R * 4);
+  t.run_kind = (uint8_t*)take(R);
+  t.scalars = (uint32_t*)take(SC_COUNT * 4 + 64);
+  t.power = (uint8_t*)take(R);
+  t.seg_l = (uint32_t*)take(R * 4);
+  t.seg_r = (uint32_t*)take(R * 4);
+  t.parent = (uint32_t*)take(R * 4);
+  t.anc[0] = (uint32_t*)take(R * 4);
+  t.anc[1] = (uint32_t*)take(R * 4);
+  t.dep[0] = (uint32_t*)take(R * 4);
+  t.dep[1] = (uint32_t*)take(R * 4);
+  if (c.hv >= 0) {
+    t.unit_flag = (uint32_t*)take(R * 4);
+    t.long_flag = (uint32_t*)take(R * 4);
+    t.unit_end = (uint32_t*)take(R * 4);
+    t.unit_par = (uint8_t*)take(R);
+    t.long_par = (uint8_t*)take(R);
+    t.unit_idx = (uint32_t*)take(R * 4);
+    t.long_idx = (uint32_t*)take(R * 4);
+    t.units = (uint32_t*)take(R * 3 * 4);
+    t.longs = (uint32_t*)take(R * 4 * 4);
+    t.long_chunks = (uint32_t*)take(R * 4);
+    t.long_off = (uint32_t*)take(R * 4);
+    t.level_cnt = (uint32_t*)take((LEVEL_SLOTS + 1) * 4);
+    t.level_start = (uint32_t*)take((LEVEL_SLOTS + 1) * 4);
+    t.level_fill = (uint32_t*)take((LEVEL_SLOTS + 1) * 4);
+    t.level_tile = (uint32_t*)take((LEVEL_SLOTS + 1) * 4);
+    t.lnodes = (uint32_t*)take(R * 4);
+    t.ltiles = (uint32_t*)take(R * 4);
+    t.ltiles_cnt = (uint32_t*)take(R * 4);
+    t.part_cap = (uint32_t)(n / c.tout + R + 2);
+    t.part = (uint2*)take((size_t)t.part_cap * 8);
+    t.scan_tmp = (uint32_t*)take(scan_tmp_words(R) * 4 + 64);
+  }
+  t.counters = (unsigned long long*)take(8 * 8);
+  t.used_bytes = off;
+  if (w) *w = t;
+  return off;
+}
+
+static int g_nsm = 0;
+static int nsm() {
+  if (!g_nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (g_nsm <= 0) g_nsm = 148;
+  }
+  return g_nsm;
+}
+
+static unsigned grid_for(size_t items, unsigned threads = 256) {
+  size_t g = (items + threads - 1) / threads;
+  size_t cap = (size_t)nsm() * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+// Exclusive scan of len u32 (out[len-1] meaningful); tmp from scan_tmp_words.
+static void scan_u32(const uint32_t* in, uint32_t* out, uint32_t len, uint32_t* tmp, cudaStream_t s) {
+  uint32_t nb = (len + SCAN_TILE - 1) / SCAN_TILE;
+  k_scan_tiles<<<nb, SCAN_THREADS, 0, s>>>(in, out, len, tmp);
+  ++g_nl;
+  if (nb > 1) {
+    scan_u32(tmp, tmp + nb, nb, tmp + 2 * nb, s);
+    k_scan_add<<<nb, SCAN_THREADS, 0, s>>>(out, len, tmp + nb);
+    ++g_nl;
+  }
+}
+
+#define VMPS_CK(call)                                                      \
+  do {                                                                     \
+    cudaError_t e_ = (call);                                               \
+    if (e_ != cudaSuccess) {                                               \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(e_);         \
+      return VMPS_ERR_CUDA;                                                \
+    }                                                                      \
+  } while (0)
+
+static vmps_status_t launch_check() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_err = std::string("kernel launch: ") + cudaGetErrorString(e);
+    return VMPS_ERR_CUDA;
+  }
+  return VMPS_OK;
+}
+
+static bool g_chain_attrs = false;
+static vmps_status_t chain_attrs() {
+  if (g_chain_attrs) return VMPS_OK;
+  const int sm = CHAIN_G * MAX_NS * 8;
+  VMPS_CK(cudaFuncSetAttribute(k_chain_compose<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  VMPS_CK(cudaFuncSetAttribute(k_chain_compose<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  VMPS_CK(cudaFuncSetAttribute(k_chain_expand<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  VMPS_CK(cudaFuncSetAttribute(k_chain_expand<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  g_chain_attrs = true;
+  return VMPS_OK;
+}
+
+// Launch helper: counts kernels for the bench's gpu_launches.
+#define LAUNCH(kern, grid, block, smem, stream, ...)           \
+  do {                                                          \
+    kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);   \
+    ++g_nl;                                                     \
+  } while (0)
+
+// Run detection + plan front half (shared by sort and merge_plan).
+template <int KT>
+static vmps_status_t front_half(const Work& w, const void* keys, cudaStream_t s) {
+  using K = typename KeyTraits<KT>::K;
+  vmps_status_t arc = chain_attrs();
+  if (arc != VMPS_OK) return arc;
+  VMPS_CK(cudaMemsetAsync(w.scalars, 0, SC_COUNT * 4, s));
+  VMPS_CK(cudaMemsetAsync(w.counters, 0, 8 * 8, s));
+  LAUNCH(k_runs_tables<KT>, w.ntiles, 128, 0, s, (const K*)keys, w.n, w.minrun, w.ns, w.bits, w.tile_tab);
+  // compose the chain of tile tables (level 0 = u32 tile tables, above = u64)
+  const size_t sm32 = (size_t)CHAIN_G * w.ns * 4, sm64 = (size_t)CHAIN_G * w.ns * 8;
+  for (int l = 0; l < w.chain_levels; ++l) {
+    if (l == 0)
+      LAUNCH(k_chain_compose<uint32_t>, w.chain_m[1], 256, sm32, s, w.tile_tab, w.chain_m[0], w.ns, w.chain_tab[0]);
+    else
+      LAUNCH(k_chain_compose<uint64_t>, w.chain_m[l + 1], 256, sm64, s, w.chain_tab[l - 1], w.chain_m[l], w.ns,
+             w.chain_tab[l]);
+  }
+  const int top = w.chain_levels;
+  if (top == 0)
+    LAUNCH(k_chain_top<uint32_t>, 1, 32, 0, s, w.tile_tab, w.chain_m[0], w.ns, w.chain_entry[0]);
+  else
+    LAUNCH(k_chain_top<uint64_t>, 1, 32, 0, s, w.chain_tab[top - 1], w.chain_m[top], w.ns, w.chain_entry[top]);
+  for (int l = top - 1; l >= 0; --l) {
+    if (l == 0)
+      LAUNCH(k_chain_expand<uint32_t>, w.chain_m[1], 256, sm32, s, w.tile_tab, w.chain_m[0], w.ns,
+             w.chain_entry[1], w.chain_entry[0]);
+    else
+      LAUNCH(k_chain_expand<uint64_t>, w.chain_m[l + 1], 256, sm64, s, w.chain_tab[l - 1], w.chain_m[l], w.ns,
+             w.chain_entry[l + 1], w.chain_entry[l]);
+  }
+  LAUNCH(k_runs_emit, w.ntiles, 32, 0, s, w.bits, w.n, w.minrun, w.chain_entry[0], w.run_start, w.run_kind,
+         w.scalars);
+  const unsigned g = grid_for(w.rmax);
+  LAUNCH(k_powers_seg, g, 256, 0, s, w.run_start, w.n, w.scalars, w.power, w.seg_l, w.seg_r);
+  LAUNCH(k_parent_init, g, 256, 0, s, w.scalars, w.power, w.seg_l, w.seg_r, w.parent, w.anc[0], w.dep[0]);
+  // depth <= max power <= 34 < 64: six rounds of pointer jumping (result in dep[0])
+  for (int rnd = 0; rnd < 6; ++rnd) {
+    int a = rnd & 1;
+    LAUNCH(k_jump, g, 256, 0, s, w.scalars, w.anc[a], w.dep[a], w.anc[a ^ 1], w.dep[a ^ 1]);
+  }
+  return launch_check();
+}
+
+static bool kernel_attrs_set[3][2] = {{false, false}, {false, false}, {false, false}};
+
+template <int KT, bool HV>
+static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaStream_t s,
+                               vmps_stats_t* st) {
+  using K = typename KeyTraits<KT>::K;
+  prof_reset();
+  g_prof_mark[0] = prof_event(s);
+  vmps_status_t rc = front_half<KT>(w, keys, s);
+  if (rc != VMPS_OK) return rc;
+  const uint32_t* dep = w.dep[0];
+  const unsigned g = grid_for(w.rmax);
+  VMPS_CK(cudaMemsetAsync(w.level_cnt, 0, (LEVEL_SLOTS + 1) * 4, s));
+  VMPS_CK(cudaMemsetAsync(w.level_fill, 0, (LEVEL_SLOTS + 1) * 4, s));
+  LAUNCH(k_class_nodes, g, 256, 0, s, w.run_start, w.scalars, w.counters, w.power, w.seg_l, w.seg_r, w.parent,
+         dep, w.fuse_z, w.unit_end, w.unit_par, w.level_cnt);
+  LAUNCH(k_class_runs, g, 256, 0, s, w.run_start, w.run_kind, w.scalars, w.power, w.seg_l, w.seg_r, dep,
+         w.fuse_z, w.rmax, w.unit_flag, w.long_flag, w.unit_end, w.unit_par, w.long_par);
+  scan_u32(w.unit_flag, w.unit_idx, w.rmax + 1, w.scan_tmp, s);
+  scan_u32(w.long_flag, w.long_idx, w.rmax + 1, w.scan_tmp, s);
+  LAUNCH(k_compact, g, 256, 0, s, w.run_start, w.scalars, w.unit_flag, w.unit_idx, w.long_flag, w.long_idx,
+         w.unit_end, w.unit_par, w.long_par, w.units, w.longs, w.long_chunks);
+  LAUNCH(k_zero_tail, g, 256, 0, s, w.long_chunks, w.scalars, (int)SC_LONG, w.rmax);
+  scan_u32(w.long_chunks, w.long_off, w.rmax + 1, w.scan_tmp, s);
+  LAUNCH(k_level_scan, 1, 32, 0, s, w.level_cnt, w.level_start, w.scalars);
+  LAUNCH(k_level_scatter, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.fuse_z,
+         w.level_start, w.level_fill, w.lnodes);
+  LAUNCH(k_level_tiles, g, 256, 0, s, w.run_start, w.scalars, w.seg_l, w.seg_r, w.lnodes, w.tout, w.rmax,
+         w.ltiles_cnt);
+  scan_u32(w.ltiles_cnt, w.ltiles, w.rmax + 1, w.scan_tmp, s);
+  LAUNCH(k_level_tile_off, 1, 128, 0, s, w.level_start, w.ltiles, w.level_tile);
+  rc = launch_check();
+  if (rc != VMPS_OK) return rc;
+  g_prof_mark[1] = prof_event(s);
+
+  // leaf engine
+  K* k0 = (K*)keys;
+  K* k1 = (K*)w.k1;
+  uint32_t* v0 = vals;
+  uint32_t* v1 = w.v1;
+  const size_t lsm = leaf_smem_bytes<KT>(HV);
+  if (!kernel_attrs_set[KT][HV]) {
+    VMPS_CK(cudaFuncSetAttribute(k_leaf_sort<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    kernel_attrs_set[KT][HV] = true;
+  }
+  const uint32_t nbatch = (uint32_t)((w.n + w.fuse_z - 1) / w.fuse_z);
+  LAUNCH((k_leaf_sort<KT, HV>), nbatch, LEAF_THREADS, lsm, s, k0, v0, k1, v1, w.units, w.scalars, w.fuse_z);
+  LAUNCH((k_long_leaves<KT, HV>), nsm() * 8, 256, 0, s, k0, v0, k1, v1, w.longs, w.long_off, w.scalars,
+         LONG_CHUNK);
+  rc = launch_check();
+  if (rc != VMPS_OK) return rc;
+  g_prof_mark[2] = prof_event(s);
+
+  // level merges, highest power first (children before parents, F3)
+  double lg = std::log2(2.0 * (double)w.n / (double)w.fuse_z);
+  int p_hi = (int)std::ceil(lg) + 1;
+  if (p_hi > LEVEL_SLOTS - 2) p_hi = LEVEL_SLOTS - 2;
+  if (p_hi < 1) p_hi = 1;
+  const unsigned gm = (unsigned)(nsm() * 8);
+  for (int p = p_hi; p >= 1; --p) {
+    int e0 = prof_event(s);
+    LAUNCH(k_partition<KT>, nsm() * 4, 256, 0, s, k0, k1, w.run_start, w.seg_l, w.seg_r, dep, w.lnodes,
+           w.ltiles, w.level_start, w.level_tile, p, w.tout, w.part);
+    int e1 = prof_event(s);
+    LAUNCH((k_merge_level<KT, HV>), gm, MERGE_BLOCK, 0, s, k0, v0, k1, v1, w.run_start, w.seg_l, w.seg_r, dep,
+           w.lnodes, w.ltiles, w.level_tile, p, w.tout, w.part);
+    ++g_nl_merge;
+    int e2 = prof_event(s);
+    if (g_prof && e0 >= 0 && e2 >= 0 && g_prof_nm < 128) {
+      g_prof_part[g_prof_np][0] = e0; g_prof_part[g_prof_np][1] = e1; g_prof_np++;
+      g_prof_lvl[g_prof_nm][0] = e1; g_prof_lvl[g_prof_nm][1] = e2; g_prof_nm++;
+    }
+  }
+  LAUNCH(k_check_levels, 1, 32, 0, s, w.level_cnt, p_hi, w.scalars);
+  rc = launch_check();
+  if (rc != VMPS_OK) return rc;
+  g_prof_mark[3] = prof_event(s);
+  if (g_prof && g_prof_host) {
+    VMPS_CK(cudaMemcpyAsync(g_prof_host, w.counters, 16, cudaMemcpyDeviceToHost, s));
+    g_prof_wbytes = (int)(key_bytes(w.kt) + (HV ? 4 : 0));
+  }
+
+  if (st) {
+    uint32_t sc[SC_COUNT];
+    unsigned long long ct[8];
+    uint32_t lc[LEVEL_SLOTS + 1];
+    VMPS_CK(cudaMemcpyAsync(sc, w.scalars, sizeof(sc), cudaMemcpyDeviceToHost, s));
+    VMPS_CK(cudaMemcpyAsync(ct, w.counters, sizeof(ct), cudaMemcpyDeviceToHost, s));
+    VMPS_CK(cudaMemcpyAsync(lc, w.level_cnt, sizeof(lc), cudaMemcpyDeviceToHost, s));
+    VMPS_CK(cudaStreamSynchronize(s));
+    if (sc[SC_ERROR]) {
+      g_err = "internal: a non-fused node has a power above the launched levels";
+      return VMPS_ERR_INTERNAL;
+    }
+    memset(st, 0, sizeof(*st));
+    st->n = w.n;
+    st->runs = sc[SC_RUNS];
+    st->merges = sc[SC_RUNS] ? sc[SC_RUNS] - 1 : 0;
+    st->merge_cost_M = ct[0];
+    st->fused_M = ct[1];
+    st->reversed_elems = sc[SC_REVERSED];
+    st->extended_runs = sc[SC_EXTENDED];
+    st->max_power = sc[SC_MAXPOW];
+    uint32_t lv = 0;
+    for (int p = 0; p <= LEVEL_SLOTS; ++p) lv += lc[p] ? 1 : 0;
+    st->levels_executed = lv;
+    st->minrun = w.minrun;
+    st->peak_extra_device_bytes = w.used_bytes;
+    st->scratch_bytes = (uint64_t)w.n * (key_bytes(w.kt) + (HV ? 4 : 0));
+    st->metadata_bytes = w.used_bytes - st->scratch_bytes;
+  }
+  return VMPS_OK;
+}
+
+}  // namespace vmps
+
+using namespace vmps;
+
+static vmps_status_t check_common(const void* keys, const void* vals, uint64_t n, vmps_key_t kt) {
+  if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) {
+    g_err = "unknown key type";
+    return VMPS_ERR_INVALID_ARG;
+  }
+  if (n >= (1ull << 32)) {
+    g_err = "n >= 2^32 is not supported";
+    return VMPS_ERR_INVALID_ARG;
+  }
+  if (n > 1 && !keys) {
+    g_err = "keys is NULL";
+    return VMPS_ERR_INVALID_ARG;
+  }
+  if (((uintptr_t)keys & 15) || ((uintptr_t)vals & 15)) {
+    g_err = "keys/vals must be 16-byte aligned";
+    return VMPS_ERR_INVALID_ARG;
+  }
+  return VMPS_OK;
+}
+
+extern "C" {
+
+vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, int64_t scratch_elems,
+                                   size_t* h_bytes) {
+  if (!h_bytes) return VMPS_ERR_INVALID_ARG;
+  if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
+  if (n >= (1ull << 32)) return VMPS_ERR_INVALID_ARG;
+  (void)scratch_elems;
+  if (n <= 1) { *h_bytes = 256; return VMPS_OK; }
+  Cfg c = make_cfg(n, kt, has_vals < 0 ? -1 : (has_vals ? 1 : 0));
+  *h_bytes = carve(c, nullptr, nullptr) + 256;
+  return VMPS_OK;
+}
+
+static vmps_status_t sort_any(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt, int64_t scratch_elems,
+                              void* ws, size_t ws_bytes, void* stream, vmps_stats_t* h_stats) {
+  vmps_status_t rc = check_common(keys, vals, n, kt);
+  if (rc != VMPS_OK) return rc;
+  if (scratch_elems != VMPS_SCRATCH_UNBOUNDED && scratch_elems < 0) {
+    g_err = "scratch_elems must be >= 0 or VMPS_SCRATCH_UNBOUNDED";
+    return VMPS_ERR_INVALID_ARG;
+  }
+  if (n <= 1) {
+    if (h_stats) { memset(h_stats, 0, sizeof(*h_stats)); h_stats->n = n; h_stats->runs = n; }
+    return VMPS_OK;
+  }
+  const int hv = vals ? 1 : 0;
+  Cfg c = make_cfg(n, kt, hv);
+  Work w;
+  size_t need = carve(c, &w, nullptr);
+  if (!ws || ws_bytes < need) {
+    g_err = "workspace too small";
+    return VMPS_ERR_BUDGET;
+  }
+  char* base = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  if ((size_t)(base - (char*)ws) + need > ws_bytes) {
+    g_err = "workspace too small after alignment";
+    return VMPS_ERR_BUDGET;
+  }
+  carve(c, &w, base);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (kt) {
+    case VMPS_KEY_U32:
+      return hv ? sort_impl<VMPS_KEY_U32, true>(w, keys, vals, s, h_stats)
+                : sort_impl<VMPS_KEY_U32, false>(w, keys, vals, s, h_stats);
+    case VMPS_KEY_U64:
+      return hv ? sort_impl<VMPS_KEY_U64, true>(w, keys, vals, s, h_stats)
+                : sort_impl<VMPS_KEY_U64, false>(w, keys, vals, s, h_stats);
+    default:
+      return hv ? sort_impl<VMPS_KEY_F32, true>(w, keys, vals, s, h_stats)
+                : sort_impl<VMPS_KEY_F32, false>(w, keys, vals, s, h_stats);
+  }
+}
+
+vmps_status_t vmps_sort_keys(void* keys, uint64_t n, vmps_key_t kt, int64_t scratch_elems, void* ws,
+                             size_t ws_bytes, void* stream, vmps_stats_t* h_stats) {
+  return sort_any(keys, nullptr, n, kt, scratch_elems, ws, ws_bytes, stream, h_stats);
+}
+
+vmps_status_t vmps_sort_pairs(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt, int64_t scratch_elems,
+                              void* ws, size_t ws_bytes, void* stream, vmps_stats_t* h_stats) {
+  if (n > 1 && !vals) {
+    g_err = "vals is NULL";
+    return VMPS_ERR_INVALID_ARG;
+  }
+  return sort_any(keys, vals, n, kt, scratch_elems, ws, ws_bytes, stream, h_stats);
+}
+
+vmps_status_t vmps_merge_plan(const void* keys, uint64_t n, vmps_key_t kt, uint64_t* run_start,
+                              uint8_t* run_kind, vmps_merge_rec_t* merges, uint64_t cap_runs,
+                              uint64_t* h_num_runs, void* ws, size_t ws_bytes, void* stream) {
+  vmps_status_t rc = check_common(keys, nullptr, n, kt);
+  if (rc != VMPS_OK) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n <= 1) {
+    if (h_num_runs) *h_num_runs = n;
+    if (n == 1) {
+      if (cap_runs < 1 || !run_start || !run_kind) { g_err = "cap_runs too small"; return VMPS_ERR_INVALID_ARG; }
+      uint64_t z = 0;
+      uint8_t kz = 0;
+      VMPS_CK(cudaMemcpyAsync(run_start, &z, 8, cudaMemcpyHostToDevice, s));
+      VMPS_CK(cudaMemcpyAsync(run_kind, &kz, 1, cudaMemcpyHostToDevice, s));
+      VMPS_CK(cudaStreamSynchronize(s));
+    }
+    return VMPS_OK;
+  }
+  if (!run_start || !run_kind || !merges) { g_err = "plan output is NULL"; return VMPS_ERR_INVALID_ARG; }
+  Cfg c = make_cfg(n, kt, -1);
+  Work w;
+  size_t need = carve(c, &w, nullptr);
+  if (!ws || ws_bytes < need) { g_err = "workspace too small"; return VMPS_ERR_BUDGET; }
+  char* base = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  if ((size_t)(base - (char*)ws) + need > ws_bytes) { g_err = "workspace too small"; return VMPS_ERR_BUDGET; }
+  carve(c, &w, base);
+  switch (kt) {
+    case VMPS_KEY_U32: rc = front_half<VMPS_KEY_U32>(w, keys, s); break;
+    case VMPS_KEY_U64: rc = front_half<VMPS_KEY_U64>(w, keys, s); break;
+    default: rc = front_half<VMPS_KEY_F32>(w, keys, s); break;
+  }
+  if (rc != VMPS_OK) return rc;
+  uint32_t r = 0;
+  VMPS_CK(cudaMemcpyAsync(&r, w.scalars + SC_RUNS, 4, cudaMemcpyDeviceToHost, s));
+  VMPS_CK(cudaStreamSynchronize(s));
+  if (h_num_runs) *h_num_runs = r;
+  if (r > cap_runs) { g_err = "cap_runs too small"; return VMPS_ERR_INVALID_ARG; }
+  k_plan_records<<<grid_for(r), 256, 0, s>>>(w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.dep[0],
+                                             w.run_kind, run_start, run_kind, merges);
+  rc = launch_check();
+  if (rc != VMPS_OK) return rc;
+  VMPS_CK(cudaStreamSynchronize(s));
+  return VMPS_OK;
+}
+
+const char* vmps_status_string(vmps_status_t s) {
+  switch (s) {
+    case VMPS_OK: return "ok";
+    case VMPS_ERR_INVALID_ARG: return "invalid argument";
+    case VMPS_ERR_ALLOC: return "allocation failed";
+    case VMPS_ERR_BUDGET: return "workspace or scratch budget too small";
+    case VMPS_ERR_CUDA: return "CUDA error";
+    case VMPS_ERR_NCCL: return "NCCL error";
+    case VMPS_ERR_INTERNAL: return "internal error";
+  }
+  return "unknown status";
+}
+
+const char* vmps_last_error(void) { return g_err.c_str(); }
+
+void vmps_profile_enable(int on) { g_prof = on != 0; }
+
+int vmps_profile_read(double* h_ms, int cap, uint64_t* h_launches, uint64_t* h_bytes) {
+  if (h_launches) { h_launches[0] = g_nl; h_launches[1] = g_nl_merge; }
+  if (!g_prof || g_prof_mark[0] < 0 || g_prof_mark[3] < 0) return 0;
+  auto el = [](int a, int b) -> double {
+    float ms = 0.f;
+    if (a < 0 || b < 0) return 0.0;
+    if (cudaEventElapsedTime(&ms, g_ev[a], g_ev[b]) != cudaSuccess) return -1.0;
+    return (double)ms;
+  };
+  double v[5];
+  v[0] = el(g_prof_mark[0], g_prof_mark[1]);
+  v[1] = el(g_prof_mark[1], g_prof_mark[2]);
+  v[2] = 0.0;
+  for (int i = 0; i < g_prof_np; ++i) v[2] += el(g_prof_part[i][0], g_prof_part[i][1]);
+  v[3] = 0.0;
+  for (int i = 0; i < g_prof_nm; ++i) v[3] += el(g_prof_lvl[i][0], g_prof_lvl[i][1]);
+  v[4] = el(g_prof_mark[0], g_prof_mark[3]);
+  int k = 0;
+  for (; k < cap && k < 5; ++k) h_ms[k] = v[k];
+  if (h_bytes && g_prof_host) {
+    unsigned long long M = g_prof_host[0], fM = g_prof_host[1];
+    h_bytes[0] = 2ull * (unsigned long long)g_prof_wbytes * (M - fM);
+    h_bytes[1] = M;
+    h_bytes[2] = fM;
+  }
+  return k;
+}
+
+void vmps_test_set_minrun(uint32_t minrun) { g_minrun_override = minrun > MAX_MINRUN ? MAX_MINRUN : minrun; }
+
+void vmps_test_set_tiles(uint32_t fuse_z, uint32_t merge_tile, uint32_t block_elems) {
+  if (fuse_z) fuse_z = std::min<uint32_t>(std::max<uint32_t>(fuse_z, 64), MAX_FUSE_Z);
+  if (merge_tile) merge_tile = std::min<uint32_t>(std::max<uint32_t>(merge_tile, 16), DEFAULT_TOUT);
+  g_fuse_z = fuse_z;
+  g_tout = merge_tile;
+  g_blk = block_elems;
+}
+
+}  // extern "C"

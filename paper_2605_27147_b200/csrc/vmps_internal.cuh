@@ -1,0 +1,125 @@
+// vmps_internal.cuh -- shared device/host definitions of libvmps (sm_100a).
+// Product code: no dependency on oracle/ (see DESIGN.md "Independence").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vmps.h"
+
+namespace vmps {
+
+// ---------------------------------------------------------------------------
+// Key order (reading R5).  Every compare maps a key to an unsigned
+// image whose integer order is the sort order; keys are never rewritten.
+// f32: NaN (any sign/payload) -> 0xFFFFFFFF (last, all equal); otherwise flip
+// all bits of negatives and the sign bit of non-negatives (-0.0 < +0.0).
+// ---------------------------------------------------------------------------
+template <int KT>
+struct KeyTraits;
+template <>
+struct KeyTraits<VMPS_KEY_U32> {
+  using K = uint32_t;
+  using O = uint32_t;
+  __device__ __forceinline__ static O ord(K x) { return x; }
+};
+template <>
+struct KeyTraits<VMPS_KEY_U64> {
+  using K = uint64_t;
+  using O = uint64_t;
+  __device__ __forceinline__ static O ord(K x) { return x; }
+};
+template <>
+struct KeyTraits<VMPS_KEY_F32> {
+  using K = uint32_t;  // raw bits
+  using O = uint32_t;
+  __device__ __forceinline__ static O ord(K x) {
+    if ((x & 0x7FFFFFFFu) > 0x7F800000u) return 0xFFFFFFFFu;
+    return x ^ ((x & 0x80000000u) ? 0xFFFFFFFFu : 0x80000000u);
+  }
+};
+
+// Run-chain states: START(o), ASC(f), DESC(f)
+// for o, f in [0, minrun), plus END.
+constexpr uint32_t ST_END = 255u;
+constexpr int RT = 4096;             // run-detection tile (elements)
+constexpr int RT_WORDS = RT / 32;    // bitmap words per tile
+constexpr int CHAIN_G = 64;          // tables composed per group
+constexpr int MAX_MINRUN = 64;
+constexpr int MAX_NS = 3 * MAX_MINRUN;
+
+// Plan / schedule defaults
+constexpr uint32_t DEFAULT_FUSE_Z = 2048;   // fused-subtree limit Z (elements)
+constexpr uint32_t MAX_FUSE_Z = 2048;
+constexpr uint32_t MERGE_BLOCK = 256;       // threads per merge CTA
+constexpr uint32_t MERGE_K = 8;             // outputs per thread
+constexpr uint32_t DEFAULT_TOUT = MERGE_BLOCK * MERGE_K;  // merge tile (outputs)
+
+// Device-side scalars (one small array in the workspace).
+enum Scalar : int {
+  SC_RUNS = 0,        // r
+  SC_UNITS,           // number of fused units
+  SC_LONG,            // number of long leaves
+  SC_LONG_CHUNKS,     // chunks over long leaves
+  SC_NONFUSED,        // number of non-fused nodes
+  SC_MAXPOW,          // max node power
+  SC_REVERSED,        // reversed elements
+  SC_EXTENDED,        // extended runs
+  SC_LEVEL_TILES,     // scratch for per-level tile count
+  SC_ERROR,           // internal consistency error flag
+  SC_COUNT = 16
+};
+constexpr int LEVEL_SLOTS = 72;  // powers 0..70
+
+// Device arrays carved from the caller's workspace.
+struct Work {
+  uint32_t n, minrun, ns, ntiles;
+  uint32_t rmax;       // capacity for runs (+2 slack)
+  uint32_t fuse_z, tout;
+  int kt, has_vals;
+  // element scratch (buffer 1 of the ping-pong pair)
+  void* k1;
+  uint32_t* v1;
+  // run detection
+  uint32_t* bits;      // (n/32 + 2) words, bit p = key[p] < key[p-1]
+  uint32_t* tile_tab;  // ntiles * ns, (state << 24) | count
+  uint64_t* chain_tab[4];  // composed levels
+  uint32_t chain_m[5];     // table counts per level (0 = tiles)
+  int chain_levels;        // number of composed levels
+  uint64_t* chain_entry[5];// entry (state << 32 | count) per table per level
+  uint32_t* run_start;     // rmax + 1
+  uint8_t* run_kind;       // rmax
+  uint32_t* scalars;       // SC_COUNT
+  // plan (boundary t in [1, r-1]; arrays sized rmax)
+  uint8_t* power;
+  uint32_t* seg_l;    // first run of node t's segment
+  uint32_t* seg_r;    // one past the last run
+  uint32_t* parent;   // boundary index, 0 = root
+  uint32_t* anc[2];   // pointer jumping
+  uint32_t* dep[2];   // depth (low 16 bits) | left-ancestor count (high 16)
+  // classification
+  uint32_t* unit_flag;   // per run: 1 = unit start
+  uint32_t* long_flag;   // per run: 1 = long leaf
+  uint32_t* unit_end;    // per run (unit starts): end position
+  uint8_t* unit_par;     // per run (unit starts): output buffer parity
+  uint8_t* long_par;     // per run (long leaves): parity | desc << 1
+  uint32_t* long_chunks; // per long leaf: chunks of work
+  uint32_t* long_off;    // exclusive scan of long_chunks
+  uint32_t* unit_idx;    // scan of unit_flag
+  uint32_t* long_idx;    // scan of long_flag
+  uint32_t* units;       // [3 * rmax]: start, end, parity (compacted)
+  uint32_t* longs;       // [4 * rmax]: start, end, parity|desc<<1, chunk offset
+  uint32_t* level_cnt;   // LEVEL_SLOTS
+  uint32_t* level_start; // LEVEL_SLOTS + 1 (node offsets)
+  uint32_t* level_fill;  // LEVEL_SLOTS
+  uint32_t* level_tile;  // LEVEL_SLOTS + 1 (tile offsets)
+  uint32_t* lnodes;      // bucketed non-fused nodes
+  uint32_t* ltiles_cnt;  // tiles per bucketed node
+  uint32_t* ltiles;      // tile offset per bucketed node (exclusive scan)
+  uint2* part;           // per tile of a level: (bucket index, corank at tile start)
+  uint32_t part_cap;
+  uint32_t* scan_tmp;    // block sums for scans
+  unsigned long long* counters;  // [0] M, [1] fused M
+  size_t used_bytes;
+};
+
+}  // namespace vmps
