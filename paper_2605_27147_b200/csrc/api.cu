@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -144,6 +145,7 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.unit_idx = (uint32_t*)take(R * 4);
     t.long_idx = (uint32_t*)take(R * 4);
     t.units = (uint32_t*)take(R * 3 * 4);
+    t.batch_first = (uint32_t*)take((n / c.fuse_z + 4) * 4);
     t.longs = (uint32_t*)take(R * 4 * 4);
     t.long_chunks = (uint32_t*)take(R * 4);
     t.long_off = (uint32_t*)take(R * 4);
@@ -154,8 +156,10 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.lnodes = (uint32_t*)take(R * 4);
     t.ltiles = (uint32_t*)take(R * 4);
     t.ltiles_cnt = (uint32_t*)take(R * 4);
-    t.part_cap = (uint32_t)(n / c.tout + R + 2);
-    t.part = (uint2*)take((size_t)t.part_cap * 8);
+    // tiles of one level: its nodes are disjoint and larger than Z, and a node
+    // [i,k) spans ceil(k/T) - floor(i/T) <= (k-i)/T + 2 aligned tiles
+    t.part_cap = (uint32_t)(n / c.tout + 2 * (n / c.fuse_z) + 8);
+    t.desc = take((size_t)t.part_cap * sizeof(TileDesc));
     t.scan_tmp = (uint32_t*)take(scan_tmp_words(R) * 4 + 64);
   }
   t.counters = (unsigned long long*)take(8 * 8);
@@ -226,10 +230,28 @@ static vmps_status_t chain_attrs() {
 }
 
 // Launch helper: counts kernels for the bench's gpu_launches.
-#define LAUNCH(kern, grid, block, smem, stream, ...)           \
-  do {                                                          \
-    kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);   \
-    ++g_nl;                                                     \
+static int g_debug_sync = -1;  // VMPS_DEBUG_SYNC=1: synchronise + check after every launch
+static bool debug_sync() {
+  if (g_debug_sync < 0) {
+    const char* e = getenv("VMPS_DEBUG_SYNC");
+    g_debug_sync = (e && e[0] == '1') ? 1 : 0;
+  }
+  return g_debug_sync == 1;
+}
+
+#define LAUNCH(kern, grid, block, smem, stream, ...)                              \
+  do {                                                                             \
+    kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                      \
+    ++g_nl;                                                                        \
+    if (debug_sync()) {                                                            \
+      cudaError_t e_ = cudaStreamSynchronize(stream);                              \
+      if (e_ == cudaSuccess) e_ = cudaGetLastError();                              \
+      if (e_ != cudaSuccess) {                                                     \
+        g_err = std::string(#kern) + ": " + cudaGetErrorString(e_);               \
+        fprintf(stderr, "vmps debug: %s\n", g_err.c_str());                      \
+        return VMPS_ERR_CUDA;                                                      \
+      }                                                                            \
+    }                                                                              \
   } while (0)
 
 // Run detection + plan front half (shared by sort and merge_plan).
@@ -322,7 +344,8 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
     kernel_attrs_set[KT][HV] = true;
   }
   const uint32_t nbatch = (uint32_t)((w.n + w.fuse_z - 1) / w.fuse_z);
-  LAUNCH((k_leaf_sort<KT, HV>), nbatch, LEAF_THREADS, lsm, s, k0, v0, k1, v1, w.units, w.scalars, w.fuse_z);
+  LAUNCH(k_batch_first, (nbatch + 256) / 256, 256, 0, s, w.units, w.scalars, w.fuse_z, nbatch, w.batch_first);
+  LAUNCH((k_leaf_sort<KT, HV>), nbatch, LEAF_THREADS, lsm, s, k0, v0, k1, v1, w.units, w.batch_first, w.fuse_z);
   LAUNCH((k_long_leaves<KT, HV>), nsm() * 8, 256, 0, s, k0, v0, k1, v1, w.longs, w.long_off, w.scalars,
          LONG_CHUNK);
   rc = launch_check();
@@ -334,14 +357,24 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   int p_hi = (int)std::ceil(lg) + 1;
   if (p_hi > LEVEL_SLOTS - 2) p_hi = LEVEL_SLOTS - 2;
   if (p_hi < 1) p_hi = 1;
-  const unsigned gm = (unsigned)(nsm() * 8);
+  using SM = MergeSmem<KT, HV>;
+  static int merge_occ[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  if (!merge_occ[KT][HV]) {
+    VMPS_CK(cudaFuncSetAttribute(k_merge_level<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SM::BYTES));
+    int occ = 0;
+    VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_merge_level<KT, HV>, MERGE_BLOCK, SM::BYTES));
+    merge_occ[KT][HV] = occ > 0 ? occ : 1;
+  }
+  const unsigned gm = (unsigned)(nsm() * merge_occ[KT][HV]);
+  TileDesc* desc = (TileDesc*)w.desc;
   for (int p = p_hi; p >= 1; --p) {
     int e0 = prof_event(s);
-    LAUNCH(k_partition<KT>, nsm() * 4, 256, 0, s, k0, k1, w.run_start, w.seg_l, w.seg_r, dep, w.lnodes,
-           w.ltiles, w.level_start, w.level_tile, p, w.tout, w.part);
+    LAUNCH(k_tile_desc<KT>, (w.part_cap + 255) / 256, 256, 0, s, k0, k1, w.run_start, w.seg_l, w.seg_r, dep, w.lnodes,
+           w.ltiles, w.level_start, w.level_tile, p, w.tout, desc, w.part_cap, w.scalars);
     int e1 = prof_event(s);
-    LAUNCH((k_merge_level<KT, HV>), gm, MERGE_BLOCK, 0, s, k0, v0, k1, v1, w.run_start, w.seg_l, w.seg_r, dep,
-           w.lnodes, w.ltiles, w.level_tile, p, w.tout, w.part);
+    LAUNCH((k_merge_level<KT, HV>), gm, MERGE_BLOCK, SM::BYTES, s, k0, v0, k1, v1, desc, w.level_tile, p,
+           w.tout, w.part_cap);
     ++g_nl_merge;
     int e2 = prof_event(s);
     if (g_prof && e0 >= 0 && e2 >= 0 && g_prof_nm < 128) {
@@ -367,7 +400,8 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
     VMPS_CK(cudaMemcpyAsync(lc, w.level_cnt, sizeof(lc), cudaMemcpyDeviceToHost, s));
     VMPS_CK(cudaStreamSynchronize(s));
     if (sc[SC_ERROR]) {
-      g_err = "internal: a non-fused node has a power above the launched levels";
+      g_err = sc[SC_ERROR] == 2 ? "internal: tile descriptor capacity exceeded"
+                                : "internal: a non-fused node has a power above the launched levels";
       return VMPS_ERR_INTERNAL;
     }
     memset(st, 0, sizeof(*st));

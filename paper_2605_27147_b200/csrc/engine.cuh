@@ -16,14 +16,15 @@
 // (merge-path co-rank per output tile, ties from the left run, Alg. 2)
 // and one merge launch (tiles staged in shared memory).
 #pragma once
+#include "ptx.cuh"
 #include "vmps_internal.cuh"
 
 namespace vmps {
 
-constexpr int LEAF_THREADS = 256;
-constexpr int LEAF_K = 16;
-constexpr int LEAF_EMAX = 2 * MAX_FUSE_Z;  // a batch holds < 2Z elements
-static_assert(LEAF_THREADS * LEAF_K == LEAF_EMAX, "leaf tile");
+constexpr int LEAF_THREADS = 512;
+constexpr int LEAF_K = 9;                         // odd: conflict-free chunk stride
+constexpr int LEAF_CAP = LEAF_THREADS * LEAF_K;   // 4608 >= 2Z - 1 (a batch holds < 2Z)
+static_assert(LEAF_CAP >= 2 * (int)MAX_FUSE_Z - 1, "leaf capacity");
 
 template <int KT>
 __device__ __forceinline__ uint32_t corank(const typename KeyTraits<KT>::K* A, uint32_t nA,
@@ -39,130 +40,252 @@ __device__ __forceinline__ uint32_t corank(const typename KeyTraits<KT>::K* A, u
   return lo;
 }
 
+// LEAF_K is odd, so thread-contiguous chunks (stride LEAF_K words) hit
+// distinct banks without padding.  Shared memory carries keys and 16-bit
+// local indices (ping-pong); payloads are gathered once at the end.  Rounds
+// whose pairs fit inside one warp's range synchronise with __syncwarp only.
 template <int KT, bool HV>
-__global__ void __launch_bounds__(LEAF_THREADS) k_leaf_sort(
+__global__ void __launch_bounds__(LEAF_THREADS, 3) k_leaf_sort(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
-    const uint32_t* __restrict__ units, const uint32_t* scalars, uint32_t fuse_z) {
+    const uint32_t* __restrict__ units, const uint32_t* __restrict__ batch_first, uint32_t fuse_z) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  K* sk = reinterpret_cast<K*>(smem_raw);
-  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + LEAF_EMAX);
-  uint16_t* us = reinterpret_cast<uint16_t*>(sv + (HV ? LEAF_EMAX : 0));
-  uint16_t* ue = us + LEAF_EMAX;
-  uint8_t* up = reinterpret_cast<uint8_t*>(ue + LEAF_EMAX);
+  K* const skb = reinterpret_cast<K*>(smem_raw);                          // 2 x LEAF_CAP keys
+  uint16_t* const sib = reinterpret_cast<uint16_t*>(skb + 2 * LEAF_CAP);  // 2 x LEAF_CAP indices
+  uint32_t* ubits = reinterpret_cast<uint32_t*>(sib + 2 * LEAF_CAP);      // unit-start bitmap
+  uint32_t* upre = ubits + LEAF_CAP / 32 + 1;  // exclusive popcount prefix per word
+  uint32_t* pcar = upre + LEAF_CAP / 32 + 1;   // parity of the unit open at each word's end
+  uint32_t* pbits = pcar + LEAF_CAP / 32 + 1;  // parity bit at each unit start
 
-  const uint32_t nunits = scalars[SC_UNITS];
-  const uint32_t lo_pos = blockIdx.x * fuse_z, hi_pos = lo_pos + fuse_z;
-  // units with start in [lo_pos, hi_pos)
-  uint32_t x0, x1;
-  {
-    uint32_t a = 0, b = nunits;
-    while (a < b) { uint32_t m = (a + b) >> 1; if (units[3 * m] < lo_pos) a = m + 1; else b = m; }
-    x0 = a;
-    b = nunits;
-    while (a < b) { uint32_t m = (a + b) >> 1; if (units[3 * m] < hi_pos) a = m + 1; else b = m; }
-    x1 = a;
-  }
+  // units with start in [b Z, (b+1) Z)
+  const uint32_t x0 = batch_first[blockIdx.x], x1 = batch_first[blockIdx.x + 1];
   if (x0 >= x1) return;
   const uint32_t bstart = units[3 * x0];
   const uint32_t E = units[3 * (x1 - 1) + 1] - bstart;
-  for (uint32_t q = threadIdx.x; q < E; q += LEAF_THREADS) {
-    sk[q] = k0[bstart + q];
-    if (HV) sv[q] = v0[bstart + q];
-    // unit of position q: last unit in [x0, x1) with start <= bstart + q
-    uint32_t a = x0, b = x1;
-    while (b - a > 1) { uint32_t m = (a + b) >> 1; if (units[3 * m] <= bstart + q) a = m; else b = m; }
-    us[q] = (uint16_t)(units[3 * a] - bstart);
-    ue[q] = (uint16_t)(units[3 * a + 1] - bstart);
-    up[q] = (uint8_t)units[3 * a + 2];
+  const uint32_t nwords = (E + 31) / 32;
+  for (uint32_t w = threadIdx.x; w < nwords; w += LEAF_THREADS) { ubits[w] = 0u; pbits[w] = 0u; }
+  __syncthreads();
+  for (uint32_t x = x0 + threadIdx.x; x < x1; x += LEAF_THREADS) {
+    const uint32_t q = units[3 * x] - bstart;
+    atomicOr(&ubits[q >> 5], 1u << (q & 31u));
+    if (units[3 * x + 2]) atomicOr(&pbits[q >> 5], 1u << (q & 31u));
+  }
+  const uint32_t q0 = threadIdx.x * LEAF_K;
+  K rk[LEAF_K];
+#pragma unroll
+  for (int i = 0; i < LEAF_K; ++i) {
+    const uint32_t q = q0 + i;
+    rk[i] = q < E ? k0[bstart + q] : K(0);
   }
   __syncthreads();
+  if (threadIdx.x < 32) {  // per-word prefix of unit starts; parity carried across words
+    uint32_t carry = 0, pc = 0;
+    for (uint32_t w0 = 0; w0 < nwords; w0 += 32) {
+      const uint32_t w = w0 + threadIdx.x;
+      const uint32_t ub = w < nwords ? ubits[w] : 0u;
+      const uint32_t c = (uint32_t)__popc(ub);
+      uint32_t incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((int)threadIdx.x >= o) incl += y;
+      }
+      if (w < nwords) upre[w] = carry + incl - c;
+      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+      const int hb = ub ? 31 - __clz(ub) : -1;
+      const int own = hb >= 0 ? (int)((w < nwords ? pbits[w] : 0u) >> hb) & 1 : -1;
+      const uint32_t has = __ballot_sync(0xFFFFFFFFu, own >= 0);
+      const uint32_t le = has & (0xFFFFFFFFu >> (31 - threadIdx.x));
+      const int src = le ? 31 - __clz(le) : -1;
+      const int ownv = __shfl_sync(0xFFFFFFFFu, own, src >= 0 ? src : 0);
+      const uint32_t pw = src >= 0 ? (uint32_t)ownv : pc;
+      if (w < nwords) pcar[w] = pw;
+      pc = __shfl_sync(0xFFFFFFFFu, pw, 31);
+    }
+  }
+  __syncthreads();
+  auto is_start = [&](uint32_t q) -> bool { return (ubits[q >> 5] >> (q & 31u)) & 1u; };
+  auto unit_of = [&](uint32_t q) -> uint32_t {
+    const uint32_t w = q >> 5;
+    return upre[w] + (uint32_t)__popc(ubits[w] & (0xFFFFFFFFu >> (31u - (q & 31u)))) - 1u;
+  };
 
-  // Phase 1: stable odd-even transposition sort of LEAF_K consecutive
-  // positions per thread, never swapping across a unit boundary.
-  const uint32_t q0 = threadIdx.x * LEAF_K;
+  // Phase 1: stable rank sort of the thread's chunk by (unit, key).
   {
-    K rk[LEAF_K];
-    uint32_t rv[LEAF_K];
-    uint16_t ru[LEAF_K];
+    uint32_t cut[LEAF_K];
+    uint32_t c = 0;
 #pragma unroll
     for (int i = 0; i < LEAF_K; ++i) {
-      uint32_t q = q0 + i;
-      rk[i] = q < E ? sk[q] : K(0);
-      rv[i] = (HV && q < E) ? sv[q] : 0u;
-      ru[i] = q < E ? us[q] : (uint16_t)0xFFFF;
+      const uint32_t q = q0 + i;
+      if (i > 0 && q < E && is_start(q)) ++c;
+      cut[i] = q < E ? c : 0xFFu;  // past-E elements rank last
     }
+    uint32_t rank[LEAF_K];
 #pragma unroll
-    for (int rnd = 0; rnd < LEAF_K; ++rnd) {
+    for (int i = 0; i < LEAF_K; ++i) rank[i] = 0;
 #pragma unroll
-      for (int i = rnd & 1; i + 1 < LEAF_K; i += 2) {
-        bool sw = ru[i] == ru[i + 1] && T::ord(rk[i + 1]) < T::ord(rk[i]);
-        if (sw) {
-          K tk = rk[i]; rk[i] = rk[i + 1]; rk[i + 1] = tk;
-          uint32_t tv = rv[i]; rv[i] = rv[i + 1]; rv[i + 1] = tv;
-        }
+    for (int i = 0; i < LEAF_K; ++i) {
+#pragma unroll
+      for (int j = i + 1; j < LEAF_K; ++j) {
+        const bool ifirst = cut[i] != cut[j] || T::ord(rk[i]) <= T::ord(rk[j]);
+        rank[j] += ifirst ? 1u : 0u;
+        rank[i] += ifirst ? 0u : 1u;
       }
     }
 #pragma unroll
     for (int i = 0; i < LEAF_K; ++i) {
-      uint32_t q = q0 + i;
-      if (q < E) { sk[q] = rk[i]; if (HV) sv[q] = rv[i]; }
+      if (q0 + i < E) {
+        skb[q0 + rank[i]] = rk[i];
+        sib[q0 + rank[i]] = (uint16_t)(q0 + i);
+      }
     }
   }
   __syncthreads();
 
-  // Phase 2: merge rounds; in the pair [x, x+2w) only the unit straddling
-  // m = x + w is merged ([max(x, start), m) with [m, min(x+2w, end))); every
-  // other unit of the pair is already in its final place.
+  // Phase 2: merge rounds (ping-pong).  In the pair [x, x+2w) only the unit
+  // straddling m = x + w is merged ([max(x, start), m) with
+  // [m, min(x+2w, end))); everything else is copied in place.
+  uint32_t cur = 0;
   for (uint32_t w = LEAF_K; w < E; w <<= 1) {
-    K rk[LEAF_K];
-    uint32_t rv[LEAF_K];
-    uint32_t a0 = 0, a1 = 0;
+    const K* sk = skb + cur * LEAF_CAP;
+    const uint16_t* si = sib + cur * LEAF_CAP;
+    K* dk = skb + (cur ^ 1u) * LEAF_CAP;
+    uint16_t* di = sib + (cur ^ 1u) * LEAF_CAP;
     if (q0 < E) {
-      uint32_t x = (q0 / (2 * w)) * (2 * w), m = x + w;
-      if (m < E && us[m] != m) {
-        uint32_t lo = max(x, (uint32_t)us[m]);
-        uint32_t hi = min(min(x + 2 * w, (uint32_t)ue[m]), E);
+      const uint32_t q1 = min(q0 + LEAF_K, E);
+      const uint32_t x = (q0 / (2 * w)) * (2 * w), m = x + w;
+      uint32_t a0 = q0, a1 = q0, lo = 0, hi = 0;
+      if (m < E && !is_start(m)) {
+        const uint32_t* u = units + 3 * (x0 + unit_of(m));
+        lo = max(x, u[0] - bstart);
+        hi = min(min(x + 2 * w, u[1] - bstart), E);
         a0 = max(q0, lo);
-        a1 = min(q0 + LEAF_K, hi);
-        if (a0 < a1) {
-          const K* A = sk + lo;
-          const K* B = sk + m;
-          uint32_t nA = m - lo, nB = hi - m, d = a0 - lo;
-          uint32_t ia = corank<KT>(A, nA, B, nB, d), ib = d - ia;
+        a1 = max(a0, min(q1, hi));
+      }
+      uint32_t ri[LEAF_K];
+      if (a0 == q0 && a1 == q0 + LEAF_K) {
+        // the whole chunk lies in the merge window: branch-free serial merge
+        const uint32_t nA = m - lo, nB = hi - m, d = q0 - lo;
+        uint32_t l = d > nB ? d - nB : 0u, h = min(d, nA);
+        while (l < h) {
+          const uint32_t mid = (l + h) >> 1;
+          if (T::ord(sk[lo + mid]) <= T::ord(sk[m + d - mid - 1])) l = mid + 1;
+          else h = mid;
+        }
+        uint32_t ia = lo + l, ib = m + d - l;  // absolute positions
+        K ka = sk[ia], kb = sk[ib];           // may read one past a side: in bounds, unused
 #pragma unroll
-          for (int s = 0; s < LEAF_K; ++s) {
-            if (a0 + s < a1) {
-              bool takeA = ib >= nB || (ia < nA && T::ord(A[ia]) <= T::ord(B[ib]));
-              if (takeA) { rk[s] = A[ia]; if (HV) rv[s] = sv[lo + ia]; ++ia; }
-              else { rk[s] = B[ib]; if (HV) rv[s] = sv[m + ib]; ++ib; }
+        for (int s2 = 0; s2 < LEAF_K; ++s2) {
+          const bool p = ib >= hi || (ia < m && T::ord(ka) <= T::ord(kb));
+          rk[s2] = p ? ka : kb;
+          ri[s2] = p ? ia : ib;
+          ia += p ? 1u : 0u;
+          ib += p ? 0u : 1u;
+          const K nx = sk[p ? ia : ib];
+          ka = p ? nx : ka;
+          kb = p ? kb : nx;
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < LEAF_K; ++s2) {
+          dk[q0 + s2] = rk[s2];
+          di[q0 + s2] = si[ri[s2]];
+        }
+      } else if (a0 >= a1) {  // nothing to merge here: copy in place
+#pragma unroll
+        for (int s2 = 0; s2 < LEAF_K; ++s2) {
+          const uint32_t pos = q0 + s2;
+          if (pos < q1) { dk[pos] = sk[pos]; di[pos] = si[pos]; }
+        }
+      } else {  // the chunk holds a unit boundary: mixed merge / copy
+        const uint32_t nA = m - lo, nB = hi - m, d = a0 - lo;
+        uint32_t l = d > nB ? d - nB : 0u, h = min(d, nA);
+        while (l < h) {
+          const uint32_t mid = (l + h) >> 1;
+          if (T::ord(sk[lo + mid]) <= T::ord(sk[m + d - mid - 1])) l = mid + 1;
+          else h = mid;
+        }
+        uint32_t ia = l, ib = d - l;
+        K ka = sk[lo + min(ia, nA - 1)];
+        K kb = sk[m + min(ib, nB - 1)];
+#pragma unroll
+        for (int s2 = 0; s2 < LEAF_K; ++s2) {
+          const uint32_t pos = q0 + s2;
+          if (pos >= a0 && pos < a1) {
+            const bool takeA = ib >= nB || (ia < nA && T::ord(ka) <= T::ord(kb));
+            if (takeA) {
+              rk[s2] = ka; ri[s2] = lo + ia; ++ia;
+              if (ia < nA) ka = sk[lo + ia];
+            } else {
+              rk[s2] = kb; ri[s2] = m + ib; ++ib;
+              if (ib < nB) kb = sk[m + ib];
             }
+          } else {
+            rk[s2] = pos < q1 ? sk[pos] : K(0);
+            ri[s2] = pos;
           }
         }
+#pragma unroll
+        for (int s2 = 0; s2 < LEAF_K; ++s2) {
+          const uint32_t pos = q0 + s2;
+          if (pos < q1) { dk[pos] = rk[s2]; di[pos] = si[ri[s2]]; }
+        }
       }
     }
-    __syncthreads();
+    cur ^= 1u;
+    // the next round's pairs stay inside one warp's range: warp-level sync
+    if (2 * (2 * w) <= 32 * LEAF_K) __syncwarp();
+    else __syncthreads();
+  }
+  __syncthreads();
+
+  // Phase 3: keys from shared memory, payloads gathered by local index (read
+  // all before writing: the payload gather may be in place), each unit to its
+  // parity buffer.
+  const K* sk = skb + cur * LEAF_CAP;
+  const uint16_t* si = sib + cur * LEAF_CAP;
+  constexpr int PER = LEAF_CAP / LEAF_THREADS;
+  uint32_t gv[PER];
+  if (HV) {
 #pragma unroll
-    for (int s = 0; s < LEAF_K; ++s) {
-      if (a0 + s < a1) { sk[a0 + s] = rk[s]; if (HV) sv[a0 + s] = rv[s]; }
+    for (int r = 0; r < PER; ++r) {
+      const uint32_t q = threadIdx.x + r * LEAF_THREADS;
+      gv[r] = q < E ? v0[bstart + si[q]] : 0u;
     }
     __syncthreads();
   }
-
-  // Phase 3: each unit to its parity buffer.
-  for (uint32_t q = threadIdx.x; q < E; q += LEAF_THREADS) {
-    if (up[q]) { k1[bstart + q] = sk[q]; if (HV) v1[bstart + q] = sv[q]; }
-    else { k0[bstart + q] = sk[q]; if (HV) v0[bstart + q] = sv[q]; }
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const uint32_t q = threadIdx.x + r * LEAF_THREADS;
+    if (q < E) {
+      const uint32_t w = q >> 5;
+      const uint32_t mk = ubits[w] & (0xFFFFFFFFu >> (31u - (q & 31u)));
+      const uint32_t par = mk ? (pbits[w] >> (31 - __clz(mk))) & 1u : pcar[w - 1];
+      if (par) { k1[bstart + q] = sk[q]; if (HV) v1[bstart + q] = gv[r]; }
+      else { k0[bstart + q] = sk[q]; if (HV) v0[bstart + q] = gv[r]; }
+    }
   }
 }
 
 template <int KT>
 inline size_t leaf_smem_bytes(bool hv) {
   using K = typename KeyTraits<KT>::K;
-  return LEAF_EMAX * (sizeof(K) + (hv ? 4 : 0) + 2 + 2 + 1);
+  (void)hv;
+  return 2 * LEAF_CAP * (sizeof(K) + 2) + 4 * (LEAF_CAP / 32 + 1) * 4 + 16;
 }
+
+// batch_first[b] = first unit whose start is >= b Z (one thread per batch).
+__global__ void k_batch_first(const uint32_t* __restrict__ units, const uint32_t* scalars,
+                              uint32_t fuse_z, uint32_t nbatch, uint32_t* __restrict__ batch_first) {
+  const uint32_t nunits = scalars[SC_UNITS];
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= nbatch; b += gridDim.x * blockDim.x) {
+    const uint64_t pos = (uint64_t)b * fuse_z;
+    uint32_t a = 0, e = nunits;
+    while (a < e) { uint32_t m = (a + e) >> 1; if ((uint64_t)units[3 * m] < pos) a = m + 1; else e = m; }
+    batch_first[b] = a;
+  }
+}
+
 
 // Long leaves (> Z): reverse strictly descending runs, place odd-depth leaves
 // into buffer 1.  Work is split into LONG_CHUNK pieces.
@@ -200,96 +323,236 @@ __global__ void __launch_bounds__(256) k_long_leaves(
   }
 }
 
-// Merge-path partition of one level: co-rank at every tile start.
+// ---------------------------------------------------------------------------
+// Level engine.  Output tiles are aligned to global positions: tile g of a
+// node [i,k) covers [max(i, g T), min(k, (g+1) T)), so every interior tile
+// starts on a T-element boundary and threads store 128-bit vectors.
+// ---------------------------------------------------------------------------
+struct __align__(16) TileDesc {
+  uint32_t i, j, k;  // the node's merge [i,j) + [j,k)
+  uint32_t lo, hi;   // output range of this tile
+  uint32_t a0, a1;   // elements of [i,j) among outputs [i,lo) / [i,hi)
+  uint32_t par;      // output buffer (depth parity)
+};
+
+// Warp-cooperative merge-path co-rank (32-ary search, ties to A): the number
+// of A elements among the first d outputs of merging A[0,nA) and B[0,nB).
 template <int KT>
-__global__ void __launch_bounds__(256) k_partition(
+__device__ __forceinline__ uint32_t warp_corank(const typename KeyTraits<KT>::K* A, uint32_t nA,
+                                                const typename KeyTraits<KT>::K* B, uint32_t nB,
+                                                uint32_t d, int lane) {
+  using T = KeyTraits<KT>;
+  uint32_t lo = d > nB ? d - nB : 0u, hi = min(d, nA);
+  // invariant: answer in [lo, hi]; P(m) = A[m] <= B[d-m-1] is true below it
+  while (hi - lo > 32) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t m = lo + (uint32_t)lane * step + step - 1;
+    const bool valid = m < hi;
+    const bool pr = valid && T::ord(A[m]) <= T::ord(B[d - m - 1]);
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, pr);
+    const uint32_t vb = __ballot_sync(0xFFFFFFFFu, valid);
+    const int c = __popc(bal);
+    const uint32_t mc1 = __shfl_sync(0xFFFFFFFFu, m, c > 0 ? c - 1 : 0);
+    const uint32_t mc = __shfl_sync(0xFFFFFFFFu, m, c < 32 ? c : 31);
+    const int nv = __popc(vb);
+    const uint32_t nlo = c > 0 ? mc1 + 1 : lo;
+    const uint32_t nhi = c < nv ? mc : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  const uint32_t m = lo + (uint32_t)lane;
+  const bool pr = m < hi && T::ord(A[m]) <= T::ord(B[d - m - 1]);
+  return lo + (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, pr));
+}
+
+// Tile descriptors of one level (one thread per tile: many independent
+// binary searches in flight hide the global-memory latency).
+template <int KT>
+__global__ void __launch_bounds__(256) k_tile_desc(
     const typename KeyTraits<KT>::K* __restrict__ k0, const typename KeyTraits<KT>::K* __restrict__ k1,
     const uint32_t* __restrict__ rs, const uint32_t* __restrict__ seg_l,
     const uint32_t* __restrict__ seg_r, const uint32_t* __restrict__ dep,
     const uint32_t* __restrict__ lnodes, const uint32_t* __restrict__ ltiles,
     const uint32_t* __restrict__ level_start, const uint32_t* __restrict__ level_tile, int p,
-    uint32_t tout, uint2* __restrict__ part) {
+    uint32_t tout, TileDesc* __restrict__ desc, uint32_t cap, uint32_t* scalars) {
   const uint32_t ls = level_start[p], le = level_start[p + 1];
   const uint32_t tb = level_tile[p], te = level_tile[p + 1];
+  if (te - tb > cap) {  // never expected: the bound in carve() is exact
+    if (blockIdx.x == 0 && threadIdx.x == 0) scalars[SC_ERROR] = 2;
+    return;
+  }
   for (uint32_t tau = tb + blockIdx.x * blockDim.x + threadIdx.x; tau < te;
        tau += gridDim.x * blockDim.x) {
-    uint32_t a = ls, b = le;  // last x with ltiles[x] <= tau
+    uint32_t a = ls, b = le;  // last bucket x with ltiles[x] <= tau
     while (b - a > 1) { uint32_t m = (a + b) >> 1; if (ltiles[m] <= tau) a = m; else b = m; }
     const uint32_t t = lnodes[a];
     const uint32_t i = rs[seg_l[t]], j = rs[t], k = rs[seg_r[t]];
-    const auto* src = (dep[t] & 1u) ? k0 : k1;
-    const uint32_t d = (tau - ltiles[a]) * tout;
-    part[tau - tb] = make_uint2(a, corank<KT>(src + i, j - i, src + j, k - j, d));
+    const uint32_t par = dep[t] & 1u;
+    const uint32_t g = i / tout + (tau - ltiles[a]);
+    const uint32_t lo = max(i, g * tout), hi = min(k, (g + 1) * tout);
+    const auto* src = par ? k0 : k1;
+    const uint32_t a0 = corank<KT>(src + i, j - i, src + j, k - j, lo - i);
+    TileDesc* D = desc + (tau - tb);
+    D->i = i; D->j = j; D->k = k; D->lo = lo; D->hi = hi; D->a0 = a0; D->par = par;
+    if (hi == k) D->a1 = j - i;
+    if (lo != i) desc[tau - tb - 1].a1 = a0;
   }
 }
 
-// One level of stable merges, persistent over the level's tiles.
+template <int KT, bool HV>
+struct MergeSmem {
+  using K = typename KeyTraits<KT>::K;
+  static constexpr uint32_t KB = DEFAULT_TOUT * sizeof(K) + 64;
+  static constexpr uint32_t VB = HV ? DEFAULT_TOUT * 4 + 64 : 0;
+  static constexpr uint32_t STAGE = KB + VB;
+  static constexpr uint32_t HDR = 256;  // 2 mbarriers at 0, 2 MergeHdr (48 B) at 64..160
+  static constexpr uint32_t BYTES = HDR + 2 * STAGE;
+};
+
+struct MergeHdr {
+  uint32_t a_base, nA, b_base, nB;    // key element offsets in the stage
+  uint32_t va_base, vb_base, lo, hi;  // value element offsets, output range
+  uint32_t par, pad[3];
+};
+static_assert(64 + 2 * sizeof(MergeHdr) <= 256, "merge smem header area");
+
+// Thread 0: fetch tile `tau` into stage `s` with 1-D bulk copies over the
+// 16-byte-aligned superset of each window (reads never cross a page).
+template <int KT, bool HV>
+__device__ __forceinline__ void merge_issue(const TileDesc* __restrict__ desc, uint32_t tau, uint32_t s,
+                                            unsigned char* smem, uint64_t* bars, MergeHdr* hdr,
+                                            const typename KeyTraits<KT>::K* k0, const uint32_t* v0,
+                                            const typename KeyTraits<KT>::K* k1, const uint32_t* v1) {
+  using SM = MergeSmem<KT, HV>;
+  using K = typename KeyTraits<KT>::K;
+  const TileDesc d = desc[tau];
+  const K* sk = d.par ? k0 : k1;
+  const uint32_t* sv = d.par ? v0 : v1;
+  const uint32_t nA = d.a1 - d.a0, cnt = d.hi - d.lo, nB = cnt - nA;
+  const uint32_t aoff = d.i + d.a0, boff = d.j + (d.lo - d.i) - d.a0;
+  unsigned char* st = smem + SM::HDR + s * SM::STAGE;
+  uint32_t total = 0;
+  MergeHdr h;
+  // keys
+  {
+    const uintptr_t ga = (uintptr_t)(sk + aoff), ga0 = ga & ~(uintptr_t)15;
+    const uint32_t bA = nA ? (uint32_t)(((ga + (uintptr_t)nA * sizeof(K) + 15) & ~(uintptr_t)15) - ga0) : 0u;
+    const uintptr_t gb = (uintptr_t)(sk + boff), gb0 = gb & ~(uintptr_t)15;
+    const uint32_t bB = nB ? (uint32_t)(((gb + (uintptr_t)nB * sizeof(K) + 15) & ~(uintptr_t)15) - gb0) : 0u;
+    h.a_base = (uint32_t)(ga - ga0) / sizeof(K);
+    h.b_base = (bA + (uint32_t)(gb - gb0)) / sizeof(K);
+    h.nA = nA;
+    h.nB = nB;
+    if (bA) { total += bA; }
+    if (bB) { total += bB; }
+    if (HV) {
+      const uintptr_t va = (uintptr_t)(sv + aoff), va0 = va & ~(uintptr_t)15;
+      const uint32_t vA = nA ? (uint32_t)(((va + (uintptr_t)nA * 4 + 15) & ~(uintptr_t)15) - va0) : 0u;
+      const uintptr_t vb = (uintptr_t)(sv + boff), vb0 = vb & ~(uintptr_t)15;
+      const uint32_t vB = nB ? (uint32_t)(((vb + (uintptr_t)nB * 4 + 15) & ~(uintptr_t)15) - vb0) : 0u;
+      h.va_base = (uint32_t)(va - va0) / 4;
+      h.vb_base = (vA + (uint32_t)(vb - vb0)) / 4;
+      total += vA + vB;
+      h.lo = d.lo; h.hi = d.hi; h.par = d.par;
+      hdr[s] = h;
+      mbar_arrive_expect_tx(&bars[s], total);
+      if (bA) bulk_g2s(st, (const void*)ga0, bA, &bars[s]);
+      if (bB) bulk_g2s(st + bA, (const void*)gb0, bB, &bars[s]);
+      if (vA) bulk_g2s(st + SM::KB, (const void*)va0, vA, &bars[s]);
+      if (vB) bulk_g2s(st + SM::KB + vA, (const void*)vb0, vB, &bars[s]);
+    } else {
+      h.va_base = h.vb_base = 0;
+      h.lo = d.lo; h.hi = d.hi; h.par = d.par;
+      hdr[s] = h;
+      mbar_arrive_expect_tx(&bars[s], total);
+      if (bA) bulk_g2s(st, (const void*)ga0, bA, &bars[s]);
+      if (bB) bulk_g2s(st + bA, (const void*)gb0, bB, &bars[s]);
+    }
+  }
+}
+
+template <typename K>
+__device__ __forceinline__ void store_vec8(K* dst, const K (&r)[MERGE_K]);
+template <>
+__device__ __forceinline__ void store_vec8<uint32_t>(uint32_t* dst, const uint32_t (&r)[MERGE_K]) {
+  st_v4(dst, r[0], r[1], r[2], r[3]);
+  st_v4(dst + 4, r[4], r[5], r[6], r[7]);
+}
+template <>
+__device__ __forceinline__ void store_vec8<uint64_t>(uint64_t* dst, const uint64_t (&r)[MERGE_K]) {
+#pragma unroll
+  for (int q = 0; q < (int)MERGE_K; q += 2)
+    st_v4(dst + q, (uint32_t)r[q], (uint32_t)(r[q] >> 32), (uint32_t)r[q + 1], (uint32_t)(r[q + 1] >> 32));
+}
+
+// One level of stable merges: persistent CTAs, double-buffered bulk copies,
+// merge-path inside the tile, 128-bit stores.
 template <int KT, bool HV>
 __global__ void __launch_bounds__(MERGE_BLOCK) k_merge_level(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
-    const uint32_t* __restrict__ rs, const uint32_t* __restrict__ seg_l,
-    const uint32_t* __restrict__ seg_r, const uint32_t* __restrict__ dep,
-    const uint32_t* __restrict__ lnodes, const uint32_t* __restrict__ ltiles,
-    const uint32_t* __restrict__ level_tile, int p, uint32_t tout,
-    const uint2* __restrict__ part) {
+    const TileDesc* __restrict__ desc, const uint32_t* __restrict__ level_tile, int p, uint32_t tout,
+    uint32_t cap) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
-  __shared__ K sk[DEFAULT_TOUT];
-  __shared__ uint32_t sv[HV ? DEFAULT_TOUT : 1];
-  const uint32_t tb = level_tile[p], count = level_tile[p + 1] - tb;
-  for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x) {
-    const uint2 pa = part[tau];
-    const uint32_t x = pa.x, a0 = pa.y;
-    const uint32_t t = lnodes[x];
-    const uint32_t i = rs[seg_l[t]], j = rs[t], k = rs[seg_r[t]];
-    const uint32_t nA = j - i, size = k - i;
-    const uint32_t d0 = (tau + tb - ltiles[x]) * tout;
-    const uint32_t d1 = min(d0 + tout, size);
-    uint32_t a1 = nA;
-    if (tau + 1 < count) {
-      const uint2 pn = part[tau + 1];
-      if (pn.x == x) a1 = pn.y;
-    }
-    const uint32_t b0 = d0 - a0, b1 = d1 - a1;
-    const uint32_t nAw = a1 - a0, cnt = d1 - d0;
-    const bool odd = dep[t] & 1u;
-    const K* srck = odd ? k0 : k1;
-    const uint32_t* srcv = odd ? v0 : v1;
-    K* dstk = odd ? k1 : k0;
-    uint32_t* dstv = odd ? v1 : v0;
-    for (uint32_t q = threadIdx.x; q < cnt; q += MERGE_BLOCK) {
-      uint32_t g = q < nAw ? i + a0 + q : j + b0 + (q - nAw);
-      sk[q] = srck[g];
-      if (HV) sv[q] = srcv[g];
-    }
-    __syncthreads();
-    K rk[MERGE_K];
-    uint32_t rv[MERGE_K];
-    const uint32_t q0 = threadIdx.x * MERGE_K;
-    if (q0 < cnt) {
-      const K* A = sk;
-      const K* B = sk + nAw;
-      const uint32_t nBw = cnt - nAw;
-      uint32_t ia = corank<KT>(A, nAw, B, nBw, q0), ib = q0 - ia;
+  using SM = MergeSmem<KT, HV>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  MergeHdr* hdr = reinterpret_cast<MergeHdr*>(smem + 64);
+  const uint32_t count = level_tile[p + 1] - level_tile[p];
+  if (blockIdx.x >= count || count > cap) return;
+  const uint32_t tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) merge_issue<KT, HV>(desc, blockIdx.x, 0, smem, bars, hdr, k0, v0, k1, v1);
+  uint32_t it = 0;
+  for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
+    const uint32_t s = it & 1u;
+    if (tid == 0 && tau + gridDim.x < count)
+      merge_issue<KT, HV>(desc, tau + gridDim.x, s ^ 1u, smem, bars, hdr, k0, v0, k1, v1);
+    mbar_wait(&bars[s], (it >> 1) & 1u);
+    const MergeHdr h = hdr[s];
+    const unsigned char* st = smem + SM::HDR + s * SM::STAGE;
+    const K* A = reinterpret_cast<const K*>(st) + h.a_base;
+    const K* B = reinterpret_cast<const K*>(st) + h.b_base;
+    const uint32_t* VA = reinterpret_cast<const uint32_t*>(st + SM::KB) + h.va_base;
+    const uint32_t* VB = reinterpret_cast<const uint32_t*>(st + SM::KB) + h.vb_base;
+    const uint32_t base = (h.lo / tout) * tout;
+    const uint32_t start = base + tid * MERGE_K;
+    if (start < h.hi && start + MERGE_K > h.lo) {
+      const uint32_t qs = max(start, h.lo), qe = min(start + MERGE_K, h.hi);
+      const uint32_t d = qs - h.lo;
+      uint32_t ia = corank<KT>(A, h.nA, B, h.nB, d), ib = d - ia;
+      K rk[MERGE_K];
+      uint32_t rv[MERGE_K];
 #pragma unroll
-      for (int s = 0; s < (int)MERGE_K; ++s) {
-        bool takeA = ib >= nBw || (ia < nAw && T::ord(A[ia]) <= T::ord(B[ib]));
-        if (takeA) { rk[s] = A[ia]; if (HV) rv[s] = sv[ia]; ++ia; }
-        else { rk[s] = B[ib]; if (HV) rv[s] = sv[nAw + ib]; ++ib; }
+      for (int q = 0; q < (int)MERGE_K; ++q) {
+        const uint32_t pos = start + q;
+        if (pos >= qs && pos < qe) {
+          const bool takeA = ib >= h.nB || (ia < h.nA && T::ord(A[ia]) <= T::ord(B[ib]));
+          if (takeA) { rk[q] = A[ia]; if (HV) rv[q] = VA[ia]; ++ia; }
+          else { rk[q] = B[ib]; if (HV) rv[q] = VB[ib]; ++ib; }
+        } else {
+          rk[q] = K(0);
+          rv[q] = 0u;
+        }
       }
-    }
-    __syncthreads();
-    if (q0 < cnt) {
+      K* dk = h.par ? k1 : k0;
+      uint32_t* dv = h.par ? v1 : v0;
+      if (qs == start && qe == start + MERGE_K) {
+        store_vec8<K>(dk + start, rk);
+        if (HV) store_vec8<uint32_t>(dv + start, rv);
+      } else {
 #pragma unroll
-      for (int s = 0; s < (int)MERGE_K; ++s) {
-        if (q0 + s < cnt) { sk[q0 + s] = rk[s]; if (HV) sv[q0 + s] = rv[s]; }
+        for (int q = 0; q < (int)MERGE_K; ++q) {
+          const uint32_t pos = start + q;
+          if (pos >= qs && pos < qe) { dk[pos] = rk[q]; if (HV) dv[pos] = rv[q]; }
+        }
       }
-    }
-    __syncthreads();
-    for (uint32_t q = threadIdx.x; q < cnt; q += MERGE_BLOCK) {
-      dstk[i + d0 + q] = sk[q];
-      if (HV) dstv[i + d0 + q] = sv[q];
     }
     __syncthreads();
   }

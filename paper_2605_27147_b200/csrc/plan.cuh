@@ -292,7 +292,13 @@ __global__ void k_level_tiles(const uint32_t* __restrict__ rs, const uint32_t* s
   const uint32_t m = scalars[SC_NONFUSED];
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= cap;
        x += gridDim.x * blockDim.x) {
-    tiles[x] = x < m ? (seg_size(rs, seg_l, seg_r, lnodes[x]) + tout - 1) / tout : 0u;
+    uint32_t c = 0;
+    if (x < m) {  // tiles aligned to global multiples of tout (see k_tile_desc)
+      uint32_t t = lnodes[x];
+      uint32_t i = rs[seg_l[t]], k = rs[seg_r[t]];
+      c = (k + tout - 1) / tout - i / tout;
+    }
+    tiles[x] = c;
   }
 }
 

@@ -107,6 +107,7 @@ struct Work {
   uint32_t* unit_idx;    // scan of unit_flag
   uint32_t* long_idx;    // scan of long_flag
   uint32_t* units;       // [3 * rmax]: start, end, parity (compacted)
+  uint32_t* batch_first; // first unit of each leaf batch (n / Z + 2)
   uint32_t* longs;       // [4 * rmax]: start, end, parity|desc<<1, chunk offset
   uint32_t* level_cnt;   // LEVEL_SLOTS
   uint32_t* level_start; // LEVEL_SLOTS + 1 (node offsets)
@@ -115,7 +116,7 @@ struct Work {
   uint32_t* lnodes;      // bucketed non-fused nodes
   uint32_t* ltiles_cnt;  // tiles per bucketed node
   uint32_t* ltiles;      // tile offset per bucketed node (exclusive scan)
-  uint2* part;           // per tile of a level: (bucket index, corank at tile start)
+  void* desc;            // TileDesc per tile of one level
   uint32_t part_cap;
   uint32_t* scan_tmp;    // block sums for scans
   unsigned long long* counters;  // [0] M, [1] fused M

@@ -1,0 +1,11 @@
+cd $GRAFT_REPO_ROOT
+R=gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q --maxfail=3 -k "not full_size" > $R/it_tests.log 2>&1; echo "tests=$?" > $R/it_status.txt
+VMPS_DEBUG_SYNC=1 timeout 300 python bench.py --steps 1 --warmup 1 --log2n 26 --no-e2e --no-cpu-baseline > $R/it_dbg26.log 2>&1; echo "dbg=$?" >> $R/it_status.txt
+timeout 600 python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline > $R/it_bench30.log 2>&1; echo "bench30=$?" >> $R/it_status.txt
+B26="python bench.py --steps 1 --warmup 1 --log2n 26 --no-e2e --no-cpu-baseline"
+if [ "${NCU:-0}" = "1" ]; then
+timeout 300 $B26 > $R/it_plain26.log 2>&1 && \
+ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_merge_level -s 25 -c 2 -o $R/prof_merge $B26 > $R/it_ncu_merge.log 2>&1 ; \
+ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_leaf_sort|k_runs_tables|k_runs_emit|k_tile_desc" -s 20 -c 6 -o $R/prof_misc $B26 > $R/it_ncu_misc.log 2>&1; echo "ncu=$?" >> $R/it_status.txt
+fi
