@@ -526,31 +526,49 @@ __global__ void __launch_bounds__(MERGE_BLOCK) k_merge_level(
     if (start < h.hi && start + MERGE_K > h.lo) {
       const uint32_t qs = max(start, h.lo), qe = min(start + MERGE_K, h.hi);
       const uint32_t d = qs - h.lo;
-      uint32_t ia = corank<KT>(A, h.nA, B, h.nB, d), ib = d - ia;
-      K rk[MERGE_K];
-      uint32_t rv[MERGE_K];
-#pragma unroll
-      for (int q = 0; q < (int)MERGE_K; ++q) {
-        const uint32_t pos = start + q;
-        if (pos >= qs && pos < qe) {
-          const bool takeA = ib >= h.nB || (ia < h.nA && T::ord(A[ia]) <= T::ord(B[ib]));
-          if (takeA) { rk[q] = A[ia]; if (HV) rv[q] = VA[ia]; ++ia; }
-          else { rk[q] = B[ib]; if (HV) rv[q] = VB[ib]; ++ib; }
-        } else {
-          rk[q] = K(0);
-          rv[q] = 0u;
-        }
-      }
+      const K* SK = reinterpret_cast<const K*>(st);
+      const uint32_t* SV = reinterpret_cast<const uint32_t*>(st + SM::KB);
       K* dk = h.par ? k1 : k0;
       uint32_t* dv = h.par ? v1 : v0;
       if (qs == start && qe == start + MERGE_K) {
+        // full chunk: branch-free serial merge over absolute stage indices;
+        // reading one past a side stays inside the stage buffer (slack)
+        const uint32_t l = corank<KT>(A, h.nA, B, h.nB, d);
+        uint32_t ia = h.a_base + l, ib = h.b_base + d - l;
+        const uint32_t ea = h.a_base + h.nA, eb = h.b_base + h.nB;
+        const int32_t dA = (int32_t)h.va_base - (int32_t)h.a_base;
+        const int32_t dB = (int32_t)h.vb_base - (int32_t)h.b_base;
+        K ka = SK[ia], kb = SK[ib];
+        K rk[MERGE_K];
+        uint32_t ri[MERGE_K];
+#pragma unroll
+        for (int q = 0; q < (int)MERGE_K; ++q) {
+          const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
+          rk[q] = pa ? ka : kb;
+          ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
+          ia += pa ? 1u : 0u;
+          ib += pa ? 0u : 1u;
+          const K nx = SK[pa ? ia : ib];
+          ka = pa ? nx : ka;
+          kb = pa ? kb : nx;
+        }
         store_vec8<K>(dk + start, rk);
-        if (HV) store_vec8<uint32_t>(dv + start, rv);
-      } else {
+        if (HV) {
+          uint32_t rv[MERGE_K];
+#pragma unroll
+          for (int q = 0; q < (int)MERGE_K; ++q) rv[q] = SV[ri[q]];
+          store_vec8<uint32_t>(dv + start, rv);
+        }
+      } else {  // tile edge: the chunk is partly outside [lo, hi)
+        uint32_t ia = corank<KT>(A, h.nA, B, h.nB, d), ib = d - ia;
 #pragma unroll
         for (int q = 0; q < (int)MERGE_K; ++q) {
           const uint32_t pos = start + q;
-          if (pos >= qs && pos < qe) { dk[pos] = rk[q]; if (HV) dv[pos] = rv[q]; }
+          if (pos >= qs && pos < qe) {
+            const bool takeA = ib >= h.nB || (ia < h.nA && T::ord(A[ia]) <= T::ord(B[ib]));
+            if (takeA) { dk[pos] = A[ia]; if (HV) dv[pos] = VA[ia]; ++ia; }
+            else { dk[pos] = B[ib]; if (HV) dv[pos] = VB[ib]; ++ib; }
+          }
         }
       }
     }
