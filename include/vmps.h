@@ -128,6 +128,33 @@ vmps_status_t vmps_merge_plan(const void* keys, uint64_t n, vmps_key_t kt, uint6
                               uint8_t* run_kind, vmps_merge_rec_t* merges, uint64_t cap_runs,
                               uint64_t* h_num_runs, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- multi-GPU building blocks (BASELINE.json north_star) ----
+ * A sharded sort runs on every rank: local vmps_sort_pairs, exact splitters
+ * by a distributed binary search over the key order image using
+ * vmps_count_rank, an NCCL all-to-all of the pieces (torch.distributed), and
+ * vmps_merge_runs over the received pieces (ordered by source rank).
+ *
+ * vmps_count_rank: keys[0,n) sorted under the key order; probes[p] (device,
+ * u64) are values of the order image (u32/u64 as is; f32 the image that
+ * makes -0.0 < +0.0 and NaNs last and equal, as a u32 in the low bits).
+ * Writes out_lt[p] = #{x : img(x) < probes[p]} and out_le[p] = #{x : img(x)
+ * <= probes[p]} (device u64 arrays).  Stream-ordered, no synchronisation. */
+vmps_status_t vmps_count_rank(const void* keys, uint64_t n, vmps_key_t kt, const uint64_t* probes,
+                              uint32_t nprobe, uint64_t* out_lt, uint64_t* out_le, void* stream);
+
+/* vmps_merge_runs: keys[0,n) (and vals, if non-NULL) consist of nruns adjacent
+ * runs, each sorted, starting at h_run_start[0] = 0 < h_run_start[1] < ...
+ * (host array).  Merges them in place into the stable sort of the array,
+ * ties to the earlier run (Alg. 2 tie rule), along a balanced tree of
+ * pairwise merges executed level by level on the level-merge engine.
+ * Workspace: vmps_merge_runs_workspace_bytes.  Synchronises `stream` once
+ * (to upload the small tree description). */
+vmps_status_t vmps_merge_runs_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals,
+                                              uint32_t nruns, size_t* h_bytes);
+vmps_status_t vmps_merge_runs(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt,
+                              const uint64_t* h_run_start, uint32_t nruns, void* ws,
+                              size_t ws_bytes, void* stream);
+
 /* Human-readable status; the last CUDA error detail of this thread. */
 const char* vmps_status_string(vmps_status_t s);
 const char* vmps_last_error(void);

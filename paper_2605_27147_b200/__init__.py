@@ -53,6 +53,7 @@ class MergeRec(ctypes.Structure):
 
 
 EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_merge_plan",
+           "vmps_count_rank", "vmps_merge_runs_workspace_bytes", "vmps_merge_runs",
            "vmps_status_string", "vmps_last_error", "vmps_profile_enable", "vmps_profile_read",
            "vmps_test_set_minrun", "vmps_test_set_tiles")
 
@@ -73,7 +74,13 @@ def lib() -> ctypes.CDLL:
         L.vmps_sort_pairs.argtypes = [vp, vp, u64, ctypes.c_int, i64, vp, sz, vp, ctypes.POINTER(Stats)]
         L.vmps_merge_plan.argtypes = [vp, u64, ctypes.c_int, vp, vp, vp, u64, ctypes.POINTER(u64),
                                       vp, sz, vp]
-        for f in ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_merge_plan"):
+        L.vmps_count_rank.argtypes = [vp, u64, ctypes.c_int, vp, ctypes.c_uint32, vp, vp, vp]
+        L.vmps_merge_runs_workspace_bytes.argtypes = [u64, ctypes.c_int, ctypes.c_int, ctypes.c_uint32,
+                                                      ctypes.POINTER(sz)]
+        L.vmps_merge_runs.argtypes = [vp, vp, u64, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
+                                      ctypes.c_uint32, vp, sz, vp]
+        for f in ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_merge_plan",
+                  "vmps_count_rank", "vmps_merge_runs_workspace_bytes", "vmps_merge_runs"):
             getattr(L, f).restype = ctypes.c_int
         L.vmps_status_string.restype = ctypes.c_char_p
         L.vmps_status_string.argtypes = [ctypes.c_int]

@@ -7,7 +7,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
+#include <vector>
 
 #include "engine.cuh"
 #include "plan.cuh"
@@ -614,6 +616,230 @@ void vmps_test_set_tiles(uint32_t fuse_z, uint32_t merge_tile, uint32_t block_el
   g_fuse_z = fuse_z;
   g_tout = merge_tile;
   g_blk = block_elems;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Multi-GPU building blocks: rank counting and merging of sorted runs.
+// ===========================================================================
+namespace vmps {
+
+template <int KT>
+__global__ void k_count_rank(const typename KeyTraits<KT>::K* __restrict__ keys, uint32_t n,
+                             const uint64_t* __restrict__ probes, uint32_t np,
+                             unsigned long long* __restrict__ lt, unsigned long long* __restrict__ le) {
+  using T = KeyTraits<KT>;
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const uint64_t v = probes[p];
+  uint32_t a = 0, b = n;  // first x with img >= v
+  while (a < b) { uint32_t m = (a + b) >> 1; if ((uint64_t)T::ord(keys[m]) < v) a = m + 1; else b = m; }
+  lt[p] = a;
+  b = n;  // first x with img > v (from a on)
+  while (a < b) { uint32_t m = (a + b) >> 1; if ((uint64_t)T::ord(keys[m]) <= v) a = m + 1; else b = m; }
+  le[p] = a;
+}
+
+// Host description of a balanced merge tree over nruns sorted runs.
+struct MRLayout {
+  uint32_t m;       // runs
+  uint32_t H;       // tree height
+  size_t off_rs, off_segl, off_segr, off_dep, off_lnodes, off_ltiles, off_lstart, off_ltile,
+      off_longs, off_longoff, off_scalars, off_desc, off_k1, off_v1, total;
+  uint32_t part_cap;
+};
+
+static MRLayout mr_layout(uint64_t n, int kt, int hv, uint32_t m) {
+  MRLayout L;
+  memset(&L, 0, sizeof(L));
+  L.m = m;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += align_up(bytes); return o; };
+  const size_t R = (size_t)m + 2;
+  L.off_k1 = take(n * key_bytes(kt));
+  L.off_v1 = hv ? take(n * 4) : 0;
+  L.off_rs = take(R * 4);
+  L.off_segl = take(R * 4);
+  L.off_segr = take(R * 4);
+  L.off_dep = take(R * 4);
+  L.off_lnodes = take(R * 4);
+  L.off_ltiles = take(R * 4);
+  L.off_lstart = take((LEVEL_SLOTS + 1) * 4);
+  L.off_ltile = take((LEVEL_SLOTS + 1) * 4);
+  L.off_longs = take(R * 4 * 4);
+  L.off_longoff = take(R * 4);
+  L.off_scalars = take(SC_COUNT * 4 + 64);
+  L.part_cap = (uint32_t)(n / DEFAULT_TOUT + 2 * (size_t)m + 8);
+  L.off_desc = take((size_t)L.part_cap * sizeof(TileDesc));
+  L.total = off;
+  return L;
+}
+
+template <int KT, bool HV>
+static vmps_status_t merge_runs_impl(void* keys, uint32_t* vals, uint64_t n, const uint64_t* h_rs,
+                                     uint32_t m, char* base, cudaStream_t s) {
+  using K = typename KeyTraits<KT>::K;
+  MRLayout L = mr_layout(n, KT, HV ? 1 : 0, m);
+  const size_t R = (size_t)m + 2;
+  // ---- build the tree on the host (balanced split at the middle run) ----
+  std::vector<uint32_t> rs(R, 0), segl(R, 0), segr(R, 0), dep(R, 0), height(R, 0);
+  for (uint32_t t = 0; t < m; ++t) rs[t] = (uint32_t)h_rs[t];
+  rs[m] = (uint32_t)n;
+  std::vector<uint32_t> leaf_depth(m, 0);
+  struct Frame { uint32_t lo, hi, depth; };
+  // recursive build via explicit post-order to compute heights
+  std::vector<uint32_t> order;  // internal nodes in post-order
+  std::function<uint32_t(uint32_t, uint32_t, uint32_t)> build = [&](uint32_t lo, uint32_t hi, uint32_t d) -> uint32_t {
+    if (hi - lo == 1) { leaf_depth[lo] = d; return 0; }
+    uint32_t mid = (lo + hi) / 2;
+    uint32_t h1 = build(lo, mid, d + 1), h2 = build(mid, hi, d + 1);
+    segl[mid] = lo; segr[mid] = hi; dep[mid] = d & 1u;
+    height[mid] = 1 + std::max(h1, h2);
+    order.push_back(mid);
+    return height[mid];
+  };
+  uint32_t H = build(0, m, 0);
+  L.H = H;
+  if (H + 2 > (uint32_t)LEVEL_SLOTS) { g_err = "merge_runs: too many runs"; return VMPS_ERR_INVALID_ARG; }
+  std::vector<uint32_t> lnodes, ltiles, lstart(LEVEL_SLOTS + 1, 0), ltile(LEVEL_SLOTS + 1, 0);
+  for (uint32_t h = 0; h <= (uint32_t)LEVEL_SLOTS - 1; ++h) {
+    lstart[h] = (uint32_t)lnodes.size();
+    for (uint32_t t : order) if (height[t] == h) lnodes.push_back(t);
+  }
+  lstart[LEVEL_SLOTS] = (uint32_t)lnodes.size();
+  uint32_t acc = 0;
+  for (uint32_t x = 0; x < lnodes.size(); ++x) {
+    ltiles.push_back(acc);
+    uint32_t t = lnodes[x];
+    uint32_t i = rs[segl[t]], k = rs[segr[t]];
+    acc += (k + DEFAULT_TOUT - 1) / DEFAULT_TOUT - i / DEFAULT_TOUT;
+  }
+  ltiles.push_back(acc);
+  for (uint32_t h = 0; h <= (uint32_t)LEVEL_SLOTS; ++h) ltile[h] = ltiles[lstart[h]];
+  // odd-depth leaves start in buffer 1 (copied there by the long-leaf kernel)
+  std::vector<uint32_t> longs, longoff;
+  uint32_t nlong = 0, chunks = 0;
+  for (uint32_t t = 0; t < m; ++t) {
+    if (leaf_depth[t] & 1u) {
+      uint32_t a = rs[t], e = rs[t + 1];
+      longs.push_back(a); longs.push_back(e); longs.push_back(1u); longs.push_back(0u);
+      longoff.push_back(chunks);
+      chunks += (e - a + LONG_CHUNK - 1) / LONG_CHUNK;
+      ++nlong;
+    }
+  }
+  longoff.push_back(chunks);
+  std::vector<uint32_t> scal(SC_COUNT, 0);
+  scal[SC_LONG] = nlong;
+  // ---- upload ----
+  auto up = [&](size_t off, const void* src, size_t bytes) -> cudaError_t {
+    if (!bytes) return cudaSuccess;
+    return cudaMemcpyAsync(base + off, src, bytes, cudaMemcpyHostToDevice, s);
+  };
+  VMPS_CK(up(L.off_rs, rs.data(), R * 4));
+  VMPS_CK(up(L.off_segl, segl.data(), R * 4));
+  VMPS_CK(up(L.off_segr, segr.data(), R * 4));
+  VMPS_CK(up(L.off_dep, dep.data(), R * 4));
+  VMPS_CK(up(L.off_lnodes, lnodes.data(), lnodes.size() * 4));
+  VMPS_CK(up(L.off_ltiles, ltiles.data(), ltiles.size() * 4));
+  VMPS_CK(up(L.off_lstart, lstart.data(), lstart.size() * 4));
+  VMPS_CK(up(L.off_ltile, ltile.data(), ltile.size() * 4));
+  VMPS_CK(up(L.off_longs, longs.data(), longs.size() * 4));
+  VMPS_CK(up(L.off_longoff, longoff.data(), longoff.size() * 4));
+  VMPS_CK(up(L.off_scalars, scal.data(), SC_COUNT * 4));
+  VMPS_CK(cudaStreamSynchronize(s));  // host vectors die at return
+  K* k0 = (K*)keys;
+  K* k1 = (K*)(base + L.off_k1);
+  uint32_t* v0 = vals;
+  uint32_t* v1 = HV ? (uint32_t*)(base + L.off_v1) : nullptr;
+  uint32_t* d_scal = (uint32_t*)(base + L.off_scalars);
+  LAUNCH((k_long_leaves<KT, HV>), nsm() * 8, 256, 0, s, k0, v0, k1, v1, (const uint32_t*)(base + L.off_longs),
+         (const uint32_t*)(base + L.off_longoff), d_scal, LONG_CHUNK);
+  using SM = MergeSmem<KT, HV>;
+  VMPS_CK(cudaFuncSetAttribute(k_merge_level<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::BYTES));
+  int occ = 0;
+  VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_merge_level<KT, HV>, MERGE_BLOCK, SM::BYTES));
+  const unsigned gm = (unsigned)(nsm() * (occ > 0 ? occ : 1));
+  TileDesc* desc = (TileDesc*)(base + L.off_desc);
+  for (uint32_t h = 1; h <= H; ++h) {
+    LAUNCH(k_tile_desc<KT>, (L.part_cap + 255) / 256, 256, 0, s, k0, k1, (const uint32_t*)(base + L.off_rs),
+           (const uint32_t*)(base + L.off_segl), (const uint32_t*)(base + L.off_segr),
+           (const uint32_t*)(base + L.off_dep), (const uint32_t*)(base + L.off_lnodes),
+           (const uint32_t*)(base + L.off_ltiles), (const uint32_t*)(base + L.off_lstart),
+           (const uint32_t*)(base + L.off_ltile), (int)h, (uint32_t)DEFAULT_TOUT, desc, L.part_cap, d_scal);
+    LAUNCH((k_merge_level<KT, HV>), gm, MERGE_BLOCK, SM::BYTES, s, k0, v0, k1, v1, desc,
+           (const uint32_t*)(base + L.off_ltile), (int)h, (uint32_t)DEFAULT_TOUT, L.part_cap);
+  }
+  return launch_check();
+}
+
+}  // namespace vmps
+
+extern "C" {
+
+vmps_status_t vmps_count_rank(const void* keys, uint64_t n, vmps_key_t kt, const uint64_t* probes,
+                              uint32_t nprobe, uint64_t* out_lt, uint64_t* out_le, void* stream) {
+  vmps_status_t rc = check_common(keys, nullptr, n, kt);
+  if (rc != VMPS_OK) return rc;
+  if (nprobe == 0) return VMPS_OK;
+  if (!probes || !out_lt || !out_le) { g_err = "NULL probe/output"; return VMPS_ERR_INVALID_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned g = (nprobe + 127) / 128;
+  switch (kt) {
+    case VMPS_KEY_U32:
+      k_count_rank<VMPS_KEY_U32><<<g, 128, 0, s>>>((const uint32_t*)keys, (uint32_t)n, probes, nprobe,
+                                                   (unsigned long long*)out_lt, (unsigned long long*)out_le);
+      break;
+    case VMPS_KEY_U64:
+      k_count_rank<VMPS_KEY_U64><<<g, 128, 0, s>>>((const uint64_t*)keys, (uint32_t)n, probes, nprobe,
+                                                   (unsigned long long*)out_lt, (unsigned long long*)out_le);
+      break;
+    default:
+      k_count_rank<VMPS_KEY_F32><<<g, 128, 0, s>>>((const uint32_t*)keys, (uint32_t)n, probes, nprobe,
+                                                   (unsigned long long*)out_lt, (unsigned long long*)out_le);
+  }
+  ++g_nl;
+  return launch_check();
+}
+
+vmps_status_t vmps_merge_runs_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, uint32_t nruns,
+                                              size_t* h_bytes) {
+  if (!h_bytes || nruns == 0) return VMPS_ERR_INVALID_ARG;
+  if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
+  if (n >= (1ull << 32)) return VMPS_ERR_INVALID_ARG;
+  *h_bytes = mr_layout(n, kt, has_vals ? 1 : 0, nruns).total + 256;
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_merge_runs(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt, const uint64_t* h_run_start,
+                              uint32_t nruns, void* ws, size_t ws_bytes, void* stream) {
+  vmps_status_t rc = check_common(keys, vals, n, kt);
+  if (rc != VMPS_OK) return rc;
+  if (!h_run_start || nruns == 0) { g_err = "no runs"; return VMPS_ERR_INVALID_ARG; }
+  if (h_run_start[0] != 0) { g_err = "run_start[0] must be 0"; return VMPS_ERR_INVALID_ARG; }
+  for (uint32_t t = 1; t < nruns; ++t)
+    if (h_run_start[t] <= h_run_start[t - 1] || h_run_start[t] >= n) {
+      g_err = "run starts must be strictly increasing and < n";
+      return VMPS_ERR_INVALID_ARG;
+    }
+  if (nruns == 1 || n <= 1) return VMPS_OK;
+  const int hv = vals ? 1 : 0;
+  MRLayout L = mr_layout(n, kt, hv, nruns);
+  char* base = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  if (!ws || (size_t)(base - (char*)ws) + L.total > ws_bytes) { g_err = "workspace too small"; return VMPS_ERR_BUDGET; }
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (kt) {
+    case VMPS_KEY_U32:
+      return hv ? merge_runs_impl<VMPS_KEY_U32, true>(keys, vals, n, h_run_start, nruns, base, s)
+                : merge_runs_impl<VMPS_KEY_U32, false>(keys, vals, n, h_run_start, nruns, base, s);
+    case VMPS_KEY_U64:
+      return hv ? merge_runs_impl<VMPS_KEY_U64, true>(keys, vals, n, h_run_start, nruns, base, s)
+                : merge_runs_impl<VMPS_KEY_U64, false>(keys, vals, n, h_run_start, nruns, base, s);
+    default:
+      return hv ? merge_runs_impl<VMPS_KEY_F32, true>(keys, vals, n, h_run_start, nruns, base, s)
+                : merge_runs_impl<VMPS_KEY_F32, false>(keys, vals, n, h_run_start, nruns, base, s);
+  }
 }
 
 }  // extern "C"
