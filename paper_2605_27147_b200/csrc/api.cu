@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "bounded.cuh"
 #include "engine.cuh"
 #include "plan.cuh"
 #include "runs.cuh"
@@ -75,9 +76,11 @@ struct Cfg {
   int kt;
   int hv;         // 1 with payload, 0 keys only, -1 plan only
   uint32_t minrun, fuse_z, tout;
+  int64_t scratch;  // VMPS_SCRATCH_UNBOUNDED or the element cap
+  uint32_t P, F;    // bounded mode: block size, scratch blocks
 };
 
-static Cfg make_cfg(uint64_t n, int kt, int hv) {
+static Cfg make_cfg(uint64_t n, int kt, int hv, int64_t scratch = VMPS_SCRATCH_UNBOUNDED) {
   Cfg c;
   c.n = n;
   c.kt = kt;
@@ -85,8 +88,23 @@ static Cfg make_cfg(uint64_t n, int kt, int hv) {
   c.minrun = g_minrun_override ? g_minrun_override : minrun_rule(n);
   c.fuse_z = g_fuse_z ? g_fuse_z : DEFAULT_FUSE_Z;
   c.tout = g_tout ? g_tout : DEFAULT_TOUT;
+  c.scratch = scratch;
+  c.P = c.F = 0;
+  if (scratch >= 0 && hv >= 0) {
+    // block size: a power of two <= min(Z, T_out) (nodes are then longer than
+    // a block, so a block meets at most 3 tile pieces), test hook override
+    // default: the largest power of two <= S / 16 (>= 16 scratch blocks)
+    uint32_t P = g_blk ? g_blk : (uint32_t)std::max<int64_t>(16, std::min<int64_t>(scratch / 16, DEFAULT_TOUT));
+    P = std::min(P, std::min(c.fuse_z, (uint32_t)DEFAULT_TOUT));
+    uint32_t p2 = 16;
+    while (p2 * 2 <= P) p2 *= 2;
+    c.P = p2;
+    c.F = (uint32_t)std::min<int64_t>(scratch / (int64_t)c.P, (int64_t)(n / c.P + 8));
+    c.tout = c.P;  // tiles = blocks
+  }
   return c;
 }
+constexpr uint32_t BD_MIN_BLOCKS = 6;
 
 static size_t key_bytes(int kt) { return kt == VMPS_KEY_U64 ? 8 : 4; }
 
@@ -111,9 +129,12 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
   t.kt = c.kt;
   t.has_vals = c.hv;
   const size_t R = (size_t)t.rmax + 2;
+  t.bounded = c.scratch >= 0 && c.hv >= 0;
   if (c.hv >= 0) {
-    t.k1 = take(n * key_bytes(c.kt));
-    t.v1 = c.hv ? (uint32_t*)take(n * 4) : nullptr;
+    const size_t se = t.bounded ? (size_t)c.F * c.P : (size_t)n;  // element scratch
+    t.k1 = take(se * key_bytes(c.kt));
+    t.v1 = c.hv ? (uint32_t*)take(se * 4) : nullptr;
+    t.scratch_bytes = se * (key_bytes(c.kt) + (c.hv ? 4 : 0));
   }
   t.bits = (uint32_t*)take(((size_t)t.ntiles * RT_WORDS + RT_WORDS + 8) * 4);
   t.tile_tab = (uint32_t*)take((size_t)t.ntiles * t.ns * 4);
@@ -165,6 +186,37 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.scan_tmp = (uint32_t*)take(scan_tmp_words(R) * 4 + 64);
   }
   t.counters = (unsigned long long*)take(8 * 8);
+  if (t.bounded) {
+    t.P = c.P;
+    t.F = c.F;
+    t.NB = (uint32_t)((n + c.P - 1) / c.P);
+    const size_t NBp = (size_t)t.NB + 8, NP = (size_t)t.NB + c.F + 8;
+    t.Tin = (uint32_t*)take(NBp * 4);
+    t.Tout = (uint32_t*)take(NBp * 4);
+    t.inv = (uint32_t*)take(NP * 4);
+    t.pool = (uint32_t*)take(NP * 4);
+    t.remain = (uint32_t*)take(NBp * 4);
+    t.dirty = (uint32_t*)take(NBp * 4);
+    t.didx = (uint32_t*)take(NBp * 4);
+    t.dlist = (uint32_t*)take(NBp * 4);
+    t.first_tile = (uint32_t*)take(NBp * 4);
+    t.bflag = (uint32_t*)take(R * 4);
+    t.bpos = (uint32_t*)take(R * 4);
+    t.blnodes = (uint32_t*)take(R * 4);
+    t.bcnt = (uint32_t*)take(R * 4);
+    t.btoff = (uint32_t*)take(R * 4);
+    t.bm = (uint32_t*)take(64);
+    t.bD = (uint32_t*)take(64);
+    t.bdesc_cap = (uint32_t)(n / c.P + 4 * (n / c.fuse_z) + 16);
+    t.bdesc = take((size_t)t.bdesc_cap * sizeof(TileDesc));
+    t.bstate = take(sizeof(BdState));
+    t.copy_batch = std::max<uint32_t>(1, c.F / 3);
+    t.clist1 = (uint32_t*)take((size_t)2 * t.copy_batch * 3 * 4 + 64);
+    t.clist2 = (uint32_t*)take((size_t)t.copy_batch * 3 * 4 + 64);
+    t.ncopy = (uint32_t*)take(64);
+    t.deferred = (uint32_t*)take((size_t)(2 * t.copy_batch + 8) * 4);
+    t.ndef = (uint32_t*)take(64);
+  }
   t.used_bytes = off;
   if (w) *w = t;
   return off;
@@ -300,6 +352,111 @@ static vmps_status_t front_half(const Work& w, const void* keys, cudaStream_t s)
   return launch_check();
 }
 
+
+// ---- scratch-bounded mode: level rounds and the final Copy (bounded.cuh) ----
+template <int KT, bool HV>
+static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0, uint32_t* v0, int p_hi,
+                                    cudaStream_t s) {
+  using K = typename KeyTraits<KT>::K;
+  BdMem<KT> M;
+  M.k0 = k0; M.v0 = v0; M.ks = (K*)w.k1; M.vs = w.v1;
+  M.NB = w.NB; M.P = w.P; M.n = w.n; M.has_partial = (w.n % w.P) != 0;
+  BdState* st = (BdState*)w.bstate;
+  const unsigned g = grid_for(w.rmax);
+  const unsigned gNB = grid_for(w.NB + 8);
+  LAUNCH(k_bd_init, gNB, 256, 0, s, st, w.pool, w.Tin, w.NB, w.F);
+  TileDesc* desc = (TileDesc*)w.bdesc;
+  BdState hs;
+  for (int p = p_hi; p >= 1; --p) {
+    LAUNCH(k_bd_flags, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.fuse_z, p, w.rmax,
+           w.bflag);
+    scan_u32(w.bflag, w.bpos, w.rmax + 1, w.scan_tmp, s);
+    LAUNCH(k_bd_nodes, g, 256, 0, s, w.run_start, w.scalars, w.seg_l, w.seg_r, w.bflag, w.bpos, w.rmax,
+           w.blnodes, w.bm);
+    LAUNCH(k_bd_tile_counts, g, 256, 0, s, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.bm, w.P, w.n, w.rmax,
+           w.bcnt);
+    scan_u32(w.bcnt, w.btoff, w.rmax + 1, w.scan_tmp, s);
+    uint32_t m = 0, total = 0;
+    VMPS_CK(cudaMemcpyAsync(&m, w.bm, 4, cudaMemcpyDeviceToHost, s));
+    VMPS_CK(cudaStreamSynchronize(s));
+    if (m == 0) continue;
+    VMPS_CK(cudaMemcpyAsync(&total, w.btoff + m, 4, cudaMemcpyDeviceToHost, s));
+    VMPS_CK(cudaStreamSynchronize(s));
+    if (total > w.bdesc_cap) { g_err = "internal: bounded tile capacity"; return VMPS_ERR_INTERNAL; }
+    LAUNCH(k_bd_tile_desc<KT>, grid_for(total), 256, 0, s, M, w.Tin, w.run_start, w.seg_l, w.seg_r, w.blnodes,
+           w.bm, w.btoff, desc);
+    VMPS_CK(cudaMemsetAsync(w.dirty, 0, (size_t)(w.NB + 1) * 4, s));
+    LAUNCH(k_bd_mark, grid_for(total), 256, 0, s, desc, w.btoff, w.bm, w.P, w.dirty);
+    scan_u32(w.dirty, w.didx, w.NB + 1, w.scan_tmp, s);
+    LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, grid_for(total)), 256, 0, s, M, desc, w.btoff, w.bm, w.dirty,
+           w.didx, w.dlist, w.first_tile, w.remain, w.bD);
+    // rounds until every dirty block of the level is produced
+    for (;;) {
+      for (int q = 0; q < 16; ++q) {
+        LAUNCH(k_bd_alloc, 1, 32, 0, s, st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
+        LAUNCH((k_bd_merge<KT, HV>), nsm() * 4, MERGE_BLOCK, 0, s, M, st, desc, w.Tin, w.Tout, w.pool, w.remain);
+      }
+      uint32_t D = 0;
+      VMPS_CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+      VMPS_CK(cudaMemcpyAsync(&D, w.bD, 4, cudaMemcpyDeviceToHost, s));
+      VMPS_CK(cudaStreamSynchronize(s));
+      if (hs.err) { g_err = "scratch budget too small for the bounded mode"; return VMPS_ERR_BUDGET; }
+      if (hs.w >= D) break;
+    }
+    LAUNCH(k_bd_commit, gNB, 256, 0, s, w.dlist, w.bD, w.Tout, w.Tin);
+    // next level starts its dirty list from zero
+    VMPS_CK(cudaMemsetAsync(&st->w, 0, 4, s));
+  }
+  // final Copy: permute the blocks into physical order
+  LAUNCH(k_bd_inverse, grid_for(w.NB + w.F), 256, 0, s, w.Tin, w.NB, w.NB + w.F, w.inv);
+  LAUNCH(k_bd_inverse2, gNB, 256, 0, s, w.Tin, w.NB, w.inv);
+  VMPS_CK(cudaMemsetAsync(w.ndef, 0, 4, s));
+  const uint32_t B = w.copy_batch;
+  for (uint32_t q0 = 0; q0 < w.NB; q0 += B) {
+    const uint32_t q1 = std::min(w.NB, q0 + B);
+    LAUNCH(k_bd_copy_plan, 1, 32, 0, s, st, w.Tin, w.inv, w.pool, w.NB, w.P, w.n, (uint32_t)M.has_partial, q0,
+           q1, w.clist1, w.clist2, w.ncopy, w.deferred, w.ndef);
+    LAUNCH((k_bd_copy<KT, HV>), 2 * B, 256, 0, s, M, w.clist1, w.ncopy, 0);
+    LAUNCH((k_bd_copy<KT, HV>), B, 256, 0, s, M, w.clist2, w.ncopy, 1);
+  }
+  VMPS_CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  VMPS_CK(cudaStreamSynchronize(s));
+  if (hs.err) { g_err = "scratch budget too small for the bounded Copy"; return VMPS_ERR_BUDGET; }
+  return launch_check();
+}
+
+template <bool HV>
+static vmps_status_t bounded_stats(const Work& w, vmps_stats_t* st, cudaStream_t s) {
+  if (g_prof && g_prof_host) {
+    VMPS_CK(cudaMemcpyAsync(g_prof_host, w.counters, 16, cudaMemcpyDeviceToHost, s));
+    g_prof_wbytes = (int)(key_bytes(w.kt) + (HV ? 4 : 0));
+  }
+  if (!st) return VMPS_OK;
+  uint32_t sc[SC_COUNT];
+  unsigned long long ct[8];
+  BdState hs;
+  VMPS_CK(cudaMemcpyAsync(sc, w.scalars, sizeof(sc), cudaMemcpyDeviceToHost, s));
+  VMPS_CK(cudaMemcpyAsync(ct, w.counters, sizeof(ct), cudaMemcpyDeviceToHost, s));
+  VMPS_CK(cudaMemcpyAsync(&hs, w.bstate, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  VMPS_CK(cudaStreamSynchronize(s));
+  memset(st, 0, sizeof(*st));
+  st->n = w.n;
+  st->runs = sc[SC_RUNS];
+  st->merges = sc[SC_RUNS] ? sc[SC_RUNS] - 1 : 0;
+  st->merge_cost_M = ct[0];
+  st->fused_M = ct[1];
+  st->reversed_elems = sc[SC_REVERSED];
+  st->extended_runs = sc[SC_EXTENDED];
+  st->max_power = sc[SC_MAXPOW];
+  st->minrun = w.minrun;
+  st->block_elems = w.P;
+  st->rounds = hs.rounds;
+  st->peak_extra_device_bytes = w.used_bytes;
+  st->scratch_bytes = w.scratch_bytes;
+  st->metadata_bytes = w.used_bytes - w.scratch_bytes;
+  return VMPS_OK;
+}
+
 static bool kernel_attrs_set[3][2] = {{false, false}, {false, false}, {false, false}};
 
 template <int KT, bool HV>
@@ -321,7 +478,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   scan_u32(w.unit_flag, w.unit_idx, w.rmax + 1, w.scan_tmp, s);
   scan_u32(w.long_flag, w.long_idx, w.rmax + 1, w.scan_tmp, s);
   LAUNCH(k_compact, g, 256, 0, s, w.run_start, w.scalars, w.unit_flag, w.unit_idx, w.long_flag, w.long_idx,
-         w.unit_end, w.unit_par, w.long_par, w.units, w.longs, w.long_chunks);
+         w.unit_end, w.unit_par, w.long_par, w.units, w.longs, w.long_chunks, w.bounded ? 0u : 1u);
   LAUNCH(k_zero_tail, g, 256, 0, s, w.long_chunks, w.scalars, (int)SC_LONG, w.rmax);
   scan_u32(w.long_chunks, w.long_off, w.rmax + 1, w.scan_tmp, s);
   LAUNCH(k_level_scan, 1, 32, 0, s, w.level_cnt, w.level_start, w.scalars);
@@ -359,6 +516,12 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   int p_hi = (int)std::ceil(lg) + 1;
   if (p_hi > LEVEL_SLOTS - 2) p_hi = LEVEL_SLOTS - 2;
   if (p_hi < 1) p_hi = 1;
+  if (w.bounded) {
+    rc = bounded_levels<KT, HV>(w, k0, v0, p_hi, s);
+    if (rc != VMPS_OK) return rc;
+    g_prof_mark[3] = prof_event(s);
+    return bounded_stats<HV>(w, st, s);
+  }
   using SM = MergeSmem<KT, HV>;
   static int merge_occ[3][2] = {{0, 0}, {0, 0}, {0, 0}};
   if (!merge_occ[KT][HV]) {
@@ -457,9 +620,8 @@ vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, int6
   if (!h_bytes) return VMPS_ERR_INVALID_ARG;
   if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
   if (n >= (1ull << 32)) return VMPS_ERR_INVALID_ARG;
-  (void)scratch_elems;
   if (n <= 1) { *h_bytes = 256; return VMPS_OK; }
-  Cfg c = make_cfg(n, kt, has_vals < 0 ? -1 : (has_vals ? 1 : 0));
+  Cfg c = make_cfg(n, kt, has_vals < 0 ? -1 : (has_vals ? 1 : 0), scratch_elems);
   *h_bytes = carve(c, nullptr, nullptr) + 256;
   return VMPS_OK;
 }
@@ -477,7 +639,11 @@ static vmps_status_t sort_any(void* keys, uint32_t* vals, uint64_t n, vmps_key_t
     return VMPS_OK;
   }
   const int hv = vals ? 1 : 0;
-  Cfg c = make_cfg(n, kt, hv);
+  Cfg c = make_cfg(n, kt, hv, scratch_elems);
+  if (scratch_elems >= 0 && c.F < BD_MIN_BLOCKS) {
+    g_err = "scratch_elems below the bounded mode's minimum (6 blocks)";
+    return VMPS_ERR_BUDGET;
+  }
   Work w;
   size_t need = carve(c, &w, nullptr);
   if (!ws || ws_bytes < need) {

@@ -1,0 +1,397 @@
+// bounded.cuh -- scratch-bounded mode (BASELINE.json north_star (4); SURVEY
+// 8(a) A9): element scratch capped at S = c sqrt(n log2 n) elements.
+//
+// The array is cut into blocks of P elements.  Physical blocks are the
+// caller's blocks 0..NB-1 plus F = floor(S / P) scratch blocks NB..NB+F-1; the
+// block table T_in maps virtual block v (positions [vP, vP+P)) to the
+// physical block holding it (the paper's page lists, as one array,
+// App. A).  Leaves are sorted in place.  Each tree level is then a
+// left-to-right stream of output blocks: a round takes free physical blocks
+// for the next dirty output blocks (T_out), runs their tiles -- merge tiles of
+// the level's nodes and copy tiles for the other elements of those blocks --
+// and every tile subtracts the elements it consumed from per-block counters;
+// a block whose counter reaches zero goes back to the free pool (a consumed
+// page is released and reused as output, Fig. 2).  At the end
+// the blocks are permuted into physical order with evictions (Copy).
+#pragma once
+#include "engine.cuh"
+#include "plan.cuh"
+
+namespace vmps {
+
+constexpr uint32_t BD_NONE = 0xFFFFFFFFu;
+
+struct BdState {          // device-side round state (one per sort)
+  uint32_t w;             // next dirty output block (index into the dirty list)
+  uint32_t tile_lo, tile_hi;
+  uint32_t err;           // 1 = no free block (budget too small)
+  uint32_t pool_count;    // free physical blocks
+  uint32_t rounds;        // rounds executed (statistics)
+  uint32_t copies;        // final Copy: block copies
+  uint32_t pad;
+};
+
+template <int KT>
+struct BdMem {
+  using K = typename KeyTraits<KT>::K;
+  K* k0; uint32_t* v0;    // caller's array
+  K* ks; uint32_t* vs;    // scratch blocks
+  uint32_t NB, P, n, has_partial;
+  __device__ __forceinline__ K* kb(uint32_t b) const {
+    return b < NB ? k0 + (size_t)b * P : ks + (size_t)(b - NB) * P;
+  }
+  __device__ __forceinline__ uint32_t* vb(uint32_t b) const {
+    return b < NB ? v0 + (size_t)b * P : vs + (size_t)(b - NB) * P;
+  }
+  __device__ __forceinline__ uint32_t vlen(uint32_t v) const {  // elements of virtual block v
+    return v + 1 < NB ? P : n - v * P;
+  }
+};
+
+// --- per-level setup ------------------------------------------------------
+// flag[t] = 1 for the non-fused nodes of power p (zero tail up to cap).
+__global__ void k_bd_flags(const uint32_t* __restrict__ rs, const uint32_t* scalars,
+                           const uint8_t* __restrict__ power, const uint32_t* __restrict__ seg_l,
+                           const uint32_t* __restrict__ seg_r, uint32_t fuse_z, int p, uint32_t cap,
+                           uint32_t* __restrict__ flag) {
+  const uint32_t r = scalars[SC_RUNS];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= cap; t += gridDim.x * blockDim.x) {
+    uint32_t f = 0;
+    if (t >= 1 && t < r && power[t] == p && seg_size(rs, seg_l, seg_r, t) > fuse_z) f = 1;
+    flag[t] = f;
+  }
+}
+
+// Nodes of the level in position order, and their tile counts: the node's
+// output tiles (one per block it touches) plus gap copy-tiles before/after it
+// inside its first/last block.
+__global__ void k_bd_nodes(const uint32_t* __restrict__ rs, const uint32_t* scalars,
+                           const uint32_t* __restrict__ seg_l, const uint32_t* __restrict__ seg_r,
+                           const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                           uint32_t cap, uint32_t* __restrict__ lnodes, uint32_t* __restrict__ m_out) {
+  const uint32_t r = scalars[SC_RUNS];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= cap; t += gridDim.x * blockDim.x) {
+    if (t < r && flag[t]) lnodes[pos[t]] = t;
+    if (t == cap) *m_out = pos[cap];
+  }
+}
+
+__device__ __forceinline__ void bd_node_geom(const uint32_t* rs, const uint32_t* seg_l, const uint32_t* seg_r,
+                                             const uint32_t* lnodes, uint32_t m, uint32_t x, uint32_t P,
+                                             uint32_t n, uint32_t* i, uint32_t* j, uint32_t* k,
+                                             uint32_t* lgap_lo, uint32_t* rgap_hi) {
+  const uint32_t t = lnodes[x];
+  *i = rs[seg_l[t]];
+  *j = rs[t];
+  *k = rs[seg_r[t]];
+  const uint32_t bs = (*i / P) * P;                                  // first block start
+  const uint32_t kprev = x > 0 ? rs[seg_r[lnodes[x - 1]]] : 0u;
+  *lgap_lo = (bs < *i && kprev <= bs) ? bs : *i;                     // [lgap_lo, i) copy tile
+  const uint32_t be = min(n, ((*k + P - 1) / P) * P);                // last block end
+  const uint32_t inext = x + 1 < m ? rs[seg_l[lnodes[x + 1]]] : n;
+  *rgap_hi = max(*k, min(be, inext));                                // [k, rgap_hi) copy tile
+}
+
+__global__ void k_bd_tile_counts(const uint32_t* __restrict__ rs, const uint32_t* __restrict__ seg_l,
+                                 const uint32_t* __restrict__ seg_r, const uint32_t* __restrict__ lnodes,
+                                 const uint32_t* __restrict__ m_ptr, uint32_t P, uint32_t n, uint32_t cap,
+                                 uint32_t* __restrict__ cnt) {
+  const uint32_t m = *m_ptr;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= cap; x += gridDim.x * blockDim.x) {
+    uint32_t c = 0;
+    if (x < m) {
+      uint32_t i, j, k, gl, gh;
+      bd_node_geom(rs, seg_l, seg_r, lnodes, m, x, P, n, &i, &j, &k, &gl, &gh);
+      c = (k + P - 1) / P - i / P + (gl < i ? 1u : 0u) + (gh > k ? 1u : 0u);
+    }
+    cnt[x] = c;
+  }
+}
+
+// Translated key load: virtual position q through the block table.
+template <int KT>
+__device__ __forceinline__ typename KeyTraits<KT>::K bd_key(const BdMem<KT>& M, const uint32_t* Tin,
+                                                            uint32_t q) {
+  return M.kb(Tin[q / M.P])[q % M.P];
+}
+
+template <int KT>
+__device__ uint32_t bd_corank(const BdMem<KT>& M, const uint32_t* Tin, uint32_t ai, uint32_t nA, uint32_t bi,
+                              uint32_t nB, uint32_t d) {
+  using T = KeyTraits<KT>;
+  uint32_t lo = d > nB ? d - nB : 0u, hi = min(d, nA);
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (T::ord(bd_key<KT>(M, Tin, ai + mid)) <= T::ord(bd_key<KT>(M, Tin, bi + d - mid - 1))) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Tile descriptors of the level in output order (one thread per tile).
+template <int KT>
+__global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_t* __restrict__ Tin,
+                                                      const uint32_t* __restrict__ rs,
+                                                      const uint32_t* __restrict__ seg_l,
+                                                      const uint32_t* __restrict__ seg_r,
+                                                      const uint32_t* __restrict__ lnodes,
+                                                      const uint32_t* __restrict__ m_ptr,
+                                                      const uint32_t* __restrict__ toff,
+                                                      TileDesc* __restrict__ desc) {
+  const uint32_t m = *m_ptr;
+  const uint32_t total = toff[m];
+  const uint32_t P = M.P, n = M.n;
+  for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x) {
+    uint32_t a = 0, b = m;  // last node x with toff[x] <= tau
+    while (b - a > 1) { uint32_t mm = (a + b) >> 1; if (toff[mm] <= tau) a = mm; else b = mm; }
+    uint32_t i, j, k, gl, gh;
+    bd_node_geom(rs, seg_l, seg_r, lnodes, m, a, P, n, &i, &j, &k, &gl, &gh);
+    uint32_t loc = tau - toff[a];
+    TileDesc D;
+    D.par = 0;
+    if (gl < i && loc == 0) {  // left gap: copy [gl, i)
+      D.i = gl; D.j = i; D.k = i; D.lo = gl; D.hi = i; D.a0 = 0; D.a1 = i - gl;
+      desc[tau] = D;
+      continue;
+    }
+    if (gl < i) --loc;
+    const uint32_t nt = (k + P - 1) / P - i / P;
+    if (loc >= nt) {  // right gap: copy [k, gh)
+      D.i = k; D.j = gh; D.k = gh; D.lo = k; D.hi = gh; D.a0 = 0; D.a1 = gh - k;
+      desc[tau] = D;
+      continue;
+    }
+    const uint32_t g = i / P + loc;
+    const uint32_t lo = max(i, g * P), hi = min(k, (g + 1) * P);
+    const uint32_t a0 = bd_corank<KT>(M, Tin, i, j - i, j, k - j, lo - i);
+    TileDesc* Dp = desc + tau;
+    Dp->i = i; Dp->j = j; Dp->k = k; Dp->lo = lo; Dp->hi = hi; Dp->a0 = a0; Dp->par = 0;
+    if (hi == k) Dp->a1 = j - i;
+    if (lo != i) desc[tau - 1].a1 = a0;
+  }
+}
+
+// Dirty output blocks (touched by a tile), their list and first tiles,
+// and the per-block counters of elements to consume.
+__global__ void k_bd_mark(const TileDesc* __restrict__ desc, const uint32_t* __restrict__ toff,
+                          const uint32_t* __restrict__ m_ptr, uint32_t P, uint32_t* __restrict__ dirty) {
+  const uint32_t total = toff[*m_ptr];
+  for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x)
+    dirty[desc[tau].lo / P] = 1u;
+}
+
+template <int KT>
+__global__ void k_bd_dirty_list(BdMem<KT> M, const TileDesc* __restrict__ desc, const uint32_t* __restrict__ toff,
+                                const uint32_t* __restrict__ m_ptr, const uint32_t* __restrict__ dirty,
+                                const uint32_t* __restrict__ didx, uint32_t* __restrict__ dlist,
+                                uint32_t* __restrict__ first_tile, uint32_t* __restrict__ remain,
+                                uint32_t* __restrict__ D_out) {
+  const uint32_t total = toff[*m_ptr];
+  const uint32_t NB = M.NB, P = M.P;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < NB; v += gridDim.x * blockDim.x) {
+    if (dirty[v]) {
+      dlist[didx[v]] = v;
+      remain[v] = M.vlen(v);
+    }
+  }
+  for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x) {
+    const uint32_t v = desc[tau].lo / P;
+    if (tau == 0 || desc[tau - 1].lo / P != v) first_tile[didx[v]] = tau;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint32_t D = didx[NB];
+    *D_out = D;
+    first_tile[D] = total;
+  }
+}
+
+// --- rounds -----------------------------------------------------------------
+// Allocate free physical blocks to the next dirty output blocks (one thread).
+__global__ void k_bd_alloc(BdState* st, const uint32_t* __restrict__ dlist, const uint32_t* __restrict__ first_tile,
+                           const uint32_t* __restrict__ D_ptr, uint32_t* __restrict__ pool,
+                           uint32_t* __restrict__ Tout, uint32_t max_take) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const uint32_t D = *D_ptr;
+  if (st->err || st->w >= D) { st->tile_lo = st->tile_hi = 0; return; }
+  uint32_t take = min(min(st->pool_count, D - st->w), max_take);
+  if (take == 0) { st->err = 1; st->tile_lo = st->tile_hi = 0; return; }
+  for (uint32_t x = 0; x < take; ++x) Tout[dlist[st->w + x]] = pool[st->pool_count - 1 - x];
+  st->pool_count -= take;
+  st->tile_lo = first_tile[st->w];
+  st->tile_hi = first_tile[st->w + take];
+  st->w += take;
+  st->rounds++;
+}
+
+__device__ __forceinline__ void bd_release(BdState* st, uint32_t* pool, uint32_t* remain, const uint32_t* Tin,
+                                           uint32_t NB, uint32_t has_partial, uint32_t v, uint32_t cnt) {
+  if (!cnt) return;
+  const uint32_t old = atomicSub(&remain[v], cnt);
+  if (old == cnt) {
+    const uint32_t b = Tin[v];
+    if (has_partial && b == NB - 1) return;  // the partial last block is never freed
+    const uint32_t at = atomicAdd(&st->pool_count, 1u);
+    pool[at] = b;
+  }
+}
+
+// Consume [q, q+len) of virtual positions: decrement the touched blocks.
+__device__ __forceinline__ void bd_consume(BdState* st, uint32_t* pool, uint32_t* remain, const uint32_t* Tin,
+                                           uint32_t NB, uint32_t P, uint32_t has_partial, uint32_t q, uint32_t len) {
+  while (len) {
+    const uint32_t v = q / P, off = q % P;
+    const uint32_t c = min(len, P - off);
+    bd_release(st, pool, remain, Tin, NB, has_partial, v, c);
+    q += c;
+    len -= c;
+  }
+}
+
+// Run the round's tiles: translated loads into shared memory, stable merge,
+// stores into the tile's output block; then release consumed input blocks.
+template <int KT, bool HV>
+__global__ void __launch_bounds__(MERGE_BLOCK) k_bd_merge(BdMem<KT> M, BdState* st, const TileDesc* __restrict__ desc,
+                                                          const uint32_t* __restrict__ Tin,
+                                                          const uint32_t* __restrict__ Tout, uint32_t* __restrict__ pool,
+                                                          uint32_t* __restrict__ remain) {
+  using T = KeyTraits<KT>;
+  using K = typename T::K;
+  __shared__ K sk[DEFAULT_TOUT];
+  __shared__ uint32_t sv[HV ? DEFAULT_TOUT : 1];
+  const uint32_t tlo = st->tile_lo, thi = st->tile_hi;
+  const uint32_t P = M.P;
+  for (uint32_t tau = tlo + blockIdx.x; tau < thi; tau += gridDim.x) {
+    const TileDesc d = desc[tau];
+    const uint32_t nA = d.a1 - d.a0, cnt = d.hi - d.lo, nB = cnt - nA;
+    const uint32_t aoff = d.i + d.a0, boff = d.j + (d.lo - d.i) - d.a0;
+    for (uint32_t q = threadIdx.x; q < cnt; q += MERGE_BLOCK) {
+      const uint32_t g = q < nA ? aoff + q : boff + (q - nA);
+      const uint32_t b = Tin[g / P], o = g % P;
+      sk[q] = M.kb(b)[o];
+      if (HV) sv[q] = M.vb(b)[o];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bd_consume(st, pool, remain, Tin, M.NB, P, M.has_partial, aoff, nA);
+      bd_consume(st, pool, remain, Tin, M.NB, P, M.has_partial, boff, nB);
+    }
+    const uint32_t v = d.lo / P;
+    K* dk = M.kb(Tout[v]);  // output block; element q lands at offset d.lo + q - v P
+    uint32_t* dv = HV ? M.vb(Tout[v]) : nullptr;
+    const uint32_t obase = d.lo - v * P;
+    for (uint32_t q0 = threadIdx.x * MERGE_K; q0 < cnt; q0 += MERGE_BLOCK * MERGE_K) {
+      uint32_t ia = corank<KT>(sk, nA, sk + nA, nB, q0), ib = q0 - ia;
+      const uint32_t qe = min(q0 + MERGE_K, cnt);
+      for (uint32_t q = q0; q < qe; ++q) {
+        const bool takeA = ib >= nB || (ia < nA && T::ord(sk[ia]) <= T::ord(sk[nA + ib]));
+        const uint32_t s = takeA ? ia : nA + ib;
+        dk[obase + q] = sk[s];
+        if (HV) dv[obase + q] = sv[s];
+        ia += takeA ? 1u : 0u;
+        ib += takeA ? 0u : 1u;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// After a level: the table maps the dirty blocks to their new homes.
+__global__ void k_bd_commit(const uint32_t* __restrict__ dlist, const uint32_t* __restrict__ D_ptr,
+                            const uint32_t* __restrict__ Tout, uint32_t* __restrict__ Tin) {
+  const uint32_t D = *D_ptr;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < D; x += gridDim.x * blockDim.x)
+    Tin[dlist[x]] = Tout[dlist[x]];
+}
+
+// --- final Copy: permute blocks into physical order --------------------------
+__global__ void k_bd_inverse(const uint32_t* __restrict__ Tin, uint32_t NB, uint32_t nphys,
+                             uint32_t* __restrict__ inv) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nphys; b += gridDim.x * blockDim.x) inv[b] = BD_NONE;
+}
+__global__ void k_bd_inverse2(const uint32_t* __restrict__ Tin, uint32_t NB, uint32_t* __restrict__ inv) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < NB; v += gridDim.x * blockDim.x) inv[Tin[v]] = v;
+}
+
+// Plan one batch of virtual blocks [q0, q1) (one thread): copy list 1 stages
+// every misplaced block into a free block and evicts later blocks that occupy
+// a target; copy list 2 writes the staged blocks home.  Blocks released by the
+// previous batch are returned to the pool first.
+__global__ void k_bd_copy_plan(BdState* st, uint32_t* __restrict__ Tin, uint32_t* __restrict__ inv,
+                               uint32_t* __restrict__ pool, uint32_t NB, uint32_t P, uint32_t n, uint32_t has_partial,
+                               uint32_t q0, uint32_t q1, uint32_t* __restrict__ c1, uint32_t* __restrict__ c2,
+                               uint32_t* __restrict__ ncopy, uint32_t* __restrict__ deferred,
+                               uint32_t* __restrict__ ndef) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (uint32_t x = 0; x < *ndef; ++x) pool[st->pool_count++] = deferred[x];
+  *ndef = 0;
+  uint32_t n1 = 0, n2 = 0;
+  if (st->err) { ncopy[0] = ncopy[1] = 0; return; }
+  auto vlen = [&](uint32_t v) -> uint32_t { return v + 1 < NB ? P : n - v * P; };
+  // a free block usable as temporary storage: never an array block < q1
+  // (those are placed targets or this batch's targets); such blocks are dropped
+  auto pop = [&]() -> uint32_t {
+    while (st->pool_count) {
+      const uint32_t b = pool[--st->pool_count];
+      if (b >= q1) return b;
+    }
+    return BD_NONE;
+  };
+  for (uint32_t q = q0; q < q1; ++q) {
+    const uint32_t src = Tin[q];
+    if (src == q) continue;
+    // evict a later virtual block that lives in physical q
+    const uint32_t w = inv[q];
+    if (w != BD_NONE && w >= q1) {
+      const uint32_t e = pop();
+      if (e == BD_NONE) { st->err = 1; break; }
+      c1[3 * n1] = q; c1[3 * n1 + 1] = e; c1[3 * n1 + 2] = vlen(w); ++n1;
+      Tin[w] = e;
+      inv[e] = w;
+      inv[q] = BD_NONE;
+    }
+    const uint32_t tmp = pop();
+    if (tmp == BD_NONE) { st->err = 1; break; }
+    c1[3 * n1] = src; c1[3 * n1 + 1] = tmp; c1[3 * n1 + 2] = vlen(q); ++n1;
+    c2[3 * n2] = tmp; c2[3 * n2 + 1] = q; c2[3 * n2 + 2] = vlen(q); ++n2;
+    deferred[(*ndef)++] = tmp;
+    if (src >= q1 && !(has_partial && src == NB - 1)) {  // the old home is free now
+      deferred[(*ndef)++] = src;
+      inv[src] = BD_NONE;
+    }
+    Tin[q] = q;
+    inv[q] = q;
+  }
+  ncopy[0] = n1;
+  ncopy[1] = n2;
+  st->copies += n1 + n2;
+}
+
+template <int KT, bool HV>
+__global__ void __launch_bounds__(256) k_bd_copy(BdMem<KT> M, const uint32_t* __restrict__ list,
+                                                 const uint32_t* __restrict__ ncopy, int which) {
+  const uint32_t nc = ncopy[which];
+  for (uint32_t c = blockIdx.x; c < nc; c += gridDim.x) {
+    const uint32_t a = list[3 * c], b = list[3 * c + 1], len = list[3 * c + 2];
+    const auto* sk = M.kb(a);
+    auto* dk = M.kb(b);
+    for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) dk[q] = sk[q];
+    if (HV) {
+      const uint32_t* sv = M.vb(a);
+      uint32_t* dv = M.vb(b);
+      for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) dv[q] = sv[q];
+    }
+  }
+}
+
+// Initial pool: the scratch blocks.
+__global__ void k_bd_init(BdState* st, uint32_t* __restrict__ pool, uint32_t* __restrict__ Tin, uint32_t NB,
+                          uint32_t F) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < NB; v += gridDim.x * blockDim.x) Tin[v] = v;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < F; x += gridDim.x * blockDim.x) pool[x] = NB + x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->w = 0; st->tile_lo = st->tile_hi = 0; st->err = 0; st->pool_count = F;
+    st->rounds = 0; st->copies = 0;
+  }
+}
+
+}  // namespace vmps

@@ -225,7 +225,8 @@ __global__ void k_compact(const uint32_t* __restrict__ rs, uint32_t* scalars,
                           const uint32_t* __restrict__ long_idx,
                           const uint32_t* __restrict__ unit_end, const uint8_t* __restrict__ unit_par,
                           const uint8_t* __restrict__ long_par, uint32_t* __restrict__ units,
-                          uint32_t* __restrict__ longs, uint32_t* __restrict__ long_chunks) {
+                          uint32_t* __restrict__ longs, uint32_t* __restrict__ long_chunks,
+                          uint32_t par_mask) {
   const uint32_t r = scalars[SC_RUNS];
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u <= r;
        u += gridDim.x * blockDim.x) {
@@ -239,11 +240,11 @@ __global__ void k_compact(const uint32_t* __restrict__ rs, uint32_t* scalars,
       uint32_t x = unit_idx[u];
       units[3 * x + 0] = rs[u];
       units[3 * x + 1] = unit_end[u];
-      units[3 * x + 2] = unit_par[u];
+      units[3 * x + 2] = unit_par[u] & par_mask;
     }
     if (long_flag[u]) {
       uint32_t x = long_idx[u];
-      uint32_t s = rs[u], e = rs[u + 1], f = long_par[u];
+      uint32_t s = rs[u], e = rs[u + 1], f = long_par[u] & (2u | par_mask);
       longs[4 * x + 0] = s;
       longs[4 * x + 1] = e;
       longs[4 * x + 2] = f;

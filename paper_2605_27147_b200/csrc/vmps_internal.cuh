@@ -120,6 +120,17 @@ struct Work {
   uint32_t part_cap;
   uint32_t* scan_tmp;    // block sums for scans
   unsigned long long* counters;  // [0] M, [1] fused M
+  // scratch-bounded mode (bounded.cuh); element scratch = F blocks of P
+  int bounded;
+  uint32_t P, F, NB;
+  uint32_t *Tin, *Tout, *inv, *pool, *remain, *dirty, *didx, *dlist, *first_tile;
+  uint32_t *bflag, *bpos, *blnodes, *bcnt, *btoff, *bm, *bD;
+  void* bdesc;
+  uint32_t bdesc_cap;
+  void* bstate;
+  uint32_t *clist1, *clist2, *ncopy, *deferred, *ndef;
+  uint32_t copy_batch;
+  size_t scratch_bytes;
   size_t used_bytes;
 };
 

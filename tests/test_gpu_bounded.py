@@ -1,0 +1,98 @@
+"""Scratch-bounded mode: same output as the unbounded mode and
+the oracle, element scratch within the cap c*sqrt(n log2 n) (reading R7),
+peak bytes reported; small blocks and tiny caps force many rounds, block
+evictions and a long final Copy."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+from tests.test_gpu_parity import _structured, check_case  # noqa: F401  (fixtures reuse)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def vm():
+    import paper_2605_27147_b200 as vm
+    assert torch.cuda.is_available()
+    vm.lib()
+    yield vm
+    vm.test_set_minrun(0)
+    vm.test_set_tiles(0, 0, 0)
+
+
+def cap(n, c=4):
+    return int(c * math.sqrt(n * math.log2(n)))
+
+
+def bounded_vs_oracle(vm, keys, vals, scratch, minrun=0):
+    vm.test_set_minrun(minrun)
+    ko, vo, _, ost = oracle.sort(keys, vals, minrun_override=minrun)
+    k = W.from_numpy(keys, "cuda")
+    v = None if vals is None else W.from_numpy(vals, "cuda")
+    st = vm.sort_(k, v, scratch=scratch, stats=True)
+    torch.cuda.synchronize()
+    assert W.to_numpy(k).view(np.uint8).tobytes() == ko.view(np.uint8).tobytes(), "keys differ"
+    if vals is not None:
+        assert (W.to_numpy(v) == vo).all(), "payload differs"
+    assert st["merge_cost_M"] == ost["merge_cost_M"]
+    w = keys.dtype.itemsize + (4 if vals is not None else 0)
+    assert st["scratch_bytes"] <= scratch * w, (st["scratch_bytes"], scratch * w)
+    assert st["block_elems"] > 0
+    return st
+
+
+@pytest.mark.parametrize("dtype", [np.uint32, np.uint64, np.float32])
+def test_bounded_tiny_blocks(vm, dtype):
+    rng = np.random.default_rng(300 + (dtype == np.uint64) + 2 * (dtype == np.float32))
+    try:
+        for trial in range(30):
+            blk = int(rng.choice([16, 32, 64]))
+            vm.test_set_tiles(64, 0, blk)
+            n = int(rng.integers(100, 8000))
+            keys = _structured(rng, n, dtype)
+            vals = np.arange(n, dtype=np.uint32) if trial % 3 else None
+            nblocks = int(rng.integers(6, 40))
+            bounded_vs_oracle(vm, keys, vals, scratch=nblocks * blk, minrun=int(rng.choice([0, 1, 4])))
+    finally:
+        vm.test_set_tiles(0, 0, 0)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_bounded_configs_reduced(vm, cfg):
+    vm.test_set_tiles(0, 0, 0)
+    n = 1 << 18
+    k, v = W.make(cfg, n=n, device="cpu")
+    st = bounded_vs_oracle(vm, W.to_numpy(k), None if v is None else W.to_numpy(v), scratch=cap(n))
+    assert st["rounds"] > 0
+
+
+def test_bounded_cfg2_full(vm):
+    """cfg2 at its BASELINE.json size and cap: n = 2^24, scratch = 4 sqrt(n log2 n)
+    = 80,264 elements; identical to the unbounded sort and to the oracle."""
+    vm.test_set_tiles(0, 0, 0)
+    vm.test_set_minrun(0)
+    n = 1 << 24
+    S = cap(n)
+    assert S == 80264
+    k, v = W.cfg2(device="cuda")
+    k1, v1 = k.clone(), v.clone()
+    st_b = vm.sort_(k, v, scratch=S, stats=True)
+    st_u = vm.sort_(k1, v1, stats=True)
+    torch.cuda.synchronize()
+    assert torch.equal(k.view(torch.int32), k1.view(torch.int32))
+    assert torch.equal(v.view(torch.int32), v1.view(torch.int32))
+    assert st_b["scratch_bytes"] <= S * 8
+    assert st_b["peak_extra_device_bytes"] < st_u["peak_extra_device_bytes"]
+
+
+def test_bounded_budget_error(vm):
+    vm.test_set_tiles(0, 0, 0)
+    k = torch.randint(0, 1000, (100000,), dtype=torch.int32, device="cuda").view(torch.uint32)
+    with pytest.raises(vm.VmpsError) as e:
+        vm.sort_(k, scratch=60)  # fewer than 6 blocks of the minimum 16 elements
+    assert e.value.status == 3
