@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-log2", type=int, default=25)
     ap.add_argument("--ref-sample-log2", type=int, default=23)
+    ap.add_argument("--bounded-reps", type=int, default=2,
+                    help="timed sorts of the scratch-bounded mode (cap 4 sqrt(n log2 n)); 0 = skip")
     return ap.parse_args()
 
 
@@ -330,6 +332,34 @@ def main():
                "ms_per_step": float(te.item()), "steps": ks}
         del hk, hv, ok_, ov_
 
+    bounded = None
+    if world == 1 and args.bounded_reps > 0:
+        import math
+        S = int(4 * math.sqrt(n * math.log2(n)))
+        keys.copy_(keys0)
+        vals.copy_(vals0)
+        bws = vm.Workspace()
+        bst = vm.sort_(keys, vals, scratch=S, stats=True, workspace=bws)  # warm-up + stats
+        bt = []
+        for _ in range(args.bounded_reps):
+            keys.copy_(keys0)
+            vals.copy_(vals0)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            vm.sort_(keys, vals, scratch=S, workspace=bws)
+            e1.record(stream)
+            e1.synchronize()
+            bt.append(e0.elapsed_time(e1))
+        bms = statistics.mean(bt)
+        bounded = {"scratch_cap_elems": S, "c": 4, "ms_per_step": bms, "value": n / (bms / 1000) / 1e9,
+                   "unit": UNIT, "slowdown_vs_unbounded": bms / ms,
+                   "scratch_bytes": bst["scratch_bytes"], "metadata_bytes": bst["metadata_bytes"],
+                   "peak_extra_device_bytes": bst["peak_extra_device_bytes"],
+                   "unbounded_peak_extra_device_bytes": stats["peak_extra_device_bytes"],
+                   "block_elems": bst["block_elems"], "rounds": bst["rounds"]}
+        del bws
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         model, ncpu = cpu_info()
@@ -352,7 +382,7 @@ def main():
                           "runs": stats["runs"], "merge_cost_M": M, "max_power": stats["max_power"],
                           "levels_executed": stats["levels_executed"]},
                "roofline": roof, "tree_roofline": tree, "phases_ms": ph,
-               "cpu_baseline": cpu, "e2e": e2e,
+               "cpu_baseline": cpu, "e2e": e2e, "bounded": bounded,
                "gpu_launches": launches, "clocks": clk, "verified": ok}
         print(json.dumps(out), flush=True)
     if world > 1:
