@@ -475,8 +475,8 @@ template <typename K>
 __device__ __forceinline__ void store_vec8(K* dst, const K (&r)[MERGE_K]);
 template <>
 __device__ __forceinline__ void store_vec8<uint32_t>(uint32_t* dst, const uint32_t (&r)[MERGE_K]) {
-  st_v4(dst, r[0], r[1], r[2], r[3]);
-  st_v4(dst + 4, r[4], r[5], r[6], r[7]);
+#pragma unroll
+  for (int q = 0; q < (int)MERGE_K; q += 4) st_v4(dst + q, r[q], r[q + 1], r[q + 2], r[q + 3]);
 }
 template <>
 __device__ __forceinline__ void store_vec8<uint64_t>(uint64_t* dst, const uint64_t (&r)[MERGE_K]) {
