@@ -339,7 +339,7 @@ static vmps_status_t front_half(const Work& w, const void* keys, cudaStream_t s)
       LAUNCH(k_chain_expand<uint64_t>, w.chain_m[l + 1], 256, sm64, s, w.chain_tab[l - 1], w.chain_m[l], w.ns,
              w.chain_entry[l + 1], w.chain_entry[l]);
   }
-  LAUNCH(k_runs_emit, w.ntiles, 32, 0, s, w.bits, w.n, w.minrun, w.chain_entry[0], w.run_start, w.run_kind,
+  LAUNCH(k_runs_emit, w.ntiles, 128, 0, s, w.bits, w.n, w.minrun, w.chain_entry[0], w.run_start, w.run_kind,
          w.scalars);
   const unsigned g = grid_for(w.rmax);
   LAUNCH(k_powers_seg, g, 256, 0, s, w.run_start, w.n, w.scalars, w.power, w.seg_l, w.seg_r);

@@ -127,7 +127,139 @@ __device__ __forceinline__ bool resolve_entry(const TileCtx& c, uint32_t s, uint
   return true;
 }
 
-// K1+K2: descent bitmap (warp ballots) and the tile's transfer table.
+// Per-word suffix tables of a tile: fs[w] / fc[w] = first position >= 32w in
+// [0, L) whose bit is set / clear (L if none).  One warp.
+__device__ __forceinline__ void tile_suffix_tables(const uint32_t* sb, uint32_t L, uint16_t* fs, uint16_t* fc,
+                                                   int lane) {
+  // each lane owns words [5 lane, 5 lane + 5) (covers 160 >= RT_WORDS + 1 words)
+  constexpr int PER = 5;
+  uint32_t ls = L, lc = L;  // first set / clear within the lane's words
+  uint32_t vs[PER], vc[PER];
+#pragma unroll
+  for (int q = PER - 1; q >= 0; --q) {
+    const uint32_t w = (uint32_t)lane * PER + q;
+    uint32_t setm = 0, clrm = 0;
+    if (32 * w < L) {
+      const uint32_t nvalid = min(32u, L - 32 * w);
+      const uint32_t vm = nvalid == 32 ? 0xFFFFFFFFu : ((1u << nvalid) - 1u);
+      setm = sb[w] & vm;
+      clrm = ~sb[w] & vm;
+    }
+    if (setm) ls = 32 * w + (uint32_t)(__ffs(setm) - 1);
+    if (clrm) lc = 32 * w + (uint32_t)(__ffs(clrm) - 1);
+    vs[q] = ls;
+    vc[q] = lc;
+  }
+  // suffix-min across lanes: the first hit of all later lanes
+  uint32_t ns = ls, nc = lc;  // lane's own first (= value at its first word)
+  uint32_t as = L, ac = L;    // min over lanes > me
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t ys = __shfl_down_sync(0xFFFFFFFFu, ns, o);
+    const uint32_t yc = __shfl_down_sync(0xFFFFFFFFu, nc, o);
+    if (lane + o < 32) { ns = min(ns, ys); nc = min(nc, yc); }
+  }
+  as = __shfl_down_sync(0xFFFFFFFFu, ns, 1);
+  ac = __shfl_down_sync(0xFFFFFFFFu, nc, 1);
+  if (lane == 31) { as = L; ac = L; }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const uint32_t w = (uint32_t)lane * PER + q;
+    if (w <= RT_WORDS + 1) {
+      fs[w] = (uint16_t)min(vs[q], as);
+      fc[w] = (uint16_t)min(vc[q], ac);
+    }
+  }
+}
+
+// first set (want) / clear bit at position >= p within [0, L), via the tables
+__device__ __forceinline__ uint32_t tile_first(const uint32_t* sb, const uint16_t* ft, uint32_t p, uint32_t L,
+                                               bool want) {
+  if (p >= L) return L;
+  const uint32_t w = p >> 5;
+  uint32_t m = want ? sb[w] : ~sb[w];
+  m &= (~0u) << (p & 31u);
+  if (32 * w + 32 > L) m &= (L - 32 * w >= 32) ? 0xFFFFFFFFu : ((1u << (L - 32 * w)) - 1u);
+  if (m) return 32 * w + (uint32_t)(__ffs(m) - 1);
+  return ft[w + 1];
+}
+
+// The tile's descent bits: thread t builds word t (positions T0+32t ..
+// T0+32t+31) from its keys and the key before them; the peek bit at T0+RT
+// (first bit of word RT_WORDS) comes from thread 0.  128-bit loads when the
+// whole word lies inside [0, n).
+template <int KT>
+__device__ __forceinline__ void build_tile_bits(const typename KeyTraits<KT>::K* __restrict__ keys, uint32_t n,
+                                                uint32_t T0, uint32_t* sb, uint32_t* __restrict__ gout) {
+  using T = KeyTraits<KT>;
+  using K = typename T::K;
+  const uint32_t t = threadIdx.x;  // blockDim.x == RT_WORDS
+  const uint32_t p0 = T0 + 32u * t;
+  uint32_t word = 0;
+  if (p0 + 32 <= n) {
+    K k[32];
+    const uint4* src = reinterpret_cast<const uint4*>(keys + p0);
+    constexpr int PER = 16 / sizeof(K);
+#pragma unroll
+    for (int q = 0; q < 32 / PER; ++q) {
+      uint4 v = __ldg(src + q);
+      const K* e = reinterpret_cast<const K*>(&v);
+#pragma unroll
+      for (int r = 0; r < PER; ++r) k[q * PER + r] = e[r];
+    }
+    const K prev = p0 >= 1 ? keys[p0 - 1] : k[0];
+    word = (p0 >= 1 && T::ord(k[0]) < T::ord(prev)) ? 1u : 0u;
+#pragma unroll
+    for (int l = 1; l < 32; ++l) word |= (T::ord(k[l]) < T::ord(k[l - 1]) ? 1u : 0u) << l;
+  } else {
+    for (uint32_t l = 0; l < 32; ++l) {
+      const uint32_t p = p0 + l;
+      if (p >= 1 && p < n && T::ord(keys[p]) < T::ord(keys[p - 1])) word |= 1u << l;
+    }
+  }
+  sb[t] = word;
+  if (p0 < n) gout[t] = word;
+  if (t == 0) {
+    const uint32_t p = T0 + RT;
+    sb[RT_WORDS] = (p < n && T::ord(keys[p]) < T::ord(keys[p - 1])) ? 1u : 0u;
+    sb[RT_WORDS + 1] = 0;
+  }
+}
+
+constexpr uint16_t NX_EXIT = 0x8000;  // nxt[x] >= NX_EXIT: exit state (low 8 bits)
+
+// nxt[x]: where the run starting at x hands over (an in-tile position, or
+// NX_EXIT | exit state).  ExtractRun, P:399 / P:756, reading R3.
+__device__ __forceinline__ void tile_successors(const uint32_t* sb, const uint16_t* fs, const uint16_t* fc,
+                                                uint32_t T0, uint32_t L, uint32_t n, uint32_t minrun,
+                                                uint16_t* nxt) {
+  const bool last_tile = T0 + L >= n;
+  // successor of a run starting at x (ExtractRun, P:399 / P:756, reading R3)
+  for (uint32_t x = threadIdx.x; x < L; x += blockDim.x) {
+    uint16_t v;
+    if (T0 + x + 1 >= n) {
+      v = NX_EXIT | ST_END;
+    } else {
+      const bool desc = get_bit(sb, x + 1);
+      const uint32_t nat = desc ? tile_first(sb, fc, x + 2, L, false) : tile_first(sb, fs, x + 1, L, true);
+      if (nat >= L) {
+        if (last_tile) v = NX_EXIT | ST_END;
+        else {
+          const uint32_t f = (x + minrun > L) ? x + minrun - L : 0u;
+          v = NX_EXIT | (desc ? st_desc(f, minrun) : st_asc(f, minrun));
+        }
+      } else {
+        const uint32_t e = max(nat, x + minrun);
+        if (T0 + e >= n) v = NX_EXIT | ST_END;
+        else if (e >= L) v = NX_EXIT | st_start(e - L);
+        else v = (uint16_t)e;
+      }
+    }
+    nxt[x] = v;
+  }
+}
+
+// K1+K2: descent bitmap (warp ballots), the successor of every potential run
+// start of the tile, and the tile's transfer table (walks = pointer chasing).
 template <int KT>
 __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT>::K* __restrict__ keys,
                                                      uint32_t n, uint32_t minrun, uint32_t ns,
@@ -135,27 +267,23 @@ __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT
                                                      uint32_t* __restrict__ tab) {
   using T = KeyTraits<KT>;
   __shared__ uint32_t sb[RT_WORDS + 2];
+  __shared__ uint16_t fs[RT_WORDS + 2], fc[RT_WORDS + 2];
+  __shared__ uint16_t nxt[RT];
   __shared__ uint32_t wres[MAX_MINRUN + 2];
+  static_assert(RT_WORDS == 128, "one thread per bitmap word");
   const uint32_t tile = blockIdx.x;
   const uint32_t T0 = tile * RT;
   const uint32_t L = min((uint32_t)RT, n - T0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int w = warp; w <= RT_WORDS; w += 4) {
-    uint32_t p = T0 + (uint32_t)w * 32u + (uint32_t)lane;
-    bool b = false;
-    if (p >= 1 && p < n) b = T::ord(keys[p]) < T::ord(keys[p - 1]);
-    uint32_t word = __ballot_sync(0xFFFFFFFFu, b);
-    if (lane == 0) {
-      sb[w] = word;
-      if (w < RT_WORDS && T0 + (uint32_t)w * 32u < n) bits_out[tile * RT_WORDS + w] = word;
-    }
-  }
+  build_tile_bits<KT>(keys, n, T0, sb, bits_out + (size_t)tile * RT_WORDS);
   if (threadIdx.x == 0) sb[RT_WORDS + 1] = 0;
   __syncthreads();
+  if (warp == 0) tile_suffix_tables(sb, L, fs, fc, lane);
+  __syncthreads();
+  tile_successors(sb, fs, fc, T0, L, n, minrun, nxt);
+  __syncthreads();
+  const uint32_t d_asc = fs[0], d_desc = fc[0];
   TileCtx c{sb, T0, L, n, minrun};
-  // walks from START(o) (o < minrun) and from the first set / clear bit
-  uint32_t d_asc = find_bit(sb, 0, L, true);
-  uint32_t d_desc = find_bit(sb, 0, L, false);
   for (uint32_t w = threadIdx.x; w < minrun + 2; w += blockDim.x) {
     uint32_t x = w < minrun ? w : (w == minrun ? d_asc : d_desc);
     uint32_t res;
@@ -163,8 +291,14 @@ __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT
       res = ST_END << 24;  // unused / not reachable
     } else {
       uint32_t cnt = 0;
-      uint32_t st = tile_walk<false>(c, x, &cnt, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
-      res = (st << 24) | cnt;
+      uint16_t v;
+      for (;;) {
+        ++cnt;
+        v = nxt[x];
+        if (v >= NX_EXIT) break;
+        x = v;
+      }
+      res = ((uint32_t)(v & 0xFFu) << 24) | cnt;
     }
     wres[w] = res;
   }
@@ -261,46 +395,111 @@ __global__ void __launch_bounds__(256) k_chain_expand(const In* __restrict__ in,
   }
 }
 
-// K4: re-walk each tile from its entry state and emit run starts and kinds.
-__global__ void __launch_bounds__(32) k_runs_emit(const uint32_t* __restrict__ gbits, uint32_t n,
-                                                  uint32_t minrun,
-                                                  const uint64_t* __restrict__ entry,
-                                                  uint32_t* __restrict__ run_start,
-                                                  uint8_t* __restrict__ run_kind,
-                                                  uint32_t* __restrict__ scalars) {
-  __shared__ uint32_t sb[RT_WORDS + 2];
+// K4: re-walk each tile from its entry state (pointer chasing over nxt),
+// mark the run starts, then emit starts and kinds in parallel.
+__global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ gbits, uint32_t n,
+                                                   uint32_t minrun,
+                                                   const uint64_t* __restrict__ entry,
+                                                   uint32_t* __restrict__ run_start,
+                                                   uint8_t* __restrict__ run_kind,
+                                                   uint32_t* __restrict__ scalars) {
+  __shared__ uint32_t sb[RT_WORDS + 4];
+  __shared__ uint16_t fs[RT_WORDS + 2], fc[RT_WORDS + 2];
+  __shared__ uint32_t startb[RT_WORDS];
+  __shared__ uint32_t wsum[4];
+  __shared__ uint32_t s_idx0, s_total, s_rev;
   const uint32_t tile = blockIdx.x;
   const uint32_t T0 = tile * RT;
   const uint32_t L = min((uint32_t)RT, n - T0);
   const uint32_t nwords = (n + 31) / 32;
-  for (uint32_t w = threadIdx.x; w < RT_WORDS + 2; w += blockDim.x) {
-    uint32_t gw = tile * RT_WORDS + w;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t w = threadIdx.x; w < RT_WORDS + 4; w += blockDim.x) {
+    const uint32_t gw = tile * RT_WORDS + w;
     sb[w] = gw < nwords ? gbits[gw] : 0u;
   }
-  __syncwarp();
-  if (threadIdx.x != 0) return;
-  TileCtx c{sb, T0, L, n, minrun};
-  uint64_t e = entry[tile];
-  uint32_t st = (uint32_t)(e >> 32), idx = (uint32_t)e;
-  uint32_t d_asc = find_bit(sb, 0, L, true);
-  uint32_t d_desc = find_bit(sb, 0, L, false);
-  uint32_t x, out, rev_open;
-  uint32_t n_rev = 0, n_ext = 0;
-  bool ended = false;
-  if (resolve_entry(c, st, d_asc, d_desc, &x, &out, &rev_open)) {
-    n_rev += rev_open;
-    uint32_t cnt = 0;
-    out = tile_walk<true>(c, x, &cnt, run_start, run_kind, gbits, &idx, &n_rev, &n_ext);
-    ended = out == ST_END;
-  } else {
-    n_rev += rev_open;
-    ended = (st != ST_END) && out == ST_END;
+  if (threadIdx.x < RT_WORDS) startb[threadIdx.x] = 0u;
+  __syncthreads();
+  if (warp == 0) tile_suffix_tables(sb, L, fs, fc, lane);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    TileCtx c{sb, T0, L, n, minrun};
+    const uint64_t e = entry[tile];
+    const uint32_t st = (uint32_t)(e >> 32);
+    uint32_t x, out, rev_open, cnt = 0;
+    bool ended;
+    if (resolve_entry(c, st, fs[0], fc[0], &x, &out, &rev_open)) {
+      // walk the chain with O(1) bit searches (ExtractRun, P:399 / P:756, R3)
+      const bool last_tile = T0 + L >= n;
+      ended = false;
+      for (;;) {
+        startb[x >> 5] |= 1u << (x & 31u);
+        ++cnt;
+        if (T0 + x + 1 >= n) { ended = true; break; }
+        const bool desc = get_bit(sb, x + 1);
+        const uint32_t nat = desc ? tile_first(sb, fc, x + 2, L, false) : tile_first(sb, fs, x + 1, L, true);
+        if (nat >= L) { ended = last_tile; break; }
+        const uint32_t e = max(nat, x + minrun);
+        if (T0 + e >= n) { ended = true; break; }
+        if (e >= L) break;
+        x = e;
+      }
+    } else {
+      ended = (st != ST_END) && out == ST_END;
+    }
+    s_idx0 = (uint32_t)e;
+    s_total = cnt;
+    s_rev = rev_open;
+    if (ended) {
+      scalars[SC_RUNS] = (uint32_t)e + cnt;
+      run_start[(uint32_t)e + cnt] = n;  // sentinel s_r = n
+    }
   }
-  if (n_rev) atomicAdd(&scalars[SC_REVERSED], n_rev);
-  if (n_ext) atomicAdd(&scalars[SC_EXTENDED], n_ext);
-  if (ended) {
-    scalars[SC_RUNS] = idx;
-    run_start[idx] = n;  // sentinel s_r = n
+  __syncthreads();
+  // exclusive scan of the per-word start counts (thread t = word t)
+  const uint32_t t = threadIdx.x;
+  const uint32_t bits = startb[t];
+  const uint32_t c = (uint32_t)__popc(bits);
+  uint32_t incl = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  uint32_t off = incl - c;
+  for (int q = 0; q < warp; ++q) off += wsum[q];
+  uint32_t idx = s_idx0 + off;
+  uint32_t n_rev = 0, n_ext = 0;
+  for (uint32_t m = bits; m; m &= m - 1) {
+    const uint32_t x = 32 * t + (uint32_t)(__ffs(m) - 1);
+    const uint32_t gx = T0 + x;
+    const bool last = gx + 1 >= n;
+    const bool desc = !last && get_bit(sb, x + 1);
+    bool ext;
+    if (gx + minrun > n) {
+      ext = true;
+    } else {  // a breaking bit inside [from, x + minrun) (at most 64 bits past the tile)
+      const uint32_t from = desc ? x + 2 : x + 1;
+      const uint32_t lim = x + minrun;
+      ext = from < lim && find_bit(sb, from, lim, !desc) < lim;
+    }
+    if (desc) {
+      const uint32_t nat = tile_first(sb, fc, x + 2, L, false);
+      n_rev += (nat < L ? nat : L) - x;  // the part in later tiles is counted there
+    }
+    run_start[idx] = gx;
+    run_kind[idx] = (uint8_t)((desc ? VMPS_RUN_DESC : 0u) | (ext ? VMPS_RUN_EXT : 0u));
+    ++idx;
+    if (ext) ++n_ext;
+  }
+  if (t == 0) n_rev += s_rev;
+  for (int o = 16; o; o >>= 1) {
+    n_rev += __shfl_xor_sync(0xFFFFFFFFu, n_rev, o);
+    n_ext += __shfl_xor_sync(0xFFFFFFFFu, n_ext, o);
+  }
+  if (lane == 0) {
+    if (n_rev) atomicAdd(&scalars[SC_REVERSED], n_rev);
+    if (n_ext) atomicAdd(&scalars[SC_EXTENDED], n_ext);
   }
 }
 
