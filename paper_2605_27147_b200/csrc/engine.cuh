@@ -174,7 +174,9 @@ __global__ void __launch_bounds__(LEAF_THREADS, 3) k_leaf_sort(
           else h = mid;
         }
         uint32_t ia = lo + l, ib = m + d - l;  // absolute positions
-        K ka = sk[ia], kb = sk[ib];           // may read one past a side: in bounds, unused
+        // heads and one-ahead prefetches of both sides (reads past a side stay
+        // inside the buffer and are never used)
+        K ka = sk[ia], kb = sk[ib], ka2 = sk[ia + 1], kb2 = sk[ib + 1];
 #pragma unroll
         for (int s2 = 0; s2 < LEAF_K; ++s2) {
           const bool p = ib >= hi || (ia < m && T::ord(ka) <= T::ord(kb));
@@ -182,9 +184,11 @@ __global__ void __launch_bounds__(LEAF_THREADS, 3) k_leaf_sort(
           ri[s2] = p ? ia : ib;
           ia += p ? 1u : 0u;
           ib += p ? 0u : 1u;
-          const K nx = sk[p ? ia : ib];
-          ka = p ? nx : ka;
-          kb = p ? kb : nx;
+          const K nx = sk[(p ? ia : ib) + 1];
+          ka = p ? ka2 : ka;
+          kb = p ? kb : kb2;
+          ka2 = p ? nx : ka2;
+          kb2 = p ? kb2 : nx;
         }
 #pragma unroll
         for (int s2 = 0; s2 < LEAF_K; ++s2) {
