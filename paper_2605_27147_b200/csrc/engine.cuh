@@ -403,14 +403,16 @@ __global__ void __launch_bounds__(256) k_tile_desc(
   }
 }
 
+constexpr uint32_t MERGE_STAGES = 2;  // tiles in flight per CTA = MERGE_STAGES - 1
+
 template <int KT, bool HV>
 struct MergeSmem {
   using K = typename KeyTraits<KT>::K;
   static constexpr uint32_t KB = DEFAULT_TOUT * sizeof(K) + 64;
   static constexpr uint32_t VB = HV ? DEFAULT_TOUT * 4 + 64 : 0;
   static constexpr uint32_t STAGE = KB + VB;
-  static constexpr uint32_t HDR = 256;  // 2 mbarriers at 0, 2 MergeHdr (48 B) at 64..160
-  static constexpr uint32_t BYTES = HDR + 2 * STAGE;
+  static constexpr uint32_t HDR = 256;  // mbarriers at 0, MergeHdr (48 B) per stage at 64
+  static constexpr uint32_t BYTES = HDR + MERGE_STAGES * STAGE;
 };
 
 struct MergeHdr {
@@ -418,18 +420,16 @@ struct MergeHdr {
   uint32_t va_base, vb_base, lo, hi;  // value element offsets, output range
   uint32_t par, pad[3];
 };
-static_assert(64 + 2 * sizeof(MergeHdr) <= 256, "merge smem header area");
+static_assert(64 + MERGE_STAGES * sizeof(MergeHdr) <= 256 && MERGE_STAGES * 8 <= 64, "merge smem header area");
 
 // Thread 0: fetch tile `tau` into stage `s` with 1-D bulk copies over the
 // 16-byte-aligned superset of each window (reads never cross a page).
 template <int KT, bool HV>
-__device__ __forceinline__ void merge_issue(const TileDesc* __restrict__ desc, uint32_t tau, uint32_t s,
-                                            unsigned char* smem, uint64_t* bars, MergeHdr* hdr,
-                                            const typename KeyTraits<KT>::K* k0, const uint32_t* v0,
+__device__ __forceinline__ void merge_issue(const TileDesc& d, uint32_t s, unsigned char* smem, uint64_t* bars,
+                                            MergeHdr* hdr, const typename KeyTraits<KT>::K* k0, const uint32_t* v0,
                                             const typename KeyTraits<KT>::K* k1, const uint32_t* v1) {
   using SM = MergeSmem<KT, HV>;
   using K = typename KeyTraits<KT>::K;
-  const TileDesc d = desc[tau];
   const K* sk = d.par ? k0 : k1;
   const uint32_t* sv = d.par ? v0 : v1;
   const uint32_t nA = d.a1 - d.a0, cnt = d.hi - d.lo, nB = cnt - nA;
@@ -492,7 +492,7 @@ __device__ __forceinline__ void store_vec8<uint64_t>(uint64_t* dst, const uint64
 // One level of stable merges: persistent CTAs, double-buffered bulk copies,
 // merge-path inside the tile, 128-bit stores.
 template <int KT, bool HV>
-__global__ void __launch_bounds__(MERGE_BLOCK) k_merge_level(
+__global__ void __launch_bounds__(MERGE_BLOCK, 3) k_merge_level(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
     const TileDesc* __restrict__ desc, const uint32_t* __restrict__ level_tile, int p, uint32_t tout,
@@ -507,18 +507,30 @@ __global__ void __launch_bounds__(MERGE_BLOCK) k_merge_level(
   if (blockIdx.x >= count || count > cap) return;
   const uint32_t tid = threadIdx.x;
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (uint32_t q = 0; q < MERGE_STAGES; ++q) mbar_init(&bars[q], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == 0) merge_issue<KT, HV>(desc, blockIdx.x, 0, smem, bars, hdr, k0, v0, k1, v1);
+  // thread 0 keeps the descriptor of the next tile to issue in registers, one
+  // issue ahead, so a bulk copy never waits for its descriptor load
+  TileDesc dn;
+  if (tid == 0) {
+    for (uint32_t q = 0; q + 1 < MERGE_STAGES; ++q)
+      if (blockIdx.x + q * gridDim.x < count)
+        merge_issue<KT, HV>(desc[blockIdx.x + q * gridDim.x], q, smem, bars, hdr, k0, v0, k1, v1);
+    const uint32_t f = blockIdx.x + (MERGE_STAGES - 1) * gridDim.x;
+    if (f < count) dn = desc[f];
+  }
   uint32_t it = 0;
   for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
-    const uint32_t s = it & 1u;
-    if (tid == 0 && tau + gridDim.x < count)
-      merge_issue<KT, HV>(desc, tau + gridDim.x, s ^ 1u, smem, bars, hdr, k0, v0, k1, v1);
-    mbar_wait(&bars[s], (it >> 1) & 1u);
+    const uint32_t s = it % MERGE_STAGES;
+    // refill the stage consumed in the previous iteration (freed by its barrier)
+    const uint32_t ahead = tau + (MERGE_STAGES - 1) * gridDim.x;
+    if (tid == 0 && ahead < count) {
+      merge_issue<KT, HV>(dn, (it + MERGE_STAGES - 1) % MERGE_STAGES, smem, bars, hdr, k0, v0, k1, v1);
+      if (ahead + gridDim.x < count) dn = desc[ahead + gridDim.x];
+    }
+    mbar_wait(&bars[s], (it / MERGE_STAGES) & 1u);
     const MergeHdr h = hdr[s];
     const unsigned char* st = smem + SM::HDR + s * SM::STAGE;
     const K* A = reinterpret_cast<const K*>(st) + h.a_base;
