@@ -274,16 +274,21 @@ def main():
     roof = None
     if mm and mb:
         achieved = mb / (mm / 1000) / 1e9
-        traffic = None
+        # DRAM bytes of the same launches from ncu (profiles/, same command at
+        # the same n), per step like `achieved`; null if absent
+        traffic, traffic_src = None, None
         tp = os.path.join(ROOT, "profiles", "merge_level_traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get("bytes_per_launch")
+                tj = json.load(open(tp))
+                traffic = tj.get("bytes_per_step")
+                traffic_src = tj.get("source")
             except Exception:
                 traffic = None
         roof = {"bound": "hbm", "kernel": "k_merge_level (all level launches of a step)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src,
+                "traffic": traffic, "traffic_unit": "bytes per step (all level-merge launches)",
+                "traffic_source": traffic_src, "peak_source": peak_src,
                 "algorithmic_bytes_per_step": mb, "merge_launches_per_step": phases[-1]["merge_launches"],
                 "kernel_ms_per_step": mm}
     tree = {"bytes_2wM": 2 * w_bytes * M, "M_over_n": M / n,
