@@ -173,6 +173,11 @@ int vmps_profile_read(double* h_ms, int cap, uint64_t* h_launches, uint64_t* h_b
  * the paper's rule; otherwise 1..64 forces minrun.  Z (fused-subtree limit),
  * T_out (merge tile) and P_blk (bounded block) = 0 restore defaults. */
 void vmps_test_set_minrun(uint32_t minrun);
+/* two_level = 1: merge two tree levels per HBM pass (only
+ * even-depth nodes materialized, up to 4-way merges); 0 (default): one
+ * level per pass.  Experimental: at 2^30 the 4-way tiles average ~1K outputs
+ * and run slower than two one-level passes. */
+void vmps_test_set_mode(int two_level);
 void vmps_test_set_tiles(uint32_t fuse_z, uint32_t merge_tile, uint32_t block_elems);
 
 #ifdef __cplusplus

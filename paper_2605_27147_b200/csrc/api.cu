@@ -13,6 +13,7 @@
 
 #include "bounded.cuh"
 #include "engine.cuh"
+#include "engine4.cuh"
 #include "plan.cuh"
 #include "runs.cuh"
 #include "vmps_internal.cuh"
@@ -23,6 +24,7 @@ static uint32_t g_minrun_override = 0;
 static uint32_t g_fuse_z = 0;
 static uint32_t g_tout = 0;
 static uint32_t g_blk = 0;
+static int g_fuse2 = 0;  // two-level fused merges (opt-in, test hook vmps_test_set_mode)
 static thread_local std::string g_err;
 
 // ---- bench profiling (process-global) ----
@@ -77,6 +79,7 @@ struct Cfg {
   int hv;         // 1 with payload, 0 keys only, -1 plan only
   uint32_t minrun, fuse_z, tout;
   int64_t scratch;  // VMPS_SCRATCH_UNBOUNDED or the element cap
+  int fuse2;
   uint32_t P, F;    // bounded mode: block size, scratch blocks
 };
 
@@ -89,6 +92,7 @@ static Cfg make_cfg(uint64_t n, int kt, int hv, int64_t scratch = VMPS_SCRATCH_U
   c.fuse_z = g_fuse_z ? g_fuse_z : DEFAULT_FUSE_Z;
   c.tout = g_tout ? g_tout : DEFAULT_TOUT;
   c.scratch = scratch;
+  c.fuse2 = (scratch < 0 && hv >= 0) ? g_fuse2 : 0;
   c.P = c.F = 0;
   if (scratch >= 0 && hv >= 0) {
     // block size: a power of two <= min(Z, T_out) (nodes are then longer than
@@ -186,6 +190,22 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.scan_tmp = (uint32_t*)take(scan_tmp_words(R) * 4 + 64);
   }
   t.counters = (unsigned long long*)take(8 * 8);
+  t.fuse2 = c.fuse2;
+  if (t.fuse2) {
+    t.lchild = (uint32_t*)take(R * 4);
+    t.rchild = (uint32_t*)take(R * 4);
+    t.n4cap = (uint32_t)(n / c.fuse_z + 4);
+    t.nr4 = take((size_t)t.n4cap * sizeof(NodeRuns));
+    t.n4cnt = (uint32_t*)take((size_t)(t.n4cap + 1) * 4);
+    t.n4off = (uint32_t*)take((size_t)(t.n4cap + 1) * 4);
+    // sample stride: the default keeps a tile (<= 4 g4) inside 512 x 8 outputs;
+    // the merge-tile test hook shrinks it so small inputs get many tiles
+    t.g4 = g_tout ? std::max<uint32_t>(1, std::min<uint32_t>(G4, g_tout / 4)) : G4;
+    t.s4cap = (uint32_t)(n / t.g4 + 4 * (n / c.fuse_z) + 16);
+    t.srank = (uint32_t*)take((size_t)t.s4cap * 4);
+    t.sc4 = take((size_t)t.s4cap * 16);
+    t.tiles4 = take((size_t)t.s4cap * sizeof(TileDesc4));
+  }
   if (t.bounded) {
     t.P = c.P;
     t.F = c.F;
@@ -472,9 +492,15 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   VMPS_CK(cudaMemsetAsync(w.level_cnt, 0, (LEVEL_SLOTS + 1) * 4, s));
   VMPS_CK(cudaMemsetAsync(w.level_fill, 0, (LEVEL_SLOTS + 1) * 4, s));
   LAUNCH(k_class_nodes, g, 256, 0, s, w.run_start, w.scalars, w.counters, w.power, w.seg_l, w.seg_r, w.parent,
-         dep, w.fuse_z, w.unit_end, w.unit_par, w.level_cnt);
+         dep, w.fuse_z, w.unit_end, w.unit_par, w.level_cnt, w.fuse2);
   LAUNCH(k_class_runs, g, 256, 0, s, w.run_start, w.run_kind, w.scalars, w.power, w.seg_l, w.seg_r, dep,
-         w.fuse_z, w.rmax, w.unit_flag, w.long_flag, w.unit_end, w.unit_par, w.long_par);
+         w.fuse_z, w.rmax, w.unit_flag, w.long_flag, w.unit_end, w.unit_par, w.long_par, w.fuse2);
+  if (w.fuse2) {
+    VMPS_CK(cudaMemsetAsync(w.lchild, 0, ((size_t)w.rmax + 2) * 4, s));
+    VMPS_CK(cudaMemsetAsync(w.rchild, 0, ((size_t)w.rmax + 2) * 4, s));
+    LAUNCH(k_child_map, g, 256, 0, s, w.run_start, w.scalars, w.seg_l, w.seg_r, w.parent, w.fuse_z, w.lchild,
+           w.rchild);
+  }
   scan_u32(w.unit_flag, w.unit_idx, w.rmax + 1, w.scan_tmp, s);
   scan_u32(w.long_flag, w.long_idx, w.rmax + 1, w.scan_tmp, s);
   LAUNCH(k_compact, g, 256, 0, s, w.run_start, w.scalars, w.unit_flag, w.unit_idx, w.long_flag, w.long_idx,
@@ -483,7 +509,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   scan_u32(w.long_chunks, w.long_off, w.rmax + 1, w.scan_tmp, s);
   LAUNCH(k_level_scan, 1, 32, 0, s, w.level_cnt, w.level_start, w.scalars);
   LAUNCH(k_level_scatter, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.fuse_z,
-         w.level_start, w.level_fill, w.lnodes);
+         w.level_start, w.level_fill, w.lnodes, dep, w.fuse2);
   LAUNCH(k_level_tiles, g, 256, 0, s, w.run_start, w.scalars, w.seg_l, w.seg_r, w.lnodes, w.tout, w.rmax,
          w.ltiles_cnt);
   scan_u32(w.ltiles_cnt, w.ltiles, w.rmax + 1, w.scan_tmp, s);
@@ -522,6 +548,39 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
     g_prof_mark[3] = prof_event(s);
     return bounded_stats<HV>(w, st, s);
   }
+  if (w.fuse2) {
+    using SM4 = Merge4Smem<KT, HV>;
+    static int occ4[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+    if (!occ4[KT][HV]) {
+      VMPS_CK(cudaFuncSetAttribute(k4_merge_level<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)SM4::BYTES));
+      int occ = 0;
+      VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_merge_level<KT, HV>, MERGE_BLOCK, SM4::BYTES));
+      occ4[KT][HV] = occ > 0 ? occ : 1;
+    }
+    const unsigned gm4 = (unsigned)(nsm() * occ4[KT][HV]);
+    NodeRuns* nr = (NodeRuns*)w.nr4;
+    TileDesc4* t4 = (TileDesc4*)w.tiles4;
+    for (int p = p_hi; p >= 1; --p) {
+      int e0 = prof_event(s);
+      LAUNCH(k4_node_runs, grid_for(w.n4cap + 1), 256, 0, s, w.run_start, w.seg_l, w.seg_r, dep, w.lchild, w.rchild,
+             w.lnodes, w.level_start, p, w.n4cap, w.g4, nr, w.n4cnt);
+      scan_u32(w.n4cnt, w.n4off, w.n4cap + 1, w.scan_tmp, s);
+      LAUNCH(k4_samples<KT>, grid_for(w.s4cap), 256, 0, s, k0, k1, nr, w.n4off, w.level_start, p, w.g4, w.srank,
+             (uint4*)w.sc4);
+      LAUNCH(k4_order, grid_for(w.s4cap), 256, 0, s, nr, w.n4off, w.level_start, p, w.g4, w.srank,
+             (const uint4*)w.sc4, t4);
+      int e1 = prof_event(s);
+      LAUNCH((k4_merge_level<KT, HV>), gm4, MERGE_BLOCK, SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.n4off,
+             w.level_start, p);
+      ++g_nl_merge;
+      int e2 = prof_event(s);
+      if (g_prof && e0 >= 0 && e2 >= 0 && g_prof_nm < 128) {
+        g_prof_part[g_prof_np][0] = e0; g_prof_part[g_prof_np][1] = e1; g_prof_np++;
+        g_prof_lvl[g_prof_nm][0] = e1; g_prof_lvl[g_prof_nm][1] = e2; g_prof_nm++;
+      }
+    }
+  } else {
   using SM = MergeSmem<KT, HV>;
   static int merge_occ[3][2] = {{0, 0}, {0, 0}, {0, 0}};
   if (!merge_occ[KT][HV]) {
@@ -547,6 +606,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       g_prof_lvl[g_prof_nm][0] = e1; g_prof_lvl[g_prof_nm][1] = e2; g_prof_nm++;
     }
   }
+  }  // level-by-level merges
   LAUNCH(k_check_levels, 1, 32, 0, s, w.level_cnt, p_hi, w.scalars);
   rc = launch_check();
   if (rc != VMPS_OK) return rc;
@@ -773,6 +833,8 @@ int vmps_profile_read(double* h_ms, int cap, uint64_t* h_launches, uint64_t* h_b
   }
   return k;
 }
+
+void vmps_test_set_mode(int two_level) { g_fuse2 = two_level ? 1 : 0; }
 
 void vmps_test_set_minrun(uint32_t minrun) { g_minrun_override = minrun > MAX_MINRUN ? MAX_MINRUN : minrun; }
 

@@ -122,6 +122,14 @@ __global__ void k_jump(const uint32_t* scalars, const uint32_t* __restrict__ anc
   }
 }
 
+// Buffer of an item (node output, unit or leaf) at tree depth t: depth parity
+// for level-by-level merges; with two-level merges (only even depths
+// materialized) the item consumed by its nearest even-depth ancestor.
+__device__ __forceinline__ uint32_t item_buf(uint32_t t, int fuse2) {
+  if (!fuse2) return t & 1u;
+  return (t & 1u) ? (1u - (((t - 1u) >> 1) & 1u)) : ((t >> 1) & 1u);
+}
+
 __device__ __forceinline__ uint32_t seg_size(const uint32_t* rs, const uint32_t* seg_l,
                                              const uint32_t* seg_r, uint32_t t) {
   return rs[seg_r[t]] - rs[seg_l[t]];
@@ -134,7 +142,7 @@ __global__ void k_class_nodes(const uint32_t* __restrict__ rs, uint32_t* scalars
                               const uint32_t* __restrict__ seg_l, const uint32_t* __restrict__ seg_r,
                               const uint32_t* __restrict__ parent, const uint32_t* __restrict__ dep,
                               uint32_t fuse_z, uint32_t* __restrict__ unit_end,
-                              uint8_t* __restrict__ unit_par, uint32_t* __restrict__ level_cnt) {
+                              uint8_t* __restrict__ unit_par, uint32_t* __restrict__ level_cnt, int fuse2) {
   const uint32_t r = scalars[SC_RUNS];
   unsigned long long m = 0, fm = 0;
   uint32_t maxp = 0;
@@ -151,9 +159,9 @@ __global__ void k_class_nodes(const uint32_t* __restrict__ rs, uint32_t* scalars
       if (psize > fuse_z) {
         uint32_t u = seg_l[t];
         unit_end[u] = rs[seg_r[t]];
-        unit_par[u] = (uint8_t)(dep[t] & 1u);
+        unit_par[u] = (uint8_t)item_buf(dep[t] & 0xFFFFu, fuse2);
       }
-    } else {
+    } else if (!fuse2 || (dep[t] & 1u) == 0) {  // two-level mode: only even depths are materialized
       atomicAdd(&level_cnt[p], 1u);
     }
   }
@@ -178,7 +186,7 @@ __global__ void k_class_runs(const uint32_t* __restrict__ rs, const uint8_t* __r
                              const uint32_t* __restrict__ dep, uint32_t fuse_z, uint32_t cap,
                              uint32_t* __restrict__ unit_flag, uint32_t* __restrict__ long_flag,
                              uint32_t* __restrict__ unit_end, uint8_t* __restrict__ unit_par,
-                             uint8_t* __restrict__ long_par) {
+                             uint8_t* __restrict__ long_par, int fuse2) {
   const uint32_t r = scalars[SC_RUNS];
   for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u <= cap;
        u += gridDim.x * blockDim.x) {
@@ -198,7 +206,7 @@ __global__ void k_class_runs(const uint32_t* __restrict__ rs, const uint8_t* __r
     if (size > fuse_z) {
       long_flag[u] = 1;
       unit_flag[u] = 0;
-      long_par[u] = (uint8_t)((dleaf & 1u) | ((kind[u] & VMPS_RUN_DESC) ? 2u : 0u));
+      long_par[u] = (uint8_t)(item_buf(dleaf, fuse2) | ((kind[u] & VMPS_RUN_DESC) ? 2u : 0u));
     } else {
       long_flag[u] = 0;
       bool start = (u == 0) || seg_size(rs, seg_l, seg_r, u) > fuse_z;
@@ -207,7 +215,7 @@ __global__ void k_class_runs(const uint32_t* __restrict__ rs, const uint8_t* __r
         bool leaf_root = (pl == 0) || seg_size(rs, seg_l, seg_r, pl) > fuse_z;
         if (leaf_root) {
           unit_end[u] = rs[u + 1];
-          unit_par[u] = (uint8_t)(dleaf & 1u);
+          unit_par[u] = (uint8_t)item_buf(dleaf, fuse2);
         }
       }
     }
@@ -273,11 +281,12 @@ __global__ void k_level_scatter(const uint32_t* __restrict__ rs, const uint32_t*
                                 const uint32_t* __restrict__ seg_l,
                                 const uint32_t* __restrict__ seg_r, uint32_t fuse_z,
                                 const uint32_t* __restrict__ level_start,
-                                uint32_t* __restrict__ level_fill, uint32_t* __restrict__ lnodes) {
+                                uint32_t* __restrict__ level_fill, uint32_t* __restrict__ lnodes,
+                                const uint32_t* __restrict__ dep, int fuse2) {
   const uint32_t r = scalars[SC_RUNS];
   for (uint32_t t = 1 + blockIdx.x * blockDim.x + threadIdx.x; t < r;
        t += gridDim.x * blockDim.x) {
-    if (seg_size(rs, seg_l, seg_r, t) > fuse_z) {
+    if (seg_size(rs, seg_l, seg_r, t) > fuse_z && (!fuse2 || (dep[t] & 1u) == 0)) {
       uint32_t p = power[t];
       uint32_t pos = level_start[p] + atomicAdd(&level_fill[p], 1u);
       lnodes[pos] = t;

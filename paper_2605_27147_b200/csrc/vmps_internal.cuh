@@ -120,6 +120,11 @@ struct Work {
   uint32_t part_cap;
   uint32_t* scan_tmp;    // block sums for scans
   unsigned long long* counters;  // [0] M, [1] fused M
+  // two-level fused merges (engine4.cuh)
+  int fuse2;
+  uint32_t *lchild, *rchild, *n4cnt, *n4off, *srank;
+  void *nr4, *sc4, *tiles4;
+  uint32_t n4cap, s4cap, g4;
   // scratch-bounded mode (bounded.cuh); element scratch = F blocks of P
   int bounded;
   uint32_t P, F, NB;
