@@ -46,6 +46,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-log2", type=int, default=25)
     ap.add_argument("--ref-sample-log2", type=int, default=23)
+    ap.add_argument("--two-level", action="store_true",
+                    help="experimental: two tree levels per merge pass (vmps_test_set_mode)")
+    ap.add_argument("--leaf-radix", action="store_true",
+                    help="experimental: radix-sort leaf engine instead of the block merge sort")
+    ap.add_argument("--fuse-z", type=int, default=0, help="experimental: fused-subtree limit Z")
     ap.add_argument("--bounded-reps", type=int, default=2,
                     help="timed sorts of the scratch-bounded mode (cap 4 sqrt(n log2 n)); 0 = skip")
     return ap.parse_args()
@@ -189,6 +194,12 @@ def main():
     if not os.path.exists(vm.LIB_PATH):
         vbuild.build()
     vm.lib()
+    if args.two_level:
+        vm.test_set_mode(True)
+    if args.leaf_radix:
+        vm.test_set_leaf(True)
+    if args.fuse_z:
+        vm.test_set_tiles(args.fuse_z, 0, 0)
 
     n = 1 << args.log2n
     keys0, vals0 = W.cfg5(n=n, device=dev, rank=rank)

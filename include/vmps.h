@@ -178,6 +178,10 @@ void vmps_test_set_minrun(uint32_t minrun);
  * level per pass.  Experimental: at 2^30 the 4-way tiles average ~1K outputs
  * and run slower than two one-level passes. */
 void vmps_test_set_mode(int two_level);
+/* Test hook: leaf engine.  0 (default): block merge sort of each leaf batch
+ * in shared memory (k_leaf_sort); 1: LSD radix sort (k_leaf_radix, slower at
+ * 2^30 cfg5: 29 vs 18 ms).  Same output (a stable sort is unique). */
+void vmps_test_set_leaf(int radix);
 void vmps_test_set_tiles(uint32_t fuse_z, uint32_t merge_tile, uint32_t block_elems);
 
 #ifdef __cplusplus

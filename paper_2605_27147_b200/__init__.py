@@ -55,7 +55,8 @@ class MergeRec(ctypes.Structure):
 EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_merge_plan",
            "vmps_count_rank", "vmps_merge_runs_workspace_bytes", "vmps_merge_runs",
            "vmps_status_string", "vmps_last_error", "vmps_profile_enable", "vmps_profile_read",
-           "vmps_test_set_minrun", "vmps_test_set_tiles", "vmps_test_set_mode")
+           "vmps_test_set_minrun", "vmps_test_set_tiles", "vmps_test_set_mode",
+           "vmps_test_set_leaf")
 
 _lib = None
 
@@ -95,6 +96,8 @@ def lib() -> ctypes.CDLL:
         L.vmps_test_set_minrun.restype = None
         L.vmps_test_set_mode.argtypes = [ctypes.c_int]
         L.vmps_test_set_mode.restype = None
+        L.vmps_test_set_leaf.argtypes = [ctypes.c_int]
+        L.vmps_test_set_leaf.restype = None
         L.vmps_test_set_tiles.argtypes = [ctypes.c_uint32] * 3
         L.vmps_test_set_tiles.restype = None
         _lib = L
@@ -240,6 +243,11 @@ def test_set_minrun(m: int) -> None:
 def test_set_mode(two_level: bool = False) -> None:
     """Test hook: two-level fused merges (experimental) or one level per HBM pass (default)."""
     lib().vmps_test_set_mode(1 if two_level else 0)
+
+
+def test_set_leaf(radix: bool = False) -> None:
+    """Test hook: leaf engine = LSD radix sort (True) or block merge sort (default)."""
+    lib().vmps_test_set_leaf(1 if radix else 0)
 
 
 def test_set_tiles(fuse_z: int = 0, merge_tile: int = 0, block_elems: int = 0) -> None:

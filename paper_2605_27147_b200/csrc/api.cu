@@ -14,6 +14,7 @@
 #include "bounded.cuh"
 #include "engine.cuh"
 #include "engine4.cuh"
+#include "leaf_radix.cuh"
 #include "plan.cuh"
 #include "runs.cuh"
 #include "vmps_internal.cuh"
@@ -24,7 +25,8 @@ static uint32_t g_minrun_override = 0;
 static uint32_t g_fuse_z = 0;
 static uint32_t g_tout = 0;
 static uint32_t g_blk = 0;
-static int g_fuse2 = 0;  // two-level fused merges (opt-in, test hook vmps_test_set_mode)
+static int g_fuse2 = 0;
+static int g_leaf_radix = 0;  // test hook vmps_test_set_leaf  // two-level fused merges (opt-in, test hook vmps_test_set_mode)
 static thread_local std::string g_err;
 
 // ---- bench profiling (process-global) ----
@@ -172,7 +174,8 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.unit_idx = (uint32_t*)take(R * 4);
     t.long_idx = (uint32_t*)take(R * 4);
     t.units = (uint32_t*)take(R * 3 * 4);
-    t.batch_first = (uint32_t*)take((n / c.fuse_z + 4) * 4);
+    t.bcap = (uint32_t)(n / (LEAF_CAP - c.fuse_z + 1) + n / c.fuse_z + 2);
+    t.batch_first = (uint32_t*)take(((size_t)t.bcap + 2) * 4);
     t.longs = (uint32_t*)take(R * 4 * 4);
     t.long_chunks = (uint32_t*)take(R * 4);
     t.long_off = (uint32_t*)take(R * 4);
@@ -524,13 +527,24 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   uint32_t* v0 = vals;
   uint32_t* v1 = w.v1;
   const size_t lsm = leaf_smem_bytes<KT>(HV);
+  const size_t rsm = LeafRadixSmem<KT>::BYTES;
   if (!kernel_attrs_set[KT][HV]) {
     VMPS_CK(cudaFuncSetAttribute(k_leaf_sort<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    VMPS_CK(cudaFuncSetAttribute(k_leaf_radix<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
     kernel_attrs_set[KT][HV] = true;
   }
-  const uint32_t nbatch = (uint32_t)((w.n + w.fuse_z - 1) / w.fuse_z);
-  LAUNCH(k_batch_first, (nbatch + 256) / 256, 256, 0, s, w.units, w.scalars, w.fuse_z, nbatch, w.batch_first);
-  LAUNCH((k_leaf_sort<KT, HV>), nbatch, LEAF_THREADS, lsm, s, k0, v0, k1, v1, w.units, w.batch_first, w.fuse_z);
+  // a batch = consecutive touching units starting in one window of Zb
+  // positions; units are <= Z long, so a batch spans < Zb + Z <= LEAF_CAP
+  // elements and fills most of the CTA.  Batches <= windows + long leaves.
+  const uint32_t zb = (uint32_t)LEAF_CAP - w.fuse_z + 1;
+  const uint32_t nbatch = w.bcap;
+  LAUNCH(k_batch_flags, g, 256, 0, s, w.units, w.scalars, zb, w.rmax, w.unit_flag);
+  scan_u32(w.unit_flag, w.unit_idx, w.rmax + 1, w.scan_tmp, s);
+  LAUNCH(k_batch_first, grid_for(nbatch + 1), 256, 0, s, w.unit_flag, w.unit_idx, w.scalars, nbatch, w.batch_first);
+  if (g_leaf_radix)
+    LAUNCH((k_leaf_radix<KT, HV>), nbatch, LEAF_THREADS, rsm, s, k0, v0, k1, v1, w.units, w.batch_first);
+  else
+    LAUNCH((k_leaf_sort<KT, HV>), nbatch, LEAF_THREADS, lsm, s, k0, v0, k1, v1, w.units, w.batch_first, w.fuse_z);
   LAUNCH((k_long_leaves<KT, HV>), nsm() * 8, 256, 0, s, k0, v0, k1, v1, w.longs, w.long_off, w.scalars,
          LONG_CHUNK);
   rc = launch_check();
@@ -835,6 +849,8 @@ int vmps_profile_read(double* h_ms, int cap, uint64_t* h_launches, uint64_t* h_b
 }
 
 void vmps_test_set_mode(int two_level) { g_fuse2 = two_level ? 1 : 0; }
+
+void vmps_test_set_leaf(int radix) { g_leaf_radix = radix ? 1 : 0; }
 
 void vmps_test_set_minrun(uint32_t minrun) { g_minrun_override = minrun > MAX_MINRUN ? MAX_MINRUN : minrun; }
 

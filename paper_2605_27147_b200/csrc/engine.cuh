@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 3) k_leaf_sort(
   uint32_t* pcar = upre + LEAF_CAP / 32 + 1;   // parity of the unit open at each word's end
   uint32_t* pbits = pcar + LEAF_CAP / 32 + 1;  // parity bit at each unit start
 
-  // units with start in [b Z, (b+1) Z)
+  // units of batch b (contiguous, < Zb + Z <= LEAF_CAP elements)
   const uint32_t x0 = batch_first[blockIdx.x], x1 = batch_first[blockIdx.x + 1];
   if (x0 >= x1) return;
   const uint32_t bstart = units[3 * x0];
@@ -278,18 +278,33 @@ inline size_t leaf_smem_bytes(bool hv) {
   return 2 * LEAF_CAP * (sizeof(K) + 2) + 4 * (LEAF_CAP / 32 + 1) * 4 + 16;
 }
 
-// batch_first[b] = first unit whose start is >= b Z (one thread per batch).
-__global__ void k_batch_first(const uint32_t* __restrict__ units, const uint32_t* scalars,
-                              uint32_t fuse_z, uint32_t nbatch, uint32_t* __restrict__ batch_first) {
+// Leaf batches: consecutive units that start in the same window of Zb
+// positions and touch (no long leaf between them).  flag[x] = unit x opens a
+// batch; zero tail up to cap so the scan sees a clean array.
+__global__ void k_batch_flags(const uint32_t* __restrict__ units, const uint32_t* scalars, uint32_t zb,
+                              uint32_t cap, uint32_t* __restrict__ flag) {
   const uint32_t nunits = scalars[SC_UNITS];
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b <= nbatch; b += gridDim.x * blockDim.x) {
-    const uint64_t pos = (uint64_t)b * fuse_z;
-    uint32_t a = 0, e = nunits;
-    while (a < e) { uint32_t m = (a + e) >> 1; if ((uint64_t)units[3 * m] < pos) a = m + 1; else e = m; }
-    batch_first[b] = a;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= cap; x += gridDim.x * blockDim.x) {
+    uint32_t f = 0;
+    if (x < nunits) {
+      const uint32_t s = units[3 * x];
+      f = x == 0 || s / zb != units[3 * (x - 1)] / zb || s != units[3 * (x - 1) + 1];
+    }
+    flag[x] = f;
   }
 }
 
+// batch_first[b] = first unit of batch b; batch_first[b] = nunits for every
+// b >= the batch count up to bcap (those CTAs exit at once).
+__global__ void k_batch_first(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ idx,
+                              const uint32_t* scalars, uint32_t bcap, uint32_t* __restrict__ batch_first) {
+  const uint32_t nunits = scalars[SC_UNITS];
+  const uint32_t nb = idx[nunits];
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < nunits; x += gridDim.x * blockDim.x)
+    if (flag[x]) batch_first[idx[x]] = x;
+  for (uint32_t b = nb + blockIdx.x * blockDim.x + threadIdx.x; b <= bcap; b += gridDim.x * blockDim.x)
+    batch_first[b] = nunits;
+}
 
 // Long leaves (> Z): reverse strictly descending runs, place odd-depth leaves
 // into buffer 1.  Work is split into LONG_CHUNK pieces.

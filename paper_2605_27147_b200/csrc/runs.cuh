@@ -225,50 +225,76 @@ __device__ __forceinline__ void build_tile_bits(const typename KeyTraits<KT>::K*
   }
 }
 
-constexpr uint16_t NX_EXIT = 0x8000;  // nxt[x] >= NX_EXIT: exit state (low 8 bits)
-
-// nxt[x]: where the run starting at x hands over (an in-tile position, or
-// NX_EXIT | exit state).  ExtractRun, P:399 / P:756, reading R3.
-__device__ __forceinline__ void tile_successors(const uint32_t* sb, const uint16_t* fs, const uint16_t* fc,
-                                                uint32_t T0, uint32_t L, uint32_t n, uint32_t minrun,
-                                                uint16_t* nxt) {
-  const bool last_tile = T0 + L >= n;
-  // successor of a run starting at x (ExtractRun, P:399 / P:756, reading R3)
-  for (uint32_t x = threadIdx.x; x < L; x += blockDim.x) {
-    uint16_t v;
-    if (T0 + x + 1 >= n) {
-      v = NX_EXIT | ST_END;
-    } else {
-      const bool desc = get_bit(sb, x + 1);
-      const uint32_t nat = desc ? tile_first(sb, fc, x + 2, L, false) : tile_first(sb, fs, x + 1, L, true);
-      if (nat >= L) {
-        if (last_tile) v = NX_EXIT | ST_END;
-        else {
-          const uint32_t f = (x + minrun > L) ? x + minrun - L : 0u;
-          v = NX_EXIT | (desc ? st_desc(f, minrun) : st_asc(f, minrun));
-        }
-      } else {
-        const uint32_t e = max(nat, x + minrun);
-        if (T0 + e >= n) v = NX_EXIT | ST_END;
-        else if (e >= L) v = NX_EXIT | st_start(e - L);
-        else v = (uint16_t)e;
-      }
-    }
-    nxt[x] = v;
+// Long-run masks of one bitmap word (thread-per-word).  For a run start x
+// with x + m < L the run is "short" iff its natural end is <= x + m (the run
+// then ends at x + m, ExtractRun's minrun extension) and "long"
+// otherwise (it ends at its natural end > x + m):
+//   la bit x: ascending run from x is long  <=> no descent in [x+1, x+m]
+//   ld bit x: descending run from x is long <=> descents at all of [x+1, x+m]
+// Sliding-window AND of width m (1 <= m <= 64) over the 96 bits of words
+// w, w+1, w+2 by doubling; bits past the tile are never consulted because
+// every window used lies inside [1, L-1].
+__device__ __forceinline__ uint32_t window_and_m(unsigned __int128 b, uint32_t m) {
+  uint32_t p = 1;  // b bit i: AND of [i, i+p)
+  while (2 * p <= m) {
+    b &= b >> p;
+    p *= 2;
   }
+  b &= b >> (m - p);         // m - p < p: two overlapping windows cover [i, i+m)
+  return (uint32_t)(b >> 1);  // bit i: AND of [i+1, i+m]
+}
+__device__ __forceinline__ void long_masks(const uint32_t* sb, uint32_t w, uint32_t m, uint32_t* la,
+                                           uint32_t* ld) {
+  const unsigned __int128 b = (unsigned __int128)sb[w] | ((unsigned __int128)sb[w + 1] << 32) |
+                              ((unsigned __int128)sb[w + 2] << 64);
+  const unsigned __int128 nb = ~b & (((unsigned __int128)1 << 96) - 1);
+  ld[w] = window_and_m(b, m);
+  la[w] = window_and_m(nb, m);
 }
 
-// K1+K2: descent bitmap (warp ballots), the successor of every potential run
-// start of the tile, and the tile's transfer table (walks = pointer chasing).
+// Walk the chain from in-tile run start x (T0 + x < n) until it leaves the
+// tile; returns the exit state, counts the starts visited and, if MARK, sets
+// them in `startb`.  ExtractRun, P:399 / P:756, reading R3.
+template <bool MARK>
+__device__ __forceinline__ uint32_t tile_walk_fast(const uint32_t* sb, const uint32_t* la, const uint32_t* ld,
+                                                   const uint16_t* fs, const uint16_t* fc, uint32_t T0,
+                                                   uint32_t L, uint32_t n, uint32_t m, uint32_t x,
+                                                   uint32_t* cnt, uint32_t* startb) {
+  const bool last_tile = T0 + L >= n;
+  uint32_t c = 0;
+  uint32_t out;
+  for (;;) {
+    ++c;
+    if (MARK) startb[x >> 5] |= 1u << (x & 31u);
+    if (T0 + x + 1 >= n) { out = ST_END; break; }
+    const bool desc = get_bit(sb, x + 1);  // x + 1 <= L: peek allowed
+    if (x + m < L) {
+      if (!get_bit(desc ? ld : la, x)) { x += m; continue; }  // short run: ends at x + m
+      const uint32_t nat = tile_first(sb, desc ? fc : fs, x + m + 1, L, !desc);
+      if (nat >= L) { out = last_tile ? ST_END : (desc ? st_desc(0u, m) : st_asc(0u, m)); break; }
+      x = nat;
+      continue;
+    }
+    // the run reaches the tile's right end
+    const uint32_t nat = desc ? tile_first(sb, fc, x + 2, L, false) : tile_first(sb, fs, x + 1, L, true);
+    if (nat >= L) { out = last_tile ? ST_END : (desc ? st_desc(x + m - L, m) : st_asc(x + m - L, m)); break; }
+    out = (T0 + x + m >= n) ? ST_END : st_start(x + m - L);
+    break;
+  }
+  *cnt = c;
+  return out;
+}
+
+// K1+K2: descent bitmap, long-run masks and the tile's transfer table: one
+// walker per entry class (offsets 0..m-1, open ascending, open descending).
 template <int KT>
 __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT>::K* __restrict__ keys,
                                                      uint32_t n, uint32_t minrun, uint32_t ns,
                                                      uint32_t* __restrict__ bits_out,
                                                      uint32_t* __restrict__ tab) {
-  using T = KeyTraits<KT>;
   __shared__ uint32_t sb[RT_WORDS + 2];
+  __shared__ uint32_t la[RT_WORDS], ld[RT_WORDS];
   __shared__ uint16_t fs[RT_WORDS + 2], fc[RT_WORDS + 2];
-  __shared__ uint16_t nxt[RT];
   __shared__ uint32_t wres[MAX_MINRUN + 2];
   static_assert(RT_WORDS == 128, "one thread per bitmap word");
   const uint32_t tile = blockIdx.x;
@@ -279,8 +305,7 @@ __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT
   if (threadIdx.x == 0) sb[RT_WORDS + 1] = 0;
   __syncthreads();
   if (warp == 0) tile_suffix_tables(sb, L, fs, fc, lane);
-  __syncthreads();
-  tile_successors(sb, fs, fc, T0, L, n, minrun, nxt);
+  long_masks(sb, threadIdx.x, minrun, la, ld);
   __syncthreads();
   const uint32_t d_asc = fs[0], d_desc = fc[0];
   TileCtx c{sb, T0, L, n, minrun};
@@ -291,14 +316,8 @@ __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT
       res = ST_END << 24;  // unused / not reachable
     } else {
       uint32_t cnt = 0;
-      uint16_t v;
-      for (;;) {
-        ++cnt;
-        v = nxt[x];
-        if (v >= NX_EXIT) break;
-        x = v;
-      }
-      res = ((uint32_t)(v & 0xFFu) << 24) | cnt;
+      const uint32_t v = tile_walk_fast<false>(sb, la, ld, fs, fc, T0, L, n, minrun, x, &cnt, nullptr);
+      res = (v << 24) | cnt;
     }
     wres[w] = res;
   }
@@ -406,6 +425,7 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
   __shared__ uint32_t sb[RT_WORDS + 4];
   __shared__ uint16_t fs[RT_WORDS + 2], fc[RT_WORDS + 2];
   __shared__ uint32_t startb[RT_WORDS];
+  __shared__ uint32_t la[RT_WORDS], ld[RT_WORDS];
   __shared__ uint32_t wsum[4];
   __shared__ uint32_t s_idx0, s_total, s_rev;
   const uint32_t tile = blockIdx.x;
@@ -420,6 +440,7 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
   if (threadIdx.x < RT_WORDS) startb[threadIdx.x] = 0u;
   __syncthreads();
   if (warp == 0) tile_suffix_tables(sb, L, fs, fc, lane);
+  long_masks(sb, threadIdx.x, minrun, la, ld);
   __syncthreads();
   if (threadIdx.x == 0) {
     TileCtx c{sb, T0, L, n, minrun};
@@ -428,21 +449,7 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
     uint32_t x, out, rev_open, cnt = 0;
     bool ended;
     if (resolve_entry(c, st, fs[0], fc[0], &x, &out, &rev_open)) {
-      // walk the chain with O(1) bit searches (ExtractRun, P:399 / P:756, R3)
-      const bool last_tile = T0 + L >= n;
-      ended = false;
-      for (;;) {
-        startb[x >> 5] |= 1u << (x & 31u);
-        ++cnt;
-        if (T0 + x + 1 >= n) { ended = true; break; }
-        const bool desc = get_bit(sb, x + 1);
-        const uint32_t nat = desc ? tile_first(sb, fc, x + 2, L, false) : tile_first(sb, fs, x + 1, L, true);
-        if (nat >= L) { ended = last_tile; break; }
-        const uint32_t e = max(nat, x + minrun);
-        if (T0 + e >= n) { ended = true; break; }
-        if (e >= L) break;
-        x = e;
-      }
+      ended = tile_walk_fast<true>(sb, la, ld, fs, fc, T0, L, n, minrun, x, &cnt, startb) == ST_END;
     } else {
       ended = (st != ST_END) && out == ST_END;
     }

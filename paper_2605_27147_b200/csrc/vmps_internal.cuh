@@ -75,6 +75,7 @@ struct Work {
   uint32_t n, minrun, ns, ntiles;
   uint32_t rmax;       // capacity for runs (+2 slack)
   uint32_t fuse_z, tout;
+  uint32_t bcap;       // leaf batches (upper bound)
   int kt, has_vals;
   // element scratch (buffer 1 of the ping-pong pair)
   void* k1;

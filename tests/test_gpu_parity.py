@@ -112,14 +112,16 @@ def test_random_small_default_tiles(vm, dtype, with_vals):
         check_case(vm, keys, vals, minrun=int(rng.choice([0, 1, 2, 7, 32])))
 
 
-@pytest.mark.parametrize("two_level", [True, False])
+@pytest.mark.parametrize("two_level,leaf_radix", [(True, False), (False, False), (False, True)])
 @pytest.mark.parametrize("dtype", [np.uint32, np.uint64, np.float32])
-def test_random_small_tiny_tiles(vm, dtype, two_level):
+def test_random_small_tiny_tiles(vm, dtype, two_level, leaf_radix):
     """Z = 64 and 16-element merge tiles (two-level sample stride 4): small
-    inputs cross every level path; both merge schedules."""
+    inputs cross every level path; both merge schedules and both leaf engines
+    (a leaf batch then holds ~70 units and spans long leaves' gaps)."""
     rng = np.random.default_rng(200 + (dtype == np.uint64) + 2 * (dtype == np.float32))
     try:
         vm.test_set_mode(two_level)
+        vm.test_set_leaf(leaf_radix)
         vm.test_set_tiles(64, 16, 0)
         for trial in range(40):
             n = int(rng.integers(2, 6000))
@@ -129,6 +131,7 @@ def test_random_small_tiny_tiles(vm, dtype, two_level):
     finally:
         vm.test_set_tiles(0, 0, 0)
         vm.test_set_mode(False)
+        vm.test_set_leaf(False)
 
 
 def test_edge_cases(vm):
@@ -151,18 +154,20 @@ def test_edge_cases(vm):
         check_case(vm, keys, vals)
 
 
-@pytest.mark.parametrize("two_level", [True, False])
+@pytest.mark.parametrize("two_level,leaf_radix", [(True, False), (False, False), (False, True)])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
-def test_configs_reduced_size_vs_oracle(vm, cfg, two_level):
+def test_configs_reduced_size_vs_oracle(vm, cfg, two_level, leaf_radix):
     """Each BASELINE.json config shape at 2^18 (many merge levels), full oracle
-    compare, both merge schedules."""
+    compare, both merge schedules and both leaf engines."""
     vm.test_set_tiles(0, 0, 0)
     vm.test_set_mode(two_level)
+    vm.test_set_leaf(leaf_radix)
     try:
         k, v = W.make(cfg, n=1 << 18, device="cpu")
         check_case(vm, W.to_numpy(k), None if v is None else W.to_numpy(v))
     finally:
         vm.test_set_mode(False)
+        vm.test_set_leaf(False)
 
 
 def _ord_image(k: torch.Tensor) -> torch.Tensor:
