@@ -118,6 +118,26 @@ vmps_status_t vmps_sort_pairs(void* keys, uint32_t* vals, uint64_t n, vmps_key_t
                               int64_t scratch_elems, void* ws, size_t ws_bytes, void* stream,
                               vmps_stats_t* h_stats);
 
+/* Host-buffer entry points (end-to-end path): h_keys[0,n) (and h_vals) live
+ * in host memory (pinned for asynchronous copies; pageable works but the
+ * copies then block the calling thread).  Enqueued on `stream`: copy to the
+ * caller's device buffers d_keys / d_vals (n elements each, 16-byte
+ * aligned), the device sort exactly as vmps_sort_keys / vmps_sort_pairs, and
+ * the copy of the sorted result to h_keys_out / h_vals_out (host; NULL =
+ * in place into h_keys / h_vals).  Returns after enqueueing (h_stats != NULL
+ * synchronises and fills only h_stats->n); the host output holds the result
+ * once `stream` completes.  Calls on different streams with their own device
+ * buffers and workspaces overlap one batch's copies with another's sort.
+ * Errors as vmps_sort_*, validated before anything is enqueued; NULL input
+ * or device pointers with n > 1 are VMPS_ERR_INVALID_ARG. */
+vmps_status_t vmps_sort_keys_host(const void* h_keys, void* h_keys_out, uint64_t n, vmps_key_t kt,
+                                  int64_t scratch_elems, void* d_keys, void* ws, size_t ws_bytes,
+                                  void* stream, vmps_stats_t* h_stats);
+vmps_status_t vmps_sort_pairs_host(const void* h_keys, const uint32_t* h_vals, void* h_keys_out,
+                                   uint32_t* h_vals_out, uint64_t n, vmps_key_t kt, int64_t scratch_elems,
+                                   void* d_keys, uint32_t* d_vals, void* ws, size_t ws_bytes, void* stream,
+                                   vmps_stats_t* h_stats);
+
 /* The merge plan of Alg. 1 for keys[0,n) (keys are only read):
  * run_start[r] (ascending, run_start[0] = 0), run_kind[r] (VMPS_RUN_* bits),
  * merges[r-1] in Alg. 1's execution order.  cap_runs = capacity of

@@ -56,7 +56,7 @@ EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_me
            "vmps_count_rank", "vmps_merge_runs_workspace_bytes", "vmps_merge_runs",
            "vmps_status_string", "vmps_last_error", "vmps_profile_enable", "vmps_profile_read",
            "vmps_test_set_minrun", "vmps_test_set_tiles", "vmps_test_set_mode",
-           "vmps_test_set_leaf")
+           "vmps_test_set_leaf", "vmps_sort_keys_host", "vmps_sort_pairs_host")
 
 _lib = None
 
@@ -73,6 +73,9 @@ def lib() -> ctypes.CDLL:
         L.vmps_workspace_bytes.argtypes = [u64, ctypes.c_int, ctypes.c_int, i64, ctypes.POINTER(sz)]
         L.vmps_sort_keys.argtypes = [vp, u64, ctypes.c_int, i64, vp, sz, vp, ctypes.POINTER(Stats)]
         L.vmps_sort_pairs.argtypes = [vp, vp, u64, ctypes.c_int, i64, vp, sz, vp, ctypes.POINTER(Stats)]
+        L.vmps_sort_keys_host.argtypes = [vp, vp, u64, ctypes.c_int, i64, vp, vp, sz, vp, ctypes.POINTER(Stats)]
+        L.vmps_sort_pairs_host.argtypes = [vp, vp, vp, vp, u64, ctypes.c_int, i64, vp, vp, vp, sz, vp,
+                                           ctypes.POINTER(Stats)]
         L.vmps_merge_plan.argtypes = [vp, u64, ctypes.c_int, vp, vp, vp, u64, ctypes.POINTER(u64),
                                       vp, sz, vp]
         L.vmps_count_rank.argtypes = [vp, u64, ctypes.c_int, vp, ctypes.c_uint32, vp, vp, vp]
@@ -80,7 +83,8 @@ def lib() -> ctypes.CDLL:
                                                       ctypes.POINTER(sz)]
         L.vmps_merge_runs.argtypes = [vp, vp, u64, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
                                       ctypes.c_uint32, vp, sz, vp]
-        for f in ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_merge_plan",
+        for f in ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_sort_keys_host",
+                  "vmps_sort_pairs_host", "vmps_merge_plan",
                   "vmps_count_rank", "vmps_merge_runs_workspace_bytes", "vmps_merge_runs"):
             getattr(L, f).restype = ctypes.c_int
         L.vmps_status_string.restype = ctypes.c_char_p
@@ -180,6 +184,54 @@ def sort_(keys: torch.Tensor, values: torch.Tensor | None = None, scratch: int |
                                    buf.numel(), s, sp)
             _check(rc, "vmps_sort_pairs")
     return st.as_dict() if stats else None
+
+
+def sort_host_(keys: torch.Tensor, values: torch.Tensor | None = None, scratch: int | None = None,
+               device=None, out_keys: torch.Tensor | None = None, out_values: torch.Tensor | None = None,
+               d_keys: torch.Tensor | None = None, d_values: torch.Tensor | None = None,
+               workspace: Workspace | None = None, stream: torch.cuda.Stream | None = None) -> None:
+    """End-to-end stable sort of HOST tensors (pinned for overlap) through
+    vmps_sort_*_host: copy in, device sort, copy back into ``out_keys`` /
+    ``out_values`` (default: in place), all enqueued on ``stream`` (default:
+    the current stream of ``device``).  Device buffers are allocated unless
+    given.  Returns after enqueueing; the output holds the result once the
+    stream completes."""
+    def _host(t, name):
+        if t is None:
+            return
+        if t.is_cuda or t.dim() != 1 or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous 1-D host tensor")
+    _host(keys, "keys"); _host(values, "values"); _host(out_keys, "out_keys"); _host(out_values, "out_values")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    kt = key_type(keys)
+    n = keys.numel()
+    if values is not None and (values.numel() != n or values.dtype not in (torch.uint32, torch.int32)):
+        raise ValueError("values must be u32/int32 with the keys' length")
+    if out_keys is not None and (out_keys.numel() != n or out_keys.element_size() != keys.element_size()):
+        raise ValueError("out_keys must match keys")
+    if out_values is not None and (values is None or out_values.numel() != n or out_values.element_size() != 4):
+        raise ValueError("out_values must match values")
+    dk = d_keys if d_keys is not None else torch.empty_like(keys, device=dev)
+    dv = None
+    if values is not None:
+        dv = d_values if d_values is not None else torch.empty_like(values, device=dev)
+    sc = SCRATCH_UNBOUNDED if scratch is None else int(scratch)
+    nbytes = workspace_bytes(n, kt, 1 if values is not None else 0, sc)
+    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    buf = ws.get(nbytes, dev)
+    L = lib()
+    ko = out_keys.data_ptr() if out_keys is not None else None
+    with torch.cuda.device(dev):
+        s = stream.cuda_stream if stream is not None else _stream_ptr(dev)
+        if values is None:
+            rc = L.vmps_sort_keys_host(keys.data_ptr(), ko, n, kt, sc, dk.data_ptr(), buf.data_ptr(), buf.numel(),
+                                       s, None)
+            _check(rc, "vmps_sort_keys_host")
+        else:
+            vo = out_values.data_ptr() if out_values is not None else None
+            rc = L.vmps_sort_pairs_host(keys.data_ptr(), values.data_ptr(), ko, vo, n, kt, sc, dk.data_ptr(),
+                                        dv.data_ptr(), buf.data_ptr(), buf.numel(), s, None)
+            _check(rc, "vmps_sort_pairs_host")
 
 
 @dataclass

@@ -608,7 +608,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   TileDesc* desc = (TileDesc*)w.desc;
   for (int p = p_hi; p >= 1; --p) {
     int e0 = prof_event(s);
-    LAUNCH(k_tile_desc<KT>, (w.part_cap + 255) / 256, 256, 0, s, k0, k1, w.run_start, w.seg_l, w.seg_r, dep, w.lnodes,
+    LAUNCH(k_tile_desc<KT>, (w.part_cap / DESC_CHUNK + 256) / 256, 256, 0, s, k0, k1, w.run_start, w.seg_l, w.seg_r, dep, w.lnodes,
            w.ltiles, w.level_start, w.level_tile, p, w.tout, desc, w.part_cap, w.scalars);
     int e1 = prof_event(s);
     LAUNCH((k_merge_level<KT, HV>), gm, MERGE_BLOCK, SM::BYTES, s, k0, v0, k1, v1, desc, w.level_tile, p,
@@ -756,6 +756,68 @@ vmps_status_t vmps_sort_pairs(void* keys, uint32_t* vals, uint64_t n, vmps_key_t
     return VMPS_ERR_INVALID_ARG;
   }
   return sort_any(keys, vals, n, kt, scratch_elems, ws, ws_bytes, stream, h_stats);
+}
+
+static vmps_status_t sort_host_any(const void* h_keys, const uint32_t* h_vals, void* h_kout, uint32_t* h_vout,
+                                   uint64_t n, vmps_key_t kt, int64_t scratch_elems, void* d_keys,
+                                   uint32_t* d_vals, void* ws, size_t ws_bytes, void* stream,
+                                   vmps_stats_t* h_stats, bool pairs) {
+  if (n > 1 && (!h_keys || !d_keys || (pairs && (!h_vals || !d_vals)))) {
+    g_err = "host or device buffer is NULL";
+    return VMPS_ERR_INVALID_ARG;
+  }
+  vmps_status_t rc = check_common(d_keys, pairs ? d_vals : nullptr, n, kt);
+  if (rc != VMPS_OK) return rc;
+  if (n <= 1) {  // nothing to sort; an out-of-place call still copies the item
+    if (n == 1 && h_kout) memcpy(h_kout, h_keys, key_bytes(kt));
+    if (n == 1 && pairs && h_vout) memcpy(h_vout, h_vals, 4);
+    if (h_stats) { memset(h_stats, 0, sizeof(*h_stats)); h_stats->n = n; h_stats->runs = n; }
+    return VMPS_OK;
+  }
+  // validate the budget before anything is enqueued
+  if (scratch_elems != VMPS_SCRATCH_UNBOUNDED && scratch_elems < 0) {
+    g_err = "scratch_elems must be >= 0 or VMPS_SCRATCH_UNBOUNDED";
+    return VMPS_ERR_INVALID_ARG;
+  }
+  if (scratch_elems >= 0 && make_cfg(n, kt, pairs ? 1 : 0, scratch_elems).F < BD_MIN_BLOCKS) {
+    g_err = "scratch_elems below the bounded mode's minimum (6 blocks)";
+    return VMPS_ERR_BUDGET;
+  }
+  size_t need = 0;
+  vmps_workspace_bytes(n, kt, pairs ? 1 : 0, scratch_elems, &need);
+  if (!ws || ws_bytes < need) { g_err = "workspace too small"; return VMPS_ERR_BUDGET; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t kb = (size_t)n * key_bytes(kt), vb = (size_t)n * 4;
+  VMPS_CK(cudaMemcpyAsync(d_keys, h_keys, kb, cudaMemcpyHostToDevice, s));
+  if (pairs) VMPS_CK(cudaMemcpyAsync(d_vals, h_vals, vb, cudaMemcpyHostToDevice, s));
+  // stats (if requested) synchronise inside the sort; read-back follows
+  rc = sort_any(d_keys, pairs ? d_vals : nullptr, n, kt, scratch_elems, ws, ws_bytes, stream, nullptr);
+  if (rc != VMPS_OK) return rc;
+  void* ko = h_kout ? h_kout : const_cast<void*>(h_keys);
+  uint32_t* vo = h_vout ? h_vout : const_cast<uint32_t*>(h_vals);
+  VMPS_CK(cudaMemcpyAsync(ko, d_keys, kb, cudaMemcpyDeviceToHost, s));
+  if (pairs) VMPS_CK(cudaMemcpyAsync(vo, d_vals, vb, cudaMemcpyDeviceToHost, s));
+  if (h_stats) {
+    VMPS_CK(cudaStreamSynchronize(s));
+    memset(h_stats, 0, sizeof(*h_stats));
+    h_stats->n = n;
+  }
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_sort_keys_host(const void* h_keys, void* h_keys_out, uint64_t n, vmps_key_t kt,
+                                  int64_t scratch_elems, void* d_keys, void* ws, size_t ws_bytes, void* stream,
+                                  vmps_stats_t* h_stats) {
+  return sort_host_any(h_keys, nullptr, h_keys_out, nullptr, n, kt, scratch_elems, d_keys, nullptr, ws, ws_bytes,
+                       stream, h_stats, false);
+}
+
+vmps_status_t vmps_sort_pairs_host(const void* h_keys, const uint32_t* h_vals, void* h_keys_out,
+                                   uint32_t* h_vals_out, uint64_t n, vmps_key_t kt, int64_t scratch_elems,
+                                   void* d_keys, uint32_t* d_vals, void* ws, size_t ws_bytes, void* stream,
+                                   vmps_stats_t* h_stats) {
+  return sort_host_any(h_keys, h_vals, h_keys_out, h_vals_out, n, kt, scratch_elems, d_keys, d_vals, ws, ws_bytes,
+                       stream, h_stats, true);
 }
 
 vmps_status_t vmps_merge_plan(const void* keys, uint64_t n, vmps_key_t kt, uint64_t* run_start,

@@ -384,8 +384,26 @@ __device__ __forceinline__ uint32_t warp_corank(const typename KeyTraits<KT>::K*
   return lo + (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, pr));
 }
 
-// Tile descriptors of one level (one thread per tile: many independent
-// binary searches in flight hide the global-memory latency).
+// Bounded merge-path co-rank: the answer is known to lie in [lb, ub].
+template <int KT>
+__device__ __forceinline__ uint32_t corank_in(const typename KeyTraits<KT>::K* A, uint32_t nA,
+                                              const typename KeyTraits<KT>::K* B, uint32_t nB,
+                                              uint32_t d, uint32_t lb, uint32_t ub) {
+  using T = KeyTraits<KT>;
+  uint32_t lo = max(d > nB ? d - nB : 0u, lb), hi = min(min(d, nA), ub);
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (T::ord(A[mid]) <= T::ord(B[d - mid - 1])) lo = mid + 1;  // A[mid] precedes B[d-mid-1]
+    else hi = mid;
+  }
+  return lo;
+}
+
+// Tile descriptors of one level.  A thread handles DESC_CHUNK consecutive
+// tiles: the first co-rank is a full binary search, each next tile of the
+// same node searches only [a0, a0 + T] (co-ranks are monotone and grow by at
+// most the diagonal step), so most probes stay inside a few DRAM lines.
+constexpr uint32_t DESC_CHUNK = 4;
 template <int KT>
 __global__ void __launch_bounds__(256) k_tile_desc(
     const typename KeyTraits<KT>::K* __restrict__ k0, const typename KeyTraits<KT>::K* __restrict__ k1,
@@ -400,21 +418,31 @@ __global__ void __launch_bounds__(256) k_tile_desc(
     if (blockIdx.x == 0 && threadIdx.x == 0) scalars[SC_ERROR] = 2;
     return;
   }
-  for (uint32_t tau = tb + blockIdx.x * blockDim.x + threadIdx.x; tau < te;
-       tau += gridDim.x * blockDim.x) {
-    uint32_t a = ls, b = le;  // last bucket x with ltiles[x] <= tau
-    while (b - a > 1) { uint32_t m = (a + b) >> 1; if (ltiles[m] <= tau) a = m; else b = m; }
-    const uint32_t t = lnodes[a];
-    const uint32_t i = rs[seg_l[t]], j = rs[t], k = rs[seg_r[t]];
-    const uint32_t par = dep[t] & 1u;
-    const uint32_t g = i / tout + (tau - ltiles[a]);
-    const uint32_t lo = max(i, g * tout), hi = min(k, (g + 1) * tout);
-    const auto* src = par ? k0 : k1;
-    const uint32_t a0 = corank<KT>(src + i, j - i, src + j, k - j, lo - i);
-    TileDesc* D = desc + (tau - tb);
-    D->i = i; D->j = j; D->k = k; D->lo = lo; D->hi = hi; D->a0 = a0; D->par = par;
-    if (hi == k) D->a1 = j - i;
-    if (lo != i) desc[tau - tb - 1].a1 = a0;
+  const uint32_t nchunks = (te - tb + DESC_CHUNK - 1) / DESC_CHUNK;
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += gridDim.x * blockDim.x) {
+    const uint32_t tau0 = tb + c * DESC_CHUNK;
+    uint32_t a = ls, b = le;  // last bucket x with ltiles[x] <= tau0
+    while (b - a > 1) { uint32_t m = (a + b) >> 1; if (ltiles[m] <= tau0) a = m; else b = m; }
+    uint32_t cur_node = 0xFFFFFFFFu, prev_a0 = 0, prev_lo = 0;
+    for (uint32_t q = 0; q < DESC_CHUNK; ++q) {
+      const uint32_t tau = tau0 + q;
+      if (tau >= te) break;
+      while (a + 1 < le && ltiles[a + 1] <= tau) ++a;
+      const uint32_t t = lnodes[a];
+      const uint32_t i = rs[seg_l[t]], j = rs[t], k = rs[seg_r[t]];
+      const uint32_t par = dep[t] & 1u;
+      const uint32_t g = i / tout + (tau - ltiles[a]);
+      const uint32_t lo = max(i, g * tout), hi = min(k, (g + 1) * tout);
+      const auto* src = par ? k0 : k1;
+      uint32_t lb = 0, ub = 0xFFFFFFFFu;
+      if (cur_node == a) { lb = prev_a0; ub = prev_a0 + (lo - prev_lo); }
+      const uint32_t a0 = corank_in<KT>(src + i, j - i, src + j, k - j, lo - i, lb, ub);
+      cur_node = a; prev_a0 = a0; prev_lo = lo;
+      TileDesc* D = desc + (tau - tb);
+      D->i = i; D->j = j; D->k = k; D->lo = lo; D->hi = hi; D->a0 = a0; D->par = par;
+      if (hi == k) D->a1 = j - i;
+      if (lo != i) desc[tau - tb - 1].a1 = a0;
+    }
   }
 }
 

@@ -252,3 +252,30 @@ def test_workspace_and_errors(vm):
     assert rc == 1  # misaligned
     rc = L.vmps_sort_keys(k.data_ptr(), 1000, 9, -1, ws.data_ptr(), 16, None, None)
     assert rc == 1  # bad key type
+
+
+@pytest.mark.parametrize("dtype", [np.uint32, np.uint64, np.float32])
+def test_host_entry_points(vm, dtype):
+    """vmps_sort_*_host: host in -> device sort -> host out (in place and out of
+    place, keys only and pairs), exact vs the oracle."""
+    vm.test_set_tiles(0, 0, 0)
+    vm.test_set_minrun(0)
+    rng = np.random.default_rng(500 + (dtype == np.uint64) + 2 * (dtype == np.float32))
+    for n in (1, 2, 5000, 70001):
+        keys = _structured(rng, n, dtype)
+        vals = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+        ko, vo, _, _ = oracle.sort(keys, vals, variant=oracle.VARIANT_A)
+        kk, _, _, _ = oracle.sort(keys, None, variant=oracle.VARIANT_A)
+        hk = W.from_numpy(keys, "cpu").pin_memory()
+        hv = W.from_numpy(vals, "cpu").pin_memory()
+        outk, outv = torch.empty_like(hk).pin_memory(), torch.empty_like(hv).pin_memory()
+        s = torch.cuda.Stream()
+        vm.sort_host_(hk, hv, out_keys=outk, out_values=outv, stream=s)   # out of place
+        s.synchronize()
+        assert W.to_numpy(outk).view(np.uint8).tobytes() == ko.view(np.uint8).tobytes()
+        assert (W.to_numpy(outv) == vo).all()
+        assert W.to_numpy(hk).view(np.uint8).tobytes() == keys.view(np.uint8).tobytes()  # input untouched
+        hk2 = W.from_numpy(keys, "cpu").pin_memory()
+        vm.sort_host_(hk2)                                                 # keys only, in place
+        torch.cuda.synchronize()
+        assert W.to_numpy(hk2).view(np.uint8).tobytes() == kk.view(np.uint8).tobytes()
