@@ -199,15 +199,7 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.rchild = (uint32_t*)take(R * 4);
     t.n4cap = (uint32_t)(n / c.fuse_z + 4);
     t.nr4 = take((size_t)t.n4cap * sizeof(NodeRuns));
-    t.n4cnt = (uint32_t*)take((size_t)(t.n4cap + 1) * 4);
-    t.n4off = (uint32_t*)take((size_t)(t.n4cap + 1) * 4);
-    // sample stride: the default keeps a tile (<= 4 g4) inside 512 x 8 outputs;
-    // the merge-tile test hook shrinks it so small inputs get many tiles
-    t.g4 = g_tout ? std::max<uint32_t>(1, std::min<uint32_t>(G4, g_tout / 4)) : G4;
-    t.s4cap = (uint32_t)(n / t.g4 + 4 * (n / c.fuse_z) + 16);
-    t.srank = (uint32_t*)take((size_t)t.s4cap * 4);
-    t.sc4 = take((size_t)t.s4cap * 16);
-    t.tiles4 = take((size_t)t.s4cap * sizeof(TileDesc4));
+    t.tiles4 = take((size_t)t.part_cap * sizeof(TileDesc4));
   }
   if (t.bounded) {
     t.P = c.P;
@@ -569,7 +561,8 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       VMPS_CK(cudaFuncSetAttribute(k4_merge_level<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)SM4::BYTES));
       int occ = 0;
-      VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_merge_level<KT, HV>, MERGE_BLOCK, SM4::BYTES));
+      VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_merge_level<KT, HV>, MERGE_BLOCK + 32,
+                                                            SM4::BYTES));
       occ4[KT][HV] = occ > 0 ? occ : 1;
     }
     const unsigned gm4 = (unsigned)(nsm() * occ4[KT][HV]);
@@ -577,16 +570,12 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
     TileDesc4* t4 = (TileDesc4*)w.tiles4;
     for (int p = p_hi; p >= 1; --p) {
       int e0 = prof_event(s);
-      LAUNCH(k4_node_runs, grid_for(w.n4cap + 1), 256, 0, s, w.run_start, w.seg_l, w.seg_r, dep, w.lchild, w.rchild,
-             w.lnodes, w.level_start, p, w.n4cap, w.g4, nr, w.n4cnt);
-      scan_u32(w.n4cnt, w.n4off, w.n4cap + 1, w.scan_tmp, s);
-      LAUNCH(k4_samples<KT>, grid_for(w.s4cap), 256, 0, s, k0, k1, nr, w.n4off, w.level_start, p, w.g4, w.srank,
-             (uint4*)w.sc4);
-      LAUNCH(k4_order, grid_for(w.s4cap), 256, 0, s, nr, w.n4off, w.level_start, p, w.g4, w.srank,
-             (const uint4*)w.sc4, t4);
+      LAUNCH(k4_node_runs, grid_for(w.n4cap), 256, 0, s, w.run_start, w.seg_l, w.seg_r, dep, w.lchild, w.rchild,
+             w.lnodes, w.level_start, p, nr);
+      LAUNCH(k4_desc<KT>, (w.part_cap / DESC_CHUNK + 256) / 256, 256, 0, s, k0, k1, nr, w.ltiles, w.level_start,
+             w.level_tile, p, w.tout, t4);
       int e1 = prof_event(s);
-      LAUNCH((k4_merge_level<KT, HV>), gm4, MERGE_BLOCK, SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.n4off,
-             w.level_start, p);
+      LAUNCH((k4_merge_level<KT, HV>), gm4, MERGE_BLOCK + 32, SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.level_tile, p);
       ++g_nl_merge;
       int e2 = prof_event(s);
       if (g_prof && e0 >= 0 && e2 >= 0 && g_prof_nm < 128) {

@@ -11,19 +11,14 @@
 // (t even ? t/2 : 1 + (t-1)/2) mod 2... precisely buf(t) below; every
 // materialized node then reads its inputs from one buffer and writes the other.
 //
-// Tiles come from sampling: every G4-th element of every run is a tile
-// boundary.  For a sample s of run j with key v, the number of elements of run
-// i that precede it in the stable order is upper_bound(run i, v) for i < j,
-// lower_bound(run i, v) for i > j, and its own index for i = j; their sum is
-// its output rank.  Between consecutive samples each run contributes at most
-// G4 elements, so a tile holds at most 4 G4 elements.
+// Tiles are aligned output windows of T = 4096 positions, like the one-level
+// engine; their exact 4-way splits come from a nested merge-path search
+// (corank4 below), so every interior tile merges exactly T outputs.
 #pragma once
 #include "engine.cuh"
 #include "plan.cuh"
 
 namespace vmps {
-
-constexpr uint32_t G4 = 1022;  // 4 G4 + 7 <= 4096: an 8-aligned cover fits 512 x 8 outputs
 
 __host__ __device__ __forceinline__ uint32_t buf2(uint32_t t) {
   return (t & 1u) ? (1u - (((t - 1u) >> 1) & 1u)) : ((t >> 1) & 1u);
@@ -32,8 +27,7 @@ __host__ __device__ __forceinline__ uint32_t buf2(uint32_t t) {
 struct NodeRuns {
   uint32_t b[5];  // run boundaries: W_r = [b[r], b[r+1]), b[0] = i, b[4] = k
   uint32_t par;   // output buffer
-  uint32_t soff;  // first sample (tile) of the node within the level
-  uint32_t pad;
+  uint32_t pad[2];
 };
 
 struct TileDesc4 {
@@ -41,13 +35,6 @@ struct TileDesc4 {
   uint32_t rank;  // output rank of the tile start within the node
   uint32_t c[4];  // elements of each run before the tile
 };
-
-__device__ __forceinline__ uint32_t runs_samples(const NodeRuns& R, uint32_t g4) {
-  uint32_t c = 0;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) c += (R.b[r + 1] - R.b[r] + g4 - 1) / g4;
-  return c;
-}
 
 // Children of non-fused nodes (only non-fused children are recorded).
 __global__ void k_child_map(const uint32_t* __restrict__ rs, const uint32_t* scalars,
@@ -64,128 +51,156 @@ __global__ void k_child_map(const uint32_t* __restrict__ rs, const uint32_t* sca
   }
 }
 
-// Runs and sample counts of the level's materialized nodes (zero tail to cap).
+// Runs of the level's materialized nodes.
 __global__ void k4_node_runs(const uint32_t* __restrict__ rs, const uint32_t* __restrict__ seg_l,
                              const uint32_t* __restrict__ seg_r, const uint32_t* __restrict__ dep,
                              const uint32_t* __restrict__ lchild, const uint32_t* __restrict__ rchild,
                              const uint32_t* __restrict__ lnodes, const uint32_t* __restrict__ level_start, int p,
-                             uint32_t cap, uint32_t g4, NodeRuns* __restrict__ nr, uint32_t* __restrict__ cnt) {
+                             NodeRuns* __restrict__ nr) {
   const uint32_t ls = level_start[p], m = level_start[p + 1] - ls;
-  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= cap; x += gridDim.x * blockDim.x) {
-    uint32_t c = 0;
-    if (x < m) {
-      const uint32_t t = lnodes[ls + x];
-      NodeRuns R;
-      const uint32_t i = rs[seg_l[t]], j = rs[t], k = rs[seg_r[t]];
-      const uint32_t u = lchild[t], v = rchild[t];
-      R.b[0] = i;
-      R.b[1] = u ? rs[u] : j;
-      R.b[2] = j;
-      R.b[3] = v ? rs[v] : k;
-      R.b[4] = k;
-      R.par = buf2(dep[t] & 0xFFFFu);
-      R.soff = 0;
-      R.pad = 0;
-      nr[x] = R;
-      c = runs_samples(R, g4);
-    }
-    cnt[x] = c;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < m; x += gridDim.x * blockDim.x) {
+    const uint32_t t = lnodes[ls + x];
+    NodeRuns R;
+    const uint32_t i = rs[seg_l[t]], j = rs[t], k = rs[seg_r[t]];
+    const uint32_t u = lchild[t], v = rchild[t];
+    R.b[0] = i;
+    R.b[1] = u ? rs[u] : j;
+    R.b[2] = j;
+    R.b[3] = v ? rs[v] : k;
+    R.b[4] = k;
+    R.par = buf2(dep[t] & 0xFFFFu);
+    R.pad[0] = R.pad[1] = 0;
+    nr[x] = R;
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact 4-way co-ranks at aligned output positions.
+//
+// X = merge(L, R), L = merge(W0, W1), R = merge(W2, W3), ties to the left at
+// both levels (Alg. 2), i.e. the stable merge of W0 W1 W2 W3.  For an
+// output diagonal d of X the split (c0, c1, c2, c3) is found by the outer
+// merge-path search over a = #L among the first d outputs, where L[a] and
+// R[d-a-1] come from inner merge-path co-ranks.  Every inner search is
+// bracketed by the co-ranks already evaluated (co-ranks are monotone and grow
+// by at most the diagonal step), so the brackets shrink with the outer window.
+// ---------------------------------------------------------------------------
 template <int KT>
-__device__ __forceinline__ uint32_t lower_bound_img(const typename KeyTraits<KT>::K* a, uint32_t n,
-                                                    typename KeyTraits<KT>::O v) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) { uint32_t m = (lo + hi) >> 1; if (KeyTraits<KT>::ord(a[m]) < v) lo = m + 1; else hi = m; }
-  return lo;
-}
-template <int KT>
-__device__ __forceinline__ uint32_t upper_bound_img(const typename KeyTraits<KT>::K* a, uint32_t n,
-                                                    typename KeyTraits<KT>::O v) {
-  uint32_t lo = 0, hi = n;
-  while (lo < hi) { uint32_t m = (lo + hi) >> 1; if (KeyTraits<KT>::ord(a[m]) <= v) lo = m + 1; else hi = m; }
-  return lo;
-}
-
-// Locate sample s of the level: node x (by the sample offsets), run r, index q.
-__device__ __forceinline__ void locate_sample(const uint32_t* soff, uint32_t m, const NodeRuns* nr, uint32_t s,
-                                              uint32_t g4, uint32_t* x, uint32_t* r, uint32_t* q) {
-  uint32_t a = 0, b = m;  // last node with soff[x] <= s
-  while (b - a > 1) { uint32_t mm = (a + b) >> 1; if (soff[mm] <= s) a = mm; else b = mm; }
-  *x = a;
-  uint32_t loc = s - soff[a];
-  const NodeRuns R = nr[a];
-  uint32_t rr = 0;
-  for (; rr < 4; ++rr) {
-    const uint32_t ns = (R.b[rr + 1] - R.b[rr] + g4 - 1) / g4;
-    if (loc < ns) break;
-    loc -= ns;
+struct InnerCR {
+  using K = typename KeyTraits<KT>::K;
+  const K* A;
+  const K* B;
+  uint32_t nA, nB;
+  uint32_t xl, cl, xh, ch;  // known co-ranks c(xl) = cl <= c(x) <= c(xh) = ch
+  __device__ __forceinline__ void init(const K* a, uint32_t na, const K* b, uint32_t nb) {
+    A = a; B = b; nA = na; nB = nb;
+    xl = 0; cl = 0; xh = na + nb; ch = na;
   }
-  *r = rr;
-  *q = loc * g4;
-}
+  // co-rank at x (xl <= x <= xh): #A among the first x outputs of merge(A, B)
+  __device__ __forceinline__ uint32_t co(uint32_t x) const {
+    uint32_t lo = max(cl, ch > xh - x ? ch - (xh - x) : 0u);
+    uint32_t hi = min(ch, cl + (x - xl));
+    lo = max(lo, x > nB ? x - nB : 0u);
+    hi = min(hi, min(x, nA));
+    return corank_in<KT>(A, nA, B, nB, x, lo, hi);
+  }
+  // element of rank x (x < nA + nB) given c = co(x)
+  __device__ __forceinline__ K elem(uint32_t x, uint32_t c) const {
+    using T = KeyTraits<KT>;
+    if (c < nA && (x - c >= nB || T::ord(A[c]) <= T::ord(B[x - c]))) return A[c];
+    return B[x - c];
+  }
+  __device__ __forceinline__ void know_low(uint32_t x, uint32_t c) { xl = x; cl = c; }
+  __device__ __forceinline__ void know_high(uint32_t x, uint32_t c) { xh = x; ch = c; }
+};
 
-// Ranks and per-run split counts of every sample of the level.
+// Split of X's first d outputs; the outer co-rank a lies in [alo, ahi]
+// (caller's bound, e.g. from the previous aligned boundary).  On return c[]
+// holds (c0, c1, c2, c3) and L / R know their co-ranks at a and d - a.
 template <int KT>
-__global__ void __launch_bounds__(256) k4_samples(const typename KeyTraits<KT>::K* __restrict__ k0,
-                                                  const typename KeyTraits<KT>::K* __restrict__ k1,
-                                                  const NodeRuns* __restrict__ nr, const uint32_t* __restrict__ soff,
-                                                  const uint32_t* __restrict__ level_start, int p, uint32_t g4,
-                                                  uint32_t* __restrict__ srank, uint4* __restrict__ sc) {
+__device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint32_t d, uint32_t alo,
+                                            uint32_t ahi, uint32_t* c) {
   using T = KeyTraits<KT>;
-  const uint32_t m = level_start[p + 1] - level_start[p];
-  const uint32_t total = soff[m];
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
-    uint32_t x, r, q;
-    locate_sample(soff, m, nr, s, g4, &x, &r, &q);
-    const NodeRuns R = nr[x];
-    const auto* src = R.par ? k0 : k1;  // inputs live in the other buffer
-    const typename T::O v = T::ord(src[R.b[r] + q]);
-    uint32_t c[4], rank = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t len = R.b[i + 1] - R.b[i];
-      uint32_t ci;
-      if (i < (int)r) ci = upper_bound_img<KT>(src + R.b[i], len, v);
-      else if (i > (int)r) ci = lower_bound_img<KT>(src + R.b[i], len, v);
-      else ci = q;
-      c[i] = ci;
-      rank += ci;
+  const uint32_t nL = L.nA + L.nB, nR = R.nA + R.nB;
+  // the known-low points stay valid (queries only move right: L at a >=
+  // a_prev, R at d - mid - 1 >= d_prev - a_prev); reset the known-high ones
+  L.know_high(nL, L.nA);
+  R.know_high(nR, R.nA);
+  alo = max(alo, d > nR ? d - nR : 0u);
+  ahi = min(ahi, min(d, nL));
+  while (alo < ahi) {
+    const uint32_t mid = (alo + ahi) >> 1;
+    const uint32_t cL = L.co(mid);
+    const uint32_t r = d - mid - 1;  // < nR since mid >= d - nR
+    const uint32_t cR = R.co(r);
+    if (T::ord(L.elem(mid, cL)) <= T::ord(R.elem(r, cR))) {  // L[mid] precedes R[d-mid-1]
+      alo = mid + 1;
+      L.know_low(mid, cL);
+      R.know_high(r, cR);
+    } else {
+      ahi = mid;
+      L.know_high(mid, cL);
+      R.know_low(r, cR);
     }
-    srank[s] = rank;
-    sc[s] = make_uint4(c[0], c[1], c[2], c[3]);
   }
+  const uint32_t a = alo;
+  const uint32_t c0 = L.co(a), c2 = R.co(d - a);
+  L.know_low(a, c0);
+  R.know_low(d - a, c2);
+  c[0] = c0; c[1] = a - c0; c[2] = c2; c[3] = d - a - c2;
+  return a;
 }
 
-// Sorted position of every sample within its node -> the tile list.
-__global__ void __launch_bounds__(256) k4_order(const NodeRuns* __restrict__ nr, const uint32_t* __restrict__ soff,
-                                                const uint32_t* __restrict__ level_start, int p, uint32_t g4,
-                                                const uint32_t* __restrict__ srank, const uint4* __restrict__ sc,
-                                                TileDesc4* __restrict__ tiles) {
-  const uint32_t m = level_start[p + 1] - level_start[p];
-  const uint32_t total = soff[m];
-  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < total; s += gridDim.x * blockDim.x) {
-    uint32_t x, r, q;
-    locate_sample(soff, m, nr, s, g4, &x, &r, &q);
-    const NodeRuns R = nr[x];
-    const uint32_t rank = srank[s];
-    uint32_t pos = q / g4, base = soff[x];
-    for (uint32_t i = 0; i < 4; ++i) {
-      const uint32_t ns = (R.b[i + 1] - R.b[i] + g4 - 1) / g4;
-      if (i != r && ns) {  // samples of run i with a smaller rank (ranks increase within a run)
-        uint32_t lo = 0, hi = ns;
-        while (lo < hi) { uint32_t mm = (lo + hi) >> 1; if (srank[base + mm] < rank) lo = mm + 1; else hi = mm; }
-        pos += lo;
+// Tile descriptors of one level of the two-level schedule: tiles aligned to
+// global multiples of T (enumerated by k_level_tiles / ltiles like the
+// one-level engine), DESC_CHUNK consecutive tiles per thread; the first
+// boundary of a chunk is a full search, the next ones search a in
+// [a_prev, a_prev + T].
+template <int KT>
+__global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* __restrict__ k0,
+                                               const typename KeyTraits<KT>::K* __restrict__ k1,
+                                               const NodeRuns* __restrict__ nr, const uint32_t* __restrict__ ltiles,
+                                               const uint32_t* __restrict__ level_start,
+                                               const uint32_t* __restrict__ level_tile, int p, uint32_t tout,
+                                               TileDesc4* __restrict__ tiles) {
+  const uint32_t ls = level_start[p], le = level_start[p + 1];
+  const uint32_t tb = level_tile[p], te = level_tile[p + 1];
+  const uint32_t nchunks = (te - tb + DESC_CHUNK - 1) / DESC_CHUNK;
+  for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks; ch += gridDim.x * blockDim.x) {
+    const uint32_t tau0 = tb + ch * DESC_CHUNK;
+    uint32_t a = ls, b = le;  // last bucket x with ltiles[x] <= tau0
+    while (b - a > 1) { uint32_t m = (a + b) >> 1; if (ltiles[m] <= tau0) a = m; else b = m; }
+    uint32_t cur = 0xFFFFFFFFu, aprev = 0, dprev = 0;
+    InnerCR<KT> L, R;
+    NodeRuns X;
+    for (uint32_t q = 0; q < DESC_CHUNK; ++q) {
+      const uint32_t tau = tau0 + q;
+      if (tau >= te) break;
+      while (a + 1 < le && ltiles[a + 1] <= tau) ++a;
+      if (a != cur) {
+        X = nr[a - ls];
+        const auto* src = X.par ? k0 : k1;  // inputs live in the other buffer
+        L.init(src + X.b[0], X.b[1] - X.b[0], src + X.b[1], X.b[2] - X.b[1]);
+        R.init(src + X.b[2], X.b[3] - X.b[2], src + X.b[3], X.b[4] - X.b[3]);
+        cur = a;
+        aprev = 0;
+        dprev = 0;
       }
-      base += ns;
+      const uint32_t i = X.b[0], k = X.b[4];
+      const uint32_t g = i / tout + (tau - ltiles[a]);
+      const uint32_t lo = max(i, g * tout);
+      const uint32_t d = lo - i;
+      uint32_t c[4];
+      const uint32_t av = corank4<KT>(L, R, d, aprev, aprev + (d - dprev), c);
+      aprev = av;
+      dprev = d;
+      TileDesc4 D;
+      D.x = a - ls;
+      D.rank = d;
+      D.c[0] = c[0]; D.c[1] = c[1]; D.c[2] = c[2]; D.c[3] = c[3];
+      tiles[tau - tb] = D;
+      (void)k;
     }
-    TileDesc4 d;
-    d.x = x;
-    d.rank = rank;
-    const uint4 c = sc[s];
-    d.c[0] = c.x; d.c[1] = c.y; d.c[2] = c.z; d.c[3] = c.w;
-    tiles[soff[x] + pos] = d;
   }
 }
 
@@ -281,168 +296,179 @@ __device__ __forceinline__ void merge4_issue(const TileDesc4& d, const TileDesc4
   }
 }
 
-// Merge-path co-rank over two shared-memory sequences (ties to A).
-template <int KT>
-__device__ __forceinline__ uint32_t corank_s(const typename KeyTraits<KT>::K* A, uint32_t nA,
-                                             const typename KeyTraits<KT>::K* B, uint32_t nB, uint32_t d) {
-  return corank<KT>(A, nA, B, nB, d);
-}
-
 // Step A: P01 = W0 (+) W1 into [0, n01), P23 = W2 (+) W3 into [n01, T4) of
-// the intermediate, KQ outputs per thread; each entry keeps the stage index of
-// its value.  A chunk straddling n01 is split into its two sub-merges.
-template <int KT, int KQ>
-__device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK, const Merge4Hdr& h,
+// the intermediate (keys + the stage index of each value), 8 outputs per
+// thread.  A chunk inside one of the two merges takes the branch-free path
+// over absolute stage indices (a read one past a window stays inside the
+// stage: windows are padded); the chunk holding n01 or T4 goes element-wise.
+template <int KT>
+__device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK, const Merge4Hdr* hp,
                                              uint32_t n01, uint32_t T4, typename KeyTraits<KT>::K* IKs,
                                              uint16_t* IIs) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
-  const uint32_t q0 = threadIdx.x * KQ, q1 = min(q0 + (uint32_t)KQ, T4);
-  uint32_t q = q0;
-  while (q < q1) {
-    const bool first = q < n01;
-    const uint32_t e = first ? min(q1, n01) : q1;
-    const uint32_t wa = first ? 0u : 2u;
-    const K* A = SK + h.kb[wa];
-    const K* B = SK + h.kb[wa + 1];
-    const uint32_t nA = h.n[wa], nB = h.n[wa + 1];
-    const uint32_t d0 = first ? q : q - n01;
-    uint32_t ia = corank<KT>(A, nA, B, nB, d0), ib = d0 - ia;
-    K ka = A[min(ia, nA ? nA - 1 : 0u)], kb = B[min(ib, nB ? nB - 1 : 0u)];
-    for (; q < e; ++q) {
-      const bool pa = ib >= nB || (ia < nA && T::ord(ka) <= T::ord(kb));
-      IKs[q] = pa ? ka : kb;
-      IIs[q] = (uint16_t)(pa ? h.vb[wa] + ia : h.vb[wa + 1] + ib);
-      ia += pa ? 1u : 0u;
-      ib += pa ? 0u : 1u;
-      if (pa) { if (ia < nA) ka = A[ia]; }
-      else { if (ib < nB) kb = B[ib]; }
-    }
-  }
-}
-
-template <int KQ>
-__device__ __forceinline__ void store_chunk(uint32_t* dst, const uint32_t (&r)[8]) {
-  if (KQ == 8) { st_v4(dst, r[0], r[1], r[2], r[3]); st_v4(dst + 4, r[4], r[5], r[6], r[7]); }
-  else if (KQ == 4) st_v4(dst, r[0], r[1], r[2], r[3]);
-  else { dst[0] = r[0]; dst[1] = r[1]; }
-}
-template <int KQ>
-__device__ __forceinline__ void store_chunk(uint64_t* dst, const uint64_t (&r)[8]) {
+  const uint32_t q0 = threadIdx.x * MERGE_K;
+  if (q0 >= T4) return;
+  // the chunk's merge(s): [q0, q0+8) meets P01 = [0, n01) and/or P23 = [n01, T4);
+  // each is a branch-free 8-step merge whose stores are predicated
+#pragma unroll 1
+  for (uint32_t part = (q0 < n01 ? 0u : 1u); part < 2u; ++part) {
+    const uint32_t plo = part ? n01 : 0u, phi = part ? T4 : n01;
+    if (q0 >= phi || q0 + MERGE_K <= plo) continue;
+    const uint32_t wa = 2u * part;
+    const uint32_t nA = hp->n[wa], nB = hp->n[wa + 1];
+    const uint32_t ka0 = hp->kb[wa], kb0 = hp->kb[wa + 1];
+    const int32_t dA = (int32_t)hp->vb[wa] - (int32_t)ka0, dB = (int32_t)hp->vb[wa + 1] - (int32_t)kb0;
+    const uint32_t qs = max(q0, plo);
+    const uint32_t d = qs - plo;
+    const uint32_t l = corank<KT>(SK + ka0, nA, SK + kb0, nB, d);
+    uint32_t ia = ka0 + l, ib = kb0 + d - l;
+    const uint32_t ea = ka0 + nA, eb = kb0 + nB;
+    K ka = SK[ia], kb = SK[ib];
+    K rk[MERGE_K];
+    uint32_t ri[MERGE_K];
 #pragma unroll
-  for (int q = 0; q < KQ; q += 2)
-    st_v4(dst + q, (uint32_t)r[q], (uint32_t)(r[q] >> 32), (uint32_t)r[q + 1], (uint32_t)(r[q + 1] >> 32));
-}
-
-// Step B: output = P01 (+) P23 for KQ-aligned chunks of global positions.
-template <int KT, bool HV, int KQ>
-__device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IKs, const uint16_t* IIs,
-                                             const uint32_t* SV, const Merge4Hdr& h, uint32_t n01, uint32_t T4,
-                                             typename KeyTraits<KT>::K* k0, uint32_t* v0,
-                                             typename KeyTraits<KT>::K* k1, uint32_t* v1) {
-  using T = KeyTraits<KT>;
-  using K = typename T::K;
-  const uint32_t start = (h.lo & ~(uint32_t)(KQ - 1)) + threadIdx.x * KQ;
-  if (!(start < h.hi && start + KQ > h.lo)) return;
-  const uint32_t qs = max(start, h.lo), qe = min(start + (uint32_t)KQ, h.hi);
-  const uint32_t d = qs - h.lo;
-  const uint32_t nA = n01, nB = T4 - n01;
-  const K* A = IKs;
-  const K* B = IKs + n01;
-  uint32_t ia = corank<KT>(A, nA, B, nB, d), ib = d - ia;
-  // carried heads; a read one past a side stays inside the intermediate
-  K ka = IKs[min(ia, T4 - 1)], kb = IKs[min(n01 + ib, T4 - 1)];
-  K rk[8];
-  uint32_t ri[8], rv[8];
-#pragma unroll
-  for (int q = 0; q < KQ; ++q) {
-    const uint32_t pos = start + q;
-    if (pos >= qs && pos < qe) {
-      const bool pa = ib >= nB || (ia < nA && T::ord(ka) <= T::ord(kb));
+    for (int q = 0; q < (int)MERGE_K; ++q) {
+      // past both ends (only in a predicated-off tail) the reads stay in the stage
+      const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
       rk[q] = pa ? ka : kb;
-      ri[q] = pa ? ia : nA + ib;
+      ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
       ia += pa ? 1u : 0u;
       ib += pa ? 0u : 1u;
-      const K nx = IKs[min(pa ? ia : nA + ib, T4 - 1)];
+      const K nx = SK[pa ? ia : ib];
       ka = pa ? nx : ka;
       kb = pa ? kb : nx;
-    } else {
-      rk[q] = K(0);
-      ri[q] = 0;
     }
-  }
-  if (HV) {
+    if (qs == q0 && q0 + MERGE_K <= phi) {
 #pragma unroll
-    for (int q = 0; q < KQ; ++q) rv[q] = SV[IIs[ri[q]]];
-  }
-  K* dk = h.par ? k1 : k0;
-  uint32_t* dv = h.par ? v1 : v0;
-  if (qs == start && qe == start + KQ) {
-    store_chunk<KQ>(dk + start, rk);
-    if (HV) store_chunk<KQ>(dv + start, rv);
-  } else {
+      for (int q = 0; q < (int)MERGE_K; ++q) IKs[q0 + q] = rk[q];
+      *reinterpret_cast<uint4*>(IIs + q0) =
+          make_uint4(ri[0] | (ri[1] << 16), ri[2] | (ri[3] << 16), ri[4] | (ri[5] << 16), ri[6] | (ri[7] << 16));
+    } else {
 #pragma unroll
-    for (int q = 0; q < KQ; ++q) {
-      const uint32_t pos = start + q;
-      if (pos >= qs && pos < qe) { dk[pos] = rk[q]; if (HV) dv[pos] = rv[q]; }
+      for (int q = 0; q < (int)MERGE_K; ++q) {
+        const uint32_t pos = qs + q;
+        if (pos < phi && pos < q0 + MERGE_K) { IKs[pos] = rk[q]; IIs[pos] = (uint16_t)ri[q]; }
+      }
     }
   }
 }
 
+template <typename K>
+__device__ __forceinline__ void store8(K* dst, const K (&r)[MERGE_K]) { store_vec8<K>(dst, r); }
+
+// Step B: output = P01 (+) P23 for 8-aligned chunks of global positions;
+// an edge chunk (partly outside [lo, hi)) runs the same branch-free merge
+// from its first in-range output and predicates its stores.
 template <int KT, bool HV>
-__global__ void __launch_bounds__(MERGE_BLOCK, 2) k4_merge_level(
-    typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
-    typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
-    const TileDesc4* __restrict__ tiles, const NodeRuns* __restrict__ nr, const uint32_t* __restrict__ soff,
-    const uint32_t* __restrict__ level_start, int p) {
+__device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IKs, const uint16_t* IIs,
+                                             const uint32_t* SV, uint32_t lo, uint32_t hi, uint32_t par,
+                                             uint32_t n01, uint32_t T4, typename KeyTraits<KT>::K* k0,
+                                             uint32_t* v0, typename KeyTraits<KT>::K* k1, uint32_t* v1) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
+  const uint32_t start = (lo & ~(uint32_t)(MERGE_K - 1)) + threadIdx.x * MERGE_K;
+  if (!(start < hi && start + MERGE_K > lo)) return;
+  K* dk = par ? k1 : k0;
+  uint32_t* dv = par ? v1 : v0;
+  const uint32_t nA = n01, nB = T4 - n01;
+  const uint32_t qs = max(start, lo);
+  const uint32_t d = qs - lo;
+  const uint32_t l = corank<KT>(IKs, nA, IKs + n01, nB, d);
+  uint32_t ia = l, ib = n01 + d - l;
+  const uint32_t ea = n01, eb = T4;
+  K ka = IKs[ia], kb = IKs[ib];  // reads past T4 stay inside the intermediate (slack)
+  K rk[MERGE_K];
+  uint32_t ri[MERGE_K];
+#pragma unroll
+  for (int q = 0; q < (int)MERGE_K; ++q) {
+    const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
+    rk[q] = pa ? ka : kb;
+    ri[q] = pa ? ia : ib;
+    ia += pa ? 1u : 0u;
+    ib += pa ? 0u : 1u;
+    const K nx = IKs[pa ? ia : ib];
+    ka = pa ? nx : ka;
+    kb = pa ? kb : nx;
+  }
+  uint32_t rv[MERGE_K];
+  if (HV) {
+#pragma unroll
+    for (int q = 0; q < (int)MERGE_K; ++q) rv[q] = SV[IIs[min(ri[q], T4 - 1)]];
+  }
+  if (qs == start && start + MERGE_K <= hi) {
+    store_vec8<K>(dk + start, rk);
+    if (HV) store_vec8<uint32_t>(dv + start, rv);
+  } else {
+#pragma unroll
+    for (int q = 0; q < (int)MERGE_K; ++q) {
+      const uint32_t pos = qs + q;
+      if (pos < hi && pos < start + MERGE_K) { dk[pos] = rk[q]; if (HV) dv[pos] = rv[q]; }
+    }
+  }
+}
+
+// The fused merge: persistent CTAs; 16 consumer warps merge, one producer
+// warp loads descriptors and issues the bulk copies of the next tile into
+// the free stage (full / empty mbarrier pairs), so no consumer ever waits on
+// a descriptor load.
+template <int KT, bool HV>
+__global__ void __launch_bounds__(MERGE_BLOCK + 32, 2) k4_merge_level(
+    typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
+    typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
+    const TileDesc4* __restrict__ tiles, const NodeRuns* __restrict__ nr,
+    const uint32_t* __restrict__ level_tile, int p) {
+  using K = typename KeyTraits<KT>::K;
   using SM = Merge4Smem<KT, HV>;
   static_assert(MERGE_BLOCK * MERGE_K == 4096, "merge4 tile");
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 2;
   Merge4Hdr* hdr = reinterpret_cast<Merge4Hdr*>(smem + 64);
   K* IKs = reinterpret_cast<K*>(smem + SM::HDR + 2 * SM::STAGE);
   uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + 2 * SM::STAGE + SM::IK);
-  const uint32_t m = level_start[p + 1] - level_start[p];
-  const uint32_t count = soff[m];
+  const uint32_t count = level_tile[p + 1] - level_tile[p];
   if (blockIdx.x >= count) return;
   const uint32_t tid = threadIdx.x;
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], MERGE_BLOCK / 32);
+    mbar_init(&empty[1], MERGE_BLOCK / 32);
     fence_mbar_init();
   }
   __syncthreads();
-  auto issue = [&](uint32_t tau, uint32_t s) {
-    const TileDesc4 d = tiles[tau];
-    const bool more = tau + 1 < count;
-    TileDesc4 dn;
-    if (more) dn = tiles[tau + 1];
-    const bool same = more && dn.x == d.x;
-    merge4_issue<KT, HV>(d, same ? &dn : nullptr, nr[d.x], s, smem, bars, hdr, k0, v0, k1, v1);
-  };
-  if (tid == 0) issue(blockIdx.x, 0);
+  if (tid >= MERGE_BLOCK) {  // producer warp
+    if (tid == MERGE_BLOCK) {
+      uint32_t it = 0;
+      for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
+        const uint32_t s = it & 1u;
+        if (it >= 2) mbar_wait(&empty[s], ((it >> 1) - 1) & 1u);
+        const TileDesc4 d = tiles[tau];
+        TileDesc4 dn;
+        const bool same = tau + 1 < count && (dn = tiles[tau + 1], dn.x == d.x);
+        merge4_issue<KT, HV>(d, same ? &dn : nullptr, nr[d.x], s, smem, full, hdr, k0, v0, k1, v1);
+      }
+    }
+    return;
+  }
+  const uint32_t lane = tid & 31u;
   uint32_t it = 0;
   for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
     const uint32_t s = it & 1u;
-    if (tid == 0 && tau + gridDim.x < count) issue(tau + gridDim.x, s ^ 1u);
-    mbar_wait(&bars[s], (it >> 1) & 1u);
-    const Merge4Hdr h = hdr[s];
+    mbar_wait(&full[s], (it >> 1) & 1u);
+    const Merge4Hdr* hp = hdr + s;
     const unsigned char* st = smem + SM::HDR + s * SM::STAGE;
     const K* SK = reinterpret_cast<const K*>(st);
     const uint32_t* SV = reinterpret_cast<const uint32_t*>(st + SM::KB);
-    const uint32_t n01 = h.n[0] + h.n[1], T4 = h.hi - h.lo;
-    // outputs per thread chosen per tile so every warp has work
-    const uint32_t kq = T4 <= 1020 ? 2u : (T4 <= 2040 ? 4u : 8u);
-    if (kq == 2) merge4_stepA<KT, 2>(SK, h, n01, T4, IKs, IIs);
-    else if (kq == 4) merge4_stepA<KT, 4>(SK, h, n01, T4, IKs, IIs);
-    else merge4_stepA<KT, 8>(SK, h, n01, T4, IKs, IIs);
-    __syncthreads();
-    if (kq == 2) merge4_stepB<KT, HV, 2>(IKs, IIs, SV, h, n01, T4, k0, v0, k1, v1);
-    else if (kq == 4) merge4_stepB<KT, HV, 4>(IKs, IIs, SV, h, n01, T4, k0, v0, k1, v1);
-    else merge4_stepB<KT, HV, 8>(IKs, IIs, SV, h, n01, T4, k0, v0, k1, v1);
-    __syncthreads();
+    const uint32_t lo = hp->lo, hi = hp->hi, par = hp->par;
+    const uint32_t n01 = hp->n[0] + hp->n[1], T4 = hi - lo;
+    merge4_stepA<KT>(SK, hp, n01, T4, IKs, IIs);
+    named_bar_sync(1, MERGE_BLOCK);
+    merge4_stepB<KT, HV>(IKs, IIs, SV, lo, hi, par, n01, T4, k0, v0, k1, v1);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // stage s is free once every warp is past step B
+    named_bar_sync(1, MERGE_BLOCK);        // the intermediate is reused by the next tile
   }
 }
 

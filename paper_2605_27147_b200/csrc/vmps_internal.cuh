@@ -123,9 +123,9 @@ struct Work {
   unsigned long long* counters;  // [0] M, [1] fused M
   // two-level fused merges (engine4.cuh)
   int fuse2;
-  uint32_t *lchild, *rchild, *n4cnt, *n4off, *srank;
-  void *nr4, *sc4, *tiles4;
-  uint32_t n4cap, s4cap, g4;
+  uint32_t *lchild, *rchild;
+  void *nr4, *tiles4;
+  uint32_t n4cap;
   // scratch-bounded mode (bounded.cuh); element scratch = F blocks of P
   int bounded;
   uint32_t P, F, NB;
