@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvmps.so")
+LIB_PATH = os.environ.get("VMPS_LIB") or os.path.join(_HERE, "libvmps.so")
 
 KEY_U32, KEY_U64, KEY_F32 = 0, 1, 2
 SCRATCH_UNBOUNDED = -1

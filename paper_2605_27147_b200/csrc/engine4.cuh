@@ -30,6 +30,8 @@ struct NodeRuns {
   uint32_t pad[2];
 };
 
+constexpr int M4_KQ = 8;  // outputs per consumer thread of the 4-way merge (256 + 32 threads)
+
 struct TileDesc4 {
   uint32_t x;     // node (local index in the level)
   uint32_t rank;  // output rank of the tile start within the node
@@ -156,6 +158,10 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
 // one-level engine), DESC_CHUNK consecutive tiles per thread; the first
 // boundary of a chunk is a full search, the next ones search a in
 // [a_prev, a_prev + T].
+#ifndef VMPS_DESC4_CHUNK
+#define VMPS_DESC4_CHUNK 8
+#endif
+constexpr uint32_t DESC4_CHUNK = VMPS_DESC4_CHUNK;
 template <int KT>
 __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* __restrict__ k0,
                                                const typename KeyTraits<KT>::K* __restrict__ k1,
@@ -165,15 +171,15 @@ __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* 
                                                TileDesc4* __restrict__ tiles) {
   const uint32_t ls = level_start[p], le = level_start[p + 1];
   const uint32_t tb = level_tile[p], te = level_tile[p + 1];
-  const uint32_t nchunks = (te - tb + DESC_CHUNK - 1) / DESC_CHUNK;
+  const uint32_t nchunks = (te - tb + DESC4_CHUNK - 1) / DESC4_CHUNK;
   for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks; ch += gridDim.x * blockDim.x) {
-    const uint32_t tau0 = tb + ch * DESC_CHUNK;
+    const uint32_t tau0 = tb + ch * DESC4_CHUNK;
     uint32_t a = ls, b = le;  // last bucket x with ltiles[x] <= tau0
     while (b - a > 1) { uint32_t m = (a + b) >> 1; if (ltiles[m] <= tau0) a = m; else b = m; }
     uint32_t cur = 0xFFFFFFFFu, aprev = 0, dprev = 0;
     InnerCR<KT> L, R;
     NodeRuns X;
-    for (uint32_t q = 0; q < DESC_CHUNK; ++q) {
+    for (uint32_t q = 0; q < DESC4_CHUNK; ++q) {
       const uint32_t tau = tau0 + q;
       if (tau >= te) break;
       while (a + 1 < le && ltiles[a + 1] <= tau) ++a;
@@ -301,20 +307,20 @@ __device__ __forceinline__ void merge4_issue(const TileDesc4& d, const TileDesc4
 // thread.  A chunk inside one of the two merges takes the branch-free path
 // over absolute stage indices (a read one past a window stays inside the
 // stage: windows are padded); the chunk holding n01 or T4 goes element-wise.
-template <int KT>
+template <int KT, int KQ>
 __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK, const Merge4Hdr* hp,
                                              uint32_t n01, uint32_t T4, typename KeyTraits<KT>::K* IKs,
                                              uint16_t* IIs) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
-  const uint32_t q0 = threadIdx.x * MERGE_K;
+  const uint32_t q0 = threadIdx.x * (uint32_t)KQ;
   if (q0 >= T4) return;
   // the chunk's merge(s): [q0, q0+8) meets P01 = [0, n01) and/or P23 = [n01, T4);
   // each is a branch-free 8-step merge whose stores are predicated
 #pragma unroll 1
   for (uint32_t part = (q0 < n01 ? 0u : 1u); part < 2u; ++part) {
     const uint32_t plo = part ? n01 : 0u, phi = part ? T4 : n01;
-    if (q0 >= phi || q0 + MERGE_K <= plo) continue;
+    if (q0 >= phi || q0 + (uint32_t)KQ <= plo) continue;
     const uint32_t wa = 2u * part;
     const uint32_t nA = hp->n[wa], nB = hp->n[wa + 1];
     const uint32_t ka0 = hp->kb[wa], kb0 = hp->kb[wa + 1];
@@ -325,10 +331,10 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
     uint32_t ia = ka0 + l, ib = kb0 + d - l;
     const uint32_t ea = ka0 + nA, eb = kb0 + nB;
     K ka = SK[ia], kb = SK[ib];
-    K rk[MERGE_K];
-    uint32_t ri[MERGE_K];
+    K rk[(uint32_t)KQ];
+    uint32_t ri[(uint32_t)KQ];
 #pragma unroll
-    for (int q = 0; q < (int)MERGE_K; ++q) {
+    for (int q = 0; q < KQ; ++q) {
       // past both ends (only in a predicated-off tail) the reads stay in the stage
       const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
       rk[q] = pa ? ka : kb;
@@ -339,36 +345,47 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
       ka = pa ? nx : ka;
       kb = pa ? kb : nx;
     }
-    if (qs == q0 && q0 + MERGE_K <= phi) {
+    if (qs == q0 && q0 + (uint32_t)KQ <= phi) {
 #pragma unroll
-      for (int q = 0; q < (int)MERGE_K; ++q) IKs[q0 + q] = rk[q];
-      *reinterpret_cast<uint4*>(IIs + q0) =
-          make_uint4(ri[0] | (ri[1] << 16), ri[2] | (ri[3] << 16), ri[4] | (ri[5] << 16), ri[6] | (ri[7] << 16));
+      for (int q = 0; q < KQ; ++q) IKs[q0 + q] = rk[q];
+#pragma unroll
+      for (int q = 0; q < KQ; q += 8)
+        *reinterpret_cast<uint4*>(IIs + q0 + q) = make_uint4(ri[q] | (ri[q + 1] << 16), ri[q + 2] | (ri[q + 3] << 16),
+                                                             ri[q + 4] | (ri[q + 5] << 16), ri[q + 6] | (ri[q + 7] << 16));
     } else {
 #pragma unroll
-      for (int q = 0; q < (int)MERGE_K; ++q) {
+      for (int q = 0; q < KQ; ++q) {
         const uint32_t pos = qs + q;
-        if (pos < phi && pos < q0 + MERGE_K) { IKs[pos] = rk[q]; IIs[pos] = (uint16_t)ri[q]; }
+        if (pos < phi && pos < q0 + (uint32_t)KQ) { IKs[pos] = rk[q]; IIs[pos] = (uint16_t)ri[q]; }
       }
     }
   }
 }
 
-template <typename K>
-__device__ __forceinline__ void store8(K* dst, const K (&r)[MERGE_K]) { store_vec8<K>(dst, r); }
+template <int KQ>
+__device__ __forceinline__ void store_chunk_g(uint32_t* dst, const uint32_t (&r)[KQ]) {
+#pragma unroll
+  for (int q = 0; q < KQ; q += 4) st_v4(dst + q, r[q], r[q + 1], r[q + 2], r[q + 3]);
+}
+template <int KQ>
+__device__ __forceinline__ void store_chunk_g(uint64_t* dst, const uint64_t (&r)[KQ]) {
+#pragma unroll
+  for (int q = 0; q < KQ; q += 2)
+    st_v4(dst + q, (uint32_t)r[q], (uint32_t)(r[q] >> 32), (uint32_t)r[q + 1], (uint32_t)(r[q + 1] >> 32));
+}
 
 // Step B: output = P01 (+) P23 for 8-aligned chunks of global positions;
 // an edge chunk (partly outside [lo, hi)) runs the same branch-free merge
 // from its first in-range output and predicates its stores.
-template <int KT, bool HV>
+template <int KT, bool HV, int KQ>
 __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IKs, const uint16_t* IIs,
                                              const uint32_t* SV, uint32_t lo, uint32_t hi, uint32_t par,
                                              uint32_t n01, uint32_t T4, typename KeyTraits<KT>::K* k0,
                                              uint32_t* v0, typename KeyTraits<KT>::K* k1, uint32_t* v1) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
-  const uint32_t start = (lo & ~(uint32_t)(MERGE_K - 1)) + threadIdx.x * MERGE_K;
-  if (!(start < hi && start + MERGE_K > lo)) return;
+  const uint32_t start = (lo & ~(uint32_t)((uint32_t)KQ - 1)) + threadIdx.x * (uint32_t)KQ;
+  if (!(start < hi && start + (uint32_t)KQ > lo)) return;
   K* dk = par ? k1 : k0;
   uint32_t* dv = par ? v1 : v0;
   const uint32_t nA = n01, nB = T4 - n01;
@@ -378,10 +395,10 @@ __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IK
   uint32_t ia = l, ib = n01 + d - l;
   const uint32_t ea = n01, eb = T4;
   K ka = IKs[ia], kb = IKs[ib];  // reads past T4 stay inside the intermediate (slack)
-  K rk[MERGE_K];
-  uint32_t ri[MERGE_K];
+  K rk[(uint32_t)KQ];
+  uint32_t ri[(uint32_t)KQ];
 #pragma unroll
-  for (int q = 0; q < (int)MERGE_K; ++q) {
+  for (int q = 0; q < KQ; ++q) {
     const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
     rk[q] = pa ? ka : kb;
     ri[q] = pa ? ia : ib;
@@ -391,19 +408,19 @@ __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IK
     ka = pa ? nx : ka;
     kb = pa ? kb : nx;
   }
-  uint32_t rv[MERGE_K];
+  uint32_t rv[(uint32_t)KQ];
   if (HV) {
 #pragma unroll
-    for (int q = 0; q < (int)MERGE_K; ++q) rv[q] = SV[IIs[min(ri[q], T4 - 1)]];
+    for (int q = 0; q < KQ; ++q) rv[q] = SV[IIs[min(ri[q], T4 - 1)]];
   }
-  if (qs == start && start + MERGE_K <= hi) {
-    store_vec8<K>(dk + start, rk);
-    if (HV) store_vec8<uint32_t>(dv + start, rv);
+  if (qs == start && start + (uint32_t)KQ <= hi) {
+    store_chunk_g<KQ>(dk + start, rk);
+    if (HV) store_chunk_g<KQ>(dv + start, rv);
   } else {
 #pragma unroll
-    for (int q = 0; q < (int)MERGE_K; ++q) {
+    for (int q = 0; q < KQ; ++q) {
       const uint32_t pos = qs + q;
-      if (pos < hi && pos < start + MERGE_K) { dk[pos] = rk[q]; if (HV) dv[pos] = rv[q]; }
+      if (pos < hi && pos < start + (uint32_t)KQ) { dk[pos] = rk[q]; if (HV) dv[pos] = rv[q]; }
     }
   }
 }
@@ -412,15 +429,15 @@ __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IK
 // warp loads descriptors and issues the bulk copies of the next tile into
 // the free stage (full / empty mbarrier pairs), so no consumer ever waits on
 // a descriptor load.
-template <int KT, bool HV>
-__global__ void __launch_bounds__(MERGE_BLOCK + 32, 2) k4_merge_level(
+template <int KT, bool HV, int KQ>
+__global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
     const TileDesc4* __restrict__ tiles, const NodeRuns* __restrict__ nr,
     const uint32_t* __restrict__ level_tile, int p) {
   using K = typename KeyTraits<KT>::K;
   using SM = Merge4Smem<KT, HV>;
-  static_assert(MERGE_BLOCK * MERGE_K == 4096, "merge4 tile");
+  constexpr uint32_t NT = 4096 / KQ;  // consumer threads
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 2;
@@ -433,13 +450,13 @@ __global__ void __launch_bounds__(MERGE_BLOCK + 32, 2) k4_merge_level(
   if (tid == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
-    mbar_init(&empty[0], MERGE_BLOCK / 32);
-    mbar_init(&empty[1], MERGE_BLOCK / 32);
+    mbar_init(&empty[0], NT / 32);
+    mbar_init(&empty[1], NT / 32);
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid >= MERGE_BLOCK) {  // producer warp
-    if (tid == MERGE_BLOCK) {
+  if (tid >= NT) {  // producer warp
+    if (tid == NT) {
       uint32_t it = 0;
       for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
         const uint32_t s = it & 1u;
@@ -463,12 +480,12 @@ __global__ void __launch_bounds__(MERGE_BLOCK + 32, 2) k4_merge_level(
     const uint32_t* SV = reinterpret_cast<const uint32_t*>(st + SM::KB);
     const uint32_t lo = hp->lo, hi = hp->hi, par = hp->par;
     const uint32_t n01 = hp->n[0] + hp->n[1], T4 = hi - lo;
-    merge4_stepA<KT>(SK, hp, n01, T4, IKs, IIs);
-    named_bar_sync(1, MERGE_BLOCK);
-    merge4_stepB<KT, HV>(IKs, IIs, SV, lo, hi, par, n01, T4, k0, v0, k1, v1);
+    merge4_stepA<KT, KQ>(SK, hp, n01, T4, IKs, IIs);
+    named_bar_sync(1, NT);
+    merge4_stepB<KT, HV, KQ>(IKs, IIs, SV, lo, hi, par, n01, T4, k0, v0, k1, v1);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);  // stage s is free once every warp is past step B
-    named_bar_sync(1, MERGE_BLOCK);        // the intermediate is reused by the next tile
+    named_bar_sync(1, NT);        // the intermediate is reused by the next tile
   }
 }
 
