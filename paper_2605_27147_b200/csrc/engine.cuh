@@ -21,9 +21,14 @@
 
 namespace vmps {
 
-constexpr int LEAF_THREADS = 512;
-constexpr int LEAF_K = 9;                         // odd: conflict-free chunk stride
-constexpr int LEAF_CAP = LEAF_THREADS * LEAF_K;   // 4608 >= 2Z - 1 (a batch holds < 2Z)
+#ifndef VMPS_LEAF_THREADS
+#define VMPS_LEAF_THREADS 384
+#define VMPS_LEAF_K 11
+#define VMPS_LEAF_MINB 4
+#endif
+constexpr int LEAF_THREADS = VMPS_LEAF_THREADS;
+constexpr int LEAF_K = VMPS_LEAF_K;               // odd: conflict-free chunk stride
+constexpr int LEAF_CAP = LEAF_THREADS * LEAF_K;   // 4224 >= 2Z - 1 (a batch holds < 2Z)
 static_assert(LEAF_CAP >= 2 * (int)MAX_FUSE_Z - 1, "leaf capacity");
 
 template <int KT>
@@ -45,7 +50,7 @@ __device__ __forceinline__ uint32_t corank(const typename KeyTraits<KT>::K* A, u
 // local indices (ping-pong); payloads are gathered once at the end.  Rounds
 // whose pairs fit inside one warp's range synchronise with __syncwarp only.
 template <int KT, bool HV>
-__global__ void __launch_bounds__(LEAF_THREADS, 3) k_leaf_sort(
+__global__ void __launch_bounds__(LEAF_THREADS, VMPS_LEAF_MINB) k_leaf_sort(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
     const uint32_t* __restrict__ units, const uint32_t* __restrict__ batch_first, uint32_t fuse_z) {

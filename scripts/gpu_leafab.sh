@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+R=gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q > $R/q_tests.log 2>&1; echo "tests=$?" > $R/q_status.txt
+B="python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline --bounded-reps 0"
+timeout 300 $B > $R/lf_384.log 2>&1
+VMPS_LIB=$PWD/paper_2605_27147_b200/libvmps_l512.so timeout 300 $B > $R/lf_512.log 2>&1
