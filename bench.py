@@ -46,8 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-log2", type=int, default=25)
     ap.add_argument("--ref-sample-log2", type=int, default=23)
-    ap.add_argument("--two-level", action="store_true",
-                    help="experimental: two tree levels per merge pass (vmps_test_set_mode)")
+    ap.add_argument("--one-level", action="store_true",
+                    help="A/B: one tree level (2-way merges) per HBM pass instead of two (4-way)")
     ap.add_argument("--leaf-radix", action="store_true",
                     help="experimental: radix-sort leaf engine instead of the block merge sort")
     ap.add_argument("--fuse-z", type=int, default=0, help="experimental: fused-subtree limit Z")
@@ -194,8 +194,8 @@ def main():
     if not os.path.exists(vm.LIB_PATH):
         vbuild.build()
     vm.lib()
-    if args.two_level:
-        vm.test_set_mode(True)
+    if args.one_level:
+        vm.test_set_mode(1)
     if args.leaf_radix:
         vm.test_set_leaf(True)
     if args.fuse_z:
@@ -296,7 +296,10 @@ def main():
                 traffic_src = tj.get("source")
             except Exception:
                 traffic = None
-        roof = {"bound": "hbm", "kernel": "k_merge_level (all level launches of a step)",
+        kname = ("k_merge_level (one tree level per HBM pass; all merge launches of a step)" if args.one_level
+                 else "k4_merge_level (two tree levels, up to 4-way merges, per HBM pass; all merge launches "
+                      "of a step)")
+        roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_unit": "bytes per step (all level-merge launches)",
                 "traffic_source": traffic_src, "peak_source": peak_src,
@@ -305,7 +308,9 @@ def main():
     tree = {"bytes_2wM": 2 * w_bytes * M, "M_over_n": M / n,
             "t_roof_ms_at_peak": 2 * w_bytes * M / (peak * 1e9) * 1000,
             "frac_of_roofline": (2 * w_bytes * M / (peak * 1e9) * 1000) / ms,
-            "fused_M_share": stats["fused_M"] / M if M else 0.0}
+            "fused_M_share": stats["fused_M"] / M if M else 0.0,
+            "hbm_merge_elems": stats["hbm_merge_elems"],
+            "hbm_merge_bytes_over_2wM": (2 * w_bytes * stats["hbm_merge_elems"]) / (2 * w_bytes * M) if M else 0.0}
     ph = {}
     if phases:
         for key in ("plan_ms", "leaf_ms", "partition_ms", "merge_ms", "total_ms"):
@@ -434,6 +439,7 @@ def main():
                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": "u32", "data": "synthetic",
                "config": {"workload": WORKLOAD, "n_per_gpu": n, "n_total": n * world,
+                          "merge_schedule": "one level per pass" if args.one_level else "two levels per pass (4-way)",
                           "key": "u32", "payload": "u32", "scratch": "unbounded",
                           "parallelism": (f"dp{world}: contiguous shards, local sort, exact splitters, "
                                           "NCCL all-to-all, local stable merge") if world > 1 else "single",

@@ -92,6 +92,9 @@ typedef struct {
   uint64_t peak_extra_device_bytes; /* workspace bytes actually used */
   uint64_t scratch_bytes;  /* element scratch part of it */
   uint64_t metadata_bytes; /* plan / table / relocation metadata part of it */
+  uint64_t hbm_merge_elems;/* elements written by the HBM merge passes (sum of the
+                              materialized non-fused node sizes; = M - fused_M with
+                              one level per pass, about half of it with two) */
 } vmps_stats_t;
 
 /* One merge of the plan: [i,j) with [j,k) at node power `power`; `order` is
@@ -193,11 +196,11 @@ int vmps_profile_read(double* h_ms, int cap, uint64_t* h_launches, uint64_t* h_b
  * the paper's rule; otherwise 1..64 forces minrun.  Z (fused-subtree limit),
  * T_out (merge tile) and P_blk (bounded block) = 0 restore defaults. */
 void vmps_test_set_minrun(uint32_t minrun);
-/* two_level = 1: merge two tree levels per HBM pass (only
- * even-depth nodes materialized, up to 4-way merges); 0 (default): one
- * level per pass.  Experimental: at 2^30 the 4-way tiles average ~1K outputs
- * and run slower than two one-level passes. */
-void vmps_test_set_mode(int two_level);
+/* Test hook: merge schedule.  2 (default, also 0): two tree levels per HBM
+ * pass -- only even-depth nodes are materialized and each merges up to four
+ * runs (its grandchildren) in one pass, so every element is read and written
+ * about half as often; 1: one level (one 2-way merge) per pass.  Same output. */
+void vmps_test_set_mode(int levels_per_pass);
 /* Test hook: leaf engine.  0 (default): block merge sort of each leaf batch
  * in shared memory (k_leaf_sort); 1: LSD radix sort (k_leaf_radix, slower at
  * 2^30 cfg5: 29 vs 18 ms).  Same output (a stable sort is unique). */

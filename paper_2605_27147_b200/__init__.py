@@ -41,7 +41,8 @@ class Stats(ctypes.Structure):
                 ("max_power", ctypes.c_uint32), ("levels_executed", ctypes.c_uint32),
                 ("minrun", ctypes.c_uint32), ("block_elems", ctypes.c_uint32),
                 ("rounds", ctypes.c_uint64), ("peak_extra_device_bytes", ctypes.c_uint64),
-                ("scratch_bytes", ctypes.c_uint64), ("metadata_bytes", ctypes.c_uint64)]
+                ("scratch_bytes", ctypes.c_uint64), ("metadata_bytes", ctypes.c_uint64),
+                ("hbm_merge_elems", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {f: int(getattr(self, f)) for f, _ in self._fields_}
@@ -292,9 +293,9 @@ def test_set_minrun(m: int) -> None:
     lib().vmps_test_set_minrun(m)
 
 
-def test_set_mode(two_level: bool = False) -> None:
-    """Test hook: two-level fused merges (experimental) or one level per HBM pass (default)."""
-    lib().vmps_test_set_mode(1 if two_level else 0)
+def test_set_mode(levels_per_pass: int = 2) -> None:
+    """Test hook: tree levels merged per HBM pass, 2 (default, 4-way merges) or 1."""
+    lib().vmps_test_set_mode(int(levels_per_pass))
 
 
 def test_set_leaf(radix: bool = False) -> None:

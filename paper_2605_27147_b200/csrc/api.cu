@@ -25,7 +25,7 @@ static uint32_t g_minrun_override = 0;
 static uint32_t g_fuse_z = 0;
 static uint32_t g_tout = 0;
 static uint32_t g_blk = 0;
-static int g_fuse2 = 0;
+static int g_fuse2 = 1;  // two tree levels per merge pass (default; vmps_test_set_mode(1) = one)
 static int g_leaf_radix = 0;  // test hook vmps_test_set_leaf  // two-level fused merges (opt-in, test hook vmps_test_set_mode)
 static thread_local std::string g_err;
 
@@ -443,7 +443,7 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
 template <bool HV>
 static vmps_status_t bounded_stats(const Work& w, vmps_stats_t* st, cudaStream_t s) {
   if (g_prof && g_prof_host) {
-    VMPS_CK(cudaMemcpyAsync(g_prof_host, w.counters, 16, cudaMemcpyDeviceToHost, s));
+    VMPS_CK(cudaMemcpyAsync(g_prof_host, w.counters, 24, cudaMemcpyDeviceToHost, s));
     g_prof_wbytes = (int)(key_bytes(w.kt) + (HV ? 4 : 0));
   }
   if (!st) return VMPS_OK;
@@ -615,7 +615,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   if (rc != VMPS_OK) return rc;
   g_prof_mark[3] = prof_event(s);
   if (g_prof && g_prof_host) {
-    VMPS_CK(cudaMemcpyAsync(g_prof_host, w.counters, 16, cudaMemcpyDeviceToHost, s));
+    VMPS_CK(cudaMemcpyAsync(g_prof_host, w.counters, 24, cudaMemcpyDeviceToHost, s));
     g_prof_wbytes = (int)(key_bytes(w.kt) + (HV ? 4 : 0));
   }
 
@@ -638,6 +638,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
     st->merges = sc[SC_RUNS] ? sc[SC_RUNS] - 1 : 0;
     st->merge_cost_M = ct[0];
     st->fused_M = ct[1];
+    st->hbm_merge_elems = ct[2];
     st->reversed_elems = sc[SC_REVERSED];
     st->extended_runs = sc[SC_EXTENDED];
     st->max_power = sc[SC_MAXPOW];
@@ -891,15 +892,15 @@ int vmps_profile_read(double* h_ms, int cap, uint64_t* h_launches, uint64_t* h_b
   int k = 0;
   for (; k < cap && k < 5; ++k) h_ms[k] = v[k];
   if (h_bytes && g_prof_host) {
-    unsigned long long M = g_prof_host[0], fM = g_prof_host[1];
-    h_bytes[0] = 2ull * (unsigned long long)g_prof_wbytes * (M - fM);
+    unsigned long long M = g_prof_host[0], fM = g_prof_host[1], hM = g_prof_host[2];
+    h_bytes[0] = 2ull * (unsigned long long)g_prof_wbytes * hM;  // read + write of every HBM merge
     h_bytes[1] = M;
     h_bytes[2] = fM;
   }
   return k;
 }
 
-void vmps_test_set_mode(int two_level) { g_fuse2 = two_level ? 1 : 0; }
+void vmps_test_set_mode(int levels_per_pass) { g_fuse2 = levels_per_pass == 1 ? 0 : 1; }
 
 void vmps_test_set_leaf(int radix) { g_leaf_radix = radix ? 1 : 0; }
 

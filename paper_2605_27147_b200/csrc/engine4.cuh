@@ -303,10 +303,13 @@ __device__ __forceinline__ void merge4_issue(const TileDesc4& d, const TileDesc4
 }
 
 // Step A: P01 = W0 (+) W1 into [0, n01), P23 = W2 (+) W3 into [n01, T4) of
-// the intermediate (keys + the stage index of each value), 8 outputs per
-// thread.  A chunk inside one of the two merges takes the branch-free path
-// over absolute stage indices (a read one past a window stays inside the
-// stage: windows are padded); the chunk holding n01 or T4 goes element-wise.
+// the intermediate (keys + the stage index of each value), KQ outputs per
+// thread.  A chunk inside one of the two merges takes the unrolled
+// branch-free path over absolute stage indices (a read one past a window
+// stays inside the stage: windows are padded).  The chunk holding n01 (and
+// the tile's last chunk) runs each of its parts for exactly its length, so
+// that thread costs about as much as the others (P23's part starts at
+// diagonal 0 and needs no search).
 template <int KT, int KQ>
 __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK, const Merge4Hdr* hp,
                                              uint32_t n01, uint32_t T4, typename KeyTraits<KT>::K* IKs,
@@ -315,27 +318,21 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
   using K = typename T::K;
   const uint32_t q0 = threadIdx.x * (uint32_t)KQ;
   if (q0 >= T4) return;
-  // the chunk's merge(s): [q0, q0+8) meets P01 = [0, n01) and/or P23 = [n01, T4);
-  // each is a branch-free 8-step merge whose stores are predicated
-#pragma unroll 1
-  for (uint32_t part = (q0 < n01 ? 0u : 1u); part < 2u; ++part) {
-    const uint32_t plo = part ? n01 : 0u, phi = part ? T4 : n01;
-    if (q0 >= phi || q0 + (uint32_t)KQ <= plo) continue;
-    const uint32_t wa = 2u * part;
+  const bool inA = q0 + (uint32_t)KQ <= n01, inB = q0 >= n01 && q0 + (uint32_t)KQ <= T4;
+  if (inA || inB) {
+    const uint32_t wa = inA ? 0u : 2u;
     const uint32_t nA = hp->n[wa], nB = hp->n[wa + 1];
     const uint32_t ka0 = hp->kb[wa], kb0 = hp->kb[wa + 1];
     const int32_t dA = (int32_t)hp->vb[wa] - (int32_t)ka0, dB = (int32_t)hp->vb[wa + 1] - (int32_t)kb0;
-    const uint32_t qs = max(q0, plo);
-    const uint32_t d = qs - plo;
+    const uint32_t d = q0 - (inA ? 0u : n01);
     const uint32_t l = corank<KT>(SK + ka0, nA, SK + kb0, nB, d);
     uint32_t ia = ka0 + l, ib = kb0 + d - l;
     const uint32_t ea = ka0 + nA, eb = kb0 + nB;
     K ka = SK[ia], kb = SK[ib];
-    K rk[(uint32_t)KQ];
-    uint32_t ri[(uint32_t)KQ];
+    K rk[KQ];
+    uint32_t ri[KQ];
 #pragma unroll
     for (int q = 0; q < KQ; ++q) {
-      // past both ends (only in a predicated-off tail) the reads stay in the stage
       const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
       rk[q] = pa ? ka : kb;
       ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
@@ -345,19 +342,39 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
       ka = pa ? nx : ka;
       kb = pa ? kb : nx;
     }
-    if (qs == q0 && q0 + (uint32_t)KQ <= phi) {
 #pragma unroll
-      for (int q = 0; q < KQ; ++q) IKs[q0 + q] = rk[q];
+    for (int q = 0; q < KQ; ++q) IKs[q0 + q] = rk[q];
 #pragma unroll
-      for (int q = 0; q < KQ; q += 8)
-        *reinterpret_cast<uint4*>(IIs + q0 + q) = make_uint4(ri[q] | (ri[q + 1] << 16), ri[q + 2] | (ri[q + 3] << 16),
-                                                             ri[q + 4] | (ri[q + 5] << 16), ri[q + 6] | (ri[q + 7] << 16));
-    } else {
-#pragma unroll
-      for (int q = 0; q < KQ; ++q) {
-        const uint32_t pos = qs + q;
-        if (pos < phi && pos < q0 + (uint32_t)KQ) { IKs[pos] = rk[q]; IIs[pos] = (uint16_t)ri[q]; }
-      }
+    for (int q = 0; q < KQ; q += 8)
+      *reinterpret_cast<uint4*>(IIs + q0 + q) = make_uint4(ri[q] | (ri[q + 1] << 16), ri[q + 2] | (ri[q + 3] << 16),
+                                                           ri[q + 4] | (ri[q + 5] << 16), ri[q + 6] | (ri[q + 7] << 16));
+    return;
+  }
+  const uint32_t q1 = min(q0 + (uint32_t)KQ, T4);
+#pragma unroll 1
+  for (uint32_t part = (q0 < n01 ? 0u : 1u); part < 2u; ++part) {
+    const uint32_t plo = part ? n01 : 0u, phi = part ? T4 : n01;
+    const uint32_t qs = max(q0, plo), qe = min(q1, phi);
+    if (qs >= qe) continue;
+    const uint32_t wa = 2u * part;
+    const uint32_t nA = hp->n[wa], nB = hp->n[wa + 1];
+    const uint32_t ka0 = hp->kb[wa], kb0 = hp->kb[wa + 1];
+    const int32_t dA = (int32_t)hp->vb[wa] - (int32_t)ka0, dB = (int32_t)hp->vb[wa + 1] - (int32_t)kb0;
+    const uint32_t d = qs - plo;
+    const uint32_t l = corank<KT>(SK + ka0, nA, SK + kb0, nB, d);
+    uint32_t ia = ka0 + l, ib = kb0 + d - l;
+    const uint32_t ea = ka0 + nA, eb = kb0 + nB;
+    K ka = SK[ia], kb = SK[ib];
+#pragma unroll 1
+    for (uint32_t pos = qs; pos < qe; ++pos) {
+      const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
+      IKs[pos] = pa ? ka : kb;
+      IIs[pos] = (uint16_t)(pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB));
+      ia += pa ? 1u : 0u;
+      ib += pa ? 0u : 1u;
+      const K nx = SK[pa ? ia : ib];
+      ka = pa ? nx : ka;
+      kb = pa ? kb : nx;
     }
   }
 }
@@ -409,14 +426,18 @@ __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IK
     kb = pa ? kb : nx;
   }
   uint32_t rv[(uint32_t)KQ];
-  if (HV) {
-#pragma unroll
-    for (int q = 0; q < KQ; ++q) rv[q] = SV[IIs[min(ri[q], T4 - 1)]];
-  }
   if (qs == start && start + (uint32_t)KQ <= hi) {
+    if (HV) {
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) rv[q] = SV[IIs[ri[q]]];
+    }
     store_chunk_g<KQ>(dk + start, rk);
     if (HV) store_chunk_g<KQ>(dv + start, rv);
   } else {
+    if (HV) {
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) rv[q] = SV[IIs[min(ri[q], T4 - 1)]];
+    }
 #pragma unroll
     for (int q = 0; q < KQ; ++q) {
       const uint32_t pos = qs + q;
@@ -460,7 +481,7 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
       uint32_t it = 0;
       for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
         const uint32_t s = it & 1u;
-        if (it >= 2) mbar_wait(&empty[s], ((it >> 1) - 1) & 1u);
+        if (it >= 2) mbar_wait_backoff(&empty[s], ((it >> 1) - 1) & 1u);
         const TileDesc4 d = tiles[tau];
         TileDesc4 dn;
         const bool same = tau + 1 < count && (dn = tiles[tau + 1], dn.x == d.x);

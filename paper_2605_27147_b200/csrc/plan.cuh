@@ -144,7 +144,7 @@ __global__ void k_class_nodes(const uint32_t* __restrict__ rs, uint32_t* scalars
                               uint32_t fuse_z, uint32_t* __restrict__ unit_end,
                               uint8_t* __restrict__ unit_par, uint32_t* __restrict__ level_cnt, int fuse2) {
   const uint32_t r = scalars[SC_RUNS];
-  unsigned long long m = 0, fm = 0;
+  unsigned long long m = 0, fm = 0, hm = 0;  // M, fused M, elements of HBM merge passes
   uint32_t maxp = 0;
   for (uint32_t t = 1 + blockIdx.x * blockDim.x + threadIdx.x; t < r;
        t += gridDim.x * blockDim.x) {
@@ -163,17 +163,20 @@ __global__ void k_class_nodes(const uint32_t* __restrict__ rs, uint32_t* scalars
       }
     } else if (!fuse2 || (dep[t] & 1u) == 0) {  // two-level mode: only even depths are materialized
       atomicAdd(&level_cnt[p], 1u);
+      hm += size;
     }
   }
   // warp-aggregate the counters
   for (int o = 16; o; o >>= 1) {
     m += __shfl_xor_sync(0xFFFFFFFFu, m, o);
     fm += __shfl_xor_sync(0xFFFFFFFFu, fm, o);
+    hm += __shfl_xor_sync(0xFFFFFFFFu, hm, o);
     maxp = max(maxp, __shfl_xor_sync(0xFFFFFFFFu, maxp, o));
   }
   if ((threadIdx.x & 31) == 0) {
     if (m) atomicAdd(&counters[0], m);
     if (fm) atomicAdd(&counters[1], fm);
+    if (hm) atomicAdd(&counters[2], hm);
     if (maxp) atomicMax(&scalars[SC_MAXPOW], maxp);
   }
 }

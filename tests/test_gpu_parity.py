@@ -112,15 +112,15 @@ def test_random_small_default_tiles(vm, dtype, with_vals):
         check_case(vm, keys, vals, minrun=int(rng.choice([0, 1, 2, 7, 32])))
 
 
-@pytest.mark.parametrize("two_level,leaf_radix", [(True, False), (False, False), (False, True)])
+@pytest.mark.parametrize("levels,leaf_radix", [(2, False), (1, False), (2, True)])
 @pytest.mark.parametrize("dtype", [np.uint32, np.uint64, np.float32])
-def test_random_small_tiny_tiles(vm, dtype, two_level, leaf_radix):
-    """Z = 64 and 16-element merge tiles (two-level sample stride 4): small
-    inputs cross every level path; both merge schedules and both leaf engines
+def test_random_small_tiny_tiles(vm, dtype, levels, leaf_radix):
+    """Z = 64 and 16-element merge tiles: small inputs cross every level path;
+    both merge schedules (1 or 2 tree levels per pass) and both leaf engines
     (a leaf batch then holds ~70 units and spans long leaves' gaps)."""
     rng = np.random.default_rng(200 + (dtype == np.uint64) + 2 * (dtype == np.float32))
     try:
-        vm.test_set_mode(two_level)
+        vm.test_set_mode(levels)
         vm.test_set_leaf(leaf_radix)
         vm.test_set_tiles(64, 16, 0)
         for trial in range(40):
@@ -130,7 +130,7 @@ def test_random_small_tiny_tiles(vm, dtype, two_level, leaf_radix):
             check_case(vm, keys, vals, minrun=int(rng.choice([0, 1, 2, 3, 16])))
     finally:
         vm.test_set_tiles(0, 0, 0)
-        vm.test_set_mode(False)
+        vm.test_set_mode()
         vm.test_set_leaf(False)
 
 
@@ -154,19 +154,19 @@ def test_edge_cases(vm):
         check_case(vm, keys, vals)
 
 
-@pytest.mark.parametrize("two_level,leaf_radix", [(True, False), (False, False), (False, True)])
+@pytest.mark.parametrize("levels,leaf_radix", [(2, False), (1, False), (2, True)])
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
-def test_configs_reduced_size_vs_oracle(vm, cfg, two_level, leaf_radix):
+def test_configs_reduced_size_vs_oracle(vm, cfg, levels, leaf_radix):
     """Each BASELINE.json config shape at 2^18 (many merge levels), full oracle
     compare, both merge schedules and both leaf engines."""
     vm.test_set_tiles(0, 0, 0)
-    vm.test_set_mode(two_level)
+    vm.test_set_mode(levels)
     vm.test_set_leaf(leaf_radix)
     try:
         k, v = W.make(cfg, n=1 << 18, device="cpu")
         check_case(vm, W.to_numpy(k), None if v is None else W.to_numpy(v))
     finally:
-        vm.test_set_mode(False)
+        vm.test_set_mode()
         vm.test_set_leaf(False)
 
 
