@@ -114,7 +114,36 @@ struct InnerCR {
   }
   __device__ __forceinline__ void know_low(uint32_t x, uint32_t c) { xl = x; cl = c; }
   __device__ __forceinline__ void know_high(uint32_t x, uint32_t c) { xh = x; ch = c; }
+  // search bounds of co(x)
+  __device__ __forceinline__ void bounds(uint32_t x, uint32_t* lo, uint32_t* hi) const {
+    uint32_t l = max(cl, ch > xh - x ? ch - (xh - x) : 0u);
+    uint32_t h = min(ch, cl + (x - xl));
+    *lo = max(l, x > nB ? x - nB : 0u);
+    *hi = min(h, min(x, nA));
+  }
 };
+
+// co(x) of L and co(y) of R as one interleaved loop: the two binary searches
+// are independent, so their probes overlap (half the dependent latency).
+template <int KT>
+__device__ __forceinline__ void co_pair(const InnerCR<KT>& L, uint32_t x, const InnerCR<KT>& R, uint32_t y,
+                                        uint32_t* cx, uint32_t* cy) {
+  using T = KeyTraits<KT>;
+  uint32_t la, ha, lb, hb;
+  L.bounds(x, &la, &ha);
+  R.bounds(y, &lb, &hb);
+  while (la < ha || lb < hb) {
+    const uint32_t ma = (la + ha) >> 1, mb = (lb + hb) >> 1;
+    const bool ga = la < ha, gb = lb < hb;
+    bool pa = false, pb = false;
+    if (ga) pa = T::ord(L.A[ma]) <= T::ord(L.B[x - ma - 1]);
+    if (gb) pb = T::ord(R.A[mb]) <= T::ord(R.B[y - mb - 1]);
+    if (ga) { if (pa) la = ma + 1; else ha = ma; }
+    if (gb) { if (pb) lb = mb + 1; else hb = mb; }
+  }
+  *cx = la;
+  *cy = lb;
+}
 
 // Split of X's first d outputs; the outer co-rank a lies in [alo, ahi]
 // (caller's bound, e.g. from the previous aligned boundary).  On return c[]
@@ -132,9 +161,9 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
   ahi = min(ahi, min(d, nL));
   while (alo < ahi) {
     const uint32_t mid = (alo + ahi) >> 1;
-    const uint32_t cL = L.co(mid);
     const uint32_t r = d - mid - 1;  // < nR since mid >= d - nR
-    const uint32_t cR = R.co(r);
+    uint32_t cL, cR;
+    co_pair<KT>(L, mid, R, r, &cL, &cR);
     if (T::ord(L.elem(mid, cL)) <= T::ord(R.elem(r, cR))) {  // L[mid] precedes R[d-mid-1]
       alo = mid + 1;
       L.know_low(mid, cL);
@@ -146,7 +175,8 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
     }
   }
   const uint32_t a = alo;
-  const uint32_t c0 = L.co(a), c2 = R.co(d - a);
+  uint32_t c0, c2;
+  co_pair<KT>(L, a, R, d - a, &c0, &c2);
   L.know_low(a, c0);
   R.know_low(d - a, c2);
   c[0] = c0; c[1] = a - c0; c[2] = c2; c[3] = d - a - c2;

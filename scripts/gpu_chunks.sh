@@ -1,5 +1,6 @@
 cd $GRAFT_REPO_ROOT
 R=gpurun_out
-B="python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline --bounded-reps 0 --two-level"
-timeout 300 $B > $R/ch_2.log 2>&1
-for c in 1 4 8; do VMPS_LIB=$PWD/paper_2605_27147_b200/libvmps_c$c.so timeout 300 $B > $R/ch_$c.log 2>&1; done
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "tiny_tiles or reduced or full_size" > $R/q_tests.log 2>&1; echo "tests=$?" > $R/q_status.txt
+B="python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline --bounded-reps 0"
+timeout 300 $B > $R/ch_8.log 2>&1
+for c in 4 16; do VMPS_LIB=$PWD/paper_2605_27147_b200/libvmps_c$c.so timeout 300 $B > $R/ch_$c.log 2>&1; done

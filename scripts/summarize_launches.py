@@ -11,7 +11,7 @@ for r in d:
     v *= {'nsecond': 1e-6, 'ns': 1e-6, 'usecond': 1e-3, 'us': 1e-3, 'msecond': 1.0, 'ms': 1.0}.get(r[ui], 1e-6)
     agg[name][0] += 1
     agg[name][1] += v
-ours = {k: v for k, v in agg.items() if k.startswith('k_')}
+ours = {k: v for k, v in agg.items() if k.startswith('k_') or k.startswith('k4_')}
 tot = sum(v[1] for v in ours.values())
 print(f'{"kernel":34s} {"launches":>8s} {"ms":>10s} {"share":>7s}')
 for k, (c, t) in sorted(ours.items(), key=lambda x: -x[1][1]):
