@@ -519,9 +519,13 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   uint32_t* v0 = vals;
   uint32_t* v1 = w.v1;
   const size_t lsm = leaf_smem_bytes<KT>(HV);
+  const size_t lsm2 = leaf_smem_bytes<KT, LEAF_SMALL>(HV);
   const size_t rsm = LeafRadixSmem<KT>::BYTES;
   if (!kernel_attrs_set[KT][HV]) {
-    VMPS_CK(cudaFuncSetAttribute(k_leaf_sort<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    VMPS_CK(cudaFuncSetAttribute(k_leaf_sort<KT, HV, LEAF_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lsm));
+    VMPS_CK(cudaFuncSetAttribute(k_leaf_sort<KT, HV, LEAF_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)lsm2));
     VMPS_CK(cudaFuncSetAttribute(k_leaf_radix<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
     kernel_attrs_set[KT][HV] = true;
   }
@@ -535,8 +539,12 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   LAUNCH(k_batch_first, grid_for(nbatch + 1), 256, 0, s, w.unit_flag, w.unit_idx, w.scalars, nbatch, w.batch_first);
   if (g_leaf_radix)
     LAUNCH((k_leaf_radix<KT, HV>), nbatch, LEAF_THREADS, rsm, s, k0, v0, k1, v1, w.units, w.batch_first);
-  else
-    LAUNCH((k_leaf_sort<KT, HV>), nbatch, LEAF_THREADS, lsm, s, k0, v0, k1, v1, w.units, w.batch_first, w.fuse_z);
+  else {
+    LAUNCH((k_leaf_sort<KT, HV, LEAF_SMALL>), nbatch, LEAF_SMALL, lsm2, s, k0, v0, k1, v1, w.units, w.batch_first,
+           w.fuse_z);
+    LAUNCH((k_leaf_sort<KT, HV, LEAF_THREADS>), nbatch, LEAF_THREADS, lsm, s, k0, v0, k1, v1, w.units,
+           w.batch_first, w.fuse_z);
+  }
   LAUNCH((k_long_leaves<KT, HV>), nsm() * 8, 256, 0, s, k0, v0, k1, v1, w.longs, w.long_off, w.scalars,
          LONG_CHUNK);
   rc = launch_check();

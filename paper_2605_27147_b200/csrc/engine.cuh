@@ -30,6 +30,8 @@ constexpr int LEAF_THREADS = VMPS_LEAF_THREADS;
 constexpr int LEAF_K = VMPS_LEAF_K;               // odd: conflict-free chunk stride
 constexpr int LEAF_CAP = LEAF_THREADS * LEAF_K;   // 4224 >= 2Z - 1 (a batch holds < 2Z)
 static_assert(LEAF_CAP >= 2 * (int)MAX_FUSE_Z - 1, "leaf capacity");
+constexpr int LEAF_SMALL = LEAF_THREADS / 2;          // half-size CTA for small batches
+constexpr int LEAF_SMALL_CAP = LEAF_SMALL * LEAF_K;   // 2112 >= Z: any single unit fits
 
 template <int KT>
 __device__ __forceinline__ uint32_t corank(const typename KeyTraits<KT>::K* A, uint32_t nA,
@@ -49,30 +51,34 @@ __device__ __forceinline__ uint32_t corank(const typename KeyTraits<KT>::K* A, u
 // distinct banks without padding.  Shared memory carries keys and 16-bit
 // local indices (ping-pong); payloads are gathered once at the end.  Rounds
 // whose pairs fit inside one warp's range synchronise with __syncwarp only.
-template <int KT, bool HV>
-__global__ void __launch_bounds__(LEAF_THREADS, VMPS_LEAF_MINB) k_leaf_sort(
+template <int KT, bool HV, int LT>
+__global__ void __launch_bounds__(LT, VMPS_LEAF_MINB * (LEAF_THREADS / LT)) k_leaf_sort(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
     const uint32_t* __restrict__ units, const uint32_t* __restrict__ batch_first, uint32_t fuse_z) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
+  constexpr int NTH = LT, CAP = LT * LEAF_K;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  K* const skb = reinterpret_cast<K*>(smem_raw);                          // 2 x LEAF_CAP keys
-  uint16_t* const sib = reinterpret_cast<uint16_t*>(skb + 2 * LEAF_CAP);  // 2 x LEAF_CAP indices
-  uint32_t* ubits = reinterpret_cast<uint32_t*>(sib + 2 * LEAF_CAP);      // unit-start bitmap
-  uint32_t* upre = ubits + LEAF_CAP / 32 + 1;  // exclusive popcount prefix per word
-  uint32_t* pcar = upre + LEAF_CAP / 32 + 1;   // parity of the unit open at each word's end
-  uint32_t* pbits = pcar + LEAF_CAP / 32 + 1;  // parity bit at each unit start
+  K* const skb = reinterpret_cast<K*>(smem_raw);                          // 2 x CAP keys
+  uint16_t* const sib = reinterpret_cast<uint16_t*>(skb + 2 * CAP);  // 2 x CAP indices
+  uint32_t* ubits = reinterpret_cast<uint32_t*>(sib + 2 * CAP);      // unit-start bitmap
+  uint32_t* upre = ubits + CAP / 32 + 1;  // exclusive popcount prefix per word
+  uint32_t* pcar = upre + CAP / 32 + 1;   // parity of the unit open at each word's end
+  uint32_t* pbits = pcar + CAP / 32 + 1;  // parity bit at each unit start
 
-  // units of batch b (contiguous, < Zb + Z <= LEAF_CAP elements)
+  // units of batch b (contiguous, < Zb + Z <= CAP elements)
   const uint32_t x0 = batch_first[blockIdx.x], x1 = batch_first[blockIdx.x + 1];
   if (x0 >= x1) return;
   const uint32_t bstart = units[3 * x0];
   const uint32_t E = units[3 * (x1 - 1) + 1] - bstart;
+  // size classes: a batch that fits the half-size CTA goes to it (few idle
+  // warps); a third, quarter-size class measured slower (one more launch)
+  if (E > (uint32_t)CAP || (LT == LEAF_THREADS && E <= (uint32_t)LEAF_SMALL_CAP)) return;
   const uint32_t nwords = (E + 31) / 32;
-  for (uint32_t w = threadIdx.x; w < nwords; w += LEAF_THREADS) { ubits[w] = 0u; pbits[w] = 0u; }
+  for (uint32_t w = threadIdx.x; w < nwords; w += NTH) { ubits[w] = 0u; pbits[w] = 0u; }
   __syncthreads();
-  for (uint32_t x = x0 + threadIdx.x; x < x1; x += LEAF_THREADS) {
+  for (uint32_t x = x0 + threadIdx.x; x < x1; x += NTH) {
     const uint32_t q = units[3 * x] - bstart;
     atomicOr(&ubits[q >> 5], 1u << (q & 31u));
     if (units[3 * x + 2]) atomicOr(&pbits[q >> 5], 1u << (q & 31u));
@@ -153,10 +159,10 @@ __global__ void __launch_bounds__(LEAF_THREADS, VMPS_LEAF_MINB) k_leaf_sort(
   // [m, min(x+2w, end))); everything else is copied in place.
   uint32_t cur = 0;
   for (uint32_t w = LEAF_K; w < E; w <<= 1) {
-    const K* sk = skb + cur * LEAF_CAP;
-    const uint16_t* si = sib + cur * LEAF_CAP;
-    K* dk = skb + (cur ^ 1u) * LEAF_CAP;
-    uint16_t* di = sib + (cur ^ 1u) * LEAF_CAP;
+    const K* sk = skb + cur * CAP;
+    const uint16_t* si = sib + cur * CAP;
+    K* dk = skb + (cur ^ 1u) * CAP;
+    uint16_t* di = sib + (cur ^ 1u) * CAP;
     if (q0 < E) {
       const uint32_t q1 = min(q0 + LEAF_K, E);
       const uint32_t x = (q0 / (2 * w)) * (2 * w), m = x + w;
@@ -251,21 +257,21 @@ __global__ void __launch_bounds__(LEAF_THREADS, VMPS_LEAF_MINB) k_leaf_sort(
   // Phase 3: keys from shared memory, payloads gathered by local index (read
   // all before writing: the payload gather may be in place), each unit to its
   // parity buffer.
-  const K* sk = skb + cur * LEAF_CAP;
-  const uint16_t* si = sib + cur * LEAF_CAP;
-  constexpr int PER = LEAF_CAP / LEAF_THREADS;
+  const K* sk = skb + cur * CAP;
+  const uint16_t* si = sib + cur * CAP;
+  constexpr int PER = CAP / NTH;
   uint32_t gv[PER];
   if (HV) {
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
-      const uint32_t q = threadIdx.x + r * LEAF_THREADS;
+      const uint32_t q = threadIdx.x + r * NTH;
       gv[r] = q < E ? v0[bstart + si[q]] : 0u;
     }
     __syncthreads();
   }
 #pragma unroll
   for (int r = 0; r < PER; ++r) {
-    const uint32_t q = threadIdx.x + r * LEAF_THREADS;
+    const uint32_t q = threadIdx.x + r * NTH;
     if (q < E) {
       const uint32_t w = q >> 5;
       const uint32_t mk = ubits[w] & (0xFFFFFFFFu >> (31u - (q & 31u)));
@@ -276,11 +282,12 @@ __global__ void __launch_bounds__(LEAF_THREADS, VMPS_LEAF_MINB) k_leaf_sort(
   }
 }
 
-template <int KT>
+template <int KT, int LT = LEAF_THREADS>
 inline size_t leaf_smem_bytes(bool hv) {
   using K = typename KeyTraits<KT>::K;
   (void)hv;
-  return 2 * LEAF_CAP * (sizeof(K) + 2) + 4 * (LEAF_CAP / 32 + 1) * 4 + 16;
+  constexpr int CAP = LT * LEAF_K;
+  return 2 * CAP * (sizeof(K) + 2) + 4 * (CAP / 32 + 1) * 4 + 16;
 }
 
 // Leaf batches: consecutive units that start in the same window of Zb
