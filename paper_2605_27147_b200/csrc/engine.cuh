@@ -52,10 +52,10 @@ __device__ __forceinline__ uint32_t corank(const typename KeyTraits<KT>::K* A, u
 // local indices (ping-pong); payloads are gathered once at the end.  Rounds
 // whose pairs fit inside one warp's range synchronise with __syncwarp only.
 template <int KT, bool HV, int LT>
-__global__ void __launch_bounds__(LT, VMPS_LEAF_MINB * (LEAF_THREADS / LT)) k_leaf_sort(
+__device__ __forceinline__ void leaf_sort_batch(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
-    const uint32_t* __restrict__ units, const uint32_t* __restrict__ batch_first, uint32_t fuse_z) {
+    const uint32_t* __restrict__ units, const uint32_t* __restrict__ batch_first, uint32_t b) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
   constexpr int NTH = LT, CAP = LT * LEAF_K;
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(LT, VMPS_LEAF_MINB * (LEAF_THREADS / LT)) k_le
   uint32_t* pbits = pcar + CAP / 32 + 1;  // parity bit at each unit start
 
   // units of batch b (contiguous, < Zb + Z <= CAP elements)
-  const uint32_t x0 = batch_first[blockIdx.x], x1 = batch_first[blockIdx.x + 1];
+  const uint32_t x0 = batch_first[b], x1 = batch_first[b + 1];
   if (x0 >= x1) return;
   const uint32_t bstart = units[3 * x0];
   const uint32_t E = units[3 * (x1 - 1) + 1] - bstart;
@@ -282,6 +282,27 @@ __global__ void __launch_bounds__(LT, VMPS_LEAF_MINB * (LEAF_THREADS / LT)) k_le
   }
 }
 
+// Persistent CTAs take batches from a work queue (atomic counter per size
+// class), so every resident CTA stays busy and no CTA is launched per empty
+// slot of the batch bound.
+template <int KT, bool HV, int LT>
+__global__ void __launch_bounds__(LT, VMPS_LEAF_MINB * (LEAF_THREADS / LT)) k_leaf_sort(
+    typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
+    typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
+    const uint32_t* __restrict__ units, const uint32_t* __restrict__ batch_first, uint32_t* scalars) {
+  __shared__ uint32_t s_b;
+  const uint32_t nb = scalars[SC_NBATCH];
+  uint32_t* q = scalars + (LT == LEAF_THREADS ? SC_LEAFQ1 : SC_LEAFQ);
+  for (;;) {
+    if (threadIdx.x == 0) s_b = atomicAdd(q, 1u);
+    __syncthreads();
+    const uint32_t b = s_b;
+    if (b >= nb) break;
+    leaf_sort_batch<KT, HV, LT>(k0, v0, k1, v1, units, batch_first, b);
+    __syncthreads();  // shared memory (and s_b) are reused by the next batch
+  }
+}
+
 template <int KT, int LT = LEAF_THREADS>
 inline size_t leaf_smem_bytes(bool hv) {
   using K = typename KeyTraits<KT>::K;
@@ -309,9 +330,10 @@ __global__ void k_batch_flags(const uint32_t* __restrict__ units, const uint32_t
 // batch_first[b] = first unit of batch b; batch_first[b] = nunits for every
 // b >= the batch count up to bcap (those CTAs exit at once).
 __global__ void k_batch_first(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ idx,
-                              const uint32_t* scalars, uint32_t bcap, uint32_t* __restrict__ batch_first) {
+                              uint32_t* scalars, uint32_t bcap, uint32_t* __restrict__ batch_first) {
   const uint32_t nunits = scalars[SC_UNITS];
   const uint32_t nb = idx[nunits];
+  if (blockIdx.x == 0 && threadIdx.x == 0) scalars[SC_NBATCH] = nb;
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < nunits; x += gridDim.x * blockDim.x)
     if (flag[x]) batch_first[idx[x]] = x;
   for (uint32_t b = nb + blockIdx.x * blockDim.x + threadIdx.x; b <= bcap; b += gridDim.x * blockDim.x)

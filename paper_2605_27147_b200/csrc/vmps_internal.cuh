@@ -66,6 +66,9 @@ enum Scalar : int {
   SC_EXTENDED,        // extended runs
   SC_LEVEL_TILES,     // scratch for per-level tile count
   SC_ERROR,           // internal consistency error flag
+  SC_NBATCH,          // leaf batches
+  SC_LEAFQ,           // leaf work queues (2 slots: one per CTA size class)
+  SC_LEAFQ1,
   SC_COUNT = 16
 };
 constexpr int LEVEL_SLOTS = 72;  // powers 0..70
