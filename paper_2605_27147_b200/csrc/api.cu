@@ -237,6 +237,17 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
   return off;
 }
 
+// Internal non-blocking stream (per device) used to capture CUDA graphs.
+constexpr int MAX_DEV = 16;
+static cudaStream_t g_aux[MAX_DEV];
+static cudaStream_t aux_stream() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= MAX_DEV) return nullptr;
+  if (!g_aux[dev] && cudaStreamCreateWithFlags(&g_aux[dev], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  return g_aux[dev];
+}
+constexpr int BD_GRAPH_ROUNDS = 48;  // bounded-mode rounds per graph launch
+
 static int g_nsm = 0;
 static int nsm() {
   if (!g_nsm) {
@@ -382,6 +393,32 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
   LAUNCH(k_bd_init, gNB, 256, 0, s, st, w.pool, w.Tin, w.NB, w.F);
   TileDesc* desc = (TileDesc*)w.bdesc;
   BdState hs;
+  // The round kernels take all their state from device memory, so a batch of
+  // rounds is captured once (on an internal stream; the caller's may be the
+  // legacy stream, which cannot be captured) and replayed on `s`.
+  cudaGraph_t rounds_graph = nullptr;
+  cudaGraphExec_t rounds_exec = nullptr;
+  if (!debug_sync()) {
+    cudaStream_t cap = aux_stream();
+    bool ok = cap && cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      for (int q = 0; q < BD_GRAPH_ROUNDS; ++q) {
+        k_bd_alloc<<<1, 32, 0, cap>>>(st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
+        k_bd_merge<KT, HV><<<nsm() * 4, MERGE_BLOCK, 0, cap>>>(M, st, desc, w.Tin, w.Tout, w.pool, w.remain);
+      }
+      ok = cudaStreamEndCapture(cap, &rounds_graph) == cudaSuccess &&
+           cudaGraphInstantiate(&rounds_exec, rounds_graph, 0) == cudaSuccess;
+    }
+    if (!ok) {  // fall back to direct launches
+      cudaGetLastError();
+      if (rounds_exec) cudaGraphExecDestroy(rounds_exec);
+      rounds_exec = nullptr;
+    }
+  }
+  struct GraphGuard {
+    cudaGraph_t& g; cudaGraphExec_t& e;
+    ~GraphGuard() { if (e) cudaGraphExecDestroy(e); if (g) cudaGraphDestroy(g); }
+  } guard{rounds_graph, rounds_exec};
   for (int p = p_hi; p >= 1; --p) {
     LAUNCH(k_bd_flags, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.fuse_z, p, w.rmax,
            w.bflag);
@@ -405,11 +442,17 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
     scan_u32(w.dirty, w.didx, w.NB + 1, w.scan_tmp, s);
     LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, grid_for(total)), 256, 0, s, M, desc, w.btoff, w.bm, w.dirty,
            w.didx, w.dlist, w.first_tile, w.remain, w.bD);
-    // rounds until every dirty block of the level is produced
+    // rounds until every dirty block of the level is produced; a batch of
+    // rounds is one CUDA graph launch (rounds past the end are no-ops)
     for (;;) {
-      for (int q = 0; q < 16; ++q) {
-        LAUNCH(k_bd_alloc, 1, 32, 0, s, st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
-        LAUNCH((k_bd_merge<KT, HV>), nsm() * 4, MERGE_BLOCK, 0, s, M, st, desc, w.Tin, w.Tout, w.pool, w.remain);
+      if (rounds_exec) {
+        VMPS_CK(cudaGraphLaunch(rounds_exec, s));
+        g_nl += 2 * BD_GRAPH_ROUNDS;
+      } else {
+        for (int q = 0; q < 16; ++q) {
+          LAUNCH(k_bd_alloc, 1, 32, 0, s, st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
+          LAUNCH((k_bd_merge<KT, HV>), nsm() * 4, MERGE_BLOCK, 0, s, M, st, desc, w.Tin, w.Tout, w.pool, w.remain);
+        }
       }
       uint32_t D = 0;
       VMPS_CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
