@@ -403,7 +403,7 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
     bool ok = cap && cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     if (ok) {
       for (int q = 0; q < BD_GRAPH_ROUNDS; ++q) {
-        k_bd_alloc<<<1, 32, 0, cap>>>(st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
+        k_bd_alloc<<<1, 1024, 0, cap>>>(st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
         k_bd_merge<KT, HV><<<nsm() * 4, MERGE_BLOCK, 0, cap>>>(M, st, desc, w.Tin, w.Tout, w.pool, w.remain);
       }
       ok = cudaStreamEndCapture(cap, &rounds_graph) == cudaSuccess &&
@@ -450,7 +450,7 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
         g_nl += 2 * BD_GRAPH_ROUNDS;
       } else {
         for (int q = 0; q < 16; ++q) {
-          LAUNCH(k_bd_alloc, 1, 32, 0, s, st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
+          LAUNCH(k_bd_alloc, 1, 1024, 0, s, st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
           LAUNCH((k_bd_merge<KT, HV>), nsm() * 4, MERGE_BLOCK, 0, s, M, st, desc, w.Tin, w.Tout, w.pool, w.remain);
         }
       }

@@ -207,20 +207,36 @@ __global__ void k_bd_dirty_list(BdMem<KT> M, const TileDesc* __restrict__ desc, 
 
 // --- rounds -----------------------------------------------------------------
 // Allocate free physical blocks to the next dirty output blocks (one thread).
-__global__ void k_bd_alloc(BdState* st, const uint32_t* __restrict__ dlist, const uint32_t* __restrict__ first_tile,
-                           const uint32_t* __restrict__ D_ptr, uint32_t* __restrict__ pool,
-                           uint32_t* __restrict__ Tout, uint32_t max_take) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const uint32_t D = *D_ptr;
-  if (st->err || st->w >= D) { st->tile_lo = st->tile_hi = 0; return; }
-  uint32_t take = min(min(st->pool_count, D - st->w), max_take);
-  if (take == 0) { st->err = 1; st->tile_lo = st->tile_hi = 0; return; }
-  for (uint32_t x = 0; x < take; ++x) Tout[dlist[st->w + x]] = pool[st->pool_count - 1 - x];
-  st->pool_count -= take;
-  st->tile_lo = first_tile[st->w];
-  st->tile_hi = first_tile[st->w + take];
-  st->w += take;
-  st->rounds++;
+__global__ void __launch_bounds__(1024) k_bd_alloc(BdState* st, const uint32_t* __restrict__ dlist,
+                                                   const uint32_t* __restrict__ first_tile,
+                                                   const uint32_t* __restrict__ D_ptr, uint32_t* __restrict__ pool,
+                                                   uint32_t* __restrict__ Tout, uint32_t max_take) {
+  // one block: thread 0 decides how many dirty output blocks this round
+  // takes, all threads map them to free physical blocks in parallel
+  __shared__ uint32_t s_take, s_w, s_pc;
+  if (threadIdx.x == 0) {
+    const uint32_t D = *D_ptr;
+    uint32_t take = 0;
+    if (st->err || st->w >= D) {
+      st->tile_lo = st->tile_hi = 0;
+    } else {
+      take = min(min(st->pool_count, D - st->w), max_take);
+      if (take == 0) { st->err = 1; st->tile_lo = st->tile_hi = 0; }
+    }
+    s_take = take;
+    s_w = st->w;
+    s_pc = st->pool_count;
+  }
+  __syncthreads();
+  const uint32_t take = s_take, w = s_w, pc = s_pc;
+  for (uint32_t x = threadIdx.x; x < take; x += blockDim.x) Tout[dlist[w + x]] = pool[pc - 1 - x];
+  if (threadIdx.x == 0 && take) {
+    st->pool_count = pc - take;
+    st->tile_lo = first_tile[w];
+    st->tile_hi = first_tile[w + take];
+    st->w = w + take;
+    st->rounds++;
+  }
 }
 
 __device__ __forceinline__ void bd_release(BdState* st, uint32_t* pool, uint32_t* remain, const uint32_t* Tin,
