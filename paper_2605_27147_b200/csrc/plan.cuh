@@ -47,11 +47,13 @@ __global__ void k_powers_seg(const uint32_t* __restrict__ rs, uint32_t n, const 
     uint32_t p = node_power(n, rs[t - 1], rs[t], rs[t + 1], &c);
     power[t] = (uint8_t)p;
     const uint32_t q = p - 1;
+    // s_u 2^q >= c 2n  <=>  s_u >= ceil(c 2n / 2^q), with s_u = rs[u] + rs[u+1]
+    // (both thresholds < 2^34: c < 2^q); the loops compare 64-bit sums only
     const u128 N2 = (u128)(2ull * n);
-    const u128 lo_thr = (u128)c * N2, hi_thr = (u128)(c + 1) * N2;
-    auto mid_scaled = [&](uint32_t u) -> u128 {
-      return ((u128)((uint64_t)rs[u] + (uint64_t)rs[u + 1])) << q;
-    };
+    const u128 one = 1;
+    const uint64_t lo_thr = (uint64_t)(((u128)c * N2 + (one << q) - 1) >> q);
+    const uint64_t hi_thr = (uint64_t)(((u128)(c + 1) * N2 + (one << q) - 1) >> q);
+    auto mid_scaled = [&](uint32_t u) -> uint64_t { return (uint64_t)rs[u] + (uint64_t)rs[u + 1]; };
     // L = smallest u in [0, t-1] with mid(u) 2^q >= c 2n (run t-1 qualifies)
     int64_t good = (int64_t)t - 1, bad = -1;
     for (int64_t step = 1;; step <<= 1) {

@@ -252,18 +252,59 @@ __device__ __forceinline__ void long_masks(const uint32_t* sb, uint32_t w, uint3
   la[w] = window_and_m(nb, m);
 }
 
+// minrun == 32 (every n = 2^k >= 64): a short run at x = 32 w + b hands over
+// to 32 (w + 1) + b, the same bit of the next bitmap word.  stop[b] is a
+// 128-bit mask over the tile's words of the positions 32 w + b where that
+// stops (a long run, or a run reaching the tile's end: x + 32 >= L), built
+// by warp ballots (a transpose of the per-word stop masks), so a walker skips
+// a whole stretch of short runs with one find-first-set.
+__device__ __forceinline__ void stop_masks32(const uint32_t* sb, const uint32_t* la, const uint32_t* ld, uint32_t L,
+                                             uint32_t* ts) {
+  const uint32_t w = threadIdx.x, lane = w & 31u, k = w >> 5;  // one thread per word
+  const uint32_t dw = (sb[w] >> 1) | (sb[w + 1] << 31);        // bit b: descent at 32 w + b + 1
+  uint32_t st = (dw & ld[w]) | (~dw & la[w]);
+  const int lim = (int)L - 32 - (int)(32 * w);                  // bits b >= lim have x + 32 >= L
+  if (lim <= 0) st = 0xFFFFFFFFu;
+  else if (lim < 32) st |= 0xFFFFFFFFu << lim;
+#pragma unroll 4
+  for (uint32_t b = 0; b < 32; ++b) {
+    const uint32_t v = __ballot_sync(0xFFFFFFFFu, (st >> b) & 1u);
+    if (lane == b) ts[4 * b + k] = v;
+  }
+}
+// first word >= w whose bit b is a stop (128 if none)
+__device__ __forceinline__ uint32_t next_stop32(const uint32_t* ts, uint32_t b, uint32_t w) {
+  for (uint32_t k = w >> 5; k < 4; ++k) {
+    uint32_t v = ts[4 * b + k];
+    if (k == (w >> 5)) v &= 0xFFFFFFFFu << (w & 31u);
+    if (v) return 32 * k + (uint32_t)(__ffs(v) - 1);
+  }
+  return 128;
+}
+
 // Walk the chain from in-tile run start x (T0 + x < n) until it leaves the
 // tile; returns the exit state, counts the starts visited and, if MARK, sets
 // them in `startb`.  ExtractRun, P:399 / P:756, reading R3.
+// With ts (minrun == 32) stretches of short runs are skipped in O(1).
 template <bool MARK>
 __device__ __forceinline__ uint32_t tile_walk_fast(const uint32_t* sb, const uint32_t* la, const uint32_t* ld,
                                                    const uint16_t* fs, const uint16_t* fc, uint32_t T0,
                                                    uint32_t L, uint32_t n, uint32_t m, uint32_t x,
-                                                   uint32_t* cnt, uint32_t* startb) {
+                                                   uint32_t* cnt, uint32_t* startb, const uint32_t* ts = nullptr) {
   const bool last_tile = T0 + L >= n;
   uint32_t c = 0;
   uint32_t out;
   for (;;) {
+    if (ts) {  // skip the short runs at bit b up to the next stop
+      const uint32_t b = x & 31u, w = x >> 5;
+      const uint32_t w2 = next_stop32(ts, b, w);
+      if (w2 > w && w2 < 128) {
+        c += w2 - w;
+        if (MARK)
+          for (uint32_t ww = w; ww < w2; ++ww) startb[ww] |= 1u << b;
+        x = 32 * w2 + b;
+      }
+    }
     ++c;
     if (MARK) startb[x >> 5] |= 1u << (x & 31u);
     if (T0 + x + 1 >= n) { out = ST_END; break; }
@@ -296,6 +337,7 @@ __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT
   __shared__ uint32_t la[RT_WORDS], ld[RT_WORDS];
   __shared__ uint16_t fs[RT_WORDS + 2], fc[RT_WORDS + 2];
   __shared__ uint32_t wres[MAX_MINRUN + 2];
+  __shared__ uint32_t ts[32 * 4];
   static_assert(RT_WORDS == 128, "one thread per bitmap word");
   const uint32_t tile = blockIdx.x;
   const uint32_t T0 = tile * RT;
@@ -307,6 +349,11 @@ __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT
   if (warp == 0) tile_suffix_tables(sb, L, fs, fc, lane);
   long_masks(sb, threadIdx.x, minrun, la, ld);
   __syncthreads();
+  const bool m32 = minrun == 32;
+  if (m32) {
+    stop_masks32(sb, la, ld, L, ts);
+    __syncthreads();
+  }
   const uint32_t d_asc = fs[0], d_desc = fc[0];
   TileCtx c{sb, T0, L, n, minrun};
   for (uint32_t w = threadIdx.x; w < minrun + 2; w += blockDim.x) {
@@ -316,7 +363,8 @@ __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT
       res = ST_END << 24;  // unused / not reachable
     } else {
       uint32_t cnt = 0;
-      const uint32_t v = tile_walk_fast<false>(sb, la, ld, fs, fc, T0, L, n, minrun, x, &cnt, nullptr);
+      const uint32_t v = tile_walk_fast<false>(sb, la, ld, fs, fc, T0, L, n, minrun, x, &cnt, nullptr,
+                                               m32 ? ts : nullptr);
       res = (v << 24) | cnt;
     }
     wres[w] = res;
@@ -426,6 +474,7 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
   __shared__ uint16_t fs[RT_WORDS + 2], fc[RT_WORDS + 2];
   __shared__ uint32_t startb[RT_WORDS];
   __shared__ uint32_t la[RT_WORDS], ld[RT_WORDS];
+  __shared__ uint32_t ts[32 * 4];
   __shared__ uint32_t wsum[4];
   __shared__ uint32_t s_idx0, s_total, s_rev;
   const uint32_t tile = blockIdx.x;
@@ -442,6 +491,11 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
   if (warp == 0) tile_suffix_tables(sb, L, fs, fc, lane);
   long_masks(sb, threadIdx.x, minrun, la, ld);
   __syncthreads();
+  const bool m32 = minrun == 32;
+  if (m32) {
+    stop_masks32(sb, la, ld, L, ts);
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     TileCtx c{sb, T0, L, n, minrun};
     const uint64_t e = entry[tile];
@@ -449,7 +503,8 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
     uint32_t x, out, rev_open, cnt = 0;
     bool ended;
     if (resolve_entry(c, st, fs[0], fc[0], &x, &out, &rev_open)) {
-      ended = tile_walk_fast<true>(sb, la, ld, fs, fc, T0, L, n, minrun, x, &cnt, startb) == ST_END;
+      ended = tile_walk_fast<true>(sb, la, ld, fs, fc, T0, L, n, minrun, x, &cnt, startb, m32 ? ts : nullptr) ==
+              ST_END;
     } else {
       ended = (st != ST_END) && out == ST_END;
     }
