@@ -358,19 +358,49 @@ __global__ void __launch_bounds__(256) k_long_leaves(
     const uint32_t len = e - s;
     const bool desc = f & 2u, odd = f & 1u;
     const uint32_t base = (c - long_off[a]) * chunk;
+    // U independent elements per thread in flight (loads first, then stores)
+    constexpr int U = 8;
     if (desc && !odd) {  // in-place reversal in buffer 0
       const uint32_t half = len / 2, lim = min(base + chunk, half);
-      for (uint32_t q = base + threadIdx.x; q < lim; q += blockDim.x) {
-        K x = k0[s + q], y = k0[e - 1 - q];
-        k0[s + q] = y; k0[e - 1 - q] = x;
-        if (HV) { uint32_t vx = v0[s + q], vy = v0[e - 1 - q]; v0[s + q] = vy; v0[e - 1 - q] = vx; }
+      for (uint32_t q0 = base + threadIdx.x; q0 < lim; q0 += U * blockDim.x) {
+        K x[U], y[U];
+        uint32_t vx[U], vy[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t q = q0 + u * blockDim.x;
+          if (q < lim) {
+            x[u] = k0[s + q]; y[u] = k0[e - 1 - q];
+            if (HV) { vx[u] = v0[s + q]; vy[u] = v0[e - 1 - q]; }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t q = q0 + u * blockDim.x;
+          if (q < lim) {
+            k0[s + q] = y[u]; k0[e - 1 - q] = x[u];
+            if (HV) { v0[s + q] = vy[u]; v0[e - 1 - q] = vx[u]; }
+          }
+        }
       }
     } else {
       const uint32_t lim = min(base + chunk, len);
-      for (uint32_t q = base + threadIdx.x; q < lim; q += blockDim.x) {
-        uint32_t src = desc ? e - 1 - q : s + q;
-        k1[s + q] = k0[src];
-        if (HV) v1[s + q] = v0[src];
+      for (uint32_t q0 = base + threadIdx.x; q0 < lim; q0 += U * blockDim.x) {
+        K x[U];
+        uint32_t vx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t q = q0 + u * blockDim.x;
+          if (q < lim) {
+            const uint32_t src = desc ? e - 1 - q : s + q;
+            x[u] = k0[src];
+            if (HV) vx[u] = v0[src];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t q = q0 + u * blockDim.x;
+          if (q < lim) { k1[s + q] = x[u]; if (HV) v1[s + q] = vx[u]; }
+        }
       }
     }
   }
