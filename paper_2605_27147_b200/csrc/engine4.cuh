@@ -476,6 +476,58 @@ __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IK
   }
 }
 
+// A tile whose runs are W0 and W2 only: merge them straight from the stage
+// (absolute stage indices; a read one past a window stays in the stage).
+template <int KT, bool HV, int KQ>
+__device__ __forceinline__ void merge4_direct(const typename KeyTraits<KT>::K* SK, const uint32_t* SV,
+                                              const Merge4Hdr* hp, uint32_t lo, uint32_t hi, uint32_t par,
+                                              typename KeyTraits<KT>::K* k0, uint32_t* v0,
+                                              typename KeyTraits<KT>::K* k1, uint32_t* v1) {
+  using T = KeyTraits<KT>;
+  using K = typename T::K;
+  const uint32_t start = (lo & ~(uint32_t)(KQ - 1)) + threadIdx.x * KQ;
+  if (!(start < hi && start + (uint32_t)KQ > lo)) return;
+  K* dk = par ? k1 : k0;
+  uint32_t* dv = par ? v1 : v0;
+  const uint32_t nA = hp->n[0], nB = hp->n[2];
+  const uint32_t ka0 = hp->kb[0], kb0 = hp->kb[2];
+  const int32_t dA = (int32_t)hp->vb[0] - (int32_t)ka0, dB = (int32_t)hp->vb[2] - (int32_t)kb0;
+  const uint32_t qs = max(start, lo);
+  const uint32_t d = qs - lo;
+  const uint32_t l = corank<KT>(SK + ka0, nA, SK + kb0, nB, d);
+  uint32_t ia = ka0 + l, ib = kb0 + d - l;
+  const uint32_t ea = ka0 + nA, eb = kb0 + nB;
+  K ka = SK[ia], kb = SK[ib];
+  K rk[KQ];
+  uint32_t ri[KQ];
+#pragma unroll
+  for (int q = 0; q < KQ; ++q) {
+    const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
+    rk[q] = pa ? ka : kb;
+    ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
+    ia += pa ? 1u : 0u;
+    ib += pa ? 0u : 1u;
+    const K nx = SK[pa ? ia : ib];
+    ka = pa ? nx : ka;
+    kb = pa ? kb : nx;
+  }
+  if (qs == start && start + (uint32_t)KQ <= hi) {
+    store_chunk_g<KQ>(dk + start, rk);
+    if (HV) {
+      uint32_t rv[KQ];
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) rv[q] = SV[ri[q]];
+      store_chunk_g<KQ>(dv + start, rv);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const uint32_t pos = qs + q;
+      if (pos < hi && pos < start + (uint32_t)KQ) { dk[pos] = rk[q]; if (HV) dv[pos] = SV[ri[q]]; }
+    }
+  }
+}
+
 // The fused merge: persistent CTAs; 16 consumer warps merge, one producer
 // warp loads descriptors and issues the bulk copies of the next tile into
 // the free stage (full / empty mbarrier pairs), so no consumer ever waits on
@@ -531,12 +583,20 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
     const uint32_t* SV = reinterpret_cast<const uint32_t*>(st + SM::KB);
     const uint32_t lo = hp->lo, hi = hp->hi, par = hp->par;
     const uint32_t n01 = hp->n[0] + hp->n[1], T4 = hi - lo;
-    merge4_stepA<KT, KQ>(SK, hp, n01, T4, IKs, IIs);
-    named_bar_sync(1, NT);
-    merge4_stepB<KT, HV, KQ>(IKs, IIs, SV, lo, hi, par, n01, T4, k0, v0, k1, v1);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);  // stage s is free once every warp is past step B
-    named_bar_sync(1, NT);        // the intermediate is reused by the next tile
+    if (hp->n[1] == 0 && hp->n[3] == 0) {
+      // both children are single runs (leaves / units): one 2-way merge
+      // straight from the stage, no intermediate
+      merge4_direct<KT, HV, KQ>(SK, SV, hp, lo, hi, par, k0, v0, k1, v1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    } else {
+      merge4_stepA<KT, KQ>(SK, hp, n01, T4, IKs, IIs);
+      named_bar_sync(1, NT);
+      merge4_stepB<KT, HV, KQ>(IKs, IIs, SV, lo, hi, par, n01, T4, k0, v0, k1, v1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // stage s is free once every warp is past step B
+      named_bar_sync(1, NT);        // the intermediate is reused by the next tile
+    }
   }
 }
 
