@@ -325,7 +325,7 @@ def main():
     e2e = None
     if not args.no_e2e and world == 1:
         NS = 3
-        ks = max(NS, min(max(args.steps, 6), 8))
+        ks = max(NS, min(max(args.steps, 8), 12))
         hk = torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)
         hv = torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)
         hk.copy_(keys0)
