@@ -258,7 +258,7 @@ struct Merge4Smem {
 struct Merge4Hdr {
   uint32_t kb[4], n[4];  // key element offset / count of each window in the stage
   uint32_t vb[4];        // value element offset of each window
-  uint32_t lo, hi, par, pad;
+  uint32_t lo, hi, par, mode;  // mode: 0 general, 1 two runs (W0, W2), 2 + w single run w
 };
 static_assert(64 + 2 * sizeof(Merge4Hdr) <= 512, "merge4 header area");
 
@@ -313,7 +313,11 @@ __device__ __forceinline__ void merge4_issue(const TileDesc4& d, const TileDesc4
   h.lo = R.b[0] + d.rank;
   h.hi = R.b[0] + rank1;
   h.par = R.par;
-  h.pad = 0;
+  {  // tile class, decided once by the producer
+    const uint32_t nz = (h.n[0] != 0) + (h.n[1] != 0) + (h.n[2] != 0) + (h.n[3] != 0);
+    h.mode = nz == 1 ? 2u + (h.n[0] ? 0u : h.n[1] ? 1u : h.n[2] ? 2u : 3u)
+                     : ((h.n[1] == 0 && h.n[3] == 0) ? 1u : 0u);
+  }
   hdr[s] = h;
   mbar_arrive_expect_tx(&bars[s], total);
   uint32_t o = 0;
@@ -476,6 +480,35 @@ __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IK
   }
 }
 
+// A tile fed by a single window: copy it (keys and values) to the output.
+template <int KT, bool HV, int KQ>
+__device__ __forceinline__ void merge4_copy(const typename KeyTraits<KT>::K* SK, const uint32_t* SV, uint32_t kb,
+                                            uint32_t vb, uint32_t lo, uint32_t hi, uint32_t par,
+                                            typename KeyTraits<KT>::K* k0, uint32_t* v0,
+                                            typename KeyTraits<KT>::K* k1, uint32_t* v1) {
+  using K = typename KeyTraits<KT>::K;
+  const uint32_t start = (lo & ~(uint32_t)(KQ - 1)) + threadIdx.x * KQ;
+  if (!(start < hi && start + (uint32_t)KQ > lo)) return;
+  K* dk = par ? k1 : k0;
+  uint32_t* dv = par ? v1 : v0;
+  if (start >= lo && start + (uint32_t)KQ <= hi) {
+    K rk[KQ];
+    uint32_t rv[KQ];
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      rk[q] = SK[kb + (start - lo) + q];
+      if (HV) rv[q] = SV[vb + (start - lo) + q];
+    }
+    store_chunk_g<KQ>(dk + start, rk);
+    if (HV) store_chunk_g<KQ>(dv + start, rv);
+  } else {
+    for (uint32_t pos = max(start, lo); pos < min(start + (uint32_t)KQ, hi); ++pos) {
+      dk[pos] = SK[kb + (pos - lo)];
+      if (HV) dv[pos] = SV[vb + (pos - lo)];
+    }
+  }
+}
+
 // A tile whose runs are W0 and W2 only: merge them straight from the stage
 // (absolute stage indices; a read one past a window stays in the stage).
 template <int KT, bool HV, int KQ>
@@ -583,7 +616,15 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
     const uint32_t* SV = reinterpret_cast<const uint32_t*>(st + SM::KB);
     const uint32_t lo = hp->lo, hi = hp->hi, par = hp->par;
     const uint32_t n01 = hp->n[0] + hp->n[1], T4 = hi - lo;
-    if (hp->n[1] == 0 && hp->n[3] == 0) {
+    const uint32_t mode = hp->mode;
+    if (mode >= 2) {
+      // run-skip tile: every output comes from one run, so
+      // the tile is a compare-free copy of that window
+      const uint32_t wsrc = mode - 2;
+      merge4_copy<KT, HV, KQ>(SK, SV, hp->kb[wsrc], hp->vb[wsrc], lo, hi, par, k0, v0, k1, v1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    } else if (mode == 1) {
       // both children are single runs (leaves / units): one 2-way merge
       // straight from the stage, no intermediate
       merge4_direct<KT, HV, KQ>(SK, SV, hp, lo, hi, par, k0, v0, k1, v1);
