@@ -165,6 +165,47 @@ vmps_status_t vmps_merge_plan(const void* keys, uint64_t n, vmps_key_t kt, uint6
 vmps_status_t vmps_count_rank(const void* keys, uint64_t n, vmps_key_t kt, const uint64_t* probes,
                               uint32_t nprobe, uint64_t* out_lt, uint64_t* out_le, void* stream);
 
+/* ---- distributed merge plan ----
+ * The plan of the concatenation of g shards (rank q holds keys[off_q,
+ * off_q + n_q) of the global array) is Alg. 1's plan of the whole array with
+ * the global n (reading R15/C13).  Building blocks, one call per
+ * rank, composed by paper_2605_27147_b200.dist.merge_plan_dist:
+ *
+ * vmps_shard_chain: the shard's transfer table of the run-detection chain
+ * (ExtractRun, P:399 / P:756, with the global minrun): for every chain state
+ * s at the shard start (START(o) = o, ASC(f) = minrun + f, DESC(f) = 2 minrun
+ * + f, o, f < minrun; END = 255), d_table[s] = (state at the shard end << 32)
+ * | runs started inside the shard.  n_end = the global n minus the shard's
+ * offset (where the chain ends, relative to the shard start), or 0xFFFFFFFF
+ * if that is >= 2^32 - 1.  d_prev: device pointer to the previous shard's last
+ * key (NULL for shard 0); d_halo: the next n_halo <= 136 keys of the global
+ * array after this shard (>= minrun + 2 of them unless the array ends
+ * sooner), so runs crossing the shard end are classified exactly.  d_table:
+ * device, 3 minrun u64.  n_local < 2^32 - 256.
+ *
+ * vmps_shard_runs: with the chain state at the shard start (composition of the
+ * previous shards' tables from START(0)), writes the shard's `count` run
+ * starts (global positions offset + local, u64) and kinds (VMPS_RUN_* bits)
+ * to device arrays.  count = d_table[entry_state] & 0xFFFFFFFF.
+ *
+ * Workspace for both: vmps_shard_workspace_bytes(n_local, kt, minrun).
+ *
+ * vmps_plan_from_runs: the merge plan (r - 1 records in Alg. 1's execution
+ * order, as vmps_merge_plan) of an array of n keys whose r runs start at
+ * d_run_start[0..r) (64-bit global positions, d_run_start[r] = n).  Workspace:
+ * vmps_plan_workspace_bytes(r).  Synchronises `stream`. */
+vmps_status_t vmps_shard_workspace_bytes(uint64_t n_local, vmps_key_t kt, uint32_t minrun, size_t* h_bytes);
+vmps_status_t vmps_shard_chain(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun, uint32_t n_end,
+                               const void* d_prev, const void* d_halo, uint32_t n_halo, uint64_t* d_table,
+                               void* ws, size_t ws_bytes, void* stream);
+vmps_status_t vmps_shard_runs(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun, uint32_t n_end,
+                              const void* d_prev, const void* d_halo, uint32_t n_halo, uint32_t entry_state,
+                              uint64_t count, uint64_t offset, uint64_t* d_run_start, uint8_t* d_run_kind, void* ws,
+                              size_t ws_bytes, void* stream);
+vmps_status_t vmps_plan_workspace_bytes(uint64_t r, size_t* h_bytes);
+vmps_status_t vmps_plan_from_runs(const uint64_t* d_run_start, uint64_t r, uint64_t n, vmps_merge_rec_t* d_merges,
+                                  void* ws, size_t ws_bytes, void* stream);
+
 /* vmps_merge_runs: keys[0,n) (and vals, if non-NULL) consist of nruns adjacent
  * runs, each sorted, starting at h_run_start[0] = 0 < h_run_start[1] < ...
  * (host array).  Merges them in place into the stable sort of the array,

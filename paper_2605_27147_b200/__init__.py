@@ -57,7 +57,9 @@ EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_me
            "vmps_count_rank", "vmps_merge_runs_workspace_bytes", "vmps_merge_runs",
            "vmps_status_string", "vmps_last_error", "vmps_profile_enable", "vmps_profile_read",
            "vmps_test_set_minrun", "vmps_test_set_tiles", "vmps_test_set_mode",
-           "vmps_test_set_leaf", "vmps_sort_keys_host", "vmps_sort_pairs_host")
+           "vmps_test_set_leaf", "vmps_sort_keys_host", "vmps_sort_pairs_host",
+           "vmps_shard_workspace_bytes", "vmps_shard_chain", "vmps_shard_runs", "vmps_plan_workspace_bytes",
+           "vmps_plan_from_runs")
 
 _lib = None
 
@@ -77,6 +79,15 @@ def lib() -> ctypes.CDLL:
         L.vmps_sort_keys_host.argtypes = [vp, vp, u64, ctypes.c_int, i64, vp, vp, sz, vp, ctypes.POINTER(Stats)]
         L.vmps_sort_pairs_host.argtypes = [vp, vp, vp, vp, u64, ctypes.c_int, i64, vp, vp, vp, sz, vp,
                                            ctypes.POINTER(Stats)]
+        u32, ci = ctypes.c_uint32, ctypes.c_int
+        L.vmps_shard_workspace_bytes.argtypes = [u64, ci, u32, ctypes.POINTER(sz)]
+        L.vmps_shard_chain.argtypes = [vp, u64, ci, u32, u32, vp, vp, u32, vp, vp, sz, vp]
+        L.vmps_shard_runs.argtypes = [vp, u64, ci, u32, u32, vp, vp, u32, u32, u64, u64, vp, vp, vp, sz, vp]
+        L.vmps_plan_workspace_bytes.argtypes = [u64, ctypes.POINTER(sz)]
+        L.vmps_plan_from_runs.argtypes = [vp, u64, u64, vp, vp, sz, vp]
+        for f in ("vmps_shard_workspace_bytes", "vmps_shard_chain", "vmps_shard_runs", "vmps_plan_workspace_bytes",
+                  "vmps_plan_from_runs"):
+            getattr(L, f).restype = ctypes.c_int
         L.vmps_merge_plan.argtypes = [vp, u64, ctypes.c_int, vp, vp, vp, u64, ctypes.POINTER(u64),
                                       vp, sz, vp]
         L.vmps_count_rank.argtypes = [vp, u64, ctypes.c_int, vp, ctypes.c_uint32, vp, vp, vp]
@@ -268,6 +279,80 @@ def merge_plan(keys: torch.Tensor, workspace: Workspace | None = None) -> Plan:
     power = (recs[:, 3] & 0xFFFFFFFF)
     merges = torch.stack([recs[:, 0], recs[:, 1], recs[:, 2], power], dim=1)
     return Plan(rs[:r], rk[:r], merges)
+
+
+def minrun_for(n: int) -> int:
+    """The paper's minrun rule: halve n (rounding up) until it is < 64."""
+    m = n
+    while m >= 64:
+        m = (m + 1) // 2
+    return max(m, 1)
+
+
+def shard_chain(keys: torch.Tensor, minrun: int, n_end: int, prev: torch.Tensor | None = None,
+                halo: torch.Tensor | None = None, workspace: Workspace | None = None) -> torch.Tensor:
+    """vmps_shard_chain: the shard's run-detection transfer table, 3 minrun
+    int64 values (exit state << 32 | runs started) on the keys' device."""
+    kt = key_type(keys)
+    dev = keys.device
+    L = lib()
+    nb = ctypes.c_size_t(0)
+    _check(L.vmps_shard_workspace_bytes(keys.numel(), kt, minrun, ctypes.byref(nb)), "vmps_shard_workspace_bytes")
+    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    buf = ws.get(int(nb.value), dev)
+    tab = torch.empty(3 * minrun, dtype=torch.int64, device=dev)
+    nh = 0 if halo is None else halo.numel()
+    with torch.cuda.device(dev):
+        rc = L.vmps_shard_chain(keys.data_ptr(), keys.numel(), kt, minrun, min(n_end, 0xFFFFFFFF),
+                                None if prev is None else prev.data_ptr(), None if nh == 0 else halo.data_ptr(),
+                                nh, tab.data_ptr(), buf.data_ptr(), buf.numel(), _stream_ptr(dev))
+    _check(rc, "vmps_shard_chain")
+    return tab
+
+
+def shard_runs(keys: torch.Tensor, minrun: int, n_end: int, entry_state: int, count: int, offset: int,
+               prev: torch.Tensor | None = None, halo: torch.Tensor | None = None, out: torch.Tensor | None = None,
+               workspace: Workspace | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """vmps_shard_runs: the shard's `count` run starts (global int64 positions,
+    written into `out` if given) and run kinds (uint8)."""
+    kt = key_type(keys)
+    dev = keys.device
+    L = lib()
+    nb = ctypes.c_size_t(0)
+    _check(L.vmps_shard_workspace_bytes(keys.numel(), kt, minrun, ctypes.byref(nb)), "vmps_shard_workspace_bytes")
+    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    buf = ws.get(int(nb.value), dev)
+    rs = out if out is not None else torch.empty(max(count, 1), dtype=torch.int64, device=dev)
+    rk = torch.empty(max(count, 1), dtype=torch.uint8, device=dev)
+    nh = 0 if halo is None else halo.numel()
+    with torch.cuda.device(dev):
+        rc = L.vmps_shard_runs(keys.data_ptr(), keys.numel(), kt, minrun, min(n_end, 0xFFFFFFFF),
+                               None if prev is None else prev.data_ptr(), None if nh == 0 else halo.data_ptr(),
+                               nh, entry_state, count, offset, rs.data_ptr(), rk.data_ptr(), buf.data_ptr(),
+                               buf.numel(), _stream_ptr(dev))
+    _check(rc, "vmps_shard_runs")
+    return rs[:count], rk[:count]
+
+
+def plan_from_runs(run_start: torch.Tensor, n: int, workspace: Workspace | None = None) -> torch.Tensor:
+    """vmps_plan_from_runs: Alg. 1's merge records (r - 1, 4) = (i, j, k, power)
+    for the r runs whose int64 starts are run_start[0..r) and run_start[r] = n."""
+    r = run_start.numel() - 1
+    dev = run_start.device
+    if r < 2:
+        return torch.empty((0, 4), dtype=torch.int64, device=dev)
+    L = lib()
+    nb = ctypes.c_size_t(0)
+    _check(L.vmps_plan_workspace_bytes(r, ctypes.byref(nb)), "vmps_plan_workspace_bytes")
+    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    buf = ws.get(int(nb.value), dev)
+    mg = torch.empty((r - 1) * 4, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        rc = L.vmps_plan_from_runs(run_start.data_ptr(), r, n, mg.data_ptr(), buf.data_ptr(), buf.numel(),
+                                   _stream_ptr(dev))
+    _check(rc, "vmps_plan_from_runs")
+    recs = mg.view(-1, 4)
+    return torch.stack([recs[:, 0], recs[:, 1], recs[:, 2], recs[:, 3] & 0xFFFFFFFF], dim=1)
 
 
 def profile_enable(on: bool = True) -> None:

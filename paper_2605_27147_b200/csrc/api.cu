@@ -342,7 +342,8 @@ static vmps_status_t front_half(const Work& w, const void* keys, cudaStream_t s)
   if (arc != VMPS_OK) return arc;
   VMPS_CK(cudaMemsetAsync(w.scalars, 0, SC_COUNT * 4, s));
   VMPS_CK(cudaMemsetAsync(w.counters, 0, 8 * 8, s));
-  LAUNCH(k_runs_tables<KT>, w.ntiles, 128, 0, s, (const K*)keys, w.n, w.minrun, w.ns, w.bits, w.tile_tab);
+  LAUNCH(k_runs_tables<KT>, w.ntiles, 128, 0, s, (const K*)keys, w.n, w.minrun, w.ns, w.bits, w.tile_tab, w.n,
+         (const K*)nullptr, (const K*)nullptr, 0u);
   // compose the chain of tile tables (level 0 = u32 tile tables, above = u64)
   const size_t sm32 = (size_t)CHAIN_G * w.ns * 4, sm64 = (size_t)CHAIN_G * w.ns * 8;
   for (int l = 0; l < w.chain_levels; ++l) {
@@ -354,9 +355,9 @@ static vmps_status_t front_half(const Work& w, const void* keys, cudaStream_t s)
   }
   const int top = w.chain_levels;
   if (top == 0)
-    LAUNCH(k_chain_top<uint32_t>, 1, 32, 0, s, w.tile_tab, w.chain_m[0], w.ns, w.chain_entry[0]);
+    LAUNCH(k_chain_top<uint32_t>, 1, 32, 0, s, w.tile_tab, w.chain_m[0], w.ns, w.chain_entry[0], 0u);
   else
-    LAUNCH(k_chain_top<uint64_t>, 1, 32, 0, s, w.chain_tab[top - 1], w.chain_m[top], w.ns, w.chain_entry[top]);
+    LAUNCH(k_chain_top<uint64_t>, 1, 32, 0, s, w.chain_tab[top - 1], w.chain_m[top], w.ns, w.chain_entry[top], 0u);
   for (int l = top - 1; l >= 0; --l) {
     if (l == 0)
       LAUNCH(k_chain_expand<uint32_t>, w.chain_m[1], 256, sm32, s, w.tile_tab, w.chain_m[0], w.ns,
@@ -366,9 +367,9 @@ static vmps_status_t front_half(const Work& w, const void* keys, cudaStream_t s)
              w.chain_entry[l + 1], w.chain_entry[l]);
   }
   LAUNCH(k_runs_emit, w.ntiles, 128, 0, s, w.bits, w.n, w.minrun, w.chain_entry[0], w.run_start, w.run_kind,
-         w.scalars);
+         w.scalars, w.n, 0u);
   const unsigned g = grid_for(w.rmax);
-  LAUNCH(k_powers_seg, g, 256, 0, s, w.run_start, w.n, w.scalars, w.power, w.seg_l, w.seg_r);
+  LAUNCH(k_powers_seg<uint32_t>, g, 256, 0, s, w.run_start, (uint64_t)w.n, w.scalars, w.power, w.seg_l, w.seg_r);
   LAUNCH(k_parent_init, g, 256, 0, s, w.scalars, w.power, w.seg_l, w.seg_r, w.parent, w.anc[0], w.dep[0]);
   // depth <= max power <= 34 < 64: six rounds of pointer jumping (result in dep[0])
   for (int rnd = 0; rnd < 6; ++rnd) {
@@ -708,6 +709,47 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
 
 using namespace vmps;
 
+namespace vmps {
+// ---- distributed plan building blocks ----
+// Run detection of one shard of a larger array: the chain's entry state at
+// the shard start comes from the caller (composition of the previous shards'
+// tables), END only at the global end (n_end), descent bits across the shard
+// edges from *d_prev (previous shard's last key) and d_halo (the next keys).
+template <int KT>
+static vmps_status_t shard_front(const Work& w, const void* keys, uint32_t n_end, const void* d_prev,
+                                 const void* d_halo, uint32_t n_halo, cudaStream_t s) {
+  using K = typename KeyTraits<KT>::K;
+  vmps_status_t arc = chain_attrs();
+  if (arc != VMPS_OK) return arc;
+  VMPS_CK(cudaMemsetAsync(w.scalars, 0, SC_COUNT * 4, s));
+  LAUNCH(k_runs_tables<KT>, w.ntiles, 128, 0, s, (const K*)keys, w.n, w.minrun, w.ns, w.bits, w.tile_tab, n_end,
+         (const K*)d_prev, (const K*)d_halo, n_halo);
+  const size_t sm32 = (size_t)CHAIN_G * w.ns * 4, sm64 = (size_t)CHAIN_G * w.ns * 8;
+  for (int l = 0; l < w.chain_levels; ++l) {
+    if (l == 0)
+      LAUNCH(k_chain_compose<uint32_t>, w.chain_m[1], 256, sm32, s, w.tile_tab, w.chain_m[0], w.ns, w.chain_tab[0]);
+    else
+      LAUNCH(k_chain_compose<uint64_t>, w.chain_m[l + 1], 256, sm64, s, w.chain_tab[l - 1], w.chain_m[l], w.ns,
+             w.chain_tab[l]);
+  }
+  return launch_check();
+}
+
+// Shard-local u32 run starts -> global u64 positions.
+__global__ void k_shard_starts(const uint32_t* __restrict__ local, uint64_t count, uint64_t offset,
+                               uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = offset + local[i];
+}
+
+template <int KT>
+static vmps_status_t shard_dispatch_front(const Work& w, const void* keys, uint32_t n_end, const void* d_prev,
+                                          const void* d_halo, uint32_t n_halo, cudaStream_t s) {
+  return shard_front<KT>(w, keys, n_end, d_prev, d_halo, n_halo, s);
+}
+
+}  // namespace vmps
+
 static vmps_status_t check_common(const void* keys, const void* vals, uint64_t n, vmps_key_t kt) {
   if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) {
     g_err = "unknown key type";
@@ -898,12 +940,163 @@ vmps_status_t vmps_merge_plan(const void* keys, uint64_t n, vmps_key_t kt, uint6
   VMPS_CK(cudaStreamSynchronize(s));
   if (h_num_runs) *h_num_runs = r;
   if (r > cap_runs) { g_err = "cap_runs too small"; return VMPS_ERR_INVALID_ARG; }
-  k_plan_records<<<grid_for(r), 256, 0, s>>>(w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.dep[0],
+  k_plan_records<uint32_t><<<grid_for(r), 256, 0, s>>>(w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.dep[0],
                                              w.run_kind, run_start, run_kind, merges);
   rc = launch_check();
   if (rc != VMPS_OK) return rc;
   VMPS_CK(cudaStreamSynchronize(s));
   return VMPS_OK;
+}
+
+static bool shard_args_ok(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun, uint32_t n_halo) {
+  if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) { g_err = "unknown key type"; return false; }
+  if (n_local < 1 || n_local >= (1ull << 32) - 256 || !keys) {
+    g_err = "shard: need 1 <= n_local < 2^32 - 256 keys";
+    return false;
+  }
+  if (minrun < 1 || minrun > MAX_MINRUN) { g_err = "shard: minrun out of range"; return false; }
+  if (n_halo > 2 * MAX_MINRUN + 8) { g_err = "shard: halo too long"; return false; }
+  if ((uintptr_t)keys & 15) { g_err = "keys must be 16-byte aligned"; return false; }
+  return true;
+}
+
+static Cfg shard_cfg(uint64_t n_local, vmps_key_t kt, uint32_t minrun) {
+  Cfg c = make_cfg(n_local, kt, -1);
+  c.minrun = minrun;
+  return c;
+}
+
+vmps_status_t vmps_shard_workspace_bytes(uint64_t n_local, vmps_key_t kt, uint32_t minrun, size_t* h_bytes) {
+  if (!h_bytes || n_local < 1 || n_local >= (1ull << 32) - 256 || minrun < 1 || minrun > MAX_MINRUN)
+    return VMPS_ERR_INVALID_ARG;
+  *h_bytes = carve(shard_cfg(n_local, kt, minrun), nullptr, nullptr) + 256;
+  return VMPS_OK;
+}
+
+static vmps_status_t shard_setup(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun,
+                                 uint32_t n_end, uint32_t n_halo, void* ws, size_t ws_bytes, Work* w) {
+  if (!shard_args_ok(keys, n_local, kt, minrun, n_halo)) return VMPS_ERR_INVALID_ARG;
+  if (n_end < n_local) { g_err = "shard: n_end < n_local"; return VMPS_ERR_INVALID_ARG; }
+  const Cfg c = shard_cfg(n_local, kt, minrun);
+  const size_t need = carve(c, nullptr, nullptr);
+  char* base = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  if (!ws || (size_t)(base - (char*)ws) + need > ws_bytes) { g_err = "workspace too small"; return VMPS_ERR_BUDGET; }
+  carve(c, w, base);
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_shard_chain(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun, uint32_t n_end,
+                               const void* d_prev, const void* d_halo, uint32_t n_halo, uint64_t* d_table,
+                               void* ws, size_t ws_bytes, void* stream) {
+  Work w;
+  vmps_status_t rc = shard_setup(keys, n_local, kt, minrun, n_end, n_halo, ws, ws_bytes, &w);
+  if (rc != VMPS_OK) return rc;
+  if (!d_table) { g_err = "table output is NULL"; return VMPS_ERR_INVALID_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (kt) {
+    case VMPS_KEY_U32: rc = shard_dispatch_front<VMPS_KEY_U32>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
+    case VMPS_KEY_U64: rc = shard_dispatch_front<VMPS_KEY_U64>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
+    default: rc = shard_dispatch_front<VMPS_KEY_F32>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
+  }
+  if (rc != VMPS_OK) return rc;
+  const int top = w.chain_levels;
+  if (top == 0) k_chain_all<uint32_t><<<1, 256, 0, s>>>(w.tile_tab, w.chain_m[0], w.ns, d_table);
+  else k_chain_all<uint64_t><<<1, 256, 0, s>>>(w.chain_tab[top - 1], w.chain_m[top], w.ns, d_table);
+  return launch_check();
+}
+
+vmps_status_t vmps_shard_runs(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun, uint32_t n_end,
+                              const void* d_prev, const void* d_halo, uint32_t n_halo, uint32_t entry_state,
+                              uint64_t count, uint64_t offset, uint64_t* d_run_start, uint8_t* d_run_kind, void* ws,
+                              size_t ws_bytes, void* stream) {
+  Work w;
+  vmps_status_t rc = shard_setup(keys, n_local, kt, minrun, n_end, n_halo, ws, ws_bytes, &w);
+  if (rc != VMPS_OK) return rc;
+  if (entry_state > ST_END || (entry_state != ST_END && entry_state >= 3 * minrun)) {
+    g_err = "shard: bad entry state";
+    return VMPS_ERR_INVALID_ARG;
+  }
+  if (count > w.rmax || (count && (!d_run_start || !d_run_kind))) { g_err = "shard: bad run count"; return VMPS_ERR_INVALID_ARG; }
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (kt) {
+    case VMPS_KEY_U32: rc = shard_dispatch_front<VMPS_KEY_U32>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
+    case VMPS_KEY_U64: rc = shard_dispatch_front<VMPS_KEY_U64>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
+    default: rc = shard_dispatch_front<VMPS_KEY_F32>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
+  }
+  if (rc != VMPS_OK) return rc;
+  const int top = w.chain_levels;
+  const size_t sm32 = (size_t)CHAIN_G * w.ns * 4, sm64 = (size_t)CHAIN_G * w.ns * 8;
+  if (top == 0)
+    LAUNCH(k_chain_top<uint32_t>, 1, 32, 0, s, w.tile_tab, w.chain_m[0], w.ns, w.chain_entry[0], entry_state);
+  else
+    LAUNCH(k_chain_top<uint64_t>, 1, 32, 0, s, w.chain_tab[top - 1], w.chain_m[top], w.ns, w.chain_entry[top],
+           entry_state);
+  for (int l = top - 1; l >= 0; --l) {
+    if (l == 0)
+      LAUNCH(k_chain_expand<uint32_t>, w.chain_m[1], 256, sm32, s, w.tile_tab, w.chain_m[0], w.ns,
+             w.chain_entry[1], w.chain_entry[0]);
+    else
+      LAUNCH(k_chain_expand<uint64_t>, w.chain_m[l + 1], 256, sm64, s, w.chain_tab[l - 1], w.chain_m[l], w.ns,
+             w.chain_entry[l + 1], w.chain_entry[l]);
+  }
+  LAUNCH(k_runs_emit, w.ntiles, 128, 0, s, w.bits, w.n, w.minrun, w.chain_entry[0], w.run_start, w.run_kind,
+         w.scalars, n_end, n_halo);
+  if (count) {
+    LAUNCH(k_shard_starts, grid_for(count), 256, 0, s, w.run_start, count, offset, d_run_start);
+    VMPS_CK(cudaMemcpyAsync(d_run_kind, w.run_kind, count, cudaMemcpyDeviceToDevice, s));
+  }
+  return launch_check();
+}
+
+// The merge plan of an array given its run starts (64-bit positions, r + 1
+// entries with run_start[r] = n): powers, tree, Alg. 1 order -- the back half
+// of vmps_merge_plan, for run lists assembled from shards (n may exceed 2^32).
+vmps_status_t vmps_plan_workspace_bytes(uint64_t r, size_t* h_bytes) {
+  if (!h_bytes || r >= (1ull << 32) - 8) return VMPS_ERR_INVALID_ARG;
+  const size_t R = (size_t)r + 2;
+  *h_bytes = 256 * 10 + R * (1 + 4 * 7) + SC_COUNT * 4 + 64;
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_plan_from_runs(const uint64_t* d_run_start, uint64_t r, uint64_t n, vmps_merge_rec_t* d_merges,
+                                  void* ws, size_t ws_bytes, void* stream) {
+  size_t need = 0;
+  if (vmps_plan_workspace_bytes(r, &need) != VMPS_OK || r < 1 || n < r || !d_run_start) {
+    g_err = "plan_from_runs: bad arguments";
+    return VMPS_ERR_INVALID_ARG;
+  }
+  if (r >= 2 && !d_merges) { g_err = "plan_from_runs: merges is NULL"; return VMPS_ERR_INVALID_ARG; }
+  if (!ws || ws_bytes < need) { g_err = "workspace too small"; return VMPS_ERR_BUDGET; }
+  if (r < 2) return VMPS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* base = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  size_t off = 0;
+  auto take = [&](size_t bytes) { void* p = base + off; off += (bytes + 255) & ~(size_t)255; return p; };
+  const size_t R = (size_t)r + 2;
+  uint8_t* power = (uint8_t*)take(R);
+  uint32_t* seg_l = (uint32_t*)take(R * 4);
+  uint32_t* seg_r = (uint32_t*)take(R * 4);
+  uint32_t* parent = (uint32_t*)take(R * 4);
+  uint32_t* anc0 = (uint32_t*)take(R * 4);
+  uint32_t* anc1 = (uint32_t*)take(R * 4);
+  uint32_t* dep0 = (uint32_t*)take(R * 4);
+  uint32_t* dep1 = (uint32_t*)take(R * 4);
+  uint32_t* scal = (uint32_t*)take(SC_COUNT * 4 + 64);
+  uint32_t hs[SC_COUNT] = {0};
+  hs[SC_RUNS] = (uint32_t)r;
+  VMPS_CK(cudaMemcpyAsync(scal, hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+  const unsigned g = grid_for(r);
+  LAUNCH(k_powers_seg<uint64_t>, g, 256, 0, s, d_run_start, n, scal, power, seg_l, seg_r);
+  LAUNCH(k_parent_init, g, 256, 0, s, scal, power, seg_l, seg_r, parent, anc0, dep0);
+  uint32_t *anc[2] = {anc0, anc1}, *dep[2] = {dep0, dep1};
+  for (int rnd = 0; rnd < 6; ++rnd) {
+    int a = rnd & 1;
+    LAUNCH(k_jump, g, 256, 0, s, scal, anc[a], dep[a], anc[a ^ 1], dep[a ^ 1]);
+  }
+  // records only (run starts / kinds are the caller's)
+  k_plan_records_only<<<g, 256, 0, s>>>(d_run_start, scal, power, seg_l, seg_r, dep0, d_merges);
+  VMPS_CK(cudaStreamSynchronize(s));  // the host array hs must outlive the copy
+  return launch_check();
 }
 
 const char* vmps_status_string(vmps_status_t s) {

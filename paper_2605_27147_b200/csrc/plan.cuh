@@ -37,7 +37,8 @@ __device__ __forceinline__ uint32_t node_power(uint64_t n, uint64_t i, uint64_t 
 }
 
 // K5 + K6: powers and segments.
-__global__ void k_powers_seg(const uint32_t* __restrict__ rs, uint32_t n, const uint32_t* scalars,
+template <typename P>
+__global__ void k_powers_seg(const P* __restrict__ rs, uint64_t n, const uint32_t* scalars,
                              uint8_t* __restrict__ power, uint32_t* __restrict__ seg_l,
                              uint32_t* __restrict__ seg_r) {
   const uint32_t r = scalars[SC_RUNS];
@@ -327,7 +328,8 @@ __global__ void k_level_tile_off(const uint32_t* __restrict__ level_start,
 // increasing (trigger, -t) with trigger = next smaller boundary = seg_r[t];
 // this is the post-order of the Cartesian tree, whose rank is
 // (seg_r[t] - 1) - (left ancestors of t) - 1.
-__global__ void k_plan_records(const uint32_t* __restrict__ rs, const uint32_t* scalars,
+template <typename P>
+__global__ void k_plan_records(const P* __restrict__ rs, const uint32_t* scalars,
                                const uint8_t* __restrict__ power, const uint32_t* __restrict__ seg_l,
                                const uint32_t* __restrict__ seg_r, const uint32_t* __restrict__ dep,
                                const uint8_t* __restrict__ kind, uint64_t* __restrict__ run_start,
@@ -340,6 +342,25 @@ __global__ void k_plan_records(const uint32_t* __restrict__ rs, const uint32_t* 
     if (t == 0) continue;
     uint32_t la = dep[t] >> 16;
     uint32_t ord = seg_r[t] - 2 - la;
+    vmps_merge_rec_t rec;
+    rec.i = rs[seg_l[t]];
+    rec.j = rs[t];
+    rec.k = rs[seg_r[t]];
+    rec.power = power[t];
+    rec.order = ord;
+    merges[ord] = rec;
+  }
+}
+
+// Merge records only (the distributed plan supplies its own run arrays).
+template <typename P>
+__global__ void k_plan_records_only(const P* __restrict__ rs, const uint32_t* scalars,
+                                    const uint8_t* __restrict__ power, const uint32_t* __restrict__ seg_l,
+                                    const uint32_t* __restrict__ seg_r, const uint32_t* __restrict__ dep,
+                                    vmps_merge_rec_t* __restrict__ merges) {
+  const uint32_t r = scalars[SC_RUNS];
+  for (uint32_t t = 1 + blockIdx.x * blockDim.x + threadIdx.x; t < r; t += gridDim.x * blockDim.x) {
+    const uint32_t ord = seg_r[t] - 2 - (dep[t] >> 16);
     vmps_merge_rec_t rec;
     rec.i = rs[seg_l[t]];
     rec.j = rs[t];

@@ -189,13 +189,22 @@ __device__ __forceinline__ uint32_t tile_first(const uint32_t* sb, const uint16_
 // whole word lies inside [0, n).
 template <int KT>
 __device__ __forceinline__ void build_tile_bits(const typename KeyTraits<KT>::K* __restrict__ keys, uint32_t n,
-                                                uint32_t T0, uint32_t* sb, uint32_t* __restrict__ gout) {
+                                                uint32_t T0, uint32_t* sb, uint32_t* __restrict__ gout,
+                                                const typename KeyTraits<KT>::K* __restrict__ prev,
+                                                const typename KeyTraits<KT>::K* __restrict__ halo,
+                                                uint32_t n_halo) {
+  // keys[0, n) is the array (or a shard of it); positions n .. n + n_halo - 1
+  // are the next shards' first keys (halo) and *prev the previous shard's last
+  // key (bit 0 = the descent into this shard), so a shard's bitmap is the
+  // global one
   using T = KeyTraits<KT>;
   using K = typename T::K;
+  auto key = [&](uint32_t p) -> K { return p < n ? keys[p] : halo[p - n]; };
+  const uint32_t nx = n + n_halo;
   const uint32_t t = threadIdx.x;  // blockDim.x == RT_WORDS
   const uint32_t p0 = T0 + 32u * t;
   uint32_t word = 0;
-  if (p0 + 32 <= n) {
+  if (p0 + 32 <= n && p0 >= 1) {
     K k[32];
     const uint4* src = reinterpret_cast<const uint4*>(keys + p0);
     constexpr int PER = 16 / sizeof(K);
@@ -206,21 +215,32 @@ __device__ __forceinline__ void build_tile_bits(const typename KeyTraits<KT>::K*
 #pragma unroll
       for (int r = 0; r < PER; ++r) k[q * PER + r] = e[r];
     }
-    const K prev = p0 >= 1 ? keys[p0 - 1] : k[0];
-    word = (p0 >= 1 && T::ord(k[0]) < T::ord(prev)) ? 1u : 0u;
+    word = T::ord(k[0]) < T::ord(keys[p0 - 1]) ? 1u : 0u;
 #pragma unroll
     for (int l = 1; l < 32; ++l) word |= (T::ord(k[l]) < T::ord(k[l - 1]) ? 1u : 0u) << l;
   } else {
     for (uint32_t l = 0; l < 32; ++l) {
       const uint32_t p = p0 + l;
-      if (p >= 1 && p < n && T::ord(keys[p]) < T::ord(keys[p - 1])) word |= 1u << l;
+      if (p == 0) word |= (prev && T::ord(keys[0]) < T::ord(*prev)) ? 1u : 0u;
+      else if (p < nx && T::ord(key(p)) < T::ord(key(p - 1))) word |= 1u << l;
     }
   }
   sb[t] = word;
-  if (p0 < n) gout[t] = word;
+  if (p0 < nx) gout[t] = word;
+  if (T0 + RT >= n && t < 8) {  // last tile of a shard: the halo's words past the tile
+    const uint32_t q0 = T0 + RT + 32u * t;
+    if (q0 < nx) {
+      uint32_t hw = 0;
+      for (uint32_t l = 0; l < 32; ++l) {
+        const uint32_t p = q0 + l;
+        if (p < nx && T::ord(key(p)) < T::ord(key(p - 1))) hw |= 1u << l;
+      }
+      gout[RT_WORDS + t] = hw;
+    }
+  }
   if (t == 0) {
     const uint32_t p = T0 + RT;
-    sb[RT_WORDS] = (p < n && T::ord(keys[p]) < T::ord(keys[p - 1])) ? 1u : 0u;
+    sb[RT_WORDS] = (p < nx && T::ord(key(p)) < T::ord(key(p - 1))) ? 1u : 0u;
     sb[RT_WORDS + 1] = 0;
   }
 }
@@ -328,11 +348,17 @@ __device__ __forceinline__ uint32_t tile_walk_fast(const uint32_t* sb, const uin
 
 // K1+K2: descent bitmap, long-run masks and the tile's transfer table: one
 // walker per entry class (offsets 0..m-1, open ascending, open descending).
+// n: keys in this array / shard; n_end: the position where the chain ends
+// (= n for a whole array or the last shard, 0xFFFFFFFF for an inner shard);
+// prev / halo: see build_tile_bits.
 template <int KT>
 __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT>::K* __restrict__ keys,
                                                      uint32_t n, uint32_t minrun, uint32_t ns,
                                                      uint32_t* __restrict__ bits_out,
-                                                     uint32_t* __restrict__ tab) {
+                                                     uint32_t* __restrict__ tab, uint32_t n_end,
+                                                     const typename KeyTraits<KT>::K* __restrict__ prev,
+                                                     const typename KeyTraits<KT>::K* __restrict__ halo,
+                                                     uint32_t n_halo) {
   __shared__ uint32_t sb[RT_WORDS + 2];
   __shared__ uint32_t la[RT_WORDS], ld[RT_WORDS];
   __shared__ uint16_t fs[RT_WORDS + 2], fc[RT_WORDS + 2];
@@ -343,7 +369,7 @@ __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT
   const uint32_t T0 = tile * RT;
   const uint32_t L = min((uint32_t)RT, n - T0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  build_tile_bits<KT>(keys, n, T0, sb, bits_out + (size_t)tile * RT_WORDS);
+  build_tile_bits<KT>(keys, n, T0, sb, bits_out + (size_t)tile * RT_WORDS, prev, halo, n_halo);
   if (threadIdx.x == 0) sb[RT_WORDS + 1] = 0;
   __syncthreads();
   if (warp == 0) tile_suffix_tables(sb, L, fs, fc, lane);
@@ -355,7 +381,7 @@ __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT
     __syncthreads();
   }
   const uint32_t d_asc = fs[0], d_desc = fc[0];
-  TileCtx c{sb, T0, L, n, minrun};
+  TileCtx c{sb, T0, L, n_end, minrun};
   for (uint32_t w = threadIdx.x; w < minrun + 2; w += blockDim.x) {
     uint32_t x = w < minrun ? w : (w == minrun ? d_asc : d_desc);
     uint32_t res;
@@ -363,7 +389,7 @@ __global__ void __launch_bounds__(128) k_runs_tables(const typename KeyTraits<KT
       res = ST_END << 24;  // unused / not reachable
     } else {
       uint32_t cnt = 0;
-      const uint32_t v = tile_walk_fast<false>(sb, la, ld, fs, fc, T0, L, n, minrun, x, &cnt, nullptr,
+      const uint32_t v = tile_walk_fast<false>(sb, la, ld, fs, fc, T0, L, n_end, minrun, x, &cnt, nullptr,
                                                m32 ? ts : nullptr);
       res = (v << 24) | cnt;
     }
@@ -423,9 +449,9 @@ __global__ void __launch_bounds__(256) k_chain_compose(const In* __restrict__ in
 // Sequential walk over <= CHAIN_G tables of the top level from START(0).
 template <typename In>
 __global__ void k_chain_top(const In* __restrict__ in, uint32_t m, uint32_t ns,
-                            uint64_t* __restrict__ entry) {
+                            uint64_t* __restrict__ entry, uint32_t st0) {
   if (threadIdx.x != 0) return;
-  uint32_t st = 0, cnt = 0;
+  uint32_t st = st0, cnt = 0;
   for (uint32_t t = 0; t < m; ++t) {
     entry[t] = ((uint64_t)st << 32) | cnt;
     if (st != ST_END) {
@@ -434,6 +460,22 @@ __global__ void k_chain_top(const In* __restrict__ in, uint32_t m, uint32_t ns,
       st = s2;
       cnt += c2;
     }
+  }
+}
+
+// A shard's transfer table: for every entry state, walk the <= CHAIN_G tables
+// of the top level (one thread per state): (exit state << 32) | runs started.
+template <typename In>
+__global__ void k_chain_all(const In* __restrict__ in, uint32_t m, uint32_t ns, uint64_t* __restrict__ out) {
+  for (uint32_t s0 = threadIdx.x; s0 < ns; s0 += blockDim.x) {
+    uint32_t st = s0, cnt = 0;
+    for (uint32_t t = 0; t < m && st != ST_END; ++t) {
+      uint32_t s2, c2;
+      unpack<In>(in[(size_t)t * ns + st], &s2, &c2);
+      st = s2;
+      cnt += c2;
+    }
+    out[s0] = ((uint64_t)st << 32) | cnt;
   }
 }
 
@@ -469,7 +511,8 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
                                                    const uint64_t* __restrict__ entry,
                                                    uint32_t* __restrict__ run_start,
                                                    uint8_t* __restrict__ run_kind,
-                                                   uint32_t* __restrict__ scalars) {
+                                                   uint32_t* __restrict__ scalars, uint32_t n_end,
+                                                   uint32_t n_halo) {
   __shared__ uint32_t sb[RT_WORDS + 4];
   __shared__ uint16_t fs[RT_WORDS + 2], fc[RT_WORDS + 2];
   __shared__ uint32_t startb[RT_WORDS];
@@ -480,7 +523,7 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
   const uint32_t tile = blockIdx.x;
   const uint32_t T0 = tile * RT;
   const uint32_t L = min((uint32_t)RT, n - T0);
-  const uint32_t nwords = (n + 31) / 32;
+  const uint32_t nwords = (n + n_halo + 31) / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (uint32_t w = threadIdx.x; w < RT_WORDS + 4; w += blockDim.x) {
     const uint32_t gw = tile * RT_WORDS + w;
@@ -497,13 +540,13 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    TileCtx c{sb, T0, L, n, minrun};
+    TileCtx c{sb, T0, L, n_end, minrun};
     const uint64_t e = entry[tile];
     const uint32_t st = (uint32_t)(e >> 32);
     uint32_t x, out, rev_open, cnt = 0;
     bool ended;
     if (resolve_entry(c, st, fs[0], fc[0], &x, &out, &rev_open)) {
-      ended = tile_walk_fast<true>(sb, la, ld, fs, fc, T0, L, n, minrun, x, &cnt, startb, m32 ? ts : nullptr) ==
+      ended = tile_walk_fast<true>(sb, la, ld, fs, fc, T0, L, n_end, minrun, x, &cnt, startb, m32 ? ts : nullptr) ==
               ST_END;
     } else {
       ended = (st != ST_END) && out == ST_END;
@@ -535,10 +578,10 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
   for (uint32_t m = bits; m; m &= m - 1) {
     const uint32_t x = 32 * t + (uint32_t)(__ffs(m) - 1);
     const uint32_t gx = T0 + x;
-    const bool last = gx + 1 >= n;
+    const bool last = gx + 1 >= n_end;
     const bool desc = !last && get_bit(sb, x + 1);
     bool ext;
-    if (gx + minrun > n) {
+    if (gx + minrun > n_end) {
       ext = true;
     } else {  // a breaking bit inside [from, x + minrun) (at most 64 bits past the tile)
       const uint32_t from = desc ? x + 2 : x + 1;

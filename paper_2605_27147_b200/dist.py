@@ -19,6 +19,9 @@ Rank p then holds global output ranks [R_p, R_{p+1}).  torch.distributed is the
 plumbing (process group, collectives); every step on the data path runs in
 libvmps kernels.  The compute ops are passed in as an object so the protocol
 itself can be exercised with gloo on CPU (tests/test_dist.py).
+
+The second protocol, merge_plan_dist, computes Alg. 1's merge plan of the
+concatenated shards without moving keys (see the section comment below).
 """
 from __future__ import annotations
 
@@ -29,7 +32,7 @@ import torch
 import torch.distributed as dist
 
 from . import (KEY_F32, KEY_U32, KEY_U64, Workspace, _check, _stream_ptr, key_type, lib,
-               sort_)
+               minrun_for, sort_)
 
 
 def image_bits(kt: int) -> int:
@@ -192,3 +195,200 @@ def sort_dist_(keys: torch.Tensor, vals: torch.Tensor | None = None, group=None)
     if vals is not None:
         vals.copy_(res.vals)
     return res
+
+
+# ---------------------------------------------------------------------------
+# Distributed merge plan: Alg. 1's plan of the
+# concatenation of the ranks' shards, without moving the keys.
+#
+# Run detection is a left-to-right chain (ExtractRun, P:399 / P:756): each
+# shard computes its transfer table (chain state at its start -> state at its
+# end, runs started) with vmps_shard_chain; composing the g tables from
+# START(0) on the host gives every shard its entry state and run count; each
+# shard then emits its run starts (global positions) with vmps_shard_runs.
+# The run list is assembled on every rank and vmps_plan_from_runs computes
+# powers, tree and Alg. 1's order (Alg. 1) -- a replicated,
+# O(r)-sized step.  Inputs crossing the shard edges: the previous shard's last
+# key (descent bit at the shard start) and the next HALO keys of the global
+# array (runs that cross the shard end are classified exactly).
+# ---------------------------------------------------------------------------
+
+ST_END = 255
+
+
+def halo_len(minrun: int) -> int:
+    """Keys after a shard's end its run classification may read: minrun + 8."""
+    return minrun + 8
+
+
+def compose_tables(tables: list) -> tuple[list[int], list[int]]:
+    """Entry states and run counts of consecutive shards from START(0).
+    tables[q]: the shard's transfer table (a list of 64-bit values: exit state
+    << 32 | runs started, indexed by entry state), or None for an empty shard
+    (identity, no runs)."""
+    st = 0
+    entries, counts = [], []
+    for t in tables:
+        entries.append(st)
+        if t is None or st == ST_END:
+            counts.append(0)
+            continue
+        v = int(t[st]) & 0xFFFFFFFFFFFFFFFF
+        counts.append(v & 0xFFFFFFFF)
+        st = v >> 32
+    return entries, counts
+
+
+def halo_from_heads(me: int, heads: list, sizes: list[int], need: int):
+    """The first `need` keys after shard `me` (fewer at the global end), from
+    the other shards' heads (heads[p] = shard p's first min(need, n_p) keys)."""
+    parts, got = [], 0
+    for p in range(me + 1, len(sizes)):
+        if got >= need:
+            break
+        take = min(sizes[p], need - got, len(heads[p]))
+        if take > 0:
+            parts.append(heads[p][:take])
+            got += take
+    return parts
+
+
+def prev_owner(me: int, sizes: list[int]) -> int:
+    """The nearest non-empty shard before `me` (-1 if none)."""
+    for p in range(me - 1, -1, -1):
+        if sizes[p] > 0:
+            return p
+    return -1
+
+
+class PlanOps:
+    """The data-path operations of the distributed plan, through the C ABI."""
+
+    def __init__(self):
+        self.ws = Workspace()
+
+    def chain(self, keys, minrun, n_end, prev, halo):
+        from . import shard_chain
+        return shard_chain(keys, minrun, n_end, prev, halo, workspace=self.ws)
+
+    def runs(self, keys, minrun, n_end, prev, halo, entry, count, offset, out_starts):
+        from . import shard_runs
+        return shard_runs(keys, minrun, n_end, entry, count, offset, prev, halo, out=out_starts,
+                          workspace=self.ws)[1]
+
+    def plan(self, starts, n):
+        from . import plan_from_runs
+        return plan_from_runs(starts, n, workspace=self.ws)
+
+
+@dataclass
+class DistPlan:
+    run_start: torch.Tensor     # int64 (r,), global positions
+    run_kind: torch.Tensor      # uint8 (r,)
+    merges: torch.Tensor        # int64 (r - 1, 4): (i, j, k, power), Alg. 1's order
+    minrun: int
+    entries: list[int]          # chain state at each shard's start
+    counts: list[int]           # runs starting in each shard
+
+
+def _cat(parts):
+    if not parts:
+        return None
+    return torch.cat(parts).contiguous() if len(parts) > 1 else parts[0].contiguous()
+
+
+def merge_plan_shards(shards: list[torch.Tensor], ops=None) -> DistPlan:
+    """The same protocol for g shards held by one process (virtual ranks):
+    the plan of torch.cat(shards), each shard processed on its own."""
+    ops = ops if ops is not None else PlanOps()
+    sizes = [s.numel() for s in shards]
+    N = sum(sizes)
+    if N == 0:
+        raise ValueError("empty array")
+    dev = next(s.device for s in shards if s.numel() > 0)
+    minrun = minrun_for(N)
+    H = halo_len(minrun)
+    offs = [sum(sizes[:q]) for q in range(len(shards))]
+    heads = [s[:min(H, s.numel())] for s in shards]
+    tables = []
+    for q, s in enumerate(shards):
+        if sizes[q] == 0:
+            tables.append(None)
+            continue
+        pq = prev_owner(q, sizes)
+        prev = shards[pq][-1:].contiguous() if pq >= 0 else None
+        halo = _cat(halo_from_heads(q, heads, sizes, H))
+        tables.append(ops.chain(s, minrun, N - offs[q], prev, halo).cpu().tolist())
+    entries, counts = compose_tables(tables)
+    r = sum(counts)
+    starts = torch.empty(r + 1, dtype=torch.int64, device=dev)
+    kinds = torch.empty(r, dtype=torch.uint8, device=dev)
+    o = 0
+    for q, s in enumerate(shards):
+        if counts[q] == 0:
+            continue
+        pq = prev_owner(q, sizes)
+        prev = shards[pq][-1:].contiguous() if pq >= 0 else None
+        halo = _cat(halo_from_heads(q, heads, sizes, H))
+        k = ops.runs(s, minrun, N - offs[q], prev, halo, entries[q], counts[q], offs[q], starts[o:o + counts[q]])
+        kinds[o:o + counts[q]].copy_(k)
+        o += counts[q]
+    starts[r] = N
+    merges = ops.plan(starts, N)
+    return DistPlan(starts[:r], kinds, merges, minrun, entries, counts)
+
+
+def merge_plan_dist(keys: torch.Tensor, group=None, ops=None) -> DistPlan:
+    """Alg. 1's merge plan of the concatenation of every rank's shard (global
+    order = rank order), replicated on every rank; the keys do not move."""
+    ops = ops if ops is not None else PlanOps()
+    g = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    dev = keys.device
+    n = keys.numel()
+    sz = torch.tensor([n], dtype=torch.int64, device=dev)
+    sizes_t = [torch.zeros_like(sz) for _ in range(g)]
+    dist.all_gather(sizes_t, sz, group=group)
+    sizes = [int(x.item()) for x in sizes_t]
+    N = sum(sizes)
+    if N == 0:
+        raise ValueError("empty array")
+    off = sum(sizes[:me])
+    minrun = minrun_for(N)
+    H = halo_len(minrun)
+    # edge keys: every shard's head (first H keys, padded) and last key
+    edge = torch.zeros(H + 1, dtype=keys.dtype, device=dev)
+    h = min(H, n)
+    if h:
+        edge[:h].copy_(keys[:h])
+        edge[H:].copy_(keys[n - 1:])
+    edges = [torch.empty_like(edge) for _ in range(g)]
+    dist.all_gather([_as_int(e) for e in edges], _as_int(edge), group=group)
+    heads = [e[:min(H, sizes[p])] for p, e in enumerate(edges)]
+    pq = prev_owner(me, sizes)
+    prev = edges[pq][H:].contiguous() if pq >= 0 else None
+    halo = _cat(halo_from_heads(me, heads, sizes, H))
+    # transfer tables -> entry states and run counts (host composition)
+    mine = ops.chain(keys, minrun, N - off, prev, halo) if n else torch.zeros(3 * minrun, dtype=torch.int64,
+                                                                            device=dev)
+    tabs = [torch.empty_like(mine) for _ in range(g)]
+    dist.all_gather(tabs, mine, group=group)
+    tables = [t.cpu().tolist() if sizes[p] else None for p, t in enumerate(tabs)]
+    entries, counts = compose_tables(tables)
+    r = sum(counts)
+    o = sum(counts[:me])
+    starts = torch.empty(r + 1, dtype=torch.int64, device=dev)
+    kinds = torch.empty(max(r, 1), dtype=torch.uint8, device=dev)
+    if counts[me]:
+        k = ops.runs(keys, minrun, N - off, prev, halo, entries[me], counts[me], off, starts[o:o + counts[me]])
+        kinds[o:o + counts[me]].copy_(k)
+    # every rank's run list to every rank (in place, rank order)
+    a = 0
+    for p in range(g):
+        if counts[p]:
+            dist.broadcast(starts[a:a + counts[p]], src=p, group=group)
+            dist.broadcast(kinds[a:a + counts[p]], src=p, group=group)
+        a += counts[p]
+    starts[r] = N
+    merges = ops.plan(starts, N)
+    return DistPlan(starts[:r], kinds[:r], merges, minrun, entries, counts)
