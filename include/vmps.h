@@ -206,6 +206,53 @@ vmps_status_t vmps_plan_workspace_bytes(uint64_t r, size_t* h_bytes);
 vmps_status_t vmps_plan_from_runs(const uint64_t* d_run_start, uint64_t r, uint64_t n, vmps_merge_rec_t* d_merges,
                                   void* ws, size_t ws_bytes, void* stream);
 
+/* ---- native multi-GPU entry points; paper_2605_27147_b200/csrc/comm.cu ----
+ * One process per GPU; NCCL (loaded with dlopen on first use) carries the
+ * exchanges.  A communicator: rank 0 calls vmps_comm_unique_id and shares the
+ * 128 bytes with the other ranks out of band (e.g. a torch.distributed
+ * broadcast); every rank calls vmps_comm_init(&c, rank, world, id, device).
+ * Errors of these calls: VMPS_ERR_NCCL / VMPS_ERR_CUDA with detail in
+ * vmps_comm_last_error().
+ *
+ * vmps_sort_keys_dist / vmps_sort_pairs_dist: the globally stable sort of the
+ * concatenation of the ranks' shards (rank order), in place: rank p ends with
+ * the global output ranks [off_p, off_p + n_local_p), off_p = sum of the
+ * earlier ranks' n_local, so each rank keeps its element count.  Steps: local
+ * vmps_sort_*; exact splitters for the output ranks off_1..off_{g-1} by a
+ * 16-ary search over the key order image (vmps_count_rank counts, summed by
+ * ncclAllReduce; 8 rounds for u32/f32, 16 for u64); the tie group at each
+ * splitter is split in rank order (lower ranks first: stability); grouped
+ * ncclSend / ncclRecv of keys and payloads; vmps_merge_runs of the received
+ * pieces in source-rank order (ties to the lower rank).  h_stats (optional)
+ * reports the local sort.  Workspace: vmps_dist_workspace_bytes.  Synchronises
+ * `stream` once per search round.
+ *
+ * vmps_merge_plan_dist: Alg. 1's merge plan of the concatenated shards with
+ * the global n (reading C13; as paper_2605_27147_b200.dist.merge_plan_dist):
+ * each rank receives the runs starting in its shard (global u64 positions,
+ * kinds) and the merges whose boundary j lies in its shard, in Alg. 1's order
+ * (the `order` field is the global execution rank); cap_runs bounds both
+ * outputs.  Workspace: vmps_merge_plan_dist_workspace_bytes(n_total, ...),
+ * n_total = the sum of all shard sizes.  Synchronises `stream`. */
+typedef struct vmps_comm_s* vmps_comm_t;
+vmps_status_t vmps_comm_unique_id(void* h_id128);
+vmps_status_t vmps_comm_init(vmps_comm_t* h_out, int rank, int world, const void* h_id128, int device);
+vmps_status_t vmps_comm_destroy(vmps_comm_t c);
+const char* vmps_comm_last_error(void);
+vmps_status_t vmps_dist_workspace_bytes(uint64_t n_local, vmps_key_t kt, int has_vals, int world,
+                                        int64_t scratch_elems, size_t* h_bytes);
+vmps_status_t vmps_sort_keys_dist(vmps_comm_t c, void* keys, uint64_t n_local, vmps_key_t kt, int64_t scratch_elems,
+                                  void* ws, size_t ws_bytes, void* stream, vmps_stats_t* h_stats);
+vmps_status_t vmps_sort_pairs_dist(vmps_comm_t c, void* keys, uint32_t* vals, uint64_t n_local, vmps_key_t kt,
+                                   int64_t scratch_elems, void* ws, size_t ws_bytes, void* stream,
+                                   vmps_stats_t* h_stats);
+vmps_status_t vmps_merge_plan_dist_workspace_bytes(uint64_t n_total, uint64_t n_local, vmps_key_t kt, int world,
+                                                   size_t* h_bytes);
+vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_local, vmps_key_t kt,
+                                   uint64_t* run_start, uint8_t* run_kind, vmps_merge_rec_t* merges,
+                                   uint64_t cap_runs, uint64_t* h_num_runs_local, uint64_t* h_num_merges_local,
+                                   void* ws, size_t ws_bytes, void* stream);
+
 /* vmps_merge_runs: keys[0,n) (and vals, if non-NULL) consist of nruns adjacent
  * runs, each sorted, starting at h_run_start[0] = 0 < h_run_start[1] < ...
  * (host array).  Merges them in place into the stable sort of the array,

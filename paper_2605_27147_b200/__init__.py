@@ -21,6 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VMPS_LIB") or os.path.join(_HERE, "libvmps.so")
 
 KEY_U32, KEY_U64, KEY_F32 = 0, 1, 2
+OK, ERR_INVALID_ARG, ERR_ALLOC, ERR_BUDGET, ERR_CUDA, ERR_NCCL, ERR_INTERNAL = range(7)
 SCRATCH_UNBOUNDED = -1
 RUN_ASC, RUN_DESC, RUN_EXT = 0, 1, 2
 
@@ -59,7 +60,9 @@ EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_me
            "vmps_test_set_minrun", "vmps_test_set_tiles", "vmps_test_set_mode",
            "vmps_test_set_leaf", "vmps_sort_keys_host", "vmps_sort_pairs_host",
            "vmps_shard_workspace_bytes", "vmps_shard_chain", "vmps_shard_runs", "vmps_plan_workspace_bytes",
-           "vmps_plan_from_runs")
+           "vmps_plan_from_runs", "vmps_comm_unique_id", "vmps_comm_init", "vmps_comm_destroy",
+           "vmps_comm_last_error", "vmps_dist_workspace_bytes", "vmps_sort_keys_dist", "vmps_sort_pairs_dist",
+           "vmps_merge_plan_dist_workspace_bytes", "vmps_merge_plan_dist")
 
 _lib = None
 
@@ -87,6 +90,21 @@ def lib() -> ctypes.CDLL:
         L.vmps_plan_from_runs.argtypes = [vp, u64, u64, vp, vp, sz, vp]
         for f in ("vmps_shard_workspace_bytes", "vmps_shard_chain", "vmps_shard_runs", "vmps_plan_workspace_bytes",
                   "vmps_plan_from_runs"):
+            getattr(L, f).restype = ctypes.c_int
+        i64 = ctypes.c_int64
+        L.vmps_comm_unique_id.argtypes = [vp]
+        L.vmps_comm_init.argtypes = [ctypes.POINTER(vp), ci, ci, vp, ci]
+        L.vmps_comm_destroy.argtypes = [vp]
+        L.vmps_comm_last_error.restype = ctypes.c_char_p
+        L.vmps_dist_workspace_bytes.argtypes = [u64, ci, ci, ci, i64, ctypes.POINTER(sz)]
+        L.vmps_sort_keys_dist.argtypes = [vp, vp, u64, ci, i64, vp, sz, vp, vp]
+        L.vmps_sort_pairs_dist.argtypes = [vp, vp, vp, u64, ci, i64, vp, sz, vp, vp]
+        L.vmps_merge_plan_dist_workspace_bytes.argtypes = [u64, u64, ci, ci, ctypes.POINTER(sz)]
+        L.vmps_merge_plan_dist.argtypes = [vp, vp, u64, ci, vp, vp, vp, u64, ctypes.POINTER(u64),
+                                           ctypes.POINTER(u64), vp, sz, vp]
+        for f in ("vmps_comm_unique_id", "vmps_comm_init", "vmps_comm_destroy", "vmps_dist_workspace_bytes",
+                  "vmps_sort_keys_dist", "vmps_sort_pairs_dist", "vmps_merge_plan_dist_workspace_bytes",
+                  "vmps_merge_plan_dist"):
             getattr(L, f).restype = ctypes.c_int
         L.vmps_merge_plan.argtypes = [vp, u64, ctypes.c_int, vp, vp, vp, u64, ctypes.POINTER(u64),
                                       vp, sz, vp]
@@ -353,6 +371,97 @@ def plan_from_runs(run_start: torch.Tensor, n: int, workspace: Workspace | None 
     _check(rc, "vmps_plan_from_runs")
     recs = mg.view(-1, 4)
     return torch.stack([recs[:, 0], recs[:, 1], recs[:, 2], recs[:, 3] & 0xFFFFFFFF], dim=1)
+
+
+# ---- native multi-GPU entry points (csrc/comm.cu) ----
+
+def _check_comm(rc: int, where: str):
+    if rc != 0:
+        raise VmpsError(rc, where, lib().vmps_comm_last_error().decode())
+
+
+def comm_unique_id() -> bytes:
+    """vmps_comm_unique_id: 128 bytes rank 0 shares with the other ranks."""
+    buf = ctypes.create_string_buffer(128)
+    _check_comm(lib().vmps_comm_unique_id(buf), "vmps_comm_unique_id")
+    return buf.raw
+
+
+class Comm:
+    """A native communicator (vmps_comm_init); destroy() or use as a context."""
+
+    def __init__(self, rank: int, world: int, uid: bytes, device: int):
+        self.ptr = ctypes.c_void_p()
+        self.rank, self.world, self.device = rank, world, device
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        _check_comm(lib().vmps_comm_init(ctypes.byref(self.ptr), rank, world, buf, device), "vmps_comm_init")
+
+    def destroy(self):
+        if self.ptr:
+            _check_comm(lib().vmps_comm_destroy(self.ptr), "vmps_comm_destroy")
+            self.ptr = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.destroy()
+
+
+def sort_dist_native_(comm: Comm, keys: torch.Tensor, values: torch.Tensor | None = None,
+                      scratch: int | None = None, stats: bool = False, workspace: Workspace | None = None):
+    """vmps_sort_*_dist: globally stable sort of the ranks' concatenated shards,
+    in place (this rank keeps global output ranks [off, off + n_local))."""
+    if not keys.is_cuda or not keys.is_contiguous() or keys.dim() != 1:
+        raise ValueError("keys must be a contiguous 1-D CUDA tensor")
+    kt = key_type(keys)
+    n = keys.numel()
+    sc = SCRATCH_UNBOUNDED if scratch is None else int(scratch)
+    L = lib()
+    nb = ctypes.c_size_t(0)
+    _check(L.vmps_dist_workspace_bytes(n, kt, 1 if values is not None else 0, comm.world, sc, ctypes.byref(nb)),
+           "vmps_dist_workspace_bytes")
+    ws = workspace if workspace is not None else _default_ws.setdefault(keys.device, Workspace())
+    buf = ws.get(int(nb.value), keys.device)
+    st = Stats()
+    sp = ctypes.byref(st) if stats else None
+    with torch.cuda.device(keys.device):
+        s = _stream_ptr(keys.device)
+        if values is None:
+            rc = L.vmps_sort_keys_dist(comm.ptr, keys.data_ptr(), n, kt, sc, buf.data_ptr(), buf.numel(), s, sp)
+        else:
+            rc = L.vmps_sort_pairs_dist(comm.ptr, keys.data_ptr(), values.data_ptr(), n, kt, sc, buf.data_ptr(),
+                                        buf.numel(), s, sp)
+    _check_comm(rc, "vmps_sort_dist")
+    return st.as_dict() if stats else None
+
+
+def merge_plan_dist_native(comm: Comm, keys: torch.Tensor, n_total: int,
+                           workspace: Workspace | None = None) -> Plan:
+    """vmps_merge_plan_dist: this rank's runs (global positions) and the merges
+    of Alg. 1's global plan whose boundary j lies in its shard."""
+    kt = key_type(keys)
+    n = keys.numel()
+    dev = keys.device
+    L = lib()
+    nb = ctypes.c_size_t(0)
+    _check(L.vmps_merge_plan_dist_workspace_bytes(n_total, n, kt, comm.world, ctypes.byref(nb)),
+           "vmps_merge_plan_dist_workspace_bytes")
+    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    buf = ws.get(int(nb.value), dev)
+    cap = max(n, 1) + 2
+    rs = torch.empty(cap, dtype=torch.int64, device=dev)
+    rk = torch.empty(cap, dtype=torch.uint8, device=dev)
+    mg = torch.empty(cap * 4, dtype=torch.int64, device=dev)
+    nr, nm = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    with torch.cuda.device(dev):
+        rc = L.vmps_merge_plan_dist(comm.ptr, keys.data_ptr(), n, kt, rs.data_ptr(), rk.data_ptr(), mg.data_ptr(),
+                                    cap, ctypes.byref(nr), ctypes.byref(nm), buf.data_ptr(), buf.numel(),
+                                    _stream_ptr(dev))
+    _check_comm(rc, "vmps_merge_plan_dist")
+    recs = mg[: 4 * int(nm.value)].view(-1, 4)
+    merges = torch.stack([recs[:, 0], recs[:, 1], recs[:, 2], recs[:, 3] & 0xFFFFFFFF, recs[:, 3] >> 32], dim=1)
+    return Plan(rs[: int(nr.value)], rk[: int(nr.value)], merges)
 
 
 def profile_enable(on: bool = True) -> None:

@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+R=gpurun_out
+B="python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline --bounded-reps 0"
+: > $R/m4v.log
+for it in 1 2; do for v in $VARIANTS; do
+  echo -n "$v " >> $R/m4v.log
+  VMPS_LIB=$PWD/paper_2605_27147_b200/libvmps_$v.so timeout 300 $B 2>/dev/null | tail -1 >> $R/m4v.log
+done; done
