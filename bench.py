@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--leaf-radix", action="store_true",
                     help="experimental: radix-sort leaf engine instead of the block merge sort")
     ap.add_argument("--fuse-z", type=int, default=0, help="experimental: fused-subtree limit Z")
+    ap.add_argument("--native-dist", action="store_true",
+                    help="N>1: the library's own NCCL protocol (vmps_sort_pairs_dist) instead of dist.py")
     ap.add_argument("--bounded-reps", type=int, default=2,
                     help="timed sorts of the scratch-bounded mode (cap 4 sqrt(n log2 n)); 0 = skip")
     return ap.parse_args()
@@ -212,7 +214,15 @@ def main():
         if world > 1:
             dist.barrier()
 
-    if world > 1:
+    if world > 1 and args.native_dist:
+        # native protocol (csrc/comm.cu): NCCL communicator owned by libvmps
+        uid = [vm.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ncomm = vm.Comm(rank, world, uid[0], local)
+
+        def do_sort():
+            vm.sort_dist_native_(ncomm, keys, vals, workspace=ws)
+    elif world > 1:
         from paper_2605_27147_b200.dist import sort_dist_
 
         def do_sort():
