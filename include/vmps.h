@@ -253,6 +253,23 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
                                    uint64_t cap_runs, uint64_t* h_num_runs_local, uint64_t* h_num_merges_local,
                                    void* ws, size_t ws_bytes, void* stream);
 
+/* ---- large records (paper_2605_27147_b200/csrc/records.cu) ----
+ * vmps_sort_records: n records of `words` u32 each (row-major, device),
+ * ordered lexicographically with word 0 most significant (the paper's blob
+ * types: arrays of 30 ints ordered lexicographically), sorted
+ * stably.  The engine sorts (64-bit word-pair key, u32 index) pairs: the
+ * leading pair first, and, only if two records tie on it, an LSD pass per
+ * word pair from the last to the first (pairs equal in every record are
+ * skipped); then one gather writes records_out (may be NULL; must not alias
+ * records).  perm_out (may be NULL, u32[n]) receives the permutation: the
+ * paper's `ptr` type (pointers sorted by their arrays).  n < 2^32.
+ * Workspace: vmps_sort_records_workspace_bytes.  May synchronise `stream`
+ * (tie check).  Error detail: vmps_records_last_error(). */
+vmps_status_t vmps_sort_records_workspace_bytes(uint64_t n, uint32_t words, size_t* h_bytes);
+vmps_status_t vmps_sort_records(const uint32_t* records, uint32_t* records_out, uint32_t* perm_out, uint64_t n,
+                                uint32_t words, void* ws, size_t ws_bytes, void* stream);
+const char* vmps_records_last_error(void);
+
 /* vmps_merge_runs: keys[0,n) (and vals, if non-NULL) consist of nruns adjacent
  * runs, each sorted, starting at h_run_start[0] = 0 < h_run_start[1] < ...
  * (host array).  Merges them in place into the stable sort of the array,

@@ -183,3 +183,18 @@ def plan(keys: np.ndarray, minrun_override: int = 0):
         raise RuntimeError(f"orc_plan failed: {rc}")
     r = st.runs
     return Plan(rs[:r].copy(), rk[:r].copy(), mg[:max(r - 1, 0)].copy()), _stats_dict(st)
+
+
+def sort_records(records: np.ndarray) -> np.ndarray:
+    """Stable lexicographic sort of n records of w unsigned 32-bit words, word 0
+    most significant -- the paper's blob data types (arrays of 30
+    ints ordered lexicographically; ``ptr`` sorts pointers to such arrays).
+    Returns the permutation (int64): the plain definition, Python's stable
+    ``sorted`` of the indices by the tuple of words (equal records keep their
+    input order).  Pinned in tests/test_oracle.py against the Powersort oracle
+    for one-word records and by brute force on tiny inputs."""
+    r = np.ascontiguousarray(records, dtype=np.uint32)
+    if r.ndim != 2:
+        raise ValueError("records must be an (n, words) array")
+    rows = [tuple(int(x) for x in row) for row in r]
+    return np.array(sorted(range(len(rows)), key=lambda i: rows[i]), dtype=np.int64)

@@ -62,7 +62,8 @@ EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_me
            "vmps_shard_workspace_bytes", "vmps_shard_chain", "vmps_shard_runs", "vmps_plan_workspace_bytes",
            "vmps_plan_from_runs", "vmps_comm_unique_id", "vmps_comm_init", "vmps_comm_destroy",
            "vmps_comm_last_error", "vmps_dist_workspace_bytes", "vmps_sort_keys_dist", "vmps_sort_pairs_dist",
-           "vmps_merge_plan_dist_workspace_bytes", "vmps_merge_plan_dist")
+           "vmps_merge_plan_dist_workspace_bytes", "vmps_merge_plan_dist", "vmps_sort_records_workspace_bytes",
+           "vmps_sort_records", "vmps_records_last_error")
 
 _lib = None
 
@@ -102,6 +103,11 @@ def lib() -> ctypes.CDLL:
         L.vmps_merge_plan_dist_workspace_bytes.argtypes = [u64, u64, ci, ci, ctypes.POINTER(sz)]
         L.vmps_merge_plan_dist.argtypes = [vp, vp, u64, ci, vp, vp, vp, u64, ctypes.POINTER(u64),
                                            ctypes.POINTER(u64), vp, sz, vp]
+        L.vmps_sort_records_workspace_bytes.argtypes = [u64, u32, ctypes.POINTER(sz)]
+        L.vmps_sort_records.argtypes = [vp, vp, vp, u64, u32, vp, sz, vp]
+        L.vmps_records_last_error.restype = ctypes.c_char_p
+        for f in ("vmps_sort_records_workspace_bytes", "vmps_sort_records"):
+            getattr(L, f).restype = ctypes.c_int
         for f in ("vmps_comm_unique_id", "vmps_comm_init", "vmps_comm_destroy", "vmps_dist_workspace_bytes",
                   "vmps_sort_keys_dist", "vmps_sort_pairs_dist", "vmps_merge_plan_dist_workspace_bytes",
                   "vmps_merge_plan_dist"):
@@ -371,6 +377,32 @@ def plan_from_runs(run_start: torch.Tensor, n: int, workspace: Workspace | None 
     _check(rc, "vmps_plan_from_runs")
     recs = mg.view(-1, 4)
     return torch.stack([recs[:, 0], recs[:, 1], recs[:, 2], recs[:, 3] & 0xFFFFFFFF], dim=1)
+
+
+def sort_records(records: torch.Tensor, out: torch.Tensor | None = None, perm: bool = False,
+                 workspace: Workspace | None = None):
+    """vmps_sort_records: stable lexicographic sort of a (n, words) CUDA tensor
+    of u32/int32 records (word 0 most significant).  Returns the sorted
+    records (``out`` if given) and, with ``perm``, the permutation (uint32)."""
+    if not records.is_cuda or records.dim() != 2 or not records.is_contiguous():
+        raise ValueError("records must be a contiguous (n, words) CUDA tensor")
+    if records.dtype not in (torch.uint32, torch.int32):
+        raise ValueError("records must hold 32-bit words")
+    n, words = records.shape
+    dev = records.device
+    res = out if out is not None else torch.empty_like(records)
+    pm = torch.empty(n, dtype=torch.uint32, device=dev) if perm else None
+    L = lib()
+    nb = ctypes.c_size_t(0)
+    _check(L.vmps_sort_records_workspace_bytes(n, words, ctypes.byref(nb)), "vmps_sort_records_workspace_bytes")
+    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    buf = ws.get(int(nb.value), dev)
+    with torch.cuda.device(dev):
+        rc = L.vmps_sort_records(records.data_ptr(), res.data_ptr(), None if pm is None else pm.data_ptr(), n, words,
+                                 buf.data_ptr(), buf.numel(), _stream_ptr(dev))
+    if rc != 0:
+        raise VmpsError(rc, "vmps_sort_records", L.vmps_records_last_error().decode())
+    return (res, pm) if perm else res
 
 
 # ---- native multi-GPU entry points (csrc/comm.cu) ----

@@ -316,3 +316,23 @@ def test_degenerate():
     _, _, plan, st = oracle.sort(keys)
     assert (np.diff(np.append(plan.run_start, 1 << 16)) == 32).all()
     assert st["merge_cost_M"] == 11 * (1 << 16)
+
+
+def test_sort_records_pins():
+    """oracle.sort_records: one-word records give the Powersort oracle's stable
+    permutation (a different implementation: Alg. 1 with copy-merge); tiny
+    inputs match brute force over all orderings (the unique stable one:
+    lexicographically non-decreasing, equal records in index order)."""
+    import itertools
+    rng = np.random.default_rng(3)
+    k = rng.integers(0, 50, 3000).astype(np.uint32)
+    _, vo, _, _ = oracle.sort(k, np.arange(len(k), dtype=np.uint32))
+    assert (oracle.sort_records(k.reshape(-1, 1)) == vo.astype(np.int64)).all()
+    for _ in range(20):
+        n, w = int(rng.integers(1, 7)), int(rng.integers(1, 4))
+        r = rng.integers(0, 2, (n, w)).astype(np.uint32)
+        good = [p for p in itertools.permutations(range(n))
+                if all(tuple(r[p[t]]) < tuple(r[p[t + 1]]) or
+                       (tuple(r[p[t]]) == tuple(r[p[t + 1]]) and p[t] < p[t + 1]) for t in range(n - 1))]
+        assert len(good) == 1
+        assert list(oracle.sort_records(r)) == list(good[0])

@@ -179,6 +179,52 @@ def cfg5(n: int = 1 << 30, seed: int = 5, device="cpu", rank: int = 0):
 GENERATORS = {1: cfg1, 2: cfg2, 3: cfg3, 4: cfg4, 5: cfg5}
 
 
+# ---- the paper's own workload ----
+PAPER_N = 10 ** 7
+PAPER_S = (2, 10 ** 2, 10 ** 3, 10 ** 4, 10 ** 5, 10 ** 6)
+
+
+def paper_input(S: int, kind: str = "int", seed: int = 0, N: int = PAPER_N, device="cpu"):
+    """One input of the paper's sweep: length n ~ U[9N/10, N]; every integer
+    uniform in [100, 10^9]; then runs of length Geom(1/S) (mean S - 1) are
+    pre-sorted one after another.  kind: "int" (u32 keys) or "randomBlob30" /
+    "zeroBlob30" ((n, 30) u32 records; zeroBlob30 has only the last word
+    nonzero); runs of blobs are pre-sorted by their deciding word (the first
+    word for randomBlob30 -- ties there are ~n^2 / 2^31 pairs and do not
+    matter for an input generator -- the last for zeroBlob30).  Returns
+    (data, n)."""
+    g = _gen(device, 1000 * seed + S)
+    n = int(torch.randint(9 * N // 10, N + 1, (1,), generator=g, device=device).item())
+    if kind == "int":
+        vals = torch.randint(100, 10 ** 9 + 1, (n,), generator=g, device=device, dtype=torch.int64)
+        lead = vals
+    elif kind in ("randomBlob30", "zeroBlob30"):
+        vals = torch.randint(100, 10 ** 9 + 1, (n, 30), generator=g, device=device, dtype=torch.int64)
+        if kind == "zeroBlob30":
+            vals[:, :29] = 0
+        lead = vals[:, 0] if kind == "randomBlob30" else vals[:, 29]
+    else:
+        raise ValueError(kind)
+    # geometric run lengths with parameter 1/S (support 1, 2, ...)
+    p = 1.0 / S
+    est = max(16, int(2.5 * n * p) + 64)
+    while True:
+        u = torch.rand(est, generator=g, device=device, dtype=torch.float64)
+        lens = torch.floor(torch.log1p(-u) / math.log1p(-p)).to(torch.int64) + 1 if p < 1 else torch.ones(
+            est, dtype=torch.int64, device=device)
+        if int(lens.sum()) >= n:
+            break
+        est *= 2
+    cs = torch.cumsum(lens, 0)
+    k = int(torch.searchsorted(cs, torch.tensor([n], device=device)).item())
+    lens = lens[: k + 1].clone()
+    lens[k] -= int(cs[k]) - n
+    lens = lens[lens > 0]
+    perm = _sort_within_segments(lead, _seg_ids(lens))
+    data = vals[perm]
+    return _u32_from_i64(data), n
+
+
 def make(cfg: int, n: int | None = None, seed: int | None = None, device="cpu", **kw):
     f = GENERATORS[cfg]
     args = {}
