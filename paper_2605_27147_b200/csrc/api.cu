@@ -624,7 +624,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       int e0 = prof_event(s);
       LAUNCH(k4_node_runs, grid_for(w.n4cap), 256, 0, s, w.run_start, w.seg_l, w.seg_r, dep, w.lchild, w.rchild,
              w.lnodes, w.level_start, p, nr);
-      LAUNCH(k4_desc<KT>, (w.part_cap / 4 + 256) / 256, 256, 0, s, k0, k1, nr, w.ltiles, w.level_start,
+      LAUNCH(k4_desc<KT>, (std::max<uint32_t>(w.part_cap / 4, std::min<uint32_t>(w.part_cap, 4 * DESC4_SERIAL_MIN)) + 256) / 256, 256, 0, s, k0, k1, nr, w.ltiles, w.level_start,
              w.level_tile, p, w.tout, t4);
       int e1 = prof_event(s);
       LAUNCH((k4_merge_level<KT, HV, M4_KQ>), gm4, 4096 / M4_KQ + 32, SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.level_tile, p);

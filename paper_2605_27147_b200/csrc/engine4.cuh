@@ -192,6 +192,10 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
 #define VMPS_DESC4_CHUNK 8
 #endif
 constexpr uint32_t DESC4_CHUNK = VMPS_DESC4_CHUNK;
+#ifndef VMPS_DESC4_SERIAL_MIN
+#define VMPS_DESC4_SERIAL_MIN 65536
+#endif
+constexpr uint32_t DESC4_SERIAL_MIN = VMPS_DESC4_SERIAL_MIN;
 template <int KT>
 __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* __restrict__ k0,
                                                const typename KeyTraits<KT>::K* __restrict__ k1,
@@ -201,10 +205,16 @@ __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* 
                                                TileDesc4* __restrict__ tiles) {
   const uint32_t ls = level_start[p], le = level_start[p + 1];
   const uint32_t tb = level_tile[p], te = level_tile[p + 1];
-  // chunk length: levels of small nodes (< 8 tiles per node on average) use
-  // chunks of 4 (more independent chains), the others DESC4_CHUNK (fewer full
-  // searches); measured per level at cfg5 2^30
-  const uint32_t chunk = (le > ls && (te - tb) < 8u * (le - ls)) ? 4u : DESC4_CHUNK;
+  // chunk length: a level of few tiles is bound by the length of each
+  // thread's chain of dependent probes, so every tile gets its own thread
+  // (below DESC4_SERIAL_MIN tiles); otherwise levels of small nodes (< 8
+  // tiles per node on average) use chunks of 4 (more independent chains),
+  // the others DESC4_CHUNK (fewer full searches); measured per level at cfg5
+  // 2^30 and at the paper's n = 10^7
+  const uint32_t ntl = te - tb;
+  const uint32_t chunk = ntl < DESC4_SERIAL_MIN ? 1u
+                         : ntl < 4u * DESC4_SERIAL_MIN ? 2u
+                         : (le > ls && ntl < 8u * (le - ls)) ? 4u : DESC4_CHUNK;
   const uint32_t nchunks = (te - tb + chunk - 1) / chunk;
   for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks; ch += gridDim.x * blockDim.x) {
     const uint32_t tau0 = tb + ch * chunk;
