@@ -377,18 +377,22 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
     uint32_t ia = ka0 + l, ib = kb0 + d - l;
     const uint32_t ea = ka0 + nA, eb = kb0 + nB;
     K ka = SK[ia], kb = SK[ib];
+    typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load
     K rk[KQ];
     uint32_t ri[KQ];
 #pragma unroll
     for (int q = 0; q < KQ; ++q) {
-      const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
+      const bool pa = ib >= eb || (ia < ea && oa <= ob);
       rk[q] = pa ? ka : kb;
       ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
       ia += pa ? 1u : 0u;
       ib += pa ? 0u : 1u;
       const K nx = SK[pa ? ia : ib];
+      const typename KeyTraits<KT>::O onx = T::ord(nx);
       ka = pa ? nx : ka;
+      oa = pa ? onx : oa;
       kb = pa ? kb : nx;
+      ob = pa ? ob : onx;
     }
 #pragma unroll
     for (int q = 0; q < KQ; ++q) IKs[q0 + q] = rk[q];
@@ -413,16 +417,20 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
     uint32_t ia = ka0 + l, ib = kb0 + d - l;
     const uint32_t ea = ka0 + nA, eb = kb0 + nB;
     K ka = SK[ia], kb = SK[ib];
+    typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load
 #pragma unroll 1
     for (uint32_t pos = qs; pos < qe; ++pos) {
-      const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
+      const bool pa = ib >= eb || (ia < ea && oa <= ob);
       IKs[pos] = pa ? ka : kb;
       IIs[pos] = (uint16_t)(pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB));
       ia += pa ? 1u : 0u;
       ib += pa ? 0u : 1u;
       const K nx = SK[pa ? ia : ib];
+      const typename KeyTraits<KT>::O onx = T::ord(nx);
       ka = pa ? nx : ka;
+      oa = pa ? onx : oa;
       kb = pa ? kb : nx;
+      ob = pa ? ob : onx;
     }
   }
 }
@@ -459,19 +467,23 @@ __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IK
   const uint32_t l = corank<KT>(IKs, nA, IKs + n01, nB, d);
   uint32_t ia = l, ib = n01 + d - l;
   const uint32_t ea = n01, eb = T4;
-  K ka = IKs[ia], kb = IKs[ib];  // reads past T4 stay inside the intermediate (slack)
+  K ka = IKs[ia], kb = IKs[ib];
+    typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load  // reads past T4 stay inside the intermediate (slack)
   K rk[(uint32_t)KQ];
   uint32_t ri[(uint32_t)KQ];
 #pragma unroll
   for (int q = 0; q < KQ; ++q) {
-    const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
+    const bool pa = ib >= eb || (ia < ea && oa <= ob);
     rk[q] = pa ? ka : kb;
     ri[q] = pa ? ia : ib;
     ia += pa ? 1u : 0u;
     ib += pa ? 0u : 1u;
     const K nx = IKs[pa ? ia : ib];
+      const typename KeyTraits<KT>::O onx = T::ord(nx);
     ka = pa ? nx : ka;
+      oa = pa ? onx : oa;
     kb = pa ? kb : nx;
+      ob = pa ? ob : onx;
   }
   uint32_t rv[(uint32_t)KQ];
   if (qs == start && start + (uint32_t)KQ <= hi) {
@@ -545,18 +557,22 @@ __device__ __forceinline__ void merge4_direct(const typename KeyTraits<KT>::K* S
   uint32_t ia = ka0 + l, ib = kb0 + d - l;
   const uint32_t ea = ka0 + nA, eb = kb0 + nB;
   K ka = SK[ia], kb = SK[ib];
+    typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load
   K rk[KQ];
   uint32_t ri[KQ];
 #pragma unroll
   for (int q = 0; q < KQ; ++q) {
-    const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
+    const bool pa = ib >= eb || (ia < ea && oa <= ob);
     rk[q] = pa ? ka : kb;
     ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
     ia += pa ? 1u : 0u;
     ib += pa ? 0u : 1u;
     const K nx = SK[pa ? ia : ib];
+      const typename KeyTraits<KT>::O onx = T::ord(nx);
     ka = pa ? nx : ka;
+      oa = pa ? onx : oa;
     kb = pa ? kb : nx;
+      ob = pa ? ob : onx;
   }
   if (qs == start && start + (uint32_t)KQ <= hi) {
     store_chunk_g<KQ>(dk + start, rk);
