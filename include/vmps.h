@@ -257,10 +257,10 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
  * vmps_sort_records: n records of `words` u32 each (row-major, device),
  * ordered lexicographically with word 0 most significant (the paper's blob
  * types: arrays of 30 ints ordered lexicographically), sorted
- * stably.  The engine sorts (64-bit word-pair key, u32 index) pairs: the
- * leading pair first, and, only if two records tie on it, an LSD pass per
- * word pair from the last to the first (pairs equal in every record are
- * skipped); then one gather writes records_out (may be NULL; must not alias
+ * stably.  The engine sorts (64-bit word-pair key, u32 index) pairs: by the
+ * first word pair that is not equal in every record, and, only if two
+ * records tie on it while a later pair varies, an LSD pass per varying word
+ * pair from the last to that one; then one gather writes records_out (may be NULL; must not alias
  * records).  perm_out (may be NULL, u32[n]) receives the permutation: the
  * paper's `ptr` type (pointers sorted by their arrays).  n < 2^32.
  * Workspace: vmps_sort_records_workspace_bytes.  May synchronise `stream`

@@ -4,13 +4,14 @@
 // stably.  The records themselves move once: the engine sorts (key, u32
 // index) pairs and one gather kernel writes the permuted records.
 //
-// Keys are 64-bit word pairs (w, w + 1).  Pass 1 sorts by the leading pair;
-// if no two adjacent sorted keys are equal, that order is already the
+// Keys are 64-bit word pairs (w, w + 1).  The deciding pair f is the first
+// one not equal in every record (pair 0 unless it is constant; then one scan
+// finds the constant pairs).  One stable sort by pair f; if no two adjacent
+// sorted keys are equal, or every later pair is constant, that order is the
 // lexicographic one.  Otherwise the order is rebuilt LSD-style from the
-// original sequence: one stable pass per word pair from the last to the
-// first (keys gathered through the current permutation), skipping pairs that
-// are equal in every record (a stable sort by a constant key is the
-// identity) -- e.g. zeroBlob30 needs only its last pair.
+// input order: one stable pass per non-constant word pair from the last to
+// f (keys gathered through the current permutation) -- a stable sort by a
+// constant key is the identity.  randomBlob30 and zeroBlob30 take one sort.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,6 +42,20 @@ __global__ void k_rec_pair_key(const uint32_t* __restrict__ rec, uint32_t words,
     diff |= k != k0;
   }
   if (__any_sync(0xFFFFFFFFu, diff) && (threadIdx.x & 31u) == 0) atomicOr(flags, 1u);
+}
+
+// mask |= bit q for every word pair q (< 64) that differs from record 0's
+__global__ void k_rec_const_pairs(const uint32_t* __restrict__ rec, uint32_t words, uint64_t n,
+                                  unsigned long long* __restrict__ mask) {
+  const uint32_t np = min((words + 1) / 2, 64u);
+  unsigned long long m = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t* r = rec + i * words;
+    for (uint32_t w = 0; w < 2 * np && w < words; ++w)
+      if (r[w] != rec[w]) m |= 1ull << (w / 2);
+  }
+  for (int o = 16; o; o >>= 1) m |= __shfl_xor_sync(0xFFFFFFFFu, m, o);
+  if ((threadIdx.x & 31u) == 0 && m) atomicOr(mask, m);
 }
 
 // flags[1] |= some adjacent keys are equal
@@ -116,26 +131,54 @@ vmps_status_t vmps_sort_records(const uint32_t* records, uint32_t* records_out, 
   const size_t sws_bytes = need - (al(n * 4 + 16) + al(n * 8 + 16) + al(64) + 256);
   const unsigned g = grid(n);
   uint32_t hf[2] = {0, 0};
-  // pass 1: leading word pair
-  k_rec_iota<<<g, 256, 0, s>>>(idx, n);
-  RK(cudaMemsetAsync(flags, 0, 8, s));
-  k_rec_pair_key<<<g, 256, 0, s>>>(records, words, 0, idx, key, n, flags);
-  if (n > 1) RV(vmps_sort_pairs(key, idx, n, VMPS_KEY_U64, VMPS_SCRATCH_UNBOUNDED, sws, sws_bytes, s, nullptr));
-  if (words > 2 && n > 1) {
-    k_rec_ties<<<g, 256, 0, s>>>(key, n, flags);
+  const uint32_t npairs = (words + 1) / 2;
+  unsigned long long* dmask = (unsigned long long*)(flags + 4);
+  auto pair_key = [&](uint32_t q) -> vmps_status_t {  // key of word pair q through idx; hf[0] = not constant
+    RK(cudaMemsetAsync(flags, 0, 8, s));
+    k_rec_pair_key<<<g, 256, 0, s>>>(records, words, 2 * q, idx, key, n, flags);
     RK(cudaMemcpyAsync(hf, flags, 8, cudaMemcpyDeviceToHost, s));
     RK(cudaStreamSynchronize(s));
-    if (hf[1]) {
-      // LSD over word pairs from the original order
-      k_rec_iota<<<g, 256, 0, s>>>(idx, n);
-      const uint32_t last = (words - 1) & ~1u;
-      for (int64_t w = last; w >= 0; w -= 2) {
-        RK(cudaMemsetAsync(flags, 0, 4, s));
-        k_rec_pair_key<<<g, 256, 0, s>>>(records, words, (uint32_t)w, idx, key, n, flags);
-        RK(cudaMemcpyAsync(hf, flags, 4, cudaMemcpyDeviceToHost, s));
-        RK(cudaStreamSynchronize(s));
-        if (!hf[0]) continue;  // constant pair: identity
-        RV(vmps_sort_pairs(key, idx, n, VMPS_KEY_U64, VMPS_SCRATCH_UNBOUNDED, sws, sws_bytes, s, nullptr));
+    return VMPS_OK;
+  };
+  k_rec_iota<<<g, 256, 0, s>>>(idx, n);
+  // the deciding pair: the first one that is not equal in every record
+  uint32_t f = 0;
+  unsigned long long mask = ~0ull;  // non-constant pairs (bit q), all unknown = set
+  bool known = false;
+  RV(pair_key(0));
+  if (!hf[0] && npairs > 1 && npairs <= 64) {
+    RK(cudaMemsetAsync(dmask, 0, 8, s));
+    k_rec_const_pairs<<<g, 256, 0, s>>>(records, words, n, dmask);
+    RK(cudaMemcpyAsync(&mask, dmask, 8, cudaMemcpyDeviceToHost, s));
+    RK(cudaStreamSynchronize(s));
+    known = true;
+    if (!mask) f = npairs;  // every record equal: the identity
+    else {
+      f = (uint32_t)__builtin_ctzll(mask);
+      RV(pair_key(f));
+    }
+  } else if (!hf[0] && npairs > 64) {
+    // many words: no constant-pair scan, LSD below decides
+    f = 0;
+  }
+  if (f < npairs && n > 1) {
+    if (hf[0]) RV(vmps_sort_pairs(key, idx, n, VMPS_KEY_U64, VMPS_SCRATCH_UNBOUNDED, sws, sws_bytes, s, nullptr));
+    // later pairs matter only if some record pair ties on pair f
+    const bool later = known ? (mask >> (f + 1)) != 0ull : f + 1 < npairs;
+    if (later) {
+      RK(cudaMemsetAsync(flags + 1, 0, 4, s));
+      k_rec_ties<<<g, 256, 0, s>>>(key, n, flags);
+      RK(cudaMemcpyAsync(hf, flags, 8, cudaMemcpyDeviceToHost, s));
+      RK(cudaStreamSynchronize(s));
+      if (hf[1]) {
+        // LSD over the non-constant pairs from the last to f, from the input order
+        k_rec_iota<<<g, 256, 0, s>>>(idx, n);
+        for (int64_t q = (int64_t)npairs - 1; q >= (int64_t)f; --q) {
+          if (known && q < 64 && !((mask >> q) & 1ull)) continue;  // constant pair: identity
+          RV(pair_key((uint32_t)q));
+          if (!hf[0]) continue;
+          RV(vmps_sort_pairs(key, idx, n, VMPS_KEY_U64, VMPS_SCRATCH_UNBOUNDED, sws, sws_bytes, s, nullptr));
+        }
       }
     }
   }

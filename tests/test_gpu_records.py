@@ -45,6 +45,22 @@ def test_blob30(kind):
     _check(r, perm_only=(kind == "ptr"))
 
 
+def test_constant_leading_pairs():
+    """Pairs 0-1 equal in every record, pair 2 decides with ties, later pairs
+    vary (the LSD path over the non-constant pairs only)."""
+    rng = np.random.default_rng(9)
+    n = 8000
+    r = np.zeros((n, 9), np.uint32)
+    r[:, 0] = 7
+    r[:, 4] = rng.integers(0, 4, n)
+    r[:, 5] = rng.integers(0, 2, n)
+    r[:, 7] = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+    r[::11, 7] = 3
+    _check(r)
+    all_equal = np.tile(np.array([[1, 2, 3]], np.uint32), (500, 1))
+    _check(all_equal)
+
+
 @pytest.mark.parametrize("words", [1, 2, 3, 5])
 def test_word_counts(words):
     rng = np.random.default_rng(words)
