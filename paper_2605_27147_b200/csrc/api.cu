@@ -405,7 +405,8 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
     if (ok) {
       for (int q = 0; q < BD_GRAPH_ROUNDS; ++q) {
         k_bd_alloc<<<1, 1024, 0, cap>>>(st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
-        k_bd_merge<KT, HV><<<nsm() * 4, MERGE_BLOCK, 0, cap>>>(M, st, desc, w.Tin, w.Tout, w.pool, w.remain);
+        k_bd_merge<KT, HV><<<nsm() * 4, MERGE_BLOCK, 0, cap>>>(M, st, desc, w.Tin, w.Tout, w.pool, w.remain,
+                                                                w.dirty);
       }
       ok = cudaStreamEndCapture(cap, &rounds_graph) == cudaSuccess &&
            cudaGraphInstantiate(&rounds_exec, rounds_graph, 0) == cudaSuccess;
@@ -439,7 +440,7 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
     LAUNCH(k_bd_tile_desc<KT>, grid_for(total), 256, 0, s, M, w.Tin, w.run_start, w.seg_l, w.seg_r, w.blnodes,
            w.bm, w.btoff, desc);
     VMPS_CK(cudaMemsetAsync(w.dirty, 0, (size_t)(w.NB + 1) * 4, s));
-    LAUNCH(k_bd_mark, grid_for(total), 256, 0, s, desc, w.btoff, w.bm, w.P, w.dirty);
+    LAUNCH(k_bd_mark<KT>, grid_for(total), 256, 0, s, M, w.Tin, desc, w.btoff, w.bm, w.P, w.dirty);
     scan_u32(w.dirty, w.didx, w.NB + 1, w.scan_tmp, s);
     LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, grid_for(total)), 256, 0, s, M, desc, w.btoff, w.bm, w.dirty,
            w.didx, w.dlist, w.first_tile, w.remain, w.bD);
@@ -452,7 +453,8 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
       } else {
         for (int q = 0; q < 16; ++q) {
           LAUNCH(k_bd_alloc, 1, 1024, 0, s, st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
-          LAUNCH((k_bd_merge<KT, HV>), nsm() * 4, MERGE_BLOCK, 0, s, M, st, desc, w.Tin, w.Tout, w.pool, w.remain);
+          LAUNCH((k_bd_merge<KT, HV>), nsm() * 4, MERGE_BLOCK, 0, s, M, st, desc, w.Tin, w.Tout, w.pool, w.remain,
+                 w.dirty);
         }
       }
       uint32_t D = 0;

@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
     TileDesc D;
     D.par = 0;
     if (gl < i && loc == 0) {  // left gap: copy [gl, i)
+      D.par = 1;  // a gap tile: identity, moves only with a dirty block
       D.i = gl; D.j = i; D.k = i; D.lo = gl; D.hi = i; D.a0 = 0; D.a1 = i - gl;
       desc[tau] = D;
       continue;
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
     if (gl < i) --loc;
     const uint32_t nt = (k + P - 1) / P - i / P;
     if (loc >= nt) {  // right gap: copy [k, gh)
+      D.par = 1;
       D.i = k; D.j = gh; D.k = gh; D.lo = k; D.hi = gh; D.a0 = 0; D.a1 = gh - k;
       desc[tau] = D;
       continue;
@@ -171,13 +173,32 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
   }
 }
 
-// Dirty output blocks (touched by a tile), their list and first tiles,
-// and the per-block counters of elements to consume.
-__global__ void k_bd_mark(const TileDesc* __restrict__ desc, const uint32_t* __restrict__ toff,
-                          const uint32_t* __restrict__ m_ptr, uint32_t P, uint32_t* __restrict__ dirty) {
+// Dirty output blocks, their list and first tiles, and the per-block
+// counters of elements to consume.  A merge tile is an identity when every
+// element it outputs already sits at its output position: the whole node is
+// a concatenation (A's last <= B's first), or the tile takes only A elements
+// with no B element before it, or only B elements after all of A (the page
+// hand-over of P:514-515 in its in-place form).  A block is dirty iff a
+// non-identity merge tile writes into it; a clean block keeps its physical
+// home and its tiles are skipped: zero bytes moved.  (An element that leaves
+// a block makes that block's own output differ there, so dirty blocks only
+// ever consume inputs from dirty blocks.)
+template <int KT>
+__global__ void k_bd_mark(BdMem<KT> M, const uint32_t* __restrict__ Tin, TileDesc* __restrict__ desc,
+                          const uint32_t* __restrict__ toff, const uint32_t* __restrict__ m_ptr, uint32_t P,
+                          uint32_t* __restrict__ dirty) {
+  using T = KeyTraits<KT>;
   const uint32_t total = toff[*m_ptr];
-  for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x)
-    dirty[desc[tau].lo / P] = 1u;
+  for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x) {
+    const TileDesc d = desc[tau];
+    if (d.par == 1) continue;  // gap tile
+    const uint32_t nA = d.j - d.i, nAt = d.a1 - d.a0, nBt = (d.hi - d.lo) - nAt;
+    const uint32_t b0 = (d.lo - d.i) - d.a0;
+    bool ident = (nBt == 0 && b0 == 0) || (nAt == 0 && d.a0 == nA);
+    if (!ident && nA > 0 && d.k > d.j)
+      ident = T::ord(bd_key<KT>(M, Tin, d.j - 1)) <= T::ord(bd_key<KT>(M, Tin, d.j));
+    if (!ident) dirty[d.lo / P] = 1u;
+  }
 }
 
 template <int KT>
@@ -196,7 +217,7 @@ __global__ void k_bd_dirty_list(BdMem<KT> M, const TileDesc* __restrict__ desc, 
   }
   for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x) {
     const uint32_t v = desc[tau].lo / P;
-    if (tau == 0 || desc[tau - 1].lo / P != v) first_tile[didx[v]] = tau;
+    if (dirty[v] && (tau == 0 || desc[tau - 1].lo / P != v)) first_tile[didx[v]] = tau;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const uint32_t D = didx[NB];
@@ -269,7 +290,8 @@ template <int KT, bool HV>
 __global__ void __launch_bounds__(MERGE_BLOCK) k_bd_merge(BdMem<KT> M, BdState* st, const TileDesc* __restrict__ desc,
                                                           const uint32_t* __restrict__ Tin,
                                                           const uint32_t* __restrict__ Tout, uint32_t* __restrict__ pool,
-                                                          uint32_t* __restrict__ remain) {
+                                                          uint32_t* __restrict__ remain,
+                                                          const uint32_t* __restrict__ dirty) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
   __shared__ K sk[DEFAULT_TOUT];
@@ -278,6 +300,7 @@ __global__ void __launch_bounds__(MERGE_BLOCK) k_bd_merge(BdMem<KT> M, BdState* 
   const uint32_t P = M.P;
   for (uint32_t tau = tlo + blockIdx.x; tau < thi; tau += gridDim.x) {
     const TileDesc d = desc[tau];
+    if (!dirty[d.lo / P]) continue;  // clean block: stays where it is
     const uint32_t nA = d.a1 - d.a0, cnt = d.hi - d.lo, nB = cnt - nA;
     const uint32_t aoff = d.i + d.a0, boff = d.j + (d.lo - d.i) - d.a0;
     for (uint32_t q = threadIdx.x; q < cnt; q += MERGE_BLOCK) {

@@ -96,3 +96,46 @@ def test_bounded_budget_error(vm):
     with pytest.raises(vm.VmpsError) as e:
         vm.sort_(k, scratch=60)  # fewer than 6 blocks of the minimum 16 elements
     assert e.value.status == 3
+
+
+def _skip_input(rng, n, kind):
+    """Inputs whose merges leave whole blocks in place: runs over disjoint,
+    increasing value ranges (every merge a concatenation), and runs whose
+    heads / tails do not overlap the neighbour (identity prefix / suffix
+    tiles next to real merges)."""
+    if kind == "concat":
+        x = np.arange(n, dtype=np.int64) * 4
+        cuts = np.sort(rng.integers(1, n, max(1, n // 300)))
+        x[cuts] -= 1  # one descent per run: many runs, disjoint ranges
+        return x.astype(np.uint32)
+    x = np.empty(n, np.int64)
+    cuts = np.concatenate([[0], np.sort(rng.integers(1, n, max(1, n // 500))), [n]])
+    base = 0
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        L = b - a
+        # a run: a low prefix, a middle that overlaps the next run, a high suffix
+        seg = np.sort(rng.integers(base, base + 3 * L, L))
+        x[a:b] = seg
+        base += L  # next run starts inside this run's range: partial overlap
+    return x.astype(np.uint32)
+
+
+@pytest.mark.parametrize("kind", ["concat", "overlap"])
+def test_bounded_block_skip(vm, kind):
+    """Clean blocks (every output already in place) are skipped -- zero bytes
+    moved -- and the result still equals the oracle; concatenations need
+    almost no rounds."""
+    rng = np.random.default_rng(77 if kind == "concat" else 78)
+    try:
+        for trial in range(12):
+            blk = int(rng.choice([16, 32, 64]))
+            vm.test_set_tiles(64, 0, blk)
+            n = int(rng.integers(2000, 20000))
+            keys = _skip_input(rng, n, kind)
+            vals = np.arange(n, dtype=np.uint32)
+            st = bounded_vs_oracle(vm, keys, vals, scratch=int(rng.integers(6, 30)) * blk,
+                                   minrun=int(rng.choice([1, 4])))
+            if kind == "concat":
+                assert st["rounds"] <= st["levels_executed"] + 2, st
+    finally:
+        vm.test_set_tiles(0, 0, 0)
