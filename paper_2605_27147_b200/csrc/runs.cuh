@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
   __shared__ uint32_t la[RT_WORDS], ld[RT_WORDS];
   __shared__ uint32_t ts[32 * 4];
   __shared__ uint32_t wsum[4];
-  __shared__ uint32_t s_idx0, s_total, s_rev;
+  __shared__ uint32_t s_idx0, s_rev;
   const uint32_t tile = blockIdx.x;
   const uint32_t T0 = tile * RT;
   const uint32_t L = min((uint32_t)RT, n - T0);
@@ -552,7 +552,6 @@ __global__ void __launch_bounds__(128) k_runs_emit(const uint32_t* __restrict__ 
       ended = (st != ST_END) && out == ST_END;
     }
     s_idx0 = (uint32_t)e;
-    s_total = cnt;
     s_rev = rev_open;
     if (ended) {
       scalars[SC_RUNS] = (uint32_t)e + cnt;
