@@ -23,7 +23,8 @@
  *     total order in which -0.0 precedes +0.0, every NaN is greater than every
  *     non-NaN and all NaNs compare equal (stable among themselves); output
  *     keys keep their bit patterns (reading R5).
- *   - n < 2^32 per call (32-bit positions inside the library); larger n
+ *   - n <= VMPS_MAX_N = 2^32 - 2^16 per call (32-bit positions inside the
+ *     library, with headroom for position + tile / minrun sums); larger n
  *     returns VMPS_ERR_INVALID_ARG.
  *   - Ownership: keys, vals and ws are caller-owned and must stay valid until
  *     the work enqueued on `stream` completes.  The library allocates no
@@ -34,7 +35,7 @@
  *     non-NULL h_stats / h_num_runs synchronises `stream` to read results.
  *   - Errors: arguments are validated before anything is enqueued.
  *       VMPS_ERR_INVALID_ARG  NULL pointer with n > 1, unknown key type,
- *                             n >= 2^32, misaligned pointer (keys/vals must be
+ *                             n > VMPS_MAX_N, misaligned pointer (keys/vals must be
  *                             16-byte aligned), cap_runs too small (the needed
  *                             count is still written to *h_num_runs);
  *       VMPS_ERR_BUDGET       ws_bytes smaller than vmps_workspace_bytes(), or
@@ -54,6 +55,8 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+
+#define VMPS_MAX_N 4294901760ull /* 2^32 - 2^16: the largest n of one call */
 
 typedef enum { VMPS_KEY_U32 = 0, VMPS_KEY_U64 = 1, VMPS_KEY_F32 = 2 } vmps_key_t;
 
@@ -181,7 +184,7 @@ vmps_status_t vmps_count_rank(const void* keys, uint64_t n, vmps_key_t kt, const
  * key (NULL for shard 0); d_halo: the next n_halo <= 136 keys of the global
  * array after this shard (>= minrun + 2 of them unless the array ends
  * sooner), so runs crossing the shard end are classified exactly.  d_table:
- * device, 3 minrun u64.  n_local < 2^32 - 256.
+ * device, 3 minrun u64.  n_local <= VMPS_MAX_N.
  *
  * vmps_shard_runs: with the chain state at the shard start (composition of the
  * previous shards' tables from START(0)), writes the shard's `count` run
@@ -262,7 +265,7 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
  * records tie on it while a later pair varies, an LSD pass per varying word
  * pair from the last to that one; then one gather writes records_out (may be NULL; must not alias
  * records).  perm_out (may be NULL, u32[n]) receives the permutation: the
- * paper's `ptr` type (pointers sorted by their arrays).  n < 2^32.
+ * paper's `ptr` type (pointers sorted by their arrays).  n <= VMPS_MAX_N.
  * Workspace: vmps_sort_records_workspace_bytes.  May synchronise `stream`
  * (tie check).  Error detail: vmps_records_last_error(). */
 vmps_status_t vmps_sort_records_workspace_bytes(uint64_t n, uint32_t words, size_t* h_bytes);

@@ -757,8 +757,8 @@ static vmps_status_t check_common(const void* keys, const void* vals, uint64_t n
     g_err = "unknown key type";
     return VMPS_ERR_INVALID_ARG;
   }
-  if (n >= (1ull << 32)) {
-    g_err = "n >= 2^32 is not supported";
+  if (n > VMPS_MAX_N) {
+    g_err = "n > VMPS_MAX_N (2^32 - 2^16) is not supported";
     return VMPS_ERR_INVALID_ARG;
   }
   if (n > 1 && !keys) {
@@ -778,7 +778,7 @@ vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, int6
                                    size_t* h_bytes) {
   if (!h_bytes) return VMPS_ERR_INVALID_ARG;
   if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
-  if (n >= (1ull << 32)) return VMPS_ERR_INVALID_ARG;
+  if (n > VMPS_MAX_N) return VMPS_ERR_INVALID_ARG;
   if (n <= 1) { *h_bytes = 256; return VMPS_OK; }
   Cfg c = make_cfg(n, kt, has_vals < 0 ? -1 : (has_vals ? 1 : 0), scratch_elems);
   *h_bytes = carve(c, nullptr, nullptr) + 256;
@@ -952,8 +952,8 @@ vmps_status_t vmps_merge_plan(const void* keys, uint64_t n, vmps_key_t kt, uint6
 
 static bool shard_args_ok(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun, uint32_t n_halo) {
   if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) { g_err = "unknown key type"; return false; }
-  if (n_local < 1 || n_local >= (1ull << 32) - 256 || !keys) {
-    g_err = "shard: need 1 <= n_local < 2^32 - 256 keys";
+  if (n_local < 1 || n_local > VMPS_MAX_N || !keys) {
+    g_err = "shard: need 1 <= n_local <= VMPS_MAX_N keys";
     return false;
   }
   if (minrun < 1 || minrun > MAX_MINRUN) { g_err = "shard: minrun out of range"; return false; }
@@ -969,7 +969,7 @@ static Cfg shard_cfg(uint64_t n_local, vmps_key_t kt, uint32_t minrun) {
 }
 
 vmps_status_t vmps_shard_workspace_bytes(uint64_t n_local, vmps_key_t kt, uint32_t minrun, size_t* h_bytes) {
-  if (!h_bytes || n_local < 1 || n_local >= (1ull << 32) - 256 || minrun < 1 || minrun > MAX_MINRUN)
+  if (!h_bytes || n_local < 1 || n_local > VMPS_MAX_N || minrun < 1 || minrun > MAX_MINRUN)
     return VMPS_ERR_INVALID_ARG;
   *h_bytes = carve(shard_cfg(n_local, kt, minrun), nullptr, nullptr) + 256;
   return VMPS_OK;
@@ -1349,7 +1349,7 @@ vmps_status_t vmps_merge_runs_workspace_bytes(uint64_t n, vmps_key_t kt, int has
                                               size_t* h_bytes) {
   if (!h_bytes || nruns == 0) return VMPS_ERR_INVALID_ARG;
   if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
-  if (n >= (1ull << 32)) return VMPS_ERR_INVALID_ARG;
+  if (n > VMPS_MAX_N) return VMPS_ERR_INVALID_ARG;
   *h_bytes = mr_layout(n, kt, has_vals ? 1 : 0, nruns).total + 256;
   return VMPS_OK;
 }

@@ -403,7 +403,7 @@ const char* vmps_comm_last_error(void) { return c_err.c_str(); }
 
 vmps_status_t vmps_dist_workspace_bytes(uint64_t n_local, vmps_key_t kt, int has_vals, int world,
                                         int64_t scratch_elems, size_t* h_bytes) {
-  if (!h_bytes || world < 1 || n_local >= (1ull << 32)) return VMPS_ERR_INVALID_ARG;
+  if (!h_bytes || world < 1 || n_local > VMPS_MAX_N) return VMPS_ERR_INVALID_ARG;
   *h_bytes = dist_layout(n_local, kt, has_vals ? 1 : 0, world, scratch_elems).total;
   return VMPS_OK;
 }
@@ -422,7 +422,7 @@ vmps_status_t vmps_sort_pairs_dist(vmps_comm_t c, void* keys, uint32_t* vals, ui
 
 vmps_status_t vmps_merge_plan_dist_workspace_bytes(uint64_t n_total, uint64_t n_local, vmps_key_t kt, int world,
                                                    size_t* h_bytes) {
-  if (!h_bytes || world < 1 || n_local > n_total || n_local >= (1ull << 32) - 256) return VMPS_ERR_INVALID_ARG;
+  if (!h_bytes || world < 1 || n_local > n_total || n_local > VMPS_MAX_N) return VMPS_ERR_INVALID_ARG;
   *h_bytes = plan_layout(n_total, n_local, kt, world).total;
   return VMPS_OK;
 }
@@ -433,7 +433,7 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
                                    void* ws, size_t ws_bytes, void* stream) {
   if (!c || !h_num_runs_local || !h_num_merges_local) return VMPS_ERR_INVALID_ARG;
   if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
-  if (n_local >= (1ull << 32) - 256) { c_err = "n_local >= 2^32 - 256"; return VMPS_ERR_INVALID_ARG; }
+  if (n_local > VMPS_MAX_N) { c_err = "n_local > VMPS_MAX_N"; return VMPS_ERR_INVALID_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
   const int g = c->world, me = c->rank;
   const size_t kb = kbytes(kt);

@@ -105,7 +105,7 @@ unsigned grid(uint64_t items) {
 extern "C" {
 
 vmps_status_t vmps_sort_records_workspace_bytes(uint64_t n, uint32_t words, size_t* h_bytes) {
-  if (!h_bytes || words == 0 || n >= (1ull << 32)) return VMPS_ERR_INVALID_ARG;
+  if (!h_bytes || words == 0 || n > VMPS_MAX_N) return VMPS_ERR_INVALID_ARG;
   size_t sb = 0;
   if (n > 1 && vmps_workspace_bytes(n, VMPS_KEY_U64, 1, VMPS_SCRATCH_UNBOUNDED, &sb) != VMPS_OK)
     return VMPS_ERR_INVALID_ARG;
@@ -115,7 +115,7 @@ vmps_status_t vmps_sort_records_workspace_bytes(uint64_t n, uint32_t words, size
 
 vmps_status_t vmps_sort_records(const uint32_t* records, uint32_t* records_out, uint32_t* perm_out, uint64_t n,
                                 uint32_t words, void* ws, size_t ws_bytes, void* stream) {
-  if (words == 0 || n >= (1ull << 32)) { r_err = "need words >= 1 and n < 2^32"; return VMPS_ERR_INVALID_ARG; }
+  if (words == 0 || n > VMPS_MAX_N) { r_err = "need words >= 1 and n <= VMPS_MAX_N"; return VMPS_ERR_INVALID_ARG; }
   if (n && (!records || (!records_out && !perm_out))) { r_err = "NULL records / outputs"; return VMPS_ERR_INVALID_ARG; }
   if (records_out && records_out == records) { r_err = "records_out must not alias records"; return VMPS_ERR_INVALID_ARG; }
   if (n == 0) return VMPS_OK;
