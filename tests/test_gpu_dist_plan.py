@@ -129,3 +129,22 @@ def test_large_sharded(vm):
     rng = np.random.default_rng(7)
     cuts = sorted(set(int(c) for c in rng.integers(1, len(glob), 7)))
     _check(vm, glob, cuts)
+
+
+@pytest.mark.parametrize("N,r", [((1 << 33) + 12345, 200_003), ((1 << 36) - 7, 50_000), (10 ** 9 + 7, 1)])
+def test_plan_from_runs_global_n(vm, N, r):
+    """vmps_plan_from_runs on 64-bit global positions (the concatenation of
+    shards can exceed 2^32 elements) vs the oracle's Alg. 1 policy on the
+    same run starts (powers P:445-446 with the global n)."""
+    rng = np.random.default_rng(r)
+    if r == 1:
+        starts = np.array([0], np.uint64)
+    else:
+        cuts = np.unique(rng.integers(1, N, r - 1, dtype=np.uint64))
+        starts = np.concatenate([[0], cuts]).astype(np.uint64)
+    d = torch.from_numpy(np.concatenate([starts, [N]]).astype(np.int64)).cuda()
+    got = vm.plan_from_runs(d, N).cpu().numpy()
+    mg, _ = oracle.policy(N, starts)
+    want = np.stack([mg["i"], mg["j"], mg["k"], mg["power"]], axis=1).astype(np.int64) if len(mg) else \
+        np.zeros((0, 4), np.int64)
+    assert got.shape == want.shape and (got == want).all()
