@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--leaf-radix", action="store_true",
                     help="experimental: radix-sort leaf engine instead of the block merge sort")
     ap.add_argument("--fuse-z", type=int, default=0, help="experimental: fused-subtree limit Z")
+    ap.add_argument("--pull-dist", action="store_true",
+                    help="N>1: pull-merge the co-ranked pieces from peer memory (dist.sort_dist_pull)")
     ap.add_argument("--native-dist", action="store_true",
                     help="N>1: the library's own NCCL protocol (vmps_sort_pairs_dist) instead of dist.py")
     ap.add_argument("--bounded-reps", type=int, default=2,
@@ -222,6 +224,14 @@ def main():
 
         def do_sort():
             vm.sort_dist_native_(ncomm, keys, vals, workspace=ws)
+    elif world > 1 and args.pull_dist:
+        # exchange fused with the final merge: pieces read from peer memory
+        from paper_2605_27147_b200.dist import sort_dist_pull
+
+        def do_sort():
+            res = sort_dist_pull(keys, vals)
+            keys.copy_(res.keys)
+            vals.copy_(res.vals)
     elif world > 1:
         from paper_2605_27147_b200.dist import sort_dist_
 

@@ -256,6 +256,33 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
                                    uint64_t cap_runs, uint64_t* h_num_runs_local, uint64_t* h_num_merges_local,
                                    void* ws, size_t ws_bytes, void* stream);
 
+/* ---- pull-merge (csrc/engine4.cuh k_pull_merge) ----
+ * vmps_merge_pieces: the stable merge of g (1..8) sorted pieces that live at
+ * arbitrary device addresses -- on a multi-GPU box the co-ranked pieces of
+ * the other ranks' shards, mapped with vmps_ipc_open (CUDA IPC over NVLink)
+ * -- written once into out_keys / out_vals [0, N), N = sum of h_counts.
+ * Ties go to the lower piece index (the lower source rank).  h_keys /
+ * h_vals / h_counts are host arrays of g entries; h_vals and out_vals may be
+ * NULL (keys only).  Pieces are read by TMA bulk copies aligned down / up to
+ * 16 bytes, so each piece must lie in an allocation that covers those bytes
+ * (any cudaMalloc allocation does).  g <= 4: one pass of the 4-way engine;
+ * g <= 8: two such passes into the two halves of the output, then one local
+ * 2-way merge (vmps_merge_runs).  Workspace:
+ * vmps_merge_pieces_workspace_bytes.
+ *
+ * vmps_ipc_handle: the CUDA IPC handle (64 bytes) of the allocation holding
+ * d_ptr and d_ptr's offset in it; vmps_ipc_open maps a peer's handle and
+ * returns base + offset; vmps_ipc_close unmaps (pass the same offset).
+ * Errors: VMPS_ERR_CUDA with detail in vmps_comm_last_error(). */
+vmps_status_t vmps_merge_pieces_workspace_bytes(uint64_t n_total, vmps_key_t kt, int has_vals, uint32_t g,
+                                                size_t* h_bytes);
+vmps_status_t vmps_merge_pieces(const void* const* h_keys, const uint32_t* const* h_vals, const uint64_t* h_counts,
+                                uint32_t g, void* out_keys, uint32_t* out_vals, vmps_key_t kt, void* ws,
+                                size_t ws_bytes, void* stream);
+vmps_status_t vmps_ipc_handle(const void* d_ptr, void* h_handle64, uint64_t* h_offset);
+vmps_status_t vmps_ipc_open(const void* h_handle64, uint64_t offset, void** h_ptr);
+vmps_status_t vmps_ipc_close(void* d_ptr, uint64_t offset);
+
 /* ---- large records (paper_2605_27147_b200/csrc/records.cu) ----
  * vmps_sort_records: n records of `words` u32 each (row-major, device),
  * ordered lexicographically with word 0 most significant (the paper's blob

@@ -63,7 +63,8 @@ EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_me
            "vmps_plan_from_runs", "vmps_comm_unique_id", "vmps_comm_init", "vmps_comm_destroy",
            "vmps_comm_last_error", "vmps_dist_workspace_bytes", "vmps_sort_keys_dist", "vmps_sort_pairs_dist",
            "vmps_merge_plan_dist_workspace_bytes", "vmps_merge_plan_dist", "vmps_sort_records_workspace_bytes",
-           "vmps_sort_records", "vmps_records_last_error")
+           "vmps_sort_records", "vmps_records_last_error", "vmps_merge_pieces_workspace_bytes",
+           "vmps_merge_pieces", "vmps_ipc_handle", "vmps_ipc_open", "vmps_ipc_close")
 
 _lib = None
 
@@ -103,6 +104,14 @@ def lib() -> ctypes.CDLL:
         L.vmps_merge_plan_dist_workspace_bytes.argtypes = [u64, u64, ci, ci, ctypes.POINTER(sz)]
         L.vmps_merge_plan_dist.argtypes = [vp, vp, u64, ci, vp, vp, vp, u64, ctypes.POINTER(u64),
                                            ctypes.POINTER(u64), vp, sz, vp]
+        L.vmps_merge_pieces_workspace_bytes.argtypes = [u64, ci, ci, u32, ctypes.POINTER(sz)]
+        L.vmps_merge_pieces.argtypes = [vp, vp, vp, u32, vp, vp, ci, vp, sz, vp]
+        L.vmps_ipc_handle.argtypes = [vp, vp, ctypes.POINTER(u64)]
+        L.vmps_ipc_open.argtypes = [vp, u64, ctypes.POINTER(vp)]
+        L.vmps_ipc_close.argtypes = [vp, u64]
+        for f in ("vmps_merge_pieces_workspace_bytes", "vmps_merge_pieces", "vmps_ipc_handle", "vmps_ipc_open",
+                  "vmps_ipc_close"):
+            getattr(L, f).restype = ctypes.c_int
         L.vmps_sort_records_workspace_bytes.argtypes = [u64, u32, ctypes.POINTER(sz)]
         L.vmps_sort_records.argtypes = [vp, vp, vp, u64, u32, vp, sz, vp]
         L.vmps_records_last_error.restype = ctypes.c_char_p
@@ -403,6 +412,51 @@ def sort_records(records: torch.Tensor, out: torch.Tensor | None = None, perm: b
     if rc != 0:
         raise VmpsError(rc, "vmps_sort_records", L.vmps_records_last_error().decode())
     return (res, pm) if perm else res
+
+
+def merge_pieces(key_ptrs: list[int], val_ptrs: list[int] | None, counts: list[int], out_keys: torch.Tensor,
+                 out_values: torch.Tensor | None = None, workspace: Workspace | None = None) -> None:
+    """vmps_merge_pieces: stable merge of g <= 8 sorted pieces given as device
+    addresses (local tensors' data_ptr() or peer mappings from ipc_open) into
+    out_keys / out_values, ties to the lower piece."""
+    g = len(counts)
+    kt = key_type(out_keys)
+    dev = out_keys.device
+    N = sum(counts)
+    L = lib()
+    nb = ctypes.c_size_t(0)
+    _check(L.vmps_merge_pieces_workspace_bytes(N, kt, 1 if out_values is not None else 0, g, ctypes.byref(nb)),
+           "vmps_merge_pieces_workspace_bytes")
+    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    buf = ws.get(int(nb.value), dev)
+    kp = (ctypes.c_void_p * g)(*key_ptrs)
+    vpa = (ctypes.c_void_p * g)(*val_ptrs) if val_ptrs is not None else None
+    cn = (ctypes.c_uint64 * g)(*counts)
+    with torch.cuda.device(dev):
+        rc = L.vmps_merge_pieces(kp, vpa, cn, g, out_keys.data_ptr(),
+                                 None if out_values is None else out_values.data_ptr(), kt, buf.data_ptr(),
+                                 buf.numel(), _stream_ptr(dev))
+    _check(rc, "vmps_merge_pieces")
+
+
+def ipc_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, t's byte offset in it)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_uint64(0)
+    _check_comm(lib().vmps_ipc_handle(t.data_ptr(), h, ctypes.byref(off)), "vmps_ipc_handle")
+    return h.raw, int(off.value)
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    """Map a peer allocation (vmps_ipc_open); returns the device address."""
+    p = ctypes.c_void_p()
+    _check_comm(lib().vmps_ipc_open(ctypes.create_string_buffer(bytes(handle), 64), offset, ctypes.byref(p)),
+                "vmps_ipc_open")
+    return int(p.value)
+
+
+def ipc_close(ptr: int, offset: int) -> None:
+    _check_comm(lib().vmps_ipc_close(ptr, offset), "vmps_ipc_close")
 
 
 # ---- native multi-GPU entry points (csrc/comm.cu) ----

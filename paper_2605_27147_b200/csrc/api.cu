@@ -1345,6 +1345,124 @@ vmps_status_t vmps_count_rank(const void* keys, uint64_t n, vmps_key_t kt, const
   return launch_check();
 }
 
+// ---- pull-merge of pieces at arbitrary addresses ----
+}  // extern "C"
+namespace vmps {
+template <int KT, bool HV>
+static vmps_status_t pull_pass(const void* const* kp, const uint32_t* const* vp, const uint64_t* cnt, uint32_t g,
+                               void* ok, uint32_t* ov, uint32_t base, TileDesc4* tiles, cudaStream_t s) {
+  using K = typename KeyTraits<KT>::K;
+  using SM4 = Merge4Smem<KT, HV>;
+  PullSrc<KT> S;
+  uint64_t N = 0;
+  for (int i = 0; i < 4; ++i) {
+    const bool on = (uint32_t)i < g && cnt[i] > 0;
+    S.kp[i] = on ? (const K*)kp[i] : nullptr;
+    S.vp[i] = (on && HV) ? vp[i] : nullptr;
+    S.n[i] = on ? (uint32_t)cnt[i] : 0u;
+    N += S.n[i];
+  }
+  S.N = (uint32_t)N;
+  S.base = base;
+  if (N == 0) return VMPS_OK;
+  static int occ[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  if (!occ[KT][HV]) {
+    VMPS_CK(cudaFuncSetAttribute(k_pull_merge<KT, HV, M4_KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SM4::BYTES));
+    int o = 0;
+    VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_pull_merge<KT, HV, M4_KQ>, 4096 / M4_KQ + 32,
+                                                          SM4::BYTES));
+    occ[KT][HV] = o > 0 ? o : 1;
+  }
+  const uint32_t ntiles = (uint32_t)((base + N + 4095) / 4096 - base / 4096);
+  const uint32_t nchunks = (ntiles + DESC4_CHUNK - 1) / DESC4_CHUNK;
+  LAUNCH(k_pull_desc<KT>, (nchunks + 255) / 256, 256, 0, s, S, ntiles, tiles);
+  LAUNCH((k_pull_merge<KT, HV, M4_KQ>), (unsigned)std::min<uint32_t>(ntiles, nsm() * occ[KT][HV]),
+         4096 / M4_KQ + 32, SM4::BYTES, s, S, (K*)ok, ov, tiles, ntiles);
+  return launch_check();
+}
+
+template <int KT, bool HV>
+static vmps_status_t pull_dispatch(const void* const* kp, const uint32_t* const* vp, const uint64_t* cnt,
+                                   uint32_t g, void* ok, uint32_t* ov, uint32_t base, TileDesc4* tiles,
+                                   cudaStream_t s) {
+  return pull_pass<KT, HV>(kp, vp, cnt, g, ok, ov, base, tiles, s);
+}
+}  // namespace vmps
+extern "C" {
+
+vmps_status_t vmps_merge_pieces_workspace_bytes(uint64_t n_total, vmps_key_t kt, int has_vals, uint32_t g,
+                                                size_t* h_bytes) {
+  if (!h_bytes || g < 1 || g > 8 || n_total > VMPS_MAX_N) return VMPS_ERR_INVALID_ARG;
+  if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
+  size_t b = align_up(((size_t)(n_total + 4095) / 4096 + 2) * sizeof(TileDesc4));
+  if (g > 4 && n_total > 1) {
+    size_t m = 0;
+    if (vmps_merge_runs_workspace_bytes(n_total, kt, has_vals, 2, &m) != VMPS_OK) return VMPS_ERR_INVALID_ARG;
+    b += align_up(m);
+  }
+  *h_bytes = b + 256;
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_merge_pieces(const void* const* h_keys, const uint32_t* const* h_vals, const uint64_t* h_counts,
+                                uint32_t g, void* out_keys, uint32_t* out_vals, vmps_key_t kt, void* ws,
+                                size_t ws_bytes, void* stream) {
+  if (!h_keys || !h_counts || g < 1 || g > 8) { g_err = "pieces: need 1..8 pieces"; return VMPS_ERR_INVALID_ARG; }
+  uint64_t N = 0;
+  for (uint32_t i = 0; i < g; ++i) {
+    if (h_counts[i] && (!h_keys[i] || (out_vals && (!h_vals || !h_vals[i])))) {
+      g_err = "pieces: NULL piece pointer";
+      return VMPS_ERR_INVALID_ARG;
+    }
+    N += h_counts[i];
+  }
+  vmps_status_t rc = check_common(out_keys, out_vals, N, kt);
+  if (rc != VMPS_OK) return rc;
+  size_t need = 0;
+  if (vmps_merge_pieces_workspace_bytes(N, kt, out_vals ? 1 : 0, g, &need) != VMPS_OK) return VMPS_ERR_INVALID_ARG;
+  if (!ws || ws_bytes < need) { g_err = "workspace too small"; return VMPS_ERR_BUDGET; }
+  if (N == 0) return VMPS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* base = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  TileDesc4* tiles = (TileDesc4*)base;
+  const size_t tb = align_up(((size_t)(N + 4095) / 4096 + 2) * sizeof(TileDesc4));  // >= tiles of either pass
+  const uint32_t* vnull[8] = {nullptr};
+  const uint32_t* const* vp = out_vals ? h_vals : vnull;
+  const size_t kb = key_bytes(kt);
+  uint64_t N1 = 0;
+  for (uint32_t i = 0; i < std::min<uint32_t>(g, 4); ++i) N1 += h_counts[i];
+  for (uint32_t part = 0; part < (g > 4 ? 2u : 1u); ++part) {
+    const uint32_t i0 = 4 * part, gg = std::min<uint32_t>(g - i0, 4);
+    // both passes write through the (aligned) output base; the second one's
+    // tiles start at position N1
+    char* okp = (char*)out_keys;
+    uint32_t* ovp = out_vals;
+    const uint32_t obase = part ? (uint32_t)N1 : 0u;
+    (void)kb;
+    if (out_vals) {
+      switch (kt) {
+        case VMPS_KEY_U32: rc = pull_dispatch<VMPS_KEY_U32, true>(h_keys + i0, vp + i0, h_counts + i0, gg, okp, ovp, obase, tiles, s); break;
+        case VMPS_KEY_U64: rc = pull_dispatch<VMPS_KEY_U64, true>(h_keys + i0, vp + i0, h_counts + i0, gg, okp, ovp, obase, tiles, s); break;
+        default: rc = pull_dispatch<VMPS_KEY_F32, true>(h_keys + i0, vp + i0, h_counts + i0, gg, okp, ovp, obase, tiles, s); break;
+      }
+    } else {
+      switch (kt) {
+        case VMPS_KEY_U32: rc = pull_dispatch<VMPS_KEY_U32, false>(h_keys + i0, vp + i0, h_counts + i0, gg, okp, nullptr, obase, tiles, s); break;
+        case VMPS_KEY_U64: rc = pull_dispatch<VMPS_KEY_U64, false>(h_keys + i0, vp + i0, h_counts + i0, gg, okp, nullptr, obase, tiles, s); break;
+        default: rc = pull_dispatch<VMPS_KEY_F32, false>(h_keys + i0, vp + i0, h_counts + i0, gg, okp, nullptr, obase, tiles, s); break;
+      }
+    }
+    if (rc != VMPS_OK) return rc;
+  }
+  if (g > 4 && N1 > 0 && N1 < N) {
+    const uint64_t st2[2] = {0, N1};
+    return vmps_merge_runs(out_keys, out_vals, N, kt, st2, 2, base + tb, ws_bytes - (size_t)(base - (char*)ws) - tb,
+                           stream);
+  }
+  return VMPS_OK;
+}
+
 vmps_status_t vmps_merge_runs_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, uint32_t nruns,
                                               size_t* h_bytes) {
   if (!h_bytes || nruns == 0) return VMPS_ERR_INVALID_ARG;

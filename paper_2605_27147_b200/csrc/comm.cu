@@ -20,6 +20,7 @@
 // NCCL calls.  NCCL is loaded with dlopen on first use (the process's
 // libnccl.so.2, e.g. the one torch already loaded), so the library has no
 // link-time NCCL dependency.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -400,6 +401,46 @@ vmps_status_t vmps_comm_destroy(vmps_comm_t c) {
 }
 
 const char* vmps_comm_last_error(void) { return c_err.c_str(); }
+
+// ---- peer mappings for the pull-merge (CUDA IPC over NVLink) ----
+vmps_status_t vmps_ipc_handle(const void* d_ptr, void* h_handle64, uint64_t* h_offset) {
+  if (!d_ptr || !h_handle64 || !h_offset) return VMPS_ERR_INVALID_ARG;
+  // the handle names the whole allocation holding d_ptr; the peer adds the offset
+  static CUresult (*get_range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+  if (!get_range) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      c_err = "cuMemGetAddressRange unavailable";
+      return VMPS_ERR_CUDA;
+    }
+    get_range = (CUresult(*)(CUdeviceptr*, size_t*, CUdeviceptr))fn;
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (CUdeviceptr)d_ptr) != CUDA_SUCCESS) { c_err = "cuMemGetAddressRange failed"; return VMPS_ERR_CUDA; }
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, (void*)base));
+  memcpy(h_handle64, &h, sizeof(h));
+  *h_offset = (uint64_t)((CUdeviceptr)d_ptr - base);
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_ipc_open(const void* h_handle64, uint64_t offset, void** h_ptr) {
+  if (!h_handle64 || !h_ptr) return VMPS_ERR_INVALID_ARG;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, h_handle64, sizeof(h));
+  void* p = nullptr;
+  CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *h_ptr = (char*)p + offset;
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_ipc_close(void* d_ptr, uint64_t offset) {
+  if (!d_ptr) return VMPS_OK;
+  CK(cudaIpcCloseMemHandle((char*)d_ptr - offset));
+  return VMPS_OK;
+}
 
 vmps_status_t vmps_dist_workspace_bytes(uint64_t n_local, vmps_key_t kt, int has_vals, int world,
                                         int64_t scratch_elems, size_t* h_bytes) {

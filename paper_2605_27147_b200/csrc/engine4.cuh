@@ -672,3 +672,192 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
 }
 
 }  // namespace vmps
+
+namespace vmps {
+// ---------------------------------------------------------------------------
+// Pull-merge: the stable merge of up to four sorted pieces
+// that live at four arbitrary device addresses -- on a multi-GPU box, the
+// co-ranked pieces of the other ranks' shards, read through peer mappings
+// (CUDA IPC over NVLink) -- written once into one output array.  It replaces
+// "all-to-all into a receive buffer, then merge the buffer": the pieces are
+// read straight from where they are, by the same TMA-staged 4-way engine.
+// Ties go to the lower piece index (the lower source rank).
+// ---------------------------------------------------------------------------
+template <int KT>
+struct PullSrc {
+  const typename KeyTraits<KT>::K* kp[4];
+  const uint32_t* vp[4];
+  uint32_t n[4];
+  uint32_t N;     // sum of n[]
+  uint32_t base;  // output position of the merge's first element (tiles align to global multiples of 4096)
+};
+
+// Tile descriptors at output positions base + d aligned to global multiples
+// of 4096 (chunks of DESC4_CHUNK tiles per thread, incremental searches as
+// k4_desc).
+template <int KT>
+__global__ void __launch_bounds__(256) k_pull_desc(PullSrc<KT> S, uint32_t ntiles, TileDesc4* __restrict__ tiles) {
+  const uint32_t nchunks = (ntiles + DESC4_CHUNK - 1) / DESC4_CHUNK;
+  for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks; ch += gridDim.x * blockDim.x) {
+    InnerCR<KT> L, R;
+    L.init(S.kp[0], S.n[0], S.kp[1], S.n[1]);
+    R.init(S.kp[2], S.n[2], S.kp[3], S.n[3]);
+    uint32_t aprev = 0, dprev = 0;
+    for (uint32_t q = 0; q < DESC4_CHUNK; ++q) {
+      const uint32_t tau = ch * DESC4_CHUNK + q;
+      if (tau >= ntiles) break;
+      const uint32_t d = tau == 0 ? 0u : (S.base / 4096u + tau) * 4096u - S.base;
+      uint32_t c[4];
+      const uint32_t av = corank4<KT>(L, R, d, aprev, aprev + (d - dprev), c);
+      aprev = av;
+      dprev = d;
+      TileDesc4 D;
+      D.x = 0;
+      D.rank = d;
+      D.c[0] = c[0]; D.c[1] = c[1]; D.c[2] = c[2]; D.c[3] = c[3];
+      tiles[tau] = D;
+    }
+  }
+}
+
+template <int KT, bool HV>
+__device__ __forceinline__ void pull_issue(const TileDesc4& d, const TileDesc4* dn_or_null, const PullSrc<KT>& S,
+                                           uint32_t s, unsigned char* smem, uint64_t* bars, Merge4Hdr* hdr) {
+  using SM = Merge4Smem<KT, HV>;
+  using K = typename KeyTraits<KT>::K;
+  uint32_t c1[4];
+  uint32_t rank1;
+  if (dn_or_null) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c1[i] = dn_or_null->c[i];
+    rank1 = dn_or_null->rank;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c1[i] = S.n[i];
+    rank1 = S.N;
+  }
+  unsigned char* st = smem + SM::HDR + s * SM::STAGE;
+  Merge4Hdr h;
+  uint32_t koff = 0, voff = 0, total = 0;
+  uintptr_t kg[4], vg[4];
+  uint32_t kbytes[4], vbytes[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t n = c1[i] - d.c[i];
+    const uintptr_t ga = (uintptr_t)(S.kp[i] + d.c[i]), ga0 = ga & ~(uintptr_t)15;
+    const uint32_t bk = n ? (uint32_t)(((ga + (uintptr_t)n * sizeof(K) + 15) & ~(uintptr_t)15) - ga0) : 0u;
+    h.kb[i] = (koff + (uint32_t)(ga - ga0)) / sizeof(K);
+    h.n[i] = n;
+    kg[i] = ga0;
+    kbytes[i] = bk;
+    koff += bk;
+    if (HV) {
+      const uintptr_t va = (uintptr_t)(S.vp[i] + d.c[i]), va0 = va & ~(uintptr_t)15;
+      const uint32_t bv = n ? (uint32_t)(((va + (uintptr_t)n * 4 + 15) & ~(uintptr_t)15) - va0) : 0u;
+      h.vb[i] = (voff + (uint32_t)(va - va0)) / 4;
+      vg[i] = va0;
+      vbytes[i] = bv;
+      voff += bv;
+    } else {
+      h.vb[i] = 0;
+    }
+    total += kbytes[i] + (HV ? vbytes[i] : 0u);
+  }
+  h.lo = S.base + d.rank;
+  h.hi = S.base + rank1;
+  h.par = 0;
+  {
+    const uint32_t nz = (h.n[0] != 0) + (h.n[1] != 0) + (h.n[2] != 0) + (h.n[3] != 0);
+    h.mode = nz == 1 ? 2u + (h.n[0] ? 0u : h.n[1] ? 1u : h.n[2] ? 2u : 3u)
+                     : ((h.n[1] == 0 && h.n[3] == 0) ? 1u : 0u);
+  }
+  hdr[s] = h;
+  mbar_arrive_expect_tx(&bars[s], total);
+  uint32_t o = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (kbytes[i]) bulk_g2s(st + o, (const void*)kg[i], kbytes[i], &bars[s]);
+    o += kbytes[i];
+  }
+  if (HV) {
+    o = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (vbytes[i]) bulk_g2s(st + SM::KB + o, (const void*)vg[i], vbytes[i], &bars[s]);
+      o += vbytes[i];
+    }
+  }
+}
+
+// Same consumer side as k4_merge_level; the producer stages the four pieces'
+// windows from their own addresses.  Output keys / values at [0, N).
+template <int KT, bool HV, int KQ>
+__global__ void __launch_bounds__(4096 / KQ + 32, 2) k_pull_merge(PullSrc<KT> S, typename KeyTraits<KT>::K* __restrict__ ok,
+                                                                   uint32_t* __restrict__ ov,
+                                                                   const TileDesc4* __restrict__ tiles, uint32_t count) {
+  using K = typename KeyTraits<KT>::K;
+  using SM = Merge4Smem<KT, HV>;
+  constexpr uint32_t NT = 4096 / KQ;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + 2;
+  Merge4Hdr* hdr = reinterpret_cast<Merge4Hdr*>(smem + 64);
+  K* IKs = reinterpret_cast<K*>(smem + SM::HDR + 2 * SM::STAGE);
+  uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + 2 * SM::STAGE + SM::IK);
+  if (blockIdx.x >= count) return;
+  const uint32_t tid = threadIdx.x;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], NT / 32);
+    mbar_init(&empty[1], NT / 32);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid >= NT) {  // producer warp
+    if (tid == NT) {
+      uint32_t it = 0;
+      for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
+        const uint32_t s = it & 1u;
+        if (it >= 2) mbar_wait_backoff(&empty[s], ((it >> 1) - 1) & 1u);
+        const TileDesc4 d = tiles[tau];
+        TileDesc4 dn;
+        const bool more = tau + 1 < count && (dn = tiles[tau + 1], true);
+        pull_issue<KT, HV>(d, more ? &dn : nullptr, S, s, smem, full, hdr);
+      }
+    }
+    return;
+  }
+  const uint32_t lane = tid & 31u;
+  uint32_t it = 0;
+  for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
+    const uint32_t s = it & 1u;
+    mbar_wait(&full[s], (it >> 1) & 1u);
+    const Merge4Hdr* hp = hdr + s;
+    const unsigned char* st = smem + SM::HDR + s * SM::STAGE;
+    const K* SK = reinterpret_cast<const K*>(st);
+    const uint32_t* SV = reinterpret_cast<const uint32_t*>(st + SM::KB);
+    const uint32_t lo = hp->lo, hi = hp->hi;
+    const uint32_t n01 = hp->n[0] + hp->n[1], T4 = hi - lo;
+    const uint32_t mode = hp->mode;
+    if (mode >= 2) {
+      const uint32_t wsrc = mode - 2;
+      merge4_copy<KT, HV, KQ>(SK, SV, hp->kb[wsrc], hp->vb[wsrc], lo, hi, 0u, ok, ov, ok, ov);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    } else if (mode == 1) {
+      merge4_direct<KT, HV, KQ>(SK, SV, hp, lo, hi, 0u, ok, ov, ok, ov);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    } else {
+      merge4_stepA<KT, KQ>(SK, hp, n01, T4, IKs, IIs);
+      named_bar_sync(1, NT);
+      merge4_stepB<KT, HV, KQ>(IKs, IIs, SV, lo, hi, 0u, n01, T4, ok, ov, ok, ov);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      named_bar_sync(1, NT);
+    }
+  }
+}
+
+}  // namespace vmps

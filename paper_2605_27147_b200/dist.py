@@ -111,15 +111,10 @@ def split_points(R: int, lt_all: list[int], le_all: list[int]) -> list[int]:
     return cuts
 
 
-def sort_dist(keys: torch.Tensor, vals: torch.Tensor | None = None, group=None,
-              ops=None) -> DistResult:
-    """Globally stable sort of the concatenation of every rank's shard.
-
-    Returns this rank's slice [R_p, R_{p+1}) of the global output.
-    """
-    ops = ops if ops is not None else VmpsOps()
+def _cuts(keys, vals, group, ops):
+    """Steps 1-2: local sort and exact splitters.  Returns (cut, sizes,
+    splitters, rounds) with cut[q][t] = elements of rank q that go to ranks < t."""
     g = dist.get_world_size(group)
-    me = dist.get_rank(group)
     kt = key_type(keys)
     dev = keys.device
     n = keys.numel()
@@ -166,6 +161,20 @@ def sort_dist(keys: torch.Tensor, vals: torch.Tensor | None = None, group=None,
         pts = split_points(R[t], lts, les)
         for q in range(g):
             cut[q][t + 1] = pts[q]
+    return cut, sizes, vstar, rounds
+
+
+def sort_dist(keys: torch.Tensor, vals: torch.Tensor | None = None, group=None,
+              ops=None) -> DistResult:
+    """Globally stable sort of the concatenation of every rank's shard.
+
+    Returns this rank's slice [R_p, R_{p+1}) of the global output.
+    """
+    ops = ops if ops is not None else VmpsOps()
+    g = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    dev = keys.device
+    cut, sizes, vstar, rounds = _cuts(keys, vals, group, ops)
     send = [cut[me][p + 1] - cut[me][p] for p in range(g)]
     recv = [cut[q][me + 1] - cut[q][me] for q in range(g)]
     # 3. exchange
@@ -392,3 +401,60 @@ def merge_plan_dist(keys: torch.Tensor, group=None, ops=None) -> DistPlan:
     starts[r] = N
     merges = ops.plan(starts, N)
     return DistPlan(starts[:r], kinds[:r], merges, minrun, entries, counts)
+
+
+
+def sort_dist_pull(keys: torch.Tensor, vals: torch.Tensor | None = None, group=None,
+                   ops=None) -> DistResult:
+    """sort_dist with the exchange and the final merge fused:
+    after the splitters, every rank maps the other ranks' sorted shards
+    (CUDA IPC over NVLink; vmps_ipc_handle / vmps_ipc_open) and merges its
+    co-ranked pieces straight from peer memory into its output
+    (vmps_merge_pieces: one TMA-staged 4-way pass for g <= 4, two plus a
+    local 2-way pass for g <= 8).  No receive buffer, no all-to-all: one HBM
+    write + read of the shard fewer than all-to-all + merge.  Barriers keep a
+    shard alive until every peer has read it."""
+    from . import ipc_close, ipc_handle, ipc_open, merge_pieces
+    ops = ops if ops is not None else VmpsOps()
+    g = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    dev = keys.device
+    cut, sizes, vstar, rounds = _cuts(keys, vals, group, ops)
+    recv = [cut[q][me + 1] - cut[q][me] for q in range(g)]
+    send = [cut[me][p + 1] - cut[me][p] for p in range(g)]
+    kb = keys.element_size()
+    # peer mappings of every shard (keys, values)
+    hk, ok_ = ipc_handle(keys)
+    mine = [hk, ok_]
+    if vals is not None:
+        hv, ov_ = ipc_handle(vals)
+        mine += [hv, ov_]
+    allh = [None] * g
+    dist.all_gather_object(allh, mine, group=group)
+    kptr, vptr, opened = [], [], []
+    for q in range(g):
+        if q == me:
+            kptr.append(keys.data_ptr())
+            vptr.append(vals.data_ptr() if vals is not None else 0)
+            continue
+        pk = ipc_open(allh[q][0], allh[q][1])
+        opened.append((pk, allh[q][1]))
+        kptr.append(pk)
+        if vals is not None:
+            pv = ipc_open(allh[q][2], allh[q][3])
+            opened.append((pv, allh[q][3]))
+            vptr.append(pv)
+    torch.cuda.current_stream(dev).synchronize()
+    dist.barrier(group=group)  # every shard is sorted and mapped
+    out_n = sum(recv)
+    ok = torch.empty(out_n, dtype=keys.dtype, device=dev)
+    ov = torch.empty(out_n, dtype=vals.dtype, device=dev) if vals is not None else None
+    kp = [kptr[q] + cut[q][me] * kb for q in range(g)]
+    vp = [vptr[q] + cut[q][me] * 4 for q in range(g)] if vals is not None else None
+    if out_n:
+        merge_pieces(kp, vp, recv, ok, ov)
+    torch.cuda.current_stream(dev).synchronize()
+    dist.barrier(group=group)  # every peer has read this shard
+    for p_, off in opened:
+        ipc_close(p_, off)
+    return DistResult(ok, ov, vstar, send, recv, rounds)
