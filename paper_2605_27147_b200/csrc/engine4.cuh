@@ -189,7 +189,7 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
 // boundary of a chunk is a full search, the next ones search a in
 // [a_prev, a_prev + T].
 #ifndef VMPS_DESC4_CHUNK
-#define VMPS_DESC4_CHUNK 8
+#define VMPS_DESC4_CHUNK 10
 #endif
 constexpr uint32_t DESC4_CHUNK = VMPS_DESC4_CHUNK;
 #ifndef VMPS_DESC4_SERIAL_MIN
