@@ -239,6 +239,13 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
 
 // Internal non-blocking stream (per device) used to capture CUDA graphs.
 constexpr int MAX_DEV = 16;
+// Per-device caches (function attributes are set per device): the current
+// device, clamped into the cache tables.
+static int dev_slot() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0) d = 0;
+  return d % MAX_DEV;
+}
 static cudaStream_t g_aux[MAX_DEV];
 static cudaStream_t aux_stream() {
   int dev = 0;
@@ -297,15 +304,16 @@ static vmps_status_t launch_check() {
   return VMPS_OK;
 }
 
-static bool g_chain_attrs = false;
+static bool g_chain_attrs[MAX_DEV] = {};
 static vmps_status_t chain_attrs() {
-  if (g_chain_attrs) return VMPS_OK;
+  const int ds = dev_slot();
+  if (g_chain_attrs[ds]) return VMPS_OK;
   const int sm = CHAIN_G * MAX_NS * 8;
   VMPS_CK(cudaFuncSetAttribute(k_chain_compose<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   VMPS_CK(cudaFuncSetAttribute(k_chain_compose<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   VMPS_CK(cudaFuncSetAttribute(k_chain_expand<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   VMPS_CK(cudaFuncSetAttribute(k_chain_expand<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-  g_chain_attrs = true;
+  g_chain_attrs[ds] = true;
   return VMPS_OK;
 }
 
@@ -518,7 +526,7 @@ static vmps_status_t bounded_stats(const Work& w, vmps_stats_t* st, cudaStream_t
   return VMPS_OK;
 }
 
-static bool kernel_attrs_set[3][2] = {{false, false}, {false, false}, {false, false}};
+static bool kernel_attrs_set[MAX_DEV][3][2] = {};
 
 template <int KT, bool HV>
 static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaStream_t s,
@@ -567,13 +575,14 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   const size_t lsm = leaf_smem_bytes<KT>(HV);
   const size_t lsm2 = leaf_smem_bytes<KT, LEAF_SMALL>(HV);
   const size_t rsm = LeafRadixSmem<KT>::BYTES;
-  if (!kernel_attrs_set[KT][HV]) {
+  const int ds = dev_slot();
+  if (!kernel_attrs_set[ds][KT][HV]) {
     VMPS_CK(cudaFuncSetAttribute(k_leaf_sort<KT, HV, LEAF_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lsm));
     VMPS_CK(cudaFuncSetAttribute(k_leaf_sort<KT, HV, LEAF_SMALL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)lsm2));
     VMPS_CK(cudaFuncSetAttribute(k_leaf_radix<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
-    kernel_attrs_set[KT][HV] = true;
+    kernel_attrs_set[ds][KT][HV] = true;
   }
   // a batch = consecutive touching units starting in one window of Zb
   // positions; units are <= Z long, so a batch spans < Zb + Z <= LEAF_CAP
@@ -610,7 +619,8 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   }
   if (w.fuse2) {
     using SM4 = Merge4Smem<KT, HV>;
-    static int occ4[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+    static int occ4_t[MAX_DEV][3][2] = {};
+    auto& occ4 = occ4_t[ds];
     if (!occ4[KT][HV]) {
       VMPS_CK(cudaFuncSetAttribute(k4_merge_level<KT, HV, M4_KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)SM4::BYTES));
@@ -639,7 +649,8 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
     }
   } else {
   using SM = MergeSmem<KT, HV>;
-  static int merge_occ[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  static int merge_occ_t[MAX_DEV][3][2] = {};
+  auto& merge_occ = merge_occ_t[ds];
   if (!merge_occ[KT][HV]) {
     VMPS_CK(cudaFuncSetAttribute(k_merge_level<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)SM::BYTES));
@@ -1365,7 +1376,8 @@ static vmps_status_t pull_pass(const void* const* kp, const uint32_t* const* vp,
   S.N = (uint32_t)N;
   S.base = base;
   if (N == 0) return VMPS_OK;
-  static int occ[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+  static int occ_t[MAX_DEV][3][2] = {};
+  auto& occ = occ_t[dev_slot()];
   if (!occ[KT][HV]) {
     VMPS_CK(cudaFuncSetAttribute(k_pull_merge<KT, HV, M4_KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)SM4::BYTES));
