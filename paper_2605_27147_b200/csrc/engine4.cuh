@@ -264,9 +264,15 @@ struct Merge4Smem {
   static constexpr uint32_t VB = HV ? 4096 * 4 + 256 : 0;
   static constexpr uint32_t STAGE = KB + VB;
   static constexpr uint32_t HDR = 512;
+#ifndef VMPS_U64_STAGES
+#define VMPS_U64_STAGES 2
+#endif
+  // stages of the TMA pipeline: u64 keys with payload use VMPS_U64_STAGES
+  // (one stage fits two CTAs per SM), all others two
+  static constexpr uint32_t NSTG = (sizeof(K) == 8 && HV) ? VMPS_U64_STAGES : 2u;
   static constexpr uint32_t IK = 4096 * sizeof(K);  // intermediate keys
   static constexpr uint32_t II = 4096 * 2;          // intermediate value indices (u16)
-  static constexpr uint32_t BYTES = HDR + 2 * STAGE + IK + II;
+  static constexpr uint32_t BYTES = HDR + NSTG * STAGE + IK + II;
 };
 
 struct Merge4Hdr {
@@ -608,8 +614,8 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 2;
   Merge4Hdr* hdr = reinterpret_cast<Merge4Hdr*>(smem + 64);
-  K* IKs = reinterpret_cast<K*>(smem + SM::HDR + 2 * SM::STAGE);
-  uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + 2 * SM::STAGE + SM::IK);
+  K* IKs = reinterpret_cast<K*>(smem + SM::HDR + SM::NSTG * SM::STAGE);
+  uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK);
   const uint32_t count = level_tile[p + 1] - level_tile[p];
   if (blockIdx.x >= count) return;
   const uint32_t tid = threadIdx.x;
@@ -625,8 +631,8 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
     if (tid == NT) {
       uint32_t it = 0;
       for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
-        const uint32_t s = it & 1u;
-        if (it >= 2) mbar_wait_backoff(&empty[s], ((it >> 1) - 1) & 1u);
+        const uint32_t s = it % SM::NSTG;
+        if (it >= SM::NSTG) mbar_wait_backoff(&empty[s], ((it / SM::NSTG) - 1) & 1u);
         const TileDesc4 d = tiles[tau];
         TileDesc4 dn;
         const bool same = tau + 1 < count && (dn = tiles[tau + 1], dn.x == d.x);
@@ -638,8 +644,8 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
   const uint32_t lane = tid & 31u;
   uint32_t it = 0;
   for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
-    const uint32_t s = it & 1u;
-    mbar_wait(&full[s], (it >> 1) & 1u);
+    const uint32_t s = it % SM::NSTG;
+    mbar_wait(&full[s], (it / SM::NSTG) & 1u);
     const Merge4Hdr* hp = hdr + s;
     const unsigned char* st = smem + SM::HDR + s * SM::STAGE;
     const K* SK = reinterpret_cast<const K*>(st);
@@ -802,8 +808,8 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k_pull_merge(PullSrc<KT> S,
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 2;
   Merge4Hdr* hdr = reinterpret_cast<Merge4Hdr*>(smem + 64);
-  K* IKs = reinterpret_cast<K*>(smem + SM::HDR + 2 * SM::STAGE);
-  uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + 2 * SM::STAGE + SM::IK);
+  K* IKs = reinterpret_cast<K*>(smem + SM::HDR + SM::NSTG * SM::STAGE);
+  uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK);
   if (blockIdx.x >= count) return;
   const uint32_t tid = threadIdx.x;
   if (tid == 0) {
@@ -818,8 +824,8 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k_pull_merge(PullSrc<KT> S,
     if (tid == NT) {
       uint32_t it = 0;
       for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
-        const uint32_t s = it & 1u;
-        if (it >= 2) mbar_wait_backoff(&empty[s], ((it >> 1) - 1) & 1u);
+        const uint32_t s = it % SM::NSTG;
+        if (it >= SM::NSTG) mbar_wait_backoff(&empty[s], ((it / SM::NSTG) - 1) & 1u);
         const TileDesc4 d = tiles[tau];
         TileDesc4 dn;
         const bool more = tau + 1 < count && (dn = tiles[tau + 1], true);
@@ -831,8 +837,8 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k_pull_merge(PullSrc<KT> S,
   const uint32_t lane = tid & 31u;
   uint32_t it = 0;
   for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
-    const uint32_t s = it & 1u;
-    mbar_wait(&full[s], (it >> 1) & 1u);
+    const uint32_t s = it % SM::NSTG;
+    mbar_wait(&full[s], (it / SM::NSTG) & 1u);
     const Merge4Hdr* hp = hdr + s;
     const unsigned char* st = smem + SM::HDR + s * SM::STAGE;
     const K* SK = reinterpret_cast<const K*>(st);
