@@ -148,9 +148,15 @@ __device__ __forceinline__ void co_pair(const InnerCR<KT>& L, uint32_t x, const 
 // Split of X's first d outputs; the outer co-rank a lies in [alo, ahi]
 // (caller's bound, e.g. from the previous aligned boundary).  On return c[]
 // holds (c0, c1, c2, c3) and L / R know their co-ranks at a and d - a.
+// hint (optional, 0xFFFFFFFF = none): an estimate of the answer; the first
+// two probes then bracket [hint - HINT_W, hint + HINT_W] instead of halving,
+// which narrows the outer search in two evaluations when the estimate holds
+// (consecutive tiles of a node split alike) and costs two when it does not.
+constexpr uint32_t HINT_W = 96;
 template <int KT>
 __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint32_t d, uint32_t alo,
-                                            uint32_t ahi, uint32_t* c) {
+                                            uint32_t ahi, uint32_t* c, uint32_t hint = 0xFFFFFFFFu,
+                                            uint32_t hw = HINT_W) {
   using T = KeyTraits<KT>;
   const uint32_t nL = L.nA + L.nB, nR = R.nA + R.nB;
   // the known-low points stay valid (queries only move right: L at a >=
@@ -159,8 +165,15 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
   R.know_high(nR, R.nA);
   alo = max(alo, d > nR ? d - nR : 0u);
   ahi = min(ahi, min(d, nL));
+  int hint_left = hint != 0xFFFFFFFFu && ahi - alo > 4 * hw ? 2 : 0;
   while (alo < ahi) {
-    const uint32_t mid = (alo + ahi) >> 1;
+    uint32_t mid = (alo + ahi) >> 1;
+    if (hint_left) {  // the probes around the hint (kept inside [alo, ahi))
+      const uint32_t p = hint_left == 2 ? (hint > alo + hw ? hint - hw : alo)
+                                        : (hint + hw < ahi ? hint + hw : ahi - 1);
+      mid = min(max(p, alo), ahi - 1);
+      --hint_left;
+    }
     const uint32_t r = d - mid - 1;  // < nR since mid >= d - nR
     uint32_t cL, cR;
     co_pair<KT>(L, mid, R, r, &cL, &cR);
@@ -192,6 +205,9 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
 #define VMPS_DESC4_CHUNK 10
 #endif
 constexpr uint32_t DESC4_CHUNK = VMPS_DESC4_CHUNK;
+#ifndef VMPS_DESC4_HINT
+#define VMPS_DESC4_HINT 1
+#endif
 #ifndef VMPS_DESC4_SERIAL_MIN
 #define VMPS_DESC4_SERIAL_MIN 65536
 #endif
@@ -220,7 +236,7 @@ __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* 
     const uint32_t tau0 = tb + ch * chunk;
     uint32_t a = ls, b = le;  // last bucket x with ltiles[x] <= tau0
     while (b - a > 1) { uint32_t m = (a + b) >> 1; if (ltiles[m] <= tau0) a = m; else b = m; }
-    uint32_t cur = 0xFFFFFFFFu, aprev = 0, dprev = 0;
+    uint32_t cur = 0xFFFFFFFFu, aprev = 0, dprev = 0, aprev2 = 0, dprev2 = 0;
     InnerCR<KT> L, R;
     NodeRuns X;
     for (uint32_t q = 0; q < chunk; ++q) {
@@ -235,13 +251,29 @@ __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* 
         cur = a;
         aprev = 0;
         dprev = 0;
+        aprev2 = 0;
+        dprev2 = 0;
       }
       const uint32_t i = X.b[0], k = X.b[4];
       const uint32_t g = i / tout + (tau - ltiles[a]);
       const uint32_t lo = max(i, g * tout);
       const uint32_t d = lo - i;
       uint32_t c[4];
-      const uint32_t av = corank4<KT>(L, R, d, aprev, aprev + (d - dprev), c);
+      // estimate: the previous tile's share of L among its outputs
+      const uint32_t hint = (cur == a && q > 0 && d > dprev && dprev > dprev2)
+                                ? aprev + (uint32_t)(((uint64_t)(aprev - aprev2) * (d - dprev)) / (dprev - dprev2))
+                                : 0xFFFFFFFFu;
+      uint32_t h = VMPS_DESC4_HINT ? hint : 0xFFFFFFFFu, hw = HINT_W;
+#if VMPS_DESC4_HINT >= 2
+      if (h == 0xFFFFFFFFu && d > 0) {  // first tile of the node in this chunk: L's share of the node
+        const uint32_t nL = (X.b[2] - X.b[0]), nX = X.b[4] - X.b[0];
+        h = (uint32_t)(((uint64_t)d * nL) / nX);
+        hw = max(HINT_W, 2u * (uint32_t)sqrtf((float)d));
+      }
+#endif
+      const uint32_t av = corank4<KT>(L, R, d, aprev, aprev + (d - dprev), c, h, hw);
+      aprev2 = aprev;
+      dprev2 = dprev;
       aprev = av;
       dprev = d;
       TileDesc4 D;
