@@ -740,13 +740,18 @@ __global__ void __launch_bounds__(256) k_pull_desc(PullSrc<KT> S, uint32_t ntile
     InnerCR<KT> L, R;
     L.init(S.kp[0], S.n[0], S.kp[1], S.n[1]);
     R.init(S.kp[2], S.n[2], S.kp[3], S.n[3]);
-    uint32_t aprev = 0, dprev = 0;
+    uint32_t aprev = 0, dprev = 0, aprev2 = 0, dprev2 = 0;
     for (uint32_t q = 0; q < DESC4_CHUNK; ++q) {
       const uint32_t tau = ch * DESC4_CHUNK + q;
       if (tau >= ntiles) break;
       const uint32_t d = tau == 0 ? 0u : (S.base / 4096u + tau) * 4096u - S.base;
       uint32_t c[4];
-      const uint32_t av = corank4<KT>(L, R, d, aprev, aprev + (d - dprev), c);
+      const uint32_t hint = (q > 0 && d > dprev && dprev > dprev2)
+                                ? aprev + (uint32_t)(((uint64_t)(aprev - aprev2) * (d - dprev)) / (dprev - dprev2))
+                                : 0xFFFFFFFFu;  // as k4_desc
+      const uint32_t av = corank4<KT>(L, R, d, aprev, aprev + (d - dprev), c, hint);
+      aprev2 = aprev;
+      dprev2 = dprev;
       aprev = av;
       dprev = d;
       TileDesc4 D;
