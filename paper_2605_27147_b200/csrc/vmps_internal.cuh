@@ -48,8 +48,11 @@ constexpr int MAX_MINRUN = 64;
 constexpr int MAX_NS = 3 * MAX_MINRUN;
 
 // Plan / schedule defaults
-constexpr uint32_t DEFAULT_FUSE_Z = 2048;   // fused-subtree limit Z (elements)
-constexpr uint32_t MAX_FUSE_Z = 2048;
+#ifndef VMPS_FUSE_Z
+#define VMPS_FUSE_Z 2048
+#endif
+constexpr uint32_t DEFAULT_FUSE_Z = VMPS_FUSE_Z;   // fused-subtree limit Z (elements)
+constexpr uint32_t MAX_FUSE_Z = VMPS_FUSE_Z;
 constexpr uint32_t MERGE_BLOCK = 512;       // threads per merge CTA
 constexpr uint32_t MERGE_K = 8;             // outputs per thread
 constexpr uint32_t DEFAULT_TOUT = MERGE_BLOCK * MERGE_K;  // merge tile (outputs)
