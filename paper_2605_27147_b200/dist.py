@@ -31,7 +31,7 @@ from dataclasses import dataclass
 import torch
 import torch.distributed as dist
 
-from . import (KEY_F32, KEY_U32, KEY_U64, Workspace, _check, _stream_ptr, key_type, lib,
+from . import (KEY_U64, Workspace, _check, _stream_ptr, key_type, lib,
                minrun_for, sort_)
 
 
