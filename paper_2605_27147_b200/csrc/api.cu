@@ -183,13 +183,17 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.level_start = (uint32_t*)take((LEVEL_SLOTS + 1) * 4);
     t.level_fill = (uint32_t*)take((LEVEL_SLOTS + 1) * 4);
     t.level_tile = (uint32_t*)take((LEVEL_SLOTS + 1) * 4);
-    t.lnodes = (uint32_t*)take(R * 4);
-    t.ltiles = (uint32_t*)take(R * 4);
-    t.ltiles_cnt = (uint32_t*)take(R * 4);
-    // tiles of one level: its nodes are disjoint and larger than Z, and a node
-    // [i,k) spans ceil(k/T) - floor(i/T) <= (k-i)/T + 2 aligned tiles
+    // level schedule of the unbounded engines (the bounded mode builds its
+    // own per-level lists)
     t.part_cap = (uint32_t)(n / c.tout + 2 * (n / c.fuse_z) + 8);
-    t.desc = take((size_t)t.part_cap * sizeof(TileDesc));
+    if (!t.bounded) {
+      t.lnodes = (uint32_t*)take(R * 4);
+      t.ltiles = (uint32_t*)take(R * 4);
+      t.ltiles_cnt = (uint32_t*)take(R * 4);
+      // tiles of one level: its nodes are disjoint and larger than Z, and a node
+      // [i,k) spans ceil(k/T) - floor(i/T) <= (k-i)/T + 2 aligned tiles
+      t.desc = take((size_t)t.part_cap * sizeof(TileDesc));
+    }
     t.scan_tmp = (uint32_t*)take(scan_tmp_words(R) * 4 + 64);
   }
   t.counters = (unsigned long long*)take(8 * 8);
@@ -215,11 +219,14 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.didx = (uint32_t*)take(NBp * 4);
     t.dlist = (uint32_t*)take(NBp * 4);
     t.first_tile = (uint32_t*)take(NBp * 4);
-    t.bflag = (uint32_t*)take(R * 4);
-    t.bpos = (uint32_t*)take(R * 4);
-    t.blnodes = (uint32_t*)take(R * 4);
-    t.bcnt = (uint32_t*)take(R * 4);
-    t.btoff = (uint32_t*)take(R * 4);
+    // per-level lists of the rounds reuse arrays that are dead by then: the
+    // pointer-jumping temporaries (anc, dep[1]) and the long-leaf compaction
+    // flags (long_flag, long_idx), all R entries of 4 bytes
+    t.bflag = t.anc[0];
+    t.bpos = t.anc[1];
+    t.blnodes = t.dep[1];
+    t.bcnt = t.long_flag;
+    t.btoff = t.long_idx;
     t.bm = (uint32_t*)take(64);
     t.bD = (uint32_t*)take(64);
     t.bdesc_cap = (uint32_t)(n / c.P + 4 * (n / c.fuse_z) + 16);
@@ -557,12 +564,14 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   LAUNCH(k_zero_tail, g, 256, 0, s, w.long_chunks, w.scalars, (int)SC_LONG, w.rmax);
   scan_u32(w.long_chunks, w.long_off, w.rmax + 1, w.scan_tmp, s);
   LAUNCH(k_level_scan, 1, 32, 0, s, w.level_cnt, w.level_start, w.scalars);
-  LAUNCH(k_level_scatter, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.fuse_z,
-         w.level_start, w.level_fill, w.lnodes, dep, w.fuse2);
-  LAUNCH(k_level_tiles, g, 256, 0, s, w.run_start, w.scalars, w.seg_l, w.seg_r, w.lnodes, w.tout, w.rmax,
-         w.ltiles_cnt);
-  scan_u32(w.ltiles_cnt, w.ltiles, w.rmax + 1, w.scan_tmp, s);
-  LAUNCH(k_level_tile_off, 1, 128, 0, s, w.level_start, w.ltiles, w.level_tile);
+  if (!w.bounded) {
+    LAUNCH(k_level_scatter, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.fuse_z,
+           w.level_start, w.level_fill, w.lnodes, dep, w.fuse2);
+    LAUNCH(k_level_tiles, g, 256, 0, s, w.run_start, w.scalars, w.seg_l, w.seg_r, w.lnodes, w.tout, w.rmax,
+           w.ltiles_cnt);
+    scan_u32(w.ltiles_cnt, w.ltiles, w.rmax + 1, w.scan_tmp, s);
+    LAUNCH(k_level_tile_off, 1, 128, 0, s, w.level_start, w.ltiles, w.level_tile);
+  }
   rc = launch_check();
   if (rc != VMPS_OK) return rc;
   g_prof_mark[1] = prof_event(s);
