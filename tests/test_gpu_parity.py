@@ -279,3 +279,27 @@ def test_host_entry_points(vm, dtype):
         vm.sort_host_(hk2)                                                 # keys only, in place
         torch.cuda.synchronize()
         assert W.to_numpy(hk2).view(np.uint8).tobytes() == kk.view(np.uint8).tobytes()
+
+
+def test_concurrent_streams(vm):
+    """Independent sorts on different streams with their own workspaces run
+    concurrently (the ABI's thread-safety convention): each equals the oracle."""
+    rng = np.random.default_rng(55)
+    cases = []
+    for dt in (np.uint32, np.uint64, np.float32, np.uint32):
+        n = int(rng.integers(200_000, 600_000))
+        k = _structured(rng, n, dt)
+        v = np.arange(n, dtype=np.uint32)
+        cases.append((k, v))
+    streams = [torch.cuda.Stream() for _ in cases]
+    wss = [vm.Workspace() for _ in cases]
+    dev = [(W.from_numpy(k, "cuda"), W.from_numpy(v, "cuda")) for k, v in cases]
+    torch.cuda.synchronize()
+    for (dk, dv), s, ws in zip(dev, streams, wss):
+        with torch.cuda.stream(s):
+            vm.sort_(dk, dv, workspace=ws)
+    torch.cuda.synchronize()
+    for (k, v), (dk, dv) in zip(cases, dev):
+        ko, vo, _, _ = oracle.sort(k, v)
+        assert W.to_numpy(dk).view(np.uint8).tobytes() == ko.view(np.uint8).tobytes()
+        assert (W.to_numpy(dv) == vo).all()
