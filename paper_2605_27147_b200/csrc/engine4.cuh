@@ -223,10 +223,10 @@ __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* 
   const uint32_t tb = level_tile[p], te = level_tile[p + 1];
   // chunk length: a level of few tiles is bound by the length of each
   // thread's chain of dependent probes, so every tile gets its own thread
-  // (below DESC4_SERIAL_MIN tiles), then two; large levels use DESC4_CHUNK
+  // (below DESC4_SERIAL_MIN tiles), then three; large levels use DESC4_CHUNK
   // (fewer full searches); measured at cfg1-5 and at the paper's n = 10^7
   const uint32_t ntl = te - tb;
-  const uint32_t chunk = ntl < DESC4_SERIAL_MIN ? 1u : ntl < 4u * DESC4_SERIAL_MIN ? 2u : DESC4_CHUNK;
+  const uint32_t chunk = ntl < DESC4_SERIAL_MIN ? 1u : ntl < 4u * DESC4_SERIAL_MIN ? 3u : DESC4_CHUNK;
   const uint32_t nchunks = (te - tb + chunk - 1) / chunk;
   for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks; ch += gridDim.x * blockDim.x) {
     const uint32_t tau0 = tb + ch * chunk;
