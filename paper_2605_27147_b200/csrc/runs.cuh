@@ -263,8 +263,25 @@ __device__ __forceinline__ uint32_t window_and_m(unsigned __int128 b, uint32_t m
   b &= b >> (m - p);         // m - p < p: two overlapping windows cover [i, i+m)
   return (uint32_t)(b >> 1);  // bit i: AND of [i+1, i+m]
 }
+// m <= 32 (minrun 32 for every n = 2^k): the windows [i+1, i+m] of the
+// word's 32 starts end at bit 63 at most, so 64-bit arithmetic suffices.
+__device__ __forceinline__ uint32_t window_and_m64(uint64_t b, uint32_t m) {
+  uint32_t p = 1;
+  while (2 * p <= m) {
+    b &= b >> p;
+    p *= 2;
+  }
+  b &= b >> (m - p);
+  return (uint32_t)(b >> 1);
+}
 __device__ __forceinline__ void long_masks(const uint32_t* sb, uint32_t w, uint32_t m, uint32_t* la,
                                            uint32_t* ld) {
+  if (m <= 32) {
+    const uint64_t b = (uint64_t)sb[w] | ((uint64_t)sb[w + 1] << 32);
+    ld[w] = window_and_m64(b, m);
+    la[w] = window_and_m64(~b, m);
+    return;
+  }
   const unsigned __int128 b = (unsigned __int128)sb[w] | ((unsigned __int128)sb[w + 1] << 32) |
                               ((unsigned __int128)sb[w + 2] << 64);
   const unsigned __int128 nb = ~b & (((unsigned __int128)1 << 96) - 1);
@@ -286,11 +303,17 @@ __device__ __forceinline__ void stop_masks32(const uint32_t* sb, const uint32_t*
   const int lim = (int)L - 32 - (int)(32 * w);                  // bits b >= lim have x + 32 >= L
   if (lim <= 0) st = 0xFFFFFFFFu;
   else if (lim < 32) st |= 0xFFFFFFFFu << lim;
-#pragma unroll 4
-  for (uint32_t b = 0; b < 32; ++b) {
-    const uint32_t v = __ballot_sync(0xFFFFFFFFu, (st >> b) & 1u);
-    if (lane == b) ts[4 * b + k] = v;
+  // 32x32 bit transpose across the warp (lane l's bit b -> lane b's bit l):
+  // five butterfly exchanges instead of 32 ballots
+  uint32_t x = st;
+#pragma unroll
+  for (uint32_t j = 16; j >= 1; j >>= 1) {
+    const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                     : j == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y << j) & ~m));
   }
+  ts[4 * lane + k] = x;
 }
 // first word >= w whose bit b is a stop (128 if none)
 __device__ __forceinline__ uint32_t next_stop32(const uint32_t* ts, uint32_t b, uint32_t w) {
