@@ -639,6 +639,10 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       occ4[KT][HV] = occ > 0 ? occ : 1;
     }
     const unsigned gm4 = (unsigned)(nsm() * occ4[KT][HV]);
+    // warp-per-tile partition for small levels: pays off while the keys stay
+    // near the L2 (its probes are many but parallel); measured at cfg1-5
+    const uint32_t desc_warp_max =
+        (VMPS_DESC4_WARP && (uint64_t)w.n * sizeof(K) <= (512ull << 20)) ? DESC4_WARP_MAX : 0u;
     NodeRuns* nr = (NodeRuns*)w.nr4;
     TileDesc4* t4 = (TileDesc4*)w.tiles4;
     for (int p = p_hi; p >= 1; --p) {
@@ -646,7 +650,10 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       LAUNCH(k4_node_runs, grid_for(w.n4cap), 256, 0, s, w.run_start, w.seg_l, w.seg_r, dep, w.lchild, w.rchild,
              w.lnodes, w.level_start, p, nr);
       LAUNCH(k4_desc<KT>, (std::max<uint32_t>(w.part_cap / 4, std::min<uint32_t>(w.part_cap, 4 * DESC4_SERIAL_MIN)) + 256) / 256, 256, 0, s, k0, k1, nr, w.ltiles, w.level_start,
-             w.level_tile, p, w.tout, t4);
+             w.level_tile, p, w.tout, t4, desc_warp_max);
+      if (desc_warp_max)
+        LAUNCH(k4_desc_warp<KT>, (32u * std::min<uint32_t>(w.part_cap, desc_warp_max) + 255) / 256, 256, 0, s, k0, k1,
+               nr, w.ltiles, w.level_start, w.level_tile, p, w.tout, t4, desc_warp_max);
       int e1 = prof_event(s);
       LAUNCH((k4_merge_level<KT, HV, M4_KQ>), gm4, 4096 / M4_KQ + 32, SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.level_tile, p);
       ++g_nl_merge;

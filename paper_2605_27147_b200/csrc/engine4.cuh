@@ -196,6 +196,58 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
   return a;
 }
 
+// The same split found by a warp: each round the 32 lanes evaluate 32
+// outer candidates spread over [alo, ahi) at once (each with its own inner
+// co-rank searches), a ballot finds the first candidate that fails, and the
+// neighbouring lanes' inner co-ranks become the next round's known points;
+// the outer range shrinks ~33x per round instead of 2x per dependent step.
+// For levels of few tiles, where each thread's chain of dependent probes is
+// the bound and the probe traffic is small.  All lanes return the split.
+template <int KT>
+__device__ __forceinline__ uint32_t corank4_warp(InnerCR<KT>& L, InnerCR<KT>& R, uint32_t d, uint32_t* c,
+                                                 uint32_t lane) {
+  using T = KeyTraits<KT>;
+  const uint32_t nL = L.nA + L.nB, nR = R.nA + R.nB;
+  uint32_t alo = d > nR ? d - nR : 0u, ahi = min(d, nL);
+  while (alo < ahi) {
+    const uint32_t w = ahi - alo;
+    // candidates m_l strictly increasing in [alo, ahi) (lanes past the range idle)
+    const bool act = w >= 32u || lane < w;
+    const uint32_t m = w >= 32u ? alo + (uint32_t)(((uint64_t)w * lane) / 32u) : alo + lane;
+    bool pr = false;
+    uint32_t cL = 0, cR = 0;
+    const uint32_t r = d - m - 1;
+    if (act) {
+      co_pair<KT>(L, m, R, r, &cL, &cR);
+      pr = T::ord(L.elem(m, cL)) <= T::ord(R.elem(r, cR));  // L[m] precedes R[d-m-1]
+    }
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, pr);
+    const uint32_t nact = w >= 32u ? 32u : w;
+    const uint32_t f = (uint32_t)__popc(bal);  // predicate is monotone: lanes [0, f) true
+    const uint32_t mT = __shfl_sync(0xFFFFFFFFu, m, f > 0 ? f - 1 : 0);
+    const uint32_t cLT = __shfl_sync(0xFFFFFFFFu, cL, f > 0 ? f - 1 : 0);
+    const uint32_t cRT = __shfl_sync(0xFFFFFFFFu, cR, f > 0 ? f - 1 : 0);
+    const uint32_t mF = __shfl_sync(0xFFFFFFFFu, m, f < 32u ? f : 31u);
+    const uint32_t cLF = __shfl_sync(0xFFFFFFFFu, cL, f < 32u ? f : 31u);
+    const uint32_t cRF = __shfl_sync(0xFFFFFFFFu, cR, f < 32u ? f : 31u);
+    if (f > 0) {
+      alo = mT + 1;
+      L.know_low(mT, cLT);
+      R.know_high(d - mT - 1, cRT);
+    }
+    if (f < nact) {
+      ahi = mF;
+      L.know_high(mF, cLF);
+      R.know_low(d - mF - 1, cRF);
+    }
+  }
+  const uint32_t a = alo;
+  uint32_t c0, c2;
+  co_pair<KT>(L, a, R, d - a, &c0, &c2);
+  c[0] = c0; c[1] = a - c0; c[2] = c2; c[3] = d - a - c2;
+  return a;
+}
+
 // Tile descriptors of one level of the two-level schedule: tiles aligned to
 // global multiples of T (enumerated by k_level_tiles / ltiles like the
 // one-level engine), DESC_CHUNK consecutive tiles per thread; the first
@@ -212,13 +264,20 @@ constexpr uint32_t DESC4_CHUNK = VMPS_DESC4_CHUNK;
 #define VMPS_DESC4_SERIAL_MIN 65536
 #endif
 constexpr uint32_t DESC4_SERIAL_MIN = VMPS_DESC4_SERIAL_MIN;
+#ifndef VMPS_DESC4_WARP
+#define VMPS_DESC4_WARP 1
+#endif
+#ifndef VMPS_DESC4_WARP_MAX
+#define VMPS_DESC4_WARP_MAX 16384
+#endif
+constexpr uint32_t DESC4_WARP_MAX = VMPS_DESC4_WARP_MAX;  // levels below this many tiles: a warp per tile
 template <int KT>
 __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* __restrict__ k0,
                                                const typename KeyTraits<KT>::K* __restrict__ k1,
                                                const NodeRuns* __restrict__ nr, const uint32_t* __restrict__ ltiles,
                                                const uint32_t* __restrict__ level_start,
                                                const uint32_t* __restrict__ level_tile, int p, uint32_t tout,
-                                               TileDesc4* __restrict__ tiles) {
+                                               TileDesc4* __restrict__ tiles, uint32_t warp_max) {
   const uint32_t ls = level_start[p], le = level_start[p + 1];
   const uint32_t tb = level_tile[p], te = level_tile[p + 1];
   // chunk length: a level of few tiles is bound by the length of each
@@ -226,6 +285,7 @@ __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* 
   // (below DESC4_SERIAL_MIN tiles), then three; large levels use DESC4_CHUNK
   // (fewer full searches); measured at cfg1-5 and at the paper's n = 10^7
   const uint32_t ntl = te - tb;
+  if (ntl < warp_max) return;  // k4_desc_warp's level
   const uint32_t chunk = ntl < DESC4_SERIAL_MIN ? 1u : ntl < 4u * DESC4_SERIAL_MIN ? 3u : DESC4_CHUNK;
   const uint32_t nchunks = (te - tb + chunk - 1) / chunk;
   for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks; ch += gridDim.x * blockDim.x) {
@@ -279,6 +339,49 @@ __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* 
       tiles[tau - tb] = D;
       (void)k;
     }
+  }
+}
+
+
+// Small levels (fewer than warp_max tiles): one warp per tile, the split by
+// corank4_warp.  Launched beside k4_desc, which skips these levels.
+template <int KT>
+__global__ void __launch_bounds__(256) k4_desc_warp(const typename KeyTraits<KT>::K* __restrict__ k0,
+                                                    const typename KeyTraits<KT>::K* __restrict__ k1,
+                                                    const NodeRuns* __restrict__ nr,
+                                                    const uint32_t* __restrict__ ltiles,
+                                                    const uint32_t* __restrict__ level_start,
+                                                    const uint32_t* __restrict__ level_tile, int p, uint32_t tout,
+                                                    TileDesc4* __restrict__ tiles, uint32_t warp_max) {
+  const uint32_t ls = level_start[p], le = level_start[p + 1];
+  const uint32_t tb = level_tile[p], te = level_tile[p + 1];
+  const uint32_t ntl = te - tb;
+  if (ntl < warp_max) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < ntl; wi += nw) {
+      const uint32_t tau = tb + wi;
+      uint32_t a = ls, b = le;
+      while (b - a > 1) { uint32_t m = (a + b) >> 1; if (ltiles[m] <= tau) a = m; else b = m; }
+      const NodeRuns X = nr[a - ls];
+      const auto* src = X.par ? k0 : k1;
+      InnerCR<KT> L, R;
+      L.init(src + X.b[0], X.b[1] - X.b[0], src + X.b[1], X.b[2] - X.b[1]);
+      R.init(src + X.b[2], X.b[3] - X.b[2], src + X.b[3], X.b[4] - X.b[3]);
+      const uint32_t i = X.b[0];
+      const uint32_t g = i / tout + (tau - ltiles[a]);
+      const uint32_t d = max(i, g * tout) - i;
+      uint32_t c[4];
+      corank4_warp<KT>(L, R, d, c, lane);
+      if (lane == 0) {
+        TileDesc4 D;
+        D.x = a - ls;
+        D.rank = d;
+        D.c[0] = c[0]; D.c[1] = c[1]; D.c[2] = c[2]; D.c[3] = c[3];
+        tiles[tau - tb] = D;
+      }
+    }
+    return;
   }
 }
 
