@@ -639,10 +639,11 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       occ4[KT][HV] = occ > 0 ? occ : 1;
     }
     const unsigned gm4 = (unsigned)(nsm() * occ4[KT][HV]);
-    // warp-per-tile partition for small levels: pays off while the keys stay
-    // near the L2 (its probes are many but parallel); measured at cfg1-5
+    // warp-per-tile partition for small levels: up to 16,384 tiles while the
+    // keys stay near the L2 (its probes are many but parallel), 4,096 beyond;
+    // measured at cfg1-5
     const uint32_t desc_warp_max =
-        (VMPS_DESC4_WARP && (uint64_t)w.n * sizeof(K) <= (512ull << 20)) ? DESC4_WARP_MAX : 0u;
+        !VMPS_DESC4_WARP ? 0u : (uint64_t)w.n * sizeof(K) <= (512ull << 20) ? DESC4_WARP_MAX : 4096u;
     NodeRuns* nr = (NodeRuns*)w.nr4;
     TileDesc4* t4 = (TileDesc4*)w.tiles4;
     for (int p = p_hi; p >= 1; --p) {
