@@ -4,14 +4,15 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
 ``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
 product path (``paper_2605_27147_b200``) never imports it and shares no code
 with it; ``vmps_oracle.c`` is a plain single-threaded C implementation of the
-paper's Alg. 1 with two merge variants (copy-merge, Fig. 1; and
-Virtual-Memory pages, Sec. 4).  See ``vmps_oracle.c`` for the passage each
+paper's Alg. 1 (P:363-386) with three merge variants (copy-merge, Fig. 1;
+Virtual-Memory pages, Sec. 4; Pingpong, Sec. 3).  See ``vmps_oracle.c`` for the passage each
 function follows and DESIGN.md for the readings of the paper it takes.
 
 Parity pins: tests/test_oracle.py (brute-force power definition, Python's
 stable ``sorted``, golden fixtures, paper bounds).  The VM variant's memory
-constants are "parity unpinned": only the paper's asymptotic
-law and the page-flow invariants are checked.
+constants are pinned only in magnitude against Fig. 4:
+the paper prints pre-allocated worst-case reserves, the oracle allocates on
+demand.
 """
 from __future__ import annotations
 
@@ -28,7 +29,7 @@ _HDR = os.path.join(_HERE, "vmps_oracle.h")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 U32, U64, F32 = 0, 1, 2
-VARIANT_A, VARIANT_B = 0, 1  # copy-merge, virtual-memory
+VARIANT_A, VARIANT_B, VARIANT_C, VARIANT_C0 = 0, 1, 2, 3  # copy-merge, virtual-memory, pingpong (+ without last-pop)
 KIND_ASC, KIND_DESC, KIND_EXT = 0, 1, 2
 
 
@@ -84,6 +85,8 @@ def lib():
         _lib.orc_plan.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32,
                                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                   ctypes.c_void_p, ctypes.POINTER(_Stats)]
+        _lib.orc_set_vm_words.restype = None
+        _lib.orc_set_vm_words.argtypes = [ctypes.c_uint32]
         _lib.orc_policy.restype = ctypes.c_int
         _lib.orc_policy.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64,
                                     ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)]
@@ -99,6 +102,11 @@ def policy(n: int, run_start) -> tuple[np.ndarray, int]:
     if rc != 0:
         raise RuntimeError(f"orc_policy failed: {rc}")
     return mg[:max(len(rs) - 1, 0)].copy(), int(ms.value)
+
+
+def set_vm_words(T: int = 0) -> None:
+    """Test hook: page-size word count of variant B (0 = the element's own)."""
+    lib().orc_set_vm_words(T)
 
 
 def minrun(n: int) -> int:

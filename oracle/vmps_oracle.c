@@ -19,6 +19,16 @@
  *   - Variant A "standard copy-merge" (Fig. 1): copy the LEFT run to
  *     a buffer, merge left-to-right back into the input, ties to the left
  *     (Alg. 2 StandardMerge).  No tail skip (reading R8).
+ *   - Variant C "Pingpong" (Sec. 3): buffers on the
+ *     stack live in stackBuf[i,j) (n extra elements), curr / next / work in
+ *     input[i,j); a pushed buffer is copied into stackBuf (line 10 of Alg. 1);
+ *     MergeBuffers merges stackBuf[i,j) with input[j,k) left to right into
+ *     input[i,k); at the last pop of a line-7 loop it instead merges right to
+ *     left into stackBuf[i,k), taking the right run's element on
+ *     ties (it must land later; SPEC's backward tie rule, reading R16), so
+ *     the push that follows copies nothing.  The final unwind (lines 12-13)
+ *     always merges into input, so Copy does nothing.  C0 is the same
+ *     without the last-pop merge.
  *   - Variant B "Virtual-Memory" (Sec. 4): pages of P elements
  *     (rounding per reading R9), free list, page
  *     lists as arrays (App. A), PushBack/PopFront,
@@ -78,6 +88,10 @@ typedef struct ctx {
   item* abuf;
   /* variant B */
   struct vm* vm;
+  /* variant C */
+  item* stack_buf;
+  int last_pop_opt;  /* C: 1, C0: 0 */
+  int last_pop;      /* set by powersort(): this merge is the last pop before a push */
 } ctx;
 
 static int less(ctx* c, const item* x, const item* y) {
@@ -237,6 +251,7 @@ typedef struct strategy {
   buf (*extract_run)(ctx*, uint64_t s);
   buf (*merge_buffers)(ctx*, buf x, buf y);
   void (*copy)(ctx*, buf curr);
+  void (*push)(ctx*, buf* b); /* optional: the buffer moves onto the stack (C) */
 } strategy;
 
 static void record_merge(ctx* c, buf x, buf y, uint32_t p) {
@@ -262,10 +277,13 @@ static void powersort(ctx* c, strategy* S) {
     uint32_t p = orc_power(n, curr.lo, curr.hi, next.hi); /* line 6 */
     while (top > 0 && pw[top - 1] >= p) {   /* line 7 */
       record_merge(c, stk[top - 1], curr, pw[top - 1]);
+      c->last_pop = !(top > 1 && pw[top - 2] >= p); /* the loop ends after this pop */
       curr = S->merge_buffers(c, stk[top - 1], curr); /* line 8 */
       top--;                                /* line 9 */
     }
+    c->last_pop = 0;
     if (top >= 71) { c->err = ORC_EINTERNAL; return; }
+    if (S->push) S->push(c, &curr);
     stk[top] = curr;                        /* line 10 */
     pw[top] = p;
     top++;
@@ -323,6 +341,60 @@ static buf a_merge(ctx* c, buf x, buf y) {
 }
 
 static void a_copy(ctx* c, buf curr) { (void)c; (void)curr; } /* already in input */
+
+/* ------------------------------------------------------------------------ */
+/* Variant C: Pingpong (Sec. 3)                                  */
+/* buf.h: 0 = the buffer lives in input[lo,hi), 1 = in stackBuf[lo,hi)      */
+/* ------------------------------------------------------------------------ */
+static buf c_extract_run(ctx* c, uint64_t s) {
+  buf b = a_extract_run(c, s); /* ExtractRun: the run stays in input */
+  b.h = 0;
+  return b;
+}
+
+/* Pushing a buffer that lives in input copies it to stackBuf. */
+static void c_push(ctx* c, buf* b) {
+  if (b->h == 1) return; /* produced by a last-pop merge: already in stackBuf */
+  for (uint64_t t = b->lo; t < b->hi; ++t) c->stack_buf[t] = c->a[t];
+  c->st->moves_staging += b->hi - b->lo;
+  b->h = 1;
+}
+
+static buf c_merge(ctx* c, buf x, buf y) {
+  item* sb = c->stack_buf;
+  item* a = c->a;
+  if (x.h != 1 || y.h != 0) { c->err = ORC_EINTERNAL; return x; }
+  c->counter = &c->st->comp_merge;
+  buf r = {x.lo, y.hi, 0};
+  if (c->last_pop_opt && c->last_pop) {
+    /* last pop: merge right to left into stackBuf[i,k); from the
+     * back, a tie outputs the right run's element first (it lands later) */
+    uint64_t xa = x.hi, xb = y.hi, o = y.hi; /* one past the next element */
+    while (xa > x.lo && xb > y.lo) {
+      if (less(c, &a[xb - 1], &sb[xa - 1])) sb[--o] = sb[--xa]; /* b < a: a is larger */
+      else sb[--o] = a[--xb];                                  /* a <= b: b goes last */
+    }
+    while (xb > y.lo) { --o; sb[o] = a[--xb]; }
+    while (xa > x.lo) { --o; sb[o] = sb[--xa]; } /* written once (no tail skip, R8) */
+    r.h = 1;
+  } else {
+    /* merge stackBuf[i,j) and input[j,k) left to right into input[i,k) */
+    uint64_t xa = x.lo, xb = y.lo, o = x.lo;
+    while (xa < x.hi && xb < y.hi) {
+      if (!less(c, &a[xb], &sb[xa])) a[o++] = sb[xa++]; /* a <= b: ties to the left */
+      else a[o++] = a[xb++];
+    }
+    while (xa < x.hi) a[o++] = sb[xa++];
+    while (xb < y.hi) { a[o] = a[xb]; o++; xb++; }
+  }
+  c->st->moves_merge_out += y.hi - x.lo;
+  c->counter = &c->st->comp_runs;
+  return r;
+}
+
+static void c_copy(ctx* c, buf curr) {
+  if (curr.h != 0) c->err = ORC_EINTERNAL; /* the final unwind merges into input */
+}
 
 /* ------------------------------------------------------------------------ */
 /* Variant B: Virtual-Memory pages (Sec. 4)                                 */
@@ -618,6 +690,9 @@ static buf d_merge(ctx* c, buf x, buf y) {
 }
 static void d_copy(ctx* c, buf curr) { (void)c; (void)curr; }
 
+static uint32_t g_vm_words = 0;
+void orc_set_vm_words(uint32_t T) { g_vm_words = T; }
+
 /* ------------------------------------------------------------------------ */
 /* entry points                                                             */
 /* ------------------------------------------------------------------------ */
@@ -652,6 +727,7 @@ static int run_common(int key_type, void* keys, uint32_t* vals, uint64_t n, int 
     }
   }
   strategy S;
+  S.push = NULL;
   if (dry) {
     S.new_buffer = d_new_buffer; S.extract_run = d_extract_run;
     S.merge_buffers = d_merge; S.copy = d_copy;
@@ -660,10 +736,18 @@ static int run_common(int key_type, void* keys, uint32_t* vals, uint64_t n, int 
     S.merge_buffers = a_merge; S.copy = a_copy;
     c.abuf = (item*)malloc(n * sizeof(item));
     if (!c.abuf) { free(c.a); return ORC_ENOMEM; }
+  } else if (variant == ORC_VARIANT_PINGPONG || variant == ORC_VARIANT_PINGPONG_PLAIN) {
+    S.new_buffer = a_new_buffer; S.extract_run = c_extract_run;
+    S.merge_buffers = c_merge; S.copy = c_copy; S.push = c_push;
+    c.stack_buf = (item*)malloc(n * sizeof(item)); /* stackBuf: n elements */
+    if (!c.stack_buf) { free(c.a); return ORC_ENOMEM; }
+    c.last_pop_opt = variant == ORC_VARIANT_PINGPONG;
+    st->peak_extra_elems = n;
   } else if (variant == ORC_VARIANT_VM) {
     S.new_buffer = b_new_buffer; S.extract_run = b_extract_run;
     S.merge_buffers = b_merge; S.copy = b_copy;
     uint32_t T = (key_type == ORC_U64 ? 2u : 1u) + (vals ? 1u : 0u); /* words (R9) */
+    if (g_vm_words) T = g_vm_words;
     vm* v = (vm*)calloc(1, sizeof(vm));
     v->P = orc_page_size(n, T);
     v->n_full_in = n / v->P;
@@ -705,6 +789,7 @@ static int run_common(int key_type, void* keys, uint32_t* vals, uint64_t n, int 
     free(v);
   }
   free(c.abuf);
+  free(c.stack_buf);
   free(c.a);
   return err;
 }

@@ -18,7 +18,9 @@ extern "C" {
 #endif
 
 enum { ORC_U32 = 0, ORC_U64 = 1, ORC_F32 = 2 };
-enum { ORC_VARIANT_COPYMERGE = 0, ORC_VARIANT_VM = 1 };
+/* variants: A copy-merge (Fig. 1), B Virtual-Memory (Sec. 4), C Pingpong (Sec. 3)
+ * with the last-pop right-to-left merge, C0 Pingpong without it */
+enum { ORC_VARIANT_COPYMERGE = 0, ORC_VARIANT_VM = 1, ORC_VARIANT_PINGPONG = 2, ORC_VARIANT_PINGPONG_PLAIN = 3 };
 enum { ORC_KIND_ASC = 0, ORC_KIND_DESC = 1, ORC_KIND_EXT = 2 };
 enum { ORC_OK = 0, ORC_EINVAL = -1, ORC_ECAP = -2, ORC_ENOMEM = -3, ORC_EINTERNAL = -4 };
 
@@ -34,7 +36,8 @@ typedef struct {
   uint64_t comp_runs, comp_merge;           /* comparisons: run formation / merge phase (C16) */
   uint64_t moves_runs;                      /* run formation: reversal + insertion sort assignments */
   uint64_t moves_merge_out;                 /* element writes of merge outputs (== M, C14) */
-  uint64_t moves_staging;                   /* A: left-run copies; B: extraction pushes */
+  uint64_t moves_staging;                   /* A: left-run copies; B: extraction pushes;
+                                               C: copies of pushed buffers into stackBuf */
   uint64_t moves_copy;                      /* B: final Copy (evictions + page copies) */
   uint64_t max_stack;                       /* max stack height */
   uint64_t reversed_elems, extended_runs;
@@ -58,6 +61,12 @@ int orc_less(int key_type, uint64_t a, uint64_t b);
 int orc_sort(int key_type, void* keys, uint32_t* vals, uint64_t n, int variant,
              uint32_t minrun_override, uint64_t* run_start, uint8_t* run_kind,
              uint64_t cap_runs, orc_merge_t* merges, orc_stats_t* st);
+
+/* Test hook (variant B only): page-size word count T used for P (reading R9)
+ * instead of the element's own (0 = the element's); lets the page flow of the
+ * paper's wider types (ptr T = 2, blob30 T = 30) be measured on the
+ * same key array.  Process-global, not thread safe. */
+void orc_set_vm_words(uint32_t T);
 
 /* Plan only: ExtractRun boundaries + Power + Alg. 1 without moving data. */
 int orc_plan(int key_type, const void* keys, uint64_t n, uint32_t minrun_override,

@@ -164,6 +164,23 @@ def test_exhaustive_binary_arrays():
                 _check_case(keys, mr)
 
 
+def test_exhaustive_tiny_c(tmp_path):
+    """AC1 at the survey's sizes: every permutation of
+    n <= 9 and every {0,1}-array of n <= 16, minruns 1/2/3/rule, all four
+    variants, vs the definition of the stable sort for those inputs (sorted
+    permutation = identity with the inverse permutation as payload; stable
+    partition for {0,1}), plus the plan / counter invariants per input
+    (tests/exhaustive_tiny.c)."""
+    import subprocess
+    exe = str(tmp_path / "exh")
+    here = os.path.dirname(os.path.abspath(__file__))
+    subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-o", exe, os.path.join(here, "exhaustive_tiny.c"),
+                           os.path.join(os.path.dirname(here), "oracle", "vmps_oracle.c"), "-lm"])
+    out = subprocess.run([exe, "9", "16"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "permutations(n<=9)=1636456" in out.stdout and "binary(n<=16)=393213" in out.stdout, out.stdout
+
+
 def _random_case(rng, n, dtype):
     kind = rng.integers(0, 5)
     if dtype == np.float32:
@@ -259,6 +276,22 @@ def test_counters_and_bounds(n):
         assert sb["moves_staging"] == n
         assert sb["moves_copy"] <= 2 * n
         assert sb["moves_merge_out"] + sb["moves_staging"] + sb["moves_copy"] <= M + 3 * n
+        # C (Pingpong, Sec. 3): same output and plan; C0 (no last-pop merge)
+        # merges left to right like A and B, so its comparisons are equal
+        (pc, pc0), (sc, sc0) = _check_case(keys, 0, variants=(oracle.VARIANT_C, oracle.VARIANT_C0))
+        for p_ in (pc, pc0):
+            assert (p_.run_start == pa.run_start).all() and (p_.merges == pa.merges).all()
+        assert sc0["comp_merge"] == sb["comp_merge"]
+        assert sc["comp_merge"] <= M - sc["merges"]             # right-to-left merges stop early too
+        assert sc["moves_merge_out"] == M and sc0["moves_merge_out"] == M
+        # every pushed fresh run is copied once, merge results never
+        assert sc["moves_staging"] <= n
+        mc = sc["moves_merge_out"] + sc["moves_staging"]
+        assert mc <= M + n
+        assert mc <= sc0["moves_merge_out"] + sc0["moves_staging"]  # SPEC AC11
+        mb = sb["moves_merge_out"] + sb["moves_staging"] + sb["moves_copy"]
+        assert abs(mb - mc) <= 3 * n                            # "same moves up to O(n)"
+        assert sc["peak_extra_elems"] == n                      # stackBuf: n T words (Fig. 4)
 
 
 @pytest.mark.parametrize("n", [10**3, 10**4, 10**5, 10**6])
@@ -278,6 +311,55 @@ def test_vm_memory_law(n):
     assert st["peak_extra_pages"] <= lg + 4
     # far below Pingpong's n*T and CPython's n/2*T words (Fig. 4)
     assert words <= 0.10 * n * T or n < 10**4
+
+
+def test_pingpong_last_pop_saves_moves():
+    """The last-pop right-to-left merge strictly saves staging
+    moves on a typical input (SPEC AC11: <= everywhere, < somewhere), and the
+    unoptimised Pingpong can copy an element more than once (its staging
+    exceeds n), which is why the paper needs the optimisation for M + n."""
+    rng = np.random.default_rng(11)
+    n = 50000
+    keys = rng.integers(0, 1 << 31, n).astype(np.uint32)
+    _, _, _, sc = oracle.sort(keys, None, variant=oracle.VARIANT_C, minrun_override=4)
+    _, _, _, sc0 = oracle.sort(keys, None, variant=oracle.VARIANT_C0, minrun_override=4)
+    assert sc["moves_staging"] < sc0["moves_staging"]
+    assert sc["moves_staging"] <= n < sc0["moves_staging"]
+
+
+# Fig. 4 (P:804-815): average extra memory of VM Powersort on the paper's
+# inputs (n ~ U[9e6, 1e7]): int 1.0 MB, ptr 1.5 MB, zeroBlob30 / randomBlob30
+# 6 MB; Pingpong = input size (36.2 MB for int).
+FIG4_VM_MB = {1: 1.0, 2: 1.5, 30: 6.0}
+
+
+def test_vm_memory_fig4_magnitude():
+    """Magnitude pin of the VM variant's main-buffer memory against Fig. 4.
+    The paper pre-allocates the worst-case reserve (App. B "Pre-allocation of
+    buffers") and reports it; the oracle takes pages on demand and
+    reports its peak.  So the peak must not exceed the printed figure, must be
+    within 100x of it (the same O(sqrt(n T log n)) regime, not O(n): Pingpong
+    needs 36.2 MB), and must grow from int to the wider types (ptr: T = 2
+    words, blob30: T = 30; page size by reading R9) in the same direction.
+    Measured ratios are recorded in DESIGN.md."""
+    import workloads as W
+    d, n = W.paper_input(100, "int", seed=0)
+    assert 9 * 10**6 <= n <= 10**7
+    keys = W.to_numpy(d)
+    peak = {}
+    try:
+        for T in (1, 2, 30):
+            oracle.set_vm_words(T)
+            _, _, _, st = oracle.sort(keys, None, variant=oracle.VARIANT_B)
+            assert st["page_elems"] == oracle.page_size(n, T)
+            peak[T] = st["peak_extra_pages"] * st["page_elems"] * T * 4 / 2**20  # MiB (Fig. 4's "MB")
+    finally:
+        oracle.set_vm_words(0)
+    for T, mb in peak.items():
+        assert FIG4_VM_MB[T] / 100 <= mb <= FIG4_VM_MB[T], (T, mb)
+    assert peak[1] <= peak[2] <= peak[30]
+    # far below Pingpong's n T (Fig. 4: 36.2 MB for int)
+    assert peak[1] < 0.01 * n * 4 / 2**20
 
 
 def test_page_size_rule():
