@@ -176,20 +176,42 @@ def workspace_bytes(n: int, kt: int, has_vals: int, scratch: int = SCRATCH_UNBOU
 
 
 class Workspace:
-    """A reusable device workspace (grown on demand) for repeated sorts."""
+    """A reusable device workspace (grown on demand) for repeated sorts.
+
+    The C ABI requires concurrent calls to use separate workspaces; one
+    Workspace may still be used from several streams one after another: every
+    use on a stream other than the allocating one is recorded
+    (``record_stream``), so the caching allocator does not hand the memory
+    out again while that stream's sort may still read it (also when the
+    buffer is replaced by a larger one)."""
 
     def __init__(self, device=None):
         self.device = torch.device(device) if device is not None else None
         self.buf = None
+        self._alloc_stream = None
 
-    def get(self, nbytes: int, device) -> torch.Tensor:
+    def get(self, nbytes: int, device, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        device = torch.device(device)
+        cur = stream if stream is not None else torch.cuda.current_stream(device)
         if self.buf is None or self.buf.numel() < nbytes or self.buf.device != device:
             self.buf = None
-            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            with torch.cuda.stream(cur):
+                self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self._alloc_stream = cur.cuda_stream
+        elif cur.cuda_stream != self._alloc_stream:
+            self.buf.record_stream(cur)
         return self.buf
 
 
+# default workspaces, one per (device, stream): sorts on different streams
+# never share one implicitly
 _default_ws: dict = {}
+
+
+def _default_workspace(device, stream: torch.cuda.Stream | None = None) -> Workspace:
+    device = torch.device(device)
+    sp = (stream if stream is not None else torch.cuda.current_stream(device)).cuda_stream
+    return _default_ws.setdefault((device, sp), Workspace())
 
 
 def _stream_ptr(device) -> int:
@@ -214,7 +236,7 @@ def sort_(keys: torch.Tensor, values: torch.Tensor | None = None, scratch: int |
             raise ValueError("values must be contiguous on the keys' device")
     sc = SCRATCH_UNBOUNDED if scratch is None else int(scratch)
     nbytes = workspace_bytes(n, kt, 1 if values is not None else 0, sc)
-    ws = workspace if workspace is not None else _default_ws.setdefault(keys.device, Workspace())
+    ws = workspace if workspace is not None else _default_workspace(keys.device)
     buf = ws.get(nbytes, keys.device)
     st = Stats()
     sp = ctypes.byref(st) if stats else None
@@ -260,10 +282,15 @@ def sort_host_(keys: torch.Tensor, values: torch.Tensor | None = None, scratch: 
     dv = None
     if values is not None:
         dv = d_values if d_values is not None else torch.empty_like(values, device=dev)
+    if stream is not None:  # buffers allocated here are used on `stream`
+        if d_keys is None:
+            dk.record_stream(stream)
+        if dv is not None and d_values is None:
+            dv.record_stream(stream)
     sc = SCRATCH_UNBOUNDED if scratch is None else int(scratch)
     nbytes = workspace_bytes(n, kt, 1 if values is not None else 0, sc)
-    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
-    buf = ws.get(nbytes, dev)
+    ws = workspace if workspace is not None else _default_workspace(dev, stream)
+    buf = ws.get(nbytes, dev, stream)
     L = lib()
     ko = out_keys.data_ptr() if out_keys is not None else None
     with torch.cuda.device(dev):
@@ -294,7 +321,7 @@ def merge_plan(keys: torch.Tensor, workspace: Workspace | None = None) -> Plan:
     n = keys.numel()
     dev = keys.device
     nbytes = workspace_bytes(n, kt, -1)
-    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    ws = workspace if workspace is not None else _default_workspace(dev)
     buf = ws.get(nbytes, dev)
     L = lib()
     nr = ctypes.c_uint64(0)
@@ -331,7 +358,7 @@ def shard_chain(keys: torch.Tensor, minrun: int, n_end: int, prev: torch.Tensor 
     L = lib()
     nb = ctypes.c_size_t(0)
     _check(L.vmps_shard_workspace_bytes(keys.numel(), kt, minrun, ctypes.byref(nb)), "vmps_shard_workspace_bytes")
-    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    ws = workspace if workspace is not None else _default_workspace(dev)
     buf = ws.get(int(nb.value), dev)
     tab = torch.empty(3 * minrun, dtype=torch.int64, device=dev)
     nh = 0 if halo is None else halo.numel()
@@ -353,7 +380,7 @@ def shard_runs(keys: torch.Tensor, minrun: int, n_end: int, entry_state: int, co
     L = lib()
     nb = ctypes.c_size_t(0)
     _check(L.vmps_shard_workspace_bytes(keys.numel(), kt, minrun, ctypes.byref(nb)), "vmps_shard_workspace_bytes")
-    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    ws = workspace if workspace is not None else _default_workspace(dev)
     buf = ws.get(int(nb.value), dev)
     rs = out if out is not None else torch.empty(max(count, 1), dtype=torch.int64, device=dev)
     rk = torch.empty(max(count, 1), dtype=torch.uint8, device=dev)
@@ -377,7 +404,7 @@ def plan_from_runs(run_start: torch.Tensor, n: int, workspace: Workspace | None 
     L = lib()
     nb = ctypes.c_size_t(0)
     _check(L.vmps_plan_workspace_bytes(r, ctypes.byref(nb)), "vmps_plan_workspace_bytes")
-    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    ws = workspace if workspace is not None else _default_workspace(dev)
     buf = ws.get(int(nb.value), dev)
     mg = torch.empty((r - 1) * 4, dtype=torch.int64, device=dev)
     with torch.cuda.device(dev):
@@ -404,7 +431,7 @@ def sort_records(records: torch.Tensor, out: torch.Tensor | None = None, perm: b
     L = lib()
     nb = ctypes.c_size_t(0)
     _check(L.vmps_sort_records_workspace_bytes(n, words, ctypes.byref(nb)), "vmps_sort_records_workspace_bytes")
-    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    ws = workspace if workspace is not None else _default_workspace(dev)
     buf = ws.get(int(nb.value), dev)
     with torch.cuda.device(dev):
         rc = L.vmps_sort_records(records.data_ptr(), res.data_ptr(), None if pm is None else pm.data_ptr(), n, words,
@@ -427,7 +454,7 @@ def merge_pieces(key_ptrs: list[int], val_ptrs: list[int] | None, counts: list[i
     nb = ctypes.c_size_t(0)
     _check(L.vmps_merge_pieces_workspace_bytes(N, kt, 1 if out_values is not None else 0, g, ctypes.byref(nb)),
            "vmps_merge_pieces_workspace_bytes")
-    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    ws = workspace if workspace is not None else _default_workspace(dev)
     buf = ws.get(int(nb.value), dev)
     kp = (ctypes.c_void_p * g)(*key_ptrs)
     vpa = (ctypes.c_void_p * g)(*val_ptrs) if val_ptrs is not None else None
@@ -507,7 +534,7 @@ def sort_dist_native_(comm: Comm, keys: torch.Tensor, values: torch.Tensor | Non
     nb = ctypes.c_size_t(0)
     _check(L.vmps_dist_workspace_bytes(n, kt, 1 if values is not None else 0, comm.world, sc, ctypes.byref(nb)),
            "vmps_dist_workspace_bytes")
-    ws = workspace if workspace is not None else _default_ws.setdefault(keys.device, Workspace())
+    ws = workspace if workspace is not None else _default_workspace(keys.device)
     buf = ws.get(int(nb.value), keys.device)
     st = Stats()
     sp = ctypes.byref(st) if stats else None
@@ -533,7 +560,7 @@ def merge_plan_dist_native(comm: Comm, keys: torch.Tensor, n_total: int,
     nb = ctypes.c_size_t(0)
     _check(L.vmps_merge_plan_dist_workspace_bytes(n_total, n, kt, comm.world, ctypes.byref(nb)),
            "vmps_merge_plan_dist_workspace_bytes")
-    ws = workspace if workspace is not None else _default_ws.setdefault(dev, Workspace())
+    ws = workspace if workspace is not None else _default_workspace(dev)
     buf = ws.get(int(nb.value), dev)
     cap = max(n, 1) + 2
     rs = torch.empty(cap, dtype=torch.int64, device=dev)

@@ -194,7 +194,10 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
       // [i,k) spans ceil(k/T) - floor(i/T) <= (k-i)/T + 2 aligned tiles
       t.desc = take((size_t)t.part_cap * sizeof(TileDesc));
     }
-    t.scan_tmp = (uint32_t*)take(scan_tmp_words(R) * 4 + 64);
+    // the bounded mode also scans its dirty-block flags (NB + 1 entries),
+    // which exceed R when the block is smaller than minrun
+    const size_t scan_len = t.bounded ? std::max<size_t>(R, (size_t)((n + c.P - 1) / c.P) + 1) : R;
+    t.scan_tmp = (uint32_t*)take(scan_tmp_words(scan_len) * 4 + 64);
   }
   t.counters = (unsigned long long*)take(8 * 8);
   t.fuse2 = c.fuse2;
@@ -651,12 +654,13 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       LAUNCH(k4_node_runs, grid_for(w.n4cap), 256, 0, s, w.run_start, w.seg_l, w.seg_r, dep, w.lchild, w.rchild,
              w.lnodes, w.level_start, p, nr);
       LAUNCH(k4_desc<KT>, (std::max<uint32_t>(w.part_cap / 4, std::min<uint32_t>(w.part_cap, 4 * DESC4_SERIAL_MIN)) + 256) / 256, 256, 0, s, k0, k1, nr, w.ltiles, w.level_start,
-             w.level_tile, p, w.tout, t4, desc_warp_max);
+             w.level_tile, p, w.tout, t4, desc_warp_max, w.part_cap, w.scalars);
       if (desc_warp_max)
         LAUNCH(k4_desc_warp<KT>, (32u * std::min<uint32_t>(w.part_cap, desc_warp_max) + 255) / 256, 256, 0, s, k0, k1,
-               nr, w.ltiles, w.level_start, w.level_tile, p, w.tout, t4, desc_warp_max);
+               nr, w.ltiles, w.level_start, w.level_tile, p, w.tout, t4, desc_warp_max, w.part_cap);
       int e1 = prof_event(s);
-      LAUNCH((k4_merge_level<KT, HV, M4_KQ>), gm4, 4096 / M4_KQ + 32, SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.level_tile, p);
+      LAUNCH((k4_merge_level<KT, HV, M4_KQ>), gm4, 4096 / M4_KQ + 32, SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.level_tile, p,
+             w.part_cap);
       ++g_nl_merge;
       int e2 = prof_event(s);
       if (g_prof && e0 >= 0 && e2 >= 0 && g_prof_nm < 128) {
@@ -693,6 +697,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   }
   }  // level-by-level merges
   LAUNCH(k_check_levels, 1, 32, 0, s, w.level_cnt, p_hi, w.scalars);
+  if (!st) LAUNCH(k_error_guard, 1, 1, 0, s, w.scalars);  // with h_stats: VMPS_ERR_INTERNAL below
   rc = launch_check();
   if (rc != VMPS_OK) return rc;
   g_prof_mark[3] = prof_event(s);

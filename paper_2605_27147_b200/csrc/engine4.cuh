@@ -277,9 +277,14 @@ __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* 
                                                const NodeRuns* __restrict__ nr, const uint32_t* __restrict__ ltiles,
                                                const uint32_t* __restrict__ level_start,
                                                const uint32_t* __restrict__ level_tile, int p, uint32_t tout,
-                                               TileDesc4* __restrict__ tiles, uint32_t warp_max) {
+                                               TileDesc4* __restrict__ tiles, uint32_t warp_max, uint32_t cap,
+                                               uint32_t* scalars) {
   const uint32_t ls = level_start[p], le = level_start[p + 1];
   const uint32_t tb = level_tile[p], te = level_tile[p + 1];
+  if (te - tb > cap) {  // never expected: the bound in carve() is exact
+    if (blockIdx.x == 0 && threadIdx.x == 0) scalars[SC_ERROR] = 2;
+    return;
+  }
   // chunk length: a level of few tiles is bound by the length of each
   // thread's chain of dependent probes, so every tile gets its own thread
   // (below DESC4_SERIAL_MIN tiles), then three; large levels use DESC4_CHUNK
@@ -352,11 +357,12 @@ __global__ void __launch_bounds__(256) k4_desc_warp(const typename KeyTraits<KT>
                                                     const uint32_t* __restrict__ ltiles,
                                                     const uint32_t* __restrict__ level_start,
                                                     const uint32_t* __restrict__ level_tile, int p, uint32_t tout,
-                                                    TileDesc4* __restrict__ tiles, uint32_t warp_max) {
+                                                    TileDesc4* __restrict__ tiles, uint32_t warp_max,
+                                                    uint32_t cap) {
   const uint32_t ls = level_start[p], le = level_start[p + 1];
   const uint32_t tb = level_tile[p], te = level_tile[p + 1];
   const uint32_t ntl = te - tb;
-  if (ntl < warp_max) {
+  if (ntl < warp_max && ntl <= cap) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < ntl; wi += nw) {
@@ -401,6 +407,8 @@ struct Merge4Smem {
   // stages of the TMA pipeline: u64 keys with payload use VMPS_U64_STAGES
   // (one stage fits two CTAs per SM), all others two
   static constexpr uint32_t NSTG = (sizeof(K) == 8 && HV) ? VMPS_U64_STAGES : 2u;
+  // the barrier area holds two full / empty pairs and the header area two Merge4Hdr
+  static_assert(NSTG >= 1 && NSTG <= 2, "merge4: at most two pipeline stages");
   static constexpr uint32_t IK = 4096 * sizeof(K);  // intermediate keys
   static constexpr uint32_t II = 4096 * 2;          // intermediate value indices (u16)
   static constexpr uint32_t BYTES = HDR + NSTG * STAGE + IK + II;
@@ -737,7 +745,7 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
     const TileDesc4* __restrict__ tiles, const NodeRuns* __restrict__ nr,
-    const uint32_t* __restrict__ level_tile, int p) {
+    const uint32_t* __restrict__ level_tile, int p, uint32_t cap) {
   using K = typename KeyTraits<KT>::K;
   using SM = Merge4Smem<KT, HV>;
   constexpr uint32_t NT = 4096 / KQ;  // consumer threads
@@ -748,7 +756,7 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
   K* IKs = reinterpret_cast<K*>(smem + SM::HDR + SM::NSTG * SM::STAGE);
   uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK);
   const uint32_t count = level_tile[p + 1] - level_tile[p];
-  if (blockIdx.x >= count) return;
+  if (blockIdx.x >= count || count > cap) return;  // count > cap: flagged by k4_desc
   const uint32_t tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(&full[0], 1);

@@ -384,6 +384,14 @@ __global__ void k_check_levels(const uint32_t* level_cnt, int p_hi, uint32_t* sc
     if (level_cnt[p]) scalars[SC_ERROR] = 1;
 }
 
+// Internal-consistency guard of a sort called without h_stats (nothing is
+// read back to report VMPS_ERR_INTERNAL): a tripped SC_ERROR aborts the
+// kernel, so the error surfaces loudly at the caller's next synchronisation
+// instead of a silently partial result.  Never expected to fire.
+__global__ void k_error_guard(const uint32_t* scalars) {
+  if (scalars[SC_ERROR]) __trap();
+}
+
 // ---------------------------------------------------------------------------
 // Exclusive scan of u32 (block scan + recursive block offsets).
 // ---------------------------------------------------------------------------

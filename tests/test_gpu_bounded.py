@@ -139,3 +139,16 @@ def test_bounded_block_skip(vm, kind):
                 assert st["rounds"] <= st["levels_executed"] + 2, st
     finally:
         vm.test_set_tiles(0, 0, 0)
+
+
+def test_bounded_blocks_below_minrun(vm):
+    """Blocks smaller than minrun at a size where the dirty-block scan (n/P + 1
+    entries) is longer than the per-run arrays (n/minrun + 2): scratch = 200
+    elements gives 16-element blocks at minrun 32 (the scan's
+    temporary was sized by the run count and overflowed).  Identical to the
+    oracle."""
+    vm.test_set_tiles(0, 0, 0)
+    n = 1 << 20
+    k, v = W.cfg2(n=n, device="cpu")
+    st = bounded_vs_oracle(vm, W.to_numpy(k), W.to_numpy(v), scratch=200)
+    assert st["block_elems"] == 16 and st["minrun"] == 32
