@@ -637,7 +637,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       VMPS_CK(cudaFuncSetAttribute(k4_merge_level<KT, HV, M4_KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)SM4::BYTES));
       int occ = 0;
-      VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_merge_level<KT, HV, M4_KQ>, 4096 / M4_KQ + 32,
+      VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_merge_level<KT, HV, M4_KQ>, m4_threads<M4_KQ>(),
                                                             SM4::BYTES));
       occ4[KT][HV] = occ > 0 ? occ : 1;
     }
@@ -654,13 +654,12 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       LAUNCH(k4_node_runs, grid_for(w.n4cap), 256, 0, s, w.run_start, w.seg_l, w.seg_r, dep, w.lchild, w.rchild,
              w.lnodes, w.level_start, p, nr);
       LAUNCH(k4_desc<KT>, (std::max<uint32_t>(w.part_cap / 4, std::min<uint32_t>(w.part_cap, 4 * DESC4_SERIAL_MIN)) + 256) / 256, 256, 0, s, k0, k1, nr, w.ltiles, w.level_start,
-             w.level_tile, p, w.tout, t4, desc_warp_max, w.part_cap, w.scalars);
+             w.level_tile, p, w.tout, t4, desc_warp_max);
       if (desc_warp_max)
         LAUNCH(k4_desc_warp<KT>, (32u * std::min<uint32_t>(w.part_cap, desc_warp_max) + 255) / 256, 256, 0, s, k0, k1,
-               nr, w.ltiles, w.level_start, w.level_tile, p, w.tout, t4, desc_warp_max, w.part_cap);
+               nr, w.ltiles, w.level_start, w.level_tile, p, w.tout, t4, desc_warp_max);
       int e1 = prof_event(s);
-      LAUNCH((k4_merge_level<KT, HV, M4_KQ>), gm4, 4096 / M4_KQ + 32, SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.level_tile, p,
-             w.part_cap);
+      LAUNCH((k4_merge_level<KT, HV, M4_KQ>), gm4, m4_threads<M4_KQ>(), SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.level_tile, p);
       ++g_nl_merge;
       int e2 = prof_event(s);
       if (g_prof && e0 >= 0 && e2 >= 0 && g_prof_nm < 128) {
@@ -696,7 +695,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
     }
   }
   }  // level-by-level merges
-  LAUNCH(k_check_levels, 1, 32, 0, s, w.level_cnt, p_hi, w.scalars);
+  LAUNCH(k_check_levels, 1, 32, 0, s, w.level_cnt, p_hi, w.scalars, w.fuse2 ? w.level_tile : nullptr, w.part_cap);
   if (!st) LAUNCH(k_error_guard, 1, 1, 0, s, w.scalars);  // with h_stats: VMPS_ERR_INTERNAL below
   rc = launch_check();
   if (rc != VMPS_OK) return rc;
@@ -1404,7 +1403,7 @@ static vmps_status_t pull_pass(const void* const* kp, const uint32_t* const* vp,
     VMPS_CK(cudaFuncSetAttribute(k_pull_merge<KT, HV, M4_KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)SM4::BYTES));
     int o = 0;
-    VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_pull_merge<KT, HV, M4_KQ>, 4096 / M4_KQ + 32,
+    VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_pull_merge<KT, HV, M4_KQ>, m4_threads<M4_KQ>(),
                                                           SM4::BYTES));
     occ[KT][HV] = o > 0 ? o : 1;
   }
@@ -1412,7 +1411,7 @@ static vmps_status_t pull_pass(const void* const* kp, const uint32_t* const* vp,
   const uint32_t nchunks = (ntiles + DESC4_CHUNK - 1) / DESC4_CHUNK;
   LAUNCH(k_pull_desc<KT>, (nchunks + 255) / 256, 256, 0, s, S, ntiles, tiles);
   LAUNCH((k_pull_merge<KT, HV, M4_KQ>), (unsigned)std::min<uint32_t>(ntiles, nsm() * occ[KT][HV]),
-         4096 / M4_KQ + 32, SM4::BYTES, s, S, (K*)ok, ov, tiles, ntiles);
+         m4_threads<M4_KQ>(), SM4::BYTES, s, S, (K*)ok, ov, tiles, ntiles);
   return launch_check();
 }
 

@@ -39,9 +39,12 @@ __device__ __forceinline__ uint32_t corank(const typename KeyTraits<KT>::K* A, u
                                            uint32_t d) {
   using T = KeyTraits<KT>;
   uint32_t lo = d > nB ? d - nB : 0u, hi = min(d, nA);
+  // B[d - mid - 1] = Bd[-mid]: both probe addresses are one multiply-add
+  // from mid (fewer instructions in this latency-bound loop)
+  const typename KeyTraits<KT>::K* Bd = B + d - 1;
   while (lo < hi) {
     uint32_t mid = (lo + hi) >> 1;
-    if (T::ord(A[mid]) <= T::ord(B[d - mid - 1])) lo = mid + 1;  // A[mid] precedes B[d-mid-1]
+    if (T::ord(A[mid]) <= T::ord(Bd[-(int32_t)mid])) lo = mid + 1;  // A[mid] precedes B[d-mid-1]
     else hi = mid;
   }
   return lo;
@@ -455,9 +458,10 @@ __device__ __forceinline__ uint32_t corank_in(const typename KeyTraits<KT>::K* A
                                               uint32_t d, uint32_t lb, uint32_t ub) {
   using T = KeyTraits<KT>;
   uint32_t lo = max(d > nB ? d - nB : 0u, lb), hi = min(min(d, nA), ub);
+  const typename KeyTraits<KT>::K* Bd = B + d - 1;  // B[d - mid - 1] = Bd[-mid]
   while (lo < hi) {
     uint32_t mid = (lo + hi) >> 1;
-    if (T::ord(A[mid]) <= T::ord(B[d - mid - 1])) lo = mid + 1;  // A[mid] precedes B[d-mid-1]
+    if (T::ord(A[mid]) <= T::ord(Bd[-(int32_t)mid])) lo = mid + 1;  // A[mid] precedes B[d-mid-1]
     else hi = mid;
   }
   return lo;

@@ -277,14 +277,9 @@ __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* 
                                                const NodeRuns* __restrict__ nr, const uint32_t* __restrict__ ltiles,
                                                const uint32_t* __restrict__ level_start,
                                                const uint32_t* __restrict__ level_tile, int p, uint32_t tout,
-                                               TileDesc4* __restrict__ tiles, uint32_t warp_max, uint32_t cap,
-                                               uint32_t* scalars) {
+                                               TileDesc4* __restrict__ tiles, uint32_t warp_max) {
   const uint32_t ls = level_start[p], le = level_start[p + 1];
   const uint32_t tb = level_tile[p], te = level_tile[p + 1];
-  if (te - tb > cap) {  // never expected: the bound in carve() is exact
-    if (blockIdx.x == 0 && threadIdx.x == 0) scalars[SC_ERROR] = 2;
-    return;
-  }
   // chunk length: a level of few tiles is bound by the length of each
   // thread's chain of dependent probes, so every tile gets its own thread
   // (below DESC4_SERIAL_MIN tiles), then three; large levels use DESC4_CHUNK
@@ -357,12 +352,11 @@ __global__ void __launch_bounds__(256) k4_desc_warp(const typename KeyTraits<KT>
                                                     const uint32_t* __restrict__ ltiles,
                                                     const uint32_t* __restrict__ level_start,
                                                     const uint32_t* __restrict__ level_tile, int p, uint32_t tout,
-                                                    TileDesc4* __restrict__ tiles, uint32_t warp_max,
-                                                    uint32_t cap) {
+                                                    TileDesc4* __restrict__ tiles, uint32_t warp_max) {
   const uint32_t ls = level_start[p], le = level_start[p + 1];
   const uint32_t tb = level_tile[p], te = level_tile[p + 1];
   const uint32_t ntl = te - tb;
-  if (ntl < warp_max && ntl <= cap) {
+  if (ntl < warp_max) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wi < ntl; wi += nw) {
@@ -409,15 +403,33 @@ struct Merge4Smem {
   static constexpr uint32_t NSTG = (sizeof(K) == 8 && HV) ? VMPS_U64_STAGES : 2u;
   // the barrier area holds two full / empty pairs and the header area two Merge4Hdr
   static_assert(NSTG >= 1 && NSTG <= 2, "merge4: at most two pipeline stages");
-  static constexpr uint32_t IK = 4096 * sizeof(K);  // intermediate keys
-  static constexpr uint32_t II = 4096 * 2;          // intermediate value indices (u16)
+  // intermediate: P01 at [0, n01), P23 at [round8(n01), round8(n01) + n23)
+  // (<= 4096 + 7 positions) plus read-ahead slack
+  static constexpr uint32_t IPOS = 4096 + 32;
+  static constexpr uint32_t IK = IPOS * sizeof(K);  // intermediate keys
+  static constexpr uint32_t II = IPOS * 2;          // intermediate value indices (u16)
   static constexpr uint32_t BYTES = HDR + NSTG * STAGE + IK + II;
 };
 
+// Consumer threads of a 4096-output tile: 4096 / KQ for the outputs plus one
+// warp, because step A lays P23 out from the first multiple of KQ at or
+// after n01, so that no thread's chunk straddles P01 and P23 (a straddling
+// thread ran two searches and two serial loops and held the whole CTA at the
+// step A barrier); the two parts then need up to 4096 / KQ + 1 chunks.
+template <int KQ>
+__host__ __device__ constexpr uint32_t m4_consumers() { return 4096u / KQ + 32u; }
+template <int KQ>
+__host__ __device__ constexpr uint32_t m4_threads() { return m4_consumers<KQ>() + 32u; }
+constexpr int M4_WARPS = 4096 / (32 * M4_KQ) + 1;  // consumer warps of a tile (17)
 struct Merge4Hdr {
   uint32_t kb[4], n[4];  // key element offset / count of each window in the stage
   uint32_t vb[4];        // value element offset of each window
   uint32_t lo, hi, par, mode;  // mode: 0 general, 1 two runs (W0, W2), 2 + w single run w
+  // step A warp boundaries (written by the producer warp once the stage has
+  // landed): bnd[w] = co-rank of the 2-way merge that intermediate position
+  // 256 w belongs to (P01 = W0 (+) W1 below n01, P23 = W2 (+) W3 above), at
+  // that position's diagonal within its merge
+  uint16_t bnd[M4_WARPS + 1];
 };
 static_assert(64 + 2 * sizeof(Merge4Hdr) <= 512, "merge4 header area");
 
@@ -503,80 +515,87 @@ __device__ __forceinline__ void merge4_issue(const TileDesc4& d, const TileDesc4
 // the tile's last chunk) runs each of its parts for exactly its length, so
 // that thread costs about as much as the others (P23's part starts at
 // diagonal 0 and needs no search).
+// Step A layout: P01 = W0 (+) W1 at intermediate positions [0, n01), P23 =
+// W2 (+) W3 at [n01p, n01p + n23) with n01p = n01 rounded up to a multiple of
+// KQ, so every thread's KQ-chunk lies in one of the two merges.
+template <int KQ>
+__device__ __forceinline__ uint32_t m4_n01p(uint32_t n01) { return (n01 + (uint32_t)KQ - 1) & ~((uint32_t)KQ - 1); }
+
+// The co-rank of intermediate position q (< n01p + n23) within its 2-way
+// merge; one lane of the producer warp per consumer warp boundary q = 256 w.
+template <int KT, int KQ>
+__device__ __forceinline__ uint32_t merge4_boundary(const typename KeyTraits<KT>::K* SK, const Merge4Hdr& h,
+                                                    uint32_t q) {
+  const uint32_t n01 = h.n[0] + h.n[1], n01p = m4_n01p<KQ>(n01);
+  const uint32_t wa = q < n01p ? 0u : 2u;
+  return corank<KT>(SK + h.kb[wa], h.n[wa], SK + h.kb[wa + 1], h.n[wa + 1], q - (q < n01p ? 0u : n01p));
+}
+
+// Step A: P01 and P23 into the intermediate (keys + the stage index of each
+// value), KQ outputs per thread by the unrolled branch-free merge over
+// absolute stage indices (a read past a window stays inside the stage:
+// windows are padded).  A part's last chunk runs all KQ steps and stores only
+// its in-range outputs.  With have_bnd, the co-rank search is bracketed by the
+// producer's co-ranks at this warp's boundaries.
 template <int KT, int KQ>
 __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK, const Merge4Hdr* hp,
-                                             uint32_t n01, uint32_t T4, typename KeyTraits<KT>::K* IKs,
-                                             uint16_t* IIs) {
+                                             typename KeyTraits<KT>::K* IKs, uint16_t* IIs, bool have_bnd) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
+  const uint32_t n01 = hp->n[0] + hp->n[1], n23 = hp->n[2] + hp->n[3];
+  const uint32_t n01p = m4_n01p<KQ>(n01);
   const uint32_t q0 = threadIdx.x * (uint32_t)KQ;
-  if (q0 >= T4) return;
-  const bool inA = q0 + (uint32_t)KQ <= n01, inB = q0 >= n01 && q0 + (uint32_t)KQ <= T4;
-  if (inA || inB) {
-    const uint32_t wa = inA ? 0u : 2u;
-    const uint32_t nA = hp->n[wa], nB = hp->n[wa + 1];
-    const uint32_t ka0 = hp->kb[wa], kb0 = hp->kb[wa + 1];
-    const int32_t dA = (int32_t)hp->vb[wa] - (int32_t)ka0, dB = (int32_t)hp->vb[wa + 1] - (int32_t)kb0;
-    const uint32_t d = q0 - (inA ? 0u : n01);
-    const uint32_t l = corank<KT>(SK + ka0, nA, SK + kb0, nB, d);
-    uint32_t ia = ka0 + l, ib = kb0 + d - l;
-    const uint32_t ea = ka0 + nA, eb = kb0 + nB;
-    K ka = SK[ia], kb = SK[ib];
-    typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load
-    K rk[KQ];
-    uint32_t ri[KQ];
+  const bool part0 = q0 < n01p;
+  const uint32_t base = part0 ? 0u : n01p, plen = part0 ? n01 : n23;
+  const uint32_t d = q0 - base;
+  if (d >= plen) return;  // past P23 (part 0 chunks always start inside P01)
+  const uint32_t wa = part0 ? 0u : 2u;
+  const uint32_t nA = hp->n[wa], nB = hp->n[wa + 1];
+  const uint32_t ka0 = hp->kb[wa], kb0 = hp->kb[wa + 1];
+  const int32_t dA = (int32_t)hp->vb[wa] - (int32_t)ka0, dB = (int32_t)hp->vb[wa + 1] - (int32_t)kb0;
+  uint32_t lb = 0u, ub = 0xFFFFFFFFu;
+  if (have_bnd) {
+    // c(x1) = c1 <= c(d) <= c(x2) = c2, c(d) - c1 <= d - x1, c2 - c(d) <= x2 - d
+    const uint32_t w = threadIdx.x >> 5;
+    const uint32_t ws = w * 32u * (uint32_t)KQ, we = ws + 32u * (uint32_t)KQ;
+    uint32_t x1 = 0u, c1 = 0u, x2 = nA + nB, c2 = nA;
+    if (ws >= base) { x1 = ws - base; c1 = hp->bnd[w]; }
+    if (we < base + plen) { x2 = we - base; c2 = hp->bnd[w + 1]; }
+    lb = max(c1, c2 > x2 - d ? c2 - (x2 - d) : 0u);
+    ub = min(c2, c1 + (d - x1));
+  }
+  const uint32_t l = corank_in<KT>(SK + ka0, nA, SK + kb0, nB, d, lb, ub);
+  uint32_t ia = ka0 + l, ib = kb0 + d - l;
+  const uint32_t ea = ka0 + nA, eb = kb0 + nB;
+  K ka = SK[ia], kb = SK[ib];
+  typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load
+  K rk[KQ];
+  uint32_t ri[KQ];
 #pragma unroll
-    for (int q = 0; q < KQ; ++q) {
-      const bool pa = ib >= eb || (ia < ea && oa <= ob);
-      rk[q] = pa ? ka : kb;
-      ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
-      ia += pa ? 1u : 0u;
-      ib += pa ? 0u : 1u;
-      const K nx = SK[pa ? ia : ib];
-      const typename KeyTraits<KT>::O onx = T::ord(nx);
-      ka = pa ? nx : ka;
-      oa = pa ? onx : oa;
-      kb = pa ? kb : nx;
-      ob = pa ? ob : onx;
-    }
+  for (int q = 0; q < KQ; ++q) {
+    const bool pa = ib >= eb || (ia < ea && oa <= ob);
+    rk[q] = pa ? ka : kb;
+    ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
+    ia += pa ? 1u : 0u;
+    ib += pa ? 0u : 1u;
+    const K nx = SK[pa ? ia : ib];
+    const typename KeyTraits<KT>::O onx = T::ord(nx);
+    ka = pa ? nx : ka;
+    oa = pa ? onx : oa;
+    kb = pa ? kb : nx;
+    ob = pa ? ob : onx;
+  }
+  if (d + (uint32_t)KQ <= plen) {
 #pragma unroll
     for (int q = 0; q < KQ; ++q) IKs[q0 + q] = rk[q];
 #pragma unroll
     for (int q = 0; q < KQ; q += 8)
       *reinterpret_cast<uint4*>(IIs + q0 + q) = make_uint4(ri[q] | (ri[q + 1] << 16), ri[q + 2] | (ri[q + 3] << 16),
                                                            ri[q + 4] | (ri[q + 5] << 16), ri[q + 6] | (ri[q + 7] << 16));
-    return;
-  }
-  const uint32_t q1 = min(q0 + (uint32_t)KQ, T4);
-#pragma unroll 1
-  for (uint32_t part = (q0 < n01 ? 0u : 1u); part < 2u; ++part) {
-    const uint32_t plo = part ? n01 : 0u, phi = part ? T4 : n01;
-    const uint32_t qs = max(q0, plo), qe = min(q1, phi);
-    if (qs >= qe) continue;
-    const uint32_t wa = 2u * part;
-    const uint32_t nA = hp->n[wa], nB = hp->n[wa + 1];
-    const uint32_t ka0 = hp->kb[wa], kb0 = hp->kb[wa + 1];
-    const int32_t dA = (int32_t)hp->vb[wa] - (int32_t)ka0, dB = (int32_t)hp->vb[wa + 1] - (int32_t)kb0;
-    const uint32_t d = qs - plo;
-    const uint32_t l = corank<KT>(SK + ka0, nA, SK + kb0, nB, d);
-    uint32_t ia = ka0 + l, ib = kb0 + d - l;
-    const uint32_t ea = ka0 + nA, eb = kb0 + nB;
-    K ka = SK[ia], kb = SK[ib];
-    typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load
-#pragma unroll 1
-    for (uint32_t pos = qs; pos < qe; ++pos) {
-      const bool pa = ib >= eb || (ia < ea && oa <= ob);
-      IKs[pos] = pa ? ka : kb;
-      IIs[pos] = (uint16_t)(pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB));
-      ia += pa ? 1u : 0u;
-      ib += pa ? 0u : 1u;
-      const K nx = SK[pa ? ia : ib];
-      const typename KeyTraits<KT>::O onx = T::ord(nx);
-      ka = pa ? nx : ka;
-      oa = pa ? onx : oa;
-      kb = pa ? kb : nx;
-      ob = pa ? ob : onx;
-    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < KQ; ++q)
+      if (d + q < plen) { IKs[q0 + q] = rk[q]; IIs[q0 + q] = (uint16_t)ri[q]; }
   }
 }
 
@@ -606,12 +625,13 @@ __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IK
   if (!(start < hi && start + (uint32_t)KQ > lo)) return;
   K* dk = par ? k1 : k0;
   uint32_t* dv = par ? v1 : v0;
+  const uint32_t n01p = m4_n01p<KQ>(n01);  // P23 starts here (step A layout)
   const uint32_t nA = n01, nB = T4 - n01;
   const uint32_t qs = max(start, lo);
   const uint32_t d = qs - lo;
-  const uint32_t l = corank<KT>(IKs, nA, IKs + n01, nB, d);
-  uint32_t ia = l, ib = n01 + d - l;
-  const uint32_t ea = n01, eb = T4;
+  const uint32_t l = corank<KT>(IKs, nA, IKs + n01p, nB, d);
+  uint32_t ia = l, ib = n01p + d - l;
+  const uint32_t ea = n01, eb = n01p + nB;
   K ka = IKs[ia], kb = IKs[ib];
     typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load  // reads past T4 stay inside the intermediate (slack)
   K rk[(uint32_t)KQ];
@@ -641,7 +661,10 @@ __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IK
   } else {
     if (HV) {
 #pragma unroll
-      for (int q = 0; q < KQ; ++q) rv[q] = SV[IIs[min(ri[q], T4 - 1)]];
+      for (int q = 0; q < KQ; ++q) {  // outputs past the tile read a valid slot (never the pad)
+        const bool ok = ri[q] < ea || (ri[q] >= n01p && ri[q] < eb);
+        rv[q] = SV[IIs[ok ? ri[q] : (nB ? eb - 1u : ea - 1u)]];
+      }
     }
 #pragma unroll
     for (int q = 0; q < KQ; ++q) {
@@ -741,42 +764,58 @@ __device__ __forceinline__ void merge4_direct(const typename KeyTraits<KT>::K* S
 // the free stage (full / empty mbarrier pairs), so no consumer ever waits on
 // a descriptor load.
 template <int KT, bool HV, int KQ>
-__global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
+__global__ void __launch_bounds__(m4_threads<KQ>(), 2) k4_merge_level(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
     const TileDesc4* __restrict__ tiles, const NodeRuns* __restrict__ nr,
-    const uint32_t* __restrict__ level_tile, int p, uint32_t cap) {
+    const uint32_t* __restrict__ level_tile, int p) {
   using K = typename KeyTraits<KT>::K;
   using SM = Merge4Smem<KT, HV>;
-  constexpr uint32_t NT = 4096 / KQ;  // consumer threads
+  constexpr uint32_t NT = m4_consumers<KQ>();  // consumer threads
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 2;
   Merge4Hdr* hdr = reinterpret_cast<Merge4Hdr*>(smem + 64);
   K* IKs = reinterpret_cast<K*>(smem + SM::HDR + SM::NSTG * SM::STAGE);
   uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK);
+  uint64_t* ready = full + 4;  // step A boundaries written (producer warp, 32 arrivals)
   const uint32_t count = level_tile[p + 1] - level_tile[p];
-  if (blockIdx.x >= count || count > cap) return;  // count > cap: flagged by k4_desc
+  if (blockIdx.x >= count) return;
   const uint32_t tid = threadIdx.x;
   if (tid == 0) {
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
     mbar_init(&empty[0], NT / 32);
     mbar_init(&empty[1], NT / 32);
+    mbar_init(&ready[0], 32);
+    mbar_init(&ready[1], 32);
     fence_mbar_init();
   }
   __syncthreads();
   if (tid >= NT) {  // producer warp
-    if (tid == NT) {
-      uint32_t it = 0;
-      for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
-        const uint32_t s = it % SM::NSTG;
+    // lane 0 issues the tile's bulk copies into the free stage; once they
+    // have landed, lanes 0..15 compute the 16 step A warp boundaries
+    // (consumers then search within a 256-wide bracket instead of the tile)
+    const uint32_t plane = tid - NT;
+    uint32_t it = 0;
+    for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
+      const uint32_t s = it % SM::NSTG;
+      if (plane == 0) {
         if (it >= SM::NSTG) mbar_wait_backoff(&empty[s], ((it / SM::NSTG) - 1) & 1u);
         const TileDesc4 d = tiles[tau];
         TileDesc4 dn;
         const bool same = tau + 1 < count && (dn = tiles[tau + 1], dn.x == d.x);
         merge4_issue<KT, HV>(d, same ? &dn : nullptr, nr[d.x], s, smem, full, hdr, k0, v0, k1, v1);
       }
+      mbar_wait_backoff(&full[s], (it / SM::NSTG) & 1u);
+      const Merge4Hdr& h = hdr[s];
+      if (h.mode == 0u && plane < (uint32_t)M4_WARPS) {
+        const uint32_t q = plane * 32u * (uint32_t)KQ;
+        if (q < m4_n01p<KQ>(h.n[0] + h.n[1]) + h.n[2] + h.n[3])
+          hdr[s].bnd[plane] =
+              (uint16_t)merge4_boundary<KT, KQ>(reinterpret_cast<const K*>(smem + SM::HDR + s * SM::STAGE), h, q);
+      }
+      mbar_arrive(&ready[s]);
     }
     return;
   }
@@ -784,7 +823,7 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
   uint32_t it = 0;
   for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
     const uint32_t s = it % SM::NSTG;
-    mbar_wait(&full[s], (it / SM::NSTG) & 1u);
+    mbar_wait(&ready[s], (it / SM::NSTG) & 1u);
     const Merge4Hdr* hp = hdr + s;
     const unsigned char* st = smem + SM::HDR + s * SM::STAGE;
     const K* SK = reinterpret_cast<const K*>(st);
@@ -806,7 +845,7 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k4_merge_level(
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     } else {
-      merge4_stepA<KT, KQ>(SK, hp, n01, T4, IKs, IIs);
+      merge4_stepA<KT, KQ>(SK, hp, IKs, IIs, true);
       named_bar_sync(1, NT);
       merge4_stepB<KT, HV, KQ>(IKs, IIs, SV, lo, hi, par, n01, T4, k0, v0, k1, v1);
       __syncwarp();
@@ -942,12 +981,12 @@ __device__ __forceinline__ void pull_issue(const TileDesc4& d, const TileDesc4* 
 // Same consumer side as k4_merge_level; the producer stages the four pieces'
 // windows from their own addresses.  Output keys / values at [0, N).
 template <int KT, bool HV, int KQ>
-__global__ void __launch_bounds__(4096 / KQ + 32, 2) k_pull_merge(PullSrc<KT> S, typename KeyTraits<KT>::K* __restrict__ ok,
+__global__ void __launch_bounds__(m4_threads<KQ>(), 2) k_pull_merge(PullSrc<KT> S, typename KeyTraits<KT>::K* __restrict__ ok,
                                                                    uint32_t* __restrict__ ov,
                                                                    const TileDesc4* __restrict__ tiles, uint32_t count) {
   using K = typename KeyTraits<KT>::K;
   using SM = Merge4Smem<KT, HV>;
-  constexpr uint32_t NT = 4096 / KQ;
+  constexpr uint32_t NT = m4_consumers<KQ>();
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 2;
@@ -1000,7 +1039,7 @@ __global__ void __launch_bounds__(4096 / KQ + 32, 2) k_pull_merge(PullSrc<KT> S,
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     } else {
-      merge4_stepA<KT, KQ>(SK, hp, n01, T4, IKs, IIs);
+      merge4_stepA<KT, KQ>(SK, hp, IKs, IIs, false);
       named_bar_sync(1, NT);
       merge4_stepB<KT, HV, KQ>(IKs, IIs, SV, lo, hi, 0u, n01, T4, ok, ov, ok, ov);
       __syncwarp();

@@ -378,10 +378,17 @@ __global__ void k_zero_tail(uint32_t* __restrict__ arr, const uint32_t* scalars,
     arr[x] = 0;
 }
 
-// Every non-fused node must lie on a launched level (p <= p_hi).
-__global__ void k_check_levels(const uint32_t* level_cnt, int p_hi, uint32_t* scalars) {
+// Every non-fused node must lie on a launched level (p <= p_hi), and (4-way
+// schedule) no level may have had more tiles than the descriptor array holds
+// (the bound in carve() is exact; checked after the fact so the hot kernels
+// carry no extra test).
+__global__ void k_check_levels(const uint32_t* level_cnt, int p_hi, uint32_t* scalars,
+                               const uint32_t* level_tile, uint32_t tile_cap) {
   for (int p = p_hi + 1 + threadIdx.x; p < LEVEL_SLOTS; p += blockDim.x)
     if (level_cnt[p]) scalars[SC_ERROR] = 1;
+  if (level_tile)
+    for (int p = 1 + threadIdx.x; p <= p_hi; p += blockDim.x)
+      if (level_tile[p + 1] - level_tile[p] > tile_cap) scalars[SC_ERROR] = 2;
 }
 
 // Internal-consistency guard of a sort called without h_stats (nothing is
