@@ -637,7 +637,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       VMPS_CK(cudaFuncSetAttribute(k4_merge_level<KT, HV, M4_KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)SM4::BYTES));
       int occ = 0;
-      VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_merge_level<KT, HV, M4_KQ>, m4_threads<M4_KQ>(),
+      VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k4_merge_level<KT, HV, M4_KQ>, M4_THREADS,
                                                             SM4::BYTES));
       occ4[KT][HV] = occ > 0 ? occ : 1;
     }
@@ -659,7 +659,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
         LAUNCH(k4_desc_warp<KT>, (32u * std::min<uint32_t>(w.part_cap, desc_warp_max) + 255) / 256, 256, 0, s, k0, k1,
                nr, w.ltiles, w.level_start, w.level_tile, p, w.tout, t4, desc_warp_max);
       int e1 = prof_event(s);
-      LAUNCH((k4_merge_level<KT, HV, M4_KQ>), gm4, m4_threads<M4_KQ>(), SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.level_tile, p);
+      LAUNCH((k4_merge_level<KT, HV, M4_KQ>), gm4, M4_THREADS, SM4::BYTES, s, k0, v0, k1, v1, t4, nr, w.level_tile, p);
       ++g_nl_merge;
       int e2 = prof_event(s);
       if (g_prof && e0 >= 0 && e2 >= 0 && g_prof_nm < 128) {
@@ -1403,7 +1403,7 @@ static vmps_status_t pull_pass(const void* const* kp, const uint32_t* const* vp,
     VMPS_CK(cudaFuncSetAttribute(k_pull_merge<KT, HV, M4_KQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)SM4::BYTES));
     int o = 0;
-    VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_pull_merge<KT, HV, M4_KQ>, m4_threads<M4_KQ>(),
+    VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_pull_merge<KT, HV, M4_KQ>, M4_THREADS,
                                                           SM4::BYTES));
     occ[KT][HV] = o > 0 ? o : 1;
   }
@@ -1411,7 +1411,7 @@ static vmps_status_t pull_pass(const void* const* kp, const uint32_t* const* vp,
   const uint32_t nchunks = (ntiles + DESC4_CHUNK - 1) / DESC4_CHUNK;
   LAUNCH(k_pull_desc<KT>, (nchunks + 255) / 256, 256, 0, s, S, ntiles, tiles);
   LAUNCH((k_pull_merge<KT, HV, M4_KQ>), (unsigned)std::min<uint32_t>(ntiles, nsm() * occ[KT][HV]),
-         m4_threads<M4_KQ>(), SM4::BYTES, s, S, (K*)ok, ov, tiles, ntiles);
+         M4_THREADS, SM4::BYTES, s, S, (K*)ok, ov, tiles, ntiles);
   return launch_check();
 }
 

@@ -30,7 +30,20 @@ struct NodeRuns {
   uint32_t pad[2];
 };
 
-constexpr int M4_KQ = 8;  // outputs per consumer thread of the 4-way merge (256 + 32 threads)
+// Threads of the 4-way merge.  Steps A and B give each thread KA = 9
+// consecutive outputs: an odd chunk length makes the threads' co-rank probes
+// and merge heads (about KA t / 2 apart) and their intermediate / staging
+// writes (KA t apart) fall into distinct shared-memory banks -- with 8 they
+// sat 4 and 8 words apart, 4- and 8-way conflicts on the pipe that bounds
+// this kernel (l1tex data-pipe wavefronts ~88% busy, profiles/).  Copy and
+// two-run tiles keep 8-output chunks stored straight to global memory (they
+// are output-aligned, 128-bit stores).  17 consumer warps cover both:
+// 4096 / 8 = 512 chunks, and up to ceil(n01 / 9) + ceil(n23 / 9) <= 457.
+constexpr int M4_KQ = 8;                       // copy / two-run tiles
+constexpr uint32_t M4_KA = 9;                  // steps A and B
+constexpr uint32_t M4_NT = 4096 / M4_KQ + 32;  // consumer threads (17 warps)
+constexpr uint32_t M4_THREADS = M4_NT + 32;    // + the producer warp
+static_assert((4096 + M4_KA - 1) / M4_KA + 1 <= M4_NT, "step A chunks");
 
 struct TileDesc4 {
   uint32_t x;     // node (local index in the level)
@@ -403,24 +416,18 @@ struct Merge4Smem {
   static constexpr uint32_t NSTG = (sizeof(K) == 8 && HV) ? VMPS_U64_STAGES : 2u;
   // the barrier area holds two full / empty pairs and the header area two Merge4Hdr
   static_assert(NSTG >= 1 && NSTG <= 2, "merge4: at most two pipeline stages");
-  // intermediate: P01 at [0, n01), P23 at [round8(n01), round8(n01) + n23)
-  // (<= 4096 + 7 positions) plus read-ahead slack
-  static constexpr uint32_t IPOS = 4096 + 32;
+  // intermediate: P01 at [0, n01), P23 at [n01p, n01p + n23), n01p = n01
+  // rounded up to a multiple of KA (<= 4096 + 8 positions), + read-ahead slack
+  static constexpr uint32_t IPOS = 4096 + 48;
   static constexpr uint32_t IK = IPOS * sizeof(K);  // intermediate keys
   static constexpr uint32_t II = IPOS * 2;          // intermediate value indices (u16)
-  static constexpr uint32_t BYTES = HDR + NSTG * STAGE + IK + II;
+  // step B output staging: keys go to the tile's stage key area (free once
+  // step A is done), values to OV; both then leave by TMA bulk stores
+  static constexpr uint32_t OV = HV ? 4096 * 4 + 64 : 0;
+  static constexpr uint32_t BYTES = HDR + NSTG * STAGE + IK + II + OV;
 };
 
-// Consumer threads of a 4096-output tile: 4096 / KQ for the outputs plus one
-// warp, because step A lays P23 out from the first multiple of KQ at or
-// after n01, so that no thread's chunk straddles P01 and P23 (a straddling
-// thread ran two searches and two serial loops and held the whole CTA at the
-// step A barrier); the two parts then need up to 4096 / KQ + 1 chunks.
-template <int KQ>
-__host__ __device__ constexpr uint32_t m4_consumers() { return 4096u / KQ + 32u; }
-template <int KQ>
-__host__ __device__ constexpr uint32_t m4_threads() { return m4_consumers<KQ>() + 32u; }
-constexpr int M4_WARPS = 4096 / (32 * M4_KQ) + 1;  // consumer warps of a tile (17)
+constexpr int M4_WARPS = M4_NT / 32;  // consumer warps of a tile (17)
 struct Merge4Hdr {
   uint32_t kb[4], n[4];  // key element offset / count of each window in the stage
   uint32_t vb[4];        // value element offset of each window
@@ -517,34 +524,44 @@ __device__ __forceinline__ void merge4_issue(const TileDesc4& d, const TileDesc4
 // diagonal 0 and needs no search).
 // Step A layout: P01 = W0 (+) W1 at intermediate positions [0, n01), P23 =
 // W2 (+) W3 at [n01p, n01p + n23) with n01p = n01 rounded up to a multiple of
-// KQ, so every thread's KQ-chunk lies in one of the two merges.
-template <int KQ>
-__device__ __forceinline__ uint32_t m4_n01p(uint32_t n01) { return (n01 + (uint32_t)KQ - 1) & ~((uint32_t)KQ - 1); }
+// KA, so every thread's KA-chunk lies in one of the two merges.
+__device__ __forceinline__ uint32_t m4_n01p(uint32_t n01) { return (n01 + M4_KA - 1u) / M4_KA * M4_KA; }
 
 // The co-rank of intermediate position q (< n01p + n23) within its 2-way
-// merge; one lane of the producer warp per consumer warp boundary q = 256 w.
-template <int KT, int KQ>
+// merge; one lane of the producer warp per consumer warp boundary q = 32 KA w.
+template <int KT>
 __device__ __forceinline__ uint32_t merge4_boundary(const typename KeyTraits<KT>::K* SK, const Merge4Hdr& h,
                                                     uint32_t q) {
-  const uint32_t n01 = h.n[0] + h.n[1], n01p = m4_n01p<KQ>(n01);
+  const uint32_t n01p = m4_n01p(h.n[0] + h.n[1]);
   const uint32_t wa = q < n01p ? 0u : 2u;
   return corank<KT>(SK + h.kb[wa], h.n[wa], SK + h.kb[wa + 1], h.n[wa + 1], q - (q < n01p ? 0u : n01p));
 }
 
+// Producer warp, once stage s has landed: the step A warp boundaries of a
+// general tile (lane w < M4_WARPS computes boundary w).
+template <int KT>
+__device__ __forceinline__ void merge4_bnds(const typename KeyTraits<KT>::K* SK, Merge4Hdr* hs, uint32_t lane) {
+  const Merge4Hdr& h = *hs;
+  if (h.mode != 0u || lane >= (uint32_t)M4_WARPS) return;
+  const uint32_t q = lane * 32u * M4_KA;
+  if (q < m4_n01p(h.n[0] + h.n[1]) + h.n[2] + h.n[3]) hs->bnd[lane] = (uint16_t)merge4_boundary<KT>(SK, h, q);
+}
+
 // Step A: P01 and P23 into the intermediate (keys + the stage index of each
-// value), KQ outputs per thread by the unrolled branch-free merge over
+// value), KA outputs per thread by the unrolled branch-free merge over
 // absolute stage indices (a read past a window stays inside the stage:
-// windows are padded).  A part's last chunk runs all KQ steps and stores only
+// windows are padded).  A part's last chunk runs all KA steps and stores only
 // its in-range outputs.  With have_bnd, the co-rank search is bracketed by the
 // producer's co-ranks at this warp's boundaries.
-template <int KT, int KQ>
+template <int KT>
 __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK, const Merge4Hdr* hp,
                                              typename KeyTraits<KT>::K* IKs, uint16_t* IIs, bool have_bnd) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
+  constexpr uint32_t KQ = M4_KA;
   const uint32_t n01 = hp->n[0] + hp->n[1], n23 = hp->n[2] + hp->n[3];
-  const uint32_t n01p = m4_n01p<KQ>(n01);
-  const uint32_t q0 = threadIdx.x * (uint32_t)KQ;
+  const uint32_t n01p = m4_n01p(n01);
+  const uint32_t q0 = threadIdx.x * KQ;
   const bool part0 = q0 < n01p;
   const uint32_t base = part0 ? 0u : n01p, plen = part0 ? n01 : n23;
   const uint32_t d = q0 - base;
@@ -557,7 +574,7 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
   if (have_bnd) {
     // c(x1) = c1 <= c(d) <= c(x2) = c2, c(d) - c1 <= d - x1, c2 - c(d) <= x2 - d
     const uint32_t w = threadIdx.x >> 5;
-    const uint32_t ws = w * 32u * (uint32_t)KQ, we = ws + 32u * (uint32_t)KQ;
+    const uint32_t ws = w * 32u * KQ, we = ws + 32u * KQ;
     uint32_t x1 = 0u, c1 = 0u, x2 = nA + nB, c2 = nA;
     if (ws >= base) { x1 = ws - base; c1 = hp->bnd[w]; }
     if (we < base + plen) { x2 = we - base; c2 = hp->bnd[w + 1]; }
@@ -572,7 +589,7 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
   K rk[KQ];
   uint32_t ri[KQ];
 #pragma unroll
-  for (int q = 0; q < KQ; ++q) {
+  for (int q = 0; q < (int)KQ; ++q) {
     const bool pa = ib >= eb || (ia < ea && oa <= ob);
     rk[q] = pa ? ka : kb;
     ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
@@ -585,16 +602,12 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
     kb = pa ? kb : nx;
     ob = pa ? ob : onx;
   }
-  if (d + (uint32_t)KQ <= plen) {
+  if (d + KQ <= plen) {
 #pragma unroll
-    for (int q = 0; q < KQ; ++q) IKs[q0 + q] = rk[q];
-#pragma unroll
-    for (int q = 0; q < KQ; q += 8)
-      *reinterpret_cast<uint4*>(IIs + q0 + q) = make_uint4(ri[q] | (ri[q + 1] << 16), ri[q + 2] | (ri[q + 3] << 16),
-                                                           ri[q + 4] | (ri[q + 5] << 16), ri[q + 6] | (ri[q + 7] << 16));
+    for (int q = 0; q < (int)KQ; ++q) { IKs[q0 + q] = rk[q]; IIs[q0 + q] = (uint16_t)ri[q]; }
   } else {
 #pragma unroll
-    for (int q = 0; q < KQ; ++q)
+    for (int q = 0; q < (int)KQ; ++q)
       if (d + q < plen) { IKs[q0 + q] = rk[q]; IIs[q0 + q] = (uint16_t)ri[q]; }
   }
 }
@@ -611,66 +624,91 @@ __device__ __forceinline__ void store_chunk_g(uint64_t* dst, const uint64_t (&r)
     st_v4(dst + q, (uint32_t)r[q], (uint32_t)(r[q] >> 32), (uint32_t)r[q + 1], (uint32_t)(r[q + 1] >> 32));
 }
 
-// Step B: output = P01 (+) P23 for 8-aligned chunks of global positions;
-// an edge chunk (partly outside [lo, hi)) runs the same branch-free merge
-// from its first in-range output and predicates its stores.
-template <int KT, bool HV, int KQ>
+// Elements per 16 bytes (a bulk copy's alignment unit).
+template <typename X>
+__host__ __device__ constexpr uint32_t vec16() { return 16u / (uint32_t)sizeof(X); }
+
+// Step B: the tile's outputs = P01 (+) P23, KA consecutive outputs per thread
+// (tile-relative positions d = KA t), written to shared staging at index
+// (lo mod vec16) + d -- the stage key area for keys, OV for values -- so that
+// the 16-byte aligned part of [lo, hi) is one bulk store per array.
+template <int KT, bool HV>
 __device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IKs, const uint16_t* IIs,
-                                             const uint32_t* SV, uint32_t lo, uint32_t hi, uint32_t par,
-                                             uint32_t n01, uint32_t T4, typename KeyTraits<KT>::K* k0,
-                                             uint32_t* v0, typename KeyTraits<KT>::K* k1, uint32_t* v1) {
+                                             const uint32_t* SV, uint32_t lo, uint32_t n01, uint32_t T4,
+                                             typename KeyTraits<KT>::K* OKs, uint32_t* OVs) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
-  const uint32_t start = (lo & ~(uint32_t)((uint32_t)KQ - 1)) + threadIdx.x * (uint32_t)KQ;
-  if (!(start < hi && start + (uint32_t)KQ > lo)) return;
-  K* dk = par ? k1 : k0;
-  uint32_t* dv = par ? v1 : v0;
-  const uint32_t n01p = m4_n01p<KQ>(n01);  // P23 starts here (step A layout)
+  constexpr uint32_t KQ = M4_KA;
+  const uint32_t d = threadIdx.x * KQ;
+  if (d >= T4) return;
+  const uint32_t n01p = m4_n01p(n01);  // P23 starts here (step A layout)
   const uint32_t nA = n01, nB = T4 - n01;
-  const uint32_t qs = max(start, lo);
-  const uint32_t d = qs - lo;
   const uint32_t l = corank<KT>(IKs, nA, IKs + n01p, nB, d);
   uint32_t ia = l, ib = n01p + d - l;
   const uint32_t ea = n01, eb = n01p + nB;
-  K ka = IKs[ia], kb = IKs[ib];
-    typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load  // reads past T4 stay inside the intermediate (slack)
-  K rk[(uint32_t)KQ];
-  uint32_t ri[(uint32_t)KQ];
+  K ka = IKs[ia], kb = IKs[ib];  // reads past the parts stay inside the intermediate (slack)
+  typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);
+  K rk[KQ];
+  uint32_t ri[KQ];
 #pragma unroll
-  for (int q = 0; q < KQ; ++q) {
+  for (int q = 0; q < (int)KQ; ++q) {
     const bool pa = ib >= eb || (ia < ea && oa <= ob);
     rk[q] = pa ? ka : kb;
     ri[q] = pa ? ia : ib;
     ia += pa ? 1u : 0u;
     ib += pa ? 0u : 1u;
     const K nx = IKs[pa ? ia : ib];
-      const typename KeyTraits<KT>::O onx = T::ord(nx);
+    const typename KeyTraits<KT>::O onx = T::ord(nx);
     ka = pa ? nx : ka;
-      oa = pa ? onx : oa;
+    oa = pa ? onx : oa;
     kb = pa ? kb : nx;
-      ob = pa ? ob : onx;
+    ob = pa ? ob : onx;
   }
-  uint32_t rv[(uint32_t)KQ];
-  if (qs == start && start + (uint32_t)KQ <= hi) {
-    if (HV) {
+  K* ok = OKs + (lo & (vec16<K>() - 1u)) + d;
+  uint32_t* ov = OVs + (lo & 3u) + d;
+  if (d + KQ <= T4) {
 #pragma unroll
-      for (int q = 0; q < KQ; ++q) rv[q] = SV[IIs[ri[q]]];
+    for (int q = 0; q < (int)KQ; ++q) {
+      ok[q] = rk[q];
+      if (HV) ov[q] = SV[IIs[ri[q]]];
     }
-    store_chunk_g<KQ>(dk + start, rk);
-    if (HV) store_chunk_g<KQ>(dv + start, rv);
   } else {
-    if (HV) {
 #pragma unroll
-      for (int q = 0; q < KQ; ++q) {  // outputs past the tile read a valid slot (never the pad)
-        const bool ok = ri[q] < ea || (ri[q] >= n01p && ri[q] < eb);
-        rv[q] = SV[IIs[ok ? ri[q] : (nB ? eb - 1u : ea - 1u)]];
+    for (int q = 0; q < (int)KQ; ++q)
+      if (d + q < T4) {
+        ok[q] = rk[q];
+        if (HV) ov[q] = SV[IIs[ri[q]]];
       }
-    }
-#pragma unroll
-    for (int q = 0; q < KQ; ++q) {
-      const uint32_t pos = qs + q;
-      if (pos < hi && pos < start + (uint32_t)KQ) { dk[pos] = rk[q]; if (HV) dv[pos] = rv[q]; }
-    }
+  }
+}
+
+// After step B (all consumers past the barrier): the staged outputs of the
+// tile leave shared memory.  Thread 0 issues one bulk store per array for the
+// 16-byte aligned part of [lo, hi) and waits until they have read shared
+// memory; threads 32.. store the < vec16 ragged elements at either end.
+template <int KT, bool HV>
+__device__ __forceinline__ void merge4_flush(const typename KeyTraits<KT>::K* OKs, const uint32_t* OVs,
+                                             uint32_t lo, uint32_t hi, typename KeyTraits<KT>::K* dk,
+                                             uint32_t* dv) {
+  using K = typename KeyTraits<KT>::K;
+  constexpr uint32_t VK = vec16<K>(), VV = 4u;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t lok = (lo + VK - 1u) & ~(VK - 1u), hik = max(hi & ~(VK - 1u), lok);
+  const uint32_t lov = (lo + VV - 1u) & ~(VV - 1u), hiv = max(hi & ~(VV - 1u), lov);
+  const K* sk = OKs - (lo & ~(VK - 1u));  // sk[g] = output g (shared)
+  const uint32_t* sv = OVs - (lo & ~(VV - 1u));
+  if (tid == 0) {
+    if (hik > lok) bulk_s2g(dk + lok, sk + lok, (hik - lok) * (uint32_t)sizeof(K));
+    if (HV && hiv > lov) bulk_s2g(dv + lov, sv + lov, (hiv - lov) * 4u);
+    bulk_commit();
+  } else if (tid >= 32u && tid < 32u + 2u * VK) {  // ragged key ends: [lo, lok) and [hik, hi)
+    const uint32_t j = tid - 32u;
+    const uint32_t g = j < VK ? lo + j : hik + (j - VK);
+    if (j < VK ? g < min(lok, hi) : g < hi) dk[g] = sk[g];
+  } else if (HV && tid >= 64u && tid < 64u + 2u * VV) {  // ragged value ends
+    const uint32_t j = tid - 64u;
+    const uint32_t g = j < VV ? lo + j : hiv + (j - VV);
+    if (j < VV ? g < min(lov, hi) : g < hi) dv[g] = sv[g];
   }
 }
 
@@ -759,26 +797,72 @@ __device__ __forceinline__ void merge4_direct(const typename KeyTraits<KT>::K* S
   }
 }
 
-// The fused merge: persistent CTAs; 16 consumer warps merge, one producer
+// One tile on the consumer side (17 warps), shared by the level merge and
+// the pull-merge.  Copy tiles and two-run tiles store 8-output chunks
+// straight to global memory; general tiles run steps A and B through the
+// intermediate and leave by bulk stores.  Every consumer warp arrives once on
+// empty[s] when it no longer needs stage s (warp 0 only after the bulk
+// stores have read the stage's key area).
+template <int KT, bool HV>
+__device__ __forceinline__ void merge4_tile(const Merge4Hdr* hp, unsigned char* st, typename KeyTraits<KT>::K* IKs,
+                                            uint16_t* IIs, uint32_t* OVs, uint64_t* empty_s, bool have_bnd,
+                                            typename KeyTraits<KT>::K* k0, uint32_t* v0,
+                                            typename KeyTraits<KT>::K* k1, uint32_t* v1) {
+  using K = typename KeyTraits<KT>::K;
+  using SM = Merge4Smem<KT, HV>;
+  const uint32_t lane = threadIdx.x & 31u;
+  K* SK = reinterpret_cast<K*>(st);
+  const uint32_t* SV = reinterpret_cast<const uint32_t*>(st + SM::KB);
+  const uint32_t lo = hp->lo, hi = hp->hi, par = hp->par;
+  const uint32_t mode = hp->mode;
+  if (mode >= 2) {
+    // run-skip tile: every output comes from one run, so
+    // the tile is a compare-free copy of that window
+    const uint32_t wsrc = mode - 2;
+    merge4_copy<KT, HV, M4_KQ>(SK, SV, hp->kb[wsrc], hp->vb[wsrc], lo, hi, par, k0, v0, k1, v1);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_s);
+  } else if (mode == 1) {
+    // both children are single runs (leaves / units): one 2-way merge
+    // straight from the stage, no intermediate
+    merge4_direct<KT, HV, M4_KQ>(SK, SV, hp, lo, hi, par, k0, v0, k1, v1);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_s);
+  } else {
+    const uint32_t n01 = hp->n[0] + hp->n[1], T4 = hi - lo;
+    merge4_stepA<KT>(SK, hp, IKs, IIs, have_bnd);
+    named_bar_sync(1, M4_NT);  // the intermediate is complete; the stage keys are dead
+    merge4_stepB<KT, HV>(IKs, IIs, SV, lo, n01, T4, SK, OVs);
+    fence_proxy_async_smem();  // staged outputs -> visible to the bulk stores
+    named_bar_sync(1, M4_NT);  // staging complete; the intermediate is free for the next tile
+    merge4_flush<KT, HV>(SK, OVs, lo, hi, par ? k1 : k0, par ? v1 : v0);
+    if (threadIdx.x == 0) bulk_wait_read0();  // the stage / OV may be overwritten from here on
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_s);
+  }
+}
+
+// The fused merge: persistent CTAs; 17 consumer warps merge, one producer
 // warp loads descriptors and issues the bulk copies of the next tile into
-// the free stage (full / empty mbarrier pairs), so no consumer ever waits on
-// a descriptor load.
+// the free stage (full / empty mbarrier pairs), then computes the step A
+// warp boundaries of that tile once it has landed (ready barrier).
 template <int KT, bool HV, int KQ>
-__global__ void __launch_bounds__(m4_threads<KQ>(), 2) k4_merge_level(
+__global__ void __launch_bounds__(M4_THREADS, 2) k4_merge_level(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
     const TileDesc4* __restrict__ tiles, const NodeRuns* __restrict__ nr,
     const uint32_t* __restrict__ level_tile, int p) {
   using K = typename KeyTraits<KT>::K;
   using SM = Merge4Smem<KT, HV>;
-  constexpr uint32_t NT = m4_consumers<KQ>();  // consumer threads
+  constexpr uint32_t NT = M4_NT;  // consumer threads
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 2;
+  uint64_t* ready = full + 4;  // step A boundaries written (producer warp, 32 arrivals)
   Merge4Hdr* hdr = reinterpret_cast<Merge4Hdr*>(smem + 64);
   K* IKs = reinterpret_cast<K*>(smem + SM::HDR + SM::NSTG * SM::STAGE);
   uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK);
-  uint64_t* ready = full + 4;  // step A boundaries written (producer warp, 32 arrivals)
+  uint32_t* OVs = reinterpret_cast<uint32_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK + SM::II);
   const uint32_t count = level_tile[p + 1] - level_tile[p];
   if (blockIdx.x >= count) return;
   const uint32_t tid = threadIdx.x;
@@ -793,9 +877,6 @@ __global__ void __launch_bounds__(m4_threads<KQ>(), 2) k4_merge_level(
   }
   __syncthreads();
   if (tid >= NT) {  // producer warp
-    // lane 0 issues the tile's bulk copies into the free stage; once they
-    // have landed, lanes 0..15 compute the 16 step A warp boundaries
-    // (consumers then search within a 256-wide bracket instead of the tile)
     const uint32_t plane = tid - NT;
     uint32_t it = 0;
     for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
@@ -808,51 +889,18 @@ __global__ void __launch_bounds__(m4_threads<KQ>(), 2) k4_merge_level(
         merge4_issue<KT, HV>(d, same ? &dn : nullptr, nr[d.x], s, smem, full, hdr, k0, v0, k1, v1);
       }
       mbar_wait_backoff(&full[s], (it / SM::NSTG) & 1u);
-      const Merge4Hdr& h = hdr[s];
-      if (h.mode == 0u && plane < (uint32_t)M4_WARPS) {
-        const uint32_t q = plane * 32u * (uint32_t)KQ;
-        if (q < m4_n01p<KQ>(h.n[0] + h.n[1]) + h.n[2] + h.n[3])
-          hdr[s].bnd[plane] =
-              (uint16_t)merge4_boundary<KT, KQ>(reinterpret_cast<const K*>(smem + SM::HDR + s * SM::STAGE), h, q);
-      }
+      merge4_bnds<KT>(reinterpret_cast<const K*>(smem + SM::HDR + s * SM::STAGE), hdr + s, plane);
       mbar_arrive(&ready[s]);
     }
     return;
   }
-  const uint32_t lane = tid & 31u;
   uint32_t it = 0;
   for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
     const uint32_t s = it % SM::NSTG;
     mbar_wait(&ready[s], (it / SM::NSTG) & 1u);
-    const Merge4Hdr* hp = hdr + s;
-    const unsigned char* st = smem + SM::HDR + s * SM::STAGE;
-    const K* SK = reinterpret_cast<const K*>(st);
-    const uint32_t* SV = reinterpret_cast<const uint32_t*>(st + SM::KB);
-    const uint32_t lo = hp->lo, hi = hp->hi, par = hp->par;
-    const uint32_t n01 = hp->n[0] + hp->n[1], T4 = hi - lo;
-    const uint32_t mode = hp->mode;
-    if (mode >= 2) {
-      // run-skip tile: every output comes from one run, so
-      // the tile is a compare-free copy of that window
-      const uint32_t wsrc = mode - 2;
-      merge4_copy<KT, HV, KQ>(SK, SV, hp->kb[wsrc], hp->vb[wsrc], lo, hi, par, k0, v0, k1, v1);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    } else if (mode == 1) {
-      // both children are single runs (leaves / units): one 2-way merge
-      // straight from the stage, no intermediate
-      merge4_direct<KT, HV, KQ>(SK, SV, hp, lo, hi, par, k0, v0, k1, v1);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    } else {
-      merge4_stepA<KT, KQ>(SK, hp, IKs, IIs, true);
-      named_bar_sync(1, NT);
-      merge4_stepB<KT, HV, KQ>(IKs, IIs, SV, lo, hi, par, n01, T4, k0, v0, k1, v1);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);  // stage s is free once every warp is past step B
-      named_bar_sync(1, NT);        // the intermediate is reused by the next tile
-    }
+    merge4_tile<KT, HV>(hdr + s, smem + SM::HDR + s * SM::STAGE, IKs, IIs, OVs, &empty[s], true, k0, v0, k1, v1);
   }
+  if (tid == 0) bulk_wait0();  // the last bulk stores are complete before the kernel ends
 }
 
 }  // namespace vmps
@@ -981,18 +1029,20 @@ __device__ __forceinline__ void pull_issue(const TileDesc4& d, const TileDesc4* 
 // Same consumer side as k4_merge_level; the producer stages the four pieces'
 // windows from their own addresses.  Output keys / values at [0, N).
 template <int KT, bool HV, int KQ>
-__global__ void __launch_bounds__(m4_threads<KQ>(), 2) k_pull_merge(PullSrc<KT> S, typename KeyTraits<KT>::K* __restrict__ ok,
-                                                                   uint32_t* __restrict__ ov,
-                                                                   const TileDesc4* __restrict__ tiles, uint32_t count) {
+__global__ void __launch_bounds__(M4_THREADS, 2) k_pull_merge(PullSrc<KT> S, typename KeyTraits<KT>::K* __restrict__ ok,
+                                                              uint32_t* __restrict__ ov,
+                                                              const TileDesc4* __restrict__ tiles, uint32_t count) {
   using K = typename KeyTraits<KT>::K;
   using SM = Merge4Smem<KT, HV>;
-  constexpr uint32_t NT = m4_consumers<KQ>();
+  constexpr uint32_t NT = M4_NT;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + 2;
+  uint64_t* ready = full + 4;
   Merge4Hdr* hdr = reinterpret_cast<Merge4Hdr*>(smem + 64);
   K* IKs = reinterpret_cast<K*>(smem + SM::HDR + SM::NSTG * SM::STAGE);
   uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK);
+  uint32_t* OVs = reinterpret_cast<uint32_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK + SM::II);
   if (blockIdx.x >= count) return;
   const uint32_t tid = threadIdx.x;
   if (tid == 0) {
@@ -1000,53 +1050,36 @@ __global__ void __launch_bounds__(m4_threads<KQ>(), 2) k_pull_merge(PullSrc<KT> 
     mbar_init(&full[1], 1);
     mbar_init(&empty[0], NT / 32);
     mbar_init(&empty[1], NT / 32);
+    mbar_init(&ready[0], 32);
+    mbar_init(&ready[1], 32);
     fence_mbar_init();
   }
   __syncthreads();
   if (tid >= NT) {  // producer warp
-    if (tid == NT) {
-      uint32_t it = 0;
-      for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
-        const uint32_t s = it % SM::NSTG;
+    const uint32_t plane = tid - NT;
+    uint32_t it = 0;
+    for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
+      const uint32_t s = it % SM::NSTG;
+      if (plane == 0) {
         if (it >= SM::NSTG) mbar_wait_backoff(&empty[s], ((it / SM::NSTG) - 1) & 1u);
         const TileDesc4 d = tiles[tau];
         TileDesc4 dn;
         const bool more = tau + 1 < count && (dn = tiles[tau + 1], true);
         pull_issue<KT, HV>(d, more ? &dn : nullptr, S, s, smem, full, hdr);
       }
+      mbar_wait_backoff(&full[s], (it / SM::NSTG) & 1u);
+      merge4_bnds<KT>(reinterpret_cast<const K*>(smem + SM::HDR + s * SM::STAGE), hdr + s, plane);
+      mbar_arrive(&ready[s]);
     }
     return;
   }
-  const uint32_t lane = tid & 31u;
   uint32_t it = 0;
   for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
     const uint32_t s = it % SM::NSTG;
-    mbar_wait(&full[s], (it / SM::NSTG) & 1u);
-    const Merge4Hdr* hp = hdr + s;
-    const unsigned char* st = smem + SM::HDR + s * SM::STAGE;
-    const K* SK = reinterpret_cast<const K*>(st);
-    const uint32_t* SV = reinterpret_cast<const uint32_t*>(st + SM::KB);
-    const uint32_t lo = hp->lo, hi = hp->hi;
-    const uint32_t n01 = hp->n[0] + hp->n[1], T4 = hi - lo;
-    const uint32_t mode = hp->mode;
-    if (mode >= 2) {
-      const uint32_t wsrc = mode - 2;
-      merge4_copy<KT, HV, KQ>(SK, SV, hp->kb[wsrc], hp->vb[wsrc], lo, hi, 0u, ok, ov, ok, ov);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    } else if (mode == 1) {
-      merge4_direct<KT, HV, KQ>(SK, SV, hp, lo, hi, 0u, ok, ov, ok, ov);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    } else {
-      merge4_stepA<KT, KQ>(SK, hp, IKs, IIs, false);
-      named_bar_sync(1, NT);
-      merge4_stepB<KT, HV, KQ>(IKs, IIs, SV, lo, hi, 0u, n01, T4, ok, ov, ok, ov);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      named_bar_sync(1, NT);
-    }
+    mbar_wait(&ready[s], (it / SM::NSTG) & 1u);
+    merge4_tile<KT, HV>(hdr + s, smem + SM::HDR + s * SM::STAGE, IKs, IIs, OVs, &empty[s], true, ok, ov, ok, ov);
   }
+  if (tid == 0) bulk_wait0();
 }
 
 }  // namespace vmps
