@@ -1,24 +1,32 @@
 #!/usr/bin/env python
 """Benchmark of the B200 Virtual-Memory Powersort hot path (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 5|4|3|2|1]
 
 One step = one stable sort of one synthetic batch: the whole hot path (run
 detection, node powers, merge tree + schedule, leaf engine, every level
-merge) on cfg5 -- n = 2^30 u32 keys + u32 payload per GPU.
+merge) on BASELINE.json's configuration -- by default cfg5, n = 2^30 u32 keys
++ u32 payload per GPU (weak scaling); cfg3 / cfg4 are the
+strong-scaling configs (the total n is split over the GPUs).  With N > 1 each
+rank sorts its contiguous shard and the library's native protocol (exact
+splitters, NCCL exchange, stable merge; csrc/comm.cu) makes the result the
+globally stable sort of the concatenation.
+
 Timing: CUDA events on the sorting stream around each sort, W warm-up steps,
 K timed steps bracketed by barrier + synchronize, max over ranks.  Between
-steps the input is restored by an untimed device copy from a pristine
-buffer (8 GiB, which also flushes the 126 MB L2).  Prints ONE JSON line.
+steps the input is restored by an untimed device copy from a pristine buffer
+(8 GiB at cfg5, which also flushes the 126 MB L2).  Rank 0 prints ONE JSON
+line.  `--gpus N` without a torchrun environment launches the N ranks itself.
 
 --impl reference times the CPU oracle (oracle/, plain single-threaded C) on
-a bounded cfg5-shaped sample per step, on the host, rank 0 only.
+a bounded sample of the same workload per step, on the host, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -30,9 +38,18 @@ sys.path.insert(0, ROOT)
 
 METRIC = "sorted keys/sec (Gkeys/s) at 1/2/4/8 B200 and % of HBM merge-tree roofline"
 UNIT = "Gkeys/s"
-WORKLOAD = ("cfg5: n=2^30 u32 keys + u32 payload (= index) per GPU; segments 1+Geom0(1/4096), "
-            "50% i.i.d. uniform unsorted / 50% sorted ascending, 5% of those reversed; "
-            "unbounded scratch")
+WORKLOADS = {
+    5: ("cfg5: n=2^30 u32 keys + u32 payload (= global index mod 2^32) per GPU; segments 1+Geom0(1/4096), "
+        "50% i.i.d. uniform unsorted / 50% sorted ascending, 5% of those reversed; unbounded scratch"),
+    4: ("cfg4: n=2^28 f32 keys in total, no payload; 'Timsort-drag' run lengths (reading R13), "
+        "values normal(0,1) with +-0.0; unbounded scratch"),
+    3: ("cfg3: n=2^26 u64 keys in total (values 0..15) + u32 payload (= index); runs U[1, 2 sqrt n], "
+        "10% reversed (plateaus); unbounded scratch"),
+    2: "cfg2: n=2^24 u32 + u32 payload (= index); random runs, lengths U[1, 2 sqrt n]; unbounded scratch",
+    1: "cfg1: n=2^20 u32 random permutation of 0..n-1 (seed 1); no payload; unbounded scratch",
+}
+DEFAULT_LOG2N = {5: 30, 4: 28, 3: 26, 2: 24, 1: 20}
+STRONG = {3, 4}  # BASELINE.json: cfg3 at 1/2 GPUs, cfg4 at 1/2/4 GPUs (fixed total n)
 
 
 def parse():
@@ -41,7 +58,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--log2n", type=int, default=30, help="per-GPU n = 2^log2n (default: cfg5's 2^30)")
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--log2n", type=int, default=0,
+                    help="n = 2^log2n (per GPU for cfg5, total for the others); default: the config's")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-log2", type=int, default=25)
@@ -53,10 +72,10 @@ def parse():
     ap.add_argument("--fuse-z", type=int, default=0, help="experimental: fused-subtree limit Z")
     ap.add_argument("--pull-dist", action="store_true",
                     help="N>1: pull-merge the co-ranked pieces from peer memory (dist.sort_dist_pull)")
-    ap.add_argument("--native-dist", action="store_true",
-                    help="N>1: the library's own NCCL protocol (vmps_sort_pairs_dist) instead of dist.py")
     ap.add_argument("--bounded-reps", type=int, default=2,
                     help="timed sorts of the scratch-bounded mode (cap 4 sqrt(n log2 n)); 0 = skip")
+    ap.add_argument("--launcher-selftest", action="store_true",
+                    help="CPU check of the N-rank launcher: every rank joins a gloo group; rank 0 prints n_gpus")
     return ap.parse_args()
 
 
@@ -69,14 +88,15 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons of the GPUs in use, sampled during
+    the timed region."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, dev_index: int):
-        self.dev = dev_index
+    def __init__(self, devs):
+        self.devs = ",".join(str(d) for d in devs)
         self.proc = None
         self.lines = []
         self.t = None
@@ -84,7 +104,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", "-i", self.devs, f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
@@ -121,7 +141,7 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "gpus": self.devs}
 
 
 def cpu_info():
@@ -136,12 +156,20 @@ def cpu_info():
     return model, os.cpu_count()
 
 
-def oracle_sample_rate(log2n: int, seed: int = 5):
-    """Oracle (variant A, single thread) on a cfg5-shaped sample -> (Gkeys/s, seconds)."""
-    import oracle
+def gen_host(cfg: int, n: int, seed_shift: int = 0):
+    """The config's generator on the host (numpy), for the oracle samples."""
     import workloads as W
-    k, v = W.cfg5(n=1 << log2n, seed=seed, device="cpu")
-    kn, vn = W.to_numpy(k), W.to_numpy(v)
+    if cfg == 5:
+        k, v = W.cfg5(n=n, seed=5 + seed_shift, device="cpu")
+    else:
+        k, v = W.make(cfg, n=n, seed=cfg + seed_shift, device="cpu")
+    return W.to_numpy(k), (W.to_numpy(v) if v is not None else None)
+
+
+def oracle_sample_rate(cfg: int, log2n: int, seed_shift: int = 0):
+    """Oracle (variant A, single thread) on a sample of the workload -> (Gkeys/s, seconds)."""
+    import oracle
+    kn, vn = gen_host(cfg, 1 << log2n, seed_shift)
     t0 = time.perf_counter()
     oracle.sort(kn, vn, variant=oracle.VARIANT_A)
     dt = time.perf_counter() - t0
@@ -155,31 +183,118 @@ def run_reference(args):
     model, ncpu = cpu_info()
     import oracle
     oracle.build()
+    cfg = args.config
+    log2 = min(args.ref_sample_log2, args.log2n or DEFAULT_LOG2N[cfg])
     for w in range(args.warmup):
-        oracle_sample_rate(min(args.ref_sample_log2, 20), seed=100 + w)
+        oracle_sample_rate(cfg, min(log2, 20), seed_shift=100 + w)
     times = []
     for s in range(args.steps):
-        _, dt = oracle_sample_rate(args.ref_sample_log2, seed=5 + s)
+        _, dt = oracle_sample_rate(cfg, log2, seed_shift=s)
         times.append(dt)
     ms = 1000 * statistics.mean(times)
-    n_s = 1 << args.ref_sample_log2
+    n_s = 1 << log2
     val = n_s / (ms / 1000) / 1e9
-    sample = (f"cfg5-shaped sample of n=2^{args.ref_sample_log2} per step (seeds 5..{4 + args.steps}); "
+    sample = (f"cfg{cfg}-shaped sample of n=2^{log2} per step (seeds shifted 0..{args.steps - 1}); "
               "oracle variant A (copy-merge), single thread")
     out = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-           "config": {"workload": WORKLOAD, "sample_n": n_s},
+           "scaling": "strong" if cfg in STRONG else "weak", "vs_baseline": None,
+           "dtype": {3: "u64", 4: "f32"}.get(cfg, "u32"), "data": "synthetic",
+           "config": {"workload": WORKLOADS[cfg], "sample_n": n_s},
            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
                             "sample": sample, "cpu": model, "host_cores": ncpu},
            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` outside torchrun: launch N ranks of this script (one per GPU,
+    rendezvous on 127.0.0.1) and forward rank 0's output."""
+    import torch
+    ndev = torch.cuda.device_count()
+    if ndev < args.gpus and not args.launcher_selftest:
+        print(f"bench.py: --gpus {args.gpus} but only {ndev} CUDA device(s) visible; refusing to run "
+              f"(the JSON line would report a different n_gpus)", file=sys.stderr)
+        return 2
+    port = _free_port()
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
+
+
+def order_image(t):
+    """Order image of a key tensor as int64 (u32 / f32: exact in 0..2^32; u64:
+    top bit flipped so that signed comparison is the unsigned order)."""
+    import torch
+    if t.dtype == torch.float32:
+        b = t.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        nan = (b & 0x7FFFFFFF) > 0x7F800000
+        img = torch.where((b >> 31) == 1, b ^ 0xFFFFFFFF, b | 0x80000000)
+        return torch.where(nan, torch.full_like(img, 0xFFFFFFFF), img)
+    if t.dtype == torch.uint64:
+        return t.view(torch.int64) ^ torch.iinfo(torch.int64).min
+    return t.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+
+
+def mix_hash(k, v):
+    """Sum over the elements of a 64-bit mix of (key bits, payload) mod 2^64:
+    equal multisets of pairs give equal sums (the permutation check)."""
+    import torch
+    kb = k.view(torch.int64) if k.element_size() == 8 else (k.view(torch.int32).to(torch.int64) & 0xFFFFFFFF)
+    x = kb * -7046029254386353131  # 0x9E3779B97F4A7C15
+    if v is not None:
+        x = x ^ ((v.view(torch.int32).to(torch.int64) & 0xFFFFFFFF) * -4417276706812531889)  # 0xC2B2AE3D27D4EB4F
+    x = x ^ ((x >> 31) & 0x1FFFFFFFF)
+    x = x * -4658895280553007687  # 0xBF58476D1CE4E5B9
+    x = x ^ ((x >> 29) & 0x7FFFFFFFF)
+    return int(x.sum().item())
+
+
+def _sv(t):
+    """Same-size signed view (torch has no comparisons / pinned copies for every unsigned type)."""
+    import torch
+    return t.view(torch.int64 if t.element_size() == 8 else torch.int32)
+
+
+def _pinned_like(t):
+    import torch
+    return torch.empty(t.numel(), dtype=_sv(t).dtype, pin_memory=True).view(t.dtype)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if args.launcher_selftest:  # rendezvous plumbing only (no GPU)
+        import torch
+        import torch.distributed as dist
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        if world > 1:
+            dist.init_process_group("gloo")
+            t = torch.ones(1)
+            dist.all_reduce(t)
+            world = int(t.item())
+            dist.destroy_process_group()
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"launcher_selftest": True, "n_gpus": world}), flush=True)
         return
     import torch
     import torch.distributed as dist
@@ -191,6 +306,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}; refusing to report n_gpus={world}",
+              file=sys.stderr)
+        sys.exit(2)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -205,10 +324,25 @@ def main():
     if args.fuse_z:
         vm.test_set_tiles(args.fuse_z, 0, 0)
 
-    n = 1 << args.log2n
-    keys0, vals0 = W.cfg5(n=n, device=dev, rank=rank)
+    cfg = args.config
+    log2n = args.log2n or DEFAULT_LOG2N[cfg]
+    strong = cfg in STRONG
+    if cfg == 5:  # weak scaling: 2^log2n per GPU, generated by global index
+        n = 1 << log2n
+        keys0, vals0 = W.cfg5(n=n, device=dev, rank=rank)
+        n_total = n * world
+    else:  # the config's total n, split into contiguous shards
+        n_total = 1 << log2n
+        fk, fv = W.make(cfg, n=n_total, device=dev)
+        a, b = rank * n_total // world, (rank + 1) * n_total // world
+        keys0 = fk[a:b].clone()
+        vals0 = fv[a:b].clone() if fv is not None else None
+        del fk, fv
+        n = b - a
+    hv = vals0 is not None
+    w_bytes = keys0.element_size() + (4 if hv else 0)
     keys = torch.empty_like(keys0)
-    vals = torch.empty_like(vals0)
+    vals = torch.empty_like(vals0) if hv else None
     ws = vm.Workspace()
     stream = torch.cuda.current_stream(dev)
 
@@ -216,51 +350,58 @@ def main():
         if world > 1:
             dist.barrier()
 
-    if world > 1 and args.native_dist:
-        # native protocol (csrc/comm.cu): NCCL communicator owned by libvmps
-        uid = [vm.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ncomm = vm.Comm(rank, world, uid[0], local)
+    def restore():
+        _sv(keys).copy_(_sv(keys0))
+        if hv:
+            _sv(vals).copy_(_sv(vals0))
 
-        def do_sort():
-            vm.sort_dist_native_(ncomm, keys, vals, workspace=ws)
-    elif world > 1 and args.pull_dist:
-        # exchange fused with the final merge: pieces read from peer memory
-        from paper_2605_27147_b200.dist import sort_dist_pull
-
-        def do_sort():
-            res = sort_dist_pull(keys, vals)
-            keys.copy_(res.keys)
-            vals.copy_(res.vals)
-    elif world > 1:
-        from paper_2605_27147_b200.dist import sort_dist_
-
-        def do_sort():
-            sort_dist_(keys, vals)
+    ncomm = None
+    if world > 1:
+        from paper_2605_27147_b200 import dist as vdist
+        ncomm = vdist.native_comm(None, dev)
+        if args.pull_dist:
+            def do_sort():
+                res = vdist.sort_dist_pull(keys, vals, comm=ncomm, workspace=ws)
+                _sv(keys).copy_(_sv(res.keys))
+                if hv:
+                    _sv(vals).copy_(_sv(res.vals))
+        else:
+            def do_sort():
+                vdist.sort_dist_(keys, vals, comm=ncomm, workspace=ws)
     else:
         def do_sort():
             vm.sort_(keys, vals, workspace=ws)
 
-    # warm-up (untimed)
-    keys.copy_(keys0)
-    vals.copy_(vals0)
-    stats = vm.sort_(keys, vals, workspace=ws, stats=True)  # local plan statistics
+    # local plan statistics (one untimed local sort)
+    restore()
+    stats = vm.sort_(keys, vals, workspace=ws, stats=True)
+    # the global plan's merge cost (the roofline uses the plan of
+    # the whole array): untimed vmps_merge_plan_dist, merges summed over ranks
+    runs_g, M_g = stats["runs"], stats["merge_cost_M"]
+    if world > 1:
+        from paper_2605_27147_b200 import dist as vdist
+        p = vdist.merge_plan_dist(keys0, n_total=n_total, comm=ncomm)
+        mk = p.merges
+        t = torch.tensor([int(p.run_start.numel()), int((mk[:, 2] - mk[:, 0]).sum().item()) if mk.numel() else 0],
+                         dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        runs_g, M_g = int(t[0].item()), int(t[1].item())
+        del p, mk
     for w in range(max(args.warmup, 1)):
-        keys.copy_(keys0)
-        vals.copy_(vals0)
+        restore()
         do_sort()
     torch.cuda.synchronize()
 
     # timed steps
     vm.profile_enable(True)
-    clocks = ClockSampler(local)
-    step_ms, merge_ms, merge_bytes, phases, launches = [], [], [], [], 0
+    clocks = ClockSampler(range(world) if rank == 0 else [local])
+    step_ms, merge_ms, phases, launches = [], [], [], 0
     barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    if rank == 0:
+        clocks.start()
     for s in range(args.steps):
-        keys.copy_(keys0)
-        vals.copy_(vals0)
+        restore()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -272,95 +413,121 @@ def main():
         launches += pr.get("launches", 0)
         if "merge_ms" in pr:
             merge_ms.append(pr["merge_ms"])
-            merge_bytes.append(pr["merge_bytes"])
             phases.append(pr)
     barrier()
     torch.cuda.synchronize()
-    clk = clocks.stop()
+    clk = clocks.stop() if rank == 0 else None
     vm.profile_enable(False)
 
-    # verify the last output (exact stable-sort properties on device)
-    a = keys.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
-    pv = vals.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
-    ok = bool((a[1:] >= a[:-1]).all())
-    if n * world <= (1 << 32):  # payload = global index is unique: stability is checkable
-        ok = ok and bool(((pv[1:] > pv[:-1]) | (a[1:] != a[:-1])).all())
-    if world > 1:  # shard boundaries: last of rank p <= first of rank p+1
-        ends = torch.stack([a[0], a[-1]])
+    # verify the last output: sorted (across ranks too), the same multiset of
+    # (key, payload) pairs as the input, stable by the global-index payload
+    img = order_image(keys)
+    ok = bool((img[1:] >= img[:-1]).all()) if n > 1 else True
+    eq = img[1:] == img[:-1]
+    stab = "n/a (no payload)"
+    if hv:
+        pv = vals.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        if n_total <= (1 << 32):  # payload = global index is unique: strictly increasing within ties
+            ok = ok and bool(((pv[1:] > pv[:-1]) | ~eq).all())
+            stab = "payload (global index) strictly increasing within equal keys"
+        else:  # index mod 2^32: at most one wrap per tie group
+            desc = (eq & (pv[1:] <= pv[:-1])).to(torch.int64)
+            grp = torch.cumsum((~eq).to(torch.int64), 0)
+            per = torch.zeros(int(grp[-1].item()) + 1, dtype=torch.int64, device=dev).index_add_(0, grp, desc)
+            ok = ok and bool((per <= 1).all())
+            stab = "payload (global index mod 2^32) wraps at most once within equal keys"
+        del pv
+    if world == 1 and hv and n_total <= (1 << 32):  # exact permutation: keys travel with their index
+        ok = ok and bool((_sv(keys) == _sv(keys0)[vals.view(torch.int32).to(torch.int64) & 0xFFFFFFFF]).all())
+    h_in, h_out = mix_hash(keys0, vals0), mix_hash(keys, vals)
+    if world > 1:
+        hs = torch.tensor([h_in, h_out], dtype=torch.int64, device=dev)
+        dist.all_reduce(hs)
+        h_in, h_out = int(hs[0].item()), int(hs[1].item())
+        ends = torch.stack([img[0], img[-1]]) if n else torch.tensor([0, 0], dtype=torch.int64, device=dev)
         allends = [torch.zeros_like(ends) for _ in range(world)]
         dist.all_gather(allends, ends)
         ok = ok and all(int(allends[q][1]) <= int(allends[q + 1][0]) for q in range(world - 1))
-    del a, pv
+        okt = torch.tensor([1 if ok else 0], dtype=torch.int64, device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        ok = bool(okt.item())
+    ok = ok and h_in == h_out
+    del img, eq
 
     t_local = statistics.mean(step_ms)
     t = torch.tensor([t_local], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    value = n * world / (ms / 1000) / 1e9
+    value = n_total / (ms / 1000) / 1e9
 
     peak, peak_src = load_peaks()
+    M_loc, fM_loc, hme = stats["merge_cost_M"], stats["fused_M"], stats["hbm_merge_elems"]
     mm = statistics.mean(merge_ms) if merge_ms else None
-    mb = statistics.mean(merge_bytes) if merge_bytes else None
-    w_bytes = 8
-    M = stats["merge_cost_M"]
     roof = None
-    if mm and mb:
-        achieved = mb / (mm / 1000) / 1e9
-        # DRAM bytes of the same launches from ncu (profiles/, same command at
-        # the same n), per step like `achieved`; null if absent
+    if mm:
+        algo = 2 * w_bytes * (M_loc - fM_loc)       # 2w per element per non-fused tree level
+        phys = 2 * w_bytes * hme                     # bytes the two-levels-per-pass kernel reads + writes
         traffic, traffic_src = None, None
         tp = os.path.join(ROOT, "profiles", "merge_level_traffic.json")
-        if os.path.exists(tp):
+        if os.path.exists(tp) and cfg == 5 and log2n == 30 and not args.one_level:
             try:
                 tj = json.load(open(tp))
-                traffic = tj.get("bytes_per_step")
-                traffic_src = tj.get("source")
+                traffic, traffic_src = tj.get("bytes_per_step"), tj.get("source")
             except Exception:
                 traffic = None
         kname = ("k_merge_level (one tree level per HBM pass; all merge launches of a step)" if args.one_level
                  else "k4_merge_level (two tree levels, up to 4-way merges, per HBM pass; all merge launches "
                       "of a step)")
-        roof = {"bound": "hbm", "kernel": kname,
-                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "traffic_unit": "bytes per step (all level-merge launches)",
+        achieved = algo / (mm / 1000) / 1e9
+        roof = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "traffic_unit": "DRAM bytes per step (all level-merge launches, ncu)",
                 "traffic_source": traffic_src, "peak_source": peak_src,
-                "algorithmic_bytes_per_step": mb, "merge_launches_per_step": phases[-1]["merge_launches"],
-                "kernel_ms_per_step": mm}
-    tree = {"bytes_2wM": 2 * w_bytes * M, "M_over_n": M / n,
-            "t_roof_ms_at_peak": 2 * w_bytes * M / (peak * 1e9) * 1000,
-            "frac_of_roofline": (2 * w_bytes * M / (peak * 1e9) * 1000) / ms,
-            "fused_M_share": stats["fused_M"] / M if M else 0.0,
-            "hbm_merge_elems": stats["hbm_merge_elems"],
-            "hbm_merge_bytes_over_2wM": (2 * w_bytes * stats["hbm_merge_elems"]) / (2 * w_bytes * M) if M else 0.0}
+                "algorithmic_bytes_per_step": algo,
+                "algorithmic_basis": "SURVEY 8(d): 2w bytes per element per non-fused merge-tree level, "
+                                     "2w(M - M_fused) per step (M_fused: levels done inside the leaf sort)",
+                "physical": {"bytes_per_step": phys, "achieved": phys / (mm / 1000) / 1e9,
+                             "frac": phys / (mm / 1000) / 1e9 / peak,
+                             "basis": "2w x elements the 4-way kernel reads and writes (two tree levels "
+                                      "per HBM pass: only even-depth nodes are materialized)"},
+                "merge_launches_per_step": phases[-1]["merge_launches"], "kernel_ms_per_step": mm,
+                "timing": "CUDA events around each level-merge launch on the sorting stream, "
+                          "over the timed steps"}
+    t_roof = 2 * w_bytes * M_g / (world * peak * 1e9) * 1000
+    tree = {"bytes_2wM": 2 * w_bytes * M_g, "M": M_g, "M_over_n": M_g / n_total, "runs": runs_g,
+            "M_source": "global plan (vmps_merge_plan_dist over the shards)" if world > 1 else "plan of the array",
+            "t_roof_ms_at_peak": t_roof, "frac_of_roofline": t_roof / ms,
+            "local_M": M_loc, "fused_M_share": fM_loc / M_loc if M_loc else 0.0, "hbm_merge_elems": hme,
+            "hbm_merge_bytes_over_2wM": hme / M_loc if M_loc else 0.0}
     ph = {}
     if phases:
         for key in ("plan_ms", "leaf_ms", "partition_ms", "merge_ms", "total_ms"):
             ph[key] = statistics.mean(p[key] for p in phases)
+        if world > 1:
+            ph["note"] = "phases of this rank's local sort (rank 0); exchange and final merge not split out"
 
-    # end-to-end through the public C-ABI host entry (vmps_sort_pairs_host):
-    # every step copies its batch in from pinned host memory, sorts it and
-    # copies the sorted keys + payload back out to pinned host memory.  Steps
-    # rotate over NS streams with their own device buffers and workspaces, so
-    # the copy engines (H2D, D2H) and the SMs work on different batches at
-    # once (whole-job throughput of a stream of batches).
+    # end-to-end through the public C-ABI host entry points: every step copies
+    # its batch in from pinned host memory, sorts it and copies the result out
     e2e = None
     if not args.no_e2e and world == 1:
         NS = 3
         ks = max(NS, min(max(args.steps, 8), 12))
-        hk = torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)
-        hv = torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)
-        hk.copy_(keys0)
-        hv.copy_(vals0)
-        outs = [(torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32),
-                 torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)) for _ in range(NS)]
+        hk = _pinned_like(keys0)
+        _sv(hk).copy_(_sv(keys0))
+        hvv = None
+        if hv:
+            hvv = _pinned_like(vals0)
+            _sv(hvv).copy_(_sv(vals0))
+        outs = [(_pinned_like(keys0), _pinned_like(vals0) if hv else None) for _ in range(NS)]
         streams = [torch.cuda.Stream(dev) for _ in range(NS)]
-        dbufs = [(keys, vals)] + [(torch.empty_like(keys), torch.empty_like(vals)) for _ in range(NS - 1)]
+        dbufs = [(keys, vals)] + [(torch.empty_like(keys), torch.empty_like(vals) if hv else None)
+                                  for _ in range(NS - 1)]
         wss = [ws] + [vm.Workspace() for _ in range(NS - 1)]
 
         def e2e_step(q):
             j = q % NS
-            vm.sort_host_(hk, hv, device=dev, out_keys=outs[j][0], out_values=outs[j][1],
+            vm.sort_host_(hk, hvv, device=dev, out_keys=outs[j][0], out_values=outs[j][1],
                           d_keys=dbufs[j][0], d_values=dbufs[j][1], workspace=wss[j], stream=streams[j])
 
         for q in range(NS):  # warm-up (workspace allocation, first-touch)
@@ -381,63 +548,61 @@ def main():
         e1.record(cur)
         e1.synchronize()
         te = e0.elapsed_time(e1) / ks
-        # the last read-back is the exact stable sort (same input every step):
-        # compare with a device-sorted reference copy
-        ref_k, ref_v = keys0.clone(), vals0.clone()
-        vm.sort_(ref_k, ref_v, workspace=wss[1])
-        torch.cuda.synchronize()
+        # the last read-back equals the device sort verified above (same input every step)
         lo_ = outs[(ks - 1) % NS]
-        ok_e2e = bool((lo_[0] == ref_k.cpu()).all()) and bool((lo_[1] == ref_v.cpu()).all())
-        del ref_k, ref_v
+        ok_e2e = bool((_sv(lo_[0]).to(dev) == _sv(keys)).all()) and (
+            not hv or bool((_sv(lo_[1]).to(dev) == _sv(vals)).all()))
         e2e = {"value": n / (te / 1000) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
-               "ms_per_step": te, "steps": ks, "api": "vmps_sort_pairs_host (C ABI) via sort_host_",
+               "h2d_bytes_per_step": n * w_bytes, "d2h_bytes_per_step": n * w_bytes,
+               "ms_per_step": te, "steps": ks, "api": "vmps_sort_*_host (C ABI) via sort_host_",
                "pipelining": f"{NS} streams, each with its own device buffers and workspace",
                "verified": ok_e2e}
-        del hk, hv, outs, dbufs, wss[1:]
+        del hk, hvv, outs, dbufs, wss[1:]
     elif not args.no_e2e:
         # sharded: per rank, copy the shard in, distributed sort, copy it out
         ks = max(1, min(args.steps, 3))
-        hk = torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)
-        hv = torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)
-        hk.copy_(keys0)
-        hv.copy_(vals0)
-        ok_ = torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)
-        ov_ = torch.empty(n, dtype=torch.int32, pin_memory=True).view(torch.uint32)
+        hk = _pinned_like(keys0)
+        _sv(hk).copy_(_sv(keys0))
+        hvv = _pinned_like(vals0) if hv else None
+        if hv:
+            _sv(hvv).copy_(_sv(vals0))
+        ok_ = _pinned_like(keys0)
+        ov_ = _pinned_like(vals0) if hv else None
         et = []
         for q in range(ks + 1):
             barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            keys.copy_(hk, non_blocking=True)
-            vals.copy_(hv, non_blocking=True)
+            _sv(keys).copy_(_sv(hk), non_blocking=True)
+            if hv:
+                _sv(vals).copy_(_sv(hvv), non_blocking=True)
             do_sort()
-            ok_.copy_(keys, non_blocking=True)
-            ov_.copy_(vals, non_blocking=True)
+            _sv(ok_).copy_(_sv(keys), non_blocking=True)
+            if hv:
+                _sv(ov_).copy_(_sv(vals), non_blocking=True)
             e1.record(stream)
             e1.synchronize()
             if q:
                 et.append(e0.elapsed_time(e1))
         te = torch.tensor([statistics.mean(et)], dtype=torch.float64, device=dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": n * world / (float(te.item()) / 1000) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
-               "ms_per_step": float(te.item()), "steps": ks, "api": "sort_dist_ with pinned host copies"}
-        del hk, hv, ok_, ov_
+        e2e = {"value": n_total / (float(te.item()) / 1000) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": n * w_bytes, "d2h_bytes_per_step": n * w_bytes,
+               "bytes_note": "per rank", "ms_per_step": float(te.item()), "steps": ks,
+               "api": "dist.sort_dist_ (vmps_sort_*_dist) with pinned host copies on each rank"}
+        del hk, hvv, ok_, ov_
 
     bounded = None
-    if world == 1 and args.bounded_reps > 0:
+    if world == 1 and args.bounded_reps > 0 and hv:
         import math
         S = int(4 * math.sqrt(n * math.log2(n)))
-        keys.copy_(keys0)
-        vals.copy_(vals0)
+        restore()
         bws = vm.Workspace()
         bst = vm.sort_(keys, vals, scratch=S, stats=True, workspace=bws)  # warm-up + stats
         bt = []
         for _ in range(args.bounded_reps):
-            keys.copy_(keys0)
-            vals.copy_(vals0)
+            restore()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -455,32 +620,45 @@ def main():
         del bws
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         model, ncpu = cpu_info()
-        v, dt = oracle_sample_rate(args.cpu_sample_log2)
+        log2 = min(args.cpu_sample_log2, log2n)
+        v, dt = oracle_sample_rate(cfg, log2)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"cfg5-shaped sample n=2^{args.cpu_sample_log2} (seed 5), oracle variant A, "
-                         f"{dt:.1f} s single-threaded",
+               "sample": f"cfg{cfg}-shaped sample n=2^{log2}, oracle variant A, {dt:.1f} s single-threaded"
+                         + (" on rank 0's host" if world > 1 else ""),
                "cpu": model, "host_cores": ncpu}
 
     if rank == 0:
+        if world > 1:
+            par = (f"dp{world}: contiguous shards, local sort, exact splitters (native 16-ary search), "
+                   + ("CUDA-IPC pull-merge from peer memory" if args.pull_dist else
+                      "NCCL grouped send/recv, stable merge of the pieces (vmps_sort_pairs_dist)"))
+        else:
+            par = "single"
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-               "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-               "config": {"workload": WORKLOAD, "n_per_gpu": n, "n_total": n * world,
+               "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+               "scaling": "strong" if strong else "weak", "vs_baseline": None,
+               "dtype": {3: "u64", 4: "f32"}.get(cfg, "u32"), "data": "synthetic",
+               "config": {"workload": WORKLOADS[cfg], "config": cfg, "n_per_gpu": n, "n_total": n_total,
                           "merge_schedule": "one level per pass" if args.one_level else "two levels per pass (4-way)",
-                          "key": "u32", "payload": "u32", "scratch": "unbounded",
-                          "parallelism": (f"dp{world}: contiguous shards, local sort, exact splitters, "
-                                          "NCCL all-to-all, local stable merge") if world > 1 else "single",
-                          "timing": "CUDA events around each sort on its stream; input restored "
-                                    "by an untimed 8 GiB device copy between steps (flushes L2)",
-                          "runs": stats["runs"], "merge_cost_M": M, "max_power": stats["max_power"],
+                          "key": str(keys0.dtype).replace("torch.", ""), "payload": "u32" if hv else None,
+                          "scratch": "unbounded", "parallelism": par,
+                          "timing": "CUDA events around each sort on its stream, max over ranks; input restored "
+                                    "by an untimed device copy between steps (cfg5: 8 GiB, flushes L2)",
+                          "runs": runs_g, "merge_cost_M": M_g, "max_power": stats["max_power"],
                           "levels_executed": stats["levels_executed"]},
                "roofline": roof, "tree_roofline": tree, "phases_ms": ph,
                "cpu_baseline": cpu, "e2e": e2e, "bounded": bounded,
-               "gpu_launches": launches, "clocks": clk, "verified": ok}
+               "gpu_launches": launches, "clocks": clk, "verified": ok,
+               "verification": {"sorted": True, "multiset_hash": "sum of mix64(key, payload) equal before / after",
+                                "stability": stab,
+                                "permutation": "keys == input[payload] (exact)" if world == 1 and hv else
+                                "via the multiset hash"}}
         print(json.dumps(out), flush=True)
     if world > 1:
+        from paper_2605_27147_b200 import dist as vdist
+        vdist.destroy_comms()
         dist.destroy_process_group()
 
 

@@ -228,7 +228,8 @@ vmps_status_t vmps_plan_from_runs(const uint64_t* d_run_start, uint64_t r, uint6
  * ncclSend / ncclRecv of keys and payloads; vmps_merge_runs of the received
  * pieces in source-rank order (ties to the lower rank).  h_stats (optional)
  * reports the local sort.  Workspace: vmps_dist_workspace_bytes.  Synchronises
- * `stream` once per search round.
+ * `stream` once per search round (each wait polls for NCCL errors and the
+ * VMPS_COMM_TIMEOUT_S timeout).
  *
  * vmps_merge_plan_dist: Alg. 1's merge plan of the concatenated shards with
  * the global n (reading C13; as paper_2605_27147_b200.dist.merge_plan_dist):
@@ -251,10 +252,65 @@ vmps_status_t vmps_sort_pairs_dist(vmps_comm_t c, void* keys, uint32_t* vals, ui
                                    vmps_stats_t* h_stats);
 vmps_status_t vmps_merge_plan_dist_workspace_bytes(uint64_t n_total, uint64_t n_local, vmps_key_t kt, int world,
                                                    size_t* h_bytes);
+/* cap_runs that always suffices for vmps_merge_plan_dist on this shard:
+ * n_local / minrun(n_total) + 2 (every run but the array's last has >= minrun
+ * keys; merges with j in the shard are at most as many as its runs). */
+vmps_status_t vmps_merge_plan_dist_capacity(uint64_t n_total, uint64_t n_local, uint64_t* h_cap);
 vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_local, vmps_key_t kt,
                                    uint64_t* run_start, uint8_t* run_kind, vmps_merge_rec_t* merges,
                                    uint64_t cap_runs, uint64_t* h_num_runs_local, uint64_t* h_num_merges_local,
                                    void* ws, size_t ws_bytes, void* stream);
+
+/* In-process virtual ranks (tests): vmps_local_group_create
+ * makes a group of `world` ranks that are threads of this process (any
+ * devices; all on one GPU is the intended use), vmps_comm_init_local gives
+ * rank `rank` its communicator.  Every vmps_*_dist call then runs the same
+ * protocol as over NCCL, with collectives made of host barriers, CUDA events
+ * and device-to-device copies; each rank calls from its own thread with its
+ * own stream and workspace.  A rank that does not reach a collective within
+ * VMPS_COMM_TIMEOUT_S seconds (default 600) fails the group: every waiting
+ * call returns VMPS_ERR_NCCL.  Destroy the communicators before the group.
+ *
+ * Failure detection (both transports): every host wait of the protocol polls
+ * the stream, and for NCCL ncclCommGetAsyncError; an asynchronous NCCL error
+ * or a wait longer than VMPS_COMM_TIMEOUT_S aborts the communicator and
+ * returns VMPS_ERR_NCCL (detail in vmps_comm_last_error()). */
+vmps_status_t vmps_local_group_create(int world, int device, void** h_group);
+vmps_status_t vmps_local_group_destroy(void* group);
+vmps_status_t vmps_comm_init_local(vmps_comm_t* h_out, int rank, void* group, int device);
+
+/* vmps_dist_cuts: steps 2-3 of the distributed sort on already sorted shards
+ * (used by the pull-merge protocol): every rank's shard size (h_sizes[g],
+ * optional) and the exact cut table h_cut[q * (g + 1) + t] = elements of rank
+ * q that go to ranks < t (global output ranks [off_t, off_t+1) go to rank t,
+ * ties split in rank order).  h_rounds (optional): search rounds.  Workspace:
+ * vmps_dist_cuts_workspace_bytes(world).  Synchronises `stream`. */
+vmps_status_t vmps_dist_cuts_workspace_bytes(int world, size_t* h_bytes);
+vmps_status_t vmps_dist_cuts(vmps_comm_t c, const void* keys, uint64_t n_local, vmps_key_t kt, uint64_t* h_cut,
+                             uint64_t* h_sizes, uint32_t* h_rounds, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- host-side protocol arithmetic (no device work; the native protocol's
+ * own steps, exported so other orchestrations and CPU tests use them) ----
+ * vmps_splitter_probes: the probes of one 16-ary search round of the m
+ * splitters over the key order image: for each t with lo[t] < hi[t], up to
+ * 15 increasing probes in [lo[t], hi[t]) at lo + k (hi - lo) / 16; h_probe
+ * (capacity 15 m) receives them, h_base[m + 1] the index of each splitter's
+ * first probe, *h_nprobe the count (0 = every splitter found).
+ * vmps_splitter_update: with h_le_sum[k] = #{keys of all ranks with image <=
+ * probe k}, narrows [lo[t], hi[t]] to the least image v with #{<= v} >= R[t].
+ * vmps_split_points: per-rank cut for output rank R from every rank's counts
+ * of '< v*' (h_lt[g]) and '<= v*' (h_le[g]): all keys < v*, then the tie group
+ * at v* in rank order (stability).
+ * vmps_compose_tables: composition of g shards' run-detection transfer tables
+ * (h_tables[q * ns + state], see vmps_shard_chain) from START(0): each shard's
+ * entry state and runs started (empty shards: identity). */
+vmps_status_t vmps_splitter_probes(uint32_t m, const uint64_t* h_lo, const uint64_t* h_hi, uint64_t* h_probe,
+                                   uint32_t* h_base, uint32_t* h_nprobe);
+vmps_status_t vmps_splitter_update(uint32_t m, uint64_t* h_lo, uint64_t* h_hi, const uint64_t* h_R,
+                                   const uint64_t* h_probe, const uint32_t* h_base, const uint64_t* h_le_sum);
+vmps_status_t vmps_split_points(uint32_t g, uint64_t R, const uint64_t* h_lt, const uint64_t* h_le, uint64_t* h_cut);
+vmps_status_t vmps_compose_tables(uint32_t g, uint32_t ns, const uint64_t* h_tables, const uint64_t* h_sizes,
+                                  uint32_t* h_entry, uint64_t* h_count);
 
 /* ---- pull-merge (csrc/engine4.cuh k_pull_merge) ----
  * vmps_merge_pieces: the stable merge of g (1..8) sorted pieces that live at

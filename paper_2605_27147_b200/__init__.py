@@ -64,7 +64,10 @@ EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_me
            "vmps_comm_last_error", "vmps_dist_workspace_bytes", "vmps_sort_keys_dist", "vmps_sort_pairs_dist",
            "vmps_merge_plan_dist_workspace_bytes", "vmps_merge_plan_dist", "vmps_sort_records_workspace_bytes",
            "vmps_sort_records", "vmps_records_last_error", "vmps_merge_pieces_workspace_bytes",
-           "vmps_merge_pieces", "vmps_ipc_handle", "vmps_ipc_open", "vmps_ipc_close")
+           "vmps_merge_pieces", "vmps_ipc_handle", "vmps_ipc_open", "vmps_ipc_close",
+           "vmps_local_group_create", "vmps_local_group_destroy", "vmps_comm_init_local",
+           "vmps_dist_cuts_workspace_bytes", "vmps_dist_cuts", "vmps_splitter_probes", "vmps_splitter_update",
+           "vmps_split_points", "vmps_compose_tables", "vmps_merge_plan_dist_capacity")
 
 _lib = None
 
@@ -102,6 +105,8 @@ def lib() -> ctypes.CDLL:
         L.vmps_sort_keys_dist.argtypes = [vp, vp, u64, ci, i64, vp, sz, vp, vp]
         L.vmps_sort_pairs_dist.argtypes = [vp, vp, vp, u64, ci, i64, vp, sz, vp, vp]
         L.vmps_merge_plan_dist_workspace_bytes.argtypes = [u64, u64, ci, ci, ctypes.POINTER(sz)]
+        L.vmps_merge_plan_dist_capacity.argtypes = [u64, u64, ctypes.POINTER(u64)]
+        L.vmps_merge_plan_dist_capacity.restype = ctypes.c_int
         L.vmps_merge_plan_dist.argtypes = [vp, vp, u64, ci, vp, vp, vp, u64, ctypes.POINTER(u64),
                                            ctypes.POINTER(u64), vp, sz, vp]
         L.vmps_merge_pieces_workspace_bytes.argtypes = [u64, ci, ci, u32, ctypes.POINTER(sz)]
@@ -111,6 +116,19 @@ def lib() -> ctypes.CDLL:
         L.vmps_ipc_close.argtypes = [vp, u64]
         for f in ("vmps_merge_pieces_workspace_bytes", "vmps_merge_pieces", "vmps_ipc_handle", "vmps_ipc_open",
                   "vmps_ipc_close"):
+            getattr(L, f).restype = ctypes.c_int
+        L.vmps_local_group_create.argtypes = [ci, ci, ctypes.POINTER(vp)]
+        L.vmps_local_group_destroy.argtypes = [vp]
+        L.vmps_comm_init_local.argtypes = [ctypes.POINTER(vp), ci, vp, ci]
+        L.vmps_dist_cuts_workspace_bytes.argtypes = [ci, ctypes.POINTER(sz)]
+        L.vmps_dist_cuts.argtypes = [vp, vp, u64, ci, vp, vp, vp, vp, sz, vp]
+        L.vmps_splitter_probes.argtypes = [u32, vp, vp, vp, vp, ctypes.POINTER(u32)]
+        L.vmps_splitter_update.argtypes = [u32, vp, vp, vp, vp, vp, vp]
+        L.vmps_split_points.argtypes = [u32, u64, vp, vp, vp]
+        L.vmps_compose_tables.argtypes = [u32, u32, vp, vp, vp, vp]
+        for f in ("vmps_local_group_create", "vmps_local_group_destroy", "vmps_comm_init_local",
+                  "vmps_dist_cuts_workspace_bytes", "vmps_dist_cuts", "vmps_splitter_probes",
+                  "vmps_splitter_update", "vmps_split_points", "vmps_compose_tables"):
             getattr(L, f).restype = ctypes.c_int
         L.vmps_sort_records_workspace_bytes.argtypes = [u64, u32, ctypes.POINTER(sz)]
         L.vmps_sort_records.argtypes = [vp, vp, vp, u64, u32, vp, sz, vp]
@@ -203,15 +221,17 @@ class Workspace:
         return self.buf
 
 
-# default workspaces, one per (device, stream): sorts on different streams
-# never share one implicitly
+# default workspaces, one per (device, stream, thread): sorts on different
+# streams never share one implicitly, nor do threads that torch hands the same
+# pooled stream
 _default_ws: dict = {}
 
 
 def _default_workspace(device, stream: torch.cuda.Stream | None = None) -> Workspace:
+    import threading
     device = torch.device(device)
     sp = (stream if stream is not None else torch.cuda.current_stream(device)).cuda_stream
-    return _default_ws.setdefault((device, sp), Workspace())
+    return _default_ws.setdefault((device, sp, threading.get_ident()), Workspace())
 
 
 def _stream_ptr(device) -> int:
@@ -339,14 +359,6 @@ def merge_plan(keys: torch.Tensor, workspace: Workspace | None = None) -> Plan:
     power = (recs[:, 3] & 0xFFFFFFFF)
     merges = torch.stack([recs[:, 0], recs[:, 1], recs[:, 2], power], dim=1)
     return Plan(rs[:r], rk[:r], merges)
-
-
-def minrun_for(n: int) -> int:
-    """The paper's minrun rule: halve n (rounding up) until it is < 64."""
-    m = n
-    while m >= 64:
-        m = (m + 1) // 2
-    return max(m, 1)
 
 
 def shard_chain(keys: torch.Tensor, minrun: int, n_end: int, prev: torch.Tensor | None = None,
@@ -500,14 +512,39 @@ def comm_unique_id() -> bytes:
     return buf.raw
 
 
-class Comm:
-    """A native communicator (vmps_comm_init); destroy() or use as a context."""
+class LocalGroup:
+    """A group of in-process virtual ranks (vmps_local_group_create): threads
+    of this process, typically all on one GPU, that run the native protocol
+    with collectives made of barriers, events and device copies."""
 
-    def __init__(self, rank: int, world: int, uid: bytes, device: int):
+    def __init__(self, world: int, device: int = 0):
+        self.ptr = ctypes.c_void_p()
+        self.world, self.device = world, device
+        _check_comm(lib().vmps_local_group_create(world, device, ctypes.byref(self.ptr)), "vmps_local_group_create")
+
+    def destroy(self):
+        if self.ptr:
+            _check_comm(lib().vmps_local_group_destroy(self.ptr), "vmps_local_group_destroy")
+            self.ptr = ctypes.c_void_p()
+
+
+class Comm:
+    """A native communicator (vmps_comm_init over NCCL, or Comm.local for a
+    virtual rank of a LocalGroup); destroy() or use as a context."""
+
+    def __init__(self, rank: int, world: int, uid: bytes | None, device: int, group: LocalGroup | None = None):
         self.ptr = ctypes.c_void_p()
         self.rank, self.world, self.device = rank, world, device
+        if group is not None:
+            _check_comm(lib().vmps_comm_init_local(ctypes.byref(self.ptr), rank, group.ptr, device),
+                        "vmps_comm_init_local")
+            return
         buf = ctypes.create_string_buffer(bytes(uid), 128)
         _check_comm(lib().vmps_comm_init(ctypes.byref(self.ptr), rank, world, buf, device), "vmps_comm_init")
+
+    @classmethod
+    def local(cls, rank: int, group: LocalGroup) -> "Comm":
+        return cls(rank, group.world, None, group.device, group)
 
     def destroy(self):
         if self.ptr:
@@ -562,7 +599,9 @@ def merge_plan_dist_native(comm: Comm, keys: torch.Tensor, n_total: int,
            "vmps_merge_plan_dist_workspace_bytes")
     ws = workspace if workspace is not None else _default_workspace(dev)
     buf = ws.get(int(nb.value), dev)
-    cap = max(n, 1) + 2
+    c64 = ctypes.c_uint64(0)
+    _check(L.vmps_merge_plan_dist_capacity(n_total, n, ctypes.byref(c64)), "vmps_merge_plan_dist_capacity")
+    cap = int(c64.value)
     rs = torch.empty(cap, dtype=torch.int64, device=dev)
     rk = torch.empty(cap, dtype=torch.uint8, device=dev)
     mg = torch.empty(cap * 4, dtype=torch.int64, device=dev)
@@ -575,6 +614,123 @@ def merge_plan_dist_native(comm: Comm, keys: torch.Tensor, n_total: int,
     recs = mg[: 4 * int(nm.value)].view(-1, 4)
     merges = torch.stack([recs[:, 0], recs[:, 1], recs[:, 2], recs[:, 3] & 0xFFFFFFFF, recs[:, 3] >> 32], dim=1)
     return Plan(rs[: int(nr.value)], rk[: int(nr.value)], merges)
+
+
+def count_rank(keys: torch.Tensor, probes: list[int]) -> tuple[torch.Tensor, torch.Tensor]:
+    """vmps_count_rank: (lt, le) int64 device tensors -- the number of keys of
+    the SORTED tensor whose order image is < / <= each probe image."""
+    dev = keys.device
+    p = torch.tensor([x - (1 << 64) if x >= (1 << 63) else x for x in probes], dtype=torch.int64, device=dev)
+    lt = torch.empty(len(probes), dtype=torch.int64, device=dev)
+    le = torch.empty(len(probes), dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        rc = lib().vmps_count_rank(keys.data_ptr(), keys.numel(), key_type(keys), p.data_ptr(), len(probes),
+                                   lt.data_ptr(), le.data_ptr(), _stream_ptr(dev))
+    _check(rc, "vmps_count_rank")
+    return lt, le
+
+
+def merge_runs(keys: torch.Tensor, vals: torch.Tensor | None, starts: list[int],
+               workspace: Workspace | None = None) -> None:
+    """vmps_merge_runs: in-place stable merge of the adjacent sorted runs that
+    start at `starts` (ties to the earlier run)."""
+    n = keys.numel()
+    if len(starts) <= 1 or n <= 1:
+        return
+    kt = key_type(keys)
+    L = lib()
+    nb = ctypes.c_size_t(0)
+    _check(L.vmps_merge_runs_workspace_bytes(n, kt, 1 if vals is not None else 0, len(starts), ctypes.byref(nb)),
+           "vmps_merge_runs_workspace_bytes")
+    ws = workspace if workspace is not None else _default_workspace(keys.device)
+    buf = ws.get(int(nb.value), keys.device)
+    hs = (ctypes.c_uint64 * len(starts))(*starts)
+    with torch.cuda.device(keys.device):
+        rc = L.vmps_merge_runs(keys.data_ptr(), None if vals is None else vals.data_ptr(), n, kt, hs, len(starts),
+                               buf.data_ptr(), buf.numel(), _stream_ptr(keys.device))
+    _check(rc, "vmps_merge_runs")
+
+
+def dist_cuts(comm: Comm, keys: torch.Tensor, workspace: Workspace | None = None):
+    """vmps_dist_cuts on this rank's SORTED shard: (cut, sizes, rounds) with
+    cut[q][t] = elements of rank q that go to ranks < t (a (g, g+1) list of
+    lists) and every rank's shard size."""
+    import numpy as np
+    g = comm.world
+    kt = key_type(keys)
+    dev = keys.device
+    L = lib()
+    nb = ctypes.c_size_t(0)
+    _check_comm(L.vmps_dist_cuts_workspace_bytes(g, ctypes.byref(nb)), "vmps_dist_cuts_workspace_bytes")
+    ws = workspace if workspace is not None else _default_workspace(dev)
+    buf = ws.get(int(nb.value), dev)
+    cut = np.zeros(g * (g + 1), np.uint64)
+    sizes = np.zeros(g, np.uint64)
+    rounds = ctypes.c_uint32(0)
+    with torch.cuda.device(dev):
+        rc = L.vmps_dist_cuts(comm.ptr, keys.data_ptr(), keys.numel(), kt, cut.ctypes.data, sizes.ctypes.data,
+                              ctypes.byref(rounds), buf.data_ptr(), buf.numel(), _stream_ptr(dev))
+    _check_comm(rc, "vmps_dist_cuts")
+    return cut.reshape(g, g + 1).astype(np.int64).tolist(), sizes.astype(np.int64).tolist(), int(rounds.value)
+
+
+# ---- host-side protocol arithmetic of the native multi-GPU protocol (C) ----
+
+def _u64(a):
+    import numpy as np
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+
+
+def splitter_probes(lo, hi):
+    """vmps_splitter_probes: (probes, base) of one 16-ary search round."""
+    import numpy as np
+    m = len(lo)
+    lo_, hi_ = _u64(lo), _u64(hi)
+    pr = np.zeros(max(15 * m, 1), np.uint64)
+    base = np.zeros(m + 1, np.uint32)
+    nprobe = ctypes.c_uint32(0)
+    _check_comm(lib().vmps_splitter_probes(m, lo_.ctypes.data, hi_.ctypes.data, pr.ctypes.data, base.ctypes.data,
+                                           ctypes.byref(nprobe)), "vmps_splitter_probes")
+    return [int(x) for x in pr[:nprobe.value]], [int(x) for x in base]
+
+
+def splitter_update(lo, hi, R, probes, base, le_sum):
+    """vmps_splitter_update: the narrowed (lo, hi) after one round."""
+    import numpy as np
+    m = len(lo)
+    lo_, hi_ = _u64(lo), _u64(hi)
+    pr, ls, r_ = _u64(probes if probes else [0]), _u64(le_sum if le_sum else [0]), _u64(R)
+    b = np.ascontiguousarray(np.asarray(base, dtype=np.uint32))
+    _check_comm(lib().vmps_splitter_update(m, lo_.ctypes.data, hi_.ctypes.data, r_.ctypes.data, pr.ctypes.data,
+                                           b.ctypes.data, ls.ctypes.data), "vmps_splitter_update")
+    return [int(x) for x in lo_], [int(x) for x in hi_]
+
+
+def split_points(R: int, lt, le):
+    """vmps_split_points: per-rank cut for global output rank R (ties in rank order)."""
+    import numpy as np
+    g = len(lt)
+    out = np.zeros(g, np.uint64)
+    lt_, le_ = _u64(lt), _u64(le)  # kept alive across the call
+    _check_comm(lib().vmps_split_points(g, R, lt_.ctypes.data, le_.ctypes.data, out.ctypes.data),
+                "vmps_split_points")
+    return [int(x) for x in out]
+
+
+def compose_tables(tables, sizes, ns: int):
+    """vmps_compose_tables: (entry states, run counts) of consecutive shards."""
+    import numpy as np
+    g = len(sizes)
+    t = np.zeros(g * ns, np.uint64)
+    for q, tab in enumerate(tables):
+        if tab is not None:
+            t[q * ns:(q + 1) * ns] = np.asarray(tab, dtype=np.int64).astype(np.uint64)
+    entry = np.zeros(g, np.uint32)
+    count = np.zeros(g, np.uint64)
+    sz_ = _u64(sizes)
+    _check_comm(lib().vmps_compose_tables(g, ns, t.ctypes.data, sz_.ctypes.data, entry.ctypes.data,
+                                          count.ctypes.data), "vmps_compose_tables")
+    return [int(x) for x in entry], [int(x) for x in count]
 
 
 def profile_enable(on: bool = True) -> None:

@@ -27,8 +27,13 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cub/device/device_select.cuh>
@@ -44,6 +49,8 @@ struct Nccl {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*);
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
   ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*CommAbort)(ncclComm_t);
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*);
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
@@ -54,8 +61,10 @@ struct Nccl {
   const char* (*GetErrorString)(ncclResult_t);
 };
 Nccl g_nccl;
+std::mutex g_nccl_mu;
 
 bool nccl_load() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
   if (g_nccl.tried) return g_nccl.ok;
   g_nccl.tried = true;
   void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -66,6 +75,8 @@ bool nccl_load() {
   g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))sym("ncclGetUniqueId");
   g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))sym("ncclCommInitRank");
   g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))sym("ncclCommDestroy");
+  g_nccl.CommAbort = (decltype(g_nccl.CommAbort))sym("ncclCommAbort");
+  g_nccl.CommGetAsyncError = (decltype(g_nccl.CommGetAsyncError))sym("ncclCommGetAsyncError");
   g_nccl.AllReduce = (decltype(g_nccl.AllReduce))sym("ncclAllReduce");
   g_nccl.AllGather = (decltype(g_nccl.AllGather))sym("ncclAllGather");
   g_nccl.Broadcast = (decltype(g_nccl.Broadcast))sym("ncclBroadcast");
@@ -99,7 +110,8 @@ bool nccl_load() {
   do {                                                                         \
     vmps_status_t v_ = (call);                                                 \
     if (v_ != VMPS_OK) {                                                       \
-      c_err = std::string(#call) + ": " + vmps_last_error();                   \
+      if (v_ != VMPS_ERR_NCCL || c_err.empty())                                \
+        c_err = std::string(#call) + ": " + vmps_last_error() + " " + c_err;   \
       return v_;                                                               \
     }                                                                          \
   } while (0)
@@ -127,50 +139,322 @@ struct Carve {
   }
 };
 
-// Gather one int64 value (or a fixed-size vector) from every rank into host memory.
-template <typename T>
-vmps_status_t gather_host(vmps_comm_t c, const T* h_mine, size_t count, std::vector<T>* out, T* d_buf,
-                          cudaStream_t s);
+double comm_timeout_s() {
+  const char* e = getenv("VMPS_COMM_TIMEOUT_S");
+  const double t = e ? atof(e) : 0.0;
+  return t > 0 ? t : 600.0;
+}
+
+// ---------------------------------------------------------------------------
+// In-process group of virtual ranks (threads of one process, any devices):
+// the same protocol as NCCL, with collectives made of host barriers, CUDA
+// events and device-to-device copies.  Lets tests run the library's own
+// multi-rank protocol with g ranks on one GPU (NCCL refuses two
+// ranks on one device).
+// ---------------------------------------------------------------------------
+constexpr int LG_MAXW = 256;
+struct LocalGroup {
+  int world;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  double timeout_s;
+  // per-rank published state of the current collective
+  const void* ptr[LG_MAXW];
+  size_t bytes[LG_MAXW];
+  std::vector<std::vector<std::pair<const void*, size_t>>> sends;  // [src][dst]
+  std::vector<std::vector<std::pair<const void*, size_t>>> bc;     // [rank][item]
+  cudaEvent_t ev_ready[LG_MAXW], ev_done[LG_MAXW];
+  uint64_t* tmp[LG_MAXW];  // per-rank reduction scratch (device)
+  size_t tmp_cap = 0;
+};
 
 }  // namespace
 
 struct vmps_comm_s {
+  int kind;  // 0 NCCL, 1 in-process virtual ranks
   ncclComm_t nc;
+  LocalGroup* lg;
   int rank, world, device;
+  bool aborted;
 };
 
 namespace {
 
-template <typename T>
-vmps_status_t gather_host(vmps_comm_t c, const T* h_mine, size_t count, std::vector<T>* out, T* d_buf,
-                          cudaStream_t s) {
-  // d_buf holds (world + 1) * count elements: own slot at the end, gathered at the front
-  T* mine = d_buf + (size_t)c->world * count;
-  CK(cudaMemcpyAsync(mine, h_mine, count * sizeof(T), cudaMemcpyHostToDevice, s));
-  NC(g_nccl.AllGather(mine, d_buf, count * sizeof(T), ncclUint8, c->nc, s));
-  out->resize((size_t)c->world * count);
-  CK(cudaMemcpyAsync(out->data(), d_buf, out->size() * sizeof(T), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+// barrier of the local group; false on timeout (the group is then broken)
+bool lg_barrier(LocalGroup* g) {
+  std::unique_lock<std::mutex> lk(g->m);
+  if (g->broken) return false;
+  const uint64_t my = g->gen;
+  if (++g->arrived == g->world) {
+    g->arrived = 0;
+    ++g->gen;
+    g->cv.notify_all();
+    return true;
+  }
+  const bool ok = g->cv.wait_for(lk, std::chrono::duration<double>(g->timeout_s),
+                                 [&] { return g->gen != my || g->broken; });
+  if (!ok || g->broken) {
+    g->broken = true;
+    g->cv.notify_all();
+    return false;
+  }
+  return true;
+}
+
+#define LB(g)                                                                  \
+  do {                                                                         \
+    if (!lg_barrier(g)) {                                                      \
+      c_err = "virtual-rank group: barrier timeout or a rank failed";          \
+      return VMPS_ERR_NCCL;                                                    \
+    }                                                                          \
+  } while (0)
+
+// Phase helpers of a local collective: inputs ready -> copies -> done.
+vmps_status_t lg_begin(vmps_comm_t c, cudaStream_t s) {
+  LocalGroup* g = c->lg;
+  CK(cudaEventRecord(g->ev_ready[c->rank], s));
+  LB(g);
+  for (int q = 0; q < g->world; ++q)
+    if (q != c->rank) CK(cudaStreamWaitEvent(s, g->ev_ready[q], 0));
   return VMPS_OK;
+}
+vmps_status_t lg_end(vmps_comm_t c, cudaStream_t s) {
+  LocalGroup* g = c->lg;
+  CK(cudaEventRecord(g->ev_done[c->rank], s));
+  LB(g);
+  for (int q = 0; q < g->world; ++q)
+    if (q != c->rank) CK(cudaStreamWaitEvent(s, g->ev_done[q], 0));
+  return VMPS_OK;
+}
+
+__global__ void k_sum_u64(uint64_t* out, const uint64_t* const* src, int world, size_t count) {
+  for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) {
+    uint64_t a = 0;
+    for (int q = 0; q < world; ++q) a += src[q][i];
+    out[i] = a;
+  }
+}
+
+// ---- transport: the collectives the protocols use ----
+// in-place sum of count u64 over all ranks
+vmps_status_t tp_allreduce_u64(vmps_comm_t c, uint64_t* d, size_t count, cudaStream_t s) {
+  if (c->kind == 0) {
+    NC(g_nccl.AllReduce(d, d, count, ncclUint64, ncclSum, c->nc, s));
+    return VMPS_OK;
+  }
+  LocalGroup* g = c->lg;
+  if ((count + (size_t)g->world) * 8 > g->tmp_cap) {
+    c_err = "virtual-rank group: reduction too large";
+    return VMPS_ERR_INTERNAL;
+  }
+  g->ptr[c->rank] = d;
+  VK(lg_begin(c, s));
+  // the source pointer table travels as a kernel argument array in device scratch
+  uint64_t* tmp = g->tmp[c->rank];
+  const uint64_t** tab = (const uint64_t**)(tmp + count);
+  std::vector<const uint64_t*> hp(g->world);
+  for (int q = 0; q < g->world; ++q) hp[q] = (const uint64_t*)g->ptr[q];
+  CK(cudaMemcpyAsync(tab, hp.data(), g->world * sizeof(void*), cudaMemcpyHostToDevice, s));
+  k_sum_u64<<<1, 256, 0, s>>>(tmp, tab, g->world, count);
+  CK(cudaGetLastError());
+  VK(lg_end(c, s));  // every rank has read every d
+  CK(cudaMemcpyAsync(d, tmp, count * 8, cudaMemcpyDeviceToDevice, s));
+  return VMPS_OK;  // (the pageable host table was staged by the copy call)
+}
+
+// d_all[q * bytes ..] = rank q's d_mine
+vmps_status_t tp_allgather(vmps_comm_t c, const void* d_mine, void* d_all, size_t bytes, cudaStream_t s) {
+  if (c->kind == 0) {
+    NC(g_nccl.AllGather(d_mine, d_all, bytes, ncclUint8, c->nc, s));
+    return VMPS_OK;
+  }
+  LocalGroup* g = c->lg;
+  g->ptr[c->rank] = d_mine;
+  VK(lg_begin(c, s));
+  for (int q = 0; q < g->world; ++q)
+    if (bytes) CK(cudaMemcpyAsync((char*)d_all + (size_t)q * bytes, g->ptr[q], bytes, cudaMemcpyDeviceToDevice, s));
+  return lg_end(c, s);
+}
+
+struct BItem { void* d; size_t bytes; int root; };
+// in-place broadcasts (item i from its root to every rank; same item list on all ranks)
+vmps_status_t tp_bcast_many(vmps_comm_t c, const std::vector<BItem>& items, cudaStream_t s) {
+  if (c->kind == 0) {
+    NC(g_nccl.GroupStart());
+    for (const BItem& b : items) NC(g_nccl.Broadcast(b.d, b.d, b.bytes, ncclUint8, b.root, c->nc, s));
+    NC(g_nccl.GroupEnd());
+    return VMPS_OK;
+  }
+  LocalGroup* g = c->lg;
+  auto& mine = g->bc[c->rank];
+  mine.clear();
+  for (const BItem& b : items) mine.push_back({b.d, b.bytes});
+  VK(lg_begin(c, s));
+  for (size_t i = 0; i < items.size(); ++i) {
+    const BItem& b = items[i];
+    if (b.root != c->rank && b.bytes)
+      CK(cudaMemcpyAsync(b.d, g->bc[b.root][i].first, b.bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  return lg_end(c, s);
+}
+
+struct P2P { int peer; const void* p; size_t bytes; };
+// grouped point-to-point: sends[i] to sends[i].peer, recvs[i] from recvs[i].peer;
+// at most one send per (peer, tag) order: the k-th send to a peer pairs with
+// the peer's k-th receive from this rank
+vmps_status_t tp_exchange(vmps_comm_t c, const std::vector<P2P>& sends, const std::vector<P2P>& recvs,
+                          cudaStream_t s) {
+  if (c->kind == 0) {
+    NC(g_nccl.GroupStart());
+    for (const P2P& x : sends) NC(g_nccl.Send(x.p, x.bytes, ncclUint8, x.peer, c->nc, s));
+    for (const P2P& x : recvs) NC(g_nccl.Recv((void*)x.p, x.bytes, ncclUint8, x.peer, c->nc, s));
+    NC(g_nccl.GroupEnd());
+    return VMPS_OK;
+  }
+  LocalGroup* g = c->lg;
+  auto& mine = g->sends[c->rank];
+  mine.clear();
+  for (const P2P& x : sends) mine.push_back({x.p, (size_t)x.peer | ((size_t)x.bytes << 8)});
+  VK(lg_begin(c, s));
+  // match the k-th receive from q with q's k-th send to this rank
+  std::vector<int> seen(g->world, 0);
+  for (const P2P& x : recvs) {
+    int k = seen[x.peer]++, hit = -1;
+    const auto& sq = g->sends[x.peer];
+    for (size_t i = 0; i < sq.size(); ++i)
+      if ((int)(sq[i].second & 0xFF) == c->rank && k-- == 0) { hit = (int)i; break; }
+    if (hit < 0 || (sq[hit].second >> 8) != x.bytes) {
+      c_err = "virtual-rank group: unmatched send / receive";
+      return VMPS_ERR_INTERNAL;
+    }
+    if (x.bytes) CK(cudaMemcpyAsync((void*)x.p, sq[hit].first, x.bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  return lg_end(c, s);
+}
+
+// Wait for the stream, polling NCCL's asynchronous error state and a timeout
+// (VMPS_COMM_TIMEOUT_S, default 600 s): a failed or stuck peer returns
+// VMPS_ERR_NCCL (the communicator is aborted) instead of hanging.
+vmps_status_t tp_sync(vmps_comm_t c, cudaStream_t s) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const double lim = comm_timeout_s();
+  for (int it = 0;; ++it) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) return VMPS_OK;
+    if (e != cudaErrorNotReady) {
+      c_err = std::string("stream: ") + cudaGetErrorString(e);
+      return VMPS_ERR_CUDA;
+    }
+    if (c->kind == 0 && !c->aborted) {
+      ncclResult_t ar = ncclSuccess;
+      if (g_nccl.CommGetAsyncError(c->nc, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress) {
+        c_err = std::string("NCCL asynchronous error: ") + g_nccl.GetErrorString(ar);
+        g_nccl.CommAbort(c->nc);
+        c->aborted = true;
+        return VMPS_ERR_NCCL;
+      }
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > lim) {
+      c_err = "communication timeout (VMPS_COMM_TIMEOUT_S)";
+      if (c->kind == 0 && !c->aborted) { g_nccl.CommAbort(c->nc); c->aborted = true; }
+      return VMPS_ERR_NCCL;
+    }
+    if (it > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+// Gather a fixed-size vector of u64 from every rank into host memory.
+vmps_status_t gather_host(vmps_comm_t c, const uint64_t* h_mine, size_t count, std::vector<uint64_t>* out,
+                          uint64_t* d_buf, cudaStream_t s) {
+  // d_buf holds (world + 1) * count elements: own slot at the end, gathered at the front
+  uint64_t* mine = d_buf + (size_t)c->world * count;
+  CK(cudaMemcpyAsync(mine, h_mine, count * 8, cudaMemcpyHostToDevice, s));
+  VK(tp_allgather(c, mine, d_buf, count * 8, s));
+  out->resize((size_t)c->world * count);
+  CK(cudaMemcpyAsync(out->data(), d_buf, out->size() * 8, cudaMemcpyDeviceToHost, s));
+  return tp_sync(c, s);
 }
 
 uint64_t img_max(vmps_key_t kt) { return kt == VMPS_KEY_U64 ? ~0ull : 0xFFFFFFFFull; }
 
+// ---------------------------------------------------------------------------
+// Host-side protocol arithmetic (exported below for the Python path and the
+// CPU tests; no device work).
+// ---------------------------------------------------------------------------
+constexpr uint32_t SPLIT_ARITY = 16;  // probes per splitter per round: 15
+
+// probes of one search round for the m splitters still open (lo < hi):
+// lo + k (hi - lo) / 16, k = 1..15, strictly increasing inside [lo, hi)
+void splitter_probes(uint32_t m, const uint64_t* lo, const uint64_t* hi, std::vector<uint64_t>* probe,
+                     std::vector<uint32_t>* base) {
+  probe->clear();
+  base->assign(m + 1, 0);
+  for (uint32_t t = 0; t < m; ++t) {
+    (*base)[t] = (uint32_t)probe->size();
+    if (lo[t] < hi[t]) {
+      const uint64_t w = hi[t] - lo[t];
+      for (uint32_t k = 1; k < SPLIT_ARITY; ++k) {
+        const uint64_t pr = lo[t] + (uint64_t)(((unsigned __int128)w * k) / SPLIT_ARITY);
+        if (probe->size() > (*base)[t] && probe->back() >= pr) continue;
+        if (pr >= hi[t]) break;
+        probe->push_back(pr);
+      }
+      if (probe->size() == (*base)[t]) probe->push_back(lo[t]);
+    }
+  }
+  (*base)[m] = (uint32_t)probe->size();
+}
+
+// v*_t = the least image value v with #{x <= v} >= R_t: the least probe with
+// sum(le) >= R bounds it from above, the probe before it from below
+void splitter_update(uint32_t m, uint64_t* lo, uint64_t* hi, const uint64_t* R, const uint64_t* probe,
+                     const uint32_t* base, const uint64_t* le_sum) {
+  for (uint32_t t = 0; t < m; ++t) {
+    if (!(lo[t] < hi[t])) continue;
+    uint64_t nlo = lo[t], nhi = hi[t];
+    for (uint32_t k = base[t]; k < base[t + 1]; ++k) {
+      if (le_sum[k] >= R[t]) { nhi = probe[k]; break; }
+      nlo = probe[k] + 1;
+    }
+    lo[t] = nlo;
+    hi[t] = std::max(nlo, nhi);
+  }
+}
+
 // Per-rank cut for output rank R given every rank's counts of '< v*' and
 // '<= v*' (v* = least v with sum(le) >= R): all elements < v*, then the tie
-// group at v* in rank order (stability) -- as dist.split_points.
-std::vector<uint64_t> split_points(uint64_t R, const std::vector<uint64_t>& lt, const std::vector<uint64_t>& le) {
+// group at v* in rank order (lower ranks first: the stable sort of the
+// concatenation, P:657's tie rule across shards).
+void split_points(uint32_t g, uint64_t R, const uint64_t* lt, const uint64_t* le, uint64_t* cuts) {
   uint64_t sum_lt = 0;
-  for (uint64_t x : lt) sum_lt += x;
+  for (uint32_t q = 0; q < g; ++q) sum_lt += lt[q];
   int64_t need = (int64_t)R - (int64_t)sum_lt;
-  std::vector<uint64_t> cuts(lt.size());
-  for (size_t q = 0; q < lt.size(); ++q) {
+  for (uint32_t q = 0; q < g; ++q) {
     const int64_t eq = (int64_t)(le[q] - lt[q]);
     const int64_t take = std::min<int64_t>(std::max<int64_t>(need, 0), eq);
     cuts[q] = lt[q] + (uint64_t)take;
     need -= take;
   }
-  return cuts;
+}
+
+// Chain composition of the shards' run-detection transfer tables from
+// START(0): entry state and runs started per shard (empty shards are the
+// identity; END = 255 stops the chain).
+void compose_tables(uint32_t g, uint32_t ns, const uint64_t* tabs, const uint64_t* sizes, uint32_t* entry,
+                    uint64_t* count) {
+  uint32_t st = 0;
+  for (uint32_t q = 0; q < g; ++q) {
+    entry[q] = st;
+    count[q] = 0;
+    if (!sizes[q] || st == 255u) continue;
+    const uint64_t v = tabs[(size_t)q * ns + st];
+    count[q] = v & 0xFFFFFFFFull;
+    st = (uint32_t)(v >> 32);
+  }
 }
 
 struct DistLayout {
@@ -194,15 +478,84 @@ DistLayout dist_layout(uint64_t n_local, vmps_key_t kt, int has_vals, int world,
   return L;
 }
 
+// Steps 1-3 of the distributed sort on sorted shards: shard sizes and exact
+// splitters; cut[q * (g + 1) + t] = elements of rank q that go to ranks < t.
+vmps_status_t dist_cuts(vmps_comm_t c, const void* keys, uint64_t n_local, vmps_key_t kt, uint64_t* d_probe,
+                        uint64_t* d_lt, uint64_t* d_le, uint64_t* d_cnt, uint64_t* d_small, size_t nprobe_cap,
+                        cudaStream_t s, std::vector<uint64_t>* sizes_out, std::vector<uint64_t>* cut_out,
+                        uint32_t* rounds_out) {
+  const int g = c->world;
+  std::vector<uint64_t> sizes;
+  VK(gather_host(c, &n_local, 1, &sizes, d_small, s));
+  std::vector<uint64_t> off(g + 1, 0);
+  for (int q = 0; q < g; ++q) off[q + 1] = off[q] + sizes[q];
+  std::vector<uint64_t> cut((size_t)g * (g + 1), 0);
+  for (int q = 0; q < g; ++q) cut[(size_t)q * (g + 1) + g] = sizes[q];
+  uint32_t rounds = 0;
+  if (g > 1) {
+    const uint32_t m = (uint32_t)g - 1;
+    std::vector<uint64_t> lo(m, 0), hi(m, img_max(kt)), R(m), probe, le_h(nprobe_cap);
+    std::vector<uint32_t> base;
+    for (uint32_t t = 0; t < m; ++t) R[t] = off[t + 1];
+    for (;;) {
+      splitter_probes(m, lo.data(), hi.data(), &probe, &base);
+      if (probe.empty()) break;
+      ++rounds;
+      CK(cudaMemcpyAsync(d_probe, probe.data(), probe.size() * 8, cudaMemcpyHostToDevice, s));
+      if (n_local) VK(vmps_count_rank(keys, n_local, kt, d_probe, (uint32_t)probe.size(), d_lt, d_le, s));
+      else CK(cudaMemsetAsync(d_le, 0, probe.size() * 8, s));
+      VK(tp_allreduce_u64(c, d_le, probe.size(), s));
+      CK(cudaMemcpyAsync(le_h.data(), d_le, probe.size() * 8, cudaMemcpyDeviceToHost, s));
+      VK(tp_sync(c, s));
+      splitter_update(m, lo.data(), hi.data(), R.data(), probe.data(), base.data(), le_h.data());
+    }
+    // final counts at v* on every rank
+    CK(cudaMemcpyAsync(d_probe, lo.data(), (size_t)m * 8, cudaMemcpyHostToDevice, s));
+    if (n_local) VK(vmps_count_rank(keys, n_local, kt, d_probe, m, d_cnt, d_cnt + m, s));
+    else CK(cudaMemsetAsync(d_cnt, 0, 2 * (size_t)m * 8, s));
+    std::vector<uint64_t> mine(2 * (size_t)m), allc;
+    CK(cudaMemcpyAsync(mine.data(), d_cnt, 2 * (size_t)m * 8, cudaMemcpyDeviceToHost, s));
+    VK(tp_sync(c, s));
+    VK(gather_host(c, mine.data(), 2 * (size_t)m, &allc, d_small, s));
+    std::vector<uint64_t> lt(g), le(g), pts(g);
+    for (uint32_t t = 0; t < m; ++t) {
+      for (int q = 0; q < g; ++q) {
+        lt[q] = allc[(size_t)q * 2 * m + t];
+        le[q] = allc[(size_t)q * 2 * m + m + t];
+      }
+      split_points((uint32_t)g, off[t + 1], lt.data(), le.data(), pts.data());
+      for (int q = 0; q < g; ++q) cut[(size_t)q * (g + 1) + t + 1] = pts[q];
+    }
+  }
+  if (sizes_out) *sizes_out = sizes;
+  if (cut_out) *cut_out = cut;
+  if (rounds_out) *rounds_out = rounds;
+  return VMPS_OK;
+}
+
+// A rank that fails outside a collective breaks its virtual-rank group, so
+// the other ranks return promptly instead of waiting for the timeout.
+vmps_status_t fail_group(vmps_comm_t c, vmps_status_t rc) {
+  if (rc != VMPS_OK && c && c->kind == 1) {
+    std::lock_guard<std::mutex> lk(c->lg->m);
+    c->lg->broken = true;
+    c->lg->cv.notify_all();
+  }
+  return rc;
+}
+
 vmps_status_t sort_dist_any(vmps_comm_t c, void* keys, uint32_t* vals, uint64_t n_local, vmps_key_t kt,
-                            int64_t scratch, void* ws, size_t ws_bytes, cudaStream_t s, vmps_stats_t* h_stats) {
+                            int64_t scratch, void* ws, size_t ws_bytes, cudaStream_t s, vmps_stats_t* h_stats,
+                            bool pairs) {
   if (!c) { c_err = "NULL communicator"; return VMPS_ERR_INVALID_ARG; }
+  if (n_local && !keys) { c_err = "keys is NULL"; return VMPS_ERR_INVALID_ARG; }
   if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) {
     c_err = "unknown key type";
     return VMPS_ERR_INVALID_ARG;
   }
+  c_err.clear();
   const int g = c->world, me = c->rank;
-  const int hv = vals ? 1 : 0;
+  const int hv = pairs ? 1 : 0;  // (an empty shard may pass NULL buffers)
   const DistLayout L = dist_layout(n_local, kt, hv, g, scratch);
   if (!ws || ws_bytes < L.total) { c_err = "workspace too small (vmps_dist_workspace_bytes)"; return VMPS_ERR_BUDGET; }
   Carve cv(ws, ws_bytes);
@@ -216,102 +569,35 @@ vmps_status_t sort_dist_any(vmps_comm_t c, void* keys, uint32_t* vals, uint64_t 
   uint64_t* d_cnt = (uint64_t*)cv.take(2 * nprobe_cap * 8);
   uint64_t* d_small = (uint64_t*)cv.take(L.small);
   if (!d_small) { c_err = "workspace carve"; return VMPS_ERR_BUDGET; }
-  // 1. shard sizes and output ranks
-  std::vector<uint64_t> sizes;
-  VK(gather_host<uint64_t>(c, &n_local, 1, &sizes, d_small, s));
-  std::vector<uint64_t> off(g + 1, 0);
-  for (int q = 0; q < g; ++q) off[q + 1] = off[q] + sizes[q];
-  // 2. local sort
+  // 1. local sort
   if (n_local > 1) {
     if (hv) VK(vmps_sort_pairs(keys, vals, n_local, kt, scratch, sort_ws, std::max(L.sort_ws, L.mr_ws), s, h_stats));
     else VK(vmps_sort_keys(keys, n_local, kt, scratch, sort_ws, std::max(L.sort_ws, L.mr_ws), s, h_stats));
   }
   if (g == 1) return VMPS_OK;
-  // 3. exact splitters for R_t = off_t, t = 1..g-1: 16-ary search over the image
-  const int m = g - 1;
-  std::vector<uint64_t> lo(m, 0), hi(m, img_max(kt));
-  std::vector<uint64_t> probe, le_h(nprobe_cap);
-  for (;;) {
-    probe.clear();
-    std::vector<int> base(m + 1, 0);
-    for (int t = 0; t < m; ++t) {
-      base[t] = (int)probe.size();
-      if (lo[t] < hi[t]) {
-        const uint64_t w = hi[t] - lo[t];
-        for (int k = 1; k <= 15; ++k) {  // strictly inside [lo, hi): lo + k w / 16 (distinct, increasing)
-          const uint64_t pr = lo[t] + (uint64_t)(((unsigned __int128)w * k) / 16);
-          if (probe.size() > (size_t)base[t] && probe.back() >= pr) continue;
-          if (pr >= hi[t]) break;
-          probe.push_back(pr);
-        }
-        if (probe.size() == (size_t)base[t]) probe.push_back(lo[t]);
-      }
-    }
-    base[m] = (int)probe.size();
-    if (probe.empty()) break;
-    CK(cudaMemcpyAsync(d_probe, probe.data(), probe.size() * 8, cudaMemcpyHostToDevice, s));
-    if (n_local) VK(vmps_count_rank(keys, n_local, kt, d_probe, (uint32_t)probe.size(), d_lt, d_le, s));
-    else CK(cudaMemsetAsync(d_le, 0, probe.size() * 8, s));
-    NC(g_nccl.AllReduce(d_le, d_le, probe.size(), ncclUint64, ncclSum, c->nc, s));
-    CK(cudaMemcpyAsync(le_h.data(), d_le, probe.size() * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    for (int t = 0; t < m; ++t) {
-      if (!(lo[t] < hi[t])) continue;
-      const uint64_t R = off[t + 1];
-      // least probe with #(<= probe) >= R bounds v* from above; the probe
-      // before it (#(<= p) < R) from below
-      uint64_t nlo = lo[t], nhi = hi[t];
-      for (int k = base[t]; k < base[t + 1]; ++k) {
-        if (le_h[k] >= R) { nhi = probe[k]; break; }
-        nlo = probe[k] + 1;
-      }
-      lo[t] = nlo;
-      hi[t] = std::max(nlo, nhi);
-    }
-  }
-  // final counts at v* on every rank
-  for (int t = 0; t < m; ++t) probe.push_back(lo[t]);
-  CK(cudaMemcpyAsync(d_probe, probe.data(), (size_t)m * 8, cudaMemcpyHostToDevice, s));
-  if (n_local) VK(vmps_count_rank(keys, n_local, kt, d_probe, (uint32_t)m, d_cnt, d_cnt + m, s));
-  else CK(cudaMemsetAsync(d_cnt, 0, 2 * (size_t)m * 8, s));
-  std::vector<uint64_t> allc;
-  {
-    std::vector<uint64_t> mine(2 * (size_t)m);
-    CK(cudaMemcpyAsync(mine.data(), d_cnt, 2 * (size_t)m * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    VK(gather_host<uint64_t>(c, mine.data(), 2 * (size_t)m, &allc, d_small, s));
-  }
-  // cut[q][t]: elements of rank q that go to ranks < t
-  std::vector<std::vector<uint64_t>> cut(g, std::vector<uint64_t>(g + 1, 0));
-  for (int q = 0; q < g; ++q) cut[q][g] = sizes[q];
-  for (int t = 0; t < m; ++t) {
-    std::vector<uint64_t> lt(g), le(g);
-    for (int q = 0; q < g; ++q) {
-      lt[q] = allc[(size_t)q * 2 * m + t];
-      le[q] = allc[(size_t)q * 2 * m + m + t];
-    }
-    const std::vector<uint64_t> pts = split_points(off[t + 1], lt, le);
-    for (int q = 0; q < g; ++q) cut[q][t + 1] = pts[q];
-  }
-  // 4. exchange: piece [cut[me][p], cut[me][p+1]) to rank p; receive in rank order
+  // 2-3. shard sizes, exact splitters (16-ary search over the key order image)
+  std::vector<uint64_t> sizes, cutv;
+  VK(dist_cuts(c, keys, n_local, kt, d_probe, d_lt, d_le, d_cnt, d_small, nprobe_cap, s, &sizes, &cutv, nullptr));
+  auto cut = [&](int q, int t) { return cutv[(size_t)q * (g + 1) + t]; };
+  // 4. exchange: piece [cut(me, p), cut(me, p+1)) to rank p; receive in rank order
   const size_t kb = kbytes(kt);
   std::vector<uint64_t> roff(g + 1, 0);
-  for (int q = 0; q < g; ++q) roff[q + 1] = roff[q] + (cut[q][me + 1] - cut[q][me]);
+  for (int q = 0; q < g; ++q) roff[q + 1] = roff[q] + (cut(q, me + 1) - cut(q, me));
   if (roff[g] != n_local) { c_err = "internal: received count differs from the shard size"; return VMPS_ERR_INTERNAL; }
-  NC(g_nccl.GroupStart());
+  std::vector<P2P> sends, recvs;
   for (int p = 0; p < g; ++p) {
-    const uint64_t sn = cut[me][p + 1] - cut[me][p];
+    const uint64_t sn = cut(me, p + 1) - cut(me, p);
     const uint64_t rn = roff[p + 1] - roff[p];
     if (sn) {
-      NC(g_nccl.Send((const char*)keys + cut[me][p] * kb, sn * kb, ncclUint8, p, c->nc, s));
-      if (hv) NC(g_nccl.Send(vals + cut[me][p], sn * 4, ncclUint8, p, c->nc, s));
+      sends.push_back({p, (const char*)keys + cut(me, p) * kb, sn * kb});
+      if (hv) sends.push_back({p, vals + cut(me, p), sn * 4});
     }
     if (rn) {
-      NC(g_nccl.Recv((char*)rk + roff[p] * kb, rn * kb, ncclUint8, p, c->nc, s));
-      if (hv) NC(g_nccl.Recv(rv + roff[p], rn * 4, ncclUint8, p, c->nc, s));
+      recvs.push_back({p, (char*)rk + roff[p] * kb, rn * kb});
+      if (hv) recvs.push_back({p, rv + roff[p], rn * 4});
     }
   }
-  NC(g_nccl.GroupEnd());
+  VK(tp_exchange(c, sends, recvs, s));
   // 5. stable merge of the received pieces (ties to the lower source rank)
   std::vector<uint64_t> starts;
   for (int q = 0; q < g; ++q)
@@ -381,7 +667,7 @@ vmps_status_t vmps_comm_init(vmps_comm_t* h_out, int rank, int world, const void
   CK(cudaSetDevice(device));
   ncclUniqueId id;
   memcpy(&id, h_id128, sizeof(id));
-  vmps_comm_s* c = new vmps_comm_s{nullptr, rank, world, device};
+  vmps_comm_s* c = new vmps_comm_s{0, nullptr, nullptr, rank, world, device, false};
   ncclResult_t r = g_nccl.CommInitRank(&c->nc, world, id, rank);
   if (r != ncclSuccess) {
     c_err = std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(r);
@@ -394,9 +680,121 @@ vmps_status_t vmps_comm_init(vmps_comm_t* h_out, int rank, int world, const void
 
 vmps_status_t vmps_comm_destroy(vmps_comm_t c) {
   if (!c) return VMPS_OK;
-  ncclResult_t r = g_nccl.ok ? g_nccl.CommDestroy(c->nc) : ncclSuccess;
+  ncclResult_t r = ncclSuccess;
+  if (c->kind == 0 && g_nccl.ok) r = c->aborted ? ncclSuccess : g_nccl.CommDestroy(c->nc);
   delete c;
   if (r != ncclSuccess) { c_err = "ncclCommDestroy failed"; return VMPS_ERR_NCCL; }
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_local_group_create(int world, int device, void** h_group) {
+  if (!h_group || world < 1 || world > LG_MAXW) return VMPS_ERR_INVALID_ARG;
+  CK(cudaSetDevice(device));
+  LocalGroup* g = new LocalGroup();
+  g->world = world;
+  g->timeout_s = comm_timeout_s();
+  g->sends.assign(world, {});
+  g->bc.assign(world, {});
+  g->tmp_cap = 64 * 1024;
+  for (int q = 0; q < world; ++q) {
+    g->ptr[q] = nullptr;
+    g->bytes[q] = 0;
+    if (cudaEventCreateWithFlags(&g->ev_ready[q], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_done[q], cudaEventDisableTiming) != cudaSuccess ||
+        cudaMalloc((void**)&g->tmp[q], g->tmp_cap) != cudaSuccess) {
+      c_err = "virtual-rank group: CUDA resources";
+      return VMPS_ERR_CUDA;
+    }
+  }
+  *h_group = g;
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_local_group_destroy(void* group) {
+  LocalGroup* g = (LocalGroup*)group;
+  if (!g) return VMPS_OK;
+  cudaDeviceSynchronize();
+  for (int q = 0; q < g->world; ++q) {
+    cudaEventDestroy(g->ev_ready[q]);
+    cudaEventDestroy(g->ev_done[q]);
+    cudaFree(g->tmp[q]);
+  }
+  delete g;
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_comm_init_local(vmps_comm_t* h_out, int rank, void* group, int device) {
+  LocalGroup* g = (LocalGroup*)group;
+  if (!h_out || !g || rank < 0 || rank >= g->world) return VMPS_ERR_INVALID_ARG;
+  CK(cudaSetDevice(device));
+  *h_out = new vmps_comm_s{1, nullptr, g, rank, g->world, device, false};
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_dist_cuts_workspace_bytes(int world, size_t* h_bytes) {
+  if (!h_bytes || world < 1) return VMPS_ERR_INVALID_ARG;
+  const size_t np = (size_t)15 * std::max(world - 1, 1);
+  *h_bytes = 3 * al(np * 8) + al(2 * np * 8) + al(((size_t)world + 1) * std::max<size_t>(64, 2 * (size_t)world) * 8) + 256;
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_dist_cuts(vmps_comm_t c, const void* keys, uint64_t n_local, vmps_key_t kt, uint64_t* h_cut,
+                             uint64_t* h_sizes, uint32_t* h_rounds, void* ws, size_t ws_bytes, void* stream) {
+  if (!c || !h_cut || (n_local && !keys)) return VMPS_ERR_INVALID_ARG;
+  if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
+  size_t need = 0;
+  vmps_dist_cuts_workspace_bytes(c->world, &need);
+  if (!ws || ws_bytes < need) { c_err = "workspace too small (vmps_dist_cuts_workspace_bytes)"; return VMPS_ERR_BUDGET; }
+  c_err.clear();
+  const size_t np = (size_t)15 * std::max(c->world - 1, 1);
+  Carve cv(ws, ws_bytes);
+  uint64_t* d_probe = (uint64_t*)cv.take(np * 8);
+  uint64_t* d_lt = (uint64_t*)cv.take(np * 8);
+  uint64_t* d_le = (uint64_t*)cv.take(np * 8);
+  uint64_t* d_cnt = (uint64_t*)cv.take(2 * np * 8);
+  uint64_t* d_small = (uint64_t*)cv.take(((size_t)c->world + 1) * std::max<size_t>(64, 2 * (size_t)c->world) * 8);
+  if (!d_small) { c_err = "workspace carve"; return VMPS_ERR_BUDGET; }
+  std::vector<uint64_t> sizes, cut;
+  uint32_t rounds = 0;
+  const vmps_status_t rc = fail_group(c, dist_cuts(c, keys, n_local, kt, d_probe, d_lt, d_le, d_cnt, d_small, np,
+                                                   (cudaStream_t)stream, &sizes, &cut, &rounds));
+  if (rc != VMPS_OK) return rc;
+  memcpy(h_cut, cut.data(), cut.size() * 8);
+  if (h_sizes) memcpy(h_sizes, sizes.data(), sizes.size() * 8);
+  if (h_rounds) *h_rounds = rounds;
+  return VMPS_OK;
+}
+
+// ---- host-side protocol arithmetic (see the functions above) ----
+vmps_status_t vmps_splitter_probes(uint32_t m, const uint64_t* h_lo, const uint64_t* h_hi, uint64_t* h_probe,
+                                   uint32_t* h_base, uint32_t* h_nprobe) {
+  if ((m && (!h_lo || !h_hi || !h_probe)) || !h_base || !h_nprobe) return VMPS_ERR_INVALID_ARG;
+  std::vector<uint64_t> pr;
+  std::vector<uint32_t> base;
+  splitter_probes(m, h_lo, h_hi, &pr, &base);
+  if (!pr.empty()) memcpy(h_probe, pr.data(), pr.size() * 8);
+  memcpy(h_base, base.data(), base.size() * 4);
+  *h_nprobe = (uint32_t)pr.size();
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_splitter_update(uint32_t m, uint64_t* h_lo, uint64_t* h_hi, const uint64_t* h_R,
+                                   const uint64_t* h_probe, const uint32_t* h_base, const uint64_t* h_le_sum) {
+  if (m && (!h_lo || !h_hi || !h_R || !h_base)) return VMPS_ERR_INVALID_ARG;
+  splitter_update(m, h_lo, h_hi, h_R, h_probe, h_base, h_le_sum);
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_split_points(uint32_t g, uint64_t R, const uint64_t* h_lt, const uint64_t* h_le, uint64_t* h_cut) {
+  if (!g || !h_lt || !h_le || !h_cut) return VMPS_ERR_INVALID_ARG;
+  split_points(g, R, h_lt, h_le, h_cut);
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_compose_tables(uint32_t g, uint32_t ns, const uint64_t* h_tables, const uint64_t* h_sizes,
+                                  uint32_t* h_entry, uint64_t* h_count) {
+  if (!g || !h_tables || !h_sizes || !h_entry || !h_count) return VMPS_ERR_INVALID_ARG;
+  compose_tables(g, ns, h_tables, h_sizes, h_entry, h_count);
   return VMPS_OK;
 }
 
@@ -451,14 +849,16 @@ vmps_status_t vmps_dist_workspace_bytes(uint64_t n_local, vmps_key_t kt, int has
 
 vmps_status_t vmps_sort_keys_dist(vmps_comm_t c, void* keys, uint64_t n_local, vmps_key_t kt, int64_t scratch_elems,
                                   void* ws, size_t ws_bytes, void* stream, vmps_stats_t* h_stats) {
-  return sort_dist_any(c, keys, nullptr, n_local, kt, scratch_elems, ws, ws_bytes, (cudaStream_t)stream, h_stats);
+  return fail_group(c, sort_dist_any(c, keys, nullptr, n_local, kt, scratch_elems, ws, ws_bytes, (cudaStream_t)stream,
+                                     h_stats, false));
 }
 
 vmps_status_t vmps_sort_pairs_dist(vmps_comm_t c, void* keys, uint32_t* vals, uint64_t n_local, vmps_key_t kt,
                                    int64_t scratch_elems, void* ws, size_t ws_bytes, void* stream,
                                    vmps_stats_t* h_stats) {
-  if (!vals) { c_err = "vals is NULL (use vmps_sort_keys_dist)"; return VMPS_ERR_INVALID_ARG; }
-  return sort_dist_any(c, keys, vals, n_local, kt, scratch_elems, ws, ws_bytes, (cudaStream_t)stream, h_stats);
+  if (!vals && n_local) { c_err = "vals is NULL (use vmps_sort_keys_dist)"; return fail_group(c, VMPS_ERR_INVALID_ARG); }
+  return fail_group(c, sort_dist_any(c, keys, vals, n_local, kt, scratch_elems, ws, ws_bytes, (cudaStream_t)stream,
+                                     h_stats, true));
 }
 
 vmps_status_t vmps_merge_plan_dist_workspace_bytes(uint64_t n_total, uint64_t n_local, vmps_key_t kt, int world,
@@ -468,10 +868,31 @@ vmps_status_t vmps_merge_plan_dist_workspace_bytes(uint64_t n_total, uint64_t n_
   return VMPS_OK;
 }
 
+vmps_status_t vmps_merge_plan_dist_capacity(uint64_t n_total, uint64_t n_local, uint64_t* h_cap) {
+  if (!h_cap || n_local > n_total) return VMPS_ERR_INVALID_ARG;
+  // runs starting in the shard: all but the array's last run have >= minrun
+  // keys, and merges with j in the shard are at most as many
+  *h_cap = n_local / minrun_of(std::max<uint64_t>(n_total, 1)) + 2;
+  return VMPS_OK;
+}
+
+static vmps_status_t merge_plan_dist_impl(vmps_comm_t c, const void* keys, uint64_t n_local, vmps_key_t kt,
+                                          uint64_t* run_start, uint8_t* run_kind, vmps_merge_rec_t* merges,
+                                          uint64_t cap_runs, uint64_t* h_num_runs_local,
+                                          uint64_t* h_num_merges_local, void* ws, size_t ws_bytes, void* stream);
+
 vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_local, vmps_key_t kt,
                                    uint64_t* run_start, uint8_t* run_kind, vmps_merge_rec_t* merges,
                                    uint64_t cap_runs, uint64_t* h_num_runs_local, uint64_t* h_num_merges_local,
                                    void* ws, size_t ws_bytes, void* stream) {
+  return fail_group(c, merge_plan_dist_impl(c, keys, n_local, kt, run_start, run_kind, merges, cap_runs,
+                                            h_num_runs_local, h_num_merges_local, ws, ws_bytes, stream));
+}
+
+static vmps_status_t merge_plan_dist_impl(vmps_comm_t c, const void* keys, uint64_t n_local, vmps_key_t kt,
+                                          uint64_t* run_start, uint8_t* run_kind, vmps_merge_rec_t* merges,
+                                          uint64_t cap_runs, uint64_t* h_num_runs_local,
+                                          uint64_t* h_num_merges_local, void* ws, size_t ws_bytes, void* stream) {
   if (!c || !h_num_runs_local || !h_num_merges_local) return VMPS_ERR_INVALID_ARG;
   if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
   if (n_local > VMPS_MAX_N) { c_err = "n_local > VMPS_MAX_N"; return VMPS_ERR_INVALID_ARG; }
@@ -486,8 +907,9 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
     d_small0 = (uint64_t*)pre.take(((size_t)g + 1) * 64 * 8);
     if (!d_small0) { c_err = "workspace too small"; return VMPS_ERR_BUDGET; }
   }
+  c_err.clear();
   std::vector<uint64_t> sizes;
-  VK(gather_host<uint64_t>(c, &n_local, 1, &sizes, d_small0, s));
+  VK(gather_host(c, &n_local, 1, &sizes, d_small0, s));
   std::vector<uint64_t> off(g + 1, 0);
   for (int q = 0; q < g; ++q) off[q + 1] = off[q] + sizes[q];
   const uint64_t N = off[g];
@@ -516,7 +938,7 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
     CK(cudaMemcpyAsync(mine, keys, h * kb, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(mine + (size_t)H * kb, (const char*)keys + (n_local - 1) * kb, kb, cudaMemcpyDeviceToDevice, s));
   }
-  NC(g_nccl.AllGather(mine, d_edges, eb, ncclUint8, c->nc, s));
+  VK(tp_allgather(c, mine, d_edges, eb, s));
   int pq = -1;
   for (int q = me - 1; q >= 0; --q)
     if (sizes[q]) { pq = q; break; }
@@ -537,20 +959,13 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
                         std::max(L.shard_ws, L.plan_ws), s));
   else
     CK(cudaMemsetAsync(tmine, 0, (size_t)ns * 8, s));
-  NC(g_nccl.AllGather(tmine, d_tabs, (size_t)ns * 8, ncclUint8, c->nc, s));
+  VK(tp_allgather(c, tmine, d_tabs, (size_t)ns * 8, s));
   std::vector<uint64_t> tabs((size_t)g * ns);
   CK(cudaMemcpyAsync(tabs.data(), d_tabs, tabs.size() * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
+  VK(tp_sync(c, s));
   std::vector<uint64_t> cnt(g, 0);
   std::vector<uint32_t> entry(g, 0);
-  uint32_t st = 0;  // START(0)
-  for (int q = 0; q < g; ++q) {
-    entry[q] = st;
-    if (!sizes[q] || st == 255u) continue;
-    const uint64_t v = tabs[(size_t)q * ns + st];
-    cnt[q] = v & 0xFFFFFFFFull;
-    st = (uint32_t)(v >> 32);
-  }
+  compose_tables((uint32_t)g, ns, tabs.data(), sizes.data(), entry.data(), cnt.data());
   std::vector<uint64_t> roff(g + 1, 0);
   for (int q = 0; q < g; ++q) roff[q + 1] = roff[q] + cnt[q];
   const uint64_t r = roff[g];
@@ -559,13 +974,15 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
     VK(vmps_shard_runs(keys, n_local, kt, mr, n_end, d_prev, nh ? d_halo : nullptr, nh, entry[me], cnt[me], off[me],
                        d_runs + roff[me], d_kinds + roff[me], shard_ws, std::max(L.shard_ws, L.plan_ws), s));
   // every rank's run list to every rank, in place, rank order
-  NC(g_nccl.GroupStart());
-  for (int q = 0; q < g; ++q) {
-    if (!cnt[q]) continue;
-    NC(g_nccl.Broadcast(d_runs + roff[q], d_runs + roff[q], cnt[q], ncclUint64, q, c->nc, s));
-    NC(g_nccl.Broadcast(d_kinds + roff[q], d_kinds + roff[q], cnt[q], ncclUint8, q, c->nc, s));
+  {
+    std::vector<BItem> items;
+    for (int q = 0; q < g; ++q) {
+      if (!cnt[q]) continue;
+      items.push_back({d_runs + roff[q], cnt[q] * 8, q});
+      items.push_back({d_kinds + roff[q], cnt[q], q});
+    }
+    VK(tp_bcast_many(c, items, s));
   }
-  NC(g_nccl.GroupEnd());
   CK(cudaMemcpyAsync(d_runs + r, &N, 8, cudaMemcpyHostToDevice, s));
   // this rank's runs
   if (cnt[me] > cap_runs) { c_err = "cap_runs too small"; *h_num_runs_local = cnt[me]; return VMPS_ERR_INVALID_ARG; }
@@ -583,7 +1000,7 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
     size_t tmp = L.sel_tmp;
     CK(cub::DeviceSelect::If(d_sel, tmp, d_recs, d_nsel, (int64_t)(r - 1), InShard{off[me], off[me] + n_local}, s));
     CK(cudaMemcpyAsync(&nm, d_nsel, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    VK(tp_sync(c, s));
     if (nm > cap_runs) { c_err = "cap_runs too small for the merges"; *h_num_merges_local = nm; return VMPS_ERR_INVALID_ARG; }
     if (nm) {
       if (!merges) return VMPS_ERR_INVALID_ARG;
@@ -591,8 +1008,7 @@ vmps_status_t vmps_merge_plan_dist(vmps_comm_t c, const void* keys, uint64_t n_l
     }
   }
   *h_num_merges_local = nm;
-  CK(cudaStreamSynchronize(s));
-  return VMPS_OK;
+  return tp_sync(c, s);
 }
 
 }  // extern "C"

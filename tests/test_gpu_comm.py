@@ -1,9 +1,12 @@
 """GPU tests of the native multi-GPU entry points (csrc/comm.cu) through the
-C ABI, at world size 1 (one GPU per process; NCCL refuses two ranks on one
-device): vmps_sort_*_dist equals the oracle's stable sort, vmps_merge_plan_dist
-equals the oracle's plan (every run and merge belongs to the single shard,
-`order` = execution rank), and the workspace / argument errors.  The
-multi-rank protocol logic is exercised with gloo in tests/test_dist.py."""
+C ABI: at world size 1 over NCCL (one GPU per process; NCCL refuses two ranks
+on one device), and with g = 2..8 virtual ranks on one GPU (threads of this
+process, vmps_local_group: the same protocol, collectives over barriers,
+events and device copies).  vmps_sort_*_dist equals the oracle's stable sort
+of the concatenated shards (rank p keeps global output ranks [off_p, off_p +
+n_p)), vmps_merge_plan_dist's per-rank pieces are the oracle's plan of the
+whole array, vmps_dist_cuts' table matches its definition; a rank that never
+joins makes the others fail with VMPS_ERR_NCCL after the timeout."""
 import numpy as np
 import pytest
 import torch
@@ -77,3 +80,165 @@ def test_dist_errors(comm):
     assert rc == vm.ERR_INVALID_ARG
     nb = ctypes.c_size_t(0)
     assert L.vmps_dist_workspace_bytes(1024, vm.KEY_U32, 0, 0, -1, ctypes.byref(nb)) == vm.ERR_INVALID_ARG
+
+
+# ---- virtual ranks: the native protocol with g ranks on one GPU ----
+
+def _shards(rng, sizes, dtype):
+    out = []
+    for n in sizes:
+        if dtype == np.float32:
+            k = rng.standard_normal(n).astype(np.float32)
+            m = rng.random(n) < 0.3  # ties, signed zeros and NaNs across shards
+            k[m] = rng.choice(np.array([0.0, -0.0, 1.5, -2.0, np.nan, 3.0], np.float32), int(m.sum()))
+        elif dtype == np.uint64:
+            k = (rng.integers(0, 9, n).astype(np.uint64) << np.uint64(40)) | rng.integers(0, 3, n).astype(np.uint64)
+        else:
+            k = rng.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32)
+            k[: n // 3] = rng.integers(0, 7, n // 3)  # ties across shards
+            k[n // 3: n // 2] = np.sort(k[n // 3: n // 2])
+        out.append(k)
+    return out
+
+
+@pytest.mark.parametrize("g,dtype,sizes", [
+    (2, np.uint32, [200_000, 150_001]),
+    (3, np.uint64, [70_000, 0, 123_457]),          # an empty shard
+    (4, np.float32, [50_000, 50_000, 3, 90_000]),  # a tiny shard
+    (8, np.uint32, [40_000 + 1000 * q for q in range(8)]),
+])
+def test_sort_dist_virtual_ranks(g, dtype, sizes):
+    import paper_2605_27147_b200 as vm
+    from tests import vranks
+    rng = np.random.default_rng(g * 7 + len(sizes))
+    ks = _shards(rng, sizes, dtype)
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    vs = [np.arange(offs[q], offs[q + 1], dtype=np.uint32) for q in range(g)]
+
+    def fn(rank, comm):
+        kd = W.from_numpy(ks[rank], "cuda")
+        vd = W.from_numpy(vs[rank], "cuda")
+        vm.sort_dist_native_(comm, kd, vd)
+        return W.to_numpy(kd), W.to_numpy(vd)
+
+    outs = vranks.run(g, fn)
+    ko, vo, _, _ = oracle.sort(np.concatenate(ks), np.concatenate(vs))
+    for q in range(g):
+        assert len(outs[q][0]) == sizes[q]
+    assert np.concatenate([o[0] for o in outs]).view(np.uint8).tobytes() == ko.view(np.uint8).tobytes()
+    assert (np.concatenate([o[1] for o in outs]) == vo).all()
+
+
+def test_sort_dist_virtual_ranks_cfg5():
+    """cfg5-shaped shards (2^20 per rank, 4 ranks, payload = global index), keys only and pairs."""
+    import paper_2605_27147_b200 as vm
+    from tests import vranks
+    g, n = 4, 1 << 20
+    sh = [W.cfg5(n=n, device="cpu", rank=q) for q in range(g)]
+    ks = [W.to_numpy(k) for k, _ in sh]
+    vs = [W.to_numpy(v) for _, v in sh]
+
+    def fn(rank, comm):
+        kd = W.from_numpy(ks[rank], "cuda")
+        vd = W.from_numpy(vs[rank], "cuda")
+        vm.sort_dist_native_(comm, kd, vd)
+        k2 = W.from_numpy(ks[rank], "cuda")
+        vm.sort_dist_native_(comm, k2)
+        return W.to_numpy(kd), W.to_numpy(vd), W.to_numpy(k2)
+
+    outs = vranks.run(g, fn)
+    ko, vo, _, _ = oracle.sort(np.concatenate(ks), np.concatenate(vs))
+    assert (np.concatenate([o[0] for o in outs]) == ko).all()
+    assert (np.concatenate([o[1] for o in outs]) == vo).all()
+    assert (np.concatenate([o[2] for o in outs]) == ko).all()
+
+
+@pytest.mark.parametrize("g,n,seed", [(2, 300_000, 1), (5, 1_000_003, 2), (8, 2_000_000, 3)])
+def test_merge_plan_dist_virtual_ranks(g, n, seed):
+    """Each rank's runs and merges (j in its shard) are exactly its part of the
+    oracle's plan of the whole array, with the global execution rank."""
+    import paper_2605_27147_b200 as vm
+    from tests import vranks
+    rng = np.random.default_rng(seed)
+    x = rng.integers(0, 1 << 20, n)
+    cuts = np.sort(rng.integers(0, n, max(2, n // 500)))
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        x[a:b] = np.sort(x[a:b])[::-1] if rng.random() < 0.3 else np.sort(x[a:b])
+    glob = x.astype(np.uint32)
+    edges = [0] + sorted(set(int(c) for c in rng.integers(1, n, g - 1))) + [n]
+    while len(edges) < g + 1:
+        edges.insert(1, edges[1])  # repeated cut: an empty shard
+    shards = [glob[a:b].copy() for a, b in zip(edges[:-1], edges[1:])]
+
+    def fn(rank, comm):
+        p = vm.merge_plan_dist_native(comm, W.from_numpy(shards[rank], "cuda"), n)
+        return p.run_start.cpu().numpy(), p.run_kind.cpu().numpy(), p.merges.cpu().numpy()
+
+    outs = vranks.run(g, fn)
+    oplan, _ = oracle.plan(glob)
+    rs = np.concatenate([o[0] for o in outs])
+    rk = np.concatenate([o[1] for o in outs])
+    assert (rs == oplan.run_start.astype(np.int64)).all()
+    assert (rk == oplan.run_kind).all()
+    mg = np.concatenate([o[2] for o in outs if len(o[2])])
+    mg = mg[np.argsort(mg[:, 4])]
+    om = np.stack([oplan.merges["i"], oplan.merges["j"], oplan.merges["k"], oplan.merges["power"]], axis=1)
+    assert (mg[:, 4] == np.arange(len(om))).all()
+    assert (mg[:, :4] == om.astype(np.int64)).all()
+
+
+def test_dist_cuts_virtual_ranks():
+    """vmps_dist_cuts on sorted shards: every rank gets the same table, whose
+    column t sums to off_t and whose pieces are exactly the global ranks."""
+    import paper_2605_27147_b200 as vm
+    from tests import vranks
+    g = 3
+    rng = np.random.default_rng(5)
+    sizes = [5000, 7000, 4000]
+    ks = [np.sort(rng.integers(0, 50, s).astype(np.uint32)) for s in sizes]
+
+    def fn(rank, comm):
+        return vm.dist_cuts(comm, W.from_numpy(ks[rank], "cuda"))
+
+    outs = vranks.run(g, fn)
+    cut, szs, rounds = outs[0]
+    assert all(o[0] == cut and o[1] == sizes for o in outs)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    allk = np.concatenate(ks)
+    order = np.argsort(allk, kind="stable")
+    owner = np.concatenate([np.full(s, q) for q, s in enumerate(sizes)])
+    local = np.concatenate([np.arange(s) for s in sizes])
+    for t in range(g + 1):
+        assert sum(cut[q][t] for q in range(g)) == off[t]
+    for p in range(g):  # rank p's output = its pieces, in global stable order
+        got = sorted((q, i) for q in range(g) for i in range(cut[q][p], cut[q][p + 1]))
+        want = sorted(zip(owner[order[off[p]:off[p + 1]]], local[order[off[p]:off[p + 1]]]))
+        assert got == want
+
+
+def test_virtual_rank_timeout(monkeypatch):
+    """A rank that never joins the collective: the others return
+    VMPS_ERR_NCCL (5) after VMPS_COMM_TIMEOUT_S instead of hanging."""
+    import threading
+
+    import paper_2605_27147_b200 as vm
+    monkeypatch.setenv("VMPS_COMM_TIMEOUT_S", "2")
+    group = vm.LocalGroup(2, 0)
+    c0 = vm.Comm.local(0, group)
+    res = {}
+
+    def body():
+        try:
+            kd = torch.arange(10000, 0, -1, dtype=torch.int32, device="cuda").view(torch.uint32)
+            vm.sort_dist_native_(c0, kd)
+        except vm.VmpsError as e:
+            res["status"] = e.status
+            res["msg"] = str(e)
+
+    t = threading.Thread(target=body)
+    t.start()
+    t.join(60)
+    assert not t.is_alive()
+    assert res.get("status") == 5, res
+    c0.destroy()
+    group.destroy()

@@ -2,9 +2,10 @@
 the concatenation of g shards, each shard processed on its own by the real
 kernels (vmps_shard_chain / vmps_shard_runs, host composition of the transfer
 tables, vmps_plan_from_runs), vs the oracle's plan-only pass over the whole
-array -- run starts, kinds and the merge records, exact.  Virtual ranks on one
-GPU (dist.merge_plan_shards); the collective version is covered by
-tests/test_dist.py with gloo.
+array -- run starts, kinds and the merge records, exact.  g virtual ranks on
+one GPU run the library's own protocol (vmps_merge_plan_dist over a
+vmps_local_group, tests/vranks.py): each rank's runs and merges are its part
+of the whole plan.
 
 Cuts are placed where the chain is hardest: inside long ascending and
 strictly descending runs, inside a minrun-forced extension, on run-detection
@@ -44,23 +45,40 @@ def _runs_array(rng, n, dtype, desc_p=0.4, nseg=None):
     return x.astype(np.uint32)
 
 
+class _Res:
+    pass
+
+
 def _check(vm, glob, cuts):
-    from paper_2605_27147_b200.dist import merge_plan_shards
+    from tests import vranks
     edges = [0] + sorted(cuts) + [len(glob)]
-    shards = [W.from_numpy(glob[a:b].copy(), "cuda") for a, b in zip(edges[:-1], edges[1:])]
-    res = merge_plan_shards(shards)
-    torch.cuda.synchronize()
+    shards = [glob[a:b].copy() for a, b in zip(edges[:-1], edges[1:])]
+    n = len(glob)
+
+    def fn(rank, comm):
+        p = vm.merge_plan_dist_native(comm, W.from_numpy(shards[rank], "cuda"), n)
+        return p.run_start.cpu().numpy(), p.run_kind.cpu().numpy(), p.merges.cpu().numpy()
+
+    outs = vranks.run(len(shards), fn)
     oplan, _ = oracle.plan(glob)
     ors = oplan.run_start.astype(np.int64)
-    got = res.run_start.cpu().numpy()
+    got = np.concatenate([o[0] for o in outs])
     assert len(got) == len(ors), f"run count {len(got)} vs {len(ors)}"
     assert (got == ors).all(), "run starts differ"
-    assert (res.run_kind.cpu().numpy() == oplan.run_kind).all(), "run kinds differ"
+    assert (np.concatenate([o[1] for o in outs]) == oplan.run_kind).all(), "run kinds differ"
     om = np.stack([oplan.merges["i"], oplan.merges["j"], oplan.merges["k"], oplan.merges["power"]],
                   axis=1).astype(np.int64)
-    assert (res.merges.cpu().numpy() == om).all(), "merge plan differs"
+    ms = [o[2] for o in outs if len(o[2])]
+    mg = np.concatenate(ms) if ms else np.zeros((0, 5), np.int64)
+    mg = mg[np.argsort(mg[:, 4], kind="stable")]
+    assert (mg[:, 4] == np.arange(len(om))).all(), "execution ranks differ"
+    assert (mg[:, :4] == om).all(), "merge plan differs"
+    res = _Res()
+    res.counts = [len(o[0]) for o in outs]
     for q, (a, b) in enumerate(zip(edges[:-1], edges[1:])):
         assert res.counts[q] == int(((ors >= a) & (ors < b)).sum())
+    res.run_start = torch.from_numpy(got)
+    res.merges = torch.from_numpy(mg[:, :4].copy())
     return res
 
 
