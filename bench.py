@@ -594,24 +594,35 @@ def main():
         del hk, hvv, ok_, ov_
 
     bounded = None
-    if world == 1 and args.bounded_reps > 0 and hv:
+    if args.bounded_reps > 0 and hv:
         import math
         S = int(4 * math.sqrt(n * math.log2(n)))
         restore()
         bws = vm.Workspace()
-        bst = vm.sort_(keys, vals, scratch=S, stats=True, workspace=bws)  # warm-up + stats
+
+        def bsort(st=False):
+            if world > 1:  # per-GPU cap, exchange staging included (merge-split protocol, comm.cu)
+                from paper_2605_27147_b200 import dist as vdist
+                return vdist.sort_dist_(keys, vals, comm=ncomm, workspace=bws, scratch=S, stats=st)
+            return vm.sort_(keys, vals, scratch=S, stats=st, workspace=bws)
+
+        bst = bsort(True)  # warm-up + stats
         bt = []
         for _ in range(args.bounded_reps):
             restore()
+            barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            vm.sort_(keys, vals, scratch=S, workspace=bws)
+            bsort()
             e1.record(stream)
             e1.synchronize()
             bt.append(e0.elapsed_time(e1))
-        bms = statistics.mean(bt)
-        bounded = {"scratch_cap_elems": S, "c": 4, "ms_per_step": bms, "value": n / (bms / 1000) / 1e9,
+        tb = torch.tensor([statistics.mean(bt)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        bms = float(tb.item())
+        bounded = {"scratch_cap_elems": S, "c": 4, "ms_per_step": bms, "value": n_total / (bms / 1000) / 1e9,
                    "unit": UNIT, "slowdown_vs_unbounded": bms / ms,
                    "scratch_bytes": bst["scratch_bytes"], "metadata_bytes": bst["metadata_bytes"],
                    "peak_extra_device_bytes": bst["peak_extra_device_bytes"],

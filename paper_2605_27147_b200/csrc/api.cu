@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges per phase (no link dependency)
+
 #include "bounded.cuh"
 #include "engine.cuh"
 #include "engine4.cuh"
@@ -42,6 +44,15 @@ static int g_prof_nm = 0, g_prof_np = 0;
 static int g_prof_mark[4] = {-1, -1, -1, -1};  // begin, after plan, after leaf, end
 static unsigned long long* g_prof_host = nullptr;  // pinned copy of counters
 static int g_prof_wbytes = 0;
+
+// NVTX ranges around the host-side enqueue of each phase (visible to
+// Nsight tools; `ncu --nvtx --nvtx-include "vmps_sort/vmps_merge/"` selects a phase).
+struct NvtxRange {
+  bool on = true;
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  void end() { if (on) { nvtxRangePop(); on = false; } }
+  ~NvtxRange() { end(); }
+};
 
 static int prof_event(cudaStream_t s) {
   if (!g_prof || g_ev_n >= 256) return -1;
@@ -256,7 +267,8 @@ static int dev_slot() {
   if (cudaGetDevice(&d) != cudaSuccess || d < 0) d = 0;
   return d % MAX_DEV;
 }
-static cudaStream_t g_aux[MAX_DEV];
+// per thread: concurrent sorts on different threads capture their own graphs
+static thread_local cudaStream_t g_aux[MAX_DEV];
 static cudaStream_t aux_stream() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev >= MAX_DEV) return nullptr;
@@ -543,6 +555,8 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
                                vmps_stats_t* st) {
   using K = typename KeyTraits<KT>::K;
   prof_reset();
+  NvtxRange nv_sort("vmps_sort");
+  NvtxRange nv_plan("vmps_plan");
   g_prof_mark[0] = prof_event(s);
   vmps_status_t rc = front_half<KT>(w, keys, s);
   if (rc != VMPS_OK) return rc;
@@ -578,8 +592,10 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   rc = launch_check();
   if (rc != VMPS_OK) return rc;
   g_prof_mark[1] = prof_event(s);
+  nv_plan.end();
 
   // leaf engine
+  NvtxRange nv_leaf("vmps_leaf");
   K* k0 = (K*)keys;
   K* k1 = (K*)w.k1;
   uint32_t* v0 = vals;
@@ -617,6 +633,8 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   rc = launch_check();
   if (rc != VMPS_OK) return rc;
   g_prof_mark[2] = prof_event(s);
+  nv_leaf.end();
+  NvtxRange nv_merge("vmps_merge");
 
   // level merges, highest power first (children before parents, F3)
   double lg = std::log2(2.0 * (double)w.n / (double)w.fuse_z);

@@ -37,6 +37,7 @@
 #include <vector>
 
 #include <cub/device/device_select.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/vmps.h"
 
@@ -327,7 +328,11 @@ vmps_status_t tp_exchange(vmps_comm_t c, const std::vector<P2P>& sends, const st
     for (size_t i = 0; i < sq.size(); ++i)
       if ((int)(sq[i].second & 0xFF) == c->rank && k-- == 0) { hit = (int)i; break; }
     if (hit < 0 || (sq[hit].second >> 8) != x.bytes) {
-      c_err = "virtual-rank group: unmatched send / receive";
+      c_err = "virtual-rank group: unmatched send / receive (rank " + std::to_string(c->rank) + " from " +
+              std::to_string(x.peer) + ", " + std::to_string(x.bytes) + " bytes; the peer posted " +
+              std::to_string(sq.size()) + " sends" +
+              (sq.empty() ? std::string() : ", first " + std::to_string(sq[0].second >> 8) + " bytes to " +
+                                                std::to_string(sq[0].second & 0xFF)) + ")";
       return VMPS_ERR_INTERNAL;
     }
     if (x.bytes) CK(cudaMemcpyAsync((void*)x.p, sq[hit].first, x.bytes, cudaMemcpyDeviceToDevice, s));
@@ -544,10 +549,215 @@ vmps_status_t fail_group(vmps_comm_t c, vmps_status_t rc) {
   return rc;
 }
 
+// ---------------------------------------------------------------------------
+// Scratch-bounded distributed sort (second half): every
+// rank's extra element memory stays within its cap S (c sqrt(n log n) per GPU,
+// exchange staging included).  There is no receive buffer: after the local
+// scratch-bounded sort, adjacent ranks repeat stable merge-splits
+// (odd-even transposition over the rank order).  In a merge-split of ranks
+// a < b = a + 1 holding sorted A and B, the pair finds by the same 16-ary
+// search the cut c = #A among the first |A| outputs of the stable merge of A B
+// (ties to A); a's tail A[c, |A|) and b's head B[0, |A| - c) swap
+// places in chunks of S/2 elements through staging (out + in = S), and each
+// rank then holds two sorted runs, merged by its local scratch-bounded sort.
+// Each step is a stable merge of two adjacent segments of the rank-ordered
+// sequence, so equal keys never change their relative order; phases repeat
+// until an even and an odd phase swap nothing, i.e. every adjacent pair is in
+// order: the unique stable sort of the concatenation, each rank keeping its
+// element count.
+// ---------------------------------------------------------------------------
+struct BdLayout {
+  size_t sort_ws, stage, small, total;
+  uint64_t C;  // staging chunk (elements)
+};
+
+BdLayout bd_layout(uint64_t n_local, vmps_key_t kt, int hv, int world, int64_t S) {
+  BdLayout L{};
+  size_t b = 0;
+  vmps_workspace_bytes(std::max<uint64_t>(n_local, 1), kt, hv, S, &b);
+  L.C = std::max<uint64_t>(1, (uint64_t)S / 2);
+  const size_t w = kbytes(kt) + (hv ? 4 : 0);
+  L.stage = al(2 * L.C * w + 64);
+  L.sort_ws = al(b);
+  L.small = al(((size_t)world * 16 + 64) * 8) * 3;
+  L.total = std::max(L.sort_ws, L.stage) + L.small + 256;  // staging overlays the sort's workspace
+  return L;
+}
+
+// k_copy_u8: plain device copy within one stream (chunks of the swap)
+vmps_status_t d2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+  return VMPS_OK;
+}
+
+vmps_status_t sort_dist_bounded(vmps_comm_t c, void* keys, uint32_t* vals, uint64_t n_local, vmps_key_t kt,
+                                int64_t S, void* ws, size_t ws_bytes, cudaStream_t s, vmps_stats_t* h_stats,
+                                bool pairs) {
+  const int g = c->world, me = c->rank;
+  const int hv = pairs ? 1 : 0;
+  const size_t kb = kbytes(kt);
+  const BdLayout L = bd_layout(n_local, kt, hv, g, S);
+  if (!ws || ws_bytes < L.total) { c_err = "workspace too small (vmps_dist_workspace_bytes)"; return VMPS_ERR_BUDGET; }
+  Carve cv(ws, ws_bytes);
+  char* big = (char*)cv.take(std::max(L.sort_ws, L.stage));
+  uint64_t* d_vec = (uint64_t*)cv.take(L.small / 3);
+  uint64_t* d_probe = (uint64_t*)cv.take(L.small / 3);
+  uint64_t* d_cnt = (uint64_t*)cv.take(L.small / 3);
+  if (!d_cnt) { c_err = "workspace carve"; return VMPS_ERR_BUDGET; }
+  const size_t big_bytes = std::max(L.sort_ws, L.stage);
+  auto local_sort = [&](vmps_stats_t* st) -> vmps_status_t {
+    if (n_local <= 1) return VMPS_OK;
+    if (hv) return vmps_sort_pairs(keys, vals, n_local, kt, S, big, big_bytes, s, st);
+    return vmps_sort_keys(keys, n_local, kt, S, big, big_bytes, s, st);
+  };
+  VK(local_sort(h_stats));
+  if (g == 1) return VMPS_OK;
+  std::vector<uint64_t> sizes;
+  VK(gather_host(c, &n_local, 1, &sizes, d_vec, s));
+  const size_t NV = (size_t)g * 16 + 2;  // per pair (slot = lower rank): 15 probe counts; + flags
+  std::vector<uint64_t> h_vec(NV), h_probe;
+  // the transposition runs over the non-empty ranks in rank order (an empty
+  // rank holds nothing to order and just joins the collectives)
+  std::vector<int> ne;
+  int my_pos = -1;
+  for (int q = 0; q < g; ++q)
+    if (sizes[q]) {
+      if (q == me) my_pos = (int)ne.size();
+      ne.push_back(q);
+    }
+  // equal shards (BASELINE.json's configs) converge within g phases (block
+  // odd-even transposition); unequal ones need more, since a merge-split moves
+  // at most the smaller shard across a rank: the limit grows with max / min
+  uint64_t nmin = ~0ull, nmax = 0;
+  for (int q : ne) { nmin = std::min(nmin, sizes[q]); nmax = std::max(nmax, sizes[q]); }
+  const int max_phase = ne.empty() ? 2 : (int)std::min<uint64_t>(1u << 20, (uint64_t)g + 8 + 2 * ((nmax + nmin - 1) / nmin));
+  int quiet = 0;
+  for (int phase = 0; quiet < 2 && phase < max_phase; ++phase) {
+    int partner = -1;
+    if (my_pos >= 0) {
+      const int pp = ((my_pos + phase) % 2 == 0) ? my_pos + 1 : my_pos - 1;
+      if (pp >= 0 && pp < (int)ne.size()) partner = ne[pp];
+    }
+    const bool paired = partner >= 0;
+    const int lower = paired ? std::min(me, partner) : -1;
+    const int upper = paired ? std::max(me, partner) : -1;
+    const uint64_t nA = paired ? sizes[lower] : 0, nB = paired ? sizes[upper] : 0;
+    // splitter v*: the least image with #(A <= v) + #(B <= v) >= |A|
+    uint64_t lo = 0, hi = img_max(kt);
+    bool open = paired && nA > 0 && nB > 0;
+    for (;;) {
+      std::vector<uint32_t> base;
+      std::vector<uint64_t> pr;
+      if (open) splitter_probes(1, &lo, &hi, &pr, &base);
+      const bool active = open && !pr.empty();
+      std::fill(h_vec.begin(), h_vec.end(), 0);
+      h_vec[NV - 1] = active ? 1 : 0;
+      CK(cudaMemcpyAsync(d_vec, h_vec.data(), NV * 8, cudaMemcpyHostToDevice, s));
+      if (active && n_local) {
+        CK(cudaMemcpyAsync(d_probe, pr.data(), pr.size() * 8, cudaMemcpyHostToDevice, s));
+        VK(vmps_count_rank(keys, n_local, kt, d_probe, (uint32_t)pr.size(), d_cnt, d_vec + (size_t)lower * 16, s));
+      }
+      VK(tp_allreduce_u64(c, d_vec, NV, s));
+      CK(cudaMemcpyAsync(h_vec.data(), d_vec, NV * 8, cudaMemcpyDeviceToHost, s));
+      VK(tp_sync(c, s));
+      if (h_vec[NV - 1] == 0) break;  // no pair is still searching
+      if (active) {
+        const uint64_t R[1] = {nA};
+        splitter_update(1, &lo, &hi, R, pr.data(), base.data(), h_vec.data() + (size_t)lower * 16);
+        open = lo < hi;
+      }
+    }
+    // both partners' counts at v* -> the cut of A, the swap length, the chunk rounds
+    std::fill(h_vec.begin(), h_vec.end(), 0);
+    uint64_t lt = 0, le = 0;
+    if (paired && nA > 0 && nB > 0 && n_local) {
+      CK(cudaMemcpyAsync(d_probe, &lo, 8, cudaMemcpyHostToDevice, s));
+      VK(vmps_count_rank(keys, n_local, kt, d_probe, 1, d_cnt, d_cnt + 1, s));
+      uint64_t two[2];
+      CK(cudaMemcpyAsync(two, d_cnt, 16, cudaMemcpyDeviceToHost, s));
+      VK(tp_sync(c, s));
+      lt = two[0];
+      le = two[1];
+      const size_t o = (size_t)lower * 16 + (me == lower ? 0 : 2);
+      h_vec[o] = lt;
+      h_vec[o + 1] = le;
+    }
+    if (paired) h_vec[(size_t)lower * 16 + 4 + (me == lower ? 0 : 1)] = L.C;  // each side's staging chunk
+    CK(cudaMemcpyAsync(d_vec, h_vec.data(), NV * 8, cudaMemcpyHostToDevice, s));
+    VK(tp_allreduce_u64(c, d_vec, NV, s));
+    CK(cudaMemcpyAsync(h_vec.data(), d_vec, NV * 8, cudaMemcpyDeviceToHost, s));
+    VK(tp_sync(c, s));
+    uint64_t cnt = 0;
+    if (paired && nA > 0 && nB > 0) {
+      const uint64_t* q = h_vec.data() + (size_t)lower * 16;
+      const uint64_t ltv[2] = {q[0], q[2]}, lev[2] = {q[1], q[3]};
+      uint64_t cut[2];
+      split_points(2, nA, ltv, lev, cut);
+      cnt = nA - cut[0];  // A's tail that moves up = B's head that moves down
+    }
+    // the pair swaps in chunks both staging buffers hold (the caps may differ)
+    const uint64_t C = paired ? std::max<uint64_t>(1, std::min(h_vec[(size_t)lower * 16 + 4],
+                                                              h_vec[(size_t)lower * 16 + 5]))
+                              : L.C;
+    const uint64_t my_rounds = (cnt + C - 1) / C;
+    // every rank runs the same number of exchange rounds (empty when done)
+    std::fill(h_vec.begin(), h_vec.end(), 0);
+    h_vec[(size_t)me] = my_rounds;
+    h_vec[NV - 2] = cnt ? 1 : 0;
+    CK(cudaMemcpyAsync(d_vec, h_vec.data(), NV * 8, cudaMemcpyHostToDevice, s));
+    VK(tp_allreduce_u64(c, d_vec, NV, s));
+    CK(cudaMemcpyAsync(h_vec.data(), d_vec, NV * 8, cudaMemcpyDeviceToHost, s));
+    VK(tp_sync(c, s));
+    uint64_t rounds = 0;
+    for (int q = 0; q < g; ++q) rounds = std::max(rounds, h_vec[(size_t)q]);
+    const bool swapped = h_vec[NV - 2] != 0;
+    // my region of the swap: A[c, |A|) on the lower rank, B[0, cnt) on the upper
+    const uint64_t r0 = (me == lower) ? nA - cnt : 0;
+    char* sk_out = big;
+    char* sk_in = big + C * kb;
+    char* sv_out = big + 2 * C * kb;
+    char* sv_in = sv_out + C * 4;
+    for (uint64_t r = 0; r < rounds; ++r) {
+      std::vector<P2P> sends, recvs;
+      const uint64_t a = r * C, b = std::min(cnt, a + C);
+      if (a < b) {
+        const size_t m = b - a;
+        VK(d2d(sk_out, (const char*)keys + (r0 + a) * kb, m * kb, s));
+        sends.push_back({partner, sk_out, m * kb});
+        recvs.push_back({partner, sk_in, m * kb});
+        if (hv) {
+          VK(d2d(sv_out, vals + r0 + a, m * 4, s));
+          sends.push_back({partner, sv_out, m * 4});
+          recvs.push_back({partner, sv_in, m * 4});
+        }
+      }
+      VK(tp_exchange(c, sends, recvs, s));
+      if (a < b) {
+        const size_t m = b - a;
+        VK(d2d((char*)keys + (r0 + a) * kb, sk_in, m * kb, s));
+        if (hv) VK(d2d(vals + r0 + a, sv_in, m * 4, s));
+      }
+    }
+    if (cnt) VK(local_sort(nullptr));  // two sorted runs -> one (stable, ties to the lower run)
+    quiet = swapped ? 0 : quiet + 1;
+  }
+  if (quiet < 2) { c_err = "internal: merge-split phases did not converge"; return VMPS_ERR_INTERNAL; }
+  if (h_stats) {  // the cap covers the exchange staging as well (it overlays the sort's scratch)
+    h_stats->scratch_bytes = std::max<uint64_t>(h_stats->scratch_bytes, 2 * L.C * (kb + (hv ? 4 : 0)));
+    h_stats->peak_extra_device_bytes = std::max<uint64_t>(h_stats->peak_extra_device_bytes, L.total);
+  }
+  return tp_sync(c, s);
+}
+
 vmps_status_t sort_dist_any(vmps_comm_t c, void* keys, uint32_t* vals, uint64_t n_local, vmps_key_t kt,
                             int64_t scratch, void* ws, size_t ws_bytes, cudaStream_t s, vmps_stats_t* h_stats,
                             bool pairs) {
   if (!c) { c_err = "NULL communicator"; return VMPS_ERR_INVALID_ARG; }
+  if (scratch >= 0) {
+    if (n_local && !keys) { c_err = "keys is NULL"; return VMPS_ERR_INVALID_ARG; }
+    c_err.clear();
+    return sort_dist_bounded(c, keys, vals, n_local, kt, scratch, ws, ws_bytes, s, h_stats, pairs);
+  }
   if (n_local && !keys) { c_err = "keys is NULL"; return VMPS_ERR_INVALID_ARG; }
   if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) {
     c_err = "unknown key type";
@@ -569,6 +779,7 @@ vmps_status_t sort_dist_any(vmps_comm_t c, void* keys, uint32_t* vals, uint64_t 
   uint64_t* d_cnt = (uint64_t*)cv.take(2 * nprobe_cap * 8);
   uint64_t* d_small = (uint64_t*)cv.take(L.small);
   if (!d_small) { c_err = "workspace carve"; return VMPS_ERR_BUDGET; }
+  struct Nv { explicit Nv(const char* m) { nvtxRangePushA(m); } ~Nv() { nvtxRangePop(); } } nv("vmps_sort_dist");
   // 1. local sort
   if (n_local > 1) {
     if (hv) VK(vmps_sort_pairs(keys, vals, n_local, kt, scratch, sort_ws, std::max(L.sort_ws, L.mr_ws), s, h_stats));
@@ -843,7 +1054,8 @@ vmps_status_t vmps_ipc_close(void* d_ptr, uint64_t offset) {
 vmps_status_t vmps_dist_workspace_bytes(uint64_t n_local, vmps_key_t kt, int has_vals, int world,
                                         int64_t scratch_elems, size_t* h_bytes) {
   if (!h_bytes || world < 1 || n_local > VMPS_MAX_N) return VMPS_ERR_INVALID_ARG;
-  *h_bytes = dist_layout(n_local, kt, has_vals ? 1 : 0, world, scratch_elems).total;
+  *h_bytes = scratch_elems >= 0 ? bd_layout(n_local, kt, has_vals ? 1 : 0, world, scratch_elems).total
+                                 : dist_layout(n_local, kt, has_vals ? 1 : 0, world, scratch_elems).total;
   return VMPS_OK;
 }
 

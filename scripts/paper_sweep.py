@@ -53,9 +53,20 @@ for kind in ("int", "randomBlob30", "zeroBlob30", "ptr"):
                     vm.sort_records(r, out=o, workspace=ws)
             fn()
             torch.cuda.synchronize()
-            lead = 0 if kind != "zeroBlob30" else 29
-            col = o[:, lead].to(torch.int64) & 0xFFFFFFFF
-            ok = bool((col[1:] >= col[:-1]).all())
+            # full verification: permutation, records_out = records[perm],
+            # stable lexicographic order over all 30 words
+            _, pm = vm.sort_records(r, perm=True, workspace=ws)
+            torch.cuda.synchronize()
+            p64 = pm.to(torch.int64) & 0xFFFFFFFF
+            a = o.to(torch.int64) & 0xFFFFFFFF
+            diff = a[1:] != a[:-1]
+            anyd = diff.any(dim=1)
+            first = torch.argmax(diff.to(torch.int32), dim=1)
+            rows = torch.arange(a.shape[0] - 1, device=a.device)
+            ok = (bool((torch.bincount(p64, minlength=n) == 1).all()) and torch.equal(o, r[p64])
+                  and bool(((~anyd) | (a[1:][rows, first] > a[:-1][rows, first])).all())
+                  and bool((anyd | (p64[1:] > p64[:-1])).all()))
+            del a, diff, anyd, first, rows, p64
             ms = timed(fn, lambda: None)
             rec.update(record_bytes=120, verified=ok)
         rec.update(ms=ms, mkeys_per_s=n / (ms / 1000) / 1e6)

@@ -242,3 +242,73 @@ def test_virtual_rank_timeout(monkeypatch):
     assert res.get("status") == 5, res
     c0.destroy()
     group.destroy()
+
+
+# ---- scratch-bounded multi-GPU sort: cap per rank, exchange staging included ----
+
+@pytest.mark.parametrize("g,dtype,sizes,minrun", [
+    (2, np.uint32, [150_000, 120_001], 0),
+    (3, np.uint64, [40_000, 0, 70_003], 0),          # an empty shard
+    (4, np.float32, [30_000, 12_000, 45_000, 20_000], 0),  # unequal shards
+    (4, np.uint32, [60_000] * 4, 4),                  # many runs (minrun 4)
+])
+def test_sort_dist_bounded_virtual_ranks(g, dtype, sizes, minrun):
+    """vmps_sort_pairs_dist with scratch_elems = 4 sqrt(n log2 n) per rank:
+    identical to the oracle's stable sort of the concatenation; the element
+    scratch (the local sorts' blocks and the swap staging) stays within the cap."""
+    import math
+
+    import paper_2605_27147_b200 as vm
+    from tests import vranks
+    rng = np.random.default_rng(31 * g + len(sizes))
+    ks = _shards(rng, sizes, dtype)
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    vs = [np.arange(offs[q], offs[q + 1], dtype=np.uint32) for q in range(g)]
+    caps = [int(4 * math.sqrt(max(s, 2) * math.log2(max(s, 2)))) for s in sizes]
+    caps = [max(c, 6 * 64) for c in caps]
+    vm.test_set_minrun(minrun)
+    try:
+        def fn(rank, comm):
+            kd = W.from_numpy(ks[rank], "cuda")
+            vd = W.from_numpy(vs[rank], "cuda")
+            st = vm.sort_dist_native_(comm, kd, vd, scratch=caps[rank], stats=True)
+            return W.to_numpy(kd), W.to_numpy(vd), st
+
+        outs = vranks.run(g, fn)
+    finally:
+        vm.test_set_minrun(0)
+    ko, vo, _, _ = oracle.sort(np.concatenate(ks), np.concatenate(vs))
+    for q in range(g):
+        assert len(outs[q][0]) == sizes[q]
+    assert np.concatenate([o[0] for o in outs]).view(np.uint8).tobytes() == ko.view(np.uint8).tobytes()
+    assert (np.concatenate([o[1] for o in outs]) == vo).all()
+    w = np.dtype(dtype).itemsize + 4
+    for q in range(g):
+        st = outs[q][2]
+        if sizes[q] > 1:
+            assert st["scratch_bytes"] <= caps[q] * w, (q, st["scratch_bytes"], caps[q] * w)
+
+
+def test_sort_dist_bounded_cfg5_virtual_ranks():
+    """cfg5-shaped shards, 2^20 per rank, 2 ranks, the cap 4 sqrt(n log2 n)."""
+    import math
+
+    import paper_2605_27147_b200 as vm
+    from tests import vranks
+    g, n = 2, 1 << 20
+    sh = [W.cfg5(n=n, device="cpu", rank=q) for q in range(g)]
+    ks = [W.to_numpy(k) for k, _ in sh]
+    vs = [W.to_numpy(v) for _, v in sh]
+    S = int(4 * math.sqrt(n * math.log2(n)))
+
+    def fn(rank, comm):
+        kd = W.from_numpy(ks[rank], "cuda")
+        vd = W.from_numpy(vs[rank], "cuda")
+        st = vm.sort_dist_native_(comm, kd, vd, scratch=S, stats=True)
+        return W.to_numpy(kd), W.to_numpy(vd), st
+
+    outs = vranks.run(g, fn)
+    ko, vo, _, _ = oracle.sort(np.concatenate(ks), np.concatenate(vs))
+    assert (np.concatenate([o[0] for o in outs]) == ko).all()
+    assert (np.concatenate([o[1] for o in outs]) == vo).all()
+    assert all(o[2]["scratch_bytes"] <= S * 8 for o in outs)
