@@ -13,8 +13,10 @@
 // bits are equal over the whole batch are skipped (OR / AND of the images),
 // as is the unit pass of a single-unit batch.
 //
-// Layout: warp w owns positions [288 w, 288 w + 288), striped (lane l, item
-// i <-> position 288 w + 32 i + l), so global loads/stores are coalesced and
+// Layout: warp w owns positions [32 K w, 32 K (w + 1)) with K = LEAF_K items
+// per lane (11 with the default 384-thread CTAs: 12 warps x 352 positions),
+// striped (lane l, item i <-> position 32 K w + 32 i + l), so global
+// loads / stores are coalesced and
 // processing items in order (i outer, lanes inner) is position order, which
 // makes the warp-level ranking (match.any + per-warp digit counters) stable.
 #pragma once
@@ -22,9 +24,9 @@
 
 namespace vmps {
 
-constexpr int LR_WARPS = LEAF_THREADS / 32;      // 16
-constexpr int LR_ITEMS = LEAF_K;                 // 9
-constexpr int LR_SPAN = 32 * LR_ITEMS;           // 288 positions per warp
+constexpr int LR_WARPS = LEAF_THREADS / 32;      // 12 (384 threads)
+constexpr int LR_ITEMS = LEAF_K;                 // 11
+constexpr int LR_SPAN = 32 * LR_ITEMS;           // 352 positions per warp
 static_assert(LR_WARPS * LR_SPAN == LEAF_CAP, "leaf radix layout");
 
 template <int KT>
