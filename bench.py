@@ -74,6 +74,9 @@ def parse():
                     help="N>1: pull-merge the co-ranked pieces from peer memory (dist.sort_dist_pull)")
     ap.add_argument("--bounded-reps", type=int, default=2,
                     help="timed sorts of the scratch-bounded mode (cap 4 sqrt(n log2 n)); 0 = skip")
+    ap.add_argument("--verify-oracle", action="store_true",
+                    help="slow, untimed: every rank's local sort vs the oracle on the host, and the global plan "
+                         "vs the oracle's plan-only pass over the whole array (rank 0; SURVEY 8(d) (i), (iii))")
     ap.add_argument("--launcher-selftest", action="store_true",
                     help="CPU check of the N-rank launcher: every rank joins a gloo group; rank 0 prints n_gpus")
     return ap.parse_args()
@@ -276,6 +279,15 @@ def _pinned_like(t):
     return torch.empty(t.numel(), dtype=_sv(t).dtype, pin_memory=True).view(t.dtype)
 
 
+def plan_hash_of(i, j, k, pw, order):
+    """Sum over merge records of a 64-bit mix of (i, j, k, power, order)."""
+    x = i * -7046029254386353131 + j * -4417276706812531889 + k * 1609587929392839161
+    x = x ^ (pw * 2246822519 + order * 3266489917)
+    x = x ^ ((x >> 31) & 0x1FFFFFFFF)
+    x = x * -4658895280553007687
+    return int(x.sum().item())
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -298,6 +310,8 @@ def main():
         return
     import torch
     import torch.distributed as dist
+
+    import numpy as np
 
     import paper_2605_27147_b200 as vm
     import workloads as W
@@ -375,18 +389,75 @@ def main():
     # local plan statistics (one untimed local sort)
     restore()
     stats = vm.sort_(keys, vals, workspace=ws, stats=True)
+    overify = {}
+    if args.verify_oracle:  # (i): this rank's local sort vs the oracle (host, single thread)
+        import oracle
+        import workloads as W
+        kh = W.to_numpy(keys0)
+        ko, vo, _, _ = oracle.sort(kh, W.to_numpy(vals0) if hv else None)
+        okl = bool((W.to_numpy(keys).view(np.uint8) == ko.view(np.uint8)).all()) and (
+            not hv or bool((W.to_numpy(vals) == vo).all()))
+        t = torch.tensor([1 if okl else 0], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        overify["local_sorts_equal_oracle"] = bool(t.item())
+        del kh, ko, vo
     # the global plan's merge cost (the roofline uses the plan of
     # the whole array): untimed vmps_merge_plan_dist, merges summed over ranks
     runs_g, M_g = stats["runs"], stats["merge_cost_M"]
+    plan_hash = None
     if world > 1:
         from paper_2605_27147_b200 import dist as vdist
         p = vdist.merge_plan_dist(keys0, n_total=n_total, comm=ncomm)
         mk = p.merges
-        t = torch.tensor([int(p.run_start.numel()), int((mk[:, 2] - mk[:, 0]).sum().item()) if mk.numel() else 0],
+        ph = 0
+        if args.verify_oracle and mk.numel():
+            ph = plan_hash_of(mk[:, 0], mk[:, 1], mk[:, 2], mk[:, 3], mk[:, 4])
+        t = torch.tensor([int(p.run_start.numel()), int((mk[:, 2] - mk[:, 0]).sum().item()) if mk.numel() else 0, ph],
                          dtype=torch.int64, device=dev)
         dist.all_reduce(t)
-        runs_g, M_g = int(t[0].item()), int(t[1].item())
+        runs_g, M_g, plan_hash = int(t[0].item()), int(t[1].item()), int(t[2].item())
         del p, mk
+    elif args.verify_oracle:
+        p = vm.merge_plan(keys0)
+        mk = p.merges
+        ordr = torch.arange(mk.shape[0], dtype=torch.int64, device=dev)
+        plan_hash = plan_hash_of(mk[:, 0], mk[:, 1], mk[:, 2], mk[:, 3], ordr) if mk.numel() else 0
+        del p, mk
+    glob = None
+    if args.verify_oracle:  # (iii): the whole array on rank 0's host (shards sent in 256 MiB pieces)
+        import workloads as W
+        parts = [W.to_numpy(keys0)] if rank == 0 else []
+        CH = (256 << 20) // keys0.element_size()
+        for q in range(1, world):
+            nq = torch.tensor([n], dtype=torch.int64, device=dev)
+            dist.broadcast(nq, src=q)
+            nq = int(nq.item())
+            buf = torch.empty(min(CH, max(nq, 1)), dtype=_sv(keys0).dtype, device=dev)
+            got = []
+            for a in range(0, nq, CH):
+                m = min(CH, nq - a)
+                if rank == q:
+                    dist.send(_sv(keys0)[a:a + m].contiguous(), dst=0)
+                elif rank == 0:
+                    dist.recv(buf[:m], src=q)
+                    got.append(buf[:m].view(keys0.dtype).cpu())
+            if rank == 0:
+                parts.append(W.to_numpy(torch.cat(got)) if got else np.zeros(0, W.to_numpy(keys0[:0]).dtype))
+        if rank == 0:
+            glob = np.concatenate(parts)
+        del parts
+    if args.verify_oracle and rank == 0:
+        import oracle
+        oplan, ost = oracle.plan(glob)
+        om = oplan.merges
+        dv = "cpu"
+        oh = plan_hash_of(*(torch.from_numpy(om[f].astype(np.int64)) for f in ("i", "j", "k", "power")),
+                          torch.arange(len(om), dtype=torch.int64)) if len(om) else 0
+        overify.update(plan_runs_equal=len(oplan.run_start) == runs_g, plan_M_equal=ost["merge_cost_M"] == M_g,
+                       plan_hash_equal=(oh - plan_hash) % (1 << 64) == 0,
+                       plan_check="hash of (i, j, k, power, order) summed over the merges")
+        del glob, oplan, om, dv
     for w in range(max(args.warmup, 1)):
         restore()
         do_sort()
@@ -662,6 +733,7 @@ def main():
                "roofline": roof, "tree_roofline": tree, "phases_ms": ph,
                "cpu_baseline": cpu, "e2e": e2e, "bounded": bounded,
                "gpu_launches": launches, "clocks": clk, "verified": ok,
+               "oracle_verification": overify or None,
                "verification": {"sorted": True, "multiset_hash": "sum of mix64(key, payload) equal before / after",
                                 "stability": stab,
                                 "permutation": "keys == input[payload] (exact)" if world == 1 and hv else
