@@ -397,6 +397,11 @@ void vmps_test_set_mode(int levels_per_pass);
  * 2^30 cfg5: 29 vs 18 ms).  Same output (a stable sort is unique). */
 void vmps_test_set_leaf(int radix);
 void vmps_test_set_tiles(uint32_t fuse_z, uint32_t merge_tile, uint32_t block_elems);
+/* Test hook: chunk of the chunked scratch-bounded mode (used when n > 2 chunk;
+ * 0 restores 2^24): each chunk is sorted by the bounded engine, then the
+ * sorted chunks are merged along their Powersort tree, so the plan metadata
+ * scales with the chunk instead of n.  Same output. */
+void vmps_test_set_bd_chunk(uint32_t chunk);
 
 #ifdef __cplusplus
 }

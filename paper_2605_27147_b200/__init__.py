@@ -67,7 +67,7 @@ EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_me
            "vmps_merge_pieces", "vmps_ipc_handle", "vmps_ipc_open", "vmps_ipc_close",
            "vmps_local_group_create", "vmps_local_group_destroy", "vmps_comm_init_local",
            "vmps_dist_cuts_workspace_bytes", "vmps_dist_cuts", "vmps_splitter_probes", "vmps_splitter_update",
-           "vmps_split_points", "vmps_compose_tables", "vmps_merge_plan_dist_capacity")
+           "vmps_split_points", "vmps_compose_tables", "vmps_merge_plan_dist_capacity", "vmps_test_set_bd_chunk")
 
 _lib = None
 
@@ -167,6 +167,8 @@ def lib() -> ctypes.CDLL:
         L.vmps_test_set_leaf.restype = None
         L.vmps_test_set_tiles.argtypes = [ctypes.c_uint32] * 3
         L.vmps_test_set_tiles.restype = None
+        L.vmps_test_set_bd_chunk.argtypes = [ctypes.c_uint32]
+        L.vmps_test_set_bd_chunk.restype = None
         _lib = L
     return _lib
 
@@ -769,3 +771,8 @@ def test_set_leaf(radix: bool = False) -> None:
 def test_set_tiles(fuse_z: int = 0, merge_tile: int = 0, block_elems: int = 0) -> None:
     """Test hook: shrink fused-subtree / merge-tile / bounded-block sizes (0 = default)."""
     lib().vmps_test_set_tiles(fuse_z, merge_tile, block_elems)
+
+
+def test_set_bd_chunk(chunk: int = 0) -> None:
+    """Test hook: chunk of the chunked scratch-bounded mode (0 = 2^24)."""
+    lib().vmps_test_set_bd_chunk(chunk)

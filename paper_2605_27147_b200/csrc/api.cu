@@ -94,6 +94,7 @@ struct Cfg {
   int64_t scratch;  // VMPS_SCRATCH_UNBOUNDED or the element cap
   int fuse2;
   uint32_t P, F;    // bounded mode: block size, scratch blocks
+  uint32_t given_runs;  // > 0: the runs are given (no run detection; per-run arrays sized by it)
 };
 
 static Cfg make_cfg(uint64_t n, int kt, int hv, int64_t scratch = VMPS_SCRATCH_UNBOUNDED) {
@@ -107,6 +108,7 @@ static Cfg make_cfg(uint64_t n, int kt, int hv, int64_t scratch = VMPS_SCRATCH_U
   c.scratch = scratch;
   c.fuse2 = (scratch < 0 && hv >= 0) ? g_fuse2 : 0;
   c.P = c.F = 0;
+  c.given_runs = 0;
   if (scratch >= 0 && hv >= 0) {
     // block size: a power of two <= min(Z, T_out) (nodes are then longer than
     // a block, so a block meets at most 3 tile pieces), test hook override
@@ -139,8 +141,8 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
   t.n = (uint32_t)n;
   t.minrun = c.minrun;
   t.ns = 3 * c.minrun;
-  t.ntiles = (uint32_t)((n + RT - 1) / RT);
-  t.rmax = (uint32_t)(n / std::max<uint32_t>(c.minrun, 1) + 2);
+  t.ntiles = c.given_runs ? 0u : (uint32_t)((n + RT - 1) / RT);
+  t.rmax = c.given_runs ? c.given_runs + 2u : (uint32_t)(n / std::max<uint32_t>(c.minrun, 1) + 2);
   t.fuse_z = c.fuse_z;
   t.tout = c.tout;
   t.kt = c.kt;
@@ -243,7 +245,8 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.btoff = t.long_idx;
     t.bm = (uint32_t*)take(64);
     t.bD = (uint32_t*)take(64);
-    t.bdesc_cap = (uint32_t)(n / c.P + 4 * (n / c.fuse_z) + 16);
+    // tiles of one level: one per output block plus gap tiles at node ends
+    t.bdesc_cap = (uint32_t)(n / c.P + 4 * std::min<uint64_t>(n / c.fuse_z, (uint64_t)t.rmax) + 16);
     t.bdesc = take((size_t)t.bdesc_cap * sizeof(TileDesc));
     t.bstate = take(sizeof(BdState));
     t.copy_batch = std::max<uint32_t>(1, c.F / 3);
@@ -275,7 +278,7 @@ static cudaStream_t aux_stream() {
   if (!g_aux[dev] && cudaStreamCreateWithFlags(&g_aux[dev], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
   return g_aux[dev];
 }
-constexpr int BD_GRAPH_ROUNDS = 48;  // bounded-mode rounds per graph launch
+constexpr int BD_GRAPH_ROUNDS = 8;  // bounded-mode rounds per graph launch
 
 static int g_nsm = 0;
 static int nsm() {
@@ -410,6 +413,26 @@ static vmps_status_t front_half(const Work& w, const void* keys, cudaStream_t s)
 }
 
 
+// Plan front half for given runs (the chunked scratch-bounded mode's top
+// level): run starts uploaded (ascending runs, sentinel n), then the same
+// powers / segments / parents / depths as front_half.
+static vmps_status_t front_half_given(const Work& w, const uint32_t* h_runs, uint32_t r, cudaStream_t s) {
+  VMPS_CK(cudaMemsetAsync(w.scalars, 0, SC_COUNT * 4, s));
+  VMPS_CK(cudaMemsetAsync(w.counters, 0, 8 * 8, s));
+  VMPS_CK(cudaMemcpyAsync(w.run_start, h_runs, (size_t)(r + 1) * 4, cudaMemcpyHostToDevice, s));
+  VMPS_CK(cudaMemsetAsync(w.run_kind, 0, r, s));
+  VMPS_CK(cudaMemcpyAsync(w.scalars + SC_RUNS, &r, 4, cudaMemcpyHostToDevice, s));
+  const unsigned g = grid_for(w.rmax);
+  LAUNCH(k_powers_seg<uint32_t>, g, 256, 0, s, w.run_start, (uint64_t)w.n, w.scalars, w.power, w.seg_l, w.seg_r);
+  LAUNCH(k_parent_init, g, 256, 0, s, w.scalars, w.power, w.seg_l, w.seg_r, w.parent, w.anc[0], w.dep[0]);
+  for (int rnd = 0; rnd < 6; ++rnd) {
+    int a = rnd & 1;
+    LAUNCH(k_jump, g, 256, 0, s, w.scalars, w.anc[a], w.dep[a], w.anc[a ^ 1], w.dep[a ^ 1]);
+  }
+  VMPS_CK(cudaStreamSynchronize(s));  // the host run list is the caller's stack memory
+  return launch_check();
+}
+
 // ---- scratch-bounded mode: level rounds and the final Copy (bounded.cuh) ----
 template <int KT, bool HV>
 static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0, uint32_t* v0, int p_hi,
@@ -475,11 +498,17 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
     LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, grid_for(total)), 256, 0, s, M, desc, w.btoff, w.bm, w.dirty,
            w.didx, w.dlist, w.first_tile, w.remain, w.bD);
     // rounds until every dirty block of the level is produced; a batch of
-    // rounds is one CUDA graph launch (rounds past the end are no-ops)
+    // rounds is one CUDA graph launch (rounds past the end are no-ops).  The
+    // first check comes after the rounds the level needs at most (its output
+    // blocks over the scratch blocks, + 1), so a level costs one host wait
+    // and only its last batch runs no-op rounds.
+    const uint32_t est = (uint32_t)((total + w.F - 1) / w.F) + 1u;
+    uint32_t first = rounds_exec ? (est + BD_GRAPH_ROUNDS - 1) / BD_GRAPH_ROUNDS : 1u;
     for (;;) {
       if (rounds_exec) {
-        VMPS_CK(cudaGraphLaunch(rounds_exec, s));
-        g_nl += 2 * BD_GRAPH_ROUNDS;
+        for (uint32_t q = 0; q < first; ++q) VMPS_CK(cudaGraphLaunch(rounds_exec, s));
+        g_nl += 2 * BD_GRAPH_ROUNDS * first;
+        first = 1;
       } else {
         for (int q = 0; q < 16; ++q) {
           LAUNCH(k_bd_alloc, 1, 1024, 0, s, st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
@@ -552,13 +581,13 @@ static bool kernel_attrs_set[MAX_DEV][3][2] = {};
 
 template <int KT, bool HV>
 static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaStream_t s,
-                               vmps_stats_t* st) {
+                               vmps_stats_t* st, const uint32_t* h_runs = nullptr) {
   using K = typename KeyTraits<KT>::K;
   prof_reset();
   NvtxRange nv_sort("vmps_sort");
   NvtxRange nv_plan("vmps_plan");
   g_prof_mark[0] = prof_event(s);
-  vmps_status_t rc = front_half<KT>(w, keys, s);
+  vmps_status_t rc = h_runs ? front_half_given(w, h_runs, w.rmax - 2, s) : front_half<KT>(w, keys, s);
   if (rc != VMPS_OK) return rc;
   const uint32_t* dep = w.dep[0];
   const unsigned g = grid_for(w.rmax);
@@ -824,16 +853,100 @@ static vmps_status_t check_common(const void* keys, const void* vals, uint64_t n
 
 extern "C" {
 
+// Chunked scratch-bounded mode (large n): the array is sorted in chunks of
+// BD_CHUNK elements, each by the bounded engine (Powersort of the chunk's
+// runs), then the sorted chunks are merged by the same engine along the
+// Powersort tree of the chunk boundaries (given runs, no run detection).  The
+// per-run metadata then scales with the chunk (n_chunk / minrun runs) and
+// the number of chunks instead of n / minrun: 3.4 GB -> ~60 MB at 2^30.  The
+// output is the unique stable sort, identical to the one-piece mode; the
+// executed merge tree differs where a natural run crosses a chunk edge.
+#ifndef VMPS_BD_CHUNK
+#define VMPS_BD_CHUNK (1u << 24)
+#endif
+static uint64_t g_bd_chunk = VMPS_BD_CHUNK;  // test hook vmps_test_set_bd_chunk
+#define BD_CHUNK g_bd_chunk
+static bool bd_chunked(uint64_t n, int64_t scratch, int hv) { return scratch >= 0 && hv >= 0 && n > 2 * BD_CHUNK; }
+static size_t bd_chunked_bytes(uint64_t n, int kt, int hv, int64_t scratch) {
+  Cfg cc = make_cfg(BD_CHUNK, kt, hv, scratch);
+  Cfg ct = make_cfg(n, kt, hv, scratch);
+  ct.given_runs = (uint32_t)((n + BD_CHUNK - 1) / BD_CHUNK);
+  return std::max(carve(cc, nullptr, nullptr), carve(ct, nullptr, nullptr));
+}
+
 vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, int64_t scratch_elems,
                                    size_t* h_bytes) {
   if (!h_bytes) return VMPS_ERR_INVALID_ARG;
   if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
   if (n > VMPS_MAX_N) return VMPS_ERR_INVALID_ARG;
   if (n <= 1) { *h_bytes = 256; return VMPS_OK; }
-  Cfg c = make_cfg(n, kt, has_vals < 0 ? -1 : (has_vals ? 1 : 0), scratch_elems);
+  const int hv = has_vals < 0 ? -1 : (has_vals ? 1 : 0);
+  if (bd_chunked(n, scratch_elems, hv)) { *h_bytes = bd_chunked_bytes(n, kt, hv, scratch_elems) + 256; return VMPS_OK; }
+  Cfg c = make_cfg(n, kt, hv, scratch_elems);
   *h_bytes = carve(c, nullptr, nullptr) + 256;
   return VMPS_OK;
 }
+
+}  // extern "C"
+
+template <int KT, bool HV>
+static vmps_status_t sort_bounded_chunked(void* keys, uint32_t* vals, uint64_t n, int64_t S, char* base,
+                                          cudaStream_t s, vmps_stats_t* st) {
+  const size_t kb = key_bytes(KT);
+  const uint32_t nch = (uint32_t)((n + BD_CHUNK - 1) / BD_CHUNK);
+  vmps_stats_t acc;
+  memset(&acc, 0, sizeof(acc));
+  size_t peak = 0, scratch_b = 0;
+  for (uint32_t c = 0; c < nch; ++c) {
+    const uint64_t off = (uint64_t)c * BD_CHUNK, nc = std::min<uint64_t>(BD_CHUNK, n - off);
+    if (nc <= 1) continue;
+    Cfg cc = make_cfg(nc, KT, HV ? 1 : 0, S);
+    Work w;
+    peak = std::max(peak, carve(cc, &w, base));
+    vmps_stats_t cs;
+    vmps_status_t rc = sort_impl<KT, HV>(w, (char*)keys + off * kb, HV ? vals + off : nullptr, s, st ? &cs : nullptr);
+    if (rc != VMPS_OK) return rc;
+    if (st) {
+      acc.runs += cs.runs;
+      acc.merge_cost_M += cs.merge_cost_M;
+      acc.fused_M += cs.fused_M;
+      acc.reversed_elems += cs.reversed_elems;
+      acc.extended_runs += cs.extended_runs;
+      acc.rounds += cs.rounds;
+      acc.max_power = std::max(acc.max_power, cs.max_power);
+      acc.levels_executed = std::max(acc.levels_executed, cs.levels_executed);
+      acc.minrun = cs.minrun;
+      scratch_b = std::max<size_t>(scratch_b, cs.scratch_bytes);
+    }
+  }
+  // top level: the sorted chunks as runs, merged along their Powersort tree
+  std::vector<uint32_t> runs(nch + 1);
+  for (uint32_t c = 0; c < nch; ++c) runs[c] = (uint32_t)((uint64_t)c * BD_CHUNK);
+  runs[nch] = (uint32_t)n;
+  Cfg ct = make_cfg(n, KT, HV ? 1 : 0, S);
+  ct.given_runs = nch;
+  Work w;
+  peak = std::max(peak, carve(ct, &w, base));
+  vmps_stats_t ts;
+  vmps_status_t rc = sort_impl<KT, HV>(w, keys, HV ? vals : nullptr, s, st ? &ts : nullptr, runs.data());
+  if (rc != VMPS_OK) return rc;
+  if (st) {
+    acc.merge_cost_M += ts.merge_cost_M;
+    acc.fused_M += ts.fused_M;
+    acc.rounds += ts.rounds;
+    acc.levels_executed += ts.levels_executed;
+    acc.n = n;
+    acc.merges = acc.runs ? acc.runs - 1 : 0;
+    acc.block_elems = ts.block_elems;
+    acc.scratch_bytes = std::max<size_t>(scratch_b, ts.scratch_bytes);
+    acc.peak_extra_device_bytes = peak;
+    acc.metadata_bytes = peak - acc.scratch_bytes;
+    *st = acc;
+  }
+  return VMPS_OK;
+}
+
+extern "C" {
 
 static vmps_status_t sort_any(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt, int64_t scratch_elems,
                               void* ws, size_t ws_bytes, void* stream, vmps_stats_t* h_stats) {
@@ -852,6 +965,26 @@ static vmps_status_t sort_any(void* keys, uint32_t* vals, uint64_t n, vmps_key_t
   if (scratch_elems >= 0 && c.F < BD_MIN_BLOCKS) {
     g_err = "scratch_elems below the bounded mode's minimum (6 blocks)";
     return VMPS_ERR_BUDGET;
+  }
+  if (bd_chunked(n, scratch_elems, hv)) {
+    const size_t need = bd_chunked_bytes(n, kt, hv, scratch_elems);
+    char* base = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    if (!ws || ws_bytes < need || (size_t)(base - (char*)ws) + need > ws_bytes) {
+      g_err = "workspace too small";
+      return VMPS_ERR_BUDGET;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (kt) {
+      case VMPS_KEY_U32:
+        return hv ? sort_bounded_chunked<VMPS_KEY_U32, true>(keys, vals, n, scratch_elems, base, s, h_stats)
+                  : sort_bounded_chunked<VMPS_KEY_U32, false>(keys, vals, n, scratch_elems, base, s, h_stats);
+      case VMPS_KEY_U64:
+        return hv ? sort_bounded_chunked<VMPS_KEY_U64, true>(keys, vals, n, scratch_elems, base, s, h_stats)
+                  : sort_bounded_chunked<VMPS_KEY_U64, false>(keys, vals, n, scratch_elems, base, s, h_stats);
+      default:
+        return hv ? sort_bounded_chunked<VMPS_KEY_F32, true>(keys, vals, n, scratch_elems, base, s, h_stats)
+                  : sort_bounded_chunked<VMPS_KEY_F32, false>(keys, vals, n, scratch_elems, base, s, h_stats);
+    }
   }
   Work w;
   size_t need = carve(c, &w, nullptr);
@@ -1199,6 +1332,8 @@ int vmps_profile_read(double* h_ms, int cap, uint64_t* h_launches, uint64_t* h_b
 void vmps_test_set_mode(int levels_per_pass) { g_fuse2 = levels_per_pass == 1 ? 0 : 1; }
 
 void vmps_test_set_leaf(int radix) { g_leaf_radix = radix ? 1 : 0; }
+
+void vmps_test_set_bd_chunk(uint32_t chunk) { g_bd_chunk = chunk ? std::max<uint32_t>(chunk, 64u) : VMPS_BD_CHUNK; }
 
 void vmps_test_set_minrun(uint32_t minrun) { g_minrun_override = minrun > MAX_MINRUN ? MAX_MINRUN : minrun; }
 

@@ -152,3 +152,32 @@ def test_bounded_blocks_below_minrun(vm):
     k, v = W.cfg2(n=n, device="cpu")
     st = bounded_vs_oracle(vm, W.to_numpy(k), W.to_numpy(v), scratch=200)
     assert st["block_elems"] == 16 and st["minrun"] == 32
+
+
+@pytest.mark.parametrize("chunk,n,dtype", [(1 << 16, 1_000_003, np.uint32), (1 << 14, 300_000, np.uint64),
+                                           (1 << 15, 500_000, np.float32)])
+def test_bounded_chunked(vm, chunk, n, dtype):
+    """The chunked scratch-bounded mode (n > 2 chunks: chunks sorted by the
+    bounded engine, then merged along their Powersort tree): identical to the
+    oracle's stable sort; element scratch within the cap; plan metadata sized
+    by the chunk, not by n."""
+    rng = np.random.default_rng(chunk + n)
+    keys = _structured(rng, n, dtype)
+    vals = np.arange(n, dtype=np.uint32)
+    S = cap(n)
+    ko, vo, _, _ = oracle.sort(keys, vals)
+    try:
+        vm.test_set_bd_chunk(chunk)
+        k = W.from_numpy(keys, "cuda")
+        v = W.from_numpy(vals, "cuda")
+        st = vm.sort_(k, v, scratch=S, stats=True)
+        torch.cuda.synchronize()
+        meta_chunked = st["metadata_bytes"]
+    finally:
+        vm.test_set_bd_chunk(0)
+    assert W.to_numpy(k).view(np.uint8).tobytes() == ko.view(np.uint8).tobytes()
+    assert (W.to_numpy(v) == vo).all()
+    w = keys.dtype.itemsize + 4
+    assert st["scratch_bytes"] <= S * w
+    st1 = vm.sort_(W.from_numpy(keys, "cuda"), W.from_numpy(vals, "cuda"), scratch=S, stats=True)
+    assert meta_chunked < st1["metadata_bytes"]
