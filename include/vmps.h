@@ -369,6 +369,19 @@ vmps_status_t vmps_merge_runs(void* keys, uint32_t* vals, uint64_t n, vmps_key_t
                               const uint64_t* h_run_start, uint32_t nruns, void* ws,
                               size_t ws_bytes, void* stream);
 
+/* vmps_merge_runs_bounded: as vmps_merge_runs (adjacent sorted runs starting
+ * at h_run_start[0] = 0 < ... < n, host array; ties to the earlier run), with
+ * the element scratch capped at scratch_elems like the bounded sort (block
+ * table, rounds into freed blocks, final Copy); the plan is built from the
+ * given runs (no run detection), so its metadata is O(nruns + n / P).
+ * Workspace: vmps_merge_runs_bounded_workspace_bytes.  Synchronises `stream`
+ * (the bounded rounds). */
+vmps_status_t vmps_merge_runs_bounded_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, uint32_t nruns,
+                                                      int64_t scratch_elems, size_t* h_bytes);
+vmps_status_t vmps_merge_runs_bounded(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt,
+                                      const uint64_t* h_run_start, uint32_t nruns, int64_t scratch_elems, void* ws,
+                                      size_t ws_bytes, void* stream);
+
 /* Human-readable status; the last CUDA error detail of this thread. */
 const char* vmps_status_string(vmps_status_t s);
 const char* vmps_last_error(void);

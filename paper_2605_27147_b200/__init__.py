@@ -67,7 +67,8 @@ EXPORTS = ("vmps_workspace_bytes", "vmps_sort_keys", "vmps_sort_pairs", "vmps_me
            "vmps_merge_pieces", "vmps_ipc_handle", "vmps_ipc_open", "vmps_ipc_close",
            "vmps_local_group_create", "vmps_local_group_destroy", "vmps_comm_init_local",
            "vmps_dist_cuts_workspace_bytes", "vmps_dist_cuts", "vmps_splitter_probes", "vmps_splitter_update",
-           "vmps_split_points", "vmps_compose_tables", "vmps_merge_plan_dist_capacity", "vmps_test_set_bd_chunk")
+           "vmps_split_points", "vmps_compose_tables", "vmps_merge_plan_dist_capacity", "vmps_test_set_bd_chunk",
+           "vmps_merge_runs_bounded_workspace_bytes", "vmps_merge_runs_bounded")
 
 _lib = None
 
@@ -167,6 +168,10 @@ def lib() -> ctypes.CDLL:
         L.vmps_test_set_leaf.restype = None
         L.vmps_test_set_tiles.argtypes = [ctypes.c_uint32] * 3
         L.vmps_test_set_tiles.restype = None
+        L.vmps_merge_runs_bounded_workspace_bytes.argtypes = [u64, ci, ci, u32, i64, ctypes.POINTER(sz)]
+        L.vmps_merge_runs_bounded.argtypes = [vp, vp, u64, ci, ctypes.POINTER(u64), u32, i64, vp, sz, vp]
+        L.vmps_merge_runs_bounded_workspace_bytes.restype = ctypes.c_int
+        L.vmps_merge_runs_bounded.restype = ctypes.c_int
         L.vmps_test_set_bd_chunk.argtypes = [ctypes.c_uint32]
         L.vmps_test_set_bd_chunk.restype = None
         _lib = L
@@ -651,6 +656,25 @@ def merge_runs(keys: torch.Tensor, vals: torch.Tensor | None, starts: list[int],
         rc = L.vmps_merge_runs(keys.data_ptr(), None if vals is None else vals.data_ptr(), n, kt, hs, len(starts),
                                buf.data_ptr(), buf.numel(), _stream_ptr(keys.device))
     _check(rc, "vmps_merge_runs")
+
+
+def merge_runs_bounded(keys: torch.Tensor, vals: torch.Tensor | None, starts: list[int], scratch: int,
+                       workspace: Workspace | None = None) -> None:
+    """vmps_merge_runs_bounded: in-place stable merge of the adjacent sorted
+    runs at `starts` with the element scratch capped at `scratch`."""
+    n = keys.numel()
+    kt = key_type(keys)
+    L = lib()
+    nb = ctypes.c_size_t(0)
+    _check(L.vmps_merge_runs_bounded_workspace_bytes(n, kt, 1 if vals is not None else 0, len(starts), scratch,
+                                                     ctypes.byref(nb)), "vmps_merge_runs_bounded_workspace_bytes")
+    ws = workspace if workspace is not None else _default_workspace(keys.device)
+    buf = ws.get(int(nb.value), keys.device)
+    hs = (ctypes.c_uint64 * len(starts))(*starts)
+    with torch.cuda.device(keys.device):
+        rc = L.vmps_merge_runs_bounded(keys.data_ptr(), None if vals is None else vals.data_ptr(), n, kt, hs,
+                                       len(starts), scratch, buf.data_ptr(), buf.numel(), _stream_ptr(keys.device))
+    _check(rc, "vmps_merge_runs_bounded")
 
 
 def dist_cuts(comm: Comm, keys: torch.Tensor, workspace: Workspace | None = None):

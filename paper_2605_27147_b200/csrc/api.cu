@@ -1333,6 +1333,64 @@ void vmps_test_set_mode(int levels_per_pass) { g_fuse2 = levels_per_pass == 1 ? 
 
 void vmps_test_set_leaf(int radix) { g_leaf_radix = radix ? 1 : 0; }
 
+// ---- scratch-bounded merge of given sorted runs (the multi-GPU bounded
+// protocol's re-merge after a swap; csrc/comm.cu) ----
+vmps_status_t vmps_merge_runs_bounded_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, uint32_t nruns,
+                                                      int64_t scratch_elems, size_t* h_bytes) {
+  if (!h_bytes || n > VMPS_MAX_N || nruns < 1 || scratch_elems < 0) return VMPS_ERR_INVALID_ARG;
+  if (kt != VMPS_KEY_U32 && kt != VMPS_KEY_U64 && kt != VMPS_KEY_F32) return VMPS_ERR_INVALID_ARG;
+  if (n <= 1) { *h_bytes = 256; return VMPS_OK; }
+  Cfg c = make_cfg(n, kt, has_vals ? 1 : 0, scratch_elems);
+  c.given_runs = nruns;
+  *h_bytes = carve(c, nullptr, nullptr) + 256;
+  return VMPS_OK;
+}
+
+vmps_status_t vmps_merge_runs_bounded(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt,
+                                      const uint64_t* h_run_start, uint32_t nruns, int64_t scratch_elems, void* ws,
+                                      size_t ws_bytes, void* stream) {
+  vmps_status_t rc = check_common(keys, vals, n, kt);
+  if (rc != VMPS_OK) return rc;
+  if (scratch_elems < 0 || !h_run_start || nruns < 1) { g_err = "bad arguments"; return VMPS_ERR_INVALID_ARG; }
+  if (n <= 1) return VMPS_OK;
+  // distinct starts inside [0, n), ascending from 0
+  std::vector<uint32_t> runs;
+  for (uint32_t q = 0; q < nruns; ++q) {
+    const uint64_t a = h_run_start[q];
+    if (a >= n || (q && a <= h_run_start[q - 1])) continue;
+    if (runs.empty() && a != 0) runs.push_back(0);
+    runs.push_back((uint32_t)a);
+  }
+  if (runs.empty() || runs[0] != 0) runs.insert(runs.begin(), 0u);
+  if (runs.size() < 2) return VMPS_OK;  // one run: already sorted
+  const uint32_t r = (uint32_t)runs.size();
+  runs.push_back((uint32_t)n);
+  const int hv = vals ? 1 : 0;
+  Cfg c = make_cfg(n, kt, hv, scratch_elems);
+  if (c.F < BD_MIN_BLOCKS) { g_err = "scratch_elems below the bounded mode's minimum (6 blocks)"; return VMPS_ERR_BUDGET; }
+  c.given_runs = r;
+  Work w;
+  const size_t need = carve(c, &w, nullptr);
+  char* base = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  if (!ws || ws_bytes < need || (size_t)(base - (char*)ws) + need > ws_bytes) {
+    g_err = "workspace too small";
+    return VMPS_ERR_BUDGET;
+  }
+  carve(c, &w, base);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (kt) {
+    case VMPS_KEY_U32:
+      return hv ? sort_impl<VMPS_KEY_U32, true>(w, keys, vals, s, nullptr, runs.data())
+                : sort_impl<VMPS_KEY_U32, false>(w, keys, vals, s, nullptr, runs.data());
+    case VMPS_KEY_U64:
+      return hv ? sort_impl<VMPS_KEY_U64, true>(w, keys, vals, s, nullptr, runs.data())
+                : sort_impl<VMPS_KEY_U64, false>(w, keys, vals, s, nullptr, runs.data());
+    default:
+      return hv ? sort_impl<VMPS_KEY_F32, true>(w, keys, vals, s, nullptr, runs.data())
+                : sort_impl<VMPS_KEY_F32, false>(w, keys, vals, s, nullptr, runs.data());
+  }
+}
+
 void vmps_test_set_bd_chunk(uint32_t chunk) { g_bd_chunk = chunk ? std::max<uint32_t>(chunk, 64u) : VMPS_BD_CHUNK; }
 
 void vmps_test_set_minrun(uint32_t minrun) { g_minrun_override = minrun > MAX_MINRUN ? MAX_MINRUN : minrun; }

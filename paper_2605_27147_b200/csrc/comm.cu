@@ -573,8 +573,10 @@ struct BdLayout {
 
 BdLayout bd_layout(uint64_t n_local, vmps_key_t kt, int hv, int world, int64_t S) {
   BdLayout L{};
-  size_t b = 0;
+  size_t b = 0, b2 = 0;
   vmps_workspace_bytes(std::max<uint64_t>(n_local, 1), kt, hv, S, &b);
+  vmps_merge_runs_bounded_workspace_bytes(std::max<uint64_t>(n_local, 1), kt, hv, 2, S, &b2);
+  b = std::max(b, b2);
   L.C = std::max<uint64_t>(1, (uint64_t)S / 2);
   const size_t w = kbytes(kt) + (hv ? 4 : 0);
   L.stage = al(2 * L.C * w + 64);
@@ -738,7 +740,11 @@ vmps_status_t sort_dist_bounded(vmps_comm_t c, void* keys, uint32_t* vals, uint6
         if (hv) VK(d2d(vals + r0 + a, sv_in, m * 4, s));
       }
     }
-    if (cnt) VK(local_sort(nullptr));  // two sorted runs -> one (stable, ties to the lower run)
+    if (cnt) {  // two sorted runs -> one: the bounded merge of given runs (ties to the first run)
+      const uint64_t runs[2] = {0, me == lower ? nA - cnt : cnt};
+      if (hv) VK(vmps_merge_runs_bounded(keys, vals, n_local, kt, runs, 2, S, big, big_bytes, s));
+      else VK(vmps_merge_runs_bounded(keys, nullptr, n_local, kt, runs, 2, S, big, big_bytes, s));
+    }
     quiet = swapped ? 0 : quiet + 1;
   }
   if (quiet < 2) { c_err = "internal: merge-split phases did not converge"; return VMPS_ERR_INTERNAL; }

@@ -181,3 +181,29 @@ def test_bounded_chunked(vm, chunk, n, dtype):
     assert st["scratch_bytes"] <= S * w
     st1 = vm.sort_(W.from_numpy(keys, "cuda"), W.from_numpy(vals, "cuda"), scratch=S, stats=True)
     assert meta_chunked < st1["metadata_bytes"]
+
+
+@pytest.mark.parametrize("nruns,n,dtype", [(2, 400_000, np.uint32), (5, 300_001, np.uint64), (9, 200_000, np.float32)])
+def test_merge_runs_bounded(vm, nruns, n, dtype):
+    """vmps_merge_runs_bounded (the multi-GPU bounded protocol's re-merge):
+    adjacent sorted runs merged in place within the scratch cap, ties to the
+    earlier run -- the stable sort of the concatenation (oracle)."""
+    rng = np.random.default_rng(nruns * 7 + n)
+    keys = _structured(rng, n, dtype)
+    cuts = sorted(set(int(c) for c in rng.integers(1, n, nruns - 1)))
+    starts = [0] + cuts
+    for a, b in zip(starts, starts[1:] + [n]):  # sort each run (stable, by the key order)
+        idx = np.argsort(R_image(keys[a:b]), kind="stable")
+        keys[a:b] = keys[a:b][idx]
+    vals = np.arange(n, dtype=np.uint32)
+    ko, vo, _, _ = oracle.sort(keys, vals)
+    k, v = W.from_numpy(keys, "cuda"), W.from_numpy(vals, "cuda")
+    vm.merge_runs_bounded(k, v, starts, scratch=cap(n))
+    torch.cuda.synchronize()
+    assert W.to_numpy(k).view(np.uint8).tobytes() == ko.view(np.uint8).tobytes()
+    assert (W.to_numpy(v) == vo).all()
+
+
+def R_image(a):
+    from tests.test_dist import image_np
+    return image_np(a)
