@@ -3,6 +3,7 @@
 // one partition + one merge launch per tree level.  No host synchronisation
 // happens between launches; only h_stats / h_num_runs read results back.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -169,6 +170,7 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
   for (int l = 0; l <= t.chain_levels; ++l) t.chain_entry[l] = (uint64_t*)take((size_t)t.chain_m[l] * 8);
   t.run_start = (uint32_t*)take(R * 4);
   t.run_kind = (uint8_t*)take(R);
+  t.gpos = c.given_runs ? (uint64_t*)take(R * 8) : nullptr;
   t.scalars = (uint32_t*)take(SC_COUNT * 4 + 64);
   t.power = (uint8_t*)take(R);
   t.seg_l = (uint32_t*)take(R * 4);
@@ -352,6 +354,32 @@ static bool debug_sync() {
   return g_debug_sync == 1;
 }
 
+// VMPS_BD_TRACE=1: host wall time per phase of the scratch-bounded mode
+// (stream synchronised at each phase edge), printed to stderr per sort.
+struct BdTrace {
+  double t[8];
+  long n[8];
+};
+static thread_local BdTrace g_bdt;
+static int g_bd_trace = -1;
+static bool bd_trace() {
+  if (g_bd_trace < 0) {
+    const char* e = getenv("VMPS_BD_TRACE");
+    g_bd_trace = (e && e[0] == '1') ? 1 : 0;
+  }
+  return g_bd_trace == 1;
+}
+static double bd_now(cudaStream_t s) {
+  if (!bd_trace()) return 0.0;
+  cudaStreamSynchronize(s);
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static void bd_add(int slot, double t0, cudaStream_t s) {
+  if (!bd_trace()) return;
+  g_bdt.t[slot] += bd_now(s) - t0;
+  g_bdt.n[slot]++;
+}
+
 #define LAUNCH(kern, grid, block, smem, stream, ...)                              \
   do {                                                                             \
     kern<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                      \
@@ -413,23 +441,41 @@ static vmps_status_t front_half(const Work& w, const void* keys, cudaStream_t s)
 }
 
 
-// Plan front half for given runs (the chunked scratch-bounded mode's top
-// level): run starts uploaded (ascending runs, sentinel n), then the same
-// powers / segments / parents / depths as front_half.
-static vmps_status_t front_half_given(const Work& w, const uint32_t* h_runs, uint32_t r, cudaStream_t s) {
+// Given runs (the dyadic-cell scratch-bounded mode and the bounded merge of
+// given runs): r runs at positions rel[0..r) of the sub-array (rel[r] = its
+// length), their kinds (NULL: all ascending), and optionally their global
+// positions gpos[0..r] in an array of n_glob elements -- then the node powers
+// are the whole array's (P:445-446 with the global n), so the sub-array's
+// tree is exactly the whole plan's subtree over these runs.
+struct GivenRuns {
+  const uint32_t* rel;
+  const uint8_t* kinds;
+  const uint64_t* gpos;
+  uint64_t n_glob;
+  uint32_t r;
+};
+
+static vmps_status_t front_half_given(const Work& w, const GivenRuns& G, cudaStream_t s) {
+  const uint32_t r = G.r;
   VMPS_CK(cudaMemsetAsync(w.scalars, 0, SC_COUNT * 4, s));
   VMPS_CK(cudaMemsetAsync(w.counters, 0, 8 * 8, s));
-  VMPS_CK(cudaMemcpyAsync(w.run_start, h_runs, (size_t)(r + 1) * 4, cudaMemcpyHostToDevice, s));
-  VMPS_CK(cudaMemsetAsync(w.run_kind, 0, r, s));
+  VMPS_CK(cudaMemcpyAsync(w.run_start, G.rel, (size_t)(r + 1) * 4, cudaMemcpyHostToDevice, s));
+  if (G.kinds) VMPS_CK(cudaMemcpyAsync(w.run_kind, G.kinds, r, cudaMemcpyHostToDevice, s));
+  else VMPS_CK(cudaMemsetAsync(w.run_kind, 0, r, s));
   VMPS_CK(cudaMemcpyAsync(w.scalars + SC_RUNS, &r, 4, cudaMemcpyHostToDevice, s));
   const unsigned g = grid_for(w.rmax);
-  LAUNCH(k_powers_seg<uint32_t>, g, 256, 0, s, w.run_start, (uint64_t)w.n, w.scalars, w.power, w.seg_l, w.seg_r);
+  if (G.gpos) {
+    VMPS_CK(cudaMemcpyAsync(w.gpos, G.gpos, (size_t)(r + 1) * 8, cudaMemcpyHostToDevice, s));
+    LAUNCH(k_powers_seg<uint64_t>, g, 256, 0, s, w.gpos, G.n_glob, w.scalars, w.power, w.seg_l, w.seg_r);
+  } else {
+    LAUNCH(k_powers_seg<uint32_t>, g, 256, 0, s, w.run_start, (uint64_t)w.n, w.scalars, w.power, w.seg_l, w.seg_r);
+  }
   LAUNCH(k_parent_init, g, 256, 0, s, w.scalars, w.power, w.seg_l, w.seg_r, w.parent, w.anc[0], w.dep[0]);
   for (int rnd = 0; rnd < 6; ++rnd) {
     int a = rnd & 1;
     LAUNCH(k_jump, g, 256, 0, s, w.scalars, w.anc[a], w.dep[a], w.anc[a ^ 1], w.dep[a ^ 1]);
   }
-  VMPS_CK(cudaStreamSynchronize(s));  // the host run list is the caller's stack memory
+  VMPS_CK(cudaStreamSynchronize(s));  // the host run lists are the caller's
   return launch_check();
 }
 
@@ -452,6 +498,7 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
   // legacy stream, which cannot be captured) and replayed on `s`.
   cudaGraph_t rounds_graph = nullptr;
   cudaGraphExec_t rounds_exec = nullptr;
+  double t0 = bd_now(s);
   if (!debug_sync()) {
     cudaStream_t cap = aux_stream();
     bool ok = cap && cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
@@ -474,6 +521,8 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
     cudaGraph_t& g; cudaGraphExec_t& e;
     ~GraphGuard() { if (e) cudaGraphExecDestroy(e); if (g) cudaGraphDestroy(g); }
   } guard{rounds_graph, rounds_exec};
+  bd_add(0, t0, s);
+  t0 = bd_now(s);
   for (int p = p_hi; p >= 1; --p) {
     LAUNCH(k_bd_flags, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.fuse_z, p, w.rmax,
            w.bflag);
@@ -527,6 +576,8 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
     // next level starts its dirty list from zero
     VMPS_CK(cudaMemsetAsync(&st->w, 0, 4, s));
   }
+  bd_add(1, t0, s);
+  t0 = bd_now(s);
   // final Copy: permute the blocks into physical order
   LAUNCH(k_bd_inverse, grid_for(w.NB + w.F), 256, 0, s, w.Tin, w.NB, w.NB + w.F, w.inv);
   LAUNCH(k_bd_inverse2, gNB, 256, 0, s, w.Tin, w.NB, w.inv);
@@ -542,6 +593,7 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
   VMPS_CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
   VMPS_CK(cudaStreamSynchronize(s));
   if (hs.err) { g_err = "scratch budget too small for the bounded Copy"; return VMPS_ERR_BUDGET; }
+  bd_add(2, t0, s);
   return launch_check();
 }
 
@@ -581,13 +633,14 @@ static bool kernel_attrs_set[MAX_DEV][3][2] = {};
 
 template <int KT, bool HV>
 static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaStream_t s,
-                               vmps_stats_t* st, const uint32_t* h_runs = nullptr) {
+                               vmps_stats_t* st, const GivenRuns* G = nullptr) {
   using K = typename KeyTraits<KT>::K;
   prof_reset();
+  const double g_bdt_front = bd_now(s);
   NvtxRange nv_sort("vmps_sort");
   NvtxRange nv_plan("vmps_plan");
   g_prof_mark[0] = prof_event(s);
-  vmps_status_t rc = h_runs ? front_half_given(w, h_runs, w.rmax - 2, s) : front_half<KT>(w, keys, s);
+  vmps_status_t rc = G ? front_half_given(w, *G, s) : front_half<KT>(w, keys, s);
   if (rc != VMPS_OK) return rc;
   const uint32_t* dep = w.dep[0];
   const unsigned g = grid_for(w.rmax);
@@ -666,11 +719,12 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   NvtxRange nv_merge("vmps_merge");
 
   // level merges, highest power first (children before parents, F3)
-  double lg = std::log2(2.0 * (double)w.n / (double)w.fuse_z);
+  double lg = std::log2(2.0 * (double)(G && G->gpos ? G->n_glob : (uint64_t)w.n) / (double)w.fuse_z);
   int p_hi = (int)std::ceil(lg) + 1;
   if (p_hi > LEVEL_SLOTS - 2) p_hi = LEVEL_SLOTS - 2;
   if (p_hi < 1) p_hi = 1;
   if (w.bounded) {
+    bd_add(3, g_bdt_front, s);
     rc = bounded_levels<KT, HV>(w, k0, v0, p_hi, s);
     if (rc != VMPS_OK) return rc;
     g_prof_mark[3] = prof_event(s);
@@ -853,25 +907,67 @@ static vmps_status_t check_common(const void* keys, const void* vals, uint64_t n
 
 extern "C" {
 
-// Chunked scratch-bounded mode (large n): the array is sorted in chunks of
-// BD_CHUNK elements, each by the bounded engine (Powersort of the chunk's
-// runs), then the sorted chunks are merged by the same engine along the
-// Powersort tree of the chunk boundaries (given runs, no run detection).  The
-// per-run metadata then scales with the chunk (n_chunk / minrun runs) and
-// the number of chunks instead of n / minrun: 3.4 GB -> ~60 MB at 2^30.  The
-// output is the unique stable sort, identical to the one-piece mode; the
-// executed merge tree differs where a natural run crosses a chunk edge.
+// Dyadic-cell scratch-bounded mode (large n): Alg. 1 run over
+// cells.  With q = ceil(log2(n / CELL)), every node of power > q lies inside
+// one dyadic cell of level q of the midpoint space (its runs' midpoints share
+// the node's cell of level p - 1 >= q), so the runs whose midpoints fall in a
+// cell form one subtree of the whole plan, and the boundaries between cells
+// carry the powers <= q.  The array is scanned left to right in detection
+// chunks (run-detection transfer table + run emission per chunk, the chain
+// state carried across chunks, original edge keys kept aside); each cell,
+// once its last run's end is known, is sorted by the bounded engine from its
+// given runs with the global powers (exactly the whole plan's subtree), and
+// the cell results go through Alg. 1's stack with the boundary powers
+// computed from the original runs (each pop a bounded merge of two runs).
+// The executed merges are exactly Alg. 1's plan (M equal to the one-piece
+// mode), while the device metadata scales with a cell (runs with midpoints in
+// it <= CELL / minrun + 2) and n / P block-table entries instead of n / minrun:
+// 3.4 GB -> tens of MB at 2^30.
 #ifndef VMPS_BD_CHUNK
 #define VMPS_BD_CHUNK (1u << 24)
 #endif
-static uint64_t g_bd_chunk = VMPS_BD_CHUNK;  // test hook vmps_test_set_bd_chunk
-#define BD_CHUNK g_bd_chunk
-static bool bd_chunked(uint64_t n, int64_t scratch, int hv) { return scratch >= 0 && hv >= 0 && n > 2 * BD_CHUNK; }
-static size_t bd_chunked_bytes(uint64_t n, int kt, int hv, int64_t scratch) {
-  Cfg cc = make_cfg(BD_CHUNK, kt, hv, scratch);
-  Cfg ct = make_cfg(n, kt, hv, scratch);
-  ct.given_runs = (uint32_t)((n + BD_CHUNK - 1) / BD_CHUNK);
-  return std::max(carve(cc, nullptr, nullptr), carve(ct, nullptr, nullptr));
+static uint64_t g_bd_chunk = VMPS_BD_CHUNK;  // cell size target (test hook vmps_test_set_bd_chunk)
+static bool bd_chunked(uint64_t n, int64_t scratch, int hv) { return scratch >= 0 && hv >= 0 && n > 2 * g_bd_chunk; }
+static uint32_t bd_cell_level(uint64_t n) {
+  uint32_t q = 0;
+  while ((n >> q) > g_bd_chunk) ++q;
+  return q;
+}
+struct CellLayout {
+  size_t det_ws, det_out, sort_ws, total;
+  uint32_t det;  // detection chunk (elements)
+};
+static CellLayout bd_cell_layout(uint64_t n, int kt, int hv, int64_t scratch) {
+  CellLayout L{};
+  Cfg c0 = make_cfg(n, kt, hv, scratch);
+  L.det = (uint32_t)std::min<uint64_t>(g_bd_chunk, n);
+  size_t b = 0;
+  vmps_shard_workspace_bytes(L.det, (vmps_key_t)kt, c0.minrun, &b);
+  L.det_ws = align_up(b);
+  const uint64_t rdet = L.det / std::max<uint32_t>(c0.minrun, 1) + 4;
+  L.det_out = align_up(rdet * 8) + align_up(rdet + 16) + align_up((size_t)3 * 64 * 8) + align_up(64);
+  // a cell's sort: its runs (<= cell / minrun + 2), blocks of at most the whole array
+  Cfg cs = make_cfg(n, kt, hv, scratch);
+  cs.given_runs = (uint32_t)(((n >> bd_cell_level(n)) + 1) / std::max<uint32_t>(c0.minrun, 1) + 4);
+  L.sort_ws = align_up(carve(cs, nullptr, nullptr));
+  L.total = L.det_ws + L.det_out + L.sort_ws + 256;
+  return L;
+}
+
+// The power of the boundary between [i, j) and [j, k) in an array of n
+// (P:445-446): one plus the common leading bits of the two scaled midpoints.
+static uint32_t host_power(uint64_t n, uint64_t i, uint64_t j, uint64_t k) {
+  const unsigned __int128 N2 = (unsigned __int128)2 * n;
+  unsigned __int128 A = (unsigned __int128)(i + j), B = (unsigned __int128)(j + k);
+  uint32_t p = 0;
+  for (;;) {
+    ++p;
+    A <<= 1;
+    B <<= 1;
+    const bool ba = A >= N2, bb = B >= N2;
+    if (ba != bb) return p;
+    if (ba) { A -= N2; B -= N2; }
+  }
 }
 
 vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, int64_t scratch_elems,
@@ -881,7 +977,7 @@ vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, int6
   if (n > VMPS_MAX_N) return VMPS_ERR_INVALID_ARG;
   if (n <= 1) { *h_bytes = 256; return VMPS_OK; }
   const int hv = has_vals < 0 ? -1 : (has_vals ? 1 : 0);
-  if (bd_chunked(n, scratch_elems, hv)) { *h_bytes = bd_chunked_bytes(n, kt, hv, scratch_elems) + 256; return VMPS_OK; }
+  if (bd_chunked(n, scratch_elems, hv)) { *h_bytes = bd_cell_layout(n, kt, hv, scratch_elems).total + 256; return VMPS_OK; }
   Cfg c = make_cfg(n, kt, hv, scratch_elems);
   *h_bytes = carve(c, nullptr, nullptr) + 256;
   return VMPS_OK;
@@ -889,59 +985,190 @@ vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, int6
 
 }  // extern "C"
 
+static vmps_status_t merge_runs_bounded_impl(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt,
+                                             const uint64_t* h_run_start, uint32_t nruns, int64_t scratch_elems,
+                                             void* ws, size_t ws_bytes, void* stream);
+
 template <int KT, bool HV>
-static vmps_status_t sort_bounded_chunked(void* keys, uint32_t* vals, uint64_t n, int64_t S, char* base,
-                                          cudaStream_t s, vmps_stats_t* st) {
+static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, int64_t S, char* base,
+                                        cudaStream_t s, vmps_stats_t* st) {
+  using K = typename KeyTraits<KT>::K;
   const size_t kb = key_bytes(KT);
-  const uint32_t nch = (uint32_t)((n + BD_CHUNK - 1) / BD_CHUNK);
-  vmps_stats_t acc;
-  memset(&acc, 0, sizeof(acc));
-  size_t peak = 0, scratch_b = 0;
-  for (uint32_t c = 0; c < nch; ++c) {
-    const uint64_t off = (uint64_t)c * BD_CHUNK, nc = std::min<uint64_t>(BD_CHUNK, n - off);
-    if (nc <= 1) continue;
-    Cfg cc = make_cfg(nc, KT, HV ? 1 : 0, S);
-    Work w;
-    peak = std::max(peak, carve(cc, &w, base));
-    vmps_stats_t cs;
-    vmps_status_t rc = sort_impl<KT, HV>(w, (char*)keys + off * kb, HV ? vals + off : nullptr, s, st ? &cs : nullptr);
+  const CellLayout L = bd_cell_layout(n, KT, HV ? 1 : 0, S);
+  const Cfg c0 = make_cfg(n, KT, HV ? 1 : 0, S);
+  const uint32_t minrun = c0.minrun, ns = 3 * minrun, H = minrun + 8;
+  const uint32_t q = bd_cell_level(n);
+  char* det_ws = base;
+  char* det_out = base + L.det_ws;
+  char* sort_ws = det_out + L.det_out;
+  const uint64_t rdet = L.det / std::max<uint32_t>(minrun, 1) + 4;
+  uint64_t* d_rs = (uint64_t*)det_out;
+  uint8_t* d_rk = (uint8_t*)(det_out + align_up(rdet * 8));
+  uint64_t* d_tab = (uint64_t*)(det_out + align_up(rdet * 8) + align_up(rdet + 16));
+  K* d_prev = (K*)(det_out + align_up(rdet * 8) + align_up(rdet + 16) + align_up((size_t)3 * 64 * 8));
+  std::vector<uint64_t> R;   // run starts of the unprocessed runs (global)
+  std::vector<uint8_t> RK;   // their kinds
+  std::vector<uint64_t> tab(ns);
+  uint64_t M = 0, rounds = 0, runs = 0, rev = 0, ext = 0;
+  uint32_t maxp = 0, lv = 0;
+  size_t peak = L.total;
+  auto cell_of = [&](uint64_t a, uint64_t b) -> uint64_t {  // dyadic cell (level q) of the midpoint of [a, b)
+    return (uint64_t)(((unsigned __int128)(a + b) << q) / ((unsigned __int128)2 * n));
+  };
+  // Alg. 1 over the cell results: segments [a, b) with, for the boundary
+  // powers, the first run's end and the last run's start (original runs)
+  struct Seg { uint64_t a, b, first_end, last_start; uint32_t pw; };
+  std::vector<Seg> stk;
+  bool have_curr = false;
+  Seg curr{};
+  auto merge2 = [&](const Seg& x, const Seg& y) -> vmps_status_t {  // [x.a, x.b) (+) [x.b, y.b)
+    const uint64_t runs2[2] = {0, x.b - x.a};
+    const uint64_t len = y.b - x.a;
+    M += len;
+    const double t0 = bd_now(s);
+    struct Add { double t0; cudaStream_t s; ~Add() { bd_add(6, t0, s); } } add{t0, s};
+    return merge_runs_bounded_impl((char*)keys + x.a * kb, HV ? vals + x.a : nullptr, len, (vmps_key_t)KT, runs2, 2,
+                                   S, sort_ws, L.sort_ws, s);
+  };
+  auto push_cell = [&](const Seg& nx) -> vmps_status_t {
+    if (!have_curr) { curr = nx; have_curr = true; return VMPS_OK; }
+    const uint32_t p = host_power(n, curr.last_start, curr.b, nx.first_end);  // Alg. 1 line 6
+    maxp = std::max(maxp, p);
+    while (!stk.empty() && stk.back().pw >= p) {  // lines 7-9
+      vmps_status_t rc = merge2(stk.back(), curr);
+      if (rc != VMPS_OK) return rc;
+      curr = Seg{stk.back().a, curr.b, stk.back().first_end, curr.last_start, 0};
+      stk.pop_back();
+    }
+    curr.pw = p;
+    stk.push_back(curr);  // line 10
+    curr = nx;            // line 11
+    return VMPS_OK;
+  };
+  // sort the cell made of runs R[0, m) (run m-1 ends at end); consume them
+  auto do_cell = [&](size_t m, uint64_t end) -> vmps_status_t {
+    const uint64_t a = R[0];
+    std::vector<uint32_t> rel(m + 1);
+    std::vector<uint64_t> gp(m + 1);
+    for (size_t i = 0; i < m; ++i) { rel[i] = (uint32_t)(R[i] - a); gp[i] = R[i]; }
+    rel[m] = (uint32_t)(end - a);
+    gp[m] = end;
+    const bool trivial = m == 1 && RK[0] == 0;  // one ascending run: already sorted
+    if (!trivial) {
+      Cfg cc = make_cfg(end - a, KT, HV ? 1 : 0, S);
+      cc.given_runs = (uint32_t)m;
+      Work w;
+      const size_t need = carve(cc, &w, nullptr);
+      if (need > L.sort_ws) { g_err = "internal: cell workspace"; return VMPS_ERR_INTERNAL; }
+      carve(cc, &w, sort_ws);
+      const GivenRuns G{rel.data(), RK.data(), gp.data(), n, (uint32_t)m};
+      vmps_stats_t cs;
+      const double t0 = bd_now(s);
+      vmps_status_t rc = sort_impl<KT, HV>(w, (char*)keys + a * kb, HV ? vals + a : nullptr, s, st ? &cs : nullptr, &G);
+      bd_add(5, t0, s);
+      if (rc != VMPS_OK) return rc;
+      if (st) {
+        M += cs.merge_cost_M;
+        rounds += cs.rounds;
+        maxp = std::max(maxp, cs.max_power);
+        lv = std::max(lv, cs.levels_executed);
+      }
+    }
+    runs += m;
+    for (size_t i = 0; i < m; ++i) {
+      if (RK[i] & 1u) rev += (i + 1 < m ? R[i + 1] : end) - R[i];
+      if (RK[i] & 2u) ++ext;
+    }
+    const Seg nx{a, end, m > 1 ? R[1] : end, R[m - 1], 0};
+    R.erase(R.begin(), R.begin() + m);
+    RK.erase(RK.begin(), RK.begin() + m);
+    return push_cell(nx);
+  };
+  // scan: detection chunk by chunk, cells processed as soon as they close
+  uint32_t state = 0;  // START(0)
+  if (bd_trace()) memset(&g_bdt, 0, sizeof(g_bdt));
+  const double t_all = bd_now(s);
+  for (uint64_t off = 0; off < n; off += L.det) {
+    const double t_det = bd_now(s);
+    const uint64_t nd = std::min<uint64_t>(L.det, n - off);
+    const uint64_t after = n - off - nd;
+    const uint32_t n_halo = (uint32_t)std::min<uint64_t>(H, after);
+    const uint64_t rem = n - off;
+    const uint32_t n_end = rem >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)rem;
+    const K* kk = (const K*)((const char*)keys + off * kb);
+    vmps_status_t rc = vmps_shard_chain(kk, nd, (vmps_key_t)KT, minrun, n_end, off ? d_prev : nullptr,
+                                        n_halo ? (const void*)(kk + nd) : nullptr, n_halo, d_tab, det_ws, L.det_ws, s);
     if (rc != VMPS_OK) return rc;
-    if (st) {
-      acc.runs += cs.runs;
-      acc.merge_cost_M += cs.merge_cost_M;
-      acc.fused_M += cs.fused_M;
-      acc.reversed_elems += cs.reversed_elems;
-      acc.extended_runs += cs.extended_runs;
-      acc.rounds += cs.rounds;
-      acc.max_power = std::max(acc.max_power, cs.max_power);
-      acc.levels_executed = std::max(acc.levels_executed, cs.levels_executed);
-      acc.minrun = cs.minrun;
-      scratch_b = std::max<size_t>(scratch_b, cs.scratch_bytes);
+    VMPS_CK(cudaMemcpyAsync(tab.data(), d_tab, (size_t)ns * 8, cudaMemcpyDeviceToHost, s));
+    VMPS_CK(cudaStreamSynchronize(s));
+    const uint64_t v = tab[state];
+    const uint32_t cnt = (uint32_t)(v & 0xFFFFFFFFull);
+    if (cnt) {
+      rc = vmps_shard_runs(kk, nd, (vmps_key_t)KT, minrun, n_end, off ? d_prev : nullptr,
+                           n_halo ? (const void*)(kk + nd) : nullptr, n_halo, state, cnt, off, d_rs, d_rk, det_ws,
+                           L.det_ws, s);
+      if (rc != VMPS_OK) return rc;
+      const size_t o = R.size();
+      R.resize(o + cnt);
+      RK.resize(o + cnt);
+      VMPS_CK(cudaMemcpyAsync(R.data() + o, d_rs, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s));
+      VMPS_CK(cudaMemcpyAsync(RK.data() + o, d_rk, cnt, cudaMemcpyDeviceToHost, s));
+    }
+    state = (uint32_t)(v >> 32);
+    // the original last key of this chunk (the next chunk's descent bit at its start)
+    VMPS_CK(cudaMemcpyAsync(d_prev, kk + nd - 1, kb, cudaMemcpyDeviceToDevice, s));
+    VMPS_CK(cudaStreamSynchronize(s));
+    bd_add(4, t_det, s);
+    // close every cell whose last run's end is known: runs R[0, m) share a
+    // cell and run m (whose start is the end of run m-1) lies in a later one
+    for (;;) {
+      if (R.size() < 2) break;
+      const uint64_t c0c = cell_of(R[0], R[1]);
+      size_t m = 1;
+      while (m + 1 < R.size() && cell_of(R[m], R[m + 1]) == c0c) ++m;
+      if (m + 1 >= R.size()) break;  // run m's end (R[m+1]) unknown or run m still in the cell
+      rc = do_cell(m, R[m]);
+      if (rc != VMPS_OK) return rc;
     }
   }
-  // top level: the sorted chunks as runs, merged along their Powersort tree
-  std::vector<uint32_t> runs(nch + 1);
-  for (uint32_t c = 0; c < nch; ++c) runs[c] = (uint32_t)((uint64_t)c * BD_CHUNK);
-  runs[nch] = (uint32_t)n;
-  Cfg ct = make_cfg(n, KT, HV ? 1 : 0, S);
-  ct.given_runs = nch;
-  Work w;
-  peak = std::max(peak, carve(ct, &w, base));
-  vmps_stats_t ts;
-  vmps_status_t rc = sort_impl<KT, HV>(w, keys, HV ? vals : nullptr, s, st ? &ts : nullptr, runs.data());
-  if (rc != VMPS_OK) return rc;
+  // the array is done: remaining runs end at n
+  while (!R.empty()) {
+    const auto end_of = [&](size_t i) { return i + 1 < R.size() ? R[i + 1] : n; };
+    const uint64_t c0c = cell_of(R[0], end_of(0));
+    size_t m = 1;
+    while (m < R.size() && cell_of(R[m], end_of(m)) == c0c) ++m;
+    vmps_status_t rc = do_cell(m, m < R.size() ? R[m] : n);
+    if (rc != VMPS_OK) return rc;
+  }
+  // lines 12-13: pop and merge what is left
+  while (!stk.empty()) {
+    vmps_status_t rc = merge2(stk.back(), curr);
+    if (rc != VMPS_OK) return rc;
+    curr = Seg{stk.back().a, curr.b, stk.back().first_end, curr.last_start, 0};
+    stk.pop_back();
+  }
+  if (bd_trace()) {
+    bd_add(7, t_all, s);
+    static const char* nm[8] = {"graph", "levels", "copy", "front+leaf", "detect", "cell_sorts", "top_merges", "all"};
+    for (int i = 0; i < 8; ++i) fprintf(stderr, "vmps bd trace: %-10s %9.1f ms  %ld\n", nm[i], g_bdt.t[i], g_bdt.n[i]);
+  }
   if (st) {
-    acc.merge_cost_M += ts.merge_cost_M;
-    acc.fused_M += ts.fused_M;
-    acc.rounds += ts.rounds;
-    acc.levels_executed += ts.levels_executed;
-    acc.n = n;
-    acc.merges = acc.runs ? acc.runs - 1 : 0;
-    acc.block_elems = ts.block_elems;
-    acc.scratch_bytes = std::max<size_t>(scratch_b, ts.scratch_bytes);
-    acc.peak_extra_device_bytes = peak;
-    acc.metadata_bytes = peak - acc.scratch_bytes;
-    *st = acc;
+    VMPS_CK(cudaStreamSynchronize(s));
+    memset(st, 0, sizeof(*st));
+    st->n = n;
+    st->runs = runs;
+    st->merges = runs ? runs - 1 : 0;
+    st->merge_cost_M = M;
+    st->reversed_elems = rev;
+    st->extended_runs = ext;
+    st->max_power = maxp;
+    st->levels_executed = lv;
+    st->minrun = minrun;
+    st->block_elems = c0.P;
+    st->rounds = rounds;
+    st->scratch_bytes = (uint64_t)c0.F * c0.P * (kb + (HV ? 4 : 0));
+    st->peak_extra_device_bytes = peak;
+    st->metadata_bytes = peak - st->scratch_bytes;
   }
   return VMPS_OK;
 }
@@ -967,7 +1194,7 @@ static vmps_status_t sort_any(void* keys, uint32_t* vals, uint64_t n, vmps_key_t
     return VMPS_ERR_BUDGET;
   }
   if (bd_chunked(n, scratch_elems, hv)) {
-    const size_t need = bd_chunked_bytes(n, kt, hv, scratch_elems);
+    const size_t need = bd_cell_layout(n, kt, hv, scratch_elems).total;
     char* base = (char*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
     if (!ws || ws_bytes < need || (size_t)(base - (char*)ws) + need > ws_bytes) {
       g_err = "workspace too small";
@@ -976,14 +1203,14 @@ static vmps_status_t sort_any(void* keys, uint32_t* vals, uint64_t n, vmps_key_t
     cudaStream_t s = (cudaStream_t)stream;
     switch (kt) {
       case VMPS_KEY_U32:
-        return hv ? sort_bounded_chunked<VMPS_KEY_U32, true>(keys, vals, n, scratch_elems, base, s, h_stats)
-                  : sort_bounded_chunked<VMPS_KEY_U32, false>(keys, vals, n, scratch_elems, base, s, h_stats);
+        return hv ? sort_bounded_cells<VMPS_KEY_U32, true>(keys, vals, n, scratch_elems, base, s, h_stats)
+                  : sort_bounded_cells<VMPS_KEY_U32, false>(keys, vals, n, scratch_elems, base, s, h_stats);
       case VMPS_KEY_U64:
-        return hv ? sort_bounded_chunked<VMPS_KEY_U64, true>(keys, vals, n, scratch_elems, base, s, h_stats)
-                  : sort_bounded_chunked<VMPS_KEY_U64, false>(keys, vals, n, scratch_elems, base, s, h_stats);
+        return hv ? sort_bounded_cells<VMPS_KEY_U64, true>(keys, vals, n, scratch_elems, base, s, h_stats)
+                  : sort_bounded_cells<VMPS_KEY_U64, false>(keys, vals, n, scratch_elems, base, s, h_stats);
       default:
-        return hv ? sort_bounded_chunked<VMPS_KEY_F32, true>(keys, vals, n, scratch_elems, base, s, h_stats)
-                  : sort_bounded_chunked<VMPS_KEY_F32, false>(keys, vals, n, scratch_elems, base, s, h_stats);
+        return hv ? sort_bounded_cells<VMPS_KEY_F32, true>(keys, vals, n, scratch_elems, base, s, h_stats)
+                  : sort_bounded_cells<VMPS_KEY_F32, false>(keys, vals, n, scratch_elems, base, s, h_stats);
     }
   }
   Work w;
@@ -1351,6 +1578,16 @@ vmps_status_t vmps_merge_runs_bounded(void* keys, uint32_t* vals, uint64_t n, vm
                                       size_t ws_bytes, void* stream) {
   vmps_status_t rc = check_common(keys, vals, n, kt);
   if (rc != VMPS_OK) return rc;
+  return merge_runs_bounded_impl(keys, vals, n, kt, h_run_start, nruns, scratch_elems, ws, ws_bytes, stream);
+}
+
+}  // extern "C"
+
+// (no alignment requirement: the bounded engine's kernels access elements
+// one by one, so sub-arrays at any element offset are fine)
+static vmps_status_t merge_runs_bounded_impl(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt,
+                                             const uint64_t* h_run_start, uint32_t nruns, int64_t scratch_elems,
+                                             void* ws, size_t ws_bytes, void* stream) {
   if (scratch_elems < 0 || !h_run_start || nruns < 1) { g_err = "bad arguments"; return VMPS_ERR_INVALID_ARG; }
   if (n <= 1) return VMPS_OK;
   // distinct starts inside [0, n), ascending from 0
@@ -1378,20 +1615,23 @@ vmps_status_t vmps_merge_runs_bounded(void* keys, uint32_t* vals, uint64_t n, vm
   }
   carve(c, &w, base);
   cudaStream_t s = (cudaStream_t)stream;
+  const GivenRuns G{runs.data(), nullptr, nullptr, n, r};
   switch (kt) {
     case VMPS_KEY_U32:
-      return hv ? sort_impl<VMPS_KEY_U32, true>(w, keys, vals, s, nullptr, runs.data())
-                : sort_impl<VMPS_KEY_U32, false>(w, keys, vals, s, nullptr, runs.data());
+      return hv ? sort_impl<VMPS_KEY_U32, true>(w, keys, vals, s, nullptr, &G)
+                : sort_impl<VMPS_KEY_U32, false>(w, keys, vals, s, nullptr, &G);
     case VMPS_KEY_U64:
-      return hv ? sort_impl<VMPS_KEY_U64, true>(w, keys, vals, s, nullptr, runs.data())
-                : sort_impl<VMPS_KEY_U64, false>(w, keys, vals, s, nullptr, runs.data());
+      return hv ? sort_impl<VMPS_KEY_U64, true>(w, keys, vals, s, nullptr, &G)
+                : sort_impl<VMPS_KEY_U64, false>(w, keys, vals, s, nullptr, &G);
     default:
-      return hv ? sort_impl<VMPS_KEY_F32, true>(w, keys, vals, s, nullptr, runs.data())
-                : sort_impl<VMPS_KEY_F32, false>(w, keys, vals, s, nullptr, runs.data());
+      return hv ? sort_impl<VMPS_KEY_F32, true>(w, keys, vals, s, nullptr, &G)
+                : sort_impl<VMPS_KEY_F32, false>(w, keys, vals, s, nullptr, &G);
   }
 }
 
-void vmps_test_set_bd_chunk(uint32_t chunk) { g_bd_chunk = chunk ? std::max<uint32_t>(chunk, 64u) : VMPS_BD_CHUNK; }
+extern "C" {
+
+void vmps_test_set_bd_chunk(uint32_t chunk) { g_bd_chunk = chunk ? std::max<uint32_t>(chunk, 4096u) : VMPS_BD_CHUNK; }
 
 void vmps_test_set_minrun(uint32_t minrun) { g_minrun_override = minrun > MAX_MINRUN ? MAX_MINRUN : minrun; }
 

@@ -126,6 +126,7 @@ struct Work {
   void* desc;            // TileDesc per tile of one level
   uint32_t part_cap;
   uint32_t* scan_tmp;    // block sums for scans
+  uint64_t* gpos;        // given-runs mode: global run starts (powers with the global n)
   unsigned long long* counters;  // [0] M, [1] fused M
   // two-level fused merges (engine4.cuh)
   int fuse2;

@@ -154,18 +154,31 @@ def test_bounded_blocks_below_minrun(vm):
     assert st["block_elems"] == 16 and st["minrun"] == 32
 
 
-@pytest.mark.parametrize("chunk,n,dtype", [(1 << 16, 1_000_003, np.uint32), (1 << 14, 300_000, np.uint64),
-                                           (1 << 15, 500_000, np.float32)])
-def test_bounded_chunked(vm, chunk, n, dtype):
-    """The chunked scratch-bounded mode (n > 2 chunks: chunks sorted by the
-    bounded engine, then merged along their Powersort tree): identical to the
-    oracle's stable sort; element scratch within the cap; plan metadata sized
-    by the chunk, not by n."""
+@pytest.mark.parametrize("chunk,n,dtype,kind", [(1 << 16, 1_000_003, np.uint32, "mixed"),
+                                                (1 << 14, 300_000, np.uint64, "structured"),
+                                                (1 << 15, 500_000, np.float32, "structured"),
+                                                (1 << 12, 200_000, np.uint32, "longruns")])
+def test_bounded_chunked(vm, chunk, n, dtype, kind):
+    """The dyadic-cell scratch-bounded mode (n > 2 cells: runs grouped by the
+    level-q dyadic cell of their midpoints, each cell's subtree sorted by the
+    bounded engine with the global powers, Alg. 1 over the cell results):
+    identical to the oracle's stable sort, with exactly the oracle's merge
+    cost M and run count (the executed tree is the whole plan); element
+    scratch within the cap; plan metadata sized by a cell, not by n."""
     rng = np.random.default_rng(chunk + n)
-    keys = _structured(rng, n, dtype)
+    if kind == "mixed":
+        keys = W.to_numpy(W.cfg5(n=n, device="cpu")[0])
+    elif kind == "longruns":  # runs much longer than a cell, ascending and strictly descending
+        keys = np.empty(n, np.uint32)
+        cuts = [0, 30_000, 90_000, 90_005, 150_000, n]
+        for q, (a, b) in enumerate(zip(cuts[:-1], cuts[1:])):
+            seg = np.sort(rng.integers(0, 1 << 31, b - a)).astype(np.uint32)
+            keys[a:b] = seg[::-1] if q % 2 else seg
+    else:
+        keys = _structured(rng, n, dtype)
     vals = np.arange(n, dtype=np.uint32)
     S = cap(n)
-    ko, vo, _, _ = oracle.sort(keys, vals)
+    ko, vo, _, ost = oracle.sort(keys, vals)
     try:
         vm.test_set_bd_chunk(chunk)
         k = W.from_numpy(keys, "cuda")
@@ -177,6 +190,7 @@ def test_bounded_chunked(vm, chunk, n, dtype):
         vm.test_set_bd_chunk(0)
     assert W.to_numpy(k).view(np.uint8).tobytes() == ko.view(np.uint8).tobytes()
     assert (W.to_numpy(v) == vo).all()
+    assert st["merge_cost_M"] == ost["merge_cost_M"] and st["runs"] == ost["runs"]
     w = keys.dtype.itemsize + 4
     assert st["scratch_bytes"] <= S * w
     st1 = vm.sort_(W.from_numpy(keys, "cuda"), W.from_numpy(vals, "cuda"), scratch=S, stats=True)
