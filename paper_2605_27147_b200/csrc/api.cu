@@ -251,12 +251,7 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.bdesc_cap = (uint32_t)(n / c.P + 4 * std::min<uint64_t>(n / c.fuse_z, (uint64_t)t.rmax) + 16);
     t.bdesc = take((size_t)t.bdesc_cap * sizeof(TileDesc));
     t.bstate = take(sizeof(BdState));
-    t.copy_batch = std::max<uint32_t>(1, c.F / 3);
-    t.clist1 = (uint32_t*)take((size_t)2 * t.copy_batch * 3 * 4 + 64);
-    t.clist2 = (uint32_t*)take((size_t)t.copy_batch * 3 * 4 + 64);
-    t.ncopy = (uint32_t*)take(64);
-    t.deferred = (uint32_t*)take((size_t)(2 * t.copy_batch + 8) * 4);
-    t.ndef = (uint32_t*)take(64);
+    t.cplists = (uint32_t*)take((size_t)2 * BD_CP_LIST * 4);
   }
   t.used_bytes = off;
   if (w) *w = t;
@@ -581,14 +576,27 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
   // final Copy: permute the blocks into physical order
   LAUNCH(k_bd_inverse, grid_for(w.NB + w.F), 256, 0, s, w.Tin, w.NB, w.NB + w.F, w.inv);
   LAUNCH(k_bd_inverse2, gNB, 256, 0, s, w.Tin, w.NB, w.inv);
-  VMPS_CK(cudaMemsetAsync(w.ndef, 0, 4, s));
-  const uint32_t B = w.copy_batch;
-  for (uint32_t q0 = 0; q0 < w.NB; q0 += B) {
-    const uint32_t q1 = std::min(w.NB, q0 + B);
-    LAUNCH(k_bd_copy_plan, 1, 32, 0, s, st, w.Tin, w.inv, w.pool, w.NB, w.P, w.n, (uint32_t)M.has_partial, q0,
-           q1, w.clist1, w.clist2, w.ncopy, w.deferred, w.ndef);
-    LAUNCH((k_bd_copy<KT, HV>), 2 * B, 256, 0, s, M, w.clist1, w.ncopy, 0);
-    LAUNCH((k_bd_copy<KT, HV>), B, 256, 0, s, M, w.clist2, w.ncopy, 1);
+  VMPS_CK(cudaMemsetAsync(&st->copy_q, 0, 4, s));
+  {
+    const int ds = dev_slot();
+    static bool copy_attr[MAX_DEV][3][2] = {};
+    static int copy_grid[MAX_DEV] = {};
+    if (!copy_attr[ds][KT][HV]) {
+      int per_sm = 0;
+      VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bd_copy_all<KT, HV>, BD_CP_THREADS, 0));
+      if (per_sm < 1) { g_err = "internal: Copy kernel not resident"; return VMPS_ERR_INTERNAL; }
+      copy_grid[ds] = nsm();
+      copy_attr[ds][KT][HV] = true;
+    }
+    BdMem<KT> Mc = M;
+    uint32_t* Tin = w.Tin;
+    uint32_t* inv = w.inv;
+    uint32_t* pool = w.pool;
+    uint32_t* lists = w.cplists;
+    void* args[] = {&Mc, &st, &Tin, &inv, &pool, &lists};
+    VMPS_CK(cudaLaunchCooperativeKernel((const void*)k_bd_copy_all<KT, HV>, dim3(copy_grid[ds]), dim3(BD_CP_THREADS),
+                                        args, 0, s));
+    ++g_nl;
   }
   VMPS_CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
   VMPS_CK(cudaStreamSynchronize(s));
@@ -727,6 +735,11 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
     bd_add(3, g_bdt_front, s);
     rc = bounded_levels<KT, HV>(w, k0, v0, p_hi, s);
     if (rc != VMPS_OK) return rc;
+    if (bd_trace() && !G) {  // one-piece bounded sort
+      static const char* nm[4] = {"graph", "levels", "copy", "front+leaf"};
+      for (int i = 0; i < 4; ++i) fprintf(stderr, "vmps bd trace: %-10s %9.1f ms  %ld\n", nm[i], g_bdt.t[i], g_bdt.n[i]);
+      memset(&g_bdt, 0, sizeof(g_bdt));
+    }
     g_prof_mark[3] = prof_event(s);
     return bounded_stats<HV>(w, st, s);
   }

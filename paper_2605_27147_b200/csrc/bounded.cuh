@@ -16,8 +16,10 @@
 #pragma once
 #include "engine.cuh"
 #include "plan.cuh"
+#include <cooperative_groups.h>
 
 namespace vmps {
+namespace cg = cooperative_groups;
 
 constexpr uint32_t BD_NONE = 0xFFFFFFFFu;
 
@@ -28,7 +30,7 @@ struct BdState {          // device-side round state (one per sort)
   uint32_t pool_count;    // free physical blocks
   uint32_t rounds;        // rounds executed (statistics)
   uint32_t copies;        // final Copy: block copies
-  uint32_t pad;
+  uint32_t copy_q;        // final Copy: virtual blocks [0, copy_q) are home
 };
 
 template <int KT>
@@ -351,74 +353,259 @@ __global__ void k_bd_inverse2(const uint32_t* __restrict__ Tin, uint32_t NB, uin
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < NB; v += gridDim.x * blockDim.x) inv[Tin[v]] = v;
 }
 
-// Plan one batch of virtual blocks [q0, q1) (one thread): copy list 1 stages
-// every misplaced block into a free block and evicts later blocks that occupy
-// a target; copy list 2 writes the staged blocks home.  Blocks released by the
-// previous batch are returned to the pool first.
-__global__ void k_bd_copy_plan(BdState* st, uint32_t* __restrict__ Tin, uint32_t* __restrict__ inv,
-                               uint32_t* __restrict__ pool, uint32_t NB, uint32_t P, uint32_t n, uint32_t has_partial,
-                               uint32_t q0, uint32_t q1, uint32_t* __restrict__ c1, uint32_t* __restrict__ c2,
-                               uint32_t* __restrict__ ncopy, uint32_t* __restrict__ deferred,
-                               uint32_t* __restrict__ ndef) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (uint32_t x = 0; x < *ndef; ++x) pool[st->pool_count++] = deferred[x];
-  *ndef = 0;
-  uint32_t n1 = 0, n2 = 0;
-  if (st->err) { ncopy[0] = ncopy[1] = 0; return; }
-  auto vlen = [&](uint32_t v) -> uint32_t { return v + 1 < NB ? P : n - v * P; };
-  // a free block usable as temporary storage: never an array block < q1
-  // (those are placed targets or this batch's targets); such blocks are dropped
-  auto pop = [&]() -> uint32_t {
-    while (st->pool_count) {
-      const uint32_t b = pool[--st->pool_count];
-      if (b >= q1) return b;
-    }
-    return BD_NONE;
-  };
-  for (uint32_t q = q0; q < q1; ++q) {
-    const uint32_t src = Tin[q];
-    if (src == q) continue;
-    // evict a later virtual block that lives in physical q
-    const uint32_t w = inv[q];
-    if (w != BD_NONE && w >= q1) {
-      const uint32_t e = pop();
-      if (e == BD_NONE) { st->err = 1; break; }
-      c1[3 * n1] = q; c1[3 * n1 + 1] = e; c1[3 * n1 + 2] = vlen(w); ++n1;
-      Tin[w] = e;
-      inv[e] = w;
-      inv[q] = BD_NONE;
-    }
-    const uint32_t tmp = pop();
-    if (tmp == BD_NONE) { st->err = 1; break; }
-    c1[3 * n1] = src; c1[3 * n1 + 1] = tmp; c1[3 * n1 + 2] = vlen(q); ++n1;
-    c2[3 * n2] = tmp; c2[3 * n2 + 1] = q; c2[3 * n2 + 2] = vlen(q); ++n2;
-    deferred[(*ndef)++] = tmp;
-    if (src >= q1 && !(has_partial && src == NB - 1)) {  // the old home is free now
-      deferred[(*ndef)++] = src;
-      inv[src] = BD_NONE;
-    }
-    Tin[q] = q;
-    inv[q] = q;
+// Final Copy as one cooperative kernel.  Virtual blocks are placed in
+// batches [q0, q1) in order (blocks < q0 are home).  For a misplaced block q:
+// the later block occupying physical q is evicted into a free block, a source
+// inside the batch (another target) is staged into a free block, and then
+// every target is written from its source or stage.  CTA 0 plans a batch in
+// parallel (its 512 threads, shared memory) while the other CTAs run the
+// previous batch's home copies; two grid barriers per batch.  Free blocks
+// usable by a batch are pool entries >= q1 (never a target); the batch is
+// halved until its evictions + stages fit them.  Sources and stages freed by
+// a batch are pooled at plan time: their data is only overwritten by the
+// next batch's phase 1, which starts after this batch's phase 2.
+constexpr uint32_t BD_CP_THREADS = 512;
+constexpr uint32_t BD_CP_BMAX = 1024;   // virtual blocks per batch (2 per planner thread)
+constexpr uint32_t BD_CP_PMAX = 4096;   // pool entries the planner looks at (top of the stack)
+constexpr uint32_t BD_CP_LIST = 9 * BD_CP_BMAX + 8;  // words per list set: phase 1 (2 B x 3), phase 2 (B x 3), counts
+
+struct BdCopySmem {
+  uint32_t src[BD_CP_BMAX], occ[BD_CP_BMAX], need[BD_CP_BMAX], pool[BD_CP_PMAX];
+  uint32_t wsum[BD_CP_THREADS / 32];
+  uint32_t q0, q1, W, pc, k, total, avail, n2, done;
+};
+
+// block-wide exclusive scan of one value per thread (BD_CP_THREADS threads)
+__device__ __forceinline__ uint32_t bd_cp_scan(uint32_t v, uint32_t* wsum, uint32_t* total) {
+  const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= (uint32_t)o) x += y;
   }
-  ncopy[0] = n1;
-  ncopy[1] = n2;
-  st->copies += n1 + n2;
+  __syncthreads();
+  if (lane == 31) wsum[wp] = x;
+  __syncthreads();
+  if (wp == 0) {
+    uint32_t w = lane < BD_CP_THREADS / 32 ? wsum[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= (uint32_t)o) w += y;
+    }
+    if (lane < BD_CP_THREADS / 32) wsum[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t before = wp ? wsum[wp - 1] : 0u;
+  *total = wsum[BD_CP_THREADS / 32 - 1];
+  return before + x - v;
+}
+
+// CTA 0: plan the next batch into list set L (returns with st->copy_q advanced,
+// or L[done] = 1 when every block is home).  Layout of L: [0] phase-1 count,
+// [1] phase-2 count, [2] done, [8 ...) phase 1 triples (src, dst, len), then
+// phase 2 triples at 8 + 6 BMAX.
+__device__ void bd_copy_plan_cta(BdState* st, uint32_t* __restrict__ Tin, uint32_t* __restrict__ inv,
+                                 uint32_t* __restrict__ pool, uint32_t NB, uint32_t P, uint32_t n,
+                                 uint32_t has_partial, uint32_t* __restrict__ L, BdCopySmem& S) {
+  const uint32_t tid = threadIdx.x;
+  auto vlen = [&](uint32_t v) -> uint32_t { return v + 1 < NB ? P : n - v * P; };
+  if (tid == 0) {
+    uint32_t q0 = st->copy_q;
+    S.q0 = q0;
+    S.W = st->err ? 0u : min(BD_CP_BMAX, NB - q0);
+    S.pc = st->pool_count;
+    S.k = min(S.pc, BD_CP_PMAX);
+  }
+  __syncthreads();
+  const uint32_t q0 = S.q0, W = S.W, pc = S.pc, k = S.k;
+  if (W == 0) {
+    if (tid == 0) { L[0] = L[1] = 0; L[2] = 1; }
+    return;
+  }
+  for (uint32_t x = tid; x < W; x += BD_CP_THREADS) {
+    S.src[x] = Tin[q0 + x];
+    S.occ[x] = inv[q0 + x];
+  }
+  for (uint32_t y = tid; y < k; y += BD_CP_THREADS) S.pool[y] = pool[pc - k + y];  // top of the stack
+  __syncthreads();
+  // the largest batch (halving from W) whose evictions + stages fit the free
+  // blocks >= q1
+  uint32_t q1 = q0 + W;
+  uint32_t total = 0, avail = 0;
+  for (;;) {
+    uint32_t mine = 0;
+    for (uint32_t x = 2 * tid; x < 2 * tid + 2; ++x) {
+      uint32_t nd = 0;
+      if (x < q1 - q0) {
+        const uint32_t q = q0 + x, src = S.src[x], occ = S.occ[x];
+        if (src != q) nd = (occ != BD_NONE && occ >= q1 ? 1u : 0u) + (src < q1 ? 1u : 0u);
+      }
+      S.need[x] = nd;
+      mine += nd;
+    }
+    uint32_t t0;
+    bd_cp_scan(mine, S.wsum, &t0);
+    uint32_t av = 0;
+    for (uint32_t y = tid; y < k; y += BD_CP_THREADS) av += S.pool[y] >= q1 ? 1u : 0u;
+    uint32_t a0;
+    bd_cp_scan(av, S.wsum, &a0);
+    total = t0;
+    avail = a0;
+    if (total <= avail || q1 == q0 + 1) break;
+    q1 = q0 + max(1u, (q1 - q0) / 2);
+  }
+  if (total > avail) {  // even one block does not fit
+    if (tid == 0) {
+      if (k == pc) st->err = 1;
+      else {  // drop the dead (< q1) entries of the window and retry next time
+        uint32_t o = pc - k;
+        for (uint32_t y = 0; y < k; ++y) if (S.pool[y] >= q1) pool[o++] = S.pool[y];
+        st->pool_count = o;
+      }
+      L[0] = L[1] = 0; L[2] = st->err;
+    }
+    return;
+  }
+  // free list: the window's entries >= q1, compacted to S.pool[0, avail)
+  uint32_t vals[BD_CP_PMAX / BD_CP_THREADS];
+  uint32_t nm = 0;
+  for (uint32_t y = tid; y < k; y += BD_CP_THREADS)
+    if (S.pool[y] >= q1) vals[nm++] = S.pool[y];
+  uint32_t tot;
+  const uint32_t fo = bd_cp_scan(nm, S.wsum, &tot);
+  __syncthreads();
+  for (uint32_t z = 0; z < nm; ++z) S.pool[fo + z] = vals[z];
+  __syncthreads();
+  // assignments
+  uint32_t nd2[2], mis[2], mine = 0, mcount = 0;
+  for (uint32_t u = 0; u < 2; ++u) {
+    const uint32_t x = 2 * tid + u;
+    nd2[u] = x < q1 - q0 ? S.need[x] : 0u;
+    mis[u] = (x < q1 - q0 && S.src[x] != q0 + x) ? 1u : 0u;
+    mine += nd2[u];
+    mcount += mis[u];
+  }
+  uint32_t t1, t2;
+  uint32_t off = bd_cp_scan(mine, S.wsum, &t1);
+  uint32_t off2 = bd_cp_scan(mcount, S.wsum, &t2);
+  // freed blocks (direct sources outside the batch, stages) go after the
+  // unused free entries: count them
+  uint32_t fr = 0;
+  for (uint32_t u = 0; u < 2; ++u) {
+    const uint32_t x = 2 * tid + u;
+    if (!mis[u]) continue;
+    const uint32_t src = S.src[x];
+    const bool stg = src < q1;
+    if (stg) ++fr;                                              // the stage block
+    else if (!(has_partial && src == NB - 1)) ++fr;              // the old home of q
+  }
+  uint32_t tf;
+  uint32_t offf = bd_cp_scan(fr, S.wsum, &tf);
+  uint32_t* L1 = L + 8;
+  uint32_t* L2 = L + 8 + 6 * BD_CP_BMAX;
+  const uint32_t base_new = pc - k + (avail - total);  // pool: [0, pc-k) untouched, unused entries, freed
+  for (uint32_t u = 0; u < 2; ++u) {
+    const uint32_t x = 2 * tid + u;
+    if (!mis[u]) continue;
+    const uint32_t q = q0 + x, src = S.src[x], occ = S.occ[x];
+    const bool ev = occ != BD_NONE && occ >= q1, stg = src < q1;
+    uint32_t o = off;
+    if (ev) {
+      const uint32_t e = S.pool[o];
+      L1[3 * o] = q; L1[3 * o + 1] = e; L1[3 * o + 2] = vlen(occ);
+      Tin[occ] = e;
+      inv[e] = occ;
+      ++o;
+    }
+    uint32_t from = src;
+    if (stg) {
+      const uint32_t t = S.pool[o];
+      L1[3 * o] = src; L1[3 * o + 1] = t; L1[3 * o + 2] = vlen(q);
+      from = t;
+      ++o;
+      pool[base_new + offf++] = t;
+    } else {
+      inv[src] = BD_NONE;
+      if (!(has_partial && src == NB - 1)) pool[base_new + offf++] = src;
+    }
+    off = o;
+    L2[3 * off2] = from; L2[3 * off2 + 1] = q; L2[3 * off2 + 2] = vlen(q);
+    ++off2;
+    Tin[q] = q;
+  }
+  __syncthreads();
+  // inv of the targets last: a stage source src < q1 is itself a target of
+  // this batch (inv[src] = src set by its own thread)
+  for (uint32_t u = 0; u < 2; ++u) {
+    const uint32_t x = 2 * tid + u;
+    if (mis[u]) inv[q0 + x] = q0 + x;
+  }
+  // unused free entries of the window
+  for (uint32_t y = total + tid; y < avail; y += BD_CP_THREADS) pool[pc - k + (y - total)] = S.pool[y];
+  __syncthreads();
+  if (tid == 0) {
+    st->pool_count = base_new + tf;
+    st->copy_q = q1;
+    st->copies += t1 + t2;
+    L[0] = t1;
+    L[1] = t2;
+    L[2] = 0;
+  }
 }
 
 template <int KT, bool HV>
-__global__ void __launch_bounds__(256) k_bd_copy(BdMem<KT> M, const uint32_t* __restrict__ list,
-                                                 const uint32_t* __restrict__ ncopy, int which) {
-  const uint32_t nc = ncopy[which];
-  for (uint32_t c = blockIdx.x; c < nc; c += gridDim.x) {
+__device__ __forceinline__ void bd_copy_list(const BdMem<KT>& M, const uint32_t* __restrict__ list, uint32_t cnt,
+                                             uint32_t first, uint32_t stride) {
+  using K = typename KeyTraits<KT>::K;
+  // 16-byte vectors when every block base is aligned (the caller's array may
+  // start anywhere: sub-arrays of the dyadic-cell mode)
+  const bool vec = ((reinterpret_cast<uintptr_t>(M.k0) | reinterpret_cast<uintptr_t>(M.v0) |
+                     reinterpret_cast<uintptr_t>(M.ks) | reinterpret_cast<uintptr_t>(M.vs)) & 15u) == 0;
+  for (uint32_t c = first; c < cnt; c += stride) {
     const uint32_t a = list[3 * c], b = list[3 * c + 1], len = list[3 * c + 2];
-    const auto* sk = M.kb(a);
-    auto* dk = M.kb(b);
-    for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) dk[q] = sk[q];
+    const K* sk = M.kb(a);
+    K* dk = M.kb(b);
+    constexpr uint32_t KV = 16 / sizeof(K);
+    const uint32_t nv = vec ? len / KV : 0u;
+    for (uint32_t q = threadIdx.x; q < nv; q += blockDim.x)
+      reinterpret_cast<uint4*>(dk)[q] = __ldcg(reinterpret_cast<const uint4*>(sk) + q);
+    for (uint32_t q = nv * KV + threadIdx.x; q < len; q += blockDim.x) dk[q] = sk[q];
     if (HV) {
       const uint32_t* sv = M.vb(a);
       uint32_t* dv = M.vb(b);
-      for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) dv[q] = sv[q];
+      const uint32_t nv4 = vec ? len / 4 : 0u;
+      for (uint32_t q = threadIdx.x; q < nv4; q += blockDim.x)
+        reinterpret_cast<uint4*>(dv)[q] = __ldcg(reinterpret_cast<const uint4*>(sv) + q);
+      for (uint32_t q = nv4 * 4 + threadIdx.x; q < len; q += blockDim.x) dv[q] = sv[q];
     }
+  }
+}
+
+// The whole Copy (cooperative launch, gridDim.x >= 2).  lists: 2 list sets of
+// BD_CP_LIST words.
+template <int KT, bool HV>
+__global__ void __launch_bounds__(BD_CP_THREADS) k_bd_copy_all(BdMem<KT> M, BdState* st, uint32_t* Tin, uint32_t* inv,
+                                                                uint32_t* pool, uint32_t* lists) {
+  __shared__ BdCopySmem S;
+  cg::grid_group grid = cg::this_grid();
+  uint32_t j = 0;
+  if (blockIdx.x == 0) bd_copy_plan_cta(st, Tin, inv, pool, M.NB, M.P, M.n, M.has_partial, lists, S);
+  grid.sync();
+  for (;;) {
+    uint32_t* L = lists + (size_t)(j & 1) * BD_CP_LIST;
+    const uint32_t n1 = ((volatile uint32_t*)L)[0], n2 = ((volatile uint32_t*)L)[1],
+                   done = ((volatile uint32_t*)L)[2];
+    if (done) break;
+    bd_copy_list<KT, HV>(M, L + 8, n1, blockIdx.x, gridDim.x);  // phase 1: evictions and stages
+    grid.sync();
+    if (blockIdx.x == 0)
+      bd_copy_plan_cta(st, Tin, inv, pool, M.NB, M.P, M.n, M.has_partial, lists + (size_t)((j + 1) & 1) * BD_CP_LIST, S);
+    else
+      bd_copy_list<KT, HV>(M, L + 8 + 6 * BD_CP_BMAX, n2, blockIdx.x - 1, gridDim.x - 1);  // phase 2: targets
+    grid.sync();
+    ++j;
   }
 }
 

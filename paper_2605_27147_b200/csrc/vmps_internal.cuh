@@ -141,8 +141,7 @@ struct Work {
   void* bdesc;
   uint32_t bdesc_cap;
   void* bstate;
-  uint32_t *clist1, *clist2, *ncopy, *deferred, *ndef;
-  uint32_t copy_batch;
+  uint32_t* cplists;      // final Copy: two list sets (bounded.cuh BD_CP_LIST words each)
   size_t scratch_bytes;
   size_t used_bytes;
 };
