@@ -267,16 +267,6 @@ static int dev_slot() {
   if (cudaGetDevice(&d) != cudaSuccess || d < 0) d = 0;
   return d % MAX_DEV;
 }
-// per thread: concurrent sorts on different threads capture their own graphs
-static thread_local cudaStream_t g_aux[MAX_DEV];
-static cudaStream_t aux_stream() {
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= MAX_DEV) return nullptr;
-  if (!g_aux[dev] && cudaStreamCreateWithFlags(&g_aux[dev], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-  return g_aux[dev];
-}
-constexpr int BD_GRAPH_ROUNDS = 8;  // bounded-mode rounds per graph launch
-
 static int g_nsm = 0;
 static int nsm() {
   if (!g_nsm) {
@@ -442,12 +432,29 @@ static vmps_status_t front_half(const Work& w, const void* keys, cudaStream_t s)
 // positions gpos[0..r] in an array of n_glob elements -- then the node powers
 // are the whole array's (P:445-446 with the global n), so the sub-array's
 // tree is exactly the whole plan's subtree over these runs.
+// The power of the boundary between [i, j) and [j, k) in an array of n
+// (P:445-446): one plus the common leading bits of the two scaled midpoints.
+static uint32_t host_power(uint64_t n, uint64_t i, uint64_t j, uint64_t k) {
+  const unsigned __int128 N2 = (unsigned __int128)2 * n;
+  unsigned __int128 A = (unsigned __int128)(i + j), B = (unsigned __int128)(j + k);
+  uint32_t p = 0;
+  for (;;) {
+    ++p;
+    A <<= 1;
+    B <<= 1;
+    const bool ba = A >= N2, bb = B >= N2;
+    if (ba != bb) return p;
+    if (ba) { A -= N2; B -= N2; }
+  }
+}
+
 struct GivenRuns {
   const uint32_t* rel;
   const uint8_t* kinds;
   const uint64_t* gpos;
   uint64_t n_glob;
   uint32_t r;
+  int p_min = 0;  // > 0: every boundary's power is >= p_min (a dyadic cell's runs), not recomputed
 };
 
 static vmps_status_t front_half_given(const Work& w, const GivenRuns& G, cudaStream_t s) {
@@ -476,7 +483,7 @@ static vmps_status_t front_half_given(const Work& w, const GivenRuns& G, cudaStr
 
 // ---- scratch-bounded mode: level rounds and the final Copy (bounded.cuh) ----
 template <int KT, bool HV>
-static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0, uint32_t* v0, int p_hi,
+static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0, uint32_t* v0, int p_hi, int p_lo,
                                     cudaStream_t s) {
   using K = typename KeyTraits<KT>::K;
   BdMem<KT> M;
@@ -485,40 +492,28 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
   BdState* st = (BdState*)w.bstate;
   const unsigned g = grid_for(w.rmax);
   const unsigned gNB = grid_for(w.NB + 8);
-  LAUNCH(k_bd_init, gNB, 256, 0, s, st, w.pool, w.Tin, w.NB, w.F);
+  const uint32_t cap = w.NB + w.F + 8;  // the pool ring (carve: NP entries)
+  LAUNCH(k_bd_init, grid_for(cap), 256, 0, s, st, w.pool, cap, w.Tin, w.NB, w.F);
   TileDesc* desc = (TileDesc*)w.bdesc;
-  BdState hs;
-  // The round kernels take all their state from device memory, so a batch of
-  // rounds is captured once (on an internal stream; the caller's may be the
-  // legacy stream, which cannot be captured) and replayed on `s`.
-  cudaGraph_t rounds_graph = nullptr;
-  cudaGraphExec_t rounds_exec = nullptr;
-  double t0 = bd_now(s);
-  if (!debug_sync()) {
-    cudaStream_t cap = aux_stream();
-    bool ok = cap && cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
-    if (ok) {
-      for (int q = 0; q < BD_GRAPH_ROUNDS; ++q) {
-        k_bd_alloc<<<1, 1024, 0, cap>>>(st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
-        k_bd_merge<KT, HV><<<nsm() * 4, MERGE_BLOCK, 0, cap>>>(M, st, desc, w.Tin, w.Tout, w.pool, w.remain,
-                                                                w.dirty);
-      }
-      ok = cudaStreamEndCapture(cap, &rounds_graph) == cudaSuccess &&
-           cudaGraphInstantiate(&rounds_exec, rounds_graph, 0) == cudaSuccess;
-    }
-    if (!ok) {  // fall back to direct launches
-      cudaGetLastError();
-      if (rounds_exec) cudaGraphExecDestroy(rounds_exec);
-      rounds_exec = nullptr;
-    }
+  // level kernel: persistent grid, shared memory for the block's inputs and outputs
+  const int ds = dev_slot();
+  static int lv_grid[MAX_DEV][3][2][16] = {};  // by log2 P
+  uint32_t lp = 0;
+  while ((1u << lp) < w.P) ++lp;
+  const size_t lsm = bd_level_smem<KT, HV>(w.P);
+  if (!lv_grid[ds][KT][HV][lp]) {
+    VMPS_CK(cudaFuncSetAttribute(k_bd_level<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)bd_level_smem<KT, HV>(DEFAULT_TOUT)));
+    int per_sm = 0;
+    VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bd_level<KT, HV>, MERGE_BLOCK, lsm));
+    lv_grid[ds][KT][HV][lp] = nsm() * std::max(per_sm, 1);
   }
-  struct GraphGuard {
-    cudaGraph_t& g; cudaGraphExec_t& e;
-    ~GraphGuard() { if (e) cudaGraphExecDestroy(e); if (g) cudaGraphDestroy(g); }
-  } guard{rounds_graph, rounds_exec};
-  bd_add(0, t0, s);
-  t0 = bd_now(s);
-  for (int p = p_hi; p >= 1; --p) {
+  const unsigned glv = (unsigned)lv_grid[ds][KT][HV][lp];
+  const unsigned gfix = nsm() * 4;
+  double t0 = bd_now(s);
+  // levels, highest power first; no host synchronisation: every kernel reads
+  // the level's sizes from device memory
+  for (int p = p_hi; p >= p_lo; --p) {
     LAUNCH(k_bd_flags, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.fuse_z, p, w.rmax,
            w.bflag);
     scan_u32(w.bflag, w.bpos, w.rmax + 1, w.scan_tmp, s);
@@ -527,52 +522,25 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
     LAUNCH(k_bd_tile_counts, g, 256, 0, s, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.bm, w.P, w.n, w.rmax,
            w.bcnt);
     scan_u32(w.bcnt, w.btoff, w.rmax + 1, w.scan_tmp, s);
-    uint32_t m = 0, total = 0;
-    VMPS_CK(cudaMemcpyAsync(&m, w.bm, 4, cudaMemcpyDeviceToHost, s));
-    VMPS_CK(cudaStreamSynchronize(s));
-    if (m == 0) continue;
-    VMPS_CK(cudaMemcpyAsync(&total, w.btoff + m, 4, cudaMemcpyDeviceToHost, s));
-    VMPS_CK(cudaStreamSynchronize(s));
-    if (total > w.bdesc_cap) { g_err = "internal: bounded tile capacity"; return VMPS_ERR_INTERNAL; }
-    LAUNCH(k_bd_tile_desc<KT>, grid_for(total), 256, 0, s, M, w.Tin, w.run_start, w.seg_l, w.seg_r, w.blnodes,
-           w.bm, w.btoff, desc);
+    LAUNCH(k_bd_tile_desc<KT>, gfix, 256, 0, s, M, w.Tin, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.bm, w.btoff,
+           w.bdesc_cap, st, desc);
     VMPS_CK(cudaMemsetAsync(w.dirty, 0, (size_t)(w.NB + 1) * 4, s));
-    LAUNCH(k_bd_mark<KT>, grid_for(total), 256, 0, s, M, w.Tin, desc, w.btoff, w.bm, w.P, w.dirty);
+    LAUNCH(k_bd_mark<KT>, gfix, 256, 0, s, M, w.Tin, desc, w.btoff, w.bm, w.P, w.dirty);
     scan_u32(w.dirty, w.didx, w.NB + 1, w.scan_tmp, s);
-    LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, grid_for(total)), 256, 0, s, M, desc, w.btoff, w.bm, w.dirty,
-           w.didx, w.dlist, w.first_tile, w.remain, w.bD);
-    // rounds until every dirty block of the level is produced; a batch of
-    // rounds is one CUDA graph launch (rounds past the end are no-ops).  The
-    // first check comes after the rounds the level needs at most (its output
-    // blocks over the scratch blocks, + 1), so a level costs one host wait
-    // and only its last batch runs no-op rounds.
-    const uint32_t est = (uint32_t)((total + w.F - 1) / w.F) + 1u;
-    uint32_t first = rounds_exec ? (est + BD_GRAPH_ROUNDS - 1) / BD_GRAPH_ROUNDS : 1u;
-    for (;;) {
-      if (rounds_exec) {
-        for (uint32_t q = 0; q < first; ++q) VMPS_CK(cudaGraphLaunch(rounds_exec, s));
-        g_nl += 2 * BD_GRAPH_ROUNDS * first;
-        first = 1;
-      } else {
-        for (int q = 0; q < 16; ++q) {
-          LAUNCH(k_bd_alloc, 1, 1024, 0, s, st, w.dlist, w.first_tile, w.bD, w.pool, w.Tout, w.F);
-          LAUNCH((k_bd_merge<KT, HV>), nsm() * 4, MERGE_BLOCK, 0, s, M, st, desc, w.Tin, w.Tout, w.pool, w.remain,
-                 w.dirty);
-        }
-      }
-      uint32_t D = 0;
-      VMPS_CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
-      VMPS_CK(cudaMemcpyAsync(&D, w.bD, 4, cudaMemcpyDeviceToHost, s));
-      VMPS_CK(cudaStreamSynchronize(s));
-      if (hs.err) { g_err = "scratch budget too small for the bounded mode"; return VMPS_ERR_BUDGET; }
-      if (hs.w >= D) break;
-    }
-    LAUNCH(k_bd_commit, gNB, 256, 0, s, w.dlist, w.bD, w.Tout, w.Tin);
-    // next level starts its dirty list from zero
-    VMPS_CK(cudaMemsetAsync(&st->w, 0, 4, s));
+    LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, gfix), 256, 0, s, M, desc, w.btoff, w.bm, w.dirty, w.didx, w.dlist,
+           w.first_tile, w.remain, w.bD);
+    LAUNCH((k_bd_level<KT, HV>), glv, MERGE_BLOCK, lsm, s, M, st, desc, w.btoff, w.bm, w.dlist, w.first_tile, w.bD,
+           w.Tin, w.Tout, w.pool, cap, w.remain);
+    LAUNCH(k_bd_commit, gNB, 256, 0, s, st, w.dlist, w.bD, w.Tout, w.Tin);
   }
+  BdState hs;
+  VMPS_CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  VMPS_CK(cudaStreamSynchronize(s));
+  if (hs.err == 2) { g_err = "internal: bounded tile capacity"; return VMPS_ERR_INTERNAL; }
+  if (hs.err) { g_err = "scratch budget too small for the bounded mode"; return VMPS_ERR_BUDGET; }
   bd_add(1, t0, s);
   t0 = bd_now(s);
+  LAUNCH(k_bd_ring_to_stack, 1, 1024, 0, s, st, w.pool, cap, w.Tout);
   // final Copy: permute the blocks into physical order
   LAUNCH(k_bd_inverse, grid_for(w.NB + w.F), 256, 0, s, w.Tin, w.NB, w.NB + w.F, w.inv);
   LAUNCH(k_bd_inverse2, gNB, 256, 0, s, w.Tin, w.NB, w.inv);
@@ -731,9 +699,24 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   int p_hi = (int)std::ceil(lg) + 1;
   if (p_hi > LEVEL_SLOTS - 2) p_hi = LEVEL_SLOTS - 2;
   if (p_hi < 1) p_hi = 1;
+  int p_lo = 1;
+  if (G && w.bounded && G->p_min > 0) {
+    p_lo = G->p_min;
+  } else if (G && w.bounded) {  // given runs: only the powers their boundaries carry
+    const uint64_t N = G->gpos ? G->n_glob : (uint64_t)w.n;
+    auto pos = [&](uint32_t i) -> uint64_t { return G->gpos ? G->gpos[i] : (uint64_t)G->rel[i]; };
+    uint32_t mn = 0xFFFFFFFFu, mx = 0;
+    for (uint32_t i = 1; i < G->r; ++i) {
+      const uint32_t pw = host_power(N, pos(i - 1), pos(i), pos(i + 1));
+      mn = std::min(mn, pw);
+      mx = std::max(mx, pw);
+    }
+    p_hi = std::min<int>(p_hi, (int)mx);
+    p_lo = G->r > 1 ? (int)mn : p_hi + 1;
+  }
   if (w.bounded) {
     bd_add(3, g_bdt_front, s);
-    rc = bounded_levels<KT, HV>(w, k0, v0, p_hi, s);
+    rc = bounded_levels<KT, HV>(w, k0, v0, p_hi, p_lo, s);
     if (rc != VMPS_OK) return rc;
     if (bd_trace() && !G) {  // one-piece bounded sort
       static const char* nm[4] = {"graph", "levels", "copy", "front+leaf"};
@@ -967,22 +950,6 @@ static CellLayout bd_cell_layout(uint64_t n, int kt, int hv, int64_t scratch) {
   return L;
 }
 
-// The power of the boundary between [i, j) and [j, k) in an array of n
-// (P:445-446): one plus the common leading bits of the two scaled midpoints.
-static uint32_t host_power(uint64_t n, uint64_t i, uint64_t j, uint64_t k) {
-  const unsigned __int128 N2 = (unsigned __int128)2 * n;
-  unsigned __int128 A = (unsigned __int128)(i + j), B = (unsigned __int128)(j + k);
-  uint32_t p = 0;
-  for (;;) {
-    ++p;
-    A <<= 1;
-    B <<= 1;
-    const bool ba = A >= N2, bb = B >= N2;
-    if (ba != bb) return p;
-    if (ba) { A -= N2; B -= N2; }
-  }
-}
-
 vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, int64_t scratch_elems,
                                    size_t* h_bytes) {
   if (!h_bytes) return VMPS_ERR_INVALID_ARG;
@@ -1074,7 +1041,7 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
       const size_t need = carve(cc, &w, nullptr);
       if (need > L.sort_ws) { g_err = "internal: cell workspace"; return VMPS_ERR_INTERNAL; }
       carve(cc, &w, sort_ws);
-      const GivenRuns G{rel.data(), RK.data(), gp.data(), n, (uint32_t)m};
+      const GivenRuns G{rel.data(), RK.data(), gp.data(), n, (uint32_t)m, (int)q + 1};
       vmps_stats_t cs;
       const double t0 = bd_now(s);
       vmps_status_t rc = sort_impl<KT, HV>(w, (char*)keys + a * kb, HV ? vals + a : nullptr, s, st ? &cs : nullptr, &G);

@@ -23,12 +23,12 @@ namespace cg = cooperative_groups;
 
 constexpr uint32_t BD_NONE = 0xFFFFFFFFu;
 
-struct BdState {          // device-side round state (one per sort)
-  uint32_t w;             // next dirty output block (index into the dirty list)
-  uint32_t tile_lo, tile_hi;
+struct BdState {          // device-side state (one per sort)
+  uint32_t head, tail;    // free-block ring (pool[x % cap]) during the levels
+  uint32_t ticket;        // next dirty output block of the level
   uint32_t err;           // 1 = no free block (budget too small)
-  uint32_t pool_count;    // free physical blocks
-  uint32_t rounds;        // rounds executed (statistics)
+  uint32_t pool_count;    // Copy: free blocks in pool[0, pool_count)
+  uint32_t rounds;        // level passes that moved data (statistics)
   uint32_t copies;        // final Copy: block copies
   uint32_t copy_q;        // final Copy: virtual blocks [0, copy_q) are home
 };
@@ -138,10 +138,14 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
                                                       const uint32_t* __restrict__ seg_r,
                                                       const uint32_t* __restrict__ lnodes,
                                                       const uint32_t* __restrict__ m_ptr,
-                                                      const uint32_t* __restrict__ toff,
-                                                      TileDesc* __restrict__ desc) {
+                                                      const uint32_t* __restrict__ toff, uint32_t cap,
+                                                      BdState* st, TileDesc* __restrict__ desc) {
   const uint32_t m = *m_ptr;
   const uint32_t total = toff[m];
+  if (total > cap) {  // capacity is sized from the plan; never expected
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&st->err, 2u);
+    return;
+  }
   const uint32_t P = M.P, n = M.n;
   for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x) {
     uint32_t a = 0, b = m;  // last node x with toff[x] <= tau
@@ -228,118 +232,189 @@ __global__ void k_bd_dirty_list(BdMem<KT> M, const TileDesc* __restrict__ desc, 
   }
 }
 
-// --- rounds -----------------------------------------------------------------
-// Allocate free physical blocks to the next dirty output blocks (one thread).
-__global__ void __launch_bounds__(1024) k_bd_alloc(BdState* st, const uint32_t* __restrict__ dlist,
-                                                   const uint32_t* __restrict__ first_tile,
-                                                   const uint32_t* __restrict__ D_ptr, uint32_t* __restrict__ pool,
-                                                   uint32_t* __restrict__ Tout, uint32_t max_take) {
-  // one block: thread 0 decides how many dirty output blocks this round
-  // takes, all threads map them to free physical blocks in parallel
-  __shared__ uint32_t s_take, s_w, s_pc;
-  if (threadIdx.x == 0) {
-    const uint32_t D = *D_ptr;
-    uint32_t take = 0;
-    if (st->err || st->w >= D) {
-      st->tile_lo = st->tile_hi = 0;
-    } else {
-      take = min(min(st->pool_count, D - st->w), max_take);
-      if (take == 0) { st->err = 1; st->tile_lo = st->tile_hi = 0; }
-    }
-    s_take = take;
-    s_w = st->w;
-    s_pc = st->pool_count;
-  }
-  __syncthreads();
-  const uint32_t take = s_take, w = s_w, pc = s_pc;
-  for (uint32_t x = threadIdx.x; x < take; x += blockDim.x) Tout[dlist[w + x]] = pool[pc - 1 - x];
-  if (threadIdx.x == 0 && take) {
-    st->pool_count = pc - take;
-    st->tile_lo = first_tile[w];
-    st->tile_hi = first_tile[w + take];
-    st->w = w + take;
-    st->rounds++;
-  }
-}
-
-__device__ __forceinline__ void bd_release(BdState* st, uint32_t* pool, uint32_t* remain, const uint32_t* Tin,
-                                           uint32_t NB, uint32_t has_partial, uint32_t v, uint32_t cnt) {
+// --- level pass: dataflow over the dirty output blocks ---------------------
+// One persistent kernel per level.  A CTA takes the next dirty output block
+// (ticket), gathers the inputs of all its tiles through T_in into shared
+// memory, releases every input block whose elements are now all consumed
+// (a consumed page goes back to the free list, Fig. 2), then takes
+// a free physical block for its output, merges the tiles in shared memory and
+// stores the block.  Free blocks circulate through a ring (pool[x % cap]):
+// a release reserves a slot with an atomic on `tail` and publishes the block
+// id; an allocation reserves a slot on `head` and waits until it is
+// published.  Inputs are released before the allocation, so a level needs no
+// more free blocks than the rounds of a block-synchronous schedule would.  A
+// CTA that waits ~1 s without a free block reports the budget as too small.
+__device__ __forceinline__ void bd_release(BdState* st, uint32_t* pool, uint32_t cap, uint32_t* remain,
+                                           const uint32_t* Tin, uint32_t NB, uint32_t has_partial, uint32_t v,
+                                           uint32_t cnt) {
   if (!cnt) return;
   const uint32_t old = atomicSub(&remain[v], cnt);
   if (old == cnt) {
     const uint32_t b = Tin[v];
     if (has_partial && b == NB - 1) return;  // the partial last block is never freed
-    const uint32_t at = atomicAdd(&st->pool_count, 1u);
-    pool[at] = b;
+    const uint32_t at = atomicAdd(&st->tail, 1u);
+    reinterpret_cast<volatile uint32_t*>(pool)[at % cap] = b;
   }
 }
 
 // Consume [q, q+len) of virtual positions: decrement the touched blocks.
-__device__ __forceinline__ void bd_consume(BdState* st, uint32_t* pool, uint32_t* remain, const uint32_t* Tin,
-                                           uint32_t NB, uint32_t P, uint32_t has_partial, uint32_t q, uint32_t len) {
+__device__ __forceinline__ void bd_consume(BdState* st, uint32_t* pool, uint32_t cap, uint32_t* remain,
+                                           const uint32_t* Tin, uint32_t NB, uint32_t P, uint32_t has_partial,
+                                           uint32_t q, uint32_t len) {
   while (len) {
     const uint32_t v = q / P, off = q % P;
     const uint32_t c = min(len, P - off);
-    bd_release(st, pool, remain, Tin, NB, has_partial, v, c);
+    bd_release(st, pool, cap, remain, Tin, NB, has_partial, v, c);
     q += c;
     len -= c;
   }
 }
 
-// Run the round's tiles: translated loads into shared memory, stable merge,
-// stores into the tile's output block; then release consumed input blocks.
+__device__ __forceinline__ uint32_t bd_alloc(BdState* st, uint32_t* pool, uint32_t cap) {
+  const uint32_t h = atomicAdd(&st->head, 1u);
+  volatile uint32_t* slot = reinterpret_cast<volatile uint32_t*>(pool) + h % cap;
+  uint32_t b = *slot;
+  if (b == BD_NONE) {
+    const long long t0 = clock64();
+    while ((b = *slot) == BD_NONE) {
+      if (*reinterpret_cast<volatile uint32_t*>(&st->err)) return BD_NONE;
+      if (clock64() - t0 > (1ll << 31)) { atomicExch(&st->err, 1u); return BD_NONE; }
+      __nanosleep(64);
+    }
+  }
+  *slot = BD_NONE;
+  return b;
+}
+
+constexpr uint32_t BD_MAX_TILES = 32;  // tile pieces of one output block (at most 3 when P <= Z)
+
 template <int KT, bool HV>
-__global__ void __launch_bounds__(MERGE_BLOCK) k_bd_merge(BdMem<KT> M, BdState* st, const TileDesc* __restrict__ desc,
-                                                          const uint32_t* __restrict__ Tin,
-                                                          const uint32_t* __restrict__ Tout, uint32_t* __restrict__ pool,
-                                                          uint32_t* __restrict__ remain,
-                                                          const uint32_t* __restrict__ dirty) {
+__global__ void __launch_bounds__(MERGE_BLOCK) k_bd_level(BdMem<KT> M, BdState* st, const TileDesc* __restrict__ desc,
+                                                          const uint32_t* __restrict__ toff,
+                                                          const uint32_t* __restrict__ m_ptr,
+                                                          const uint32_t* __restrict__ dlist,
+                                                          const uint32_t* __restrict__ first_tile,
+                                                          const uint32_t* __restrict__ D_ptr,
+                                                          const uint32_t* __restrict__ Tin, uint32_t* __restrict__ Tout,
+                                                          uint32_t* __restrict__ pool, uint32_t cap,
+                                                          uint32_t* __restrict__ remain) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
-  __shared__ K sk[DEFAULT_TOUT];
-  __shared__ uint32_t sv[HV ? DEFAULT_TOUT : 1];
-  const uint32_t tlo = st->tile_lo, thi = st->tile_hi;
+  extern __shared__ __align__(16) unsigned char bd_smem[];
   const uint32_t P = M.P;
-  for (uint32_t tau = tlo + blockIdx.x; tau < thi; tau += gridDim.x) {
-    const TileDesc d = desc[tau];
-    if (!dirty[d.lo / P]) continue;  // clean block: stays where it is
-    const uint32_t nA = d.a1 - d.a0, cnt = d.hi - d.lo, nB = cnt - nA;
-    const uint32_t aoff = d.i + d.a0, boff = d.j + (d.lo - d.i) - d.a0;
-    for (uint32_t q = threadIdx.x; q < cnt; q += MERGE_BLOCK) {
-      const uint32_t g = q < nA ? aoff + q : boff + (q - nA);
-      const uint32_t b = Tin[g / P], o = g % P;
-      sk[q] = M.kb(b)[o];
-      if (HV) sv[q] = M.vb(b)[o];
+  K* ik = reinterpret_cast<K*>(bd_smem);
+  K* ok = ik + P;
+  uint32_t* iv = reinterpret_cast<uint32_t*>(ok + P);
+  uint32_t* ov = iv + (HV ? P : 0);
+  __shared__ TileDesc s_t[BD_MAX_TILES];
+  __shared__ uint32_t s_d, s_nt, s_b;
+  const uint32_t D = *D_ptr, total = toff[*m_ptr];
+  const uint32_t tid = threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(M.k0) | reinterpret_cast<uintptr_t>(M.v0) |
+                     reinterpret_cast<uintptr_t>(M.ks) | reinterpret_cast<uintptr_t>(M.vs)) & 15u) == 0;
+  if (blockIdx.x == 0 && tid == 0 && D) atomicAdd(&st->rounds, 1u);
+  for (;;) {
+    if (tid == 0) s_d = atomicAdd(&st->ticket, 1u);
+    __syncthreads();
+    const uint32_t d = s_d;
+    if (d >= D || *reinterpret_cast<volatile uint32_t*>(&st->err)) break;
+    const uint32_t v = dlist[d], vbase = v * P, len = M.vlen(v);
+    if (tid < 32) {  // the block's tiles: consecutive descriptors from first_tile[d] with lo in block v
+      const uint32_t tau = first_tile[d] + tid;
+      TileDesc t{};
+      bool in = tau < total;
+      if (in) { t = desc[tau]; in = t.lo / P == v; }
+      const uint32_t mask = __ballot_sync(0xFFFFFFFFu, in);
+      const uint32_t nt = __ffs(~mask) ? __ffs(~mask) - 1 : 32u;  // tiles are contiguous
+      if (in && tid < nt) s_t[tid] = t;
+      if (tid == 0) {
+        s_nt = nt;
+        if (nt == 32) atomicExch(&st->err, 1u);
+      }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      bd_consume(st, pool, remain, Tin, M.NB, P, M.has_partial, aoff, nA);
-      bd_consume(st, pool, remain, Tin, M.NB, P, M.has_partial, boff, nB);
-    }
-    const uint32_t v = d.lo / P;
-    K* dk = M.kb(Tout[v]);  // output block; element q lands at offset d.lo + q - v P
-    uint32_t* dv = HV ? M.vb(Tout[v]) : nullptr;
-    const uint32_t obase = d.lo - v * P;
-    for (uint32_t q0 = threadIdx.x * MERGE_K; q0 < cnt; q0 += MERGE_BLOCK * MERGE_K) {
-      uint32_t ia = corank<KT>(sk, nA, sk + nA, nB, q0), ib = q0 - ia;
-      const uint32_t qe = min(q0 + MERGE_K, cnt);
-      for (uint32_t q = q0; q < qe; ++q) {
-        const bool takeA = ib >= nB || (ia < nA && T::ord(sk[ia]) <= T::ord(sk[nA + ib]));
-        const uint32_t s = takeA ? ia : nA + ib;
-        dk[obase + q] = sk[s];
-        if (HV) dv[obase + q] = sv[s];
-        ia += takeA ? 1u : 0u;
-        ib += takeA ? 0u : 1u;
+    const uint32_t nt = s_nt;
+    // gather: tile x's A part then B part at its output offsets
+    for (uint32_t x = 0; x < nt; ++x) {
+      const TileDesc t = s_t[x];
+      const uint32_t nA = t.a1 - t.a0, cnt = t.hi - t.lo, o = t.lo - vbase;
+      const uint32_t aoff = t.i + t.a0, boff = t.j + (t.lo - t.i) - t.a0;
+      for (uint32_t q = tid; q < cnt; q += MERGE_BLOCK) {
+        const uint32_t g = q < nA ? aoff + q : boff + (q - nA);
+        const uint32_t b = Tin[g / P], w = g % P;
+        ik[o + q] = M.kb(b)[w];
+        if (HV) iv[o + q] = M.vb(b)[w];
       }
+    }
+    __syncthreads();
+    if (tid == 0) {  // release consumed inputs, then take the output block
+      for (uint32_t x = 0; x < nt; ++x) {
+        const TileDesc t = s_t[x];
+        const uint32_t nA = t.a1 - t.a0, nB = (t.hi - t.lo) - nA;
+        bd_consume(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, t.i + t.a0, nA);
+        bd_consume(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, t.j + (t.lo - t.i) - t.a0, nB);
+      }
+      const uint32_t b = bd_alloc(st, pool, cap);
+      s_b = b;
+      if (b != BD_NONE) Tout[v] = b;
+    }
+    // stable merge of each tile inside shared memory (ties to A)
+    for (uint32_t x = 0; x < nt; ++x) {
+      const TileDesc t = s_t[x];
+      const uint32_t nA = t.a1 - t.a0, cnt = t.hi - t.lo, o = t.lo - vbase, nB = cnt - nA;
+      const K* A = ik + o;
+      const K* B = A + nA;
+      for (uint32_t q0 = tid * MERGE_K; q0 < cnt; q0 += MERGE_BLOCK * MERGE_K) {
+        uint32_t ia = corank<KT>(A, nA, B, nB, q0), ib = q0 - ia;
+        const uint32_t qe = min(q0 + MERGE_K, cnt);
+        for (uint32_t q = q0; q < qe; ++q) {
+          const bool takeA = ib >= nB || (ia < nA && T::ord(A[ia]) <= T::ord(B[ib]));
+          const uint32_t sidx = takeA ? ia : nA + ib;
+          ok[o + q] = A[sidx];
+          if (HV) ov[o + q] = iv[o + sidx];
+          ia += takeA ? 1u : 0u;
+          ib += takeA ? 0u : 1u;
+        }
+      }
+    }
+    __syncthreads();
+    const uint32_t b = s_b;
+    if (b == BD_NONE) break;
+    K* dk = M.kb(b);
+    constexpr uint32_t KV = 16 / sizeof(K);
+    const uint32_t nv = vec ? len / KV : 0u;
+    for (uint32_t q = tid; q < nv; q += MERGE_BLOCK) reinterpret_cast<uint4*>(dk)[q] = reinterpret_cast<const uint4*>(ok)[q];
+    for (uint32_t q = nv * KV + tid; q < len; q += MERGE_BLOCK) dk[q] = ok[q];
+    if (HV) {
+      uint32_t* dv = M.vb(b);
+      const uint32_t nv4 = vec ? len / 4 : 0u;
+      for (uint32_t q = tid; q < nv4; q += MERGE_BLOCK) reinterpret_cast<uint4*>(dv)[q] = reinterpret_cast<const uint4*>(ov)[q];
+      for (uint32_t q = nv4 * 4 + tid; q < len; q += MERGE_BLOCK) dv[q] = ov[q];
     }
     __syncthreads();
   }
 }
 
+template <int KT, bool HV>
+constexpr size_t bd_level_smem(uint32_t P) {
+  return (size_t)2 * P * (sizeof(typename KeyTraits<KT>::K) + (HV ? 4 : 0));
+}
+
+// The ring's free blocks into pool[0, count) for the Copy (one CTA).
+__global__ void __launch_bounds__(1024) k_bd_ring_to_stack(BdState* st, uint32_t* __restrict__ pool, uint32_t cap,
+                                                           uint32_t* __restrict__ tmp) {
+  const uint32_t h = st->head, cnt = st->tail - h;
+  for (uint32_t x = threadIdx.x; x < cnt; x += blockDim.x) tmp[x] = pool[(h + x) % cap];
+  __syncthreads();
+  for (uint32_t x = threadIdx.x; x < cnt; x += blockDim.x) pool[x] = tmp[x];
+  if (threadIdx.x == 0) st->pool_count = cnt;
+}
+
 // After a level: the table maps the dirty blocks to their new homes.
-__global__ void k_bd_commit(const uint32_t* __restrict__ dlist, const uint32_t* __restrict__ D_ptr,
+__global__ void k_bd_commit(BdState* st, const uint32_t* __restrict__ dlist, const uint32_t* __restrict__ D_ptr,
                             const uint32_t* __restrict__ Tout, uint32_t* __restrict__ Tin) {
   const uint32_t D = *D_ptr;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->ticket = 0;  // the next level starts from its first dirty block
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < D; x += gridDim.x * blockDim.x)
     Tin[dlist[x]] = Tout[dlist[x]];
 }
@@ -610,13 +685,15 @@ __global__ void __launch_bounds__(BD_CP_THREADS) k_bd_copy_all(BdMem<KT> M, BdSt
 }
 
 // Initial pool: the scratch blocks.
-__global__ void k_bd_init(BdState* st, uint32_t* __restrict__ pool, uint32_t* __restrict__ Tin, uint32_t NB,
-                          uint32_t F) {
+// Initial ring: the scratch blocks, every other slot empty.
+__global__ void k_bd_init(BdState* st, uint32_t* __restrict__ pool, uint32_t cap, uint32_t* __restrict__ Tin,
+                          uint32_t NB, uint32_t F) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < NB; v += gridDim.x * blockDim.x) Tin[v] = v;
-  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < F; x += gridDim.x * blockDim.x) pool[x] = NB + x;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < cap; x += gridDim.x * blockDim.x)
+    pool[x] = x < F ? NB + x : BD_NONE;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    st->w = 0; st->tile_lo = st->tile_hi = 0; st->err = 0; st->pool_count = F;
-    st->rounds = 0; st->copies = 0;
+    st->head = 0; st->tail = F; st->ticket = 0; st->err = 0; st->pool_count = 0;
+    st->rounds = 0; st->copies = 0; st->copy_q = 0;
   }
 }
 
