@@ -96,6 +96,7 @@ struct Cfg {
   int fuse2;
   uint32_t P, F;    // bounded mode: block size, scratch blocks
   uint32_t given_runs;  // > 0: the runs are given (no run detection; per-run arrays sized by it)
+  uint32_t gt_nb = 0;   // > 0: the block table is external (the whole array's, gt_nb blocks)
 };
 
 static Cfg make_cfg(uint64_t n, int kt, int hv, int64_t scratch = VMPS_SCRATCH_UNBOUNDED) {
@@ -150,7 +151,7 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
   t.has_vals = c.hv;
   const size_t R = (size_t)t.rmax + 2;
   t.bounded = c.scratch >= 0 && c.hv >= 0;
-  if (c.hv >= 0) {
+  if (c.hv >= 0 && !c.gt_nb) {
     const size_t se = t.bounded ? (size_t)c.F * c.P : (size_t)n;  // element scratch
     t.k1 = take(se * key_bytes(c.kt));
     t.v1 = c.hv ? (uint32_t*)take(se * 4) : nullptr;
@@ -211,7 +212,8 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     }
     // the bounded mode also scans its dirty-block flags (NB + 1 entries),
     // which exceed R when the block is smaller than minrun
-    const size_t scan_len = t.bounded ? std::max<size_t>(R, (size_t)((n + c.P - 1) / c.P) + 1) : R;
+    const size_t nbs = c.gt_nb ? (size_t)c.gt_nb : (size_t)((n + c.P - 1) / c.P);
+    const size_t scan_len = t.bounded ? std::max<size_t>(R, nbs + 1) : R;
     t.scan_tmp = (uint32_t*)take(scan_tmp_words(scan_len) * 4 + 64);
   }
   t.counters = (unsigned long long*)take(8 * 8);
@@ -227,16 +229,6 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.P = c.P;
     t.F = c.F;
     t.NB = (uint32_t)((n + c.P - 1) / c.P);
-    const size_t NBp = (size_t)t.NB + 8, NP = (size_t)t.NB + c.F + 8;
-    t.Tin = (uint32_t*)take(NBp * 4);
-    t.Tout = (uint32_t*)take(NBp * 4);
-    t.inv = (uint32_t*)take(NP * 4);
-    t.pool = (uint32_t*)take(NP * 4);
-    t.remain = (uint32_t*)take(NBp * 4);
-    t.dirty = (uint32_t*)take(NBp * 4);
-    t.didx = (uint32_t*)take(NBp * 4);
-    t.dlist = (uint32_t*)take(NBp * 4);
-    t.first_tile = (uint32_t*)take(NBp * 4);
     // per-level lists of the rounds reuse arrays that are dead by then: the
     // pointer-jumping temporaries (anc, dep[1]) and the long-leaf compaction
     // flags (long_flag, long_idx), all R entries of 4 bytes
@@ -247,6 +239,18 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.btoff = t.long_idx;
     t.bm = (uint32_t*)take(64);
     t.bD = (uint32_t*)take(64);
+  }
+  if (t.bounded && !c.gt_nb) {
+    const size_t NBp = (size_t)t.NB + 8, NP = (size_t)t.NB + c.F + 8;
+    t.Tin = (uint32_t*)take(NBp * 4);
+    t.Tout = (uint32_t*)take(NBp * 4);
+    t.inv = (uint32_t*)take(NP * 4);
+    t.pool = (uint32_t*)take(NP * 4);
+    t.remain = (uint32_t*)take(NBp * 4);
+    t.dirty = (uint32_t*)take(NBp * 4);
+    t.didx = (uint32_t*)take(NBp * 4);
+    t.dlist = (uint32_t*)take(NBp * 4);
+    t.first_tile = (uint32_t*)take(NBp * 4);
     // tiles of one level: one per output block plus gap tiles at node ends
     t.bdesc_cap = (uint32_t)(n / c.P + 4 * std::min<uint64_t>(n / c.fuse_z, (uint64_t)t.rmax) + 16);
     t.bdesc = take((size_t)t.bdesc_cap * sizeof(TileDesc));
@@ -481,26 +485,75 @@ static vmps_status_t front_half_given(const Work& w, const GivenRuns& G, cudaStr
   return launch_check();
 }
 
-// ---- scratch-bounded mode: level rounds and the final Copy (bounded.cuh) ----
-template <int KT, bool HV>
-static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0, uint32_t* v0, int p_hi, int p_lo,
-                                    cudaStream_t s) {
+// ---- scratch-bounded mode: level passes and the final Copy (bounded.cuh) ----
+// The block table of one bounded sort: its own (one-piece mode) or the whole
+// array's, shared by the cells and top merges of the dyadic-cell mode.
+struct BdCtx {
+  void* k0; uint32_t* v0;  // the whole array (virtual position 0)
+  void* ks; uint32_t* vs;  // the F scratch blocks
+  uint32_t n, NB, P, F;
+  uint32_t *Tin, *Tout, *inv, *pool, *remain, *dirty, *didx, *dlist, *first_tile, *cplists;
+  void* bstate;
+  void* bdesc;
+  uint32_t bdesc_cap;
+  uint32_t cap() const { return NB + F + 8; }  // the pool ring (NP entries)
+};
+
+static BdCtx ctx_of_work(const Work& w, void* k0, uint32_t* v0) {
+  BdCtx C;
+  C.k0 = k0; C.v0 = v0; C.ks = w.k1; C.vs = w.v1;
+  C.n = w.n; C.NB = w.NB; C.P = w.P; C.F = w.F;
+  C.Tin = w.Tin; C.Tout = w.Tout; C.inv = w.inv; C.pool = w.pool; C.remain = w.remain; C.dirty = w.dirty;
+  C.didx = w.didx; C.dlist = w.dlist; C.first_tile = w.first_tile; C.cplists = w.cplists;
+  C.bstate = w.bstate; C.bdesc = w.bdesc; C.bdesc_cap = w.bdesc_cap;
+  return C;
+}
+
+template <int KT>
+static BdMem<KT> bd_mem(const BdCtx& C) {
   using K = typename KeyTraits<KT>::K;
   BdMem<KT> M;
-  M.k0 = k0; M.v0 = v0; M.ks = (K*)w.k1; M.vs = w.v1;
-  M.NB = w.NB; M.P = w.P; M.n = w.n; M.has_partial = (w.n % w.P) != 0;
-  BdState* st = (BdState*)w.bstate;
+  M.k0 = (K*)C.k0; M.v0 = C.v0; M.ks = (K*)C.ks; M.vs = C.vs;
+  M.NB = C.NB; M.P = C.P; M.n = C.n; M.has_partial = (C.n % C.P) != 0;
+  return M;
+}
+
+static vmps_status_t bd_init(const BdCtx& C, cudaStream_t s) {
+  LAUNCH(k_bd_init, grid_for(C.cap()), 256, 0, s, (BdState*)C.bstate, C.pool, C.cap(), C.Tin, C.inv, C.NB, C.F);
+  return VMPS_OK;
+}
+
+static vmps_status_t bd_check(const BdCtx& C, cudaStream_t s, const char* what) {
+  BdState hs;
+  VMPS_CK(cudaMemcpyAsync(&hs, C.bstate, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  VMPS_CK(cudaStreamSynchronize(s));
+  if (hs.err == 2) { g_err = "internal: bounded tile capacity"; return VMPS_ERR_INTERNAL; }
+  if (hs.err) { g_err = std::string("scratch budget too small for the bounded ") + what; return VMPS_ERR_BUDGET; }
+  return launch_check();
+}
+
+// Level passes p_hi .. p_lo over the runs of w (positions relative to `base`
+// in the whole array; made absolute here), restricted to the blocks they
+// touch.  fuse_z: nodes of at most this size belong to the leaf stage.
+template <int KT, bool HV>
+static vmps_status_t bd_levels(const BdCtx& C, const Work& w, uint64_t base, int p_hi, int p_lo, uint32_t fuse_z,
+                               cudaStream_t s) {
+  if (p_lo > p_hi) return VMPS_OK;
+  const BdMem<KT> M = bd_mem<KT>(C);
+  BdState* st = (BdState*)C.bstate;
   const unsigned g = grid_for(w.rmax);
-  const unsigned gNB = grid_for(w.NB + 8);
-  const uint32_t cap = w.NB + w.F + 8;  // the pool ring (carve: NP entries)
-  LAUNCH(k_bd_init, grid_for(cap), 256, 0, s, st, w.pool, cap, w.Tin, w.NB, w.F);
-  TileDesc* desc = (TileDesc*)w.bdesc;
+  const uint32_t vb0 = (uint32_t)(base / C.P);
+  const uint32_t vb1 = (uint32_t)std::min<uint64_t>(C.NB, (base + w.n + C.P - 1) / C.P);
+  const uint32_t nbr = vb1 - vb0;
+  const unsigned gNB = grid_for(nbr + 8);
+  TileDesc* desc = (TileDesc*)C.bdesc;
+  if (base) LAUNCH(k_rs_add_base, g, 256, 0, s, w.run_start, w.scalars, (uint32_t)base);
   // level kernel: persistent grid, shared memory for the block's inputs and outputs
   const int ds = dev_slot();
   static int lv_grid[MAX_DEV][3][2][16] = {};  // by log2 P
   uint32_t lp = 0;
-  while ((1u << lp) < w.P) ++lp;
-  const size_t lsm = bd_level_smem<KT, HV>(w.P);
+  while ((1u << lp) < C.P) ++lp;
+  const size_t lsm = bd_level_smem<KT, HV>(C.P);
   if (!lv_grid[ds][KT][HV][lp]) {
     VMPS_CK(cudaFuncSetAttribute(k_bd_level<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)bd_level_smem<KT, HV>(DEFAULT_TOUT)));
@@ -510,67 +563,70 @@ static vmps_status_t bounded_levels(const Work& w, typename KeyTraits<KT>::K* k0
   }
   const unsigned glv = (unsigned)lv_grid[ds][KT][HV][lp];
   const unsigned gfix = nsm() * 4;
-  double t0 = bd_now(s);
-  // levels, highest power first; no host synchronisation: every kernel reads
-  // the level's sizes from device memory
+  // highest power first; no host synchronisation: every kernel reads the
+  // level's sizes from device memory
   for (int p = p_hi; p >= p_lo; --p) {
-    LAUNCH(k_bd_flags, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, w.fuse_z, p, w.rmax,
+    LAUNCH(k_bd_flags, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, fuse_z, p, w.rmax,
            w.bflag);
     scan_u32(w.bflag, w.bpos, w.rmax + 1, w.scan_tmp, s);
     LAUNCH(k_bd_nodes, g, 256, 0, s, w.run_start, w.scalars, w.seg_l, w.seg_r, w.bflag, w.bpos, w.rmax,
            w.blnodes, w.bm);
-    LAUNCH(k_bd_tile_counts, g, 256, 0, s, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.bm, w.P, w.n, w.rmax,
+    LAUNCH(k_bd_tile_counts, g, 256, 0, s, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.bm, C.P, C.n, w.rmax,
            w.bcnt);
     scan_u32(w.bcnt, w.btoff, w.rmax + 1, w.scan_tmp, s);
-    LAUNCH(k_bd_tile_desc<KT>, gfix, 256, 0, s, M, w.Tin, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.bm, w.btoff,
-           w.bdesc_cap, st, desc);
-    VMPS_CK(cudaMemsetAsync(w.dirty, 0, (size_t)(w.NB + 1) * 4, s));
-    LAUNCH(k_bd_mark<KT>, gfix, 256, 0, s, M, w.Tin, desc, w.btoff, w.bm, w.P, w.dirty);
-    scan_u32(w.dirty, w.didx, w.NB + 1, w.scan_tmp, s);
-    LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, gfix), 256, 0, s, M, desc, w.btoff, w.bm, w.dirty, w.didx, w.dlist,
-           w.first_tile, w.remain, w.bD);
-    LAUNCH((k_bd_level<KT, HV>), glv, MERGE_BLOCK, lsm, s, M, st, desc, w.btoff, w.bm, w.dlist, w.first_tile, w.bD,
-           w.Tin, w.Tout, w.pool, cap, w.remain);
-    LAUNCH(k_bd_commit, gNB, 256, 0, s, st, w.dlist, w.bD, w.Tout, w.Tin);
+    LAUNCH(k_bd_tile_desc<KT>, gfix, 256, 0, s, M, C.Tin, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.bm, w.btoff,
+           C.bdesc_cap, st, desc);
+    VMPS_CK(cudaMemsetAsync(C.dirty, 0, (size_t)(nbr + 1) * 4, s));
+    LAUNCH(k_bd_mark<KT>, gfix, 256, 0, s, M, C.Tin, desc, w.btoff, w.bm, C.P, vb0, C.dirty);
+    scan_u32(C.dirty, C.didx, nbr + 1, w.scan_tmp, s);
+    LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, gfix), 256, 0, s, M, desc, w.btoff, w.bm, C.dirty, C.didx, vb0, nbr,
+           C.dlist, C.first_tile, C.remain, w.bD);
+    LAUNCH((k_bd_level<KT, HV>), glv, MERGE_BLOCK, lsm, s, M, st, desc, w.btoff, w.bm, C.dlist, C.first_tile, w.bD,
+           C.Tin, C.Tout, C.pool, C.cap(), C.remain);
+    LAUNCH(k_bd_commit, gNB, 256, 0, s, st, C.dlist, w.bD, C.Tout, C.Tin, C.inv);
   }
-  BdState hs;
-  VMPS_CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
-  VMPS_CK(cudaStreamSynchronize(s));
-  if (hs.err == 2) { g_err = "internal: bounded tile capacity"; return VMPS_ERR_INTERNAL; }
-  if (hs.err) { g_err = "scratch budget too small for the bounded mode"; return VMPS_ERR_BUDGET; }
-  bd_add(1, t0, s);
-  t0 = bd_now(s);
-  LAUNCH(k_bd_ring_to_stack, 1, 1024, 0, s, st, w.pool, cap, w.Tout);
-  // final Copy: permute the blocks into physical order
-  LAUNCH(k_bd_inverse, grid_for(w.NB + w.F), 256, 0, s, w.Tin, w.NB, w.NB + w.F, w.inv);
-  LAUNCH(k_bd_inverse2, gNB, 256, 0, s, w.Tin, w.NB, w.inv);
+  return VMPS_OK;
+}
+
+// Final Copy: permute the blocks into physical order (one cooperative kernel).
+template <int KT, bool HV>
+static vmps_status_t bd_copy(const BdCtx& C, cudaStream_t s) {
+  BdState* st = (BdState*)C.bstate;
+  LAUNCH(k_bd_ring_to_stack, 1, 1024, 0, s, st, C.pool, C.cap(), C.Tout);
+  LAUNCH(k_bd_inverse, grid_for(C.NB + C.F), 256, 0, s, C.Tin, C.NB, C.NB + C.F, C.inv);
+  LAUNCH(k_bd_inverse2, grid_for(C.NB + 8), 256, 0, s, C.Tin, C.NB, C.inv);
   VMPS_CK(cudaMemsetAsync(&st->copy_q, 0, 4, s));
-  {
-    const int ds = dev_slot();
-    static bool copy_attr[MAX_DEV][3][2] = {};
-    static int copy_grid[MAX_DEV] = {};
-    if (!copy_attr[ds][KT][HV]) {
-      int per_sm = 0;
-      VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bd_copy_all<KT, HV>, BD_CP_THREADS, 0));
-      if (per_sm < 1) { g_err = "internal: Copy kernel not resident"; return VMPS_ERR_INTERNAL; }
-      copy_grid[ds] = nsm();
-      copy_attr[ds][KT][HV] = true;
-    }
-    BdMem<KT> Mc = M;
-    uint32_t* Tin = w.Tin;
-    uint32_t* inv = w.inv;
-    uint32_t* pool = w.pool;
-    uint32_t* lists = w.cplists;
-    void* args[] = {&Mc, &st, &Tin, &inv, &pool, &lists};
-    VMPS_CK(cudaLaunchCooperativeKernel((const void*)k_bd_copy_all<KT, HV>, dim3(copy_grid[ds]), dim3(BD_CP_THREADS),
-                                        args, 0, s));
-    ++g_nl;
+  const int ds = dev_slot();
+  static bool copy_attr[MAX_DEV][3][2] = {};
+  if (!copy_attr[ds][KT][HV]) {
+    int per_sm = 0;
+    VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bd_copy_all<KT, HV>, BD_CP_THREADS, 0));
+    if (per_sm < 1) { g_err = "internal: Copy kernel not resident"; return VMPS_ERR_INTERNAL; }
+    copy_attr[ds][KT][HV] = true;
   }
-  VMPS_CK(cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s));
-  VMPS_CK(cudaStreamSynchronize(s));
-  if (hs.err) { g_err = "scratch budget too small for the bounded Copy"; return VMPS_ERR_BUDGET; }
-  bd_add(2, t0, s);
-  return launch_check();
+  BdMem<KT> Mc = bd_mem<KT>(C);
+  uint32_t* Tin = C.Tin;
+  uint32_t* inv = C.inv;
+  uint32_t* pool = C.pool;
+  uint32_t* lists = C.cplists;
+  void* args[] = {&Mc, &st, &Tin, &inv, &pool, &lists};
+  VMPS_CK(cudaLaunchCooperativeKernel((const void*)k_bd_copy_all<KT, HV>, dim3(nsm()), dim3(BD_CP_THREADS), args, 0,
+                                      s));
+  ++g_nl;
+  return VMPS_OK;
+}
+
+// Bring virtual block b back to its own physical block (dyadic-cell mode:
+// the first block of a range that is read in place, after the previous range
+// rewrote it through the table).
+template <int KT, bool HV>
+static vmps_status_t bd_home(const BdCtx& C, uint32_t b, uint32_t* d_slot, cudaStream_t s) {
+  if (b >= C.NB) return VMPS_OK;
+  BdState* st = (BdState*)C.bstate;
+  VMPS_CK(cudaMemsetAsync(d_slot, 0xFF, 4, s));
+  LAUNCH(k_bd_find_free, nsm() * 2, 256, 0, s, st, C.Tin, C.pool, C.cap(), b, d_slot);
+  LAUNCH((k_bd_home<KT, HV>), 1, 512, 0, s, bd_mem<KT>(C), st, C.Tin, C.inv, C.pool, C.cap(), b, d_slot);
+  return VMPS_OK;
 }
 
 template <bool HV>
@@ -585,7 +641,8 @@ static vmps_status_t bounded_stats(const Work& w, vmps_stats_t* st, cudaStream_t
   BdState hs;
   VMPS_CK(cudaMemcpyAsync(sc, w.scalars, sizeof(sc), cudaMemcpyDeviceToHost, s));
   VMPS_CK(cudaMemcpyAsync(ct, w.counters, sizeof(ct), cudaMemcpyDeviceToHost, s));
-  VMPS_CK(cudaMemcpyAsync(&hs, w.bstate, sizeof(hs), cudaMemcpyDeviceToHost, s));
+  VMPS_CK(cudaMemcpyAsync(&hs, w.gt_ctx ? ((const BdCtx*)w.gt_ctx)->bstate : w.bstate, sizeof(hs),
+                          cudaMemcpyDeviceToHost, s));
   VMPS_CK(cudaStreamSynchronize(s));
   memset(st, 0, sizeof(*st));
   st->n = w.n;
@@ -716,11 +773,28 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   }
   if (w.bounded) {
     bd_add(3, g_bdt_front, s);
-    rc = bounded_levels<KT, HV>(w, k0, v0, p_hi, p_lo, s);
+    double t0 = bd_now(s);
+    if (w.gt_ctx) {  // a cell of the dyadic-cell mode: the whole array's table, no Copy
+      const BdCtx& C = *(const BdCtx*)w.gt_ctx;
+      rc = bd_levels<KT, HV>(C, w, w.gt_base, p_hi, p_lo, w.fuse_z, s);
+      if (rc == VMPS_OK) rc = bd_check(C, s, "mode");
+      bd_add(1, t0, s);
+      if (rc != VMPS_OK) return rc;
+      return bounded_stats<HV>(w, st, s);
+    }
+    const BdCtx C = ctx_of_work(w, k0, v0);
+    rc = bd_init(C, s);
+    if (rc == VMPS_OK) rc = bd_levels<KT, HV>(C, w, 0, p_hi, p_lo, w.fuse_z, s);
+    if (rc == VMPS_OK) rc = bd_check(C, s, "mode");
+    bd_add(1, t0, s);
+    t0 = bd_now(s);
+    if (rc == VMPS_OK) rc = bd_copy<KT, HV>(C, s);
+    if (rc == VMPS_OK) rc = bd_check(C, s, "Copy");
+    bd_add(2, t0, s);
     if (rc != VMPS_OK) return rc;
     if (bd_trace() && !G) {  // one-piece bounded sort
-      static const char* nm[4] = {"graph", "levels", "copy", "front+leaf"};
-      for (int i = 0; i < 4; ++i) fprintf(stderr, "vmps bd trace: %-10s %9.1f ms  %ld\n", nm[i], g_bdt.t[i], g_bdt.n[i]);
+      static const char* nm[4] = {"-", "levels", "copy", "front+leaf"};
+      for (int i = 1; i < 4; ++i) fprintf(stderr, "vmps bd trace: %-10s %9.1f ms  %ld\n", nm[i], g_bdt.t[i], g_bdt.n[i]);
       memset(&g_bdt, 0, sizeof(g_bdt));
     }
     g_prof_mark[3] = prof_event(s);
@@ -930,9 +1004,45 @@ static uint32_t bd_cell_level(uint64_t n) {
   return q;
 }
 struct CellLayout {
-  size_t det_ws, det_out, sort_ws, total;
-  uint32_t det;  // detection chunk (elements)
+  size_t det_ws, det_out, sort_ws, gt, total;
+  uint32_t det;    // detection chunk (elements)
+  uint32_t rcell;  // runs of one cell, at most
 };
+// The whole array's block table and element scratch (dyadic-cell mode).
+static size_t carve_gt(const Cfg& c, uint32_t rcell, char* base, BdCtx* C) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> void* {
+    void* p = base ? (void*)(base + off) : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  BdCtx t{};
+  t.n = (uint32_t)c.n;
+  t.P = c.P;
+  t.F = c.F;
+  t.NB = (uint32_t)((c.n + c.P - 1) / c.P);
+  const size_t se = (size_t)c.F * c.P;
+  t.ks = take(se * key_bytes(c.kt));
+  t.vs = c.hv ? (uint32_t*)take(se * 4) : nullptr;
+  const size_t NBp = (size_t)t.NB + 8, NP = (size_t)t.NB + c.F + 8;
+  t.Tin = (uint32_t*)take(NBp * 4);
+  t.Tout = (uint32_t*)take(NBp * 4);
+  t.inv = (uint32_t*)take(NP * 4);
+  t.pool = (uint32_t*)take(NP * 4);
+  t.remain = (uint32_t*)take(NBp * 4);
+  t.dirty = (uint32_t*)take(NBp * 4);
+  t.didx = (uint32_t*)take(NBp * 4);
+  t.dlist = (uint32_t*)take(NBp * 4);
+  t.first_tile = (uint32_t*)take(NBp * 4);
+  // a level of a cell: its blocks plus gap tiles at node ends (nodes <= runs / 2)
+  t.bdesc_cap = t.NB + 2 * rcell + 16;
+  t.bdesc = take((size_t)t.bdesc_cap * sizeof(TileDesc));
+  t.bstate = take(sizeof(BdState));
+  t.cplists = (uint32_t*)take((size_t)2 * BD_CP_LIST * 4);
+  take(64);  // bd_home's slot
+  if (C) *C = t;
+  return off;
+}
 static CellLayout bd_cell_layout(uint64_t n, int kt, int hv, int64_t scratch) {
   CellLayout L{};
   Cfg c0 = make_cfg(n, kt, hv, scratch);
@@ -942,11 +1052,14 @@ static CellLayout bd_cell_layout(uint64_t n, int kt, int hv, int64_t scratch) {
   L.det_ws = align_up(b);
   const uint64_t rdet = L.det / std::max<uint32_t>(c0.minrun, 1) + 4;
   L.det_out = align_up(rdet * 8) + align_up(rdet + 16) + align_up((size_t)3 * 64 * 8) + align_up(64);
-  // a cell's sort: its runs (<= cell / minrun + 2), blocks of at most the whole array
+  // a cell's sort: its runs (<= cell / minrun + 2); the block table is the whole array's
+  L.rcell = (uint32_t)(((n >> bd_cell_level(n)) + 1) / std::max<uint32_t>(c0.minrun, 1) + 4);
   Cfg cs = make_cfg(n, kt, hv, scratch);
-  cs.given_runs = (uint32_t)(((n >> bd_cell_level(n)) + 1) / std::max<uint32_t>(c0.minrun, 1) + 4);
+  cs.given_runs = L.rcell;
+  cs.gt_nb = (uint32_t)((n + c0.P - 1) / c0.P);
   L.sort_ws = align_up(carve(cs, nullptr, nullptr));
-  L.total = L.det_ws + L.det_out + L.sort_ws + 256;
+  L.gt = align_up(carve_gt(c0, L.rcell, nullptr, nullptr));
+  L.total = L.det_ws + L.det_out + L.sort_ws + L.gt + 256;
   return L;
 }
 
@@ -965,10 +1078,6 @@ vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, int6
 
 }  // extern "C"
 
-static vmps_status_t merge_runs_bounded_impl(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt,
-                                             const uint64_t* h_run_start, uint32_t nruns, int64_t scratch_elems,
-                                             void* ws, size_t ws_bytes, void* stream);
-
 template <int KT, bool HV>
 static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, int64_t S, char* base,
                                         cudaStream_t s, vmps_stats_t* st) {
@@ -978,20 +1087,28 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
   const Cfg c0 = make_cfg(n, KT, HV ? 1 : 0, S);
   const uint32_t minrun = c0.minrun, ns = 3 * minrun, H = minrun + 8;
   const uint32_t q = bd_cell_level(n);
+  const uint32_t NB = (uint32_t)((n + c0.P - 1) / c0.P);
   char* det_ws = base;
   char* det_out = base + L.det_ws;
   char* sort_ws = det_out + L.det_out;
+  BdCtx C;
+  carve_gt(c0, L.rcell, sort_ws + L.sort_ws, &C);
+  C.k0 = keys;
+  C.v0 = vals;
+  uint32_t* d_slot = (uint32_t*)((char*)C.cplists + align_up((size_t)2 * BD_CP_LIST * 4));
   const uint64_t rdet = L.det / std::max<uint32_t>(minrun, 1) + 4;
   uint64_t* d_rs = (uint64_t*)det_out;
   uint8_t* d_rk = (uint8_t*)(det_out + align_up(rdet * 8));
   uint64_t* d_tab = (uint64_t*)(det_out + align_up(rdet * 8) + align_up(rdet + 16));
   K* d_prev = (K*)(det_out + align_up(rdet * 8) + align_up(rdet + 16) + align_up((size_t)3 * 64 * 8));
+  vmps_status_t rc = bd_init(C, s);
+  if (rc != VMPS_OK) return rc;
   std::vector<uint64_t> R;   // run starts of the unprocessed runs (global)
   std::vector<uint8_t> RK;   // their kinds
+  size_t R0 = 0;             // first unprocessed run
   std::vector<uint64_t> tab(ns);
-  uint64_t M = 0, rounds = 0, runs = 0, rev = 0, ext = 0;
+  uint64_t M = 0, runs = 0, rev = 0, ext = 0;
   uint32_t maxp = 0, lv = 0;
-  size_t peak = L.total;
   auto cell_of = [&](uint64_t a, uint64_t b) -> uint64_t {  // dyadic cell (level q) of the midpoint of [a, b)
     return (uint64_t)(((unsigned __int128)(a + b) << q) / ((unsigned __int128)2 * n));
   };
@@ -1001,22 +1118,39 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
   std::vector<Seg> stk;
   bool have_curr = false;
   Seg curr{};
-  auto merge2 = [&](const Seg& x, const Seg& y) -> vmps_status_t {  // [x.a, x.b) (+) [x.b, y.b)
-    const uint64_t runs2[2] = {0, x.b - x.a};
+  // a top merge [x.a, x.b) (+) [x.b, y.b): one node through the shared table
+  auto merge2 = [&](const Seg& x, const Seg& y) -> vmps_status_t {
     const uint64_t len = y.b - x.a;
     M += len;
     const double t0 = bd_now(s);
-    struct Add { double t0; cudaStream_t s; ~Add() { bd_add(6, t0, s); } } add{t0, s};
-    return merge_runs_bounded_impl((char*)keys + x.a * kb, HV ? vals + x.a : nullptr, len, (vmps_key_t)KT, runs2, 2,
-                                   S, sort_ws, L.sort_ws, s);
+    Cfg cc = make_cfg(len, KT, HV ? 1 : 0, S);
+    cc.given_runs = 2;
+    cc.gt_nb = NB;
+    Work w;
+    if (carve(cc, nullptr, nullptr) > L.sort_ws) { g_err = "internal: top merge workspace"; return VMPS_ERR_INTERNAL; }
+    carve(cc, &w, sort_ws);
+    const uint32_t hrs[3] = {0, (uint32_t)(x.b - x.a), (uint32_t)len};
+    const uint32_t hseg[4] = {0, 0, 0, 2};  // seg_l[1] = 0, seg_r[1] = 2
+    uint32_t hsc[SC_COUNT] = {};
+    hsc[SC_RUNS] = 2;
+    const uint8_t hpw[2] = {0, 1};
+    VMPS_CK(cudaMemcpyAsync(w.run_start, hrs, sizeof(hrs), cudaMemcpyHostToDevice, s));
+    VMPS_CK(cudaMemcpyAsync(w.seg_l, hseg, 8, cudaMemcpyHostToDevice, s));
+    VMPS_CK(cudaMemcpyAsync(w.seg_r, hseg + 2, 8, cudaMemcpyHostToDevice, s));
+    VMPS_CK(cudaMemcpyAsync(w.power, hpw, 2, cudaMemcpyHostToDevice, s));
+    VMPS_CK(cudaMemcpyAsync(w.scalars, hsc, sizeof(hsc), cudaMemcpyHostToDevice, s));
+    vmps_status_t r2 = bd_levels<KT, HV>(C, w, x.a, 1, 1, 0u, s);
+    VMPS_CK(cudaStreamSynchronize(s));  // the host arrays above are the stack's
+    bd_add(6, t0, s);
+    return r2;
   };
   auto push_cell = [&](const Seg& nx) -> vmps_status_t {
     if (!have_curr) { curr = nx; have_curr = true; return VMPS_OK; }
     const uint32_t p = host_power(n, curr.last_start, curr.b, nx.first_end);  // Alg. 1 line 6
     maxp = std::max(maxp, p);
     while (!stk.empty() && stk.back().pw >= p) {  // lines 7-9
-      vmps_status_t rc = merge2(stk.back(), curr);
-      if (rc != VMPS_OK) return rc;
+      vmps_status_t r2 = merge2(stk.back(), curr);
+      if (r2 != VMPS_OK) return r2;
       curr = Seg{stk.back().a, curr.b, stk.back().first_end, curr.last_start, 0};
       stk.pop_back();
     }
@@ -1025,43 +1159,53 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
     curr = nx;            // line 11
     return VMPS_OK;
   };
-  // sort the cell made of runs R[0, m) (run m-1 ends at end); consume them
+  // sort the cell made of runs R[R0, R0 + m) (the last ends at end); consume them
   auto do_cell = [&](size_t m, uint64_t end) -> vmps_status_t {
-    const uint64_t a = R[0];
+    const uint64_t* Rr = R.data() + R0;
+    const uint8_t* RKr = RK.data() + R0;
+    const uint64_t a = Rr[0];
     std::vector<uint32_t> rel(m + 1);
     std::vector<uint64_t> gp(m + 1);
-    for (size_t i = 0; i < m; ++i) { rel[i] = (uint32_t)(R[i] - a); gp[i] = R[i]; }
+    for (size_t i = 0; i < m; ++i) { rel[i] = (uint32_t)(Rr[i] - a); gp[i] = Rr[i]; }
     rel[m] = (uint32_t)(end - a);
     gp[m] = end;
-    const bool trivial = m == 1 && RK[0] == 0;  // one ascending run: already sorted
+    const bool trivial = m == 1 && RKr[0] == 0;  // one ascending run: already sorted
     if (!trivial) {
+      vmps_status_t r2 = bd_home<KT, HV>(C, (uint32_t)(a / c0.P), d_slot, s);  // read in place below
+      if (r2 != VMPS_OK) return r2;
       Cfg cc = make_cfg(end - a, KT, HV ? 1 : 0, S);
       cc.given_runs = (uint32_t)m;
+      cc.gt_nb = NB;
       Work w;
       const size_t need = carve(cc, &w, nullptr);
-      if (need > L.sort_ws) { g_err = "internal: cell workspace"; return VMPS_ERR_INTERNAL; }
+      if (need > L.sort_ws || m > L.rcell) { g_err = "internal: cell workspace"; return VMPS_ERR_INTERNAL; }
       carve(cc, &w, sort_ws);
-      const GivenRuns G{rel.data(), RK.data(), gp.data(), n, (uint32_t)m, (int)q + 1};
+      w.gt_ctx = &C;
+      w.gt_base = a;
+      const GivenRuns G{rel.data(), RKr, gp.data(), n, (uint32_t)m, (int)q + 1};
       vmps_stats_t cs;
       const double t0 = bd_now(s);
-      vmps_status_t rc = sort_impl<KT, HV>(w, (char*)keys + a * kb, HV ? vals + a : nullptr, s, st ? &cs : nullptr, &G);
+      r2 = sort_impl<KT, HV>(w, (char*)keys + a * kb, HV ? vals + a : nullptr, s, st ? &cs : nullptr, &G);
       bd_add(5, t0, s);
-      if (rc != VMPS_OK) return rc;
+      if (r2 != VMPS_OK) return r2;
       if (st) {
         M += cs.merge_cost_M;
-        rounds += cs.rounds;
         maxp = std::max(maxp, cs.max_power);
         lv = std::max(lv, cs.levels_executed);
       }
     }
     runs += m;
     for (size_t i = 0; i < m; ++i) {
-      if (RK[i] & 1u) rev += (i + 1 < m ? R[i + 1] : end) - R[i];
-      if (RK[i] & 2u) ++ext;
+      if (RKr[i] & 1u) rev += (i + 1 < m ? Rr[i + 1] : end) - Rr[i];
+      if (RKr[i] & 2u) ++ext;
     }
-    const Seg nx{a, end, m > 1 ? R[1] : end, R[m - 1], 0};
-    R.erase(R.begin(), R.begin() + m);
-    RK.erase(RK.begin(), RK.begin() + m);
+    const Seg nx{a, end, m > 1 ? Rr[1] : end, Rr[m - 1], 0};
+    R0 += m;
+    if (R0 > (1u << 16) && R0 * 2 > R.size()) {  // drop the consumed prefix
+      R.erase(R.begin(), R.begin() + R0);
+      RK.erase(RK.begin(), RK.begin() + R0);
+      R0 = 0;
+    }
     return push_cell(nx);
   };
   // scan: detection chunk by chunk, cells processed as soon as they close
@@ -1076,8 +1220,12 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
     const uint64_t rem = n - off;
     const uint32_t n_end = rem >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)rem;
     const K* kk = (const K*)((const char*)keys + off * kb);
-    vmps_status_t rc = vmps_shard_chain(kk, nd, (vmps_key_t)KT, minrun, n_end, off ? d_prev : nullptr,
-                                        n_halo ? (const void*)(kk + nd) : nullptr, n_halo, d_tab, det_ws, L.det_ws, s);
+    // the chunk is read in place: its first block may have been rewritten
+    // through the table by the cells before it
+    rc = bd_home<KT, HV>(C, (uint32_t)(off / c0.P), d_slot, s);
+    if (rc != VMPS_OK) return rc;
+    rc = vmps_shard_chain(kk, nd, (vmps_key_t)KT, minrun, n_end, off ? d_prev : nullptr,
+                          n_halo ? (const void*)(kk + nd) : nullptr, n_halo, d_tab, det_ws, L.det_ws, s);
     if (rc != VMPS_OK) return rc;
     VMPS_CK(cudaMemcpyAsync(tab.data(), d_tab, (size_t)ns * 8, cudaMemcpyDeviceToHost, s));
     VMPS_CK(cudaStreamSynchronize(s));
@@ -1099,40 +1247,54 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
     VMPS_CK(cudaMemcpyAsync(d_prev, kk + nd - 1, kb, cudaMemcpyDeviceToDevice, s));
     VMPS_CK(cudaStreamSynchronize(s));
     bd_add(4, t_det, s);
-    // close every cell whose last run's end is known: runs R[0, m) share a
-    // cell and run m (whose start is the end of run m-1) lies in a later one
+    // close every cell whose last run's end is known: runs R[R0, R0+m) share
+    // a cell and run R0+m (whose start is the end of run R0+m-1) lies in a later one
     for (;;) {
-      if (R.size() < 2) break;
-      const uint64_t c0c = cell_of(R[0], R[1]);
+      const size_t avail = R.size() - R0;
+      if (avail < 2) break;
+      const uint64_t* Rr = R.data() + R0;
+      const uint64_t c0c = cell_of(Rr[0], Rr[1]);
       size_t m = 1;
-      while (m + 1 < R.size() && cell_of(R[m], R[m + 1]) == c0c) ++m;
-      if (m + 1 >= R.size()) break;  // run m's end (R[m+1]) unknown or run m still in the cell
-      rc = do_cell(m, R[m]);
+      while (m + 1 < avail && cell_of(Rr[m], Rr[m + 1]) == c0c) ++m;
+      if (m + 1 >= avail) break;  // run m's end unknown or run m still in the cell
+      rc = do_cell(m, Rr[m]);
       if (rc != VMPS_OK) return rc;
     }
   }
   // the array is done: remaining runs end at n
-  while (!R.empty()) {
-    const auto end_of = [&](size_t i) { return i + 1 < R.size() ? R[i + 1] : n; };
-    const uint64_t c0c = cell_of(R[0], end_of(0));
+  while (R0 < R.size()) {
+    const size_t avail = R.size() - R0;
+    const uint64_t* Rr = R.data() + R0;
+    const auto end_of = [&](size_t i) { return i + 1 < avail ? Rr[i + 1] : n; };
+    const uint64_t c0c = cell_of(Rr[0], end_of(0));
     size_t m = 1;
-    while (m < R.size() && cell_of(R[m], end_of(m)) == c0c) ++m;
-    vmps_status_t rc = do_cell(m, m < R.size() ? R[m] : n);
+    while (m < avail && cell_of(Rr[m], end_of(m)) == c0c) ++m;
+    rc = do_cell(m, m < avail ? Rr[m] : n);
     if (rc != VMPS_OK) return rc;
   }
   // lines 12-13: pop and merge what is left
   while (!stk.empty()) {
-    vmps_status_t rc = merge2(stk.back(), curr);
+    rc = merge2(stk.back(), curr);
     if (rc != VMPS_OK) return rc;
     curr = Seg{stk.back().a, curr.b, stk.back().first_end, curr.last_start, 0};
     stk.pop_back();
   }
+  rc = bd_check(C, s, "mode");
+  if (rc != VMPS_OK) return rc;
+  // one Copy for the whole array
+  const double t_cp = bd_now(s);
+  rc = bd_copy<KT, HV>(C, s);
+  if (rc == VMPS_OK) rc = bd_check(C, s, "Copy");
+  if (rc != VMPS_OK) return rc;
+  bd_add(2, t_cp, s);
   if (bd_trace()) {
     bd_add(7, t_all, s);
-    static const char* nm[8] = {"graph", "levels", "copy", "front+leaf", "detect", "cell_sorts", "top_merges", "all"};
-    for (int i = 0; i < 8; ++i) fprintf(stderr, "vmps bd trace: %-10s %9.1f ms  %ld\n", nm[i], g_bdt.t[i], g_bdt.n[i]);
+    static const char* nm[8] = {"-", "levels", "copy", "front+leaf", "detect", "cell_sorts", "top_merges", "all"};
+    for (int i = 1; i < 8; ++i) fprintf(stderr, "vmps bd trace: %-10s %9.1f ms  %ld\n", nm[i], g_bdt.t[i], g_bdt.n[i]);
   }
   if (st) {
+    BdState hs;
+    VMPS_CK(cudaMemcpyAsync(&hs, C.bstate, sizeof(hs), cudaMemcpyDeviceToHost, s));
     VMPS_CK(cudaStreamSynchronize(s));
     memset(st, 0, sizeof(*st));
     st->n = n;
@@ -1145,13 +1307,17 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
     st->levels_executed = lv;
     st->minrun = minrun;
     st->block_elems = c0.P;
-    st->rounds = rounds;
+    st->rounds = hs.rounds;
     st->scratch_bytes = (uint64_t)c0.F * c0.P * (kb + (HV ? 4 : 0));
-    st->peak_extra_device_bytes = peak;
-    st->metadata_bytes = peak - st->scratch_bytes;
+    st->peak_extra_device_bytes = L.total;
+    st->metadata_bytes = L.total - st->scratch_bytes;
   }
   return VMPS_OK;
 }
+
+static vmps_status_t merge_runs_bounded_impl(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt,
+                                             const uint64_t* h_run_start, uint32_t nruns, int64_t scratch_elems,
+                                             void* ws, size_t ws_bytes, void* stream);
 
 extern "C" {
 

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
 template <int KT>
 __global__ void k_bd_mark(BdMem<KT> M, const uint32_t* __restrict__ Tin, TileDesc* __restrict__ desc,
                           const uint32_t* __restrict__ toff, const uint32_t* __restrict__ m_ptr, uint32_t P,
-                          uint32_t* __restrict__ dirty) {
+                          uint32_t vb0, uint32_t* __restrict__ dirty) {
   using T = KeyTraits<KT>;
   const uint32_t total = toff[*m_ptr];
   for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x) {
@@ -203,33 +203,41 @@ __global__ void k_bd_mark(BdMem<KT> M, const uint32_t* __restrict__ Tin, TileDes
     bool ident = (nBt == 0 && b0 == 0) || (nAt == 0 && d.a0 == nA);
     if (!ident && nA > 0 && d.k > d.j)
       ident = T::ord(bd_key<KT>(M, Tin, d.j - 1)) <= T::ord(bd_key<KT>(M, Tin, d.j));
-    if (!ident) dirty[d.lo / P] = 1u;
+    if (!ident) dirty[d.lo / P - vb0] = 1u;
   }
 }
 
+// Dirty blocks of the range [vb0, vb0 + nbr) (flags and their scan are
+// indexed relative to vb0): their list, first tiles and consumption counters.
 template <int KT>
 __global__ void k_bd_dirty_list(BdMem<KT> M, const TileDesc* __restrict__ desc, const uint32_t* __restrict__ toff,
                                 const uint32_t* __restrict__ m_ptr, const uint32_t* __restrict__ dirty,
-                                const uint32_t* __restrict__ didx, uint32_t* __restrict__ dlist,
-                                uint32_t* __restrict__ first_tile, uint32_t* __restrict__ remain,
-                                uint32_t* __restrict__ D_out) {
+                                const uint32_t* __restrict__ didx, uint32_t vb0, uint32_t nbr,
+                                uint32_t* __restrict__ dlist, uint32_t* __restrict__ first_tile,
+                                uint32_t* __restrict__ remain, uint32_t* __restrict__ D_out) {
   const uint32_t total = toff[*m_ptr];
-  const uint32_t NB = M.NB, P = M.P;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < NB; v += gridDim.x * blockDim.x) {
-    if (dirty[v]) {
-      dlist[didx[v]] = v;
-      remain[v] = M.vlen(v);
+  const uint32_t P = M.P;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < nbr; x += gridDim.x * blockDim.x) {
+    if (dirty[x]) {
+      dlist[didx[x]] = vb0 + x;
+      remain[vb0 + x] = M.vlen(vb0 + x);
     }
   }
   for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x) {
-    const uint32_t v = desc[tau].lo / P;
-    if (dirty[v] && (tau == 0 || desc[tau - 1].lo / P != v)) first_tile[didx[v]] = tau;
+    const uint32_t x = desc[tau].lo / P - vb0;
+    if (dirty[x] && (tau == 0 || desc[tau - 1].lo / P - vb0 != x)) first_tile[didx[x]] = tau;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint32_t D = didx[NB];
+    const uint32_t D = didx[nbr];
     *D_out = D;
     first_tile[D] = total;
   }
+}
+
+// Run starts of a sub-array made absolute (the shared block table's positions).
+__global__ void k_rs_add_base(uint32_t* __restrict__ rs, const uint32_t* scalars, uint32_t base) {
+  const uint32_t r = scalars[SC_RUNS];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= r; t += gridDim.x * blockDim.x) rs[t] += base;
 }
 
 // --- level pass: dataflow over the dirty output blocks ---------------------
@@ -412,11 +420,74 @@ __global__ void __launch_bounds__(1024) k_bd_ring_to_stack(BdState* st, uint32_t
 
 // After a level: the table maps the dirty blocks to their new homes.
 __global__ void k_bd_commit(BdState* st, const uint32_t* __restrict__ dlist, const uint32_t* __restrict__ D_ptr,
-                            const uint32_t* __restrict__ Tout, uint32_t* __restrict__ Tin) {
+                            const uint32_t* __restrict__ Tout, uint32_t* __restrict__ Tin, uint32_t* __restrict__ inv) {
   const uint32_t D = *D_ptr;
   if (blockIdx.x == 0 && threadIdx.x == 0) st->ticket = 0;  // the next level starts from its first dirty block
-  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < D; x += gridDim.x * blockDim.x)
-    Tin[dlist[x]] = Tout[dlist[x]];
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < D; x += gridDim.x * blockDim.x) {
+    const uint32_t v = dlist[x], b = Tout[v];
+    Tin[v] = b;
+    inv[b] = v;  // occupant of b (stale for freed blocks: check Tin[inv[b]] == b)
+  }
+}
+
+// bd_home, step 1: the ring slot holding physical block b, if b is free.
+__global__ void k_bd_find_free(const BdState* st, const uint32_t* __restrict__ Tin, const uint32_t* __restrict__ pool,
+                               uint32_t cap, uint32_t b, uint32_t* __restrict__ slot) {
+  if (Tin[b] == b) return;
+  const uint32_t h = st->head, cnt = st->tail - h;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < cnt; x += gridDim.x * blockDim.x)
+    if (pool[(h + x) % cap] == b) *slot = (h + x) % cap;
+}
+
+// bd_home, step 2 (one CTA): move virtual block b home.  Physical b is free
+// (its ring slot now holds b's old location) or holds another virtual block
+// u, which moves to a free block first.
+template <int KT, bool HV>
+__global__ void __launch_bounds__(512) k_bd_home(BdMem<KT> M, BdState* st, uint32_t* __restrict__ Tin,
+                                                 uint32_t* __restrict__ inv, uint32_t* __restrict__ pool, uint32_t cap,
+                                                 uint32_t b, const uint32_t* __restrict__ slot) {
+  using K = typename KeyTraits<KT>::K;
+  const uint32_t src = Tin[b];
+  if (src == b || st->err) return;
+  const uint32_t u = inv[b];
+  const bool occupied = u < M.NB && u != b && Tin[u] == b;
+  auto copy = [&](uint32_t from, uint32_t to, uint32_t len) {
+    const K* sk = M.kb(from);
+    K* dk = M.kb(to);
+    for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) dk[q] = sk[q];
+    if (HV) {
+      const uint32_t* sv = M.vb(from);
+      uint32_t* dv = M.vb(to);
+      for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) dv[q] = sv[q];
+    }
+  };
+  if (occupied) {
+    const uint32_t h = st->head;
+    if (st->tail == h) { if (threadIdx.x == 0) st->err = 1; return; }
+    const uint32_t e = pool[h % cap];
+    copy(b, e, M.vlen(u));
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      pool[h % cap] = BD_NONE;
+      st->head = h + 1;
+      Tin[u] = e;
+      inv[e] = u;
+    }
+  }
+  copy(src, b, M.vlen(b));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const bool partial_home = M.has_partial && src == M.NB - 1;  // never pooled
+    if (!occupied && *slot != 0xFFFFFFFFu) {
+      pool[*slot] = partial_home ? BD_NONE : src;  // b's ring slot now offers src
+    } else if (!partial_home) {
+      const uint32_t t = st->tail;
+      pool[t % cap] = src;
+      st->tail = t + 1;
+    }
+    Tin[b] = b;
+    inv[b] = b;
+  }
 }
 
 // --- final Copy: permute blocks into physical order --------------------------
@@ -687,10 +758,12 @@ __global__ void __launch_bounds__(BD_CP_THREADS) k_bd_copy_all(BdMem<KT> M, BdSt
 // Initial pool: the scratch blocks.
 // Initial ring: the scratch blocks, every other slot empty.
 __global__ void k_bd_init(BdState* st, uint32_t* __restrict__ pool, uint32_t cap, uint32_t* __restrict__ Tin,
-                          uint32_t NB, uint32_t F) {
+                          uint32_t* __restrict__ inv, uint32_t NB, uint32_t F) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < NB; v += gridDim.x * blockDim.x) Tin[v] = v;
-  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < cap; x += gridDim.x * blockDim.x)
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < cap; x += gridDim.x * blockDim.x) {
     pool[x] = x < F ? NB + x : BD_NONE;
+    inv[x] = x < NB ? x : BD_NONE;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->head = 0; st->tail = F; st->ticket = 0; st->err = 0; st->pool_count = 0;
     st->rounds = 0; st->copies = 0; st->copy_q = 0;

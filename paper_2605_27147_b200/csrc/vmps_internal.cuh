@@ -142,6 +142,11 @@ struct Work {
   uint32_t bdesc_cap;
   void* bstate;
   uint32_t* cplists;      // final Copy: two list sets (bounded.cuh BD_CP_LIST words each)
+  // dyadic-cell mode: the block table (and element scratch) of the whole
+  // array lives outside this sort (api.cu BdCtx); positions here are
+  // relative to gt_base
+  const void* gt_ctx;
+  uint64_t gt_base;
   size_t scratch_bytes;
   size_t used_bytes;
 };
