@@ -346,8 +346,8 @@ static bool debug_sync() {
 // VMPS_BD_TRACE=1: host wall time per phase of the scratch-bounded mode
 // (stream synchronised at each phase edge), printed to stderr per sort.
 struct BdTrace {
-  double t[8];
-  long n[8];
+  double t[12];
+  long n[12];
 };
 static thread_local BdTrace g_bdt;
 static int g_bd_trace = -1;
@@ -459,17 +459,48 @@ struct GivenRuns {
   uint64_t n_glob;
   uint32_t r;
   int p_min = 0;  // > 0: every boundary's power is >= p_min (a dyadic cell's runs), not recomputed
+  // device-resident runs (dyadic-cell mode): global starts ring[(first + i) % cap]
+  // and kinds, relative to `base`, the last ending at `end` (rel/kinds/gpos unused)
+  const uint64_t* d_ring = nullptr;
+  const uint8_t* d_ring_kind = nullptr;
+  uint64_t ring_cap = 0, ring_first = 0, base = 0, end = 0;
+  bool global() const { return gpos || d_ring; }
 };
+
+// Given runs from the device ring of the dyadic-cell mode.
+__global__ void k_given_from_ring(uint32_t* __restrict__ rs, uint8_t* __restrict__ kind, uint64_t* __restrict__ gpos,
+                                  uint32_t* __restrict__ scalars, const uint64_t* __restrict__ ring,
+                                  const uint8_t* __restrict__ ring_kind, uint64_t cap, uint64_t first, uint32_t r,
+                                  uint64_t base, uint64_t end) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= r; i += gridDim.x * blockDim.x) {
+    const uint64_t g = i < r ? ring[(first + i) % cap] : end;
+    rs[i] = (uint32_t)(g - base);
+    gpos[i] = g;
+    if (i < r) kind[i] = ring_kind[(first + i) % cap];
+    if (i == 0) scalars[SC_RUNS] = r;
+  }
+}
 
 static vmps_status_t front_half_given(const Work& w, const GivenRuns& G, cudaStream_t s) {
   const uint32_t r = G.r;
   VMPS_CK(cudaMemsetAsync(w.scalars, 0, SC_COUNT * 4, s));
   VMPS_CK(cudaMemsetAsync(w.counters, 0, 8 * 8, s));
+  const unsigned g = grid_for(w.rmax);
+  if (G.d_ring) {
+    LAUNCH(k_given_from_ring, g, 256, 0, s, w.run_start, w.run_kind, w.gpos, w.scalars, G.d_ring, G.d_ring_kind,
+           G.ring_cap, G.ring_first, r, G.base, G.end);
+    LAUNCH(k_powers_seg<uint64_t>, g, 256, 0, s, w.gpos, G.n_glob, w.scalars, w.power, w.seg_l, w.seg_r);
+    LAUNCH(k_parent_init, g, 256, 0, s, w.scalars, w.power, w.seg_l, w.seg_r, w.parent, w.anc[0], w.dep[0]);
+    for (int rnd = 0; rnd < 6; ++rnd) {
+      int a = rnd & 1;
+      LAUNCH(k_jump, g, 256, 0, s, w.scalars, w.anc[a], w.dep[a], w.anc[a ^ 1], w.dep[a ^ 1]);
+    }
+    return launch_check();
+  }
   VMPS_CK(cudaMemcpyAsync(w.run_start, G.rel, (size_t)(r + 1) * 4, cudaMemcpyHostToDevice, s));
   if (G.kinds) VMPS_CK(cudaMemcpyAsync(w.run_kind, G.kinds, r, cudaMemcpyHostToDevice, s));
   else VMPS_CK(cudaMemsetAsync(w.run_kind, 0, r, s));
   VMPS_CK(cudaMemcpyAsync(w.scalars + SC_RUNS, &r, 4, cudaMemcpyHostToDevice, s));
-  const unsigned g = grid_for(w.rmax);
   if (G.gpos) {
     VMPS_CK(cudaMemcpyAsync(w.gpos, G.gpos, (size_t)(r + 1) * 8, cudaMemcpyHostToDevice, s));
     LAUNCH(k_powers_seg<uint64_t>, g, 256, 0, s, w.gpos, G.n_glob, w.scalars, w.power, w.seg_l, w.seg_r);
@@ -752,7 +783,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   NvtxRange nv_merge("vmps_merge");
 
   // level merges, highest power first (children before parents, F3)
-  double lg = std::log2(2.0 * (double)(G && G->gpos ? G->n_glob : (uint64_t)w.n) / (double)w.fuse_z);
+  double lg = std::log2(2.0 * (double)(G && G->global() ? G->n_glob : (uint64_t)w.n) / (double)w.fuse_z);
   int p_hi = (int)std::ceil(lg) + 1;
   if (p_hi > LEVEL_SLOTS - 2) p_hi = LEVEL_SLOTS - 2;
   if (p_hi < 1) p_hi = 1;
@@ -984,17 +1015,24 @@ extern "C" {
 // cell form one subtree of the whole plan, and the boundaries between cells
 // carry the powers <= q.  The array is scanned left to right in detection
 // chunks (run-detection transfer table + run emission per chunk, the chain
-// state carried across chunks, original edge keys kept aside); each cell,
-// once its last run's end is known, is sorted by the bounded engine from its
-// given runs with the global powers (exactly the whole plan's subtree), and
-// the cell results go through Alg. 1's stack with the boundary powers
-// computed from the original runs (each pop a bounded merge of two runs).
-// The executed merges are exactly Alg. 1's plan (M equal to the one-piece
-// mode), while the device metadata scales with a cell (runs with midpoints in
-// it <= CELL / minrun + 2) and n / P block-table entries instead of n / minrun:
-// 3.4 GB -> tens of MB at 2^30.
+// state carried across chunks, original edge keys kept aside, the runs kept in
+// a device ring); each cell, once its last run's end is known, is sorted by
+// the bounded engine from its runs with the global powers (exactly the whole
+// plan's subtree), and the cell results go through Alg. 1's stack with the
+// boundary powers computed from the original runs (each pop one level pass
+// of a single node).  Cells and pops write through ONE block table of the
+// whole array (the paper's page table): a range read in place (a
+// cell's leaves, a detection chunk) first brings its first block home, the
+// only block an earlier range can have rewritten; one Copy at the end.  The
+// executed merges are exactly Alg. 1's plan (M equal to the one-piece mode),
+// while the device metadata scales with a cell (runs with midpoints in it
+// <= CELL / minrun + 2) plus n / P block-table entries instead of n / minrun
+// run entries: 3.4 GB -> 93 MB at cfg5 (2^30, CELL = 2^23).
 #ifndef VMPS_BD_CHUNK
-#define VMPS_BD_CHUNK (1u << 24)
+#define VMPS_BD_CHUNK (1u << 23)
+#endif
+#ifndef VMPS_BD_DET
+#define VMPS_BD_DET (1u << 22)  // run-detection chunk of the dyadic-cell mode (elements)
 #endif
 static uint64_t g_bd_chunk = VMPS_BD_CHUNK;  // cell size target (test hook vmps_test_set_bd_chunk)
 static bool bd_chunked(uint64_t n, int64_t scratch, int hv) { return scratch >= 0 && hv >= 0 && n > 2 * g_bd_chunk; }
@@ -1007,6 +1045,7 @@ struct CellLayout {
   size_t det_ws, det_out, sort_ws, gt, total;
   uint32_t det;    // detection chunk (elements)
   uint32_t rcell;  // runs of one cell, at most
+  uint64_t ring;   // device ring of unconsumed runs (entries)
 };
 // The whole array's block table and element scratch (dyadic-cell mode).
 static size_t carve_gt(const Cfg& c, uint32_t rcell, char* base, BdCtx* C) {
@@ -1046,14 +1085,16 @@ static size_t carve_gt(const Cfg& c, uint32_t rcell, char* base, BdCtx* C) {
 static CellLayout bd_cell_layout(uint64_t n, int kt, int hv, int64_t scratch) {
   CellLayout L{};
   Cfg c0 = make_cfg(n, kt, hv, scratch);
-  L.det = (uint32_t)std::min<uint64_t>(g_bd_chunk, n);
+  L.det = (uint32_t)std::min<uint64_t>(std::min<uint64_t>(g_bd_chunk, VMPS_BD_DET), n);
   size_t b = 0;
   vmps_shard_workspace_bytes(L.det, (vmps_key_t)kt, c0.minrun, &b);
   L.det_ws = align_up(b);
   const uint64_t rdet = L.det / std::max<uint32_t>(c0.minrun, 1) + 4;
-  L.det_out = align_up(rdet * 8) + align_up(rdet + 16) + align_up((size_t)3 * 64 * 8) + align_up(64);
   // a cell's sort: its runs (<= cell / minrun + 2); the block table is the whole array's
   L.rcell = (uint32_t)(((n >> bd_cell_level(n)) + 1) / std::max<uint32_t>(c0.minrun, 1) + 4);
+  L.ring = L.rcell + rdet + 16;  // unconsumed runs: an open cell's and one detection chunk's
+  L.det_out = align_up(rdet * 8) + align_up(rdet + 16) + align_up((size_t)3 * 64 * 8) + align_up(64) +
+              align_up(L.ring * 8) + align_up(L.ring);
   Cfg cs = make_cfg(n, kt, hv, scratch);
   cs.given_runs = L.rcell;
   cs.gt_nb = (uint32_t)((n + c0.P - 1) / c0.P);
@@ -1101,16 +1142,25 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
   uint8_t* d_rk = (uint8_t*)(det_out + align_up(rdet * 8));
   uint64_t* d_tab = (uint64_t*)(det_out + align_up(rdet * 8) + align_up(rdet + 16));
   K* d_prev = (K*)(det_out + align_up(rdet * 8) + align_up(rdet + 16) + align_up((size_t)3 * 64 * 8));
+  uint64_t* d_ring = (uint64_t*)((char*)d_prev + align_up(64));
+  uint8_t* d_ring_kind = (uint8_t*)d_ring + align_up(L.ring * 8);
+  uint64_t g_total = 0;  // runs appended to the ring
   vmps_status_t rc = bd_init(C, s);
   if (rc != VMPS_OK) return rc;
-  std::vector<uint64_t> R;   // run starts of the unprocessed runs (global)
+  std::vector<uint64_t> R;   // run starts of the unprocessed runs (global; R[0] is run gbase)
   std::vector<uint8_t> RK;   // their kinds
   size_t R0 = 0;             // first unprocessed run
+  uint64_t gbase = 0;
   std::vector<uint64_t> tab(ns);
   uint64_t M = 0, runs = 0, rev = 0, ext = 0;
   uint32_t maxp = 0, lv = 0;
   auto cell_of = [&](uint64_t a, uint64_t b) -> uint64_t {  // dyadic cell (level q) of the midpoint of [a, b)
     return (uint64_t)(((unsigned __int128)(a + b) << q) / ((unsigned __int128)2 * n));
+  };
+  // the least a + b whose cell is after cell c: ceil((c + 1) 2n / 2^q)
+  auto cell_end = [&](uint64_t c) -> uint64_t {
+    const unsigned __int128 num = (unsigned __int128)(c + 1) * 2 * n;
+    return (uint64_t)((num + (((unsigned __int128)1 << q) - 1)) >> q);
   };
   // Alg. 1 over the cell results: segments [a, b) with, for the boundary
   // powers, the first run's end and the last run's start (original runs)
@@ -1161,17 +1211,16 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
   };
   // sort the cell made of runs R[R0, R0 + m) (the last ends at end); consume them
   auto do_cell = [&](size_t m, uint64_t end) -> vmps_status_t {
+    const double tdc = bd_now(s);
+    struct Add { double t0; cudaStream_t s; ~Add() { bd_add(9, t0, s); } } add_dc{tdc, s};
     const uint64_t* Rr = R.data() + R0;
     const uint8_t* RKr = RK.data() + R0;
     const uint64_t a = Rr[0];
-    std::vector<uint32_t> rel(m + 1);
-    std::vector<uint64_t> gp(m + 1);
-    for (size_t i = 0; i < m; ++i) { rel[i] = (uint32_t)(Rr[i] - a); gp[i] = Rr[i]; }
-    rel[m] = (uint32_t)(end - a);
-    gp[m] = end;
     const bool trivial = m == 1 && RKr[0] == 0;  // one ascending run: already sorted
     if (!trivial) {
+      const double th = bd_now(s);
       vmps_status_t r2 = bd_home<KT, HV>(C, (uint32_t)(a / c0.P), d_slot, s);  // read in place below
+      bd_add(0, th, s);
       if (r2 != VMPS_OK) return r2;
       Cfg cc = make_cfg(end - a, KT, HV ? 1 : 0, S);
       cc.given_runs = (uint32_t)m;
@@ -1182,7 +1231,13 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
       carve(cc, &w, sort_ws);
       w.gt_ctx = &C;
       w.gt_base = a;
-      const GivenRuns G{rel.data(), RKr, gp.data(), n, (uint32_t)m, (int)q + 1};
+      GivenRuns G{nullptr, nullptr, nullptr, n, (uint32_t)m, (int)q + 1};
+      G.d_ring = d_ring;
+      G.d_ring_kind = d_ring_kind;
+      G.ring_cap = L.ring;
+      G.ring_first = gbase + R0;
+      G.base = a;
+      G.end = end;
       vmps_stats_t cs;
       const double t0 = bd_now(s);
       r2 = sort_impl<KT, HV>(w, (char*)keys + a * kb, HV ? vals + a : nullptr, s, st ? &cs : nullptr, &G);
@@ -1195,15 +1250,18 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
       }
     }
     runs += m;
-    for (size_t i = 0; i < m; ++i) {
-      if (RKr[i] & 1u) rev += (i + 1 < m ? Rr[i + 1] : end) - Rr[i];
-      if (RKr[i] & 2u) ++ext;
+    if (st) {
+      for (size_t i = 0; i < m; ++i) {
+        if (RKr[i] & 1u) rev += (i + 1 < m ? Rr[i + 1] : end) - Rr[i];
+        if (RKr[i] & 2u) ++ext;
+      }
     }
     const Seg nx{a, end, m > 1 ? Rr[1] : end, Rr[m - 1], 0};
     R0 += m;
     if (R0 > (1u << 16) && R0 * 2 > R.size()) {  // drop the consumed prefix
       R.erase(R.begin(), R.begin() + R0);
       RK.erase(RK.begin(), RK.begin() + R0);
+      gbase += R0;
       R0 = 0;
     }
     return push_cell(nx);
@@ -1222,7 +1280,9 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
     const K* kk = (const K*)((const char*)keys + off * kb);
     // the chunk is read in place: its first block may have been rewritten
     // through the table by the cells before it
+    const double th = bd_now(s);
     rc = bd_home<KT, HV>(C, (uint32_t)(off / c0.P), d_slot, s);
+    bd_add(0, th, s);
     if (rc != VMPS_OK) return rc;
     rc = vmps_shard_chain(kk, nd, (vmps_key_t)KT, minrun, n_end, off ? d_prev : nullptr,
                           n_halo ? (const void*)(kk + nd) : nullptr, n_halo, d_tab, det_ws, L.det_ws, s);
@@ -1241,6 +1301,16 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
       RK.resize(o + cnt);
       VMPS_CK(cudaMemcpyAsync(R.data() + o, d_rs, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s));
       VMPS_CK(cudaMemcpyAsync(RK.data() + o, d_rk, cnt, cudaMemcpyDeviceToHost, s));
+      // and into the device ring the cells read their runs from
+      if (R.size() - R0 > L.ring) { g_err = "internal: run ring"; return VMPS_ERR_INTERNAL; }
+      const uint64_t at = g_total % L.ring, n1 = std::min<uint64_t>(cnt, L.ring - at);
+      VMPS_CK(cudaMemcpyAsync(d_ring + at, d_rs, n1 * 8, cudaMemcpyDeviceToDevice, s));
+      VMPS_CK(cudaMemcpyAsync(d_ring_kind + at, d_rk, n1, cudaMemcpyDeviceToDevice, s));
+      if (n1 < cnt) {
+        VMPS_CK(cudaMemcpyAsync(d_ring, d_rs + n1, (cnt - n1) * 8, cudaMemcpyDeviceToDevice, s));
+        VMPS_CK(cudaMemcpyAsync(d_ring_kind, d_rk + n1, cnt - n1, cudaMemcpyDeviceToDevice, s));
+      }
+      g_total += cnt;
     }
     state = (uint32_t)(v >> 32);
     // the original last key of this chunk (the next chunk's descent bit at its start)
@@ -1250,13 +1320,15 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
     // close every cell whose last run's end is known: runs R[R0, R0+m) share
     // a cell and run R0+m (whose start is the end of run R0+m-1) lies in a later one
     for (;;) {
+      const double tc = bd_now(s);
       const size_t avail = R.size() - R0;
       if (avail < 2) break;
       const uint64_t* Rr = R.data() + R0;
-      const uint64_t c0c = cell_of(Rr[0], Rr[1]);
+      const uint64_t T = cell_end(cell_of(Rr[0], Rr[1]));
       size_t m = 1;
-      while (m + 1 < avail && cell_of(Rr[m], Rr[m + 1]) == c0c) ++m;
+      while (m + 1 < avail && Rr[m] + Rr[m + 1] < T) ++m;
       if (m + 1 >= avail) break;  // run m's end unknown or run m still in the cell
+      bd_add(8, tc, s);
       rc = do_cell(m, Rr[m]);
       if (rc != VMPS_OK) return rc;
     }
@@ -1266,9 +1338,9 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
     const size_t avail = R.size() - R0;
     const uint64_t* Rr = R.data() + R0;
     const auto end_of = [&](size_t i) { return i + 1 < avail ? Rr[i + 1] : n; };
-    const uint64_t c0c = cell_of(Rr[0], end_of(0));
+    const uint64_t T = cell_end(cell_of(Rr[0], end_of(0)));
     size_t m = 1;
-    while (m < avail && cell_of(Rr[m], end_of(m)) == c0c) ++m;
+    while (m < avail && Rr[m] + end_of(m) < T) ++m;
     rc = do_cell(m, m < avail ? Rr[m] : n);
     if (rc != VMPS_OK) return rc;
   }
@@ -1289,8 +1361,9 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
   bd_add(2, t_cp, s);
   if (bd_trace()) {
     bd_add(7, t_all, s);
-    static const char* nm[8] = {"-", "levels", "copy", "front+leaf", "detect", "cell_sorts", "top_merges", "all"};
-    for (int i = 1; i < 8; ++i) fprintf(stderr, "vmps bd trace: %-10s %9.1f ms  %ld\n", nm[i], g_bdt.t[i], g_bdt.n[i]);
+    static const char* nm[10] = {"home", "levels", "copy", "front+leaf", "detect", "cell_sorts", "top_merges", "all",
+                                 "close", "do_cell"};
+    for (int i = 0; i < 10; ++i) fprintf(stderr, "vmps bd trace: %-10s %9.1f ms  %ld\n", nm[i], g_bdt.t[i], g_bdt.n[i]);
   }
   if (st) {
     BdState hs;

@@ -294,7 +294,7 @@ __device__ __forceinline__ uint32_t bd_alloc(BdState* st, uint32_t* pool, uint32
   return b;
 }
 
-constexpr uint32_t BD_MAX_TILES = 32;  // tile pieces of one output block (at most 3 when P <= Z)
+constexpr uint32_t BD_MAX_TILES = 32;  // descriptors looked at per output block (at most 3 pieces when P <= Z)
 
 template <int KT, bool HV>
 __global__ void __launch_bounds__(MERGE_BLOCK) k_bd_level(BdMem<KT> M, BdState* st, const TileDesc* __restrict__ desc,
@@ -336,8 +336,8 @@ __global__ void __launch_bounds__(MERGE_BLOCK) k_bd_level(BdMem<KT> M, BdState* 
       const uint32_t nt = __ffs(~mask) ? __ffs(~mask) - 1 : 32u;  // tiles are contiguous
       if (in && tid < nt) s_t[tid] = t;
       if (tid == 0) {
-        s_nt = nt;
-        if (nt == 32) atomicExch(&st->err, 1u);
+        s_nt = min(nt, 16u);
+        if (nt > 16) atomicExch(&st->err, 2u);  // never: at most 3 pieces when P <= Z
       }
     }
     __syncthreads();
@@ -355,16 +355,20 @@ __global__ void __launch_bounds__(MERGE_BLOCK) k_bd_level(BdMem<KT> M, BdState* 
       }
     }
     __syncthreads();
-    if (tid == 0) {  // release consumed inputs, then take the output block
-      for (uint32_t x = 0; x < nt; ++x) {
-        const TileDesc t = s_t[x];
-        const uint32_t nA = t.a1 - t.a0, nB = (t.hi - t.lo) - nA;
-        bd_consume(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, t.i + t.a0, nA);
-        bd_consume(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, t.j + (t.lo - t.i) - t.a0, nB);
+    if (tid < 32) {  // warp 0: release consumed inputs (a lane per tile part), then take the output block
+      if (tid < 2 * nt) {
+        const TileDesc t = s_t[tid >> 1];
+        const uint32_t nA = t.a1 - t.a0;
+        if (tid & 1) bd_consume(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, t.j + (t.lo - t.i) - t.a0,
+                                (t.hi - t.lo) - nA);
+        else bd_consume(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, t.i + t.a0, nA);
       }
-      const uint32_t b = bd_alloc(st, pool, cap);
-      s_b = b;
-      if (b != BD_NONE) Tout[v] = b;
+      __syncwarp();
+      if (tid == 0) {
+        const uint32_t b = bd_alloc(st, pool, cap);
+        s_b = b;
+        if (b != BD_NONE) Tout[v] = b;
+      }
     }
     // stable merge of each tile inside shared memory (ties to A)
     for (uint32_t x = 0; x < nt; ++x) {
