@@ -117,6 +117,7 @@ static Cfg make_cfg(uint64_t n, int kt, int hv, int64_t scratch = VMPS_SCRATCH_U
     // default: the largest power of two <= S / 16 (>= 16 scratch blocks)
     uint32_t P = g_blk ? g_blk : (uint32_t)std::max<int64_t>(16, std::min<int64_t>(scratch / 16, DEFAULT_TOUT));
     P = std::min(P, std::min(c.fuse_z, (uint32_t)DEFAULT_TOUT));
+    P = std::min(P, BD_THREADS * MERGE_K);  // a level-pass CTA holds one block's outputs in registers
     uint32_t p2 = 16;
     while (p2 * 2 <= P) p2 *= 2;
     c.P = p2;
@@ -546,6 +547,8 @@ static BdMem<KT> bd_mem(const BdCtx& C) {
   BdMem<KT> M;
   M.k0 = (K*)C.k0; M.v0 = C.v0; M.ks = (K*)C.ks; M.vs = C.vs;
   M.NB = C.NB; M.P = C.P; M.n = C.n; M.has_partial = (C.n % C.P) != 0;
+  M.lg = 0;
+  while ((1u << M.lg) < C.P) ++M.lg;
   return M;
 }
 
@@ -589,7 +592,7 @@ static vmps_status_t bd_levels(const BdCtx& C, const Work& w, uint64_t base, int
     VMPS_CK(cudaFuncSetAttribute(k_bd_level<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)bd_level_smem<KT, HV>(DEFAULT_TOUT)));
     int per_sm = 0;
-    VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bd_level<KT, HV>, MERGE_BLOCK, lsm));
+    VMPS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bd_level<KT, HV>, BD_THREADS, lsm));
     lv_grid[ds][KT][HV][lp] = nsm() * std::max(per_sm, 1);
   }
   const unsigned glv = (unsigned)lv_grid[ds][KT][HV][lp];
@@ -612,7 +615,7 @@ static vmps_status_t bd_levels(const BdCtx& C, const Work& w, uint64_t base, int
     scan_u32(C.dirty, C.didx, nbr + 1, w.scan_tmp, s);
     LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, gfix), 256, 0, s, M, desc, w.btoff, w.bm, C.dirty, C.didx, vb0, nbr,
            C.dlist, C.first_tile, C.remain, w.bD);
-    LAUNCH((k_bd_level<KT, HV>), glv, MERGE_BLOCK, lsm, s, M, st, desc, w.btoff, w.bm, C.dlist, C.first_tile, w.bD,
+    LAUNCH((k_bd_level<KT, HV>), glv, BD_THREADS, lsm, s, M, st, desc, w.btoff, w.bm, C.dlist, C.first_tile, w.bD,
            C.Tin, C.Tout, C.pool, C.cap(), C.remain);
     LAUNCH(k_bd_commit, gNB, 256, 0, s, st, C.dlist, w.bD, C.Tout, C.Tin, C.inv);
   }

@@ -16,6 +16,7 @@
 #pragma once
 #include "engine.cuh"
 #include "plan.cuh"
+#include "ptx.cuh"
 #include <cooperative_groups.h>
 
 namespace vmps {
@@ -39,14 +40,15 @@ struct BdMem {
   K* k0; uint32_t* v0;    // caller's array
   K* ks; uint32_t* vs;    // scratch blocks
   uint32_t NB, P, n, has_partial;
+  uint32_t lg;            // log2 P (P is a power of two)
   __device__ __forceinline__ K* kb(uint32_t b) const {
-    return b < NB ? k0 + (size_t)b * P : ks + (size_t)(b - NB) * P;
+    return b < NB ? k0 + ((size_t)b << lg) : ks + ((size_t)(b - NB) << lg);
   }
   __device__ __forceinline__ uint32_t* vb(uint32_t b) const {
-    return b < NB ? v0 + (size_t)b * P : vs + (size_t)(b - NB) * P;
+    return b < NB ? v0 + ((size_t)b << lg) : vs + ((size_t)(b - NB) << lg);
   }
   __device__ __forceinline__ uint32_t vlen(uint32_t v) const {  // elements of virtual block v
-    return v + 1 < NB ? P : n - v * P;
+    return v + 1 < NB ? P : n - (v << lg);
   }
 };
 
@@ -114,7 +116,7 @@ __global__ void k_bd_tile_counts(const uint32_t* __restrict__ rs, const uint32_t
 template <int KT>
 __device__ __forceinline__ typename KeyTraits<KT>::K bd_key(const BdMem<KT>& M, const uint32_t* Tin,
                                                             uint32_t q) {
-  return M.kb(Tin[q / M.P])[q % M.P];
+  return M.kb(Tin[q >> M.lg])[q & (M.P - 1)];
 }
 
 template <int KT>
@@ -270,7 +272,7 @@ __device__ __forceinline__ void bd_consume(BdState* st, uint32_t* pool, uint32_t
                                            const uint32_t* Tin, uint32_t NB, uint32_t P, uint32_t has_partial,
                                            uint32_t q, uint32_t len) {
   while (len) {
-    const uint32_t v = q / P, off = q % P;
+    const uint32_t v = q / P, off = q & (P - 1);
     const uint32_t c = min(len, P - off);
     bd_release(st, pool, cap, remain, Tin, NB, has_partial, v, c);
     q += c;
@@ -294,10 +296,119 @@ __device__ __forceinline__ uint32_t bd_alloc(BdState* st, uint32_t* pool, uint32
   return b;
 }
 
+#ifndef VMPS_BD_THREADS
+#define VMPS_BD_THREADS 256
+#endif
+constexpr uint32_t BD_THREADS = VMPS_BD_THREADS;  // threads of a level-pass CTA (MERGE_K outputs each)
 constexpr uint32_t BD_MAX_TILES = 32;  // descriptors looked at per output block (at most 3 pieces when P <= Z)
 
+// Per-block header of the level pass: the tiles of one dirty output block and
+// the physical pieces its inputs occupy (each part of <= P elements spans at
+// most two blocks).
+struct BdHdr {
+  uint32_t d, v, nt, valid;
+  TileDesc t[16];
+  uint32_t part[32][2];  // virtual start, length of part x (tile x/2: A part, then B part)
+  uint32_t pc[64][4];    // pieces: physical block, offset in it, length, destination offset
+};
+
+__device__ __forceinline__ void cp_async_el(void* dst, const void* src, int bytes) {
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Warp 1: take the next dirty output block, read its tiles and resolve the
+// physical pieces of their inputs through T_in.
+template <int KT>
+__device__ __forceinline__ void bd_fill_hdr(const BdMem<KT>& M, BdState* st, const TileDesc* __restrict__ desc,
+                                            uint32_t total, const uint32_t* __restrict__ dlist,
+                                            const uint32_t* __restrict__ first_tile, uint32_t D,
+                                            const uint32_t* __restrict__ Tin, BdHdr& H) {
+  const uint32_t lane = threadIdx.x & 31u, P = M.P;
+  uint32_t d = 0;
+  if (lane == 0) d = atomicAdd(&st->ticket, 1u);
+  d = __shfl_sync(0xFFFFFFFFu, d, 0);
+  const bool ok = d < D && !*reinterpret_cast<volatile uint32_t*>(&st->err);
+  if (!ok) {
+    if (lane == 0) H.valid = 0;
+    return;
+  }
+  const uint32_t v = dlist[d];
+  const uint32_t tau = first_tile[d] + lane;
+  TileDesc t{};
+  bool in = tau < total;
+  if (in) { t = desc[tau]; in = (t.lo >> M.lg) == v; }
+  const uint32_t mask = __ballot_sync(0xFFFFFFFFu, in);
+  uint32_t nt = __ffs(~mask) ? __ffs(~mask) - 1 : 32u;  // tiles are contiguous
+  if (nt > 16) {
+    if (lane == 0) atomicExch(&st->err, 2u);  // never: at most 3 pieces when P <= Z
+    nt = 16;
+  }
+  if (lane < nt) H.t[lane] = t;
+  __syncwarp();
+  if (lane < 2 * nt) {  // part `lane`: its virtual range and its (at most two) physical pieces
+    const TileDesc u = H.t[lane >> 1];
+    const uint32_t nA = u.a1 - u.a0, vbase = v << M.lg;
+    uint32_t gq, len, dst;
+    if (lane & 1) { gq = u.j + (u.lo - u.i) - u.a0; len = (u.hi - u.lo) - nA; dst = u.lo - vbase + nA; }
+    else { gq = u.i + u.a0; len = nA; dst = u.lo - vbase; }
+    H.part[lane][0] = gq;
+    H.part[lane][1] = len;
+    const uint32_t off = gq & (P - 1), c = min(len, P - off);
+    H.pc[2 * lane][0] = len ? Tin[gq >> M.lg] : 0u;
+    H.pc[2 * lane][1] = off;
+    H.pc[2 * lane][2] = c;
+    H.pc[2 * lane][3] = dst;
+    const uint32_t rest = len - c;
+    H.pc[2 * lane + 1][0] = rest ? Tin[(gq + c) >> M.lg] : 0u;
+    H.pc[2 * lane + 1][1] = 0;
+    H.pc[2 * lane + 1][2] = rest;
+    H.pc[2 * lane + 1][3] = dst + c;
+  }
+  if (lane == 0) { H.d = d; H.v = v; H.nt = nt; H.valid = 1; }
+}
+
+// All threads: start the asynchronous gather of a block's inputs into a stage.
 template <int KT, bool HV>
-__global__ void __launch_bounds__(MERGE_BLOCK) k_bd_level(BdMem<KT> M, BdState* st, const TileDesc* __restrict__ desc,
+__device__ __forceinline__ void bd_issue(const BdMem<KT>& M, const BdHdr& H, typename KeyTraits<KT>::K* sk,
+                                         uint32_t* sv) {
+  using K = typename KeyTraits<KT>::K;
+  const uint32_t npc = 4 * H.nt;
+  for (uint32_t x = 0; x < npc; ++x) {
+    const uint32_t c = H.pc[x][2];
+    if (!c) continue;
+    const uint32_t b = H.pc[x][0], off = H.pc[x][1], dst = H.pc[x][3];
+    const K* gk = M.kb(b) + off;
+    for (uint32_t q = threadIdx.x; q < c; q += BD_THREADS) cp_async_el(sk + dst + q, gk + q, (int)sizeof(K));
+    if (HV) {
+      const uint32_t* gv = M.vb(b) + off;
+      for (uint32_t q = threadIdx.x; q < c; q += BD_THREADS) cp_async_el(sv + dst + q, gv + q, 4);
+    }
+  }
+  cp_async_commit();
+}
+
+// Warp 0: release the input blocks a header's tiles consume.
+__device__ __forceinline__ void bd_release_hdr(BdState* st, uint32_t* pool, uint32_t cap, uint32_t* remain,
+                                               const uint32_t* Tin, uint32_t NB, uint32_t P, uint32_t has_partial,
+                                               const BdHdr& H) {
+  const uint32_t lane = threadIdx.x & 31u;
+  if (lane < 2 * H.nt) bd_consume(st, pool, cap, remain, Tin, NB, P, has_partial, H.part[lane][0], H.part[lane][1]);
+}
+
+// One level pass.  A CTA pipelines two dirty output blocks: while it merges
+// block t (inputs in stage t & 1) the inputs of block t+1 stream into the
+// other stage (cp.async) and warp 1 reads the tiles of block t+2.  Before
+// block t takes its output block, block t+1's inputs have landed and are
+// released, so whenever every CTA waits for a free block, every taken
+// block has released its inputs (no fewer free blocks than an in-order
+// round schedule would have).
+template <int KT, bool HV>
+__global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* st, const TileDesc* __restrict__ desc,
                                                           const uint32_t* __restrict__ toff,
                                                           const uint32_t* __restrict__ m_ptr,
                                                           const uint32_t* __restrict__ dlist,
@@ -308,85 +419,86 @@ __global__ void __launch_bounds__(MERGE_BLOCK) k_bd_level(BdMem<KT> M, BdState* 
                                                           uint32_t* __restrict__ remain) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
+  constexpr uint32_t OPT = MERGE_K;  // outputs per thread (P <= BD_THREADS * MERGE_K)
   extern __shared__ __align__(16) unsigned char bd_smem[];
   const uint32_t P = M.P;
-  K* ik = reinterpret_cast<K*>(bd_smem);
-  K* ok = ik + P;
-  uint32_t* iv = reinterpret_cast<uint32_t*>(ok + P);
-  uint32_t* ov = iv + (HV ? P : 0);
-  __shared__ TileDesc s_t[BD_MAX_TILES];
-  __shared__ uint32_t s_d, s_nt, s_b;
+  K* const stk0 = reinterpret_cast<K*>(bd_smem);
+  uint32_t* const stv0 = reinterpret_cast<uint32_t*>(stk0 + 2 * P);
+  auto stk = [&](uint32_t s) { return stk0 + s * P; };
+  auto stv = [&](uint32_t s) { return stv0 + (HV ? s * P : 0u); };
+  __shared__ BdHdr hdr[3];
+  __shared__ uint32_t s_b;
   const uint32_t D = *D_ptr, total = toff[*m_ptr];
-  const uint32_t tid = threadIdx.x;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5;
   const bool vec = ((reinterpret_cast<uintptr_t>(M.k0) | reinterpret_cast<uintptr_t>(M.v0) |
                      reinterpret_cast<uintptr_t>(M.ks) | reinterpret_cast<uintptr_t>(M.vs)) & 15u) == 0;
   if (blockIdx.x == 0 && tid == 0 && D) atomicAdd(&st->rounds, 1u);
-  for (;;) {
-    if (tid == 0) s_d = atomicAdd(&st->ticket, 1u);
-    __syncthreads();
-    const uint32_t d = s_d;
-    if (d >= D || *reinterpret_cast<volatile uint32_t*>(&st->err)) break;
-    const uint32_t v = dlist[d], vbase = v * P, len = M.vlen(v);
-    if (tid < 32) {  // the block's tiles: consecutive descriptors from first_tile[d] with lo in block v
-      const uint32_t tau = first_tile[d] + tid;
-      TileDesc t{};
-      bool in = tau < total;
-      if (in) { t = desc[tau]; in = t.lo / P == v; }
-      const uint32_t mask = __ballot_sync(0xFFFFFFFFu, in);
-      const uint32_t nt = __ffs(~mask) ? __ffs(~mask) - 1 : 32u;  // tiles are contiguous
-      if (in && tid < nt) s_t[tid] = t;
-      if (tid == 0) {
-        s_nt = min(nt, 16u);
-        if (nt > 16) atomicExch(&st->err, 2u);  // never: at most 3 pieces when P <= Z
+  // prologue: block t = first ticket, gathered and released; header of t+1
+  if (warp == 1) bd_fill_hdr<KT>(M, st, desc, total, dlist, first_tile, D, Tin, hdr[0]);
+  __syncthreads();
+  if (!hdr[0].valid) return;
+  bd_issue<KT, HV>(M, hdr[0], stk(0), stv(0));
+  if (warp == 1) bd_fill_hdr<KT>(M, st, desc, total, dlist, first_tile, D, Tin, hdr[1]);
+  cp_async_wait_all();
+  __syncthreads();
+  if (warp == 0) bd_release_hdr(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, hdr[0]);
+  __syncthreads();
+  for (uint32_t it = 0;; ++it) {
+    const uint32_t s = it & 1u;
+    const BdHdr& H0 = hdr[it % 3];
+    BdHdr& H1 = hdr[(it + 1) % 3];
+    BdHdr& H2 = hdr[(it + 2) % 3];
+    const bool more = H1.valid;
+    if (more) bd_issue<KT, HV>(M, H1, stk(s ^ 1u), stv(s ^ 1u));
+    if (warp == 1) {
+      if (more) bd_fill_hdr<KT>(M, st, desc, total, dlist, first_tile, D, Tin, H2);
+      else if ((tid & 31u) == 0) H2.valid = 0;
+    }
+    // merge block t into registers: this thread's outputs [OPT tid, OPT tid + OPT)
+    const uint32_t v = H0.v, vbase = v << M.lg, len = M.vlen(v);
+    const uint32_t c0 = tid * OPT, c1 = min(c0 + OPT, len);
+    K* const sk = stk(s);
+    uint32_t* const sv = stv(s);
+    K rk[OPT];
+    uint32_t rv[OPT];
+    for (uint32_t x = 0; x < H0.nt; ++x) {
+      const TileDesc t = H0.t[x];
+      const uint32_t o = t.lo - vbase, cnt = t.hi - t.lo, nA = t.a1 - t.a0, nB = cnt - nA;
+      if (o >= c1 || o + cnt <= c0) continue;
+      const uint32_t s0 = max(c0, o) - o;
+      const K* A = sk + o;
+      const K* B = A + nA;
+      uint32_t ia = corank<KT>(A, nA, B, nB, s0), ib = s0 - ia;
+#pragma unroll
+      for (uint32_t r = 0; r < OPT; ++r) {
+        const uint32_t pos = c0 + r;
+        if (pos >= o && pos < o + cnt && pos < c1) {
+          const bool takeA = ib >= nB || (ia < nA && T::ord(A[ia]) <= T::ord(B[ib]));
+          const uint32_t sidx = takeA ? ia : nA + ib;
+          rk[r] = A[sidx];
+          if (HV) rv[r] = sv[o + sidx];
+          ia += takeA ? 1u : 0u;
+          ib += takeA ? 0u : 1u;
+        }
       }
     }
-    __syncthreads();
-    const uint32_t nt = s_nt;
-    // gather: tile x's A part then B part at its output offsets
-    for (uint32_t x = 0; x < nt; ++x) {
-      const TileDesc t = s_t[x];
-      const uint32_t nA = t.a1 - t.a0, cnt = t.hi - t.lo, o = t.lo - vbase;
-      const uint32_t aoff = t.i + t.a0, boff = t.j + (t.lo - t.i) - t.a0;
-      for (uint32_t q = tid; q < cnt; q += MERGE_BLOCK) {
-        const uint32_t g = q < nA ? aoff + q : boff + (q - nA);
-        const uint32_t b = Tin[g / P], w = g % P;
-        ik[o + q] = M.kb(b)[w];
-        if (HV) iv[o + q] = M.vb(b)[w];
+    __syncthreads();  // every input of block t has been read
+#pragma unroll
+    for (uint32_t r = 0; r < OPT; ++r) {
+      if (c0 + r < c1) {
+        sk[c0 + r] = rk[r];
+        if (HV) sv[c0 + r] = rv[r];
       }
     }
+    cp_async_wait_all();  // block t+1's inputs have landed
     __syncthreads();
-    if (tid < 32) {  // warp 0: release consumed inputs (a lane per tile part), then take the output block
-      if (tid < 2 * nt) {
-        const TileDesc t = s_t[tid >> 1];
-        const uint32_t nA = t.a1 - t.a0;
-        if (tid & 1) bd_consume(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, t.j + (t.lo - t.i) - t.a0,
-                                (t.hi - t.lo) - nA);
-        else bd_consume(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, t.i + t.a0, nA);
-      }
+    if (warp == 0) {
+      if (more) bd_release_hdr(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, H1);
       __syncwarp();
       if (tid == 0) {
         const uint32_t b = bd_alloc(st, pool, cap);
         s_b = b;
         if (b != BD_NONE) Tout[v] = b;
-      }
-    }
-    // stable merge of each tile inside shared memory (ties to A)
-    for (uint32_t x = 0; x < nt; ++x) {
-      const TileDesc t = s_t[x];
-      const uint32_t nA = t.a1 - t.a0, cnt = t.hi - t.lo, o = t.lo - vbase, nB = cnt - nA;
-      const K* A = ik + o;
-      const K* B = A + nA;
-      for (uint32_t q0 = tid * MERGE_K; q0 < cnt; q0 += MERGE_BLOCK * MERGE_K) {
-        uint32_t ia = corank<KT>(A, nA, B, nB, q0), ib = q0 - ia;
-        const uint32_t qe = min(q0 + MERGE_K, cnt);
-        for (uint32_t q = q0; q < qe; ++q) {
-          const bool takeA = ib >= nB || (ia < nA && T::ord(A[ia]) <= T::ord(B[ib]));
-          const uint32_t sidx = takeA ? ia : nA + ib;
-          ok[o + q] = A[sidx];
-          if (HV) ov[o + q] = iv[o + sidx];
-          ia += takeA ? 1u : 0u;
-          ib += takeA ? 0u : 1u;
-        }
       }
     }
     __syncthreads();
@@ -395,15 +507,18 @@ __global__ void __launch_bounds__(MERGE_BLOCK) k_bd_level(BdMem<KT> M, BdState* 
     K* dk = M.kb(b);
     constexpr uint32_t KV = 16 / sizeof(K);
     const uint32_t nv = vec ? len / KV : 0u;
-    for (uint32_t q = tid; q < nv; q += MERGE_BLOCK) reinterpret_cast<uint4*>(dk)[q] = reinterpret_cast<const uint4*>(ok)[q];
-    for (uint32_t q = nv * KV + tid; q < len; q += MERGE_BLOCK) dk[q] = ok[q];
+    for (uint32_t q = tid; q < nv; q += BD_THREADS)
+      reinterpret_cast<uint4*>(dk)[q] = reinterpret_cast<const uint4*>(sk)[q];
+    for (uint32_t q = nv * KV + tid; q < len; q += BD_THREADS) dk[q] = sk[q];
     if (HV) {
       uint32_t* dv = M.vb(b);
       const uint32_t nv4 = vec ? len / 4 : 0u;
-      for (uint32_t q = tid; q < nv4; q += MERGE_BLOCK) reinterpret_cast<uint4*>(dv)[q] = reinterpret_cast<const uint4*>(ov)[q];
-      for (uint32_t q = nv4 * 4 + tid; q < len; q += MERGE_BLOCK) dv[q] = ov[q];
+      for (uint32_t q = tid; q < nv4; q += BD_THREADS)
+        reinterpret_cast<uint4*>(dv)[q] = reinterpret_cast<const uint4*>(sv)[q];
+      for (uint32_t q = nv4 * 4 + tid; q < len; q += BD_THREADS) dv[q] = sv[q];
     }
-    __syncthreads();
+    __syncthreads();  // stage s is free for block t+2; header slot t is free
+    if (!more) break;
   }
 }
 
