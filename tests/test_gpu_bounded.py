@@ -197,6 +197,30 @@ def test_bounded_chunked(vm, chunk, n, dtype, kind):
     assert meta_chunked < st1["metadata_bytes"]
 
 
+@pytest.mark.parametrize("blk,n,dtype,hv,minrun", [(32, 150_001, np.float32, False, 0), (64, 200_000, np.uint64, True, 4),
+                                                    (16, 70_003, np.uint32, True, 1), (16, 90_000, np.uint32, False, 0)])
+def test_bounded_cells_small_blocks(vm, blk, n, dtype, hv, minrun):
+    """Dyadic cells of 4096 elements over one shared block table whose
+    blocks (16-64 elements, Z = 64) are far smaller than a cell: cell edges
+    fall inside blocks, so the first block of most cells and detection
+    chunks is brought home before it is read in place (bd_home); keys only
+    and with payload, a partial last block; result, M and run count equal
+    the oracle's."""
+    rng = np.random.default_rng(blk * 1000 + n)
+    keys = _structured(rng, n, dtype)
+    vals = np.arange(n, dtype=np.uint32) if hv else None
+    try:
+        vm.test_set_tiles(64, 0, blk)
+        vm.test_set_bd_chunk(4096)
+        st = bounded_vs_oracle(vm, keys, vals, scratch=12 * blk, minrun=minrun)
+        _, _, _, ost = oracle.sort(keys, vals, minrun_override=minrun)
+        assert st["runs"] == ost["runs"]
+    finally:
+        vm.test_set_bd_chunk(0)
+        vm.test_set_tiles(0, 0, 0)
+        vm.test_set_minrun(0)
+
+
 @pytest.mark.parametrize("nruns,n,dtype", [(2, 400_000, np.uint32), (5, 300_001, np.uint64), (9, 200_000, np.float32)])
 def test_merge_runs_bounded(vm, nruns, n, dtype):
     """vmps_merge_runs_bounded (the multi-GPU bounded protocol's re-merge):
