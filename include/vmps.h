@@ -91,7 +91,7 @@ typedef struct {
   uint32_t levels_executed;/* merge levels with at least one HBM merge */
   uint32_t minrun;
   uint32_t block_elems;    /* bounded mode: block size P_blk (0 if unbounded) */
-  uint64_t rounds;         /* bounded mode: merge rounds (0 if unbounded) */
+  uint64_t rounds;         /* bounded mode: level passes that moved data (0 if unbounded) */
   uint64_t peak_extra_device_bytes; /* workspace bytes actually used */
   uint64_t scratch_bytes;  /* element scratch part of it */
   uint64_t metadata_bytes; /* plan / table / relocation metadata part of it */
@@ -115,7 +115,14 @@ vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals,
 
 /* Stable in-place sort of keys[0,n) (layout: contiguous array of the key
  * type).  scratch_elems: VMPS_SCRATCH_UNBOUNDED, or a cap on element scratch
- * (bounded mode: the output is identical; BASELINE.json north_star (4)). */
+ * (bounded mode: the output is identical; BASELINE.json north_star (4); the
+ * paper's VM Powersort).  Bounded mode: one dataflow pass per
+ * merge level through a block table (free blocks reused as soon as their
+ * elements are consumed), then the Copy into physical order; above two cells
+ * of 2^23 elements the plan is processed in dyadic cells of the run
+ * midpoints so that metadata is O(cell / minrun + n / P) and the
+ * executed merges are still exactly Alg. 1's.  The bounded mode synchronises
+ * `stream` (per cell and at the end). */
 vmps_status_t vmps_sort_keys(void* keys, uint64_t n, vmps_key_t kt, int64_t scratch_elems,
                              void* ws, size_t ws_bytes, void* stream, vmps_stats_t* h_stats);
 
@@ -372,10 +379,10 @@ vmps_status_t vmps_merge_runs(void* keys, uint32_t* vals, uint64_t n, vmps_key_t
 /* vmps_merge_runs_bounded: as vmps_merge_runs (adjacent sorted runs starting
  * at h_run_start[0] = 0 < ... < n, host array; ties to the earlier run), with
  * the element scratch capped at scratch_elems like the bounded sort (block
- * table, rounds into freed blocks, final Copy); the plan is built from the
- * given runs (no run detection), so its metadata is O(nruns + n / P).
+ * table, level passes into freed blocks, final Copy); the plan is built from
+ * the given runs (no run detection), so its metadata is O(nruns + n / P).
  * Workspace: vmps_merge_runs_bounded_workspace_bytes.  Synchronises `stream`
- * (the bounded rounds). */
+ * (the bounded mode's error check). */
 vmps_status_t vmps_merge_runs_bounded_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, uint32_t nruns,
                                                       int64_t scratch_elems, size_t* h_bytes);
 vmps_status_t vmps_merge_runs_bounded(void* keys, uint32_t* vals, uint64_t n, vmps_key_t kt,
