@@ -214,7 +214,8 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     // the bounded mode also scans its dirty-block flags (NB + 1 entries),
     // which exceed R when the block is smaller than minrun
     const size_t nbs = c.gt_nb ? (size_t)c.gt_nb : (size_t)((n + c.P - 1) / c.P);
-    const size_t scan_len = t.bounded ? std::max<size_t>(R, nbs + 1) : R;
+    const size_t nlt = ((size_t)t.rmax + BD_LVL_TILE) / BD_LVL_TILE;  // level-schedule tiles over [0, rmax]
+    const size_t scan_len = t.bounded ? std::max<size_t>(std::max<size_t>(R, nbs + 1), BD_LVL_BINS * nlt + 1) : R;
     t.scan_tmp = (uint32_t*)take(scan_tmp_words(scan_len) * 4 + 64);
   }
   t.counters = (unsigned long long*)take(8 * 8);
@@ -240,6 +241,9 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.btoff = t.long_idx;
     t.bm = (uint32_t*)take(64);
     t.bD = (uint32_t*)take(64);
+    const size_t nlt = ((size_t)t.rmax + BD_LVL_TILE) / BD_LVL_TILE;
+    t.lvl_hist = (uint32_t*)take((BD_LVL_BINS * nlt + 1) * 4);
+    t.lvl_hscan = (uint32_t*)take((BD_LVL_BINS * nlt + 1) * 4);
   }
   if (t.bounded && !c.gt_nb) {
     const size_t NBp = (size_t)t.NB + 8, NP = (size_t)t.NB + c.F + 8;
@@ -599,24 +603,28 @@ static vmps_status_t bd_levels(const BdCtx& C, const Work& w, uint64_t base, int
   const unsigned gfix = nsm() * 4;
   // highest power first; no host synchronisation: every kernel reads the
   // level's sizes from device memory
+  // the call's level schedule: non-fused nodes bucketed by power (stable),
+  // tile counts of every node, once
+  const uint32_t nlt = (w.rmax + BD_LVL_TILE) / BD_LVL_TILE;
+  LAUNCH(k_lvl_hist, nlt, BD_LVL_TILE, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, fuse_z, nlt,
+         w.lvl_hist);
+  scan_u32(w.lvl_hist, w.lvl_hscan, BD_LVL_BINS * nlt + 1, w.scan_tmp, s);
+  LAUNCH(k_lvl_scatter, nlt, BD_LVL_TILE, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, fuse_z, nlt,
+         w.lvl_hscan, w.blnodes);
+  LAUNCH(k_bd_tile_counts, g, 256, 0, s, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.lvl_hscan, nlt, C.P, C.n,
+         w.rmax, w.bcnt);
+  scan_u32(w.bcnt, w.btoff, w.rmax + 1, w.scan_tmp, s);
   for (int p = p_hi; p >= p_lo; --p) {
-    LAUNCH(k_bd_flags, g, 256, 0, s, w.run_start, w.scalars, w.power, w.seg_l, w.seg_r, fuse_z, p, w.rmax,
-           w.bflag);
-    scan_u32(w.bflag, w.bpos, w.rmax + 1, w.scan_tmp, s);
-    LAUNCH(k_bd_nodes, g, 256, 0, s, w.run_start, w.scalars, w.seg_l, w.seg_r, w.bflag, w.bpos, w.rmax,
-           w.blnodes, w.bm);
-    LAUNCH(k_bd_tile_counts, g, 256, 0, s, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.bm, C.P, C.n, w.rmax,
-           w.bcnt);
-    scan_u32(w.bcnt, w.btoff, w.rmax + 1, w.scan_tmp, s);
+    LAUNCH(k_bd_level_info, 1, 32, 0, s, w.lvl_hscan, nlt, w.btoff, p, w.bm);
     LAUNCH(k_bd_tile_desc<KT>, gfix, 256, 0, s, M, C.Tin, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.bm, w.btoff,
            C.bdesc_cap, st, desc);
     VMPS_CK(cudaMemsetAsync(C.dirty, 0, (size_t)(nbr + 1) * 4, s));
-    LAUNCH(k_bd_mark<KT>, gfix, 256, 0, s, M, C.Tin, desc, w.btoff, w.bm, C.P, vb0, C.dirty);
+    LAUNCH(k_bd_mark<KT>, gfix, 256, 0, s, M, C.Tin, desc, w.bm, C.P, vb0, C.dirty);
     scan_u32(C.dirty, C.didx, nbr + 1, w.scan_tmp, s);
-    LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, gfix), 256, 0, s, M, desc, w.btoff, w.bm, C.dirty, C.didx, vb0, nbr,
-           C.dlist, C.first_tile, C.remain, w.bD);
-    LAUNCH((k_bd_level<KT, HV>), glv, BD_THREADS, lsm, s, M, st, desc, w.btoff, w.bm, C.dlist, C.first_tile, w.bD,
-           C.Tin, C.Tout, C.pool, C.cap(), C.remain);
+    LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, gfix), 256, 0, s, M, desc, w.bm, C.dirty, C.didx, vb0, nbr, C.dlist,
+           C.first_tile, C.remain, w.bD);
+    LAUNCH((k_bd_level<KT, HV>), glv, BD_THREADS, lsm, s, M, st, desc, w.bm, C.dlist, C.first_tile, w.bD, C.Tin,
+           C.Tout, C.pool, C.cap(), C.remain);
     LAUNCH(k_bd_commit, gNB, 256, 0, s, st, C.dlist, w.bD, C.Tout, C.Tin, C.inv);
   }
   return VMPS_OK;

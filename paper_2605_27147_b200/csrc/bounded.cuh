@@ -53,31 +53,84 @@ struct BdMem {
 };
 
 // --- per-level setup ------------------------------------------------------
-// flag[t] = 1 for the non-fused nodes of power p (zero tail up to cap).
-__global__ void k_bd_flags(const uint32_t* __restrict__ rs, const uint32_t* scalars,
-                           const uint8_t* __restrict__ power, const uint32_t* __restrict__ seg_l,
-                           const uint32_t* __restrict__ seg_r, uint32_t fuse_z, int p, uint32_t cap,
-                           uint32_t* __restrict__ flag) {
+// --- the call's level schedule, built once --------------------------------
+// The non-fused nodes (segment > fuse_z) bucketed by power, in position order
+// inside each bucket (a stable counting sort: per-tile histograms, one scan in
+// bucket-major order, a stable scatter), so that level p is the slice
+// [hscan[p T], hscan[(p + 1) T]) of lnodes (T tiles of 1024 boundaries).
+constexpr uint32_t BD_LVL_TILE = 1024;
+constexpr uint32_t BD_LVL_BINS = 64;
+
+__device__ __forceinline__ uint32_t bd_node_bin(const uint32_t* rs, const uint32_t* seg_l, const uint32_t* seg_r,
+                                                const uint8_t* power, uint32_t r, uint32_t fuse_z, uint32_t t) {
+  if (t < 1 || t >= r) return BD_LVL_BINS;
+  return seg_size(rs, seg_l, seg_r, t) > fuse_z ? (uint32_t)power[t] : BD_LVL_BINS;
+}
+
+__global__ void __launch_bounds__(BD_LVL_TILE) k_lvl_hist(const uint32_t* __restrict__ rs, const uint32_t* scalars,
+                                                          const uint8_t* __restrict__ power,
+                                                          const uint32_t* __restrict__ seg_l,
+                                                          const uint32_t* __restrict__ seg_r, uint32_t fuse_z,
+                                                          uint32_t ntiles, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[BD_LVL_BINS];
   const uint32_t r = scalars[SC_RUNS];
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= cap; t += gridDim.x * blockDim.x) {
-    uint32_t f = 0;
-    if (t >= 1 && t < r && power[t] == p && seg_size(rs, seg_l, seg_r, t) > fuse_z) f = 1;
-    flag[t] = f;
+  if (threadIdx.x < BD_LVL_BINS) h[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t t = blockIdx.x * BD_LVL_TILE + threadIdx.x;
+  const uint32_t bin = bd_node_bin(rs, seg_l, seg_r, power, r, fuse_z, t);
+  if (bin < BD_LVL_BINS) atomicAdd(&h[bin], 1u);
+  __syncthreads();
+  if (threadIdx.x < BD_LVL_BINS) hist[threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+  if (blockIdx.x == 0 && threadIdx.x == 0) hist[BD_LVL_BINS * ntiles] = 0;  // the scan's total slot
+}
+
+__global__ void __launch_bounds__(BD_LVL_TILE) k_lvl_scatter(const uint32_t* __restrict__ rs, const uint32_t* scalars,
+                                                             const uint8_t* __restrict__ power,
+                                                             const uint32_t* __restrict__ seg_l,
+                                                             const uint32_t* __restrict__ seg_r, uint32_t fuse_z,
+                                                             uint32_t ntiles, const uint32_t* __restrict__ hscan,
+                                                             uint32_t* __restrict__ lnodes) {
+  __shared__ uint32_t wc[BD_LVL_TILE / 32][BD_LVL_BINS];  // per-warp bucket counts
+  const uint32_t r = scalars[SC_RUNS];
+  const uint32_t lane = threadIdx.x & 31u, wp = threadIdx.x >> 5;
+  for (uint32_t x = threadIdx.x; x < (BD_LVL_TILE / 32) * BD_LVL_BINS; x += BD_LVL_TILE) (&wc[0][0])[x] = 0;
+  __syncthreads();
+  const uint32_t t = blockIdx.x * BD_LVL_TILE + threadIdx.x;
+  const uint32_t bin = bd_node_bin(rs, seg_l, seg_r, power, r, fuse_z, t);
+  const uint32_t peers = __match_any_sync(0xFFFFFFFFu, bin);
+  const uint32_t rank = (uint32_t)__popc(peers & ((1u << lane) - 1u));
+  if (bin < BD_LVL_BINS && rank == 0) wc[wp][bin] = (uint32_t)__popc(peers);
+  __syncthreads();
+  if (bin < BD_LVL_BINS) {
+    uint32_t pos = hscan[bin * ntiles + blockIdx.x] + rank;
+    for (uint32_t w = 0; w < wp; ++w) pos += wc[w][bin];
+    lnodes[pos] = t;
   }
 }
 
-// Nodes of the level in position order, and their tile counts: the node's
-// output tiles (one per block it touches) plus gap copy-tiles before/after it
-// inside its first/last block.
-__global__ void k_bd_nodes(const uint32_t* __restrict__ rs, const uint32_t* scalars,
-                           const uint32_t* __restrict__ seg_l, const uint32_t* __restrict__ seg_r,
-                           const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
-                           uint32_t cap, uint32_t* __restrict__ lnodes, uint32_t* __restrict__ m_out) {
-  const uint32_t r = scalars[SC_RUNS];
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= cap; t += gridDim.x * blockDim.x) {
-    if (t < r && flag[t]) lnodes[pos[t]] = t;
-    if (t == cap) *m_out = pos[cap];
+// Tile counts of every bucketed node (neighbours only within its level) and,
+// per level pass, the level's slice: info = {ls, m, first tile, tiles}.
+__device__ __forceinline__ void bd_level_of(const uint32_t* hscan, uint32_t ntiles, uint32_t x, uint32_t* ls,
+                                            uint32_t* le) {
+  uint32_t lo = 0, hi = BD_LVL_BINS;  // last bin p with hscan[p T] <= x
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (hscan[mid * ntiles] <= x) lo = mid;
+    else hi = mid;
   }
+  while (lo + 1 < BD_LVL_BINS && hscan[(lo + 1) * ntiles] <= x) ++lo;  // skip empty bins
+  *ls = hscan[lo * ntiles];
+  *le = hscan[(lo + 1) * ntiles];
+}
+
+__global__ void k_bd_level_info(const uint32_t* __restrict__ hscan, uint32_t ntiles,
+                                const uint32_t* __restrict__ toff, int p, uint32_t* __restrict__ info) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const uint32_t ls = hscan[(uint32_t)p * ntiles], le = hscan[(uint32_t)(p + 1) * ntiles];
+  info[0] = ls;
+  info[1] = le - ls;
+  info[2] = toff[ls];
+  info[3] = toff[le] - toff[ls];
 }
 
 __device__ __forceinline__ void bd_node_geom(const uint32_t* rs, const uint32_t* seg_l, const uint32_t* seg_r,
@@ -98,14 +151,15 @@ __device__ __forceinline__ void bd_node_geom(const uint32_t* rs, const uint32_t*
 
 __global__ void k_bd_tile_counts(const uint32_t* __restrict__ rs, const uint32_t* __restrict__ seg_l,
                                  const uint32_t* __restrict__ seg_r, const uint32_t* __restrict__ lnodes,
-                                 const uint32_t* __restrict__ m_ptr, uint32_t P, uint32_t n, uint32_t cap,
-                                 uint32_t* __restrict__ cnt) {
-  const uint32_t m = *m_ptr;
+                                 const uint32_t* __restrict__ hscan, uint32_t ntiles, uint32_t P, uint32_t n,
+                                 uint32_t cap, uint32_t* __restrict__ cnt) {
+  const uint32_t X = hscan[BD_LVL_BINS * ntiles];
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= cap; x += gridDim.x * blockDim.x) {
     uint32_t c = 0;
-    if (x < m) {
-      uint32_t i, j, k, gl, gh;
-      bd_node_geom(rs, seg_l, seg_r, lnodes, m, x, P, n, &i, &j, &k, &gl, &gh);
+    if (x < X) {
+      uint32_t ls, le, i, j, k, gl, gh;
+      bd_level_of(hscan, ntiles, x, &ls, &le);
+      bd_node_geom(rs, seg_l, seg_r, lnodes + ls, le - ls, x - ls, P, n, &i, &j, &k, &gl, &gh);
       c = (k + P - 1) / P - i / P + (gl < i ? 1u : 0u) + (gh > k ? 1u : 0u);
     }
     cnt[x] = c;
@@ -138,23 +192,24 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
                                                       const uint32_t* __restrict__ rs,
                                                       const uint32_t* __restrict__ seg_l,
                                                       const uint32_t* __restrict__ seg_r,
-                                                      const uint32_t* __restrict__ lnodes,
-                                                      const uint32_t* __restrict__ m_ptr,
-                                                      const uint32_t* __restrict__ toff, uint32_t cap,
+                                                      const uint32_t* __restrict__ lnodes_all,
+                                                      const uint32_t* __restrict__ info,
+                                                      const uint32_t* __restrict__ toff_all, uint32_t cap,
                                                       BdState* st, TileDesc* __restrict__ desc) {
-  const uint32_t m = *m_ptr;
-  const uint32_t total = toff[m];
+  const uint32_t ls = info[0], m = info[1], T0 = info[2], total = info[3];
+  const uint32_t* lnodes = lnodes_all + ls;
+  const uint32_t* toff = toff_all + ls;
   if (total > cap) {  // capacity is sized from the plan; never expected
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicExch(&st->err, 2u);
     return;
   }
   const uint32_t P = M.P, n = M.n;
   for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x) {
-    uint32_t a = 0, b = m;  // last node x with toff[x] <= tau
-    while (b - a > 1) { uint32_t mm = (a + b) >> 1; if (toff[mm] <= tau) a = mm; else b = mm; }
+    uint32_t a = 0, b = m;  // last node x with toff[x] - T0 <= tau
+    while (b - a > 1) { uint32_t mm = (a + b) >> 1; if (toff[mm] - T0 <= tau) a = mm; else b = mm; }
     uint32_t i, j, k, gl, gh;
     bd_node_geom(rs, seg_l, seg_r, lnodes, m, a, P, n, &i, &j, &k, &gl, &gh);
-    uint32_t loc = tau - toff[a];
+    uint32_t loc = tau - (toff[a] - T0);
     TileDesc D;
     D.par = 0;
     if (gl < i && loc == 0) {  // left gap: copy [gl, i)
@@ -193,10 +248,9 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
 // ever consume inputs from dirty blocks.)
 template <int KT>
 __global__ void k_bd_mark(BdMem<KT> M, const uint32_t* __restrict__ Tin, TileDesc* __restrict__ desc,
-                          const uint32_t* __restrict__ toff, const uint32_t* __restrict__ m_ptr, uint32_t P,
-                          uint32_t vb0, uint32_t* __restrict__ dirty) {
+                          const uint32_t* __restrict__ info, uint32_t P, uint32_t vb0, uint32_t* __restrict__ dirty) {
   using T = KeyTraits<KT>;
-  const uint32_t total = toff[*m_ptr];
+  const uint32_t total = info[3];
   for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x) {
     const TileDesc d = desc[tau];
     if (d.par == 1) continue;  // gap tile
@@ -212,12 +266,11 @@ __global__ void k_bd_mark(BdMem<KT> M, const uint32_t* __restrict__ Tin, TileDes
 // Dirty blocks of the range [vb0, vb0 + nbr) (flags and their scan are
 // indexed relative to vb0): their list, first tiles and consumption counters.
 template <int KT>
-__global__ void k_bd_dirty_list(BdMem<KT> M, const TileDesc* __restrict__ desc, const uint32_t* __restrict__ toff,
-                                const uint32_t* __restrict__ m_ptr, const uint32_t* __restrict__ dirty,
-                                const uint32_t* __restrict__ didx, uint32_t vb0, uint32_t nbr,
-                                uint32_t* __restrict__ dlist, uint32_t* __restrict__ first_tile,
+__global__ void k_bd_dirty_list(BdMem<KT> M, const TileDesc* __restrict__ desc, const uint32_t* __restrict__ info,
+                                const uint32_t* __restrict__ dirty, const uint32_t* __restrict__ didx, uint32_t vb0,
+                                uint32_t nbr, uint32_t* __restrict__ dlist, uint32_t* __restrict__ first_tile,
                                 uint32_t* __restrict__ remain, uint32_t* __restrict__ D_out) {
-  const uint32_t total = toff[*m_ptr];
+  const uint32_t total = info[3];
   const uint32_t P = M.P;
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < nbr; x += gridDim.x * blockDim.x) {
     if (dirty[x]) {
@@ -409,8 +462,7 @@ __device__ __forceinline__ void bd_release_hdr(BdState* st, uint32_t* pool, uint
 // round schedule would have).
 template <int KT, bool HV>
 __global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* st, const TileDesc* __restrict__ desc,
-                                                          const uint32_t* __restrict__ toff,
-                                                          const uint32_t* __restrict__ m_ptr,
+                                                          const uint32_t* __restrict__ info,
                                                           const uint32_t* __restrict__ dlist,
                                                           const uint32_t* __restrict__ first_tile,
                                                           const uint32_t* __restrict__ D_ptr,
@@ -428,7 +480,7 @@ __global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* s
   auto stv = [&](uint32_t s) { return stv0 + (HV ? s * P : 0u); };
   __shared__ BdHdr hdr[3];
   __shared__ uint32_t s_b;
-  const uint32_t D = *D_ptr, total = toff[*m_ptr];
+  const uint32_t D = *D_ptr, total = info[3];
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
   const bool vec = ((reinterpret_cast<uintptr_t>(M.k0) | reinterpret_cast<uintptr_t>(M.v0) |
                      reinterpret_cast<uintptr_t>(M.ks) | reinterpret_cast<uintptr_t>(M.vs)) & 15u) == 0;

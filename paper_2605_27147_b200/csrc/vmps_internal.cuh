@@ -138,6 +138,7 @@ struct Work {
   uint32_t P, F, NB;
   uint32_t *Tin, *Tout, *inv, *pool, *remain, *dirty, *didx, *dlist, *first_tile;
   uint32_t *bflag, *bpos, *blnodes, *bcnt, *btoff, *bm, *bD;
+  uint32_t *lvl_hist, *lvl_hscan;  // level schedule: per-tile power histograms and their scan
   void* bdesc;
   uint32_t bdesc_cap;
   void* bstate;
