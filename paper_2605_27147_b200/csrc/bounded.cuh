@@ -355,15 +355,29 @@ __device__ __forceinline__ uint32_t bd_alloc(BdState* st, uint32_t* pool, uint32
 constexpr uint32_t BD_THREADS = VMPS_BD_THREADS;  // threads of a level-pass CTA (MERGE_K outputs each)
 constexpr uint32_t BD_MAX_TILES = 32;  // descriptors looked at per output block (at most 3 pieces when P <= Z)
 
-// Per-block header of the level pass: the tiles of one dirty output block and
-// the physical pieces its inputs occupy (each part of <= P elements spans at
-// most two blocks).
+// Per-block header of the level pass: the tiles of one dirty output block,
+// the inputs of each tile (part 2x = its A range, 2x+1 = its B range, each of
+// <= P elements, so spanning at most two physical blocks) and where each part
+// lands in the stage.  A part's keys occupy their own stage region, whose start
+// is 16-byte aligned and offset by the part's misalignment in global memory
+// (ko = region start + gq mod (16 / sizeof(K))), so that each of its (at most
+// two) pieces is ONE bulk copy (cp.async.bulk, TMA engine) of the 16-byte
+// aligned superset of the piece; values likewise (vo).
 struct BdHdr {
   uint32_t d, v, nt, valid;
+  uint32_t nslow;       // pieces gathered element by element (unaligned arrays / the caller's partial last block)
+  uint32_t pad[3];
   TileDesc t[16];
-  uint32_t part[32][2];  // virtual start, length of part x (tile x/2: A part, then B part)
-  uint32_t pc[64][4];    // pieces: physical block, offset in it, length, destination offset
+  uint32_t part[32][2];  // virtual start, length of part x
+  uint32_t ko[32], vo[32];  // stage index of part x's first key / value
+  uint32_t pcb[32][2];   // physical blocks of part x's two pieces; bit 31: gathered element-wise
 };
+constexpr uint32_t BD_SLOW = 0x80000000u;
+
+// Slack after each part's region: the superset rounding (< one 16-byte unit
+// on either side) plus the branch-free merge's read one past a part's end.
+// (V = elements per 16 bytes of the array: 16 / sizeof(K) for keys, 4 for values.)
+__host__ __device__ constexpr uint32_t bd_stage_elems(uint32_t P, uint32_t V) { return P + 32u * 3u * V + 64u; }
 
 __device__ __forceinline__ void cp_async_el(void* dst, const void* src, int bytes) {
   if (bytes == 8)
@@ -374,13 +388,16 @@ __device__ __forceinline__ void cp_async_el(void* dst, const void* src, int byte
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Warp 1: take the next dirty output block, read its tiles and resolve the
-// physical pieces of their inputs through T_in.
+// Warp 1: take the next dirty output block, read its tiles, resolve the
+// physical pieces of their inputs through T_in and lay the parts out in the
+// stage.  vec: every block base is 16-byte aligned (bulk copies allowed).
 template <int KT>
 __device__ __forceinline__ void bd_fill_hdr(const BdMem<KT>& M, BdState* st, const TileDesc* __restrict__ desc,
                                             uint32_t total, const uint32_t* __restrict__ dlist,
                                             const uint32_t* __restrict__ first_tile, uint32_t D,
-                                            const uint32_t* __restrict__ Tin, BdHdr& H) {
+                                            const uint32_t* __restrict__ Tin, bool vec, BdHdr& H) {
+  using K = typename KeyTraits<KT>::K;
+  constexpr uint32_t VK = 16u / (uint32_t)sizeof(K), VV = 4u;
   const uint32_t lane = threadIdx.x & 31u, P = M.P;
   uint32_t d = 0;
   if (lane == 0) d = atomicAdd(&st->ticket, 1u);
@@ -403,46 +420,121 @@ __device__ __forceinline__ void bd_fill_hdr(const BdMem<KT>& M, BdState* st, con
   }
   if (lane < nt) H.t[lane] = t;
   __syncwarp();
-  if (lane < 2 * nt) {  // part `lane`: its virtual range and its (at most two) physical pieces
+  // part `lane`: its virtual range, its (at most two) physical pieces, its regions
+  uint32_t gq = 0, len = 0;
+  if (lane < 2 * nt) {
     const TileDesc u = H.t[lane >> 1];
-    const uint32_t nA = u.a1 - u.a0, vbase = v << M.lg;
-    uint32_t gq, len, dst;
-    if (lane & 1) { gq = u.j + (u.lo - u.i) - u.a0; len = (u.hi - u.lo) - nA; dst = u.lo - vbase + nA; }
-    else { gq = u.i + u.a0; len = nA; dst = u.lo - vbase; }
+    const uint32_t nA = u.a1 - u.a0;
+    if (lane & 1) { gq = u.j + (u.lo - u.i) - u.a0; len = (u.hi - u.lo) - nA; }
+    else { gq = u.i + u.a0; len = nA; }
+  }
+  const uint32_t sk = gq & (VK - 1u), sv = gq & (VV - 1u);
+  // region sizes (multiples of the 16-byte unit) and their exclusive prefix
+  uint32_t rk = len ? ((sk + len + VK - 1u) / VK + 2u) * VK : 0u;
+  uint32_t rv = len ? ((sv + len + VV - 1u) / VV + 2u) * VV : 0u;
+  uint32_t ik = rk, iv = rv;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t yk = __shfl_up_sync(0xFFFFFFFFu, ik, o), yv = __shfl_up_sync(0xFFFFFFFFu, iv, o);
+    if ((int)lane >= o) { ik += yk; iv += yv; }
+  }
+  uint32_t slow = 0;
+  if (lane < 2 * nt) {
     H.part[lane][0] = gq;
     H.part[lane][1] = len;
-    const uint32_t off = gq & (P - 1), c = min(len, P - off);
-    H.pc[2 * lane][0] = len ? Tin[gq >> M.lg] : 0u;
-    H.pc[2 * lane][1] = off;
-    H.pc[2 * lane][2] = c;
-    H.pc[2 * lane][3] = dst;
-    const uint32_t rest = len - c;
-    H.pc[2 * lane + 1][0] = rest ? Tin[(gq + c) >> M.lg] : 0u;
-    H.pc[2 * lane + 1][1] = 0;
-    H.pc[2 * lane + 1][2] = rest;
-    H.pc[2 * lane + 1][3] = dst + c;
+    H.ko[lane] = ik - rk + sk;
+    H.vo[lane] = iv - rv + sv;
+    const uint32_t off = gq & (P - 1), c = min(len, P - off), rest = len - c;
+    const uint32_t b1 = len ? Tin[gq >> M.lg] : 0u, b2 = rest ? Tin[(gq + c) >> M.lg] : 0u;
+    // the caller's partial last block ends at n: no superset reads there
+    const bool bk1 = vec && !(M.has_partial && b1 == M.NB - 1);
+    const bool bk2 = vec && !(M.has_partial && b2 == M.NB - 1);
+    H.pcb[lane][0] = b1 | (bk1 ? 0u : BD_SLOW);
+    H.pcb[lane][1] = b2 | (bk2 ? 0u : BD_SLOW);
+    slow = (c && !bk1 ? 1u : 0u) + (rest && !bk2 ? 1u : 0u);
   }
-  if (lane == 0) { H.d = d; H.v = v; H.nt = nt; H.valid = 1; }
+  slow = __reduce_add_sync(0xFFFFFFFFu, slow);
+  if (lane == 0) { H.d = d; H.v = v; H.nt = nt; H.nslow = slow; H.valid = 1; }
 }
 
-// All threads: start the asynchronous gather of a block's inputs into a stage.
+// Warp 0: start the gather of a block's inputs into a stage.  Lane x issues
+// part x's bulk copies (keys, then values) after lane 0 has announced the
+// block's transaction bytes on `bar`; every thread then copies the pieces
+// that cannot go in bulk element by element (cp.async).
 template <int KT, bool HV>
 __device__ __forceinline__ void bd_issue(const BdMem<KT>& M, const BdHdr& H, typename KeyTraits<KT>::K* sk,
-                                         uint32_t* sv) {
+                                         uint32_t* sv, uint64_t* bar) {
   using K = typename KeyTraits<KT>::K;
-  const uint32_t npc = 4 * H.nt;
-  for (uint32_t x = 0; x < npc; ++x) {
-    const uint32_t c = H.pc[x][2];
-    if (!c) continue;
-    const uint32_t b = H.pc[x][0], off = H.pc[x][1], dst = H.pc[x][3];
-    const K* gk = M.kb(b) + off;
-    for (uint32_t q = threadIdx.x; q < c; q += BD_THREADS) cp_async_el(sk + dst + q, gk + q, (int)sizeof(K));
-    if (HV) {
-      const uint32_t* gv = M.vb(b) + off;
-      for (uint32_t q = threadIdx.x; q < c; q += BD_THREADS) cp_async_el(sv + dst + q, gv + q, 4);
+  constexpr uint32_t VK = 16u / (uint32_t)sizeof(K), VV = 4u;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, P = M.P;
+  const uint32_t np = 2 * H.nt;
+  if (tid < 32) {
+    uint32_t gq = 0, len = 0, c = 0, rest = 0, b1 = 0, b2 = 0, off = 0, sgk = 0, sgv = 0, bytes = 0;
+    if (lane < np) {
+      gq = H.part[lane][0];
+      len = H.part[lane][1];
+      off = gq & (P - 1);
+      c = min(len, P - off);
+      rest = len - c;
+      b1 = H.pcb[lane][0];
+      b2 = H.pcb[lane][1];
+      sgk = gq & (VK - 1u);
+      sgv = gq & (VV - 1u);
+      if (c && !(b1 & BD_SLOW))
+        bytes += ((sgk + c + VK - 1u) / VK) * 16u + (HV ? ((sgv + c + VV - 1u) / VV) * 16u : 0u);
+      if (rest && !(b2 & BD_SLOW))
+        bytes += ((rest + VK - 1u) / VK) * 16u + (HV ? ((rest + VV - 1u) / VV) * 16u : 0u);
+    }
+    const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, bytes);
+    if (lane == 0) {
+      fence_proxy_async_smem();  // this stage's earlier generic reads precede the bulk writes
+      mbar_arrive_expect_tx(bar, total);
+    }
+    __syncwarp();
+    if (bytes) {
+      const uint32_t ko = H.ko[lane], vo = H.vo[lane];
+      if (c && !(b1 & BD_SLOW)) {
+        bulk_g2s(sk + ko - sgk, M.kb(b1) + off - sgk, ((sgk + c + VK - 1u) / VK) * 16u, bar);
+        if (HV) bulk_g2s(sv + vo - sgv, M.vb(b1) + off - sgv, ((sgv + c + VV - 1u) / VV) * 16u, bar);
+      }
+      if (rest && !(b2 & BD_SLOW)) {
+        bulk_g2s(sk + ko + c, M.kb(b2), ((rest + VK - 1u) / VK) * 16u, bar);
+        if (HV) bulk_g2s(sv + vo + c, M.vb(b2), ((rest + VV - 1u) / VV) * 16u, bar);
+      }
     }
   }
-  cp_async_commit();
+  if (H.nslow) {  // element-wise pieces (unaligned arrays, the caller's partial last block)
+    for (uint32_t x = 0; x < np; ++x) {
+      const uint32_t gq = H.part[x][0], len = H.part[x][1], off = gq & (P - 1);
+      const uint32_t c = min(len, P - off), rest = len - c;
+      const uint32_t b1 = H.pcb[x][0], b2 = H.pcb[x][1];
+      if (c && (b1 & BD_SLOW)) {
+        const K* gk = M.kb(b1 & ~BD_SLOW) + off;
+        for (uint32_t q = tid; q < c; q += BD_THREADS) cp_async_el(sk + H.ko[x] + q, gk + q, (int)sizeof(K));
+        if (HV) {
+          const uint32_t* gv = M.vb(b1 & ~BD_SLOW) + off;
+          for (uint32_t q = tid; q < c; q += BD_THREADS) cp_async_el(sv + H.vo[x] + q, gv + q, 4);
+        }
+      }
+      if (rest && (b2 & BD_SLOW)) {
+        const K* gk = M.kb(b2 & ~BD_SLOW);
+        for (uint32_t q = tid; q < rest; q += BD_THREADS) cp_async_el(sk + H.ko[x] + c + q, gk + q, (int)sizeof(K));
+        if (HV) {
+          const uint32_t* gv = M.vb(b2 & ~BD_SLOW);
+          for (uint32_t q = tid; q < rest; q += BD_THREADS) cp_async_el(sv + H.vo[x] + c + q, gv + q, 4);
+        }
+      }
+    }
+    cp_async_commit();
+  }
+}
+
+// A stage has landed: its bulk copies (mbarrier phase) and, when the block
+// has element-wise pieces, this thread's cp.async groups (the caller then
+// synchronises the CTA before anyone reads them).
+__device__ __forceinline__ void bd_wait(const BdHdr& H, uint64_t* bar, uint32_t parity) {
+  mbar_wait(bar, parity);
+  if (H.nslow) cp_async_wait_all();
 }
 
 // Warp 0: release the input blocks a header's tiles consume.
@@ -455,11 +547,13 @@ __device__ __forceinline__ void bd_release_hdr(BdState* st, uint32_t* pool, uint
 
 // One level pass.  A CTA pipelines two dirty output blocks: while it merges
 // block t (inputs in stage t & 1) the inputs of block t+1 stream into the
-// other stage (cp.async) and warp 1 reads the tiles of block t+2.  Before
-// block t takes its output block, block t+1's inputs have landed and are
-// released, so whenever every CTA waits for a free block, every taken
-// block has released its inputs (no fewer free blocks than an in-order
-// round schedule would have).
+// other stage (bulk copies on mbarrier t+1 & 1) and warp 1 reads the tiles of
+// block t+2.  Before block t takes its output block, block t+1's inputs have
+// landed and are released, so whenever every CTA waits for a free block,
+// every taken block has released its inputs (no fewer free blocks than an
+// in-order round schedule would have).  The merged outputs stay in registers
+// and are stored straight into the output block (128-bit stores).  One CTA
+// barrier per block (two when the block has element-wise pieces).
 template <int KT, bool HV>
 __global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* st, const TileDesc* __restrict__ desc,
                                                           const uint32_t* __restrict__ info,
@@ -472,111 +566,147 @@ __global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* s
   using T = KeyTraits<KT>;
   using K = typename T::K;
   constexpr uint32_t OPT = MERGE_K;  // outputs per thread (P <= BD_THREADS * MERGE_K)
-  extern __shared__ __align__(16) unsigned char bd_smem[];
+  constexpr uint32_t VK = 16u / (uint32_t)sizeof(K);
+  extern __shared__ __align__(128) unsigned char bd_smem[];
   const uint32_t P = M.P;
+  const uint32_t SEK = bd_stage_elems(P, VK), SEV = bd_stage_elems(P, 4u);
   K* const stk0 = reinterpret_cast<K*>(bd_smem);
-  uint32_t* const stv0 = reinterpret_cast<uint32_t*>(stk0 + 2 * P);
-  auto stk = [&](uint32_t s) { return stk0 + s * P; };
-  auto stv = [&](uint32_t s) { return stv0 + (HV ? s * P : 0u); };
+  uint32_t* const stv0 = reinterpret_cast<uint32_t*>(stk0 + 2 * SEK);
+  auto stk = [&](uint32_t s) { return stk0 + s * SEK; };
+  auto stv = [&](uint32_t s) { return stv0 + (HV ? s * SEV : 0u); };
   __shared__ BdHdr hdr[3];
-  __shared__ uint32_t s_b;
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ uint32_t s_b[2];
   const uint32_t D = *D_ptr, total = info[3];
   const uint32_t tid = threadIdx.x, warp = tid >> 5;
   const bool vec = ((reinterpret_cast<uintptr_t>(M.k0) | reinterpret_cast<uintptr_t>(M.v0) |
                      reinterpret_cast<uintptr_t>(M.ks) | reinterpret_cast<uintptr_t>(M.vs)) & 15u) == 0;
   if (blockIdx.x == 0 && tid == 0 && D) atomicAdd(&st->rounds, 1u);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
   // prologue: block t = first ticket, gathered and released; header of t+1
-  if (warp == 1) bd_fill_hdr<KT>(M, st, desc, total, dlist, first_tile, D, Tin, hdr[0]);
+  if (warp == 1) bd_fill_hdr<KT>(M, st, desc, total, dlist, first_tile, D, Tin, vec, hdr[0]);
   __syncthreads();
   if (!hdr[0].valid) return;
-  bd_issue<KT, HV>(M, hdr[0], stk(0), stv(0));
-  if (warp == 1) bd_fill_hdr<KT>(M, st, desc, total, dlist, first_tile, D, Tin, hdr[1]);
-  cp_async_wait_all();
+  bd_issue<KT, HV>(M, hdr[0], stk(0), stv(0), &bar[0]);
+  if (warp == 1) bd_fill_hdr<KT>(M, st, desc, total, dlist, first_tile, D, Tin, vec, hdr[1]);
+  bd_wait(hdr[0], &bar[0], 0u);
   __syncthreads();
   if (warp == 0) bd_release_hdr(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, hdr[0]);
-  __syncthreads();
   for (uint32_t it = 0;; ++it) {
     const uint32_t s = it & 1u;
     const BdHdr& H0 = hdr[it % 3];
     BdHdr& H1 = hdr[(it + 1) % 3];
     BdHdr& H2 = hdr[(it + 2) % 3];
     const bool more = H1.valid;
-    if (more) bd_issue<KT, HV>(M, H1, stk(s ^ 1u), stv(s ^ 1u));
+    if (more) bd_issue<KT, HV>(M, H1, stk(s ^ 1u), stv(s ^ 1u), &bar[s ^ 1u]);
     if (warp == 1) {
-      if (more) bd_fill_hdr<KT>(M, st, desc, total, dlist, first_tile, D, Tin, H2);
+      if (more) bd_fill_hdr<KT>(M, st, desc, total, dlist, first_tile, D, Tin, vec, H2);
       else if ((tid & 31u) == 0) H2.valid = 0;
     }
     // merge block t into registers: this thread's outputs [OPT tid, OPT tid + OPT)
-    const uint32_t v = H0.v, vbase = v << M.lg, len = M.vlen(v);
+    const uint32_t v = H0.v, vbase = v << M.lg, len = M.vlen(v), nt = H0.nt;
     const uint32_t c0 = tid * OPT, c1 = min(c0 + OPT, len);
-    K* const sk = stk(s);
-    uint32_t* const sv = stv(s);
+    const K* const sk = stk(s);
+    const uint32_t* const sv = stv(s);
     K rk[OPT];
     uint32_t rv[OPT];
-    for (uint32_t x = 0; x < H0.nt; ++x) {
-      const TileDesc t = H0.t[x];
-      const uint32_t o = t.lo - vbase, cnt = t.hi - t.lo, nA = t.a1 - t.a0, nB = cnt - nA;
-      if (o >= c1 || o + cnt <= c0) continue;
-      const uint32_t s0 = max(c0, o) - o;
-      const K* A = sk + o;
-      const K* B = A + nA;
-      uint32_t ia = corank<KT>(A, nA, B, nB, s0), ib = s0 - ia;
+    if (nt == 1 && H0.t[0].lo == vbase && H0.t[0].hi == vbase + len && c1 == c0 + OPT) {
+      // the block is one merge tile and the chunk is full: branch-free merge
+      // over absolute stage indices (a read one past a part stays in its slack)
+      const TileDesc t = H0.t[0];
+      const uint32_t nA = t.a1 - t.a0, nB = len - nA;
+      const uint32_t koA = H0.ko[0], koB = H0.ko[1];
+      const int32_t dA = (int32_t)H0.vo[0] - (int32_t)koA, dB = (int32_t)H0.vo[1] - (int32_t)koB;
+      const uint32_t l = corank<KT>(sk + koA, nA, sk + koB, nB, c0);
+      uint32_t ia = koA + l, ib = koB + c0 - l;
+      const uint32_t ea = koA + nA, eb = koB + nB;
+      K ka = sk[ia], kb = sk[ib];
+      typename T::O oa = T::ord(ka), ob = T::ord(kb);
+      uint32_t ri[OPT];
 #pragma unroll
       for (uint32_t r = 0; r < OPT; ++r) {
-        const uint32_t pos = c0 + r;
-        if (pos >= o && pos < o + cnt && pos < c1) {
-          const bool takeA = ib >= nB || (ia < nA && T::ord(A[ia]) <= T::ord(B[ib]));
-          const uint32_t sidx = takeA ? ia : nA + ib;
-          rk[r] = A[sidx];
-          if (HV) rv[r] = sv[o + sidx];
-          ia += takeA ? 1u : 0u;
-          ib += takeA ? 0u : 1u;
+        const bool pa = ib >= eb || (ia < ea && oa <= ob);
+        rk[r] = pa ? ka : kb;
+        ri[r] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
+        ia += pa ? 1u : 0u;
+        ib += pa ? 0u : 1u;
+        const K nx = sk[pa ? ia : ib];
+        const typename T::O onx = T::ord(nx);
+        ka = pa ? nx : ka;
+        oa = pa ? onx : oa;
+        kb = pa ? kb : nx;
+        ob = pa ? ob : onx;
+      }
+      if (HV) {
+#pragma unroll
+        for (uint32_t r = 0; r < OPT; ++r) rv[r] = sv[ri[r]];
+      }
+    } else {
+      for (uint32_t x = 0; x < nt; ++x) {
+        const TileDesc t = H0.t[x];
+        const uint32_t o = t.lo - vbase, cnt = t.hi - t.lo, nA = t.a1 - t.a0, nB = cnt - nA;
+        if (o >= c1 || o + cnt <= c0) continue;
+        const uint32_t s0 = max(c0, o) - o;
+        const K* A = sk + H0.ko[2 * x];
+        const K* B = sk + H0.ko[2 * x + 1];
+        const uint32_t* VA = sv + H0.vo[2 * x];
+        const uint32_t* VB = sv + H0.vo[2 * x + 1];
+        uint32_t ia = corank<KT>(A, nA, B, nB, s0), ib = s0 - ia;
+#pragma unroll
+        for (uint32_t r = 0; r < OPT; ++r) {
+          const uint32_t pos = c0 + r;
+          if (pos >= o && pos < o + cnt && pos < c1) {
+            const bool takeA = ib >= nB || (ia < nA && T::ord(A[ia]) <= T::ord(B[ib]));
+            rk[r] = takeA ? A[ia] : B[ib];
+            if (HV) rv[r] = takeA ? VA[ia] : VB[ib];
+            ia += takeA ? 1u : 0u;
+            ib += takeA ? 0u : 1u;
+          }
         }
       }
     }
-    __syncthreads();  // every input of block t has been read
-#pragma unroll
-    for (uint32_t r = 0; r < OPT; ++r) {
-      if (c0 + r < c1) {
-        sk[c0 + r] = rk[r];
-        if (HV) sv[c0 + r] = rv[r];
-      }
+    if (more) {
+      bd_wait(H1, &bar[s ^ 1u], ((it + 1) >> 1) & 1u);  // block t+1's inputs have landed
+      if (H1.nslow) __syncthreads();                    // (element-wise pieces: every thread's)
     }
-    cp_async_wait_all();  // block t+1's inputs have landed
-    __syncthreads();
     if (warp == 0) {
       if (more) bd_release_hdr(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, H1);
       __syncwarp();
       if (tid == 0) {
         const uint32_t b = bd_alloc(st, pool, cap);
-        s_b = b;
+        s_b[s] = b;
         if (b != BD_NONE) Tout[v] = b;
       }
     }
-    __syncthreads();
-    const uint32_t b = s_b;
+    __syncthreads();  // stage s and header t are no longer read; the output block is known
+    const uint32_t b = s_b[s];
     if (b == BD_NONE) break;
     K* dk = M.kb(b);
-    constexpr uint32_t KV = 16 / sizeof(K);
-    const uint32_t nv = vec ? len / KV : 0u;
-    for (uint32_t q = tid; q < nv; q += BD_THREADS)
-      reinterpret_cast<uint4*>(dk)[q] = reinterpret_cast<const uint4*>(sk)[q];
-    for (uint32_t q = nv * KV + tid; q < len; q += BD_THREADS) dk[q] = sk[q];
-    if (HV) {
-      uint32_t* dv = M.vb(b);
-      const uint32_t nv4 = vec ? len / 4 : 0u;
-      for (uint32_t q = tid; q < nv4; q += BD_THREADS)
-        reinterpret_cast<uint4*>(dv)[q] = reinterpret_cast<const uint4*>(sv)[q];
-      for (uint32_t q = nv4 * 4 + tid; q < len; q += BD_THREADS) dv[q] = sv[q];
+    uint32_t* dv = HV ? M.vb(b) : nullptr;
+    if (vec && c1 == c0 + OPT) {
+      store_vec8<K>(dk + c0, rk);
+      if (HV) store_vec8<uint32_t>(dv + c0, rv);
+    } else {
+#pragma unroll
+      for (uint32_t r = 0; r < OPT; ++r)
+        if (c0 + r < c1) {
+          dk[c0 + r] = rk[r];
+          if (HV) dv[c0 + r] = rv[r];
+        }
     }
-    __syncthreads();  // stage s is free for block t+2; header slot t is free
     if (!more) break;
   }
 }
 
 template <int KT, bool HV>
 constexpr size_t bd_level_smem(uint32_t P) {
-  return (size_t)2 * P * (sizeof(typename KeyTraits<KT>::K) + (HV ? 4 : 0));
+  return (size_t)2 * bd_stage_elems(P, 16u / (uint32_t)sizeof(typename KeyTraits<KT>::K)) *
+             sizeof(typename KeyTraits<KT>::K) +
+         (HV ? (size_t)2 * bd_stage_elems(P, 4u) * 4 : 0);
 }
 
 // The ring's free blocks into pool[0, count) for the Copy (one CTA).
