@@ -818,8 +818,9 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
     double t0 = bd_now(s);
     if (w.gt_ctx) {  // a cell of the dyadic-cell mode: the whole array's table, no Copy
       const BdCtx& C = *(const BdCtx*)w.gt_ctx;
+      // no host synchronisation per cell: errors stay in the shared state
+      // (every level kernel stops on them) and the caller checks it once
       rc = bd_levels<KT, HV>(C, w, w.gt_base, p_hi, p_lo, w.fuse_z, s);
-      if (rc == VMPS_OK) rc = bd_check(C, s, "mode");
       bd_add(1, t0, s);
       if (rc != VMPS_OK) return rc;
       return bounded_stats<HV>(w, st, s);
@@ -1103,7 +1104,7 @@ static CellLayout bd_cell_layout(uint64_t n, int kt, int hv, int64_t scratch) {
   const uint64_t rdet = L.det / std::max<uint32_t>(c0.minrun, 1) + 4;
   // a cell's sort: its runs (<= cell / minrun + 2); the block table is the whole array's
   L.rcell = (uint32_t)(((n >> bd_cell_level(n)) + 1) / std::max<uint32_t>(c0.minrun, 1) + 4);
-  L.ring = L.rcell + rdet + 16;  // unconsumed runs: an open cell's and one detection chunk's
+  L.ring = L.rcell + 2 * rdet + 16;  // unconsumed runs: an open cell's and two detection chunks'
   L.det_out = align_up(rdet * 8) + align_up(rdet + 16) + align_up((size_t)3 * 64 * 8) + align_up(64) +
               align_up(L.ring * 8) + align_up(L.ring);
   Cfg cs = make_cfg(n, kt, hv, scratch);
@@ -1129,6 +1130,43 @@ vmps_status_t vmps_workspace_bytes(uint64_t n, vmps_key_t kt, int has_vals, int6
 }
 
 }  // extern "C"
+
+static vmps_status_t shard_runs_impl(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun,
+                                     uint32_t n_end, const void* d_prev, const void* d_halo, uint32_t n_halo,
+                                     uint32_t entry_state, uint64_t count, uint64_t offset, uint64_t* d_run_start,
+                                     uint8_t* d_run_kind, void* ws, size_t ws_bytes, void* stream, bool front_done);
+
+// Pinned host staging of the dyadic-cell mode's detection (per host thread,
+// grown on demand): the chain table and one chunk's run starts / kinds.
+struct DetHost {
+  uint64_t* tab = nullptr;
+  uint64_t* rs = nullptr;
+  uint8_t* rk = nullptr;
+  size_t ntab = 0, nrs = 0;
+  ~DetHost() {
+    if (tab) cudaFreeHost(tab);
+    if (rs) cudaFreeHost(rs);
+    if (rk) cudaFreeHost(rk);
+  }
+  bool reserve(size_t nt, size_t nr) {
+    if (nt > ntab) {
+      if (tab) cudaFreeHost(tab);
+      tab = nullptr;
+      if (cudaMallocHost(&tab, nt * 8) != cudaSuccess) { ntab = 0; return false; }
+      ntab = nt;
+    }
+    if (nr > nrs) {
+      if (rs) cudaFreeHost(rs);
+      if (rk) cudaFreeHost(rk);
+      rs = nullptr;
+      rk = nullptr;
+      if (cudaMallocHost(&rs, nr * 8) != cudaSuccess || cudaMallocHost(&rk, nr) != cudaSuccess) { nrs = 0; return false; }
+      nrs = nr;
+    }
+    return true;
+  }
+};
+static thread_local DetHost g_det_host;
 
 template <int KT, bool HV>
 static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, int64_t S, char* base,
@@ -1190,18 +1228,10 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
     Work w;
     if (carve(cc, nullptr, nullptr) > L.sort_ws) { g_err = "internal: top merge workspace"; return VMPS_ERR_INTERNAL; }
     carve(cc, &w, sort_ws);
-    const uint32_t hrs[3] = {0, (uint32_t)(x.b - x.a), (uint32_t)len};
-    const uint32_t hseg[4] = {0, 0, 0, 2};  // seg_l[1] = 0, seg_r[1] = 2
-    uint32_t hsc[SC_COUNT] = {};
-    hsc[SC_RUNS] = 2;
-    const uint8_t hpw[2] = {0, 1};
-    VMPS_CK(cudaMemcpyAsync(w.run_start, hrs, sizeof(hrs), cudaMemcpyHostToDevice, s));
-    VMPS_CK(cudaMemcpyAsync(w.seg_l, hseg, 8, cudaMemcpyHostToDevice, s));
-    VMPS_CK(cudaMemcpyAsync(w.seg_r, hseg + 2, 8, cudaMemcpyHostToDevice, s));
-    VMPS_CK(cudaMemcpyAsync(w.power, hpw, 2, cudaMemcpyHostToDevice, s));
-    VMPS_CK(cudaMemcpyAsync(w.scalars, hsc, sizeof(hsc), cudaMemcpyHostToDevice, s));
+    // two runs [0, x.b - x.a) [x.b - x.a, len), one node of power 1 (no host copy, no sync)
+    LAUNCH(k_bd_top_setup, 1, 64, 0, s, w.run_start, w.seg_l, w.seg_r, w.power, w.scalars,
+           (uint32_t)(x.b - x.a), (uint32_t)len);
     vmps_status_t r2 = bd_levels<KT, HV>(C, w, x.a, 1, 1, 0u, s);
-    VMPS_CK(cudaStreamSynchronize(s));  // the host arrays above are the stack's
     bd_add(6, t0, s);
     return r2;
   };
@@ -1277,59 +1307,9 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
     }
     return push_cell(nx);
   };
-  // scan: detection chunk by chunk, cells processed as soon as they close
-  uint32_t state = 0;  // START(0)
-  if (bd_trace()) memset(&g_bdt, 0, sizeof(g_bdt));
-  const double t_all = bd_now(s);
-  for (uint64_t off = 0; off < n; off += L.det) {
-    const double t_det = bd_now(s);
-    const uint64_t nd = std::min<uint64_t>(L.det, n - off);
-    const uint64_t after = n - off - nd;
-    const uint32_t n_halo = (uint32_t)std::min<uint64_t>(H, after);
-    const uint64_t rem = n - off;
-    const uint32_t n_end = rem >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)rem;
-    const K* kk = (const K*)((const char*)keys + off * kb);
-    // the chunk is read in place: its first block may have been rewritten
-    // through the table by the cells before it
-    const double th = bd_now(s);
-    rc = bd_home<KT, HV>(C, (uint32_t)(off / c0.P), d_slot, s);
-    bd_add(0, th, s);
-    if (rc != VMPS_OK) return rc;
-    rc = vmps_shard_chain(kk, nd, (vmps_key_t)KT, minrun, n_end, off ? d_prev : nullptr,
-                          n_halo ? (const void*)(kk + nd) : nullptr, n_halo, d_tab, det_ws, L.det_ws, s);
-    if (rc != VMPS_OK) return rc;
-    VMPS_CK(cudaMemcpyAsync(tab.data(), d_tab, (size_t)ns * 8, cudaMemcpyDeviceToHost, s));
-    VMPS_CK(cudaStreamSynchronize(s));
-    const uint64_t v = tab[state];
-    const uint32_t cnt = (uint32_t)(v & 0xFFFFFFFFull);
-    if (cnt) {
-      rc = vmps_shard_runs(kk, nd, (vmps_key_t)KT, minrun, n_end, off ? d_prev : nullptr,
-                           n_halo ? (const void*)(kk + nd) : nullptr, n_halo, state, cnt, off, d_rs, d_rk, det_ws,
-                           L.det_ws, s);
-      if (rc != VMPS_OK) return rc;
-      const size_t o = R.size();
-      R.resize(o + cnt);
-      RK.resize(o + cnt);
-      VMPS_CK(cudaMemcpyAsync(R.data() + o, d_rs, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s));
-      VMPS_CK(cudaMemcpyAsync(RK.data() + o, d_rk, cnt, cudaMemcpyDeviceToHost, s));
-      // and into the device ring the cells read their runs from
-      if (R.size() - R0 > L.ring) { g_err = "internal: run ring"; return VMPS_ERR_INTERNAL; }
-      const uint64_t at = g_total % L.ring, n1 = std::min<uint64_t>(cnt, L.ring - at);
-      VMPS_CK(cudaMemcpyAsync(d_ring + at, d_rs, n1 * 8, cudaMemcpyDeviceToDevice, s));
-      VMPS_CK(cudaMemcpyAsync(d_ring_kind + at, d_rk, n1, cudaMemcpyDeviceToDevice, s));
-      if (n1 < cnt) {
-        VMPS_CK(cudaMemcpyAsync(d_ring, d_rs + n1, (cnt - n1) * 8, cudaMemcpyDeviceToDevice, s));
-        VMPS_CK(cudaMemcpyAsync(d_ring_kind, d_rk + n1, cnt - n1, cudaMemcpyDeviceToDevice, s));
-      }
-      g_total += cnt;
-    }
-    state = (uint32_t)(v >> 32);
-    // the original last key of this chunk (the next chunk's descent bit at its start)
-    VMPS_CK(cudaMemcpyAsync(d_prev, kk + nd - 1, kb, cudaMemcpyDeviceToDevice, s));
-    VMPS_CK(cudaStreamSynchronize(s));
-    bd_add(4, t_det, s);
-    // close every cell whose last run's end is known: runs R[R0, R0+m) share
-    // a cell and run R0+m (whose start is the end of run R0+m-1) lies in a later one
+  // Close every cell whose last run's end is known: runs R[R0, R0+m) share a
+  // cell and run R0+m (whose start is the end of run R0+m-1) lies in a later one.
+  auto close_cells = [&]() -> vmps_status_t {
     for (;;) {
       const double tc = bd_now(s);
       const size_t avail = R.size() - R0;
@@ -1340,10 +1320,113 @@ static vmps_status_t sort_bounded_cells(void* keys, uint32_t* vals, uint64_t n, 
       while (m + 1 < avail && Rr[m] + Rr[m + 1] < T) ++m;
       if (m + 1 >= avail) break;  // run m's end unknown or run m still in the cell
       bd_add(8, tc, s);
-      rc = do_cell(m, Rr[m]);
+      vmps_status_t r2 = do_cell(m, Rr[m]);
+      if (r2 != VMPS_OK) return r2;
+    }
+    return VMPS_OK;
+  };
+  // Scan: detection chunk by chunk on a second stream, one chunk ahead of the
+  // cells.  While the cells closed by the runs of chunks < i run on s, the
+  // runs of chunk i and the chain table of chunk i+1 are computed on sd.  No
+  // cell reaches chunk i: a closed cell ends at a known run start (< the start
+  // of chunk i, a block boundary), so chunk i's blocks, its halo and its last
+  // key are still the caller's originals when sd reads them.  The ring copy of
+  // chunk i's runs waits for the cells issued one iteration earlier (the ring
+  // holds an open cell's runs and two chunks').
+  if (!g_det_host.reserve(ns, rdet)) { g_err = "cudaMallocHost (detection staging)"; return VMPS_ERR_CUDA; }
+  DetHost& hb = g_det_host;
+  struct StreamGuard {
+    cudaStream_t sd = nullptr;
+    cudaEvent_t ev = nullptr;
+    ~StreamGuard() {
+      if (sd) { cudaStreamSynchronize(sd); cudaStreamDestroy(sd); }
+      if (ev) cudaEventDestroy(ev);
+    }
+  } sg;
+  VMPS_CK(cudaStreamCreateWithFlags(&sg.sd, cudaStreamNonBlocking));
+  VMPS_CK(cudaEventCreateWithFlags(&sg.ev, cudaEventDisableTiming));
+  cudaStream_t sd = sg.sd;
+  uint32_t state = 0;  // START(0)
+  if (bd_trace()) memset(&g_bdt, 0, sizeof(g_bdt));
+  const double t_all = bd_now(s);
+  const uint64_t nchunks = (n + L.det - 1) / L.det;
+  struct ChunkArgs { uint64_t off, nd; uint32_t n_halo, n_end; const K* kk; };
+  auto chunk = [&](uint64_t i) -> ChunkArgs {
+    ChunkArgs c;
+    c.off = i * L.det;
+    c.nd = std::min<uint64_t>(L.det, n - c.off);
+    c.n_halo = (uint32_t)std::min<uint64_t>(H, n - c.off - c.nd);
+    const uint64_t rem = n - c.off;
+    c.n_end = rem >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)rem;
+    c.kk = (const K*)((const char*)keys + c.off * kb);
+    return c;
+  };
+  auto issue_chain = [&](uint64_t i) -> vmps_status_t {
+    const ChunkArgs c = chunk(i);
+    vmps_status_t r2 = vmps_shard_chain(c.kk, c.nd, (vmps_key_t)KT, minrun, c.n_end, c.off ? d_prev : nullptr,
+                                        c.n_halo ? (const void*)(c.kk + c.nd) : nullptr, c.n_halo, d_tab, det_ws,
+                                        L.det_ws, sd);
+    if (r2 != VMPS_OK) return r2;
+    VMPS_CK(cudaMemcpyAsync(hb.tab, d_tab, (size_t)ns * 8, cudaMemcpyDeviceToHost, sd));
+    return VMPS_OK;
+  };
+  rc = issue_chain(0);
+  if (rc != VMPS_OK) return rc;
+  uint32_t pending = 0;  // runs of the previous chunk staged in hb.rs / hb.rk
+  for (uint64_t i = 0; i < nchunks; ++i) {
+    const double t_det = bd_now(s);
+    VMPS_CK(cudaStreamSynchronize(sd));
+    if (pending) {  // runs of chunk i-1: to the host list (their ring copy is complete)
+      const size_t o = R.size();
+      R.insert(R.end(), hb.rs, hb.rs + pending);
+      RK.insert(RK.end(), hb.rk, hb.rk + pending);
+      (void)o;
+      pending = 0;
+    }
+    const ChunkArgs c = chunk(i);
+    const uint64_t v = hb.tab[state];
+    const uint32_t cnt = (uint32_t)(v & 0xFFFFFFFFull);
+    if (cnt) {
+      rc = shard_runs_impl(c.kk, c.nd, (vmps_key_t)KT, minrun, c.n_end, c.off ? d_prev : nullptr,
+                           c.n_halo ? (const void*)(c.kk + c.nd) : nullptr, c.n_halo, state, cnt, c.off, d_rs, d_rk,
+                           det_ws, L.det_ws, sd, true);
+      if (rc != VMPS_OK) return rc;
+      VMPS_CK(cudaMemcpyAsync(hb.rs, d_rs, (size_t)cnt * 8, cudaMemcpyDeviceToHost, sd));
+      VMPS_CK(cudaMemcpyAsync(hb.rk, d_rk, cnt, cudaMemcpyDeviceToHost, sd));
+    }
+    state = (uint32_t)(v >> 32);
+    // the original last key of this chunk (the next chunk's descent bit at its start)
+    VMPS_CK(cudaMemcpyAsync(d_prev, c.kk + c.nd - 1, kb, cudaMemcpyDeviceToDevice, sd));
+    if (i + 1 < nchunks) {
+      rc = issue_chain(i + 1);
       if (rc != VMPS_OK) return rc;
     }
+    if (cnt) {  // into the device ring the cells read their runs from
+      if (R.size() - R0 + cnt > L.ring) { g_err = "internal: run ring"; return VMPS_ERR_INTERNAL; }
+      VMPS_CK(cudaStreamWaitEvent(sd, sg.ev, 0));  // the cells of the previous iteration are done
+      const uint64_t at = g_total % L.ring, n1 = std::min<uint64_t>(cnt, L.ring - at);
+      VMPS_CK(cudaMemcpyAsync(d_ring + at, d_rs, n1 * 8, cudaMemcpyDeviceToDevice, sd));
+      VMPS_CK(cudaMemcpyAsync(d_ring_kind + at, d_rk, n1, cudaMemcpyDeviceToDevice, sd));
+      if (n1 < cnt) {
+        VMPS_CK(cudaMemcpyAsync(d_ring, d_rs + n1, (cnt - n1) * 8, cudaMemcpyDeviceToDevice, sd));
+        VMPS_CK(cudaMemcpyAsync(d_ring_kind, d_rk + n1, cnt - n1, cudaMemcpyDeviceToDevice, sd));
+      }
+      g_total += cnt;
+      pending = cnt;
+    }
+    bd_add(4, t_det, s);
+    rc = close_cells();
+    if (rc != VMPS_OK) return rc;
+    VMPS_CK(cudaEventRecord(sg.ev, s));  // the next ring copy waits for these cells
   }
+  VMPS_CK(cudaStreamSynchronize(sd));
+  if (pending) {
+    R.insert(R.end(), hb.rs, hb.rs + pending);
+    RK.insert(RK.end(), hb.rk, hb.rk + pending);
+    pending = 0;
+  }
+  rc = close_cells();
+  if (rc != VMPS_OK) return rc;
   // the array is done: remaining runs end at n
   while (R0 < R.size()) {
     const size_t avail = R.size() - R0;
@@ -1647,10 +1730,13 @@ vmps_status_t vmps_shard_chain(const void* keys, uint64_t n_local, vmps_key_t kt
   return launch_check();
 }
 
-vmps_status_t vmps_shard_runs(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun, uint32_t n_end,
-                              const void* d_prev, const void* d_halo, uint32_t n_halo, uint32_t entry_state,
-                              uint64_t count, uint64_t offset, uint64_t* d_run_start, uint8_t* d_run_kind, void* ws,
-                              size_t ws_bytes, void* stream) {
+}  // extern "C"
+// front_done: the workspace already holds this shard's tables (the previous
+// call on it was vmps_shard_chain with the same arguments, same stream)
+static vmps_status_t shard_runs_impl(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun,
+                                     uint32_t n_end, const void* d_prev, const void* d_halo, uint32_t n_halo,
+                                     uint32_t entry_state, uint64_t count, uint64_t offset, uint64_t* d_run_start,
+                                     uint8_t* d_run_kind, void* ws, size_t ws_bytes, void* stream, bool front_done) {
   Work w;
   vmps_status_t rc = shard_setup(keys, n_local, kt, minrun, n_end, n_halo, ws, ws_bytes, &w);
   if (rc != VMPS_OK) return rc;
@@ -1660,12 +1746,14 @@ vmps_status_t vmps_shard_runs(const void* keys, uint64_t n_local, vmps_key_t kt,
   }
   if (count > w.rmax || (count && (!d_run_start || !d_run_kind))) { g_err = "shard: bad run count"; return VMPS_ERR_INVALID_ARG; }
   cudaStream_t s = (cudaStream_t)stream;
-  switch (kt) {
-    case VMPS_KEY_U32: rc = shard_dispatch_front<VMPS_KEY_U32>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
-    case VMPS_KEY_U64: rc = shard_dispatch_front<VMPS_KEY_U64>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
-    default: rc = shard_dispatch_front<VMPS_KEY_F32>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
+  if (!front_done) {
+    switch (kt) {
+      case VMPS_KEY_U32: rc = shard_dispatch_front<VMPS_KEY_U32>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
+      case VMPS_KEY_U64: rc = shard_dispatch_front<VMPS_KEY_U64>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
+      default: rc = shard_dispatch_front<VMPS_KEY_F32>(w, keys, n_end, d_prev, d_halo, n_halo, s); break;
+    }
+    if (rc != VMPS_OK) return rc;
   }
-  if (rc != VMPS_OK) return rc;
   const int top = w.chain_levels;
   const size_t sm32 = (size_t)CHAIN_G * w.ns * 4, sm64 = (size_t)CHAIN_G * w.ns * 8;
   if (top == 0)
@@ -1688,6 +1776,14 @@ vmps_status_t vmps_shard_runs(const void* keys, uint64_t n_local, vmps_key_t kt,
     VMPS_CK(cudaMemcpyAsync(d_run_kind, w.run_kind, count, cudaMemcpyDeviceToDevice, s));
   }
   return launch_check();
+}
+extern "C" {
+vmps_status_t vmps_shard_runs(const void* keys, uint64_t n_local, vmps_key_t kt, uint32_t minrun, uint32_t n_end,
+                              const void* d_prev, const void* d_halo, uint32_t n_halo, uint32_t entry_state,
+                              uint64_t count, uint64_t offset, uint64_t* d_run_start, uint8_t* d_run_kind, void* ws,
+                              size_t ws_bytes, void* stream) {
+  return shard_runs_impl(keys, n_local, kt, minrun, n_end, d_prev, d_halo, n_halo, entry_state, count, offset,
+                         d_run_start, d_run_kind, ws, ws_bytes, stream, false);
 }
 
 // The merge plan of an array given its run starts (64-bit positions, r + 1

@@ -289,6 +289,19 @@ __global__ void k_bd_dirty_list(BdMem<KT> M, const TileDesc* __restrict__ desc, 
   }
 }
 
+// A top merge of the dyadic-cell mode as a two-run plan: runs [0, nx) and
+// [nx, len), one node (t = 1) of power 1 covering both.
+__global__ void k_bd_top_setup(uint32_t* __restrict__ rs, uint32_t* __restrict__ seg_l, uint32_t* __restrict__ seg_r,
+                               uint8_t* __restrict__ power, uint32_t* __restrict__ scalars, uint32_t nx, uint32_t len) {
+  if (threadIdx.x == 0) {
+    rs[0] = 0; rs[1] = nx; rs[2] = len;
+    seg_l[0] = 0; seg_l[1] = 0;
+    seg_r[0] = 0; seg_r[1] = 2;
+    power[0] = 0; power[1] = 1;
+  }
+  for (uint32_t i = threadIdx.x; i < SC_COUNT; i += blockDim.x) scalars[i] = i == SC_RUNS ? 2u : 0u;
+}
+
 // Run starts of a sub-array made absolute (the shared block table's positions).
 __global__ void k_rs_add_base(uint32_t* __restrict__ rs, const uint32_t* scalars, uint32_t base) {
   const uint32_t r = scalars[SC_RUNS];
