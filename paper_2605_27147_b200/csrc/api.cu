@@ -557,7 +557,8 @@ static BdMem<KT> bd_mem(const BdCtx& C) {
 }
 
 static vmps_status_t bd_init(const BdCtx& C, cudaStream_t s) {
-  LAUNCH(k_bd_init, grid_for(C.cap()), 256, 0, s, (BdState*)C.bstate, C.pool, C.cap(), C.Tin, C.inv, C.NB, C.F);
+  LAUNCH(k_bd_init, grid_for(C.cap()), 256, 0, s, (BdState*)C.bstate, C.pool, C.cap(), C.Tin, C.inv, C.NB, C.F,
+         C.dirty);
   return VMPS_OK;
 }
 
@@ -615,17 +616,22 @@ static vmps_status_t bd_levels(const BdCtx& C, const Work& w, uint64_t base, int
          w.rmax, w.bcnt);
   scan_u32(w.bcnt, w.btoff, w.rmax + 1, w.scan_tmp, s);
   for (int p = p_hi; p >= p_lo; --p) {
-    LAUNCH(k_bd_level_info, 1, 32, 0, s, w.lvl_hscan, nlt, w.btoff, p, w.bm);
-    LAUNCH(k_bd_tile_desc<KT>, gfix, 256, 0, s, M, C.Tin, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.bm, w.btoff,
-           C.bdesc_cap, st, desc);
-    VMPS_CK(cudaMemsetAsync(C.dirty, 0, (size_t)(nbr + 1) * 4, s));
-    LAUNCH(k_bd_mark<KT>, gfix, 256, 0, s, M, C.Tin, desc, w.bm, C.P, vb0, C.dirty);
-    scan_u32(C.dirty, C.didx, nbr + 1, w.scan_tmp, s);
-    LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, gfix), 256, 0, s, M, desc, w.bm, C.dirty, C.didx, vb0, nbr, C.dlist,
-           C.first_tile, C.remain, w.bD);
+    // tile descriptors + dirty flags (the level's slice of the schedule read
+    // on the device), dirty list, level pass, commit: 4 launches per pass on
+    // block ranges up to BD_SMALL_MAX, the scan launches above that
+    LAUNCH(k_bd_tile_desc<KT>, gfix, 256, 0, s, M, C.Tin, w.run_start, w.seg_l, w.seg_r, w.blnodes, w.lvl_hscan, nlt,
+           p, w.btoff, C.bdesc_cap, st, desc, w.bm, vb0, C.dirty);
+    if (nbr <= BD_SMALL_MAX) {
+      LAUNCH((k_bd_dirty_small<KT>), 1, BD_SMALL_THREADS, 0, s, M, desc, w.bm, C.dirty, C.didx, vb0, nbr, C.dlist,
+             C.first_tile, C.remain, w.bD);
+    } else {
+      scan_u32(C.dirty, C.didx, nbr + 1, w.scan_tmp, s);
+      LAUNCH((k_bd_dirty_list<KT>), std::max(gNB, gfix), 256, 0, s, M, desc, w.bm, C.dirty, C.didx, vb0, nbr,
+             C.dlist, C.first_tile, C.remain, w.bD);
+    }
     LAUNCH((k_bd_level<KT, HV>), glv, BD_THREADS, lsm, s, M, st, desc, w.bm, C.dlist, C.first_tile, w.bD, C.Tin,
            C.Tout, C.pool, C.cap(), C.remain);
-    LAUNCH(k_bd_commit, gNB, 256, 0, s, st, C.dlist, w.bD, C.Tout, C.Tin, C.inv);
+    LAUNCH(k_bd_commit, gNB, 256, 0, s, st, C.dlist, w.bD, C.Tout, C.Tin, C.inv, C.dirty, vb0);
   }
   return VMPS_OK;
 }

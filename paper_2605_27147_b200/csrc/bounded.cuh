@@ -123,16 +123,6 @@ __device__ __forceinline__ void bd_level_of(const uint32_t* hscan, uint32_t ntil
   *le = hscan[(lo + 1) * ntiles];
 }
 
-__global__ void k_bd_level_info(const uint32_t* __restrict__ hscan, uint32_t ntiles,
-                                const uint32_t* __restrict__ toff, int p, uint32_t* __restrict__ info) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const uint32_t ls = hscan[(uint32_t)p * ntiles], le = hscan[(uint32_t)(p + 1) * ntiles];
-  info[0] = ls;
-  info[1] = le - ls;
-  info[2] = toff[ls];
-  info[3] = toff[le] - toff[ls];
-}
-
 __device__ __forceinline__ void bd_node_geom(const uint32_t* rs, const uint32_t* seg_l, const uint32_t* seg_r,
                                              const uint32_t* lnodes, uint32_t m, uint32_t x, uint32_t P,
                                              uint32_t n, uint32_t* i, uint32_t* j, uint32_t* k,
@@ -186,17 +176,33 @@ __device__ uint32_t bd_corank(const BdMem<KT>& M, const uint32_t* Tin, uint32_t 
   return lo;
 }
 
-// Tile descriptors of the level in output order (one thread per tile).
+// Tile descriptors of the level in output order (one thread per tile), and
+// the dirty output blocks.  A merge tile is an identity when every element it
+// outputs already sits at its output position: the whole node is a
+// concatenation (A's last <= B's first), or the tile takes only A elements
+// with no B element before it, or only B elements after all of A (the page
+// hand-over of P:514-515 in its in-place form).  A block is dirty iff a
+// non-identity merge tile writes into it; a clean block keeps its physical
+// home and its tiles are skipped: zero bytes moved.  (An element that leaves
+// a block makes that block's own output differ there, so dirty blocks only
+// ever consume inputs from dirty blocks.)  The level's slice of the schedule
+// (info: first node, nodes, first tile, tiles) is read here and published
+// for the later kernels of the pass.
 template <int KT>
 __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_t* __restrict__ Tin,
                                                       const uint32_t* __restrict__ rs,
                                                       const uint32_t* __restrict__ seg_l,
                                                       const uint32_t* __restrict__ seg_r,
                                                       const uint32_t* __restrict__ lnodes_all,
-                                                      const uint32_t* __restrict__ info,
+                                                      const uint32_t* __restrict__ hscan, uint32_t nlt, int p,
                                                       const uint32_t* __restrict__ toff_all, uint32_t cap,
-                                                      BdState* st, TileDesc* __restrict__ desc) {
-  const uint32_t ls = info[0], m = info[1], T0 = info[2], total = info[3];
+                                                      BdState* st, TileDesc* __restrict__ desc,
+                                                      uint32_t* __restrict__ info, uint32_t vb0,
+                                                      uint32_t* __restrict__ dirty) {
+  using T = KeyTraits<KT>;
+  const uint32_t ls = hscan[(uint32_t)p * nlt], le = hscan[(uint32_t)(p + 1) * nlt];
+  const uint32_t m = le - ls, T0 = toff_all[ls], total = toff_all[le] - T0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { info[0] = ls; info[1] = m; info[2] = T0; info[3] = total; }
   const uint32_t* lnodes = lnodes_all + ls;
   const uint32_t* toff = toff_all + ls;
   if (total > cap) {  // capacity is sized from the plan; never expected
@@ -228,38 +234,70 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
     }
     const uint32_t g = i / P + loc;
     const uint32_t lo = max(i, g * P), hi = min(k, (g + 1) * P);
-    const uint32_t a0 = bd_corank<KT>(M, Tin, i, j - i, j, k - j, lo - i);
-    TileDesc* Dp = desc + tau;
-    Dp->i = i; Dp->j = j; Dp->k = k; Dp->lo = lo; Dp->hi = hi; Dp->a0 = a0; Dp->par = 0;
-    if (hi == k) Dp->a1 = j - i;
-    if (lo != i) desc[tau - 1].a1 = a0;
+    const uint32_t nA = j - i, nB = k - j;
+    const uint32_t a0 = lo == i ? 0u : bd_corank<KT>(M, Tin, i, nA, j, nB, lo - i);
+    const uint32_t a1 = hi == k ? nA : bd_corank<KT>(M, Tin, i, nA, j, nB, hi - i);
+    D.i = i; D.j = j; D.k = k; D.lo = lo; D.hi = hi; D.a0 = a0; D.a1 = a1;
+    desc[tau] = D;
+    const uint32_t nAt = a1 - a0, nBt = (hi - lo) - nAt, b0 = (lo - i) - a0;
+    bool ident = (nBt == 0 && b0 == 0) || (nAt == 0 && a0 == nA);
+    if (!ident && nA > 0 && nB > 0) ident = T::ord(bd_key<KT>(M, Tin, j - 1)) <= T::ord(bd_key<KT>(M, Tin, j));
+    if (!ident) dirty[lo / P - vb0] = 1u;
   }
 }
 
-// Dirty output blocks, their list and first tiles, and the per-block
-// counters of elements to consume.  A merge tile is an identity when every
-// element it outputs already sits at its output position: the whole node is
-// a concatenation (A's last <= B's first), or the tile takes only A elements
-// with no B element before it, or only B elements after all of A (the page
-// hand-over of P:514-515 in its in-place form).  A block is dirty iff a
-// non-identity merge tile writes into it; a clean block keeps its physical
-// home and its tiles are skipped: zero bytes moved.  (An element that leaves
-// a block makes that block's own output differ there, so dirty blocks only
-// ever consume inputs from dirty blocks.)
+// Small passes (a block range up to BD_SMALL_MAX): the scan of the dirty
+// flags, the dirty list, first tiles, consumption counters and count, by one
+// CTA of 1024 threads in place of the scan launches + k_bd_dirty_list.
+constexpr uint32_t BD_SMALL_THREADS = 1024;
+constexpr uint32_t BD_SMALL_MAX = 32768;
 template <int KT>
-__global__ void k_bd_mark(BdMem<KT> M, const uint32_t* __restrict__ Tin, TileDesc* __restrict__ desc,
-                          const uint32_t* __restrict__ info, uint32_t P, uint32_t vb0, uint32_t* __restrict__ dirty) {
-  using T = KeyTraits<KT>;
-  const uint32_t total = info[3];
-  for (uint32_t tau = blockIdx.x * blockDim.x + threadIdx.x; tau < total; tau += gridDim.x * blockDim.x) {
-    const TileDesc d = desc[tau];
-    if (d.par == 1) continue;  // gap tile
-    const uint32_t nA = d.j - d.i, nAt = d.a1 - d.a0, nBt = (d.hi - d.lo) - nAt;
-    const uint32_t b0 = (d.lo - d.i) - d.a0;
-    bool ident = (nBt == 0 && b0 == 0) || (nAt == 0 && d.a0 == nA);
-    if (!ident && nA > 0 && d.k > d.j)
-      ident = T::ord(bd_key<KT>(M, Tin, d.j - 1)) <= T::ord(bd_key<KT>(M, Tin, d.j));
-    if (!ident) dirty[d.lo / P - vb0] = 1u;
+__global__ void __launch_bounds__(BD_SMALL_THREADS) k_bd_dirty_small(
+    BdMem<KT> M, const TileDesc* __restrict__ desc, const uint32_t* __restrict__ info,
+    const uint32_t* __restrict__ dirty, uint32_t* __restrict__ didx, uint32_t vb0, uint32_t nbr,
+    uint32_t* __restrict__ dlist, uint32_t* __restrict__ first_tile, uint32_t* __restrict__ remain,
+    uint32_t* __restrict__ D_out) {
+  __shared__ uint32_t wsum[BD_SMALL_THREADS / 32];
+  __shared__ uint32_t s_carry[2];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if (tid == 0) s_carry[0] = 0;
+  __syncthreads();
+  uint32_t it = 0;
+  for (uint32_t base = 0; base < nbr; base += BD_SMALL_THREADS, ++it) {
+    const uint32_t x = base + tid;
+    const uint32_t f = x < nbr ? dirty[x] : 0u;
+    const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f != 0u);
+    if (lane == 0) wsum[warp] = (uint32_t)__popc(bal);
+    __syncthreads();
+    const uint32_t carry = s_carry[it & 1u];
+    if (warp == 0) {
+      const uint32_t w = wsum[lane];
+      uint32_t incl = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((int)lane >= o) incl += y;
+      }
+      wsum[lane] = incl - w;
+      if (lane == 31) s_carry[(it + 1u) & 1u] = carry + incl;
+    }
+    __syncthreads();
+    if (f) {
+      const uint32_t idx = carry + wsum[warp] + (uint32_t)__popc(bal & ((1u << lane) - 1u));
+      didx[x] = idx;
+      dlist[idx] = vb0 + x;
+      remain[vb0 + x] = M.vlen(vb0 + x);
+    }
+    __syncthreads();
+  }
+  const uint32_t total = info[3], P = M.P, D = s_carry[it & 1u];
+  for (uint32_t tau = tid; tau < total; tau += BD_SMALL_THREADS) {
+    const uint32_t x = desc[tau].lo / P - vb0;
+    if (dirty[x] && (tau == 0 || desc[tau - 1].lo / P - vb0 != x)) first_tile[didx[x]] = tau;
+  }
+  if (tid == 0) {
+    *D_out = D;
+    first_tile[D] = total;
   }
 }
 
@@ -320,32 +358,6 @@ __global__ void k_rs_add_base(uint32_t* __restrict__ rs, const uint32_t* scalars
 // published.  Inputs are released before the allocation, so a level needs no
 // more free blocks than the rounds of a block-synchronous schedule would.  A
 // CTA that waits ~1 s without a free block reports the budget as too small.
-__device__ __forceinline__ void bd_release(BdState* st, uint32_t* pool, uint32_t cap, uint32_t* remain,
-                                           const uint32_t* Tin, uint32_t NB, uint32_t has_partial, uint32_t v,
-                                           uint32_t cnt) {
-  if (!cnt) return;
-  const uint32_t old = atomicSub(&remain[v], cnt);
-  if (old == cnt) {
-    const uint32_t b = Tin[v];
-    if (has_partial && b == NB - 1) return;  // the partial last block is never freed
-    const uint32_t at = atomicAdd(&st->tail, 1u);
-    reinterpret_cast<volatile uint32_t*>(pool)[at % cap] = b;
-  }
-}
-
-// Consume [q, q+len) of virtual positions: decrement the touched blocks.
-__device__ __forceinline__ void bd_consume(BdState* st, uint32_t* pool, uint32_t cap, uint32_t* remain,
-                                           const uint32_t* Tin, uint32_t NB, uint32_t P, uint32_t has_partial,
-                                           uint32_t q, uint32_t len) {
-  while (len) {
-    const uint32_t v = q / P, off = q & (P - 1);
-    const uint32_t c = min(len, P - off);
-    bd_release(st, pool, cap, remain, Tin, NB, has_partial, v, c);
-    q += c;
-    len -= c;
-  }
-}
-
 __device__ __forceinline__ uint32_t bd_alloc(BdState* st, uint32_t* pool, uint32_t cap) {
   const uint32_t h = atomicAdd(&st->head, 1u);
   volatile uint32_t* slot = reinterpret_cast<volatile uint32_t*>(pool) + h % cap;
@@ -550,12 +562,42 @@ __device__ __forceinline__ void bd_wait(const BdHdr& H, uint64_t* bar, uint32_t 
   if (H.nslow) cp_async_wait_all();
 }
 
-// Warp 0: release the input blocks a header's tiles consume.
-__device__ __forceinline__ void bd_release_hdr(BdState* st, uint32_t* pool, uint32_t cap, uint32_t* remain,
-                                               const uint32_t* Tin, uint32_t NB, uint32_t P, uint32_t has_partial,
-                                               const BdHdr& H) {
+// Warp 0: release the input blocks a header's tiles consume (lane x: part x,
+// whose <= 2 pieces touch virtual blocks gq / P and gq / P + 1, physical
+// blocks from the header).  A block whose counter reaches zero is free; when
+// `keep` the first such block is returned to the caller (the CTA's own next
+// output block: no trip through the shared ring), the others go to the ring.
+// Returns BD_NONE when no block was kept.
+__device__ __forceinline__ uint32_t bd_release_hdr(BdState* st, uint32_t* pool, uint32_t cap, uint32_t* remain,
+                                                   uint32_t NB, uint32_t P, uint32_t lg, uint32_t has_partial,
+                                                   const BdHdr& H, bool keep) {
   const uint32_t lane = threadIdx.x & 31u;
-  if (lane < 2 * H.nt) bd_consume(st, pool, cap, remain, Tin, NB, P, has_partial, H.part[lane][0], H.part[lane][1]);
+  uint32_t f0 = BD_NONE, f1 = BD_NONE;
+  if (lane < 2 * H.nt) {
+    const uint32_t gq = H.part[lane][0], len = H.part[lane][1], off = gq & (P - 1);
+    const uint32_t c = min(len, P - off), rest = len - c;
+    auto rel = [&](uint32_t v, uint32_t phys, uint32_t cnt) -> uint32_t {
+      if (!cnt) return BD_NONE;
+      const uint32_t old = atomicSub(&remain[v], cnt);
+      if (old != cnt) return BD_NONE;
+      if (has_partial && phys == NB - 1) return BD_NONE;  // the partial last block is never freed
+      return phys;
+    };
+    f0 = rel(gq >> lg, H.pcb[lane][0] & ~BD_SLOW, c);
+    f1 = rel((gq >> lg) + 1u, H.pcb[lane][1] & ~BD_SLOW, rest);
+  }
+  const uint32_t m0 = __ballot_sync(0xFFFFFFFFu, f0 != BD_NONE), m1 = __ballot_sync(0xFFFFFFFFu, f1 != BD_NONE);
+  // the kept block: the lowest lane's f0, else the lowest lane's f1
+  const uint32_t kl = keep ? (m0 ? (uint32_t)__ffs(m0) - 1u : m1 ? (uint32_t)__ffs(m1) - 1u : 32u) : 32u;
+  const bool kf0 = m0 != 0u;
+  const uint32_t kept = kl < 32u ? __shfl_sync(0xFFFFFFFFu, kf0 ? f0 : f1, kl) : BD_NONE;
+  auto push = [&](uint32_t b) {
+    const uint32_t at = atomicAdd(&st->tail, 1u);
+    reinterpret_cast<volatile uint32_t*>(pool)[at % cap] = b;
+  };
+  if (f0 != BD_NONE && !(lane == kl && kf0)) push(f0);
+  if (f1 != BD_NONE && !(lane == kl && !kf0)) push(f1);
+  return kept;
 }
 
 // One level pass.  A CTA pipelines two dirty output blocks: while it merges
@@ -608,7 +650,7 @@ __global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* s
   if (warp == 1) bd_fill_hdr<KT>(M, st, desc, total, dlist, first_tile, D, Tin, vec, hdr[1]);
   bd_wait(hdr[0], &bar[0], 0u);
   __syncthreads();
-  if (warp == 0) bd_release_hdr(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, hdr[0]);
+  if (warp == 0) bd_release_hdr(st, pool, cap, remain, M.NB, P, M.lg, M.has_partial, hdr[0], false);
   for (uint32_t it = 0;; ++it) {
     const uint32_t s = it & 1u;
     const BdHdr& H0 = hdr[it % 3];
@@ -687,10 +729,12 @@ __global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* s
       if (H1.nslow) __syncthreads();                    // (element-wise pieces: every thread's)
     }
     if (warp == 0) {
-      if (more) bd_release_hdr(st, pool, cap, remain, Tin, M.NB, P, M.has_partial, H1);
-      __syncwarp();
+      // release block t+1's inputs, then take block t's output block: one the
+      // release just freed if any (no ring round trip), else from the ring
+      const uint32_t kept =
+          more ? bd_release_hdr(st, pool, cap, remain, M.NB, P, M.lg, M.has_partial, H1, true) : BD_NONE;
       if (tid == 0) {
-        const uint32_t b = bd_alloc(st, pool, cap);
+        const uint32_t b = kept != BD_NONE ? kept : bd_alloc(st, pool, cap);
         s_b[s] = b;
         if (b != BD_NONE) Tout[v] = b;
       }
@@ -734,13 +778,15 @@ __global__ void __launch_bounds__(1024) k_bd_ring_to_stack(BdState* st, uint32_t
 
 // After a level: the table maps the dirty blocks to their new homes.
 __global__ void k_bd_commit(BdState* st, const uint32_t* __restrict__ dlist, const uint32_t* __restrict__ D_ptr,
-                            const uint32_t* __restrict__ Tout, uint32_t* __restrict__ Tin, uint32_t* __restrict__ inv) {
+                            const uint32_t* __restrict__ Tout, uint32_t* __restrict__ Tin, uint32_t* __restrict__ inv,
+                            uint32_t* __restrict__ dirty, uint32_t vb0) {
   const uint32_t D = *D_ptr;
   if (blockIdx.x == 0 && threadIdx.x == 0) st->ticket = 0;  // the next level starts from its first dirty block
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < D; x += gridDim.x * blockDim.x) {
     const uint32_t v = dlist[x], b = Tout[v];
     Tin[v] = b;
     inv[b] = v;  // occupant of b (stale for freed blocks: check Tin[inv[b]] == b)
+    dirty[v - vb0] = 0;  // the next pass starts from clean flags
   }
 }
 
@@ -1072,8 +1118,10 @@ __global__ void __launch_bounds__(BD_CP_THREADS) k_bd_copy_all(BdMem<KT> M, BdSt
 // Initial pool: the scratch blocks.
 // Initial ring: the scratch blocks, every other slot empty.
 __global__ void k_bd_init(BdState* st, uint32_t* __restrict__ pool, uint32_t cap, uint32_t* __restrict__ Tin,
-                          uint32_t* __restrict__ inv, uint32_t NB, uint32_t F) {
+                          uint32_t* __restrict__ inv, uint32_t NB, uint32_t F, uint32_t* __restrict__ dirty) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < NB; v += gridDim.x * blockDim.x) Tin[v] = v;
+  // dirty flags start (and, cleared by every commit, stay) zero
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < NB + 8; v += gridDim.x * blockDim.x) dirty[v] = 0;
   for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < cap; x += gridDim.x * blockDim.x) {
     pool[x] = x < F ? NB + x : BD_NONE;
     inv[x] = x < NB ? x : BD_NONE;
