@@ -258,7 +258,7 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.first_tile = (uint32_t*)take(NBp * 4);
     // tiles of one level: one per output block plus gap tiles at node ends
     t.bdesc_cap = (uint32_t)(n / c.P + 4 * std::min<uint64_t>(n / c.fuse_z, (uint64_t)t.rmax) + 16);
-    t.bdesc = take((size_t)t.bdesc_cap * sizeof(TileDesc));
+    t.bdesc = take((size_t)t.bdesc_cap * sizeof(BdTile));
     t.bstate = take(sizeof(BdState));
     t.cplists = (uint32_t*)take((size_t)2 * BD_CP_LIST * 4);
   }
@@ -585,7 +585,7 @@ static vmps_status_t bd_levels(const BdCtx& C, const Work& w, uint64_t base, int
   const uint32_t vb1 = (uint32_t)std::min<uint64_t>(C.NB, (base + w.n + C.P - 1) / C.P);
   const uint32_t nbr = vb1 - vb0;
   const unsigned gNB = grid_for(nbr + 8);
-  TileDesc* desc = (TileDesc*)C.bdesc;
+  BdTile* desc = (BdTile*)C.bdesc;
   if (base) LAUNCH(k_rs_add_base, g, 256, 0, s, w.run_start, w.scalars, (uint32_t)base);
   // level kernel: persistent grid, shared memory for the block's inputs and outputs
   const int ds = dev_slot();
@@ -1093,7 +1093,7 @@ static size_t carve_gt(const Cfg& c, uint32_t rcell, char* base, BdCtx* C) {
   t.first_tile = (uint32_t*)take(NBp * 4);
   // a level of a cell: its blocks plus gap tiles at node ends (nodes <= runs / 2)
   t.bdesc_cap = t.NB + 2 * rcell + 16;
-  t.bdesc = take((size_t)t.bdesc_cap * sizeof(TileDesc));
+  t.bdesc = take((size_t)t.bdesc_cap * sizeof(BdTile));
   t.bstate = take(sizeof(BdState));
   t.cplists = (uint32_t*)take((size_t)2 * BD_CP_LIST * 4);
   take(64);  // bd_home's slot

@@ -176,6 +176,15 @@ __device__ uint32_t bd_corank(const BdMem<KT>& M, const uint32_t* Tin, uint32_t 
   return lo;
 }
 
+// A tile of a bounded level pass: output positions [lo, hi) of the node
+// [i, k) whose runs are [i, j) and [j, k); a0 / a1 = elements of [i, j)
+// among the node's first lo - i / hi - i outputs.  A gap tile (copy of the
+// elements between nodes) is a node with an empty right run.  (k is not
+// needed once the tile is cut: 24 bytes per tile.)
+struct BdTile {
+  uint32_t i, j, lo, hi, a0, a1;
+};
+
 // Tile descriptors of the level in output order (one thread per tile), and
 // the dirty output blocks.  A merge tile is an identity when every element it
 // outputs already sits at its output position: the whole node is a
@@ -196,7 +205,7 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
                                                       const uint32_t* __restrict__ lnodes_all,
                                                       const uint32_t* __restrict__ hscan, uint32_t nlt, int p,
                                                       const uint32_t* __restrict__ toff_all, uint32_t cap,
-                                                      BdState* st, TileDesc* __restrict__ desc,
+                                                      BdState* st, BdTile* __restrict__ desc,
                                                       uint32_t* __restrict__ info, uint32_t vb0,
                                                       uint32_t* __restrict__ dirty) {
   using T = KeyTraits<KT>;
@@ -216,19 +225,16 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
     uint32_t i, j, k, gl, gh;
     bd_node_geom(rs, seg_l, seg_r, lnodes, m, a, P, n, &i, &j, &k, &gl, &gh);
     uint32_t loc = tau - (toff[a] - T0);
-    TileDesc D;
-    D.par = 0;
-    if (gl < i && loc == 0) {  // left gap: copy [gl, i)
-      D.par = 1;  // a gap tile: identity, moves only with a dirty block
-      D.i = gl; D.j = i; D.k = i; D.lo = gl; D.hi = i; D.a0 = 0; D.a1 = i - gl;
+    BdTile D;
+    if (gl < i && loc == 0) {  // left gap: copy [gl, i) (an identity: moves only with a dirty block)
+      D.i = gl; D.j = i; D.lo = gl; D.hi = i; D.a0 = 0; D.a1 = i - gl;
       desc[tau] = D;
       continue;
     }
     if (gl < i) --loc;
     const uint32_t nt = (k + P - 1) / P - i / P;
     if (loc >= nt) {  // right gap: copy [k, gh)
-      D.par = 1;
-      D.i = k; D.j = gh; D.k = gh; D.lo = k; D.hi = gh; D.a0 = 0; D.a1 = gh - k;
+      D.i = k; D.j = gh; D.lo = k; D.hi = gh; D.a0 = 0; D.a1 = gh - k;
       desc[tau] = D;
       continue;
     }
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(256) k_bd_tile_desc(BdMem<KT> M, const uint32_
     const uint32_t nA = j - i, nB = k - j;
     const uint32_t a0 = lo == i ? 0u : bd_corank<KT>(M, Tin, i, nA, j, nB, lo - i);
     const uint32_t a1 = hi == k ? nA : bd_corank<KT>(M, Tin, i, nA, j, nB, hi - i);
-    D.i = i; D.j = j; D.k = k; D.lo = lo; D.hi = hi; D.a0 = a0; D.a1 = a1;
+    D.i = i; D.j = j; D.lo = lo; D.hi = hi; D.a0 = a0; D.a1 = a1;
     desc[tau] = D;
     const uint32_t nAt = a1 - a0, nBt = (hi - lo) - nAt, b0 = (lo - i) - a0;
     bool ident = (nBt == 0 && b0 == 0) || (nAt == 0 && a0 == nA);
@@ -253,7 +259,7 @@ constexpr uint32_t BD_SMALL_THREADS = 1024;
 constexpr uint32_t BD_SMALL_MAX = 32768;
 template <int KT>
 __global__ void __launch_bounds__(BD_SMALL_THREADS) k_bd_dirty_small(
-    BdMem<KT> M, const TileDesc* __restrict__ desc, const uint32_t* __restrict__ info,
+    BdMem<KT> M, const BdTile* __restrict__ desc, const uint32_t* __restrict__ info,
     const uint32_t* __restrict__ dirty, uint32_t* __restrict__ didx, uint32_t vb0, uint32_t nbr,
     uint32_t* __restrict__ dlist, uint32_t* __restrict__ first_tile, uint32_t* __restrict__ remain,
     uint32_t* __restrict__ D_out) {
@@ -304,7 +310,7 @@ __global__ void __launch_bounds__(BD_SMALL_THREADS) k_bd_dirty_small(
 // Dirty blocks of the range [vb0, vb0 + nbr) (flags and their scan are
 // indexed relative to vb0): their list, first tiles and consumption counters.
 template <int KT>
-__global__ void k_bd_dirty_list(BdMem<KT> M, const TileDesc* __restrict__ desc, const uint32_t* __restrict__ info,
+__global__ void k_bd_dirty_list(BdMem<KT> M, const BdTile* __restrict__ desc, const uint32_t* __restrict__ info,
                                 const uint32_t* __restrict__ dirty, const uint32_t* __restrict__ didx, uint32_t vb0,
                                 uint32_t nbr, uint32_t* __restrict__ dlist, uint32_t* __restrict__ first_tile,
                                 uint32_t* __restrict__ remain, uint32_t* __restrict__ D_out) {
@@ -392,7 +398,7 @@ struct BdHdr {
   uint32_t d, v, nt, valid;
   uint32_t nslow;       // pieces gathered element by element (unaligned arrays / the caller's partial last block)
   uint32_t pad[3];
-  TileDesc t[16];
+  BdTile t[16];
   uint32_t part[32][2];  // virtual start, length of part x
   uint32_t ko[32], vo[32];  // stage index of part x's first key / value
   uint32_t pcb[32][2];   // physical blocks of part x's two pieces; bit 31: gathered element-wise
@@ -417,7 +423,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // physical pieces of their inputs through T_in and lay the parts out in the
 // stage.  vec: every block base is 16-byte aligned (bulk copies allowed).
 template <int KT>
-__device__ __forceinline__ void bd_fill_hdr(const BdMem<KT>& M, BdState* st, const TileDesc* __restrict__ desc,
+__device__ __forceinline__ void bd_fill_hdr(const BdMem<KT>& M, BdState* st, const BdTile* __restrict__ desc,
                                             uint32_t total, const uint32_t* __restrict__ dlist,
                                             const uint32_t* __restrict__ first_tile, uint32_t D,
                                             const uint32_t* __restrict__ Tin, bool vec, BdHdr& H) {
@@ -434,7 +440,7 @@ __device__ __forceinline__ void bd_fill_hdr(const BdMem<KT>& M, BdState* st, con
   }
   const uint32_t v = dlist[d];
   const uint32_t tau = first_tile[d] + lane;
-  TileDesc t{};
+  BdTile t{};
   bool in = tau < total;
   if (in) { t = desc[tau]; in = (t.lo >> M.lg) == v; }
   const uint32_t mask = __ballot_sync(0xFFFFFFFFu, in);
@@ -448,7 +454,7 @@ __device__ __forceinline__ void bd_fill_hdr(const BdMem<KT>& M, BdState* st, con
   // part `lane`: its virtual range, its (at most two) physical pieces, its regions
   uint32_t gq = 0, len = 0;
   if (lane < 2 * nt) {
-    const TileDesc u = H.t[lane >> 1];
+    const BdTile u = H.t[lane >> 1];
     const uint32_t nA = u.a1 - u.a0;
     if (lane & 1) { gq = u.j + (u.lo - u.i) - u.a0; len = (u.hi - u.lo) - nA; }
     else { gq = u.i + u.a0; len = nA; }
@@ -610,7 +616,7 @@ __device__ __forceinline__ uint32_t bd_release_hdr(BdState* st, uint32_t* pool, 
 // and are stored straight into the output block (128-bit stores).  One CTA
 // barrier per block (two when the block has element-wise pieces).
 template <int KT, bool HV>
-__global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* st, const TileDesc* __restrict__ desc,
+__global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* st, const BdTile* __restrict__ desc,
                                                           const uint32_t* __restrict__ info,
                                                           const uint32_t* __restrict__ dlist,
                                                           const uint32_t* __restrict__ first_tile,
@@ -672,7 +678,7 @@ __global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* s
     if (nt == 1 && H0.t[0].lo == vbase && H0.t[0].hi == vbase + len && c1 == c0 + OPT) {
       // the block is one merge tile and the chunk is full: branch-free merge
       // over absolute stage indices (a read one past a part stays in its slack)
-      const TileDesc t = H0.t[0];
+      const BdTile t = H0.t[0];
       const uint32_t nA = t.a1 - t.a0, nB = len - nA;
       const uint32_t koA = H0.ko[0], koB = H0.ko[1];
       const int32_t dA = (int32_t)H0.vo[0] - (int32_t)koA, dB = (int32_t)H0.vo[1] - (int32_t)koB;
@@ -702,7 +708,7 @@ __global__ void __launch_bounds__(BD_THREADS) k_bd_level(BdMem<KT> M, BdState* s
       }
     } else {
       for (uint32_t x = 0; x < nt; ++x) {
-        const TileDesc t = H0.t[x];
+        const BdTile t = H0.t[x];
         const uint32_t o = t.lo - vbase, cnt = t.hi - t.lo, nA = t.a1 - t.a0, nB = cnt - nA;
         if (o >= c1 || o + cnt <= c0) continue;
         const uint32_t s0 = max(c0, o) - o;
