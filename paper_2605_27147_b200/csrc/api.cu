@@ -80,6 +80,17 @@ static uint32_t minrun_rule(uint64_t n) {
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+#ifndef VMPS_LEAF_ZB_SMALL
+#define VMPS_LEAF_ZB_SMALL 1
+#endif
+// Leaf batch window Zb: a batch (touching units starting in one window) spans
+// < Zb + Z positions.  VMPS_LEAF_ZB_SMALL: windows sized for the half-size CTA
+// (every batch fits it; cfg5 leaf 12.88 -> 12.64 ms), except in the bounded
+// mode, whose metadata (n / Zb batch slots) must stay small.
+static uint32_t leaf_zb(uint32_t fuse_z, bool bounded) {
+  const bool small = VMPS_LEAF_ZB_SMALL && !bounded && (uint32_t)LEAF_SMALL_CAP > fuse_z;
+  return (small ? (uint32_t)LEAF_SMALL_CAP : (uint32_t)LEAF_CAP) - fuse_z + 1;
+}
 
 static size_t scan_tmp_words(size_t len) {
   size_t nb = (len + SCAN_TILE - 1) / SCAN_TILE;
@@ -191,7 +202,7 @@ static size_t carve(const Cfg& c, Work* w, char* base) {
     t.unit_idx = (uint32_t*)take(R * 4);
     t.long_idx = (uint32_t*)take(R * 4);
     t.units = (uint32_t*)take(R * 3 * 4);
-    t.bcap = (uint32_t)(n / (LEAF_CAP - c.fuse_z + 1) + n / c.fuse_z + 2);
+    t.bcap = (uint32_t)(n / leaf_zb(c.fuse_z, c.scratch >= 0) + n / c.fuse_z + 2);
     t.batch_first = (uint32_t*)take(((size_t)t.bcap + 2) * 4);
     t.longs = (uint32_t*)take(R * 4 * 4);
     t.long_chunks = (uint32_t*)take(R * 4);
@@ -778,7 +789,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   // a batch = consecutive touching units starting in one window of Zb
   // positions; units are <= Z long, so a batch spans < Zb + Z <= LEAF_CAP
   // elements and fills most of the CTA.  Batches <= windows + long leaves.
-  const uint32_t zb = (uint32_t)LEAF_CAP - w.fuse_z + 1;
+  const uint32_t zb = leaf_zb(w.fuse_z, w.bounded);
   const uint32_t nbatch = w.bcap;
   LAUNCH(k_batch_flags, g, 256, 0, s, w.units, w.scalars, zb, w.rmax, w.unit_flag);
   scan_u32(w.unit_flag, w.unit_idx, w.rmax + 1, w.scan_tmp, s);
