@@ -40,7 +40,10 @@ struct NodeRuns {
 // are output-aligned, 128-bit stores).  17 consumer warps cover both:
 // 4096 / 8 = 512 chunks, and up to ceil(n01 / 9) + ceil(n23 / 9) <= 457.
 constexpr int M4_KQ = 8;                       // copy / two-run tiles
-constexpr uint32_t M4_KA = 9;                  // steps A and B
+#ifndef VMPS_M4_KA
+#define VMPS_M4_KA 9
+#endif
+constexpr uint32_t M4_KA = VMPS_M4_KA;         // steps A and B (odd)
 constexpr uint32_t M4_NT = 4096 / M4_KQ + 32;  // consumer threads (17 warps)
 constexpr uint32_t M4_THREADS = M4_NT + 32;    // + the producer warp
 static_assert((4096 + M4_KA - 1) / M4_KA + 1 <= M4_NT, "step A chunks");
