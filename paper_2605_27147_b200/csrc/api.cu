@@ -799,8 +799,9 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   else {
     LAUNCH((k_leaf_sort<KT, HV, LEAF_SMALL>), nsm() * 2 * VMPS_LEAF_MINB, LEAF_SMALL, lsm2, s, k0, v0, k1, v1,
            w.units, w.batch_first, w.scalars);
-    LAUNCH((k_leaf_sort<KT, HV, LEAF_THREADS>), nsm() * VMPS_LEAF_MINB, LEAF_THREADS, lsm, s, k0, v0, k1, v1,
-           w.units, w.batch_first, w.scalars);
+    if (zb + w.fuse_z - 1 > (uint32_t)LEAF_SMALL_CAP)  // some batch may exceed the half-size CTA
+      LAUNCH((k_leaf_sort<KT, HV, LEAF_THREADS>), nsm() * VMPS_LEAF_MINB, LEAF_THREADS, lsm, s, k0, v0, k1, v1,
+             w.units, w.batch_first, w.scalars);
   }
   LAUNCH((k_long_leaves<KT, HV>), nsm() * 8, 256, 0, s, k0, v0, k1, v1, w.longs, w.long_off, w.scalars,
          LONG_CHUNK);
