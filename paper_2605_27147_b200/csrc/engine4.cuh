@@ -431,7 +431,7 @@ struct Merge4Smem {
 };
 
 constexpr int M4_WARPS = M4_NT / 32;  // consumer warps of a tile (17)
-struct Merge4Hdr {
+struct alignas(16) Merge4Hdr {
   uint32_t kb[4], n[4];  // key element offset / count of each window in the stage
   uint32_t vb[4];        // value element offset of each window
   uint32_t lo, hi, par, mode;  // mode: 0 general, 1 two runs (W0, W2), 2 + w single run w
@@ -442,6 +442,24 @@ struct Merge4Hdr {
   uint16_t bnd[M4_WARPS + 1];
 };
 static_assert(64 + 2 * sizeof(Merge4Hdr) <= 512, "merge4 header area");
+
+// A consumer thread's copy of a tile header: four 128-bit shared-memory loads
+// (broadcast) instead of a scalar load per field and use -- the header reads
+// were ~5% of the shared-memory wavefronts of this LSU-bound kernel.
+struct M4H {
+  uint32_t kb[4], n[4], vb[4];
+  uint32_t lo, hi, par, mode;
+};
+__device__ __forceinline__ M4H m4_load_hdr(const Merge4Hdr* hp) {
+  const uint4* q = reinterpret_cast<const uint4*>(hp);
+  const uint4 a = q[0], b = q[1], c = q[2], d = q[3];
+  M4H h;
+  h.kb[0] = a.x; h.kb[1] = a.y; h.kb[2] = a.z; h.kb[3] = a.w;
+  h.n[0] = b.x; h.n[1] = b.y; h.n[2] = b.z; h.n[3] = b.w;
+  h.vb[0] = c.x; h.vb[1] = c.y; h.vb[2] = c.z; h.vb[3] = c.w;
+  h.lo = d.x; h.hi = d.y; h.par = d.z; h.mode = d.w;
+  return h;
+}
 
 template <int KT, bool HV>
 __device__ __forceinline__ void merge4_issue(const TileDesc4& d, const TileDesc4* dn_or_null, const NodeRuns& R,
@@ -557,12 +575,12 @@ __device__ __forceinline__ void merge4_bnds(const typename KeyTraits<KT>::K* SK,
 // its in-range outputs.  With have_bnd, the co-rank search is bracketed by the
 // producer's co-ranks at this warp's boundaries.
 template <int KT>
-__device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK, const Merge4Hdr* hp,
+__device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK, const M4H& h, const uint16_t* bnd,
                                              typename KeyTraits<KT>::K* IKs, uint16_t* IIs, bool have_bnd) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
   constexpr uint32_t KQ = M4_KA;
-  const uint32_t n01 = hp->n[0] + hp->n[1], n23 = hp->n[2] + hp->n[3];
+  const uint32_t n01 = h.n[0] + h.n[1], n23 = h.n[2] + h.n[3];
   const uint32_t n01p = m4_n01p(n01);
   const uint32_t q0 = threadIdx.x * KQ;
   const bool part0 = q0 < n01p;
@@ -570,17 +588,18 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
   const uint32_t d = q0 - base;
   if (d >= plen) return;  // past P23 (part 0 chunks always start inside P01)
   const uint32_t wa = part0 ? 0u : 2u;
-  const uint32_t nA = hp->n[wa], nB = hp->n[wa + 1];
-  const uint32_t ka0 = hp->kb[wa], kb0 = hp->kb[wa + 1];
-  const int32_t dA = (int32_t)hp->vb[wa] - (int32_t)ka0, dB = (int32_t)hp->vb[wa + 1] - (int32_t)kb0;
+  const uint32_t nA = part0 ? h.n[0] : h.n[2], nB = part0 ? h.n[1] : h.n[3];
+  const uint32_t ka0 = part0 ? h.kb[0] : h.kb[2], kb0 = part0 ? h.kb[1] : h.kb[3];
+  const int32_t dA = (int32_t)(part0 ? h.vb[0] : h.vb[2]) - (int32_t)ka0,
+                dB = (int32_t)(part0 ? h.vb[1] : h.vb[3]) - (int32_t)kb0;
   uint32_t lb = 0u, ub = 0xFFFFFFFFu;
   if (have_bnd) {
     // c(x1) = c1 <= c(d) <= c(x2) = c2, c(d) - c1 <= d - x1, c2 - c(d) <= x2 - d
     const uint32_t w = threadIdx.x >> 5;
     const uint32_t ws = w * 32u * KQ, we = ws + 32u * KQ;
     uint32_t x1 = 0u, c1 = 0u, x2 = nA + nB, c2 = nA;
-    if (ws >= base) { x1 = ws - base; c1 = hp->bnd[w]; }
-    if (we < base + plen) { x2 = we - base; c2 = hp->bnd[w + 1]; }
+    if (ws >= base) { x1 = ws - base; c1 = bnd[w]; }
+    if (we < base + plen) { x2 = we - base; c2 = bnd[w + 1]; }
     lb = max(c1, c2 > x2 - d ? c2 - (x2 - d) : 0u);
     ub = min(c2, c1 + (d - x1));
   }
@@ -748,7 +767,7 @@ __device__ __forceinline__ void merge4_copy(const typename KeyTraits<KT>::K* SK,
 // (absolute stage indices; a read one past a window stays in the stage).
 template <int KT, bool HV, int KQ>
 __device__ __forceinline__ void merge4_direct(const typename KeyTraits<KT>::K* SK, const uint32_t* SV,
-                                              const Merge4Hdr* hp, uint32_t lo, uint32_t hi, uint32_t par,
+                                              const M4H& h, uint32_t lo, uint32_t hi, uint32_t par,
                                               typename KeyTraits<KT>::K* k0, uint32_t* v0,
                                               typename KeyTraits<KT>::K* k1, uint32_t* v1) {
   using T = KeyTraits<KT>;
@@ -757,9 +776,9 @@ __device__ __forceinline__ void merge4_direct(const typename KeyTraits<KT>::K* S
   if (!(start < hi && start + (uint32_t)KQ > lo)) return;
   K* dk = par ? k1 : k0;
   uint32_t* dv = par ? v1 : v0;
-  const uint32_t nA = hp->n[0], nB = hp->n[2];
-  const uint32_t ka0 = hp->kb[0], kb0 = hp->kb[2];
-  const int32_t dA = (int32_t)hp->vb[0] - (int32_t)ka0, dB = (int32_t)hp->vb[2] - (int32_t)kb0;
+  const uint32_t nA = h.n[0], nB = h.n[2];
+  const uint32_t ka0 = h.kb[0], kb0 = h.kb[2];
+  const int32_t dA = (int32_t)h.vb[0] - (int32_t)ka0, dB = (int32_t)h.vb[2] - (int32_t)kb0;
   const uint32_t qs = max(start, lo);
   const uint32_t d = qs - lo;
   const uint32_t l = corank<KT>(SK + ka0, nA, SK + kb0, nB, d);
@@ -816,24 +835,27 @@ __device__ __forceinline__ void merge4_tile(const Merge4Hdr* hp, unsigned char* 
   const uint32_t lane = threadIdx.x & 31u;
   K* SK = reinterpret_cast<K*>(st);
   const uint32_t* SV = reinterpret_cast<const uint32_t*>(st + SM::KB);
-  const uint32_t lo = hp->lo, hi = hp->hi, par = hp->par;
-  const uint32_t mode = hp->mode;
+  const M4H h = m4_load_hdr(hp);
+  const uint32_t lo = h.lo, hi = h.hi, par = h.par;
+  const uint32_t mode = h.mode;
   if (mode >= 2) {
     // run-skip tile: every output comes from one run, so
     // the tile is a compare-free copy of that window
     const uint32_t wsrc = mode - 2;
-    merge4_copy<KT, HV, M4_KQ>(SK, SV, hp->kb[wsrc], hp->vb[wsrc], lo, hi, par, k0, v0, k1, v1);
+    const uint32_t kbw = wsrc == 0 ? h.kb[0] : wsrc == 1 ? h.kb[1] : wsrc == 2 ? h.kb[2] : h.kb[3];
+    const uint32_t vbw = wsrc == 0 ? h.vb[0] : wsrc == 1 ? h.vb[1] : wsrc == 2 ? h.vb[2] : h.vb[3];
+    merge4_copy<KT, HV, M4_KQ>(SK, SV, kbw, vbw, lo, hi, par, k0, v0, k1, v1);
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_s);
   } else if (mode == 1) {
     // both children are single runs (leaves / units): one 2-way merge
     // straight from the stage, no intermediate
-    merge4_direct<KT, HV, M4_KQ>(SK, SV, hp, lo, hi, par, k0, v0, k1, v1);
+    merge4_direct<KT, HV, M4_KQ>(SK, SV, h, lo, hi, par, k0, v0, k1, v1);
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_s);
   } else {
-    const uint32_t n01 = hp->n[0] + hp->n[1], T4 = hi - lo;
-    merge4_stepA<KT>(SK, hp, IKs, IIs, have_bnd);
+    const uint32_t n01 = h.n[0] + h.n[1], T4 = hi - lo;
+    merge4_stepA<KT>(SK, h, hp->bnd, IKs, IIs, have_bnd);
     named_bar_sync(1, M4_NT);  // the intermediate is complete; the stage keys are dead
     merge4_stepB<KT, HV>(IKs, IIs, SV, lo, n01, T4, SK, OVs);
     fence_proxy_async_smem();  // staged outputs -> visible to the bulk stores
