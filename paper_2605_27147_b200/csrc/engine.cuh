@@ -354,9 +354,18 @@ __global__ void __launch_bounds__(256) k_long_leaves(
   using K = typename KeyTraits<KT>::K;
   const uint32_t nlong = scalars[SC_LONG];
   const uint32_t total = long_off[nlong];
-  for (uint32_t c = blockIdx.x; c < total; c += gridDim.x) {
-    uint32_t a = 0, b = nlong;  // last x with long_off[x] <= c
-    while (b - a > 1) { uint32_t m = (a + b) >> 1; if (long_off[m] <= c) a = m; else b = m; }
+  // a contiguous range of chunks per CTA: one search for the first chunk's
+  // leaf, then the leaf index only moves forward (a search per chunk was a
+  // chain of ~17 dependent loads per 4096 elements)
+  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+  const uint32_t c0 = blockIdx.x * per, c1 = min(total, c0 + per);
+  uint32_t a = 0;
+  if (c0 < c1) {
+    uint32_t b = nlong;  // last x with long_off[x] <= c0
+    while (b - a > 1) { uint32_t m = (a + b) >> 1; if (long_off[m] <= c0) a = m; else b = m; }
+  }
+  for (uint32_t c = c0; c < c1; ++c) {
+    while (a + 1 < nlong && long_off[a + 1] <= c) ++a;
     const uint32_t s = longs[4 * a], e = longs[4 * a + 1], f = longs[4 * a + 2];
     const uint32_t len = e - s;
     const bool desc = f & 2u, odd = f & 1u;

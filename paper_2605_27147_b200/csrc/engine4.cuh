@@ -587,7 +587,6 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
   const uint32_t base = part0 ? 0u : n01p, plen = part0 ? n01 : n23;
   const uint32_t d = q0 - base;
   if (d >= plen) return;  // past P23 (part 0 chunks always start inside P01)
-  const uint32_t wa = part0 ? 0u : 2u;
   const uint32_t nA = part0 ? h.n[0] : h.n[2], nB = part0 ? h.n[1] : h.n[3];
   const uint32_t ka0 = part0 ? h.kb[0] : h.kb[2], kb0 = part0 ? h.kb[1] : h.kb[3];
   const int32_t dA = (int32_t)(part0 ? h.vb[0] : h.vb[2]) - (int32_t)ka0,
