@@ -44,6 +44,10 @@ constexpr int M4_KQ = 8;                       // copy / two-run tiles
 #define VMPS_M4_KA 9
 #endif
 constexpr uint32_t M4_KA = VMPS_M4_KA;         // steps A and B (odd)
+#ifndef VMPS_M4_IV
+#define VMPS_M4_IV 1
+#endif
+constexpr bool M4_IV = VMPS_M4_IV;             // step A carries the payload (see Merge4Smem)
 constexpr uint32_t M4_NT = 4096 / M4_KQ + 32;  // consumer threads (17 warps)
 constexpr uint32_t M4_THREADS = M4_NT + 32;    // + the producer warp
 static_assert((4096 + M4_KA - 1) / M4_KA + 1 <= M4_NT, "step A chunks");
@@ -423,10 +427,13 @@ struct Merge4Smem {
   // rounded up to a multiple of KA (<= 4096 + 8 positions), + read-ahead slack
   static constexpr uint32_t IPOS = 4096 + 48;
   static constexpr uint32_t IK = IPOS * sizeof(K);  // intermediate keys
-  static constexpr uint32_t II = IPOS * 2;          // intermediate value indices (u16)
+  // intermediate payload: with M4_IV the values themselves (u32, gathered
+  // by step A next to its key loads), else the stage index of each value (u16)
+  static constexpr uint32_t II = !HV ? 0u : M4_IV ? IPOS * 4 : IPOS * 2;
   // step B output staging: keys go to the tile's stage key area (free once
-  // step A is done), values to OV; both then leave by TMA bulk stores
-  static constexpr uint32_t OV = HV ? 4096 * 4 + 64 : 0;
+  // step A is done), values to the stage value area with M4_IV (step A has
+  // read it) or else to OV; both then leave by TMA bulk stores
+  static constexpr uint32_t OV = (HV && !M4_IV) ? 4096 * 4 + 64 : 0;
   static constexpr uint32_t BYTES = HDR + NSTG * STAGE + IK + II + OV;
 };
 
@@ -535,6 +542,37 @@ __device__ __forceinline__ void merge4_issue(const TileDesc4& d, const TileDesc4
   }
 }
 
+
+// KQ consecutive outputs of a stable 2-way merge in shared memory, A at
+// [ia, ea) and B at [ib, eb) (absolute indices into S), ties to A.
+// rk = keys, ri = the index of each output in S plus dA / dB (the position
+// of its value).  Reads one past a part stay inside S (padded).  (A second,
+// test-free path for chunks that cannot exhaust a part measured slower:
+// 68.4 vs 67.1 ms at cfg5 -- the two unrolled bodies diverge inside warps.)
+template <int KT, int KQ>
+__device__ __forceinline__ void merge_serial(const typename KeyTraits<KT>::K* S, uint32_t ia, uint32_t ib,
+                                             uint32_t ea, uint32_t eb, int32_t dA, int32_t dB,
+                                             typename KeyTraits<KT>::K (&rk)[KQ], uint32_t (&ri)[KQ]) {
+  using T = KeyTraits<KT>;
+  using K = typename T::K;
+  K ka = S[ia], kb = S[ib];
+  typename T::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load
+#pragma unroll
+  for (int q = 0; q < KQ; ++q) {
+    const bool pa = ib >= eb || (ia < ea && oa <= ob);
+    rk[q] = pa ? ka : kb;
+    ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
+    ia += pa ? 1u : 0u;
+    ib += pa ? 0u : 1u;
+    const K nx = S[pa ? ia : ib];
+    const typename T::O onx = T::ord(nx);
+    ka = pa ? nx : ka;
+    oa = pa ? onx : oa;
+    kb = pa ? kb : nx;
+    ob = pa ? ob : onx;
+  }
+}
+
 // Step A: P01 = W0 (+) W1 into [0, n01), P23 = W2 (+) W3 into [n01, T4) of
 // the intermediate (keys + the stage index of each value), KQ outputs per
 // thread.  A chunk inside one of the two merges takes the unrolled
@@ -574,9 +612,10 @@ __device__ __forceinline__ void merge4_bnds(const typename KeyTraits<KT>::K* SK,
 // windows are padded).  A part's last chunk runs all KA steps and stores only
 // its in-range outputs.  With have_bnd, the co-rank search is bracketed by the
 // producer's co-ranks at this warp's boundaries.
-template <int KT>
-__device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK, const M4H& h, const uint16_t* bnd,
-                                             typename KeyTraits<KT>::K* IKs, uint16_t* IIs, bool have_bnd) {
+template <int KT, bool HV>
+__device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK, const uint32_t* SV, const M4H& h,
+                                             const uint16_t* bnd, typename KeyTraits<KT>::K* IKs, void* IX,
+                                             bool have_bnd) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
   constexpr uint32_t KQ = M4_KA;
@@ -603,33 +642,24 @@ __device__ __forceinline__ void merge4_stepA(const typename KeyTraits<KT>::K* SK
     ub = min(c2, c1 + (d - x1));
   }
   const uint32_t l = corank_in<KT>(SK + ka0, nA, SK + kb0, nB, d, lb, ub);
-  uint32_t ia = ka0 + l, ib = kb0 + d - l;
-  const uint32_t ea = ka0 + nA, eb = kb0 + nB;
-  K ka = SK[ia], kb = SK[ib];
-  typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load
   K rk[KQ];
   uint32_t ri[KQ];
-#pragma unroll
-  for (int q = 0; q < (int)KQ; ++q) {
-    const bool pa = ib >= eb || (ia < ea && oa <= ob);
-    rk[q] = pa ? ka : kb;
-    ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
-    ia += pa ? 1u : 0u;
-    ib += pa ? 0u : 1u;
-    const K nx = SK[pa ? ia : ib];
-    const typename KeyTraits<KT>::O onx = T::ord(nx);
-    ka = pa ? nx : ka;
-    oa = pa ? onx : oa;
-    kb = pa ? kb : nx;
-    ob = pa ? ob : onx;
-  }
+  merge_serial<KT, (int)KQ>(SK, ka0 + l, kb0 + d - l, ka0 + nA, kb0 + nB, dA, dB, rk, ri);
+  uint32_t* IVs = reinterpret_cast<uint32_t*>(IX);
+  uint16_t* IIs = reinterpret_cast<uint16_t*>(IX);
   if (d + KQ <= plen) {
 #pragma unroll
-    for (int q = 0; q < (int)KQ; ++q) { IKs[q0 + q] = rk[q]; IIs[q0 + q] = (uint16_t)ri[q]; }
+    for (int q = 0; q < (int)KQ; ++q) {
+      IKs[q0 + q] = rk[q];
+      if (HV) { if (M4_IV) IVs[q0 + q] = SV[ri[q]]; else IIs[q0 + q] = (uint16_t)ri[q]; }
+    }
   } else {
 #pragma unroll
     for (int q = 0; q < (int)KQ; ++q)
-      if (d + q < plen) { IKs[q0 + q] = rk[q]; IIs[q0 + q] = (uint16_t)ri[q]; }
+      if (d + q < plen) {
+        IKs[q0 + q] = rk[q];
+        if (HV) { if (M4_IV) IVs[q0 + q] = SV[ri[q]]; else IIs[q0 + q] = (uint16_t)ri[q]; }
+      }
   }
 }
 
@@ -654,51 +684,38 @@ __host__ __device__ constexpr uint32_t vec16() { return 16u / (uint32_t)sizeof(X
 // (lo mod vec16) + d -- the stage key area for keys, OV for values -- so that
 // the 16-byte aligned part of [lo, hi) is one bulk store per array.
 template <int KT, bool HV>
-__device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IKs, const uint16_t* IIs,
+__device__ __forceinline__ void merge4_stepB(const typename KeyTraits<KT>::K* IKs, const void* IX,
                                              const uint32_t* SV, uint32_t lo, uint32_t n01, uint32_t T4,
                                              typename KeyTraits<KT>::K* OKs, uint32_t* OVs) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
   constexpr uint32_t KQ = M4_KA;
   const uint32_t d = threadIdx.x * KQ;
-  if (d >= T4) return;
   const uint32_t n01p = m4_n01p(n01);  // P23 starts here (step A layout)
   const uint32_t nA = n01, nB = T4 - n01;
+  // (bracketing this search by a 32-ary warp co-rank at the warp's first
+  // output measured slower: cfg5 68.2 vs 67.0 ms, cfg4 7.50 vs 7.11 ms)
+  if (d >= T4) return;
   const uint32_t l = corank<KT>(IKs, nA, IKs + n01p, nB, d);
-  uint32_t ia = l, ib = n01p + d - l;
-  const uint32_t ea = n01, eb = n01p + nB;
-  K ka = IKs[ia], kb = IKs[ib];  // reads past the parts stay inside the intermediate (slack)
-  typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);
   K rk[KQ];
-  uint32_t ri[KQ];
-#pragma unroll
-  for (int q = 0; q < (int)KQ; ++q) {
-    const bool pa = ib >= eb || (ia < ea && oa <= ob);
-    rk[q] = pa ? ka : kb;
-    ri[q] = pa ? ia : ib;
-    ia += pa ? 1u : 0u;
-    ib += pa ? 0u : 1u;
-    const K nx = IKs[pa ? ia : ib];
-    const typename KeyTraits<KT>::O onx = T::ord(nx);
-    ka = pa ? nx : ka;
-    oa = pa ? onx : oa;
-    kb = pa ? kb : nx;
-    ob = pa ? ob : onx;
-  }
+  uint32_t ri[KQ];  // reads past the parts stay inside the intermediate (slack)
+  merge_serial<KT, (int)KQ>(IKs, l, n01p + d - l, n01, n01p + nB, 0, 0, rk, ri);
   K* ok = OKs + (lo & (vec16<K>() - 1u)) + d;
   uint32_t* ov = OVs + (lo & 3u) + d;
+  const uint32_t* IVs = reinterpret_cast<const uint32_t*>(IX);
+  const uint16_t* IIs = reinterpret_cast<const uint16_t*>(IX);
   if (d + KQ <= T4) {
 #pragma unroll
     for (int q = 0; q < (int)KQ; ++q) {
       ok[q] = rk[q];
-      if (HV) ov[q] = SV[IIs[ri[q]]];
+      if (HV) ov[q] = M4_IV ? IVs[ri[q]] : SV[IIs[ri[q]]];
     }
   } else {
 #pragma unroll
     for (int q = 0; q < (int)KQ; ++q)
       if (d + q < T4) {
         ok[q] = rk[q];
-        if (HV) ov[q] = SV[IIs[ri[q]]];
+        if (HV) ov[q] = M4_IV ? IVs[ri[q]] : SV[IIs[ri[q]]];
       }
   }
 }
@@ -781,26 +798,9 @@ __device__ __forceinline__ void merge4_direct(const typename KeyTraits<KT>::K* S
   const uint32_t qs = max(start, lo);
   const uint32_t d = qs - lo;
   const uint32_t l = corank<KT>(SK + ka0, nA, SK + kb0, nB, d);
-  uint32_t ia = ka0 + l, ib = kb0 + d - l;
-  const uint32_t ea = ka0 + nA, eb = kb0 + nB;
-  K ka = SK[ia], kb = SK[ib];
-    typename KeyTraits<KT>::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load
   K rk[KQ];
   uint32_t ri[KQ];
-#pragma unroll
-  for (int q = 0; q < KQ; ++q) {
-    const bool pa = ib >= eb || (ia < ea && oa <= ob);
-    rk[q] = pa ? ka : kb;
-    ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
-    ia += pa ? 1u : 0u;
-    ib += pa ? 0u : 1u;
-    const K nx = SK[pa ? ia : ib];
-      const typename KeyTraits<KT>::O onx = T::ord(nx);
-    ka = pa ? nx : ka;
-      oa = pa ? onx : oa;
-    kb = pa ? kb : nx;
-      ob = pa ? ob : onx;
-  }
+  merge_serial<KT, KQ>(SK, ka0 + l, kb0 + d - l, ka0 + nA, kb0 + nB, dA, dB, rk, ri);
   if (qs == start && start + (uint32_t)KQ <= hi) {
     store_chunk_g<KQ>(dk + start, rk);
     if (HV) {
@@ -826,7 +826,7 @@ __device__ __forceinline__ void merge4_direct(const typename KeyTraits<KT>::K* S
 // stores have read the stage's key area).
 template <int KT, bool HV>
 __device__ __forceinline__ void merge4_tile(const Merge4Hdr* hp, unsigned char* st, typename KeyTraits<KT>::K* IKs,
-                                            uint16_t* IIs, uint32_t* OVs, uint64_t* empty_s, bool have_bnd,
+                                            void* IX, uint32_t* OVa, uint64_t* empty_s, bool have_bnd,
                                             typename KeyTraits<KT>::K* k0, uint32_t* v0,
                                             typename KeyTraits<KT>::K* k1, uint32_t* v1) {
   using K = typename KeyTraits<KT>::K;
@@ -854,9 +854,10 @@ __device__ __forceinline__ void merge4_tile(const Merge4Hdr* hp, unsigned char* 
     if (lane == 0) mbar_arrive(empty_s);
   } else {
     const uint32_t n01 = h.n[0] + h.n[1], T4 = hi - lo;
-    merge4_stepA<KT>(SK, h, hp->bnd, IKs, IIs, have_bnd);
-    named_bar_sync(1, M4_NT);  // the intermediate is complete; the stage keys are dead
-    merge4_stepB<KT, HV>(IKs, IIs, SV, lo, n01, T4, SK, OVs);
+    merge4_stepA<KT, HV>(SK, SV, h, hp->bnd, IKs, IX, have_bnd);
+    named_bar_sync(1, M4_NT);  // the intermediate is complete; the stage keys (and with M4_IV values) are dead
+    uint32_t* OVs = M4_IV ? reinterpret_cast<uint32_t*>(st + SM::KB) : OVa;
+    merge4_stepB<KT, HV>(IKs, IX, SV, lo, n01, T4, SK, OVs);
     fence_proxy_async_smem();  // staged outputs -> visible to the bulk stores
     named_bar_sync(1, M4_NT);  // staging complete; the intermediate is free for the next tile
     merge4_flush<KT, HV>(SK, OVs, lo, hi, par ? k1 : k0, par ? v1 : v0);
@@ -885,7 +886,7 @@ __global__ void __launch_bounds__(M4_THREADS, 2) k4_merge_level(
   uint64_t* ready = full + 4;  // step A boundaries written (producer warp, 32 arrivals)
   Merge4Hdr* hdr = reinterpret_cast<Merge4Hdr*>(smem + 64);
   K* IKs = reinterpret_cast<K*>(smem + SM::HDR + SM::NSTG * SM::STAGE);
-  uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK);
+  void* IX = smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK;
   uint32_t* OVs = reinterpret_cast<uint32_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK + SM::II);
   const uint32_t count = level_tile[p + 1] - level_tile[p];
   if (blockIdx.x >= count) return;
@@ -922,7 +923,7 @@ __global__ void __launch_bounds__(M4_THREADS, 2) k4_merge_level(
   for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
     const uint32_t s = it % SM::NSTG;
     mbar_wait(&ready[s], (it / SM::NSTG) & 1u);
-    merge4_tile<KT, HV>(hdr + s, smem + SM::HDR + s * SM::STAGE, IKs, IIs, OVs, &empty[s], true, k0, v0, k1, v1);
+    merge4_tile<KT, HV>(hdr + s, smem + SM::HDR + s * SM::STAGE, IKs, IX, OVs, &empty[s], true, k0, v0, k1, v1);
   }
   if (tid == 0) bulk_wait0();  // the last bulk stores are complete before the kernel ends
 }
@@ -1065,7 +1066,7 @@ __global__ void __launch_bounds__(M4_THREADS, 2) k_pull_merge(PullSrc<KT> S, typ
   uint64_t* ready = full + 4;
   Merge4Hdr* hdr = reinterpret_cast<Merge4Hdr*>(smem + 64);
   K* IKs = reinterpret_cast<K*>(smem + SM::HDR + SM::NSTG * SM::STAGE);
-  uint16_t* IIs = reinterpret_cast<uint16_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK);
+  void* IX = smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK;
   uint32_t* OVs = reinterpret_cast<uint32_t*>(smem + SM::HDR + SM::NSTG * SM::STAGE + SM::IK + SM::II);
   if (blockIdx.x >= count) return;
   const uint32_t tid = threadIdx.x;
@@ -1101,7 +1102,7 @@ __global__ void __launch_bounds__(M4_THREADS, 2) k_pull_merge(PullSrc<KT> S, typ
   for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
     const uint32_t s = it % SM::NSTG;
     mbar_wait(&ready[s], (it / SM::NSTG) & 1u);
-    merge4_tile<KT, HV>(hdr + s, smem + SM::HDR + s * SM::STAGE, IKs, IIs, OVs, &empty[s], true, ok, ov, ok, ov);
+    merge4_tile<KT, HV>(hdr + s, smem + SM::HDR + s * SM::STAGE, IKs, IX, OVs, &empty[s], true, ok, ov, ok, ov);
   }
   if (tid == 0) bulk_wait0();
 }
