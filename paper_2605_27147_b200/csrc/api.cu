@@ -797,10 +797,10 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
   if (g_leaf_radix)
     LAUNCH((k_leaf_radix<KT, HV>), nbatch, LEAF_THREADS, rsm, s, k0, v0, k1, v1, w.units, w.batch_first);
   else {
-    LAUNCH((k_leaf_sort<KT, HV, LEAF_SMALL>), nsm() * 2 * VMPS_LEAF_MINB, LEAF_SMALL, lsm2, s, k0, v0, k1, v1,
+    LAUNCH((k_leaf_sort<KT, HV, LEAF_SMALL>), nsm() * 2 * leaf_minb<KT>(), LEAF_SMALL, lsm2, s, k0, v0, k1, v1,
            w.units, w.batch_first, w.scalars);
     if (zb + w.fuse_z - 1 > (uint32_t)LEAF_SMALL_CAP)  // some batch may exceed the half-size CTA
-      LAUNCH((k_leaf_sort<KT, HV, LEAF_THREADS>), nsm() * VMPS_LEAF_MINB, LEAF_THREADS, lsm, s, k0, v0, k1, v1,
+      LAUNCH((k_leaf_sort<KT, HV, LEAF_THREADS>), nsm() * leaf_minb<KT>(), LEAF_THREADS, lsm, s, k0, v0, k1, v1,
              w.units, w.batch_first, w.scalars);
   }
   LAUNCH((k_long_leaves<KT, HV>), nsm() * 8, 256, 0, s, k0, v0, k1, v1, w.longs, w.long_off, w.scalars,

@@ -285,11 +285,206 @@ __device__ __forceinline__ void leaf_sort_batch(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Composite-key leaf (4-byte keys, VMPS_LEAF_C): every element of the batch
+// becomes one u64 c = unit ordinal (19 bits) | order image of the key (32) |
+// batch position (13).  The units of a batch are consecutive and a unit's
+// fused subtree ends as the stable sort of its elements (Alg. 1's merges of
+// sorted runs, ties to the left run, keep equal keys in input order),
+// so the whole batch sorted by c is exactly every unit's result in place --
+// and the c are distinct, so the rounds below are plain merges of one u64
+// stream: no unit boundaries inside the rounds (no unit lookups, no mixed
+// merge / copy chunks), no separate index array to gather each round, and
+// the payload is gathered once at the end by the position bits.  Positions
+// [E, Ep) hold all-ones sentinels (Ep = E rounded up to LEAF_K).
+// ---------------------------------------------------------------------------
+#ifndef VMPS_LEAF_C
+#define VMPS_LEAF_C 1
+#endif
+template <int KT>
+__host__ __device__ constexpr bool leaf_composite() {
+  return VMPS_LEAF_C && sizeof(typename KeyTraits<KT>::K) == 4;
+}
+// resident CTAs of the full-size class per SM (the half-size class: twice as many)
+template <int KT>
+__host__ __device__ constexpr int leaf_minb() { return leaf_composite<KT>() ? 3 : VMPS_LEAF_MINB; }
+
+template <int KT, bool HV, int LT>
+__device__ __forceinline__ void leaf_sort_batch_c(
+    typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
+    typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
+    const uint32_t* __restrict__ units, const uint32_t* __restrict__ batch_first, uint32_t b) {
+  using T = KeyTraits<KT>;
+  using K = typename T::K;
+  static_assert(sizeof(K) == 4, "composite leaf: 4-byte keys");
+  static_assert(LT * LEAF_K <= 8192, "composite leaf: 13 position bits");
+  constexpr int NTH = LT, CAP = LT * LEAF_K;
+  constexpr uint64_t SENT = ~0ull;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* const scb = reinterpret_cast<uint64_t*>(smem_raw);  // 2 x CAP composites
+  uint32_t* ubits = reinterpret_cast<uint32_t*>(scb + 2 * CAP);  // unit-start bitmap
+  uint32_t* upre = ubits + CAP / 32 + 1;  // exclusive popcount prefix per word
+  uint32_t* pcar = upre + CAP / 32 + 1;   // parity of the unit open at each word's end
+  uint32_t* pbits = pcar + CAP / 32 + 1;  // parity bit at each unit start
+
+  const uint32_t x0 = batch_first[b], x1 = batch_first[b + 1];
+  if (x0 >= x1) return;
+  const uint32_t bstart = units[3 * x0];
+  const uint32_t E = units[3 * (x1 - 1) + 1] - bstart;
+  if (E > (uint32_t)CAP || (LT == LEAF_THREADS && E <= (uint32_t)LEAF_SMALL_CAP)) return;
+  const uint32_t nwords = (E + 31) / 32;
+  for (uint32_t w = threadIdx.x; w < nwords; w += NTH) { ubits[w] = 0u; pbits[w] = 0u; }
+  __syncthreads();
+  for (uint32_t x = x0 + threadIdx.x; x < x1; x += NTH) {
+    const uint32_t q = units[3 * x] - bstart;
+    atomicOr(&ubits[q >> 5], 1u << (q & 31u));
+    if (units[3 * x + 2]) atomicOr(&pbits[q >> 5], 1u << (q & 31u));
+  }
+  const uint32_t q0 = threadIdx.x * LEAF_K;
+  K rk[LEAF_K];
+#pragma unroll
+  for (int i = 0; i < LEAF_K; ++i) {
+    const uint32_t q = q0 + i;
+    rk[i] = q < E ? k0[bstart + q] : K(0);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // per-word prefix of unit starts; parity carried across words
+    uint32_t carry = 0, pc = 0;
+    for (uint32_t w0 = 0; w0 < nwords; w0 += 32) {
+      const uint32_t w = w0 + threadIdx.x;
+      const uint32_t ub = w < nwords ? ubits[w] : 0u;
+      const uint32_t c = (uint32_t)__popc(ub);
+      uint32_t incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if ((int)threadIdx.x >= o) incl += y;
+      }
+      if (w < nwords) upre[w] = carry + incl - c;
+      carry += __shfl_sync(0xFFFFFFFFu, incl, 31);
+      const int hb = ub ? 31 - __clz(ub) : -1;
+      const int own = hb >= 0 ? (int)((w < nwords ? pbits[w] : 0u) >> hb) & 1 : -1;
+      const uint32_t has = __ballot_sync(0xFFFFFFFFu, own >= 0);
+      const uint32_t le = has & (0xFFFFFFFFu >> (31 - threadIdx.x));
+      const int src = le ? 31 - __clz(le) : -1;
+      const int ownv = __shfl_sync(0xFFFFFFFFu, own, src >= 0 ? src : 0);
+      const uint32_t pw = src >= 0 ? (uint32_t)ownv : pc;
+      if (w < nwords) pcar[w] = pw;
+      pc = __shfl_sync(0xFFFFFFFFu, pw, 31);
+    }
+  }
+  __syncthreads();
+
+  // Phase 1: composites of the thread's chunk, stable rank sort, into buffer 0.
+  const uint32_t Ep = (E + LEAF_K - 1) / LEAF_K * LEAF_K;
+  if (q0 < E) {
+    uint32_t u;
+    {
+      const uint32_t w = q0 >> 5;
+      u = upre[w] + (uint32_t)__popc(ubits[w] & (0xFFFFFFFFu >> (31u - (q0 & 31u)))) - 1u;
+    }
+    uint64_t c[LEAF_K];
+#pragma unroll
+    for (int i = 0; i < LEAF_K; ++i) {
+      const uint32_t q = q0 + i;
+      if (i > 0 && q < E && ((ubits[q >> 5] >> (q & 31u)) & 1u)) ++u;
+      c[i] = q < E ? ((uint64_t)u << 45) | ((uint64_t)T::ord(rk[i]) << 13) | (uint64_t)q : SENT;
+    }
+    uint32_t rank[LEAF_K];
+#pragma unroll
+    for (int i = 0; i < LEAF_K; ++i) rank[i] = 0;
+#pragma unroll
+    for (int i = 0; i < LEAF_K; ++i) {
+#pragma unroll
+      for (int j = i + 1; j < LEAF_K; ++j) {
+        const bool ifirst = c[i] <= c[j];
+        rank[j] += ifirst ? 1u : 0u;
+        rank[i] += ifirst ? 0u : 1u;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < LEAF_K; ++i) scb[q0 + rank[i]] = c[i];
+  }
+  __syncthreads();
+
+  // Phase 2: merge rounds over [0, Ep) (ping-pong): pairs [x, x+w) + [x+w, x+2w).
+  uint32_t cur = 0;
+  for (uint32_t w = LEAF_K; w < E; w <<= 1) {
+    const uint64_t* sk = scb + cur * CAP;
+    uint64_t* dk = scb + (cur ^ 1u) * CAP;
+    if (q0 < Ep) {
+      const uint32_t x = (q0 / (2 * w)) * (2 * w), m = x + w;
+      if (m < Ep) {
+        const uint32_t hi = min(x + 2 * w, Ep), nB = hi - m, d = q0 - x;
+        uint32_t l = d > nB ? d - nB : 0u, h = min(d, w);
+        while (l < h) {
+          const uint32_t mid = (l + h) >> 1;
+          if (sk[x + mid] <= sk[m + d - mid - 1]) l = mid + 1;
+          else h = mid;
+        }
+        uint32_t ia = x + l, ib = m + d - l;  // absolute positions
+        uint64_t ka = sk[ia], kb = sk[ib];     // a read at hi stays inside shared memory, unused
+        uint64_t o[LEAF_K];
+#pragma unroll
+        for (int s2 = 0; s2 < LEAF_K; ++s2) {
+          const bool p = ib >= hi || (ia < m && ka <= kb);
+          o[s2] = p ? ka : kb;
+          ia += p ? 1u : 0u;
+          ib += p ? 0u : 1u;
+          const uint64_t nx = sk[p ? ia : ib];
+          ka = p ? nx : ka;
+          kb = p ? kb : nx;
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < LEAF_K; ++s2) dk[q0 + s2] = o[s2];
+      } else {  // no partner: copy
+#pragma unroll
+        for (int s2 = 0; s2 < LEAF_K; ++s2) dk[q0 + s2] = sk[q0 + s2];
+      }
+    }
+    cur ^= 1u;
+    // the next round's pairs stay inside one warp's range: warp-level sync
+    if (2 * (2 * w) <= 32 * LEAF_K) __syncwarp();
+    else __syncthreads();
+  }
+  __syncthreads();
+
+  // Phase 3: keys (u32: from the composite; f32: gathered, the order image of
+  // NaNs is not invertible) and payloads gathered by position (read all before
+  // writing: the gathers may be in place), each unit to its parity buffer.
+  const uint64_t* sk = scb + cur * CAP;
+  constexpr int PER = CAP / NTH;
+  K gk[PER];
+  uint32_t gv[PER];
+  constexpr bool GK = KT != VMPS_KEY_U32;
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const uint32_t q = threadIdx.x + r * NTH;
+    if (q < E) {
+      const uint64_t c = sk[q];
+      const uint32_t src = (uint32_t)c & 0x1FFFu;
+      gk[r] = GK ? k0[bstart + src] : (K)(uint32_t)(c >> 13);
+      if (HV) gv[r] = v0[bstart + src];
+    }
+  }
+  if (HV || GK) __syncthreads();
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const uint32_t q = threadIdx.x + r * NTH;
+    if (q < E) {
+      const uint32_t w = q >> 5;
+      const uint32_t mk = ubits[w] & (0xFFFFFFFFu >> (31u - (q & 31u)));
+      const uint32_t par = mk ? (pbits[w] >> (31 - __clz(mk))) & 1u : pcar[w - 1];
+      if (par) { k1[bstart + q] = gk[r]; if (HV) v1[bstart + q] = gv[r]; }
+      else { k0[bstart + q] = gk[r]; if (HV) v0[bstart + q] = gv[r]; }
+    }
+  }
+}
+
 // Persistent CTAs take batches from a work queue (atomic counter per size
 // class), so every resident CTA stays busy and no CTA is launched per empty
 // slot of the batch bound.
 template <int KT, bool HV, int LT>
-__global__ void __launch_bounds__(LT, VMPS_LEAF_MINB * (LEAF_THREADS / LT)) k_leaf_sort(
+__global__ void __launch_bounds__(LT, leaf_minb<KT>() * (LEAF_THREADS / LT)) k_leaf_sort(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
     const uint32_t* __restrict__ units, const uint32_t* __restrict__ batch_first, uint32_t* scalars) {
@@ -301,7 +496,8 @@ __global__ void __launch_bounds__(LT, VMPS_LEAF_MINB * (LEAF_THREADS / LT)) k_le
     __syncthreads();
     const uint32_t b = s_b;
     if (b >= nb) break;
-    leaf_sort_batch<KT, HV, LT>(k0, v0, k1, v1, units, batch_first, b);
+    if constexpr (leaf_composite<KT>()) leaf_sort_batch_c<KT, HV, LT>(k0, v0, k1, v1, units, batch_first, b);
+    else leaf_sort_batch<KT, HV, LT>(k0, v0, k1, v1, units, batch_first, b);
     __syncthreads();  // shared memory (and s_b) are reused by the next batch
   }
 }
@@ -311,6 +507,7 @@ inline size_t leaf_smem_bytes(bool hv) {
   using K = typename KeyTraits<KT>::K;
   (void)hv;
   constexpr int CAP = LT * LEAF_K;
+  if (leaf_composite<KT>()) return 2 * CAP * 8 + 4 * (CAP / 32 + 1) * 4 + 16;
   return 2 * CAP * (sizeof(K) + 2) + 4 * (CAP / 32 + 1) * 4 + 16;
 }
 
