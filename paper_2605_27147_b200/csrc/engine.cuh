@@ -408,11 +408,11 @@ __device__ __forceinline__ void leaf_sort_batch_c(
 
   // Phase 2: merge rounds over [0, Ep) (ping-pong): pairs [x, x+w) + [x+w, x+2w).
   uint32_t cur = 0;
-  for (uint32_t w = LEAF_K; w < E; w <<= 1) {
+  for (uint32_t w = LEAF_K, wc = 1; w < E; w <<= 1, wc <<= 1) {  // wc = w / LEAF_K chunks
     const uint64_t* sk = scb + cur * CAP;
     uint64_t* dk = scb + (cur ^ 1u) * CAP;
     if (q0 < Ep) {
-      const uint32_t x = (q0 / (2 * w)) * (2 * w), m = x + w;
+      const uint32_t x = (threadIdx.x & ~(2 * wc - 1)) * LEAF_K, m = x + w;  // pair start, no division
       if (m < Ep) {
         const uint32_t hi = min(x + 2 * w, Ep), nB = hi - m, d = q0 - x;
         uint32_t l = d > nB ? d - nB : 0u, h = min(d, w);
