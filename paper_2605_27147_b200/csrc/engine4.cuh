@@ -904,18 +904,27 @@ __global__ void __launch_bounds__(M4_THREADS, 2) k4_merge_level(
   if (tid >= NT) {  // producer warp
     const uint32_t plane = tid - NT;
     uint32_t it = 0;
+    // the next tile's descriptors (and its node) are loaded before the wait
+    // for its stage, so their latency overlaps the consumers' current tile
+    TileDesc4 d, dn;
+    NodeRuns R;
+    bool same = false;
+    auto fetch = [&](uint32_t t) {
+      d = tiles[t];
+      same = t + 1 < count && (dn = tiles[t + 1], dn.x == d.x);
+      R = nr[d.x];
+    };
+    if (plane == 0) fetch(blockIdx.x);
     for (uint32_t tau = blockIdx.x; tau < count; tau += gridDim.x, ++it) {
       const uint32_t s = it % SM::NSTG;
       if (plane == 0) {
         if (it >= SM::NSTG) mbar_wait_backoff(&empty[s], ((it / SM::NSTG) - 1) & 1u);
-        const TileDesc4 d = tiles[tau];
-        TileDesc4 dn;
-        const bool same = tau + 1 < count && (dn = tiles[tau + 1], dn.x == d.x);
-        merge4_issue<KT, HV>(d, same ? &dn : nullptr, nr[d.x], s, smem, full, hdr, k0, v0, k1, v1);
+        merge4_issue<KT, HV>(d, same ? &dn : nullptr, R, s, smem, full, hdr, k0, v0, k1, v1);
       }
       mbar_wait_backoff(&full[s], (it / SM::NSTG) & 1u);
       merge4_bnds<KT>(reinterpret_cast<const K*>(smem + SM::HDR + s * SM::STAGE), hdr + s, plane);
       mbar_arrive(&ready[s]);
+      if (plane == 0 && tau + gridDim.x < count) fetch(tau + gridDim.x);
     }
     return;
   }

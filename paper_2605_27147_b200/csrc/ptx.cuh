@@ -3,6 +3,10 @@
 #pragma once
 #include <stdint.h>
 
+#ifndef VMPS_BACKOFF_NS
+#define VMPS_BACKOFF_NS 200
+#endif
+
 namespace vmps {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -68,7 +72,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
         : "r"(addr), "r"(parity)
         : "memory");
     if (ok) return;
-    __nanosleep(200);
+    if (VMPS_BACKOFF_NS) __nanosleep(VMPS_BACKOFF_NS);
   }
 }
 
