@@ -301,6 +301,9 @@ __device__ __forceinline__ void leaf_sort_batch(
 #ifndef VMPS_LEAF_C
 #define VMPS_LEAF_C 1
 #endif
+#ifndef VMPS_LEAF_SKIP
+#define VMPS_LEAF_SKIP 1
+#endif
 template <int KT>
 __host__ __device__ constexpr bool leaf_composite() {
   return VMPS_LEAF_C && sizeof(typename KeyTraits<KT>::K) == 4;
@@ -413,7 +416,9 @@ __device__ __forceinline__ void leaf_sort_batch_c(
     uint64_t* dk = scb + (cur ^ 1u) * CAP;
     if (q0 < Ep) {
       const uint32_t x = (threadIdx.x & ~(2 * wc - 1)) * LEAF_K, m = x + w;  // pair start, no division
-      if (m < Ep) {
+      // a pair already in order (A's last <= B's first: presorted stretches)
+      // is its own merge: copy, no search
+      if (m < Ep && !(VMPS_LEAF_SKIP && sk[m - 1] <= sk[m])) {
         const uint32_t hi = min(x + 2 * w, Ep), nB = hi - m, d = q0 - x;
         uint32_t l = d > nB ? d - nB : 0u, h = min(d, w);
         while (l < h) {
@@ -436,7 +441,7 @@ __device__ __forceinline__ void leaf_sort_batch_c(
         }
 #pragma unroll
         for (int s2 = 0; s2 < LEAF_K; ++s2) dk[q0 + s2] = o[s2];
-      } else {  // no partner: copy
+      } else {  // no partner, or the pair is in order: copy
 #pragma unroll
         for (int s2 = 0; s2 < LEAF_K; ++s2) dk[q0 + s2] = sk[q0 + s2];
       }
