@@ -42,18 +42,33 @@ __global__ void k_powers_seg(const P* __restrict__ rs, uint64_t n, const uint32_
                              uint8_t* __restrict__ power, uint32_t* __restrict__ seg_l,
                              uint32_t* __restrict__ seg_r) {
   const uint32_t r = scalars[SC_RUNS];
+  const bool pow2 = (n & (n - 1)) == 0;
+  const uint32_t L2n = 64u - (uint32_t)__clzll((long long)(2 * n)) - 1u;  // log2(2n) when pow2
   for (uint32_t t = 1 + blockIdx.x * blockDim.x + threadIdx.x; t < r;
        t += gridDim.x * blockDim.x) {
-    uint64_t c;
-    uint32_t p = node_power(n, rs[t - 1], rs[t], rs[t + 1], &c);
+    uint64_t c, lo_thr, hi_thr;
+    uint32_t p;
+    if (pow2) {
+      // 2n = 2^L: a = A / 2^L exactly, so floor(a 2^p) = A >> (L - p) and the
+      // least p where A and B differ is L - h, h = the highest bit of A ^ B;
+      // the common prefix c = A >> (h + 1) and 2n / 2^q = 2^(h+1) (q = p - 1)
+      const uint64_t A = (uint64_t)rs[t - 1] + rs[t], B = (uint64_t)rs[t] + rs[t + 1];
+      const uint32_t h = 63u - (uint32_t)__clzll((long long)(A ^ B));
+      p = L2n - h;
+      c = A >> (h + 1);
+      lo_thr = c << (h + 1);
+      hi_thr = (c + 1) << (h + 1);
+    } else {
+      p = node_power(n, rs[t - 1], rs[t], rs[t + 1], &c);
+      const uint32_t q = p - 1;
+      // s_u 2^q >= c 2n  <=>  s_u >= ceil(c 2n / 2^q), with s_u = rs[u] + rs[u+1]
+      // (both thresholds < 2^34: c < 2^q); the loops compare 64-bit sums only
+      const u128 N2 = (u128)(2ull * n);
+      const u128 one = 1;
+      lo_thr = (uint64_t)(((u128)c * N2 + (one << q) - 1) >> q);
+      hi_thr = (uint64_t)(((u128)(c + 1) * N2 + (one << q) - 1) >> q);
+    }
     power[t] = (uint8_t)p;
-    const uint32_t q = p - 1;
-    // s_u 2^q >= c 2n  <=>  s_u >= ceil(c 2n / 2^q), with s_u = rs[u] + rs[u+1]
-    // (both thresholds < 2^34: c < 2^q); the loops compare 64-bit sums only
-    const u128 N2 = (u128)(2ull * n);
-    const u128 one = 1;
-    const uint64_t lo_thr = (uint64_t)(((u128)c * N2 + (one << q) - 1) >> q);
-    const uint64_t hi_thr = (uint64_t)(((u128)(c + 1) * N2 + (one << q) - 1) >> q);
     auto mid_scaled = [&](uint32_t u) -> uint64_t { return (uint64_t)rs[u] + (uint64_t)rs[u + 1]; };
     // L = smallest u in [0, t-1] with mid(u) 2^q >= c 2n (run t-1 qualifies)
     int64_t good = (int64_t)t - 1, bad = -1;
