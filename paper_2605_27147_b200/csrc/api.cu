@@ -92,6 +92,9 @@ static uint32_t leaf_zb(uint32_t fuse_z, bool bounded) {
   return (small ? (uint32_t)LEAF_SMALL_CAP : (uint32_t)LEAF_CAP) - fuse_z + 1;
 }
 
+#ifndef VMPS_SCAN1
+#define VMPS_SCAN1 1
+#endif
 static size_t scan_tmp_words(size_t len) {
   size_t nb = (len + SCAN_TILE - 1) / SCAN_TILE;
   if (nb <= 1) return 2;
@@ -308,6 +311,14 @@ static unsigned grid_for(size_t items, unsigned threads = 256) {
 
 // Exclusive scan of len u32 (out[len-1] meaningful); tmp from scan_tmp_words.
 static void scan_u32(const uint32_t* in, uint32_t* out, uint32_t len, uint32_t* tmp, cudaStream_t s) {
+  if (VMPS_SCAN1 && len > 0) {  // single pass; the tile status words fit in tmp (len / 2048 + 2 words)
+    const uint32_t nt = (len + SCAN1_TILE - 1) / SCAN1_TILE;
+    unsigned long long* st = reinterpret_cast<unsigned long long*>(((uintptr_t)tmp + 7) & ~(uintptr_t)7);
+    cudaMemsetAsync(st, 0, (size_t)nt * 8, s);
+    k_scan1<<<nt, SCAN1_THREADS, 0, s>>>(in, out, len, st);
+    ++g_nl;
+    return;
+  }
   uint32_t nb = (len + SCAN_TILE - 1) / SCAN_TILE;
   k_scan_tiles<<<nb, SCAN_THREADS, 0, s>>>(in, out, len, tmp);
   ++g_nl;

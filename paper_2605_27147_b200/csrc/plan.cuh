@@ -466,4 +466,98 @@ __global__ void k_scan_add(uint32_t* __restrict__ out, uint32_t len, const uint3
     if (base + q < len) out[base + q] += add;
 }
 
+
+// Single-pass exclusive scan (decoupled look-back): a CTA scans its tile of
+// SCAN1_TILE values (128-bit loads / stores), publishes its aggregate, then
+// warp 0 sums its predecessors' published values 32 at a time until it meets
+// an inclusive prefix, and publishes its own.  Status word per tile:
+// bit 32 = aggregate, bit 33 = inclusive prefix, low 32 bits the value
+// (zeroed before the launch).  A CTA waits only on lower-numbered tiles,
+// which are dispatched before it.  One read and one write of the array,
+// against four passes and a recursion for k_scan_tiles / k_scan_add.
+constexpr int SCAN1_THREADS = 256;
+constexpr int SCAN1_ITEMS = 16;
+constexpr int SCAN1_TILE = SCAN1_THREADS * SCAN1_ITEMS;
+
+__global__ void __launch_bounds__(SCAN1_THREADS) k_scan1(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                         uint32_t len, unsigned long long* status) {
+  __shared__ uint32_t wsum[SCAN1_THREADS / 32];
+  __shared__ uint32_t s_prefix;
+  const uint32_t tile = blockIdx.x;
+  const uint32_t base = tile * SCAN1_TILE + threadIdx.x * SCAN1_ITEMS;
+  const bool vec = base + SCAN1_ITEMS <= len && ((((uintptr_t)in) | ((uintptr_t)out)) & 15u) == 0;
+  uint32_t v[SCAN1_ITEMS], s = 0;
+  if (vec) {
+    const uint4* src = reinterpret_cast<const uint4*>(in + base);
+#pragma unroll
+    for (int q = 0; q < SCAN1_ITEMS / 4; ++q) {
+      const uint4 x = src[q];
+      v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < SCAN1_ITEMS; ++q) v[q] = base + q < len ? in[base + q] : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < SCAN1_ITEMS; ++q) s += v[q];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = lane < SCAN1_THREADS / 32 ? wsum[lane] : 0u;
+    uint32_t wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < SCAN1_THREADS / 32) wsum[lane] = wi - w;
+    const uint32_t total = __shfl_sync(0xFFFFFFFFu, wi, SCAN1_THREADS / 32 - 1);
+    volatile unsigned long long* st = status;
+    uint32_t prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st[0] = (2ull << 32) | total;
+    } else {
+      if (lane == 0) st[tile] = (1ull << 32) | total;
+      for (int32_t j = (int32_t)tile - 1 - lane;; j -= 32) {
+        unsigned long long x = 2ull << 32;  // before tile 0: an empty inclusive prefix
+        if (j >= 0)
+          do { x = st[j]; } while ((x >> 32) == 0);
+        const uint32_t isp = __ballot_sync(0xFFFFFFFFu, (x >> 32) & 2u);
+        const int stop = isp ? __ffs(isp) - 1 : 32;  // nearest predecessor with a prefix
+        uint32_t val = lane <= stop ? (uint32_t)x : 0u;
+        for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(0xFFFFFFFFu, val, o);
+        prefix += val;
+        if (isp) break;
+      }
+      if (lane == 0) st[tile] = (2ull << 32) | (uint32_t)(prefix + total);
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  uint32_t run = s_prefix + wsum[warp] + incl - s;
+  if (vec) {
+    uint4* dst = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+    for (int q = 0; q < SCAN1_ITEMS / 4; ++q) {
+      uint4 y;
+      y.x = run; run += v[4 * q];
+      y.y = run; run += v[4 * q + 1];
+      y.z = run; run += v[4 * q + 2];
+      y.w = run; run += v[4 * q + 3];
+      dst[q] = y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < SCAN1_ITEMS; ++q) {
+      if (base + q < len) out[base + q] = run;
+      run += v[q];
+    }
+  }
+}
+
 }  // namespace vmps

@@ -7,4 +7,4 @@ for it in 1 2; do for v in $VARIANTS; do
   echo -n "$v " >> $R/m4v.log
   VMPS_LIB=$PWD/paper_2605_27147_b200/libvmps_$v.so timeout 300 $B 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(json.dumps({'ms': round(d['ms_per_step'],2), **{k: round(v,2) for k,v in d['phases_ms'].items()}, 'ok': d['verified']}))" >> $R/m4v.log
 done; done
-bash scripts/gpu_merge_ncu.sh
+[ -n "$NO_NCU" ] || bash scripts/gpu_merge_ncu.sh
