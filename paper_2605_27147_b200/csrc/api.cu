@@ -1073,7 +1073,7 @@ extern "C" {
 #define VMPS_BD_CHUNK (1u << 23)
 #endif
 #ifndef VMPS_BD_DET
-#define VMPS_BD_DET (1u << 22)  // run-detection chunk of the dyadic-cell mode (elements)
+#define VMPS_BD_DET (1u << 23)  // run-detection chunk of the dyadic-cell mode (elements)
 #endif
 static uint64_t g_bd_chunk = VMPS_BD_CHUNK;  // cell size target (test hook vmps_test_set_bd_chunk)
 static bool bd_chunked(uint64_t n, int64_t scratch, int hv) { return scratch >= 0 && hv >= 0 && n > 2 * g_bd_chunk; }
@@ -1114,8 +1114,10 @@ static size_t carve_gt(const Cfg& c, uint32_t rcell, char* base, BdCtx* C) {
   t.didx = (uint32_t*)take(NBp * 4);
   t.dlist = (uint32_t*)take(NBp * 4);
   t.first_tile = (uint32_t*)take(NBp * 4);
-  // a level of a cell: its blocks plus gap tiles at node ends (nodes <= runs / 2)
-  t.bdesc_cap = t.NB + 2 * rcell + 16;
+  // a level's tiles: the nodes of one power are disjoint and hold >= 2 runs
+  // each (<= rcell / 2 nodes); a node spans its blocks (+1 shared with a
+  // neighbour) plus <= 2 gap tiles: <= NB + 1.5 rcell
+  t.bdesc_cap = t.NB + rcell + rcell / 2 + 16;
   t.bdesc = take((size_t)t.bdesc_cap * sizeof(BdTile));
   t.bstate = take(sizeof(BdState));
   t.cplists = (uint32_t*)take((size_t)2 * BD_CP_LIST * 4);
