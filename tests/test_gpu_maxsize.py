@@ -4,7 +4,8 @@ past 2^31 (where a signed 32-bit position would overflow), checked by exact
 properties that determine a stable sort uniquely at any size: keys
 non-decreasing under the key order, the payload (= input position) a
 permutation, increasing within every run of equal keys; for keys only,
-non-decreasing plus an unchanged multiset fingerprint.  Inputs mix unsorted,
+non-decreasing plus an unchanged multiset fingerprint (high-16-bit
+histogram and a nonlinear mix sum).  Inputs mix unsorted,
 sorted and strictly descending segments (every run kind) and are built chunk
 by chunk on the device."""
 import numpy as np
@@ -71,18 +72,34 @@ def test_sort_pairs_past_2_31():
     del k, v, k0, seen
 
 
+def _fingerprint(k, C=1 << 27):
+    """Multiset fingerprint: the 65,536-bin histogram of the keys' high 16 bits
+    plus a wrapped int64 sum of a nonlinear mix of every key -- a dropped,
+    duplicated or altered key changes one of them (w.h.p. for the mix)."""
+    n = k.numel()
+    hist = torch.zeros(1 << 16, dtype=torch.int64, device=k.device)
+    mix = torch.zeros((), dtype=torch.int64, device=k.device)
+    for a in range(0, n, C):
+        x = _img(k[a:min(n, a + C)])
+        hist += torch.bincount(x >> 16, minlength=1 << 16)
+        y = (x * 40503) ^ (x >> 7)
+        y = y * 2654435761 + (y >> 13) * 97
+        mix += y.sum()
+    return hist, int(mix.item())
+
+
 def test_sort_keys_max_n():
     import paper_2605_27147_b200 as vm
     dev = torch.device("cuda")
     n = (1 << 32) - (1 << 16)  # VMPS_MAX_N
     k = _fill(n, 32, dev)
-    f0 = (_img(k[: n // 2]).sum().item(), _img(k[n // 2:]).sum().item())
+    h0, m0 = _fingerprint(k)
     vm.sort_(k)
     torch.cuda.synchronize()
     _check_sorted(k)
-    total0 = f0[0] + f0[1]
-    total1 = _img(k[: n // 2]).sum().item() + _img(k[n // 2:]).sum().item()
-    assert total0 == total1, "multiset changed"
+    h1, m1 = _fingerprint(k)
+    assert bool(torch.equal(h0, h1)), "multiset changed (high-16-bit histogram)"
+    assert m0 == m1, "multiset changed (mix sum)"
     del k
 
 
