@@ -454,33 +454,35 @@ __device__ __forceinline__ void leaf_sort_batch_c(
   __syncthreads();
 
   // Phase 3: keys (u32: from the composite; f32: gathered, the order image of
-  // NaNs is not invertible) and payloads gathered by position (read all before
-  // writing: the gathers may be in place), each unit to its parity buffer.
+  // NaNs is not invertible) and payloads gathered by position, each unit to
+  // its parity buffer.  The batch's payloads (and f32 keys) are first read
+  // coalesced into the free ping-pong buffer -- all global reads precede the
+  // barrier, so the in-place writes below cannot overtake them -- and
+  // gathered from shared memory.
   const uint64_t* sk = scb + cur * CAP;
   constexpr int PER = CAP / NTH;
-  K gk[PER];
-  uint32_t gv[PER];
   constexpr bool GK = KT != VMPS_KEY_U32;
+  uint32_t* sv = reinterpret_cast<uint32_t*>(scb + (cur ^ 1u) * CAP);  // 2 CAP words: values, then f32 keys
+  if (HV || GK) {
+    for (uint32_t q = threadIdx.x; q < E; q += NTH) {
+      if (HV) sv[q] = v0[bstart + q];
+      if (GK) sv[CAP + q] = (uint32_t)k0[bstart + q];
+    }
+    __syncthreads();
+  }
 #pragma unroll
   for (int r = 0; r < PER; ++r) {
     const uint32_t q = threadIdx.x + r * NTH;
     if (q < E) {
       const uint64_t c = sk[q];
       const uint32_t src = (uint32_t)c & 0x1FFFu;
-      gk[r] = GK ? k0[bstart + src] : (K)(uint32_t)(c >> 13);
-      if (HV) gv[r] = v0[bstart + src];
-    }
-  }
-  if (HV || GK) __syncthreads();
-#pragma unroll
-  for (int r = 0; r < PER; ++r) {
-    const uint32_t q = threadIdx.x + r * NTH;
-    if (q < E) {
+      const K gk = GK ? (K)sv[CAP + src] : (K)(uint32_t)(c >> 13);
+      const uint32_t gv = HV ? sv[src] : 0u;
       const uint32_t w = q >> 5;
       const uint32_t mk = ubits[w] & (0xFFFFFFFFu >> (31u - (q & 31u)));
       const uint32_t par = mk ? (pbits[w] >> (31 - __clz(mk))) & 1u : pcar[w - 1];
-      if (par) { k1[bstart + q] = gk[r]; if (HV) v1[bstart + q] = gv[r]; }
-      else { k0[bstart + q] = gk[r]; if (HV) v0[bstart + q] = gv[r]; }
+      if (par) { k1[bstart + q] = gk; if (HV) v1[bstart + q] = gv; }
+      else { k0[bstart + q] = gk; if (HV) v0[bstart + q] = gv; }
     }
   }
 }
