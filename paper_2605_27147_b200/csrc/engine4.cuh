@@ -173,6 +173,22 @@ __device__ __forceinline__ void co_pair(const InnerCR<KT>& L, uint32_t x, const 
 // which narrows the outer search in two evaluations when the estimate holds
 // (consecutive tiles of a node split alike) and costs two when it does not.
 constexpr uint32_t HINT_W = 96;
+#ifndef VMPS_DESC4_INTERP
+#define VMPS_DESC4_INTERP 1
+#endif
+constexpr bool DESC4_INTERP = VMPS_DESC4_INTERP;  // regula falsi steps in the outer search
+// The gap a - b the regula falsi interpolates: integer keys by value; f32 by
+// the float values (their order images are not linear in the value), NaN
+// (no interpolation) when either is not finite.
+template <int KT>
+__device__ __forceinline__ double interp_gap(typename KeyTraits<KT>::K a, typename KeyTraits<KT>::K b) {
+  if constexpr (KT == VMPS_KEY_F32) {
+    const float fa = __uint_as_float(a), fb = __uint_as_float(b);
+    return (isfinite(fa) && isfinite(fb)) ? (double)fa - (double)fb : (double)NAN;
+  } else {
+    return (double)a - (double)b;
+  }
+}
 template <int KT>
 __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint32_t d, uint32_t alo,
                                             uint32_t ahi, uint32_t* c, uint32_t hint = 0xFFFFFFFFu,
@@ -186,26 +202,53 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
   alo = max(alo, d > nR ? d - nR : 0u);
   ahi = min(ahi, min(d, nL));
   int hint_left = hint != 0xFFFFFFFFu && ahi - alo > 4 * hw ? 2 : 0;
+  // Illinois regula falsi on g(m) = L[m] - R[d-m-1] (order images; g <= 0
+  // below the answer, > 0 from it): once both bracket ends carry a value, the
+  // next probe is the interpolated zero crossing, the end that stays put
+  // twice has its value halved, and a step that does not halve the bracket
+  // is followed by a bisection step.  The bracket invariant is the same as
+  // bisection's, so the answer is exact whatever the keys; on i.i.d. keys g
+  // is near linear and a few outer evaluations replace ~10.
+  double glo = 0.0, ghi = 0.0;
+  bool klo = false, khi = false, bis = false;
+  int side = 0;
   while (alo < ahi) {
     uint32_t mid = (alo + ahi) >> 1;
+    const uint32_t w0 = ahi - alo;
+    bool interp = false;
     if (hint_left) {  // the probes around the hint (kept inside [alo, ahi))
       const uint32_t p = hint_left == 2 ? (hint > alo + hw ? hint - hw : alo)
                                         : (hint + hw < ahi ? hint + hw : ahi - 1);
       mid = min(max(p, alo), ahi - 1);
       --hint_left;
+    } else if (DESC4_INTERP && klo && khi && !bis && ghi > glo && !isnan(glo) && !isnan(ghi)) {
+      const double t = -glo / (ghi - glo);  // in [0, 1]
+      const double x = (double)alo - 1.0 + t * (double)(w0 + 1);
+      mid = x <= (double)alo ? alo : x >= (double)(ahi - 1) ? ahi - 1 : (uint32_t)x;
+      interp = true;
     }
     const uint32_t r = d - mid - 1;  // < nR since mid >= d - nR
     uint32_t cL, cR;
     co_pair<KT>(L, mid, R, r, &cL, &cR);
-    if (T::ord(L.elem(mid, cL)) <= T::ord(R.elem(r, cR))) {  // L[mid] precedes R[d-mid-1]
+    const auto kL = L.elem(mid, cL), kR = R.elem(r, cR);
+    const auto oL = T::ord(kL), oR = T::ord(kR);
+    const double g = interp_gap<KT>(kL, kR);
+    if (oL <= oR) {  // L[mid] precedes R[d-mid-1]
       alo = mid + 1;
       L.know_low(mid, cL);
       R.know_high(r, cR);
+      glo = g; klo = true;
+      if (side == 1) ghi *= 0.5;
+      side = 1;
     } else {
       ahi = mid;
       L.know_high(mid, cL);
       R.know_low(r, cR);
+      ghi = g; khi = true;
+      if (side == 2) glo *= 0.5;
+      side = 2;
     }
+    bis = interp && 2 * (ahi - alo) > w0;
   }
   const uint32_t a = alo;
   uint32_t c0, c2;
