@@ -143,8 +143,70 @@ struct InnerCR {
   }
 };
 
+#ifndef VMPS_DESC4_INTERP
+#define VMPS_DESC4_INTERP 1
+#endif
+constexpr bool DESC4_INTERP = VMPS_DESC4_INTERP;  // regula falsi steps in the outer search
+// The gap a - b the regula falsi interpolates: integer keys by value; f32 by
+// the float values (their order images are not linear in the value), NaN
+// (no interpolation) when either is not finite.
+template <int KT>
+__device__ __forceinline__ double interp_gap(typename KeyTraits<KT>::K a, typename KeyTraits<KT>::K b) {
+  if constexpr (KT == VMPS_KEY_F32) {
+    const float fa = __uint_as_float(a), fb = __uint_as_float(b);
+    return (isfinite(fa) && isfinite(fb)) ? (double)fa - (double)fb : (double)NAN;
+  } else {
+    return (double)a - (double)b;
+  }
+}
+
+// Illinois regula falsi for a bracketed search of the first m in [lo, hi]
+// with g(m) > 0 (g non-decreasing; here g(m) = A[m] - B[x-m-1] on a merge
+// diagonal): once both bracket ends carry a g value the probe is the
+// interpolated zero crossing, the end that stays put twice has its value
+// halved, and a step that does not halve the bracket is followed by a
+// bisection step.  The bracket invariant is bisection's, so the result is
+// exact whatever the keys; on i.i.d. keys g is near linear and a few probes
+// replace log2(hi - lo).
+struct RFalsi {
+  double glo, ghi;
+  bool klo, khi, bis;
+  int side;
+  __device__ __forceinline__ void init() {
+    glo = ghi = 0.0;
+    klo = khi = bis = false;
+    side = 0;
+  }
+  __device__ __forceinline__ uint32_t probe(uint32_t lo, uint32_t hi, bool* interp) const {
+    *interp = false;
+    if (klo && khi && !bis && ghi > glo && !isnan(glo) && !isnan(ghi)) {
+      const double t = -glo / (ghi - glo);  // in [0, 1]
+      const double x = (double)lo - 1.0 + t * (double)(hi - lo + 1);
+      *interp = true;
+      return x <= (double)lo ? lo : x >= (double)(hi - 1) ? hi - 1 : (uint32_t)x;
+    }
+    return (lo + hi) >> 1;
+  }
+  // p: g(m) <= 0 at the probe m; w0 / w1 the bracket widths before / after
+  __device__ __forceinline__ void update(bool p, double g, uint32_t w0, uint32_t w1, bool interp) {
+    if (p) {
+      glo = g; klo = true;
+      if (side == 1) ghi *= 0.5;
+      side = 1;
+    } else {
+      ghi = g; khi = true;
+      if (side == 2) glo *= 0.5;
+      side = 2;
+    }
+    bis = interp && 2 * w1 > w0;
+  }
+};
+
 // co(x) of L and co(y) of R as one interleaved loop: the two binary searches
 // are independent, so their probes overlap (half the dependent latency).
+// (Regula falsi here too measured slower: cfg5 partition 5.0 -> 8.1 ms --
+// the known points already bracket these searches tightly, and the two
+// bisection probes it needs first plus the extra registers cost more.)
 template <int KT>
 __device__ __forceinline__ void co_pair(const InnerCR<KT>& L, uint32_t x, const InnerCR<KT>& R, uint32_t y,
                                         uint32_t* cx, uint32_t* cy) {
@@ -172,23 +234,10 @@ __device__ __forceinline__ void co_pair(const InnerCR<KT>& L, uint32_t x, const 
 // two probes then bracket [hint - HINT_W, hint + HINT_W] instead of halving,
 // which narrows the outer search in two evaluations when the estimate holds
 // (consecutive tiles of a node split alike) and costs two when it does not.
-constexpr uint32_t HINT_W = 96;
-#ifndef VMPS_DESC4_INTERP
-#define VMPS_DESC4_INTERP 1
+#ifndef VMPS_HINT_W
+#define VMPS_HINT_W 96
 #endif
-constexpr bool DESC4_INTERP = VMPS_DESC4_INTERP;  // regula falsi steps in the outer search
-// The gap a - b the regula falsi interpolates: integer keys by value; f32 by
-// the float values (their order images are not linear in the value), NaN
-// (no interpolation) when either is not finite.
-template <int KT>
-__device__ __forceinline__ double interp_gap(typename KeyTraits<KT>::K a, typename KeyTraits<KT>::K b) {
-  if constexpr (KT == VMPS_KEY_F32) {
-    const float fa = __uint_as_float(a), fb = __uint_as_float(b);
-    return (isfinite(fa) && isfinite(fb)) ? (double)fa - (double)fb : (double)NAN;
-  } else {
-    return (double)a - (double)b;
-  }
-}
+constexpr uint32_t HINT_W = VMPS_HINT_W;
 template <int KT>
 __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint32_t d, uint32_t alo,
                                             uint32_t ahi, uint32_t* c, uint32_t hint = 0xFFFFFFFFu,
@@ -202,16 +251,10 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
   alo = max(alo, d > nR ? d - nR : 0u);
   ahi = min(ahi, min(d, nL));
   int hint_left = hint != 0xFFFFFFFFu && ahi - alo > 4 * hw ? 2 : 0;
-  // Illinois regula falsi on g(m) = L[m] - R[d-m-1] (order images; g <= 0
-  // below the answer, > 0 from it): once both bracket ends carry a value, the
-  // next probe is the interpolated zero crossing, the end that stays put
-  // twice has its value halved, and a step that does not halve the bracket
-  // is followed by a bisection step.  The bracket invariant is the same as
-  // bisection's, so the answer is exact whatever the keys; on i.i.d. keys g
-  // is near linear and a few outer evaluations replace ~10.
-  double glo = 0.0, ghi = 0.0;
-  bool klo = false, khi = false, bis = false;
-  int side = 0;
+  // Illinois regula falsi (RFalsi) on g(m) = L[m] - R[d-m-1], g <= 0 below
+  // the answer: on i.i.d. keys a few outer evaluations replace ~10
+  RFalsi rf;
+  rf.init();
   while (alo < ahi) {
     uint32_t mid = (alo + ahi) >> 1;
     const uint32_t w0 = ahi - alo;
@@ -221,11 +264,8 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
                                         : (hint + hw < ahi ? hint + hw : ahi - 1);
       mid = min(max(p, alo), ahi - 1);
       --hint_left;
-    } else if (DESC4_INTERP && klo && khi && !bis && ghi > glo && !isnan(glo) && !isnan(ghi)) {
-      const double t = -glo / (ghi - glo);  // in [0, 1]
-      const double x = (double)alo - 1.0 + t * (double)(w0 + 1);
-      mid = x <= (double)alo ? alo : x >= (double)(ahi - 1) ? ahi - 1 : (uint32_t)x;
-      interp = true;
+    } else if (DESC4_INTERP) {
+      mid = rf.probe(alo, ahi, &interp);
     }
     const uint32_t r = d - mid - 1;  // < nR since mid >= d - nR
     uint32_t cL, cR;
@@ -237,18 +277,12 @@ __device__ __forceinline__ uint32_t corank4(InnerCR<KT>& L, InnerCR<KT>& R, uint
       alo = mid + 1;
       L.know_low(mid, cL);
       R.know_high(r, cR);
-      glo = g; klo = true;
-      if (side == 1) ghi *= 0.5;
-      side = 1;
     } else {
       ahi = mid;
       L.know_high(mid, cL);
       R.know_low(r, cR);
-      ghi = g; khi = true;
-      if (side == 2) glo *= 0.5;
-      side = 2;
     }
-    bis = interp && 2 * (ahi - alo) > w0;
+    rf.update(oL <= oR, g, w0, ahi - alo, interp);
   }
   const uint32_t a = alo;
   uint32_t c0, c2;
@@ -317,7 +351,7 @@ __device__ __forceinline__ uint32_t corank4_warp(InnerCR<KT>& L, InnerCR<KT>& R,
 // boundary of a chunk is a full search, the next ones search a in
 // [a_prev, a_prev + T].
 #ifndef VMPS_DESC4_CHUNK
-#define VMPS_DESC4_CHUNK 10
+#define VMPS_DESC4_CHUNK 6
 #endif
 constexpr uint32_t DESC4_CHUNK = VMPS_DESC4_CHUNK;
 #ifndef VMPS_DESC4_HINT
