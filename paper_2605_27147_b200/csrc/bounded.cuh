@@ -163,17 +163,35 @@ __device__ __forceinline__ typename KeyTraits<KT>::K bd_key(const BdMem<KT>& M, 
   return M.kb(Tin[q >> M.lg])[q & (M.P - 1)];
 }
 
+#ifndef VMPS_BD_RF
+#define VMPS_BD_RF 1
+#endif
 template <int KT>
 __device__ uint32_t bd_corank(const BdMem<KT>& M, const uint32_t* Tin, uint32_t ai, uint32_t nA, uint32_t bi,
                               uint32_t nB, uint32_t d) {
   using T = KeyTraits<KT>;
   uint32_t lo = d > nB ? d - nB : 0u, hi = min(d, nA);
-  while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if (T::ord(bd_key<KT>(M, Tin, ai + mid)) <= T::ord(bd_key<KT>(M, Tin, bi + d - mid - 1))) lo = mid + 1;
-    else hi = mid;
+  if constexpr (VMPS_BD_RF) {  // regula falsi steps (RFalsi, engine4.cuh): exact, fewer dependent probes
+    RFalsi rf;
+    rf.init();
+    while (lo < hi) {
+      bool interp;
+      const uint32_t mid = rf.probe(lo, hi, &interp), w0 = hi - lo;
+      const auto a = bd_key<KT>(M, Tin, ai + mid), b = bd_key<KT>(M, Tin, bi + d - mid - 1);
+      const bool p = T::ord(a) <= T::ord(b);
+      if (p) lo = mid + 1;
+      else hi = mid;
+      rf.update(p, interp_gap<KT>(a, b), w0, hi - lo, interp);
+    }
+    return lo;
+  } else {
+    while (lo < hi) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (T::ord(bd_key<KT>(M, Tin, ai + mid)) <= T::ord(bd_key<KT>(M, Tin, bi + d - mid - 1))) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
   }
-  return lo;
 }
 
 // A tile of a bounded level pass: output positions [lo, hi) of the node

@@ -33,6 +33,61 @@ static_assert(LEAF_CAP >= 2 * (int)MAX_FUSE_Z - 1, "leaf capacity");
 constexpr int LEAF_SMALL = LEAF_THREADS / 2;          // half-size CTA for small batches
 constexpr int LEAF_SMALL_CAP = LEAF_SMALL * LEAF_K;   // 2112 >= Z: any single unit fits
 
+// The gap a - b the regula falsi interpolates: integer keys by value; f32 by
+// the float values (their order images are not linear in the value), NaN
+// (no interpolation) when either is not finite.
+template <int KT>
+__device__ __forceinline__ double interp_gap(typename KeyTraits<KT>::K a, typename KeyTraits<KT>::K b) {
+  if constexpr (KT == VMPS_KEY_F32) {
+    const float fa = __uint_as_float(a), fb = __uint_as_float(b);
+    return (isfinite(fa) && isfinite(fb)) ? (double)fa - (double)fb : (double)NAN;
+  } else {
+    return (double)a - (double)b;
+  }
+}
+
+// Illinois regula falsi for a bracketed search of the first m in [lo, hi]
+// with g(m) > 0 (g non-decreasing; here g(m) = A[m] - B[x-m-1] on a merge
+// diagonal): once both bracket ends carry a g value the probe is the
+// interpolated zero crossing, the end that stays put twice has its value
+// halved, and a step that does not halve the bracket is followed by a
+// bisection step.  The bracket invariant is bisection's, so the result is
+// exact whatever the keys; on i.i.d. keys g is near linear and a few probes
+// replace log2(hi - lo).
+struct RFalsi {
+  double glo, ghi;
+  bool klo, khi, bis;
+  int side;
+  __device__ __forceinline__ void init() {
+    glo = ghi = 0.0;
+    klo = khi = bis = false;
+    side = 0;
+  }
+  __device__ __forceinline__ uint32_t probe(uint32_t lo, uint32_t hi, bool* interp) const {
+    *interp = false;
+    if (klo && khi && !bis && ghi > glo && !isnan(glo) && !isnan(ghi)) {
+      const double t = -glo / (ghi - glo);  // in [0, 1]
+      const double x = (double)lo - 1.0 + t * (double)(hi - lo + 1);
+      *interp = true;
+      return x <= (double)lo ? lo : x >= (double)(hi - 1) ? hi - 1 : (uint32_t)x;
+    }
+    return (lo + hi) >> 1;
+  }
+  // p: g(m) <= 0 at the probe m; w0 / w1 the bracket widths before / after
+  __device__ __forceinline__ void update(bool p, double g, uint32_t w0, uint32_t w1, bool interp) {
+    if (p) {
+      glo = g; klo = true;
+      if (side == 1) ghi *= 0.5;
+      side = 1;
+    } else {
+      ghi = g; khi = true;
+      if (side == 2) glo *= 0.5;
+      side = 2;
+    }
+    bis = interp && 2 * w1 > w0;
+  }
+};
+
 template <int KT>
 __device__ __forceinline__ uint32_t corank(const typename KeyTraits<KT>::K* A, uint32_t nA,
                                            const typename KeyTraits<KT>::K* B, uint32_t nB,
