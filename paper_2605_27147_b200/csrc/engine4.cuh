@@ -300,7 +300,7 @@ __device__ __forceinline__ uint32_t corank4_warp(InnerCR<KT>& L, InnerCR<KT>& R,
 #endif
 constexpr uint32_t DESC4_CHUNK = VMPS_DESC4_CHUNK;
 #ifndef VMPS_DESC4_HINT
-#define VMPS_DESC4_HINT 1
+#define VMPS_DESC4_HINT 2
 #endif
 #ifndef VMPS_DESC4_SERIAL_MIN
 #define VMPS_DESC4_SERIAL_MIN 65536
@@ -363,7 +363,10 @@ __global__ void __launch_bounds__(256) k4_desc(const typename KeyTraits<KT>::K* 
                                 : 0xFFFFFFFFu;
       uint32_t h = VMPS_DESC4_HINT ? hint : 0xFFFFFFFFu, hw = HINT_W;
 #if VMPS_DESC4_HINT >= 2
-      if (h == 0xFFFFFFFFu && d > 0) {  // first tile of the node in this chunk: L's share of the node
+      // first tile of the node in this chunk: L's share of the node, +- 2 sqrt(d)
+      // (with the regula falsi steps after the two hint probes this helps
+      // structured inputs too: cfg4 6.95 -> 6.53 ms, cfg5 partition 4.75 -> 4.55)
+      if (h == 0xFFFFFFFFu && d > 0) {
         const uint32_t nL = (X.b[2] - X.b[0]), nX = X.b[4] - X.b[0];
         h = (uint32_t)(((uint64_t)d * nL) / nX);
         hw = max(HINT_W, 2u * (uint32_t)sqrtf((float)d));
