@@ -251,17 +251,36 @@ __device__ __forceinline__ uint32_t corank4_warp(InnerCR<KT>& L, InnerCR<KT>& R,
   using T = KeyTraits<KT>;
   const uint32_t nL = L.nA + L.nB, nR = R.nA + R.nB;
   uint32_t alo = d > nR ? d - nR : 0u, ahi = min(d, nL);
+  // g = L[m] - R[d-m-1] at alo - 1 and at ahi once known (warp-uniform): a
+  // round after the first spreads its candidates over a window of 1/32 of
+  // the bracket around the interpolated crossing (regula falsi, as in
+  // corank4), so a hit narrows the bracket ~1000x; a miss (all candidates on
+  // one side) is followed by a uniform round
+  double gT = (double)NAN, gF = (double)NAN;
+  bool missed = false;
   while (alo < ahi) {
-    const uint32_t w = ahi - alo;
-    // candidates m_l strictly increasing in [alo, ahi) (lanes past the range idle)
+    uint32_t wl = alo, w = ahi - alo;
+    bool win = false;
+    if (DESC4_INTERP && w >= 256u && !missed && !isnan(gT) && !isnan(gF) && gF > gT) {
+      const double x = (double)alo - 1.0 + (-gT / (gF - gT)) * (double)(w + 1);
+      const uint32_t cx = x <= (double)alo ? alo : x >= (double)(ahi - 1) ? ahi - 1 : (uint32_t)x;
+      const uint32_t half = max(16u, w >> 6);
+      wl = cx > alo + half ? cx - half : alo;
+      w = min(ahi, cx + half + 1) - wl;
+      win = true;
+    }
+    // candidates m_l strictly increasing in [wl, wl + w) (lanes past the range idle)
     const bool act = w >= 32u || lane < w;
-    const uint32_t m = w >= 32u ? alo + (uint32_t)(((uint64_t)w * lane) / 32u) : alo + lane;
+    const uint32_t m = w >= 32u ? wl + (uint32_t)(((uint64_t)w * lane) / 32u) : wl + lane;
     bool pr = false;
+    double g = 0.0;
     uint32_t cL = 0, cR = 0;
     const uint32_t r = d - m - 1;
     if (act) {
       co_pair<KT>(L, m, R, r, &cL, &cR);
-      pr = T::ord(L.elem(m, cL)) <= T::ord(R.elem(r, cR));  // L[m] precedes R[d-m-1]
+      const auto kL = L.elem(m, cL), kR = R.elem(r, cR);
+      pr = T::ord(kL) <= T::ord(kR);  // L[m] precedes R[d-m-1]
+      g = interp_gap<KT>(kL, kR);
     }
     const uint32_t bal = __ballot_sync(0xFFFFFFFFu, pr);
     const uint32_t nact = w >= 32u ? 32u : w;
@@ -272,16 +291,21 @@ __device__ __forceinline__ uint32_t corank4_warp(InnerCR<KT>& L, InnerCR<KT>& R,
     const uint32_t mF = __shfl_sync(0xFFFFFFFFu, m, f < 32u ? f : 31u);
     const uint32_t cLF = __shfl_sync(0xFFFFFFFFu, cL, f < 32u ? f : 31u);
     const uint32_t cRF = __shfl_sync(0xFFFFFFFFu, cR, f < 32u ? f : 31u);
+    const double gTn = __shfl_sync(0xFFFFFFFFu, g, f > 0 ? f - 1 : 0);
+    const double gFn = __shfl_sync(0xFFFFFFFFu, g, f < 32u ? f : 31u);
     if (f > 0) {
       alo = mT + 1;
       L.know_low(mT, cLT);
       R.know_high(d - mT - 1, cRT);
+      gT = gTn;
     }
     if (f < nact) {
       ahi = mF;
       L.know_high(mF, cLF);
       R.know_low(d - mF - 1, cRF);
+      gF = gFn;
     }
+    missed = win && (f == 0 || f == nact);
   }
   const uint32_t a = alo;
   uint32_t c0, c2;
