@@ -92,6 +92,9 @@ static uint32_t leaf_zb(uint32_t fuse_z, bool bounded) {
   return (small ? (uint32_t)LEAF_SMALL_CAP : (uint32_t)LEAF_CAP) - fuse_z + 1;
 }
 
+#ifndef VMPS_DESC4_WARP_MAX_BIG
+#define VMPS_DESC4_WARP_MAX_BIG 4096u  // warp-per-tile partition below this many tiles, arrays > 512 MB of keys
+#endif
 #ifndef VMPS_SCAN1
 #define VMPS_SCAN1 1
 #endif
@@ -889,7 +892,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
     // keys stay near the L2 (its probes are many but parallel), 4,096 beyond;
     // measured at cfg1-5
     const uint32_t desc_warp_max =
-        !VMPS_DESC4_WARP ? 0u : (uint64_t)w.n * sizeof(K) <= (512ull << 20) ? DESC4_WARP_MAX : 4096u;
+        !VMPS_DESC4_WARP ? 0u : (uint64_t)w.n * sizeof(K) <= (512ull << 20) ? DESC4_WARP_MAX : VMPS_DESC4_WARP_MAX_BIG;
     NodeRuns* nr = (NodeRuns*)w.nr4;
     TileDesc4* t4 = (TileDesc4*)w.tiles4;
     for (int p = p_hi; p >= 1; --p) {
