@@ -61,3 +61,15 @@ def test_reference_arm_line():
     for key in ("impl", "metric", "value", "unit", "cpu_baseline", "e2e", "config", "higher_is_better"):
         assert key in d
     assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_launcher_two_ranks():
+    """`bench.py --gpus 2` outside torchrun spawns two ranks that join one gloo
+    group (the launcher's rendezvous plumbing, no GPU); rank 0 reports n_gpus = 2."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launcher-selftest"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d == {"launcher_selftest": True, "n_gpus": 2}
