@@ -48,6 +48,10 @@ constexpr uint32_t M4_KA = VMPS_M4_KA;         // steps A and B (odd)
 #define VMPS_M4_IV 1
 #endif
 constexpr bool M4_IV = VMPS_M4_IV;             // step A carries the payload (see Merge4Smem)
+#ifndef VMPS_M4_PF
+#define VMPS_M4_PF 1
+#endif
+constexpr bool M4_PF = VMPS_M4_PF;             // merge_serial with one-ahead prefetch
 constexpr uint32_t M4_NT = 4096 / M4_KQ + 32;  // consumer threads (17 warps)
 constexpr uint32_t M4_THREADS = M4_NT + 32;    // + the producer warp
 static_assert((4096 + M4_KA - 1) / M4_KA + 1 <= M4_NT, "step A chunks");
@@ -604,6 +608,28 @@ __device__ __forceinline__ void merge_serial(const typename KeyTraits<KT>::K* S,
                                              typename KeyTraits<KT>::K (&rk)[KQ], uint32_t (&ri)[KQ]) {
   using T = KeyTraits<KT>;
   using K = typename T::K;
+  if constexpr (M4_PF && KT == VMPS_KEY_U32) {
+    // heads and one-ahead prefetches of both sides: the load issued at a step
+    // is first needed a step later, so its latency leaves the compare ->
+    // select -> load chain (reads past a part stay inside the padded buffer).
+    // u32 only: with f32 (order image per compare) and u64 keys (registers)
+    // it measured slower (cfg4 6.54 -> 6.88 ms, cfg3 5.49 -> 5.58 ms)
+    K ka = S[ia], kb = S[ib], ka2 = S[ia + 1], kb2 = S[ib + 1];
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const bool pa = ib >= eb || (ia < ea && T::ord(ka) <= T::ord(kb));
+      rk[q] = pa ? ka : kb;
+      ri[q] = pa ? (uint32_t)((int32_t)ia + dA) : (uint32_t)((int32_t)ib + dB);
+      ia += pa ? 1u : 0u;
+      ib += pa ? 0u : 1u;
+      const K nx = S[(pa ? ia : ib) + 1];
+      ka = pa ? ka2 : ka;
+      kb = pa ? kb : kb2;
+      ka2 = pa ? nx : ka2;
+      kb2 = pa ? kb2 : nx;
+    }
+    return;
+  }
   K ka = S[ia], kb = S[ib];
   typename T::O oa = T::ord(ka), ob = T::ord(kb);  // order images, computed once per load
 #pragma unroll
