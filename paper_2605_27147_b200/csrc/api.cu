@@ -817,7 +817,7 @@ static vmps_status_t sort_impl(const Work& w, void* keys, uint32_t* vals, cudaSt
       LAUNCH((k_leaf_sort<KT, HV, LEAF_THREADS>), nsm() * leaf_minb<KT>(), LEAF_THREADS, lsm, s, k0, v0, k1, v1,
              w.units, w.batch_first, w.scalars);
   }
-  LAUNCH((k_long_leaves<KT, HV>), nsm() * 8, 256, 0, s, k0, v0, k1, v1, w.longs, w.long_off, w.scalars,
+  LAUNCH((k_long_leaves<KT, HV>), nsm() * VMPS_LONG_MINB, 256, 0, s, k0, v0, k1, v1, w.longs, w.long_off, w.scalars,
          LONG_CHUNK);
   rc = launch_check();
   if (rc != VMPS_OK) return rc;
@@ -2139,7 +2139,7 @@ static vmps_status_t merge_runs_impl(void* keys, uint32_t* vals, uint64_t n, con
   uint32_t* v0 = vals;
   uint32_t* v1 = HV ? (uint32_t*)(base + L.off_v1) : nullptr;
   uint32_t* d_scal = (uint32_t*)(base + L.off_scalars);
-  LAUNCH((k_long_leaves<KT, HV>), nsm() * 8, 256, 0, s, k0, v0, k1, v1, (const uint32_t*)(base + L.off_longs),
+  LAUNCH((k_long_leaves<KT, HV>), nsm() * VMPS_LONG_MINB, 256, 0, s, k0, v0, k1, v1, (const uint32_t*)(base + L.off_longs),
          (const uint32_t*)(base + L.off_longoff), d_scal, LONG_CHUNK);
   using SM = MergeSmem<KT, HV>;
   VMPS_CK(cudaFuncSetAttribute(k_merge_level<KT, HV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM::BYTES));

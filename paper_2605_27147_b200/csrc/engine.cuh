@@ -602,10 +602,16 @@ __global__ void k_batch_first(const uint32_t* __restrict__ flag, const uint32_t*
     batch_first[b] = nunits;
 }
 
+#ifndef VMPS_LONG_U
+#define VMPS_LONG_U 8  // elements per thread in flight per batch of a long-leaf copy
+#endif
+#ifndef VMPS_LONG_MINB
+#define VMPS_LONG_MINB 4  // resident CTAs per SM (caps registers at 64: 80 left 3 CTAs; 6 and 8 spill)
+#endif
 // Long leaves (> Z): reverse strictly descending runs, place odd-depth leaves
 // into buffer 1.  Work is split into LONG_CHUNK pieces.
 template <int KT, bool HV>
-__global__ void __launch_bounds__(256) k_long_leaves(
+__global__ void __launch_bounds__(256, VMPS_LONG_MINB) k_long_leaves(
     typename KeyTraits<KT>::K* __restrict__ k0, uint32_t* __restrict__ v0,
     typename KeyTraits<KT>::K* __restrict__ k1, uint32_t* __restrict__ v1,
     const uint32_t* __restrict__ longs, const uint32_t* __restrict__ long_off,
@@ -629,15 +635,17 @@ __global__ void __launch_bounds__(256) k_long_leaves(
     const uint32_t len = e - s;
     const bool desc = f & 2u, odd = f & 1u;
     const uint32_t base = (c - long_off[a]) * chunk;
-    // U independent elements per thread in flight (loads first, then stores)
-    constexpr int U = 8;
+    // U independent elements per thread in flight (loads first, then stores);
+    // the reversal holds two of each (both ends), so half as many
+    constexpr int U = VMPS_LONG_U;
     if (desc && !odd) {  // in-place reversal in buffer 0
+      constexpr int UR = U / 2;
       const uint32_t half = len / 2, lim = min(base + chunk, half);
-      for (uint32_t q0 = base + threadIdx.x; q0 < lim; q0 += U * blockDim.x) {
-        K x[U], y[U];
-        uint32_t vx[U], vy[U];
+      for (uint32_t q0 = base + threadIdx.x; q0 < lim; q0 += UR * blockDim.x) {
+        K x[UR], y[UR];
+        uint32_t vx[UR], vy[UR];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < UR; ++u) {
           const uint32_t q = q0 + u * blockDim.x;
           if (q < lim) {
             x[u] = k0[s + q]; y[u] = k0[e - 1 - q];
@@ -645,7 +653,7 @@ __global__ void __launch_bounds__(256) k_long_leaves(
           }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < UR; ++u) {
           const uint32_t q = q0 + u * blockDim.x;
           if (q < lim) {
             k0[s + q] = y[u]; k0[e - 1 - q] = x[u];
