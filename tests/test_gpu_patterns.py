@@ -1,4 +1,6 @@
-"""GPU parity on structured inputs at ~2^20 (ragged n): the default schedule
+"""GPU parity on structured inputs at ~2^20 (ragged n; among them skewed
+key values -- powers of two, two far-apart clusters -- in sorted and
+reversed segments): the default schedule
 (two tree levels per HBM pass, 4-way merges) and one level per pass, both
 leaf engines' default, against the CPU oracle, bit-exact (keys, payloads,
 run count and merge cost)."""
@@ -34,6 +36,17 @@ def _patterns(n, rng):
     for a, b in zip(cuts[:-1:2], cuts[1::2]):
         r[a:b] = np.sort(r[a:b])[::-1] if (a & 1) else np.sort(r[a:b])
     yield "mixed_runs", r
+    # skewed key values with sorted / reversed segments: huge gaps, heavy ties
+    # and two far-apart clusters stress the partition's regula falsi probes
+    # (interpolated positions, exact brackets) at every merge level
+    def runs_of(v):
+        cuts = np.sort(rng.integers(0, n, 400))
+        for a, b in zip(cuts[:-1:2], cuts[1::2]):
+            v[a:b] = np.sort(v[a:b])[::-1] if (a & 1) else np.sort(v[a:b])
+        return v
+    yield "pow2_skew", runs_of(np.left_shift(np.uint64(1), rng.integers(0, 64, n).astype(np.uint64)))
+    lo = rng.integers(0, 1000, n).astype(np.uint64)
+    yield "two_clusters", runs_of(np.where(rng.random(n) < 0.5, lo, np.uint64(0xFFFFFFFFFFFFFFFF) - lo))
 
 
 @pytest.fixture(scope="module")
