@@ -84,3 +84,32 @@ def test_patterns_vs_oracle(vm, levels, dtype):
             assert st["runs"] == ost["runs"] and st["merge_cost_M"] == ost["merge_cost_M"], name
     finally:
         vm.test_set_mode()
+
+
+@pytest.mark.parametrize("dtype", [np.uint32, np.uint64, np.float32])
+def test_patterns_small_tiles_vs_oracle(vm, dtype):
+    """The same patterns with 16-output merge tiles: ~65,000 tiles per level,
+    so the large-level partition path runs (a thread per chain of hinted
+    4-way splits with regula falsi steps) instead of the warp-per-tile one."""
+    rng = np.random.default_rng(900 + (dtype == np.uint64) * 3 + (dtype == np.float32) * 5)
+    vm.test_set_mode(2)
+    vm.test_set_tiles(0, 16, 0)
+    vm.test_set_minrun(0)
+    try:
+        for name, base in _patterns(N, rng):
+            if dtype == np.float32:
+                keys = (base.astype(np.float64) - N / 2).astype(np.float32)
+            else:
+                keys = base.astype(dtype)
+            vals = np.arange(N, dtype=np.uint32)
+            ko, vo, _, ost = oracle.sort(keys, vals, variant=oracle.VARIANT_A)
+            k = W.from_numpy(keys, "cuda")
+            v = W.from_numpy(vals, "cuda")
+            st = vm.sort_(k, v, stats=True)
+            torch.cuda.synchronize()
+            assert W.to_numpy(k).view(np.uint8).tobytes() == ko.view(np.uint8).tobytes(), name
+            assert (W.to_numpy(v) == vo).all(), name
+            assert st["runs"] == ost["runs"] and st["merge_cost_M"] == ost["merge_cost_M"], name
+    finally:
+        vm.test_set_mode()
+        vm.test_set_tiles(0, 0, 0)
