@@ -21,3 +21,35 @@ def test_fuzz_against_definition(seed):
     failed, skipped, _ = fuzz_gpu.run(40, seed)
     assert not failed, failed[:3]
     assert skipped <= 4
+
+
+@pytest.mark.parametrize("seed", [11, 22, 33])
+def test_fuzz_plan_against_oracle(seed):
+    """The merge plan (run starts, kinds, Alg. 1's merges with powers, in
+    order) of the fuzz patterns at n <= 2^18 and random minrun, against the
+    oracle's plan (ExtractRun P:399/756, power P:445-446, Alg. 1)."""
+    import numpy as np
+    import oracle
+    import paper_2605_27147_b200 as vm
+    import fuzz_gpu
+    import workloads as W
+    rng = np.random.default_rng(seed)
+    pats = ["uniform", "few", "equal", "segments", "segments_rev", "mixed", "sawtooth", "sorted", "reversed"]
+    try:
+        for _ in range(25):
+            kt = str(rng.choice(["u32", "u64", "f32"]))
+            n = int(np.exp(rng.uniform(np.log(2), np.log(1 << 18))))
+            pat = str(rng.choice(pats))
+            minrun = int(rng.choice([0, 0, 1, 3, 8, 32]))
+            k0 = fuzz_gpu.gen(rng, n, kt, pat)
+            vm.test_set_minrun(minrun)
+            op, _ = oracle.plan(k0, minrun_override=minrun)
+            p = vm.merge_plan(W.from_numpy(k0, "cuda"))
+            case = (kt, n, pat, minrun)
+            assert (p.run_start.cpu().numpy() == op.run_start.astype(np.int64)).all(), case
+            assert (p.run_kind.cpu().numpy() == op.run_kind).all(), case
+            got = [tuple(int(x) for x in row) for row in p.merges.cpu().numpy()]
+            want = [(int(m["i"]), int(m["j"]), int(m["k"]), int(m["power"])) for m in op.merges]
+            assert got == want, case
+    finally:
+        vm.test_set_minrun(0)
