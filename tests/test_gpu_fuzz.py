@@ -53,3 +53,40 @@ def test_fuzz_plan_against_oracle(seed):
             assert got == want, case
     finally:
         vm.test_set_minrun(0)
+
+
+@pytest.mark.parametrize("seed", [7, 8])
+def test_fuzz_host_buffers(seed):
+    """The host-buffer entry points (vmps_sort_*_host: copy in, device sort,
+    copy out, one stream), in place and out of place, pageable and pinned
+    host memory, against the stable sort by definition."""
+    import numpy as np
+    import torch
+    import paper_2605_27147_b200 as vm
+    import fuzz_gpu
+    rng = np.random.default_rng(seed)
+    for _ in range(12):
+        kt = str(rng.choice(["u32", "u64", "f32"]))
+        n = int(np.exp(rng.uniform(0, np.log(1 << 21))))
+        pat = str(rng.choice(["uniform", "few", "segments", "mixed", "sawtooth", "reversed"]))
+        hv, pin, oop = bool(rng.random() < 0.7), bool(rng.random() < 0.5), bool(rng.random() < 0.5)
+        k0 = fuzz_gpu.gen(rng, n, kt, pat)
+        perm = np.argsort(fuzz_gpu.order_image(k0, kt), kind="stable")
+        bits = k0.view(np.uint64) if kt == "u64" else k0.view(np.uint32)
+        # f32 keys travel as a float32 tensor (an int32 one would be read as u32)
+        kh = torch.from_numpy(k0.copy() if kt == "f32" else bits.view(np.int64 if kt == "u64" else np.int32).copy())
+        vh = torch.arange(n, dtype=torch.int32) if hv else None
+        if pin:
+            kh = kh.pin_memory()
+            vh = None if vh is None else vh.pin_memory()
+        ko = torch.empty_like(kh) if oop else None
+        vo = torch.empty_like(vh) if (oop and hv) else None
+        vm.sort_host_(kh, vh, out_keys=ko, out_values=vo)
+        torch.cuda.synchronize()
+        rk = (ko if oop else kh).numpy().view(bits.dtype)  # bit patterns
+        case = (kt, n, pat, hv, pin, oop)
+        assert np.array_equal(rk, bits[perm]), case
+        if hv:
+            assert np.array_equal((vo if oop else vh).numpy().astype(np.int64), perm), case
+        if oop:  # the input is left as it was
+            assert np.array_equal(kh.numpy().view(bits.dtype), bits), case
