@@ -90,3 +90,50 @@ def test_fuzz_host_buffers(seed):
             assert np.array_equal((vo if oop else vh).numpy().astype(np.int64), perm), case
         if oop:  # the input is left as it was
             assert np.array_equal(kh.numpy().view(bits.dtype), bits), case
+
+
+@pytest.mark.parametrize("seed", [5, 6])
+def test_fuzz_dist_virtual_ranks(seed):
+    """The native multi-GPU sort (vmps_sort_*_dist: exact splitters, tie split
+    in rank order, exchange, stable merge) on g = 2..6 virtual ranks with
+    random shard sizes (empty shards, one non-empty shard) and the fuzz
+    patterns (heavy ties included): the concatenated rank outputs are the
+    stable sort of the concatenated shards by definition, and every rank
+    keeps its element count."""
+    import numpy as np
+    import paper_2605_27147_b200 as vm
+    import fuzz_gpu
+    import workloads as W
+    from tests import vranks
+    rng = np.random.default_rng(seed)
+    for _ in range(4):
+        g = int(rng.integers(2, 7))
+        kt = str(rng.choice(["u32", "u64", "f32"]))
+        pat = str(rng.choice(["uniform", "few", "equal", "segments", "mixed", "sawtooth"]))
+        r = rng.random()
+        if r < 0.2:
+            sizes = [0] * g
+            sizes[int(rng.integers(0, g))] = int(rng.integers(1, 200_000))
+        else:
+            sizes = [int(rng.integers(0, 300_000)) if rng.random() < 0.8 else 0 for _ in range(g)]
+        n = sum(sizes)
+        k0 = fuzz_gpu.gen(rng, n, kt, pat)
+        offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        ks = [k0[offs[q]:offs[q + 1]].copy() for q in range(g)]
+        vs = [np.arange(offs[q], offs[q + 1], dtype=np.uint32) for q in range(g)]
+
+        def fn(rank, comm):
+            kd = W.from_numpy(ks[rank], "cuda")
+            vd = W.from_numpy(vs[rank], "cuda")
+            vm.sort_dist_native_(comm, kd, vd)
+            return W.to_numpy(kd), W.to_numpy(vd)
+
+        outs = vranks.run(g, fn)
+        perm = np.argsort(fuzz_gpu.order_image(k0, kt), kind="stable")
+        bits = k0.view(np.uint64) if kt == "u64" else k0.view(np.uint32)
+        case = (g, kt, pat, sizes)
+        for q in range(g):
+            assert len(outs[q][0]) == sizes[q], case
+        got = np.concatenate([o[0] for o in outs]).view(bits.dtype)
+        assert np.array_equal(got, bits[perm]), case
+        assert np.array_equal(np.concatenate([o[1] for o in outs]).astype(np.int64), perm), case
