@@ -137,3 +137,28 @@ def test_fuzz_dist_virtual_ranks(seed):
         got = np.concatenate([o[0] for o in outs]).view(bits.dtype)
         assert np.array_equal(got, bits[perm]), case
         assert np.array_equal(np.concatenate([o[1] for o in outs]).astype(np.int64), perm), case
+
+
+@pytest.mark.parametrize("seed", [9, 10])
+def test_fuzz_records(seed):
+    """vmps_sort_records on random record widths 1..33 words,
+    with word values drawn from small alphabets (long tied prefixes, equal
+    records) or the full range, against the stable lexicographic sort by
+    definition (numpy lexsort: stable, word 0 most significant)."""
+    import numpy as np
+    import torch
+    import paper_2605_27147_b200 as vm
+    rng = np.random.default_rng(seed)
+    for _ in range(10):
+        words = int(rng.integers(1, 34))
+        n = int(np.exp(rng.uniform(0, np.log(300_000))))
+        alpha = int(rng.choice([1, 2, 3, 16, 2**32]))
+        r = rng.integers(0, alpha, (n, words), dtype=np.uint64).astype(np.uint32)
+        if rng.random() < 0.3 and n > 1:  # runs of equal records
+            r = r[np.sort(rng.integers(0, n, n))]
+        want = np.lexsort(r.T[::-1]) if n else np.zeros(0, np.int64)
+        out, pm = vm.sort_records(torch.from_numpy(r.view(np.int32).copy()).cuda(), perm=True)
+        torch.cuda.synchronize()
+        case = (words, n, alpha)
+        assert np.array_equal(pm.cpu().numpy().astype(np.int64), want), case
+        assert out.cpu().numpy().view(np.uint32).tobytes() == r[want].tobytes(), case
