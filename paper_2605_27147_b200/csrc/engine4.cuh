@@ -52,6 +52,10 @@ constexpr bool M4_IV = VMPS_M4_IV;             // step A carries the payload (se
 #define VMPS_M4_PF 1
 #endif
 constexpr bool M4_PF = VMPS_M4_PF;             // merge_serial with one-ahead prefetch
+#ifndef VMPS_M4_EVICT_FIRST
+#define VMPS_M4_EVICT_FIRST 1
+#endif
+constexpr bool M4_EVICT_FIRST = VMPS_M4_EVICT_FIRST;  // 4-byte keys: the level merge's bulk loads evict-first in L2
 constexpr uint32_t M4_NT = 4096 / M4_KQ + 32;  // consumer threads (17 warps)
 constexpr uint32_t M4_THREADS = M4_NT + 32;    // + the producer warp
 static_assert((4096 + M4_KA - 1) / M4_KA + 1 <= M4_NT, "step A chunks");
@@ -528,6 +532,7 @@ __device__ __forceinline__ void merge4_issue(const TileDesc4& d, const TileDesc4
                                              const typename KeyTraits<KT>::K* k1, const uint32_t* v1) {
   using SM = Merge4Smem<KT, HV>;
   using K = typename KeyTraits<KT>::K;
+  constexpr bool EF = M4_EVICT_FIRST && sizeof(K) == 4;  // inputs read once per pass
   const K* sk = R.par ? k0 : k1;
   const uint32_t* sv = R.par ? v0 : v1;
   uint32_t c1[4];
@@ -582,14 +587,14 @@ __device__ __forceinline__ void merge4_issue(const TileDesc4& d, const TileDesc4
   uint32_t o = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    if (kbytes[i]) bulk_g2s(st + o, (const void*)kg[i], kbytes[i], &bars[s]);
+    if (kbytes[i]) bulk_g2s<EF>(st + o, (const void*)kg[i], kbytes[i], &bars[s]);
     o += kbytes[i];
   }
   if (HV) {
     o = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      if (vbytes[i]) bulk_g2s(st + SM::KB + o, (const void*)vg[i], vbytes[i], &bars[s]);
+      if (vbytes[i]) bulk_g2s<EF>(st + SM::KB + o, (const void*)vg[i], vbytes[i], &bars[s]);
       o += vbytes[i];
     }
   }
