@@ -8,7 +8,8 @@ every NaN -> the maximum image).  The payload is the input position, so the
 output payload must be exactly that permutation and the output keys the
 input keys gathered by it.
 
-usage: python scripts/fuzz_gpu.py [CASES] [SEED]   (prints one JSON line per
+usage: python scripts/fuzz_gpu.py [CASES] [SEED] [MAXLOG]   (MAXLOG > 23: 60% of
+the cases have 2^21 <= n < 2^MAXLOG; prints one JSON line per
 failure and a summary line; exit 1 on any failure)"""
 import json, math, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -87,7 +88,7 @@ def to_host_bits(t: torch.Tensor, kt: str) -> np.ndarray:
     return t.view(torch.int32).cpu().numpy().view(np.uint32)
 
 
-def run(cases: int, seed: int):
+def run(cases: int, seed: int, maxlog: int = 23):
     """Run `cases` random cases from `seed`; returns (failed case dicts,
     cases skipped for a refused scratch budget, elements sorted)."""
     rng = np.random.default_rng(seed)
@@ -99,10 +100,10 @@ def run(cases: int, seed: int):
             r = rng.random()
             if r < 0.05:
                 n = int(rng.integers(0, 8))
-            elif r < 0.9:
+            elif r < (0.9 if maxlog <= 23 else 0.4):
                 n = int(math.exp(rng.uniform(math.log(8), math.log(1 << 21))))
             else:
-                n = int(rng.integers(1 << 21, 1 << 23))
+                n = int(rng.integers(1 << 21, 1 << maxlog))
             pat = str(rng.choice(pats))
             hv = bool(rng.random() < 0.75)
             minrun = int(rng.choice([0, 0, 0, 1, 2, 4, 7, 16, 33])) if n < (1 << 20) else 0
@@ -153,11 +154,12 @@ def run(cases: int, seed: int):
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 300
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 2026
+    maxlog = int(sys.argv[3]) if len(sys.argv) > 3 else 23
     t0 = time.time()
-    failed, skipped, tot = run(cases, seed)
+    failed, skipped, tot = run(cases, seed, maxlog)
     for f in failed:
         print(json.dumps({"fail": f}), flush=True)
-    print(json.dumps({"cases": cases, "seed": seed, "failures": len(failed), "skipped_budget": skipped,
+    print(json.dumps({"cases": cases, "seed": seed, "maxlog": maxlog, "failures": len(failed), "skipped_budget": skipped,
                       "elements": tot, "seconds": round(time.time() - t0, 1)}), flush=True)
     sys.exit(1 if failed else 0)
 
